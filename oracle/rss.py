@@ -1,0 +1,205 @@
+"""Oracle: recursive strong skeletonization (RS-S) factorization and solve
+(test infrastructure only).
+
+Follows, step by step and in the paper's notation:
+* PAPER.md L873-897 (§4.2): upward pass, fine → coarse; the actives of a parent
+  are the union of its children's skeletons (ascending tree order, reading C11);
+  stop after level 2 (reading C12), remaining actives B_t go to a dense LU.
+* PAPER.md L1880-1914 (§5.1.3, simultaneous skeletonization): one ID of
+  M = [A_QB ; A_BQᵀ ; s_γ K_γB √D_B ; s_γ (√D_B S_Bγ)ᵀ]  (proxy rows iff P ≠ ∅,
+  readings C3/C4/C5/C12; Q = Chebyshev-2 owners minus N, reading C6).
+* PAPER.md L739-825 (Eqs. pap → strong-skel-elim): E/F with the shared T (plain
+  transpose), X_RR = A_RR − TᵀA_SR − A_RS T + TᵀA_SS T, X_RS = A_RS − TᵀA_SS,
+  X_SR = A_SR − A_SS T, X_RN = A_RN − TᵀA_SN, X_NR = A_NR − A_NS T; LU(X_RR);
+  Schur update of (S∪N)²:  −X_{(S∪N)R} X_RR⁻¹ X_{R(S∪N)}.
+* V = P E⁻¹ L⁻¹, W = U⁻¹ F⁻¹ Pᵀ stored in factored
+  form; A⁻¹ ≈ W₁⁻¹⋯W_M⁻¹ P_t D⁻¹ P_tᵀ V_M⁻¹⋯V₁⁻¹ with sign-toggled inverses.
+* Order within a level (reading C8): colours 0..7, Morton order inside a colour,
+  and the snapshot rule — N/Q/P membership and Q rows use the actives as of the
+  start of the colour phase.
+* Reading C1: the √w-scaled matrix Ã = W^{½} A W^{-½} is factorized;
+  solve returns x = W^{-½} Ã⁻¹ (W^{½} b) in the caller's ordering.
+
+State is DENSE mode: the whole current Ã is one n×n complex128
+array; Q/N/B blocks are slices, E/F/Schur writes go in place on (S∪N)², R
+rows/columns are never read again.  Suitable for n ≤ ~20,000.
+
+Pins (tests/test_oracle_rss.py): n ≤ leaf_max → exactly a dense LU solve;
+dense-literal check that the stored factors of each box applied to the whole
+matrix give the zero pattern of Eq. strong-skel-elim and ‖Z_{R,F}‖ ≤ ε-level;
+ε → 1e-12 reproduces a dense LU solve; residual ‖Ax−b‖/‖b‖ ≤ 10ε against the
+brute-force matvec; proxy-vs-full-complement compression of every box.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import scipy.linalg as sla
+
+from . import kernel as kern
+from .idqr import interp_decomp, proxy_count, proxy_points
+from .tree import Tree
+
+
+@dataclasses.dataclass
+class BoxRecord:
+    box: int
+    level: int
+    Bs: np.ndarray   # skeleton indices (tree order), pivot order
+    Br: np.ndarray   # redundant indices
+    SN: np.ndarray   # S ∪ N indices (frame of Lp / Up)
+    T: np.ndarray    # k × r
+    lu: tuple        # scipy lu_factor of X_RR
+    Lp: np.ndarray   # X_{(S∪N)R} X_RR⁻¹   ((k+|N|) × r)
+    Up: np.ndarray   # X_RR⁻¹ X_{R(S∪N)}   (r × (k+|N|))
+
+
+@dataclasses.dataclass
+class Factorization:
+    tree: Tree
+    k: float
+    eps: float
+    sw: np.ndarray          # √w in tree order
+    records: list
+    Bt: np.ndarray          # root actives (tree order, ascending)
+    root_lu: tuple
+    stats: dict
+
+
+def _gen(A, rows, cols):
+    return A[np.ix_(rows, cols)]
+
+
+def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
+           rho_factor: float = 2.0, A_init: np.ndarray | None = None,
+           keep_dense: bool = False, hook=None) -> Factorization:
+    """Factorize Ã.  ``hook(stage, ctx)`` (tests only) is called per eliminated box with
+    stage 'pre' (before the Schur update) and 'post' (after); ctx holds the index sets,
+    the ID and the live dense matrix."""
+    tree = Tree(points, leaf_max)
+    perm = tree.perm
+    X = np.asarray(points, dtype=np.float64)[perm]
+    NX = np.asarray(normals, dtype=np.float64)[perm]
+    sw = np.sqrt(np.asarray(weights, dtype=np.float64)[perm])
+    A = kern.dense_scaled(k, X, NX, sw) if A_init is None else A_init.copy()
+
+    active = {}
+    for b in range(len(tree.level)):
+        if tree.is_leaf(b):
+            active[b] = np.arange(tree.start[b], tree.end[b], dtype=np.int64)
+    records = []
+    stats = dict(levels={}, n=tree.n, nlevels=tree.nlevels)
+
+    for lvl in range(tree.nlevels - 1, 1, -1):
+        for B in tree.levels[lvl]:
+            if not tree.is_leaf(B):
+                active[B] = np.sort(np.concatenate([active[c] for c in tree.children[B]]))
+        owners = tree.owners(lvl)
+        side = tree.box_side(lvl)
+        rho = rho_factor * side
+        n_gamma = proxy_count(k, rho, eps)
+        lst = dict(boxes=0, skipped=0, ranks=[], b=[], nN=[], nQ=[], rows=[], n_gamma=n_gamma)
+        for colour in range(8):
+            phase = [B for B in tree.levels[lvl] if tree.colour(B) == colour]
+            snap = {o: active[o] for o in owners}
+            total = sum(v.size for v in snap.values())
+            for B in phase:
+                Bidx = snap[B]
+                b = Bidx.size
+                if b == 0:
+                    continue
+                Nl, Ql = tree.near_q(B)
+                nN = sum(snap[o].size for o in Nl)
+                nQ = sum(snap[o].size for o in Ql)
+                nF = total - b - nN
+                if nF == 0:                       # F = ∅ → S = B, no-op (C12)
+                    lst["skipped"] += 1
+                    continue
+                nP = nF - nQ
+                Qidx = (np.concatenate([snap[o] for o in Ql]) if Ql
+                        else np.zeros(0, dtype=np.int64))
+                rows = [_gen(A, Qidx, Bidx), _gen(A, Bidx, Qidx).T]
+                if nP > 0:                         # proxy rows iff P ≠ ∅ (C12)
+                    Y, s_g = proxy_points(tree.box_centre(B), rho, n_gamma)
+                    Kout = kern.combined_field(k, Y, X[Bidx], NX[Bidx]) * sw[Bidx][None, :]
+                    Sin = kern.green(k, X[Bidx], Y).T * sw[Bidx][None, :]
+                    rows += [s_g * Kout, s_g * Sin]
+                M = np.vstack(rows)
+                P, kk, T = interp_decomp(M, eps)
+                Bs = Bidx[P[:kk]]
+                Br = Bidx[P[kk:]]
+                Nidx = (np.concatenate([active[o] for o in Nl]) if Nl
+                        else np.zeros(0, dtype=np.int64))
+                lst["boxes"] += 1
+                lst["ranks"].append(kk)
+                lst["b"].append(b)
+                lst["nN"].append(Nidx.size)
+                lst["nQ"].append(Qidx.size)
+                lst["rows"].append(M.shape[0])
+                if Br.size == 0:                   # k = b: nothing to eliminate (C13)
+                    continue
+                # --- E/F transforms (Eq. pap and the X blocks that follow it)
+                A_RR = _gen(A, Br, Br); A_RS = _gen(A, Br, Bs); A_SR = _gen(A, Bs, Br)
+                A_SS = _gen(A, Bs, Bs); A_RN = _gen(A, Br, Nidx); A_NR = _gen(A, Nidx, Br)
+                A_SN = _gen(A, Bs, Nidx); A_NS = _gen(A, Nidx, Bs)
+                X_RR = A_RR - T.T @ A_SR - A_RS @ T + T.T @ A_SS @ T
+                X_RS = A_RS - T.T @ A_SS
+                X_SR = A_SR - A_SS @ T
+                X_RN = A_RN - T.T @ A_SN
+                X_NR = A_NR - A_NS @ T
+                # --- L/U with pivot block X_RR (Eq. strong-skel-elim)
+                lu = sla.lu_factor(X_RR, check_finite=False)
+                X_cR = np.vstack([X_SR, X_NR])
+                X_Rc = np.hstack([X_RS, X_RN])
+                Lp = sla.lu_solve(lu, X_cR.T, trans=1).T
+                Up = sla.lu_solve(lu, X_Rc)
+                SN = np.concatenate([Bs, Nidx])
+                if hook is not None:
+                    Fidx = np.concatenate([snap[o] for o in owners if o != B and o not in Nl] or
+                                          [np.zeros(0, dtype=np.int64)])
+                    ctx = dict(B=B, level=lvl, Bs=Bs, Br=Br, Nidx=Nidx, Qidx=Qidx, Fidx=Fidx,
+                               T=T, A=A, M=M, nP=nP)
+                    hook("pre", ctx)
+                A[np.ix_(SN, SN)] -= X_cR @ Up         # Schur complement update
+                if hook is not None:
+                    hook("post", ctx)
+                records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up))
+                active[B] = np.sort(Bs)
+        lst["ranks"] = np.asarray(lst["ranks"])
+        stats["levels"][lvl] = lst
+
+    alive = np.zeros(tree.n, dtype=bool)
+    for b in range(len(tree.level)):
+        if tree.is_leaf(b):
+            alive[tree.start[b]:tree.end[b]] = True
+    for r in records:
+        alive[r.Br] = False
+    Bt = np.nonzero(alive)[0]
+    root_lu = sla.lu_factor(_gen(A, Bt, Bt), check_finite=False)
+    stats["n0"] = int(Bt.size)
+    f = Factorization(tree, k, eps, sw, records, Bt, root_lu, stats)
+    if keep_dense:
+        f.A_final = A
+    return f
+
+
+def solve(f: Factorization, b: np.ndarray) -> np.ndarray:
+    """x ≈ A⁻¹ b for BASELINE.json's unscaled A; b is n or n×nrhs in caller order."""
+    b = np.asarray(b, dtype=np.complex128)
+    vec = b.ndim == 1
+    bb = b[:, None] if vec else b
+    perm = f.tree.perm
+    y = bb[perm] * f.sw[:, None]                    # W^{½} b in tree order (C1)
+    for r in f.records:                             # V_M⁻¹ ⋯ V_1⁻¹ : E then L, then D⁻¹ on R
+        y[r.Br] -= r.T.T @ y[r.Bs]
+        y[r.SN] -= r.Lp @ y[r.Br]
+        y[r.Br] = sla.lu_solve(r.lu, y[r.Br])
+    if f.Bt.size:
+        y[f.Bt] = sla.lu_solve(f.root_lu, y[f.Bt])  # P_t D⁻¹ P_tᵀ on the root block
+    for r in reversed(f.records):                   # W_1⁻¹ ⋯ W_M⁻¹ : U then F
+        y[r.Br] -= r.Up @ y[r.SN]
+        y[r.Bs] -= r.T @ y[r.Br]
+    x = np.empty_like(y)
+    x[perm] = y / f.sw[:, None]
+    return x[:, 0] if vec else x
