@@ -1,0 +1,133 @@
+/*
+ * fmmlu.h — C ABI of the B200-native FMM-LU hot path (libfmmlu.so).
+ *
+ * The library factorizes and solves the dense combined-field Helmholtz
+ * Nyström system of PAPER.md Eq. disc1 (L443-450) with the BASELINE.json
+ * conventions:
+ *
+ *     A = ½ I + (D − i k S) W,   K(x,y) = n(y)·∇_y G(x,y) − i k G(x,y),
+ *     G(x,y) = e^{ik|x−y|}/(4π|x−y|),   K(x_i,x_i) := 0,   W = diag(w)
+ *
+ * (PAPER.md L408-421 Eqs. greenfunhelm/comb_ref, L2033-2038 Eq. num-inteq),
+ * by recursive strong skeletonization (RS-S) over a level-restricted adaptive
+ * octree (§4) with proxy-surface compression and the
+ * simultaneous incoming/outgoing interpolative decomposition of PAPER.md §5.1
+ * (L1373-1914).  Internally the √w-scaled matrix Ã = W^{½} A W^{−½} is
+ * factorized (PAPER.md Eq. disc3); results are in A's variables.
+ *
+ * Memory: every array argument may be a HOST pointer or a CUDA DEVICE pointer
+ * on the current device (detected with cudaPointerGetAttributes).  Host
+ * arguments are copied in (and, for fmmlu_solve, back out) inside the call.
+ * Complex numbers are interleaved (re, im) doubles (= C99 double complex =
+ * cuDoubleComplex = torch.complex128).  The caller keeps ownership of all
+ * argument buffers; the handle owns all internal device memory.
+ *
+ * Streams: all device work is issued on the handle's stream (default: a
+ * stream the handle creates; see fmmlu_set_stream).  fmmlu_tree,
+ * fmmlu_factor and fmmlu_solve return after their work is complete.
+ *
+ * Errors: every function returns 0 on success or a negative FMMLU_E* code;
+ * fmmlu_last_error() gives a human-readable message for the calling thread's
+ * last failure.  No function aborts the process.
+ *
+ * Concurrency: a handle is single-threaded (one call at a time).  There is no
+ * CPU fallback: the compute path runs only on the GPU and fails with
+ * FMMLU_ECUDA if no usable sm_100 device is present.
+ */
+#ifndef FMMLU_H
+#define FMMLU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMMLU_OK 0
+#define FMMLU_EINVAL (-1)    /* bad argument (see each function)                         */
+#define FMMLU_EDEPTH (-2)    /* tree deeper than 20 levels (duplicate points) */
+#define FMMLU_ESINGULAR (-3) /* exactly singular pivot block X_RR or root block          */
+#define FMMLU_ENOMEM (-4)    /* device or host allocation failed                         */
+#define FMMLU_ESTATE (-5)    /* call order violated (e.g. solve before factor)           */
+#define FMMLU_ENOTIMPL (-6)  /* stage not built                                          */
+#define FMMLU_ECUDA (-7)     /* CUDA runtime / launch error                              */
+
+typedef struct fmmlu_handle fmmlu_handle;
+
+typedef struct fmmlu_stats_t {
+  int64_t n;              /* number of unknowns                                   */
+  int32_t nlevels;        /* octree levels (0 .. nlevels-1) after 2:1 balancing  */
+  int32_t nboxes;         /* boxes in the tree                                    */
+  int32_t nleaves;        /* leaf boxes                                           */
+  int32_t n_eliminated;   /* boxes skeletonized (with |R| > 0)                    */
+  int64_t n0;             /* size of the dense root block B_t */
+  int32_t max_rank;       /* largest |S| over skeletonized boxes                  */
+  int32_t max_b;          /* largest number of actives in a skeletonized box      */
+  int64_t factor_bytes;   /* device bytes held by the factor store                */
+  int64_t peak_bytes;     /* device high-water mark of the handle                 */
+  double t_tree_ms;       /* last fmmlu_tree wall time                            */
+  double t_factor_ms;     /* last fmmlu_factor wall time                          */
+  double t_solve_ms;      /* last fmmlu_solve wall time                           */
+  double t_root_ms;       /* root LU part of the last factor                      */
+  double t_levels_ms[24]; /* per-level part of the last factor (index = level)    */
+  int32_t n_singular_warn;/* near-singular pivot warnings                         */
+  int32_t ranks_sum[24];  /* Σ|S| per level                                       */
+  int32_t boxes[24];      /* skeletonized boxes per level                         */
+} fmmlu_stats_t;
+
+/* Build the adaptive level-restricted octree over the n points
+ * (readings C14, C6-C8 of SURVEY.md §8(c)).
+ *   points  : n×3 row-major (x0,y0,z0,x1,...) fp64, host or device
+ *   normals : n×3 row-major unit outward normals n(x_i)
+ *   weights : n smooth quadrature weights w_i > 0
+ *   n       : ≥ 1;  leaf_max : s ≥ 1 (split a box while it holds more than s points)
+ *   out     : receives a new handle (set to NULL on failure)
+ * Errors: EINVAL (n < 1, leaf_max < 1, NULL pointer, w ≤ 0 or non-finite,
+ * |‖n_i‖ − 1| > 1e-10), EDEPTH, ENOMEM, ECUDA. */
+int fmmlu_tree(const double* points, const double* normals, const double* weights,
+               int64_t n, int leaf_max, fmmlu_handle** out);
+
+/* Factorize A (wavenumber k, η = k) by RS-S at ID tolerance eps
+ * (ID per L606-638 with the stopping rule of reading C9;
+ * proxy surface per readings C4/C5).  Replaces any previous factorization.
+ * Errors: EINVAL (k ≤ 0 or non-finite, eps ∉ (0,1)), ESINGULAR, ENOMEM, ECUDA. */
+int fmmlu_factor(fmmlu_handle* h, double k, double eps);
+
+/* Solve A x = b in place for nrhs right-hand sides (PAPER.md L920-924:
+ * A⁻¹ ≈ W₁⁻¹⋯W_M⁻¹ P_t D⁻¹ P_tᵀ V_M⁻¹⋯V₁⁻¹, sign-toggled factors L833-858).
+ *   rhs  : n×nrhs column-major complex128 (host or device); in: b, out: x
+ *   nrhs : ≥ 1
+ * Errors: EINVAL (NULL rhs, nrhs < 1), ESTATE (no factorization), ENOMEM, ECUDA. */
+int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs);
+
+/* Apply the (unfactored) matrix: y = A x by brute-force O(n²) summation on the
+ * GPU (test/measurement infrastructure for residuals; reading C17).
+ *   x, y : n×nrhs column-major complex128 (host or device; y may not alias x)
+ * Errors: EINVAL, ESTATE (no tree), ECUDA. */
+int fmmlu_matvec(fmmlu_handle* h, double k, const void* x, void* y, int nrhs);
+
+/* Release the handle and all device memory it owns.  NULL is a no-op. */
+int fmmlu_destroy(fmmlu_handle* h);
+
+/* Message for the calling thread's most recent failure ("" if none). */
+const char* fmmlu_last_error(void);
+
+/* Statistics of the handle's tree / last factor / last solve. */
+int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out);
+
+/* Issue subsequent work on cuda_stream (a cudaStream_t; NULL = the handle's
+ * own stream).  The caller keeps ownership of the stream. */
+int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
+
+/* Tree order: perm[i] = caller index of the i-th point in tree (Morton) order.
+ * perm: int64[n] host buffer. */
+int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm);
+
+/* Measure FP64 peak on this device: DFMA (kind=0) or DMMA m8n8k4 (kind=1)
+ * throughput in TFLOP/s (roofline denominator; not part of the method). */
+int fmmlu_probe_fp64(int kind, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMMLU_H */

@@ -1,0 +1,1175 @@
+// libfmmlu: C ABI + host orchestration of the RS-S factorization on one B200.
+//
+// Host C++ keeps only integer bookkeeping (tree, owners, index lists, task
+// descriptors); every floating-point step of the method runs in the CUDA kernels
+// of kernels.cu / gemm.cu:
+//   level ℓ = L-1 … 2:
+//     build the level's block-sparse current-matrix store ("BSR": one dense block
+//       per owner pair at Chebyshev separation ≤ 2, entries = pure kernel or the
+//       Schur-updated value carried over from level ℓ+1)          [k_build]
+//     colour c = 0 … 7 (reading C8; boxes of one colour are independent):
+//       M = [A_QB; A_BQᵀ; proxy rows]       [k_copy, k_proxy]
+//       CPQR ID → perm, k; T = R11⁻¹R12      [k_cpqr, k_trsm_T]
+//       E/F transforms with T (Eq. pap … X blocks, L739-788)      [DMMA GEMM]
+//       X_RR⁻¹ (Gauss-Jordan), Up = X_RR⁻¹X_{R(S∪N)}, Lp = X_{(S∪N)R}X_RR⁻¹   [k_gj, GEMM]
+//       Schur update Δ_{(S∪N)²} −= Lp X_{R(S∪N)} scattered into the BSR (L813-825) [GEMM+atomics]
+//   root: B_t dense block → X⁻¹ (L894-918)                        [k_build, k_gj_coop]
+// Solve: upward sweep over phases, root apply, downward sweep.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/fmmlu.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "tree.h"
+
+using namespace fmmlu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// --------------------------------------------------------------------------- device memory
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      st = o.st;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t b, cudaStream_t s) {
+    release();
+    st = s;
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMallocAsync(&p, b, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(FMMLU_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed");
+    }
+    bytes = b;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// Collects host arrays and uploads them in one H2D copy.
+struct Stage {
+  std::vector<char> host;
+  DBuf dev;
+  template <class T> size_t add(const std::vector<T>& v) {
+    size_t off = (host.size() + 15) & ~size_t(15);
+    host.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+  void upload(cudaStream_t s) {
+    dev.alloc(host.size() + 16, s);
+    if (!host.empty())
+      FMMLU_CUDA(cudaMemcpyAsync(dev.p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+  }
+  template <class T> T* ptr(size_t off) const { return reinterpret_cast<T*>(dev.as<char>() + off); }
+};
+
+struct Phase {  // one (level, colour) elimination phase
+  int level, colour;
+  DBuf fac;    // complex: T | Xinv | Up | Lp per box
+  DBuf idx;    // int: S | R | N per box
+  DBuf recs;   // BoxRec[nrec]
+  int nrec = 0, kmax = 0, rmax = 0;
+  size_t fac_bytes = 0;
+};
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
+
+struct fmmlu_handle {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  Tree tree;
+  int64_t n = 0;
+  DBuf geo;   // 7 × n doubles, tree order
+  DBuf perm;  // int64 tree pos -> caller index
+  Geo g{};
+  // factor
+  bool factored = false;
+  double k = 0, eps = 0;
+  std::vector<Phase> phases;
+  DBuf root;       // n0 × n0 complex: X_t⁻¹
+  DBuf root_rows;  // int n0
+  int64_t n0 = 0;
+  fmmlu_stats_t stats{};
+  size_t cur_bytes = 0, peak_bytes = 0;
+};
+
+namespace {
+
+void track(fmmlu_handle* h, long long delta) {
+  h->cur_bytes += delta;
+  h->peak_bytes = std::max(h->peak_bytes, h->cur_bytes);
+}
+
+int proxy_count(double k, double rho, double eps) {
+  // n_γ = 2p(p+1), p = max(8, ⌈κ + 1.8 (log10(1/ε))^{2/3} κ^{1/3}⌉), κ = kρ (reading C5)
+  double kap = k * rho;
+  double p = std::ceil(kap + 1.8 * std::pow(std::log10(1.0 / eps), 2.0 / 3.0) * std::cbrt(kap));
+  int pi = std::max(8, (int)p);
+  return 2 * pi * (pi + 1);
+}
+
+constexpr int kTile = 64;
+
+void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, const GemmProblem& p) {
+  if (p.m <= 0 || p.n <= 0 || p.k <= 0) return;
+  int id = (int)probs.size();
+  probs.push_back(p);
+  for (int tm = 0; tm < (p.m + kTile - 1) / kTile; ++tm)
+    for (int tn = 0; tn < (p.n + kTile - 1) / kTile; ++tn) tiles.push_back({id, tm, tn});
+}
+
+void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cplx alpha,
+               int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep) {
+  if (tiles.empty()) return;
+  Stage s;
+  size_t op = s.add(probs), ot = s.add(tiles);
+  s.upload(st);
+  gemm_batched(s.ptr<GemmProblem>(op), s.ptr<GemmTile>(ot), (int)tiles.size(), alpha, scatter, bsr, st);
+  keep.push_back(std::move(s.dev));
+  probs.clear();
+  tiles.clear();
+}
+
+// ---------------------------------------------------------------------------- factorization
+struct LevelBSR {
+  int level = -1;
+  std::vector<int> owners;                 // box ids
+  std::unordered_map<int, int> local;      // box id -> local owner index
+  std::vector<std::vector<int>> act;       // actives at level start (sorted)
+  std::unordered_map<long long, long long> pairoff;  // a*no+b -> complex offset
+  DBuf bsr;
+  long long size = 0;
+  long long key(int a, int b) const { return (long long)a * (long long)owners.size() + b; }
+  long long off(int a, int b) const {
+    auto it = pairoff.find(key(a, b));
+    return it == pairoff.end() ? -1 : it->second;
+  }
+};
+
+void factor_impl(fmmlu_handle* h, double k, double eps) {
+  cudaStream_t st = h->stream;
+  Tree& T = h->tree;
+  const int L = T.nlevels;
+  const int n = (int)h->n;
+  h->phases.clear();
+  h->root.release();
+  h->root_rows.release();
+  h->factored = false;
+  fmmlu_stats_t& S = h->stats;
+  std::memset(S.t_levels_ms, 0, sizeof(S.t_levels_ms));
+  std::memset(S.ranks_sum, 0, sizeof(S.ranks_sum));
+  std::memset(S.boxes, 0, sizeof(S.boxes));
+  S.n_eliminated = 0;
+  S.max_rank = 0;
+  S.max_b = 0;
+  S.factor_bytes = 0;
+  DBuf status;
+  status.alloc(16, st);
+  FMMLU_CUDA(cudaMemsetAsync(status.p, 0, 16, st));
+
+  // actives per box (sorted global tree-order indices)
+  std::vector<std::vector<int>> act(T.boxes.size());
+  for (size_t b = 0; b < T.boxes.size(); ++b)
+    if (T.boxes[b].leaf())
+      for (int i = T.boxes[b].start; i < T.boxes[b].end; ++i) act[b].push_back(i);
+
+  std::vector<int> prevOwner(n, -1), prevPos(n, -1);  // level ℓ+1 owner (local) / position
+  LevelBSR prev;
+  std::vector<DBuf> keep;  // per-phase temporaries kept alive until the phase syncs
+
+  for (int lvl = L - 1; lvl >= 2; --lvl) {
+    double tl0 = now_ms();
+    LevelBSR cur;
+    cur.level = lvl;
+    for (int b : T.levels[lvl]) {
+      if (!T.boxes[b].leaf()) {
+        std::vector<int> u;
+        const Box& B = T.boxes[b];
+        for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), act[B.child[c]].begin(), act[B.child[c]].end());
+        std::sort(u.begin(), u.end());
+        act[b] = u;
+      }
+      cur.owners.push_back(b);
+    }
+    for (int m = 0; m < lvl; ++m)
+      for (int b : T.levels[m])
+        if (T.boxes[b].leaf()) cur.owners.push_back(b);
+    const int no = (int)cur.owners.size();
+    for (int i = 0; i < no; ++i) cur.local[cur.owners[i]] = i;
+    cur.act.resize(no);
+    for (int i = 0; i < no; ++i) cur.act[i] = act[cur.owners[i]];
+    // neighbour lists (sep ≤ 2) and BSR layout
+    std::vector<std::vector<int>> nb(no);
+    std::vector<int> tmp;
+    long long off = 0;
+    for (int a = 0; a < no; ++a) {
+      T.neighbours2(cur.owners[a], lvl, tmp);
+      nb[a].push_back(a);
+      for (int o : tmp) nb[a].push_back(cur.local.at(o));
+      std::sort(nb[a].begin(), nb[a].end());
+      for (int b : nb[a]) {
+        cur.pairoff[cur.key(a, b)] = off;
+        off += (long long)cur.act[a].size() * cur.act[b].size();
+      }
+    }
+    cur.size = off;
+    cur.bsr.alloc((size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
+    track(h, cur.bsr.bytes);
+
+    // ---- build the level's BSR (kernel entries, or carried-over Schur-updated values)
+    {
+      std::vector<int> gidx, slot, pos, bld, rowoff(no);
+      std::vector<long long> tab;
+      std::vector<std::vector<int>> slots_of(no);  // prev-level owners (local) per slot
+      for (int a = 0; a < no; ++a) {
+        rowoff[a] = (int)gidx.size();
+        for (int g : cur.act[a]) {
+          gidx.push_back(g);
+          int po = prev.level >= 0 ? prevOwner[g] : -1;
+          int s = -1;
+          if (po >= 0) {
+            auto& sl = slots_of[a];
+            auto it = std::find(sl.begin(), sl.end(), po);
+            if (it == sl.end()) {
+              sl.push_back(po);
+              s = (int)sl.size() - 1;
+            } else {
+              s = (int)(it - sl.begin());
+            }
+          }
+          slot.push_back(s);
+          pos.push_back(po >= 0 ? prevPos[g] : 0);
+        }
+      }
+      std::vector<int> bldoff(no);
+      for (int a = 0; a < no; ++a) {
+        bldoff[a] = (int)bld.size();
+        for (int po : slots_of[a]) bld.push_back((int)prev.act[po].size());
+        if (slots_of[a].empty()) bld.push_back(0);
+      }
+      std::vector<BuildTask> tasks;
+      for (int a = 0; a < no; ++a)
+        for (int b : nb[a]) {
+          int ra = (int)cur.act[a].size(), cb = (int)cur.act[b].size();
+          if (ra == 0 || cb == 0) continue;
+          int ns = std::max<int>(1, (int)std::max(slots_of[a].size(), slots_of[b].size()));
+          int toff = (int)tab.size();
+          tab.resize(tab.size() + (size_t)ns * ns, -1);
+          for (size_t i = 0; i < slots_of[a].size(); ++i)
+            for (size_t j = 0; j < slots_of[b].size(); ++j)
+              tab[toff + i * ns + j] = prev.off(slots_of[a][i], slots_of[b][j]);
+          long long dst = cur.pairoff[cur.key(a, b)];
+          for (int i0 = 0; i0 < ra; i0 += kTile)
+            for (int j0 = 0; j0 < cb; j0 += kTile) {
+              BuildTask t;
+              t.dst = dst;
+              t.ldd = ra;
+              t.rows_off = rowoff[a];
+              t.cols_off = rowoff[b];
+              t.i0 = i0;
+              t.j0 = j0;
+              t.ni = std::min(kTile, ra - i0);
+              t.nj = std::min(kTile, cb - j0);
+              t.ns = ns;
+              t.tab_off = toff;
+              t.bld_off = bldoff[a];
+              tasks.push_back(t);
+            }
+        }
+      if (tab.empty()) tab.push_back(-1);
+      Stage s;
+      size_t o_t = s.add(tasks), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_tab = s.add(tab),
+             o_b = s.add(bld);
+      s.upload(st);
+      launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
+                   s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), cur.bsr.as<cplx>(), h->g, k, st);
+      keep.push_back(std::move(s.dev));
+    }
+    if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
+    prev.bsr.release();
+
+    // current actives (positions within the level-start actives)
+    std::vector<std::vector<int>> curpos(no);
+    for (int a = 0; a < no; ++a) {
+      curpos[a].resize(cur.act[a].size());
+      for (size_t i = 0; i < cur.act[a].size(); ++i) curpos[a][i] = (int)i;
+    }
+    long long total_active = 0;
+    for (int a = 0; a < no; ++a) total_active += (long long)cur.act[a].size();
+    const double side = T.box_side(lvl);
+    const double rho = 2.0 * side;
+    const int ngamma = proxy_count(k, rho, eps);
+    const double sg = std::sqrt(4.0 * M_PI * rho * rho / ngamma);
+
+    for (int colour = 0; colour < 8; ++colour) {
+      // ------------------------------------------------ boxes of this phase
+      struct BoxJob {
+        int a;  // local owner index of B
+        int b;
+        std::vector<int> N, Q;  // local owner indices
+        int nN = 0, nQ = 0;
+        bool proxy = false;
+        int m = 0;
+        long long Moff = 0, Toff = 0;
+        int permoff = 0;
+        int k = 0;
+      };
+      std::vector<BoxJob> jobs;
+      for (int bx : T.levels[lvl]) {
+        if (T.colour(bx) != colour) continue;
+        int a = cur.local.at(bx);
+        int b = (int)curpos[a].size();
+        if (b == 0) continue;
+        BoxJob J;
+        J.a = a;
+        J.b = b;
+        for (int o : nb[a]) {
+          if (o == a || curpos[o].empty()) continue;
+          int sp = T.sep(bx, cur.owners[o], lvl);
+          if (sp <= 1) {
+            J.N.push_back(o);
+            J.nN += (int)curpos[o].size();
+          } else {
+            J.Q.push_back(o);
+            J.nQ += (int)curpos[o].size();
+          }
+        }
+        long long nF = total_active - b - J.nN;
+        if (nF == 0) continue;  // F = ∅ → S = B (reading C12)
+        long long nP = nF - J.nQ;
+        J.proxy = nP > 0;
+        J.m = 2 * J.nQ + (J.proxy ? 2 * ngamma : 0);
+        jobs.push_back(std::move(J));
+      }
+      if (jobs.empty()) continue;
+      const int nj = (int)jobs.size();
+
+      // ------------------------------------------------ ID stage
+      long long wsM = 0, wsT = 0;
+      int permtot = 0, bmax = 0;
+      for (auto& J : jobs) {
+        J.Moff = wsM;
+        wsM += (long long)J.m * J.b;
+        J.Toff = wsT;
+        wsT += (long long)(J.b / 2 + 1) * (J.b - J.b / 2 + 1);
+        J.permoff = permtot;
+        permtot += J.b;
+        bmax = std::max(bmax, J.b);
+      }
+      DBuf M, Tb, permd, kd;
+      M.alloc(wsM * sizeof(cplx), st);
+      Tb.alloc(wsT * sizeof(cplx), st);
+      permd.alloc((size_t)permtot * sizeof(int), st);
+      kd.alloc((size_t)nj * sizeof(int), st);
+      track(h, M.bytes + Tb.bytes);
+      {
+        std::vector<CopyTask> cps;
+        std::vector<int> maps;
+        std::vector<ProxyTask> pts;
+        std::vector<IdTask> ids;
+        std::vector<int> gidx;
+        for (auto& J : jobs) {
+          int row = 0;
+          long long bb = cur.pairoff[cur.key(J.a, J.a)];
+          (void)bb;
+          for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
+            int mo = (int)maps.size();
+            maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+            CopyTask c{};
+            c.src = cur.off(q, J.a);
+            c.lds = (int)cur.act[q].size();
+            c.dst = J.Moff + row;
+            c.ldd = J.m;
+            c.rows = (int)curpos[q].size();
+            c.cols = J.b;
+            c.trans = 0;
+            c.rmap_off = mo;
+            c.cmap_off = -1;
+            cps.push_back(c);
+            row += c.rows;
+          }
+          for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
+            int mo = (int)maps.size();
+            maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+            CopyTask c{};
+            c.src = cur.off(J.a, q);
+            c.lds = J.b;
+            c.dst = J.Moff + row;
+            c.ldd = J.m;
+            c.rows = (int)curpos[q].size();
+            c.cols = J.b;
+            c.trans = 1;
+            c.rmap_off = mo;
+            c.cmap_off = -1;
+            cps.push_back(c);
+            row += c.rows;
+          }
+          if (J.proxy) {
+            ProxyTask p{};
+            p.dst = J.Moff;
+            p.ld = J.m;
+            p.row0 = row;
+            p.b = J.b;
+            p.idx_off = (int)gidx.size();
+            gidx.insert(gidx.end(), cur.act[J.a].begin(), cur.act[J.a].end());
+            p.ngamma = ngamma;
+            double c3[3];
+            T.box_centre(cur.owners[J.a], c3);
+            p.cx = c3[0];
+            p.cy = c3[1];
+            p.cz = c3[2];
+            p.rho = rho;
+            p.sg = sg;
+            pts.push_back(p);
+          }
+          IdTask it{};
+          it.M = J.Moff;
+          it.m = J.m;
+          it.b = J.b;
+          it.out_off = J.permoff;
+          it.T = J.Toff;
+          ids.push_back(it);
+        }
+        if (maps.empty()) maps.push_back(0);
+        if (gidx.empty()) gidx.push_back(0);
+        Stage s;
+        size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_i = s.add(ids), o_g = s.add(gidx);
+        s.upload(st);
+        launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), M.as<cplx>(), st);
+        launch_proxy(s.ptr<ProxyTask>(o_p), (int)pts.size(), s.ptr<int>(o_g), M.as<cplx>(), h->g, k, st);
+        launch_cpqr(s.ptr<IdTask>(o_i), nj, M.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st, bmax);
+        launch_trsm_T(s.ptr<IdTask>(o_i), kd.as<int>(), nj, M.as<cplx>(), Tb.as<cplx>(), st);
+        keep.push_back(std::move(s.dev));
+      }
+      std::vector<int> hk(nj), hperm(permtot);
+      FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FMMLU_CUDA(cudaStreamSynchronize(st));
+      keep.clear();
+      track(h, -(long long)M.bytes);
+      M.release();
+
+      // ------------------------------------------------ elimination stage
+      std::vector<int> el;  // jobs with r > 0
+      for (int j = 0; j < nj; ++j) {
+        jobs[j].k = hk[j];
+        int r = jobs[j].b - hk[j];
+        S.ranks_sum[lvl] += hk[j];
+        S.boxes[lvl] += 1;
+        S.max_rank = std::max(S.max_rank, hk[j]);
+        S.max_b = std::max(S.max_b, jobs[j].b);
+        if (r > 0) el.push_back(j);
+      }
+      if (!el.empty()) {
+        Phase ph;
+        ph.level = lvl;
+        ph.colour = colour;
+        // sizes
+        long long wsW = 0, facsz = 0;
+        int idxsz = 0;
+        std::vector<long long> WBoff(nj), WNoff(nj);
+        std::vector<BoxRec> recs;
+        for (int j : el) {
+          BoxJob& J = jobs[j];
+          int r = J.b - J.k, kk = J.k, kn = kk + J.nN;
+          WBoff[j] = wsW;
+          wsW += (long long)J.b * (J.b + J.nN);
+          WNoff[j] = wsW;
+          wsW += (long long)J.nN * J.b;
+          BoxRec R{};
+          R.k = kk;
+          R.r = r;
+          R.nN = J.nN;
+          R.T = facsz;
+          facsz += (long long)kk * r;
+          R.Xi = facsz;
+          facsz += (long long)r * r;
+          R.Up = facsz;
+          facsz += (long long)r * kn;
+          R.Lp = facsz;
+          facsz += (long long)kn * r;
+          R.idxS = idxsz;
+          idxsz += kk;
+          R.idxR = idxsz;
+          idxsz += r;
+          R.idxN = idxsz;
+          idxsz += J.nN;
+          recs.push_back(R);
+          ph.kmax = std::max(ph.kmax, kk);
+          ph.rmax = std::max(ph.rmax, r);
+          S.n_eliminated += 1;
+        }
+        DBuf W;
+        W.alloc((size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
+        ph.fac.alloc((size_t)std::max<long long>(facsz, 1) * sizeof(cplx), st);
+        FMMLU_CUDA(cudaMemsetAsync(ph.fac.p, 0, ph.fac.bytes, st));
+        ph.idx.alloc((size_t)std::max(idxsz, 1) * sizeof(int), st);
+        ph.fac_bytes = ph.fac.bytes + ph.idx.bytes;
+        track(h, W.bytes + ph.fac.bytes + ph.idx.bytes);
+        S.factor_bytes += ph.fac.bytes + ph.idx.bytes;
+        cplx* Wp = W.as<cplx>();
+        cplx* F = ph.fac.as<cplx>();
+
+        std::vector<CopyTask> cps, cpsT, cpsX;
+        std::vector<int> maps, hidx(idxsz);
+        std::vector<int> fslot, fpos, fbld;
+        std::vector<long long> ftab;
+        std::vector<long long> gjoff;
+        std::vector<int> gjdim;
+        struct FrameRef { int slot_off, tab_off, bld_off, ns; };
+        std::vector<FrameRef> frames;
+        for (size_t e = 0; e < el.size(); ++e) {
+          BoxJob& J = jobs[el[e]];
+          BoxRec& R = recs[e];
+          const int kk = J.k, r = R.r, b = J.b;
+          const int* pm = &hperm[J.permoff];
+          // local order [R | S] of B's columns
+          int rf = (int)maps.size();
+          for (int i = kk; i < b; ++i) maps.push_back(pm[i]);
+          for (int i = 0; i < kk; ++i) maps.push_back(pm[i]);
+          const std::vector<int>& aB = cur.act[J.a];
+          for (int i = 0; i < kk; ++i) hidx[R.idxS + i] = aB[pm[i]];
+          for (int i = 0; i < r; ++i) hidx[R.idxR + i] = aB[pm[kk + i]];
+          // W_B = [A_BB | A_BN] (rows/cols of B in [R|S] order), W_N = A_NB
+          CopyTask c{};
+          c.src = cur.off(J.a, J.a);
+          c.lds = b;
+          c.dst = WBoff[el[e]];
+          c.ldd = b;
+          c.rows = b;
+          c.cols = b;
+          c.trans = 0;
+          c.rmap_off = rf;
+          c.cmap_off = rf;
+          cps.push_back(c);
+          int noff = 0;
+          for (int o : J.N) {
+            int mo = (int)maps.size();
+            maps.insert(maps.end(), curpos[o].begin(), curpos[o].end());
+            int no_ = (int)curpos[o].size();
+            for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
+            CopyTask a{};
+            a.src = cur.off(J.a, o);
+            a.lds = b;
+            a.dst = WBoff[el[e]] + (long long)(b + noff) * b;
+            a.ldd = b;
+            a.rows = b;
+            a.cols = no_;
+            a.trans = 0;
+            a.rmap_off = rf;
+            a.cmap_off = mo;
+            cps.push_back(a);
+            CopyTask d{};
+            d.src = cur.off(o, J.a);
+            d.lds = (int)cur.act[o].size();
+            d.dst = WNoff[el[e]] + noff;
+            d.ldd = std::max(J.nN, 1);
+            d.rows = no_;
+            d.cols = b;
+            d.trans = 0;
+            d.rmap_off = mo;
+            d.cmap_off = rf;
+            cps.push_back(d);
+            noff += no_;
+          }
+          // T → factor store (k × r)
+          if (kk > 0 && r > 0) {
+            CopyTask t{};
+            t.src = J.Toff;
+            t.lds = kk;
+            t.dst = R.T;
+            t.ldd = kk;
+            t.rows = kk;
+            t.cols = r;
+            t.trans = 0;
+            t.rmap_off = -1;
+            t.cmap_off = -1;
+            cpsT.push_back(t);
+          }
+          // X_RR → Xinv slot (after E/F)
+          CopyTask x{};
+          x.src = WBoff[el[e]];
+          x.lds = b;
+          x.dst = R.Xi;
+          x.ldd = r;
+          x.rows = r;
+          x.cols = r;
+          x.trans = 0;
+          x.rmap_off = -1;
+          x.cmap_off = -1;
+          cpsX.push_back(x);
+          gjoff.push_back(R.Xi);
+          gjdim.push_back(r);
+          // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
+          FrameRef fr;
+          fr.slot_off = (int)fslot.size();
+          fr.ns = 1 + (int)J.N.size();
+          for (int i = 0; i < kk; ++i) {
+            fslot.push_back(0);
+            fpos.push_back(pm[i]);
+          }
+          for (size_t i = 0; i < J.N.size(); ++i)
+            for (int p : curpos[J.N[i]]) {
+              fslot.push_back(1 + (int)i);
+              fpos.push_back(p);
+            }
+          fr.tab_off = (int)ftab.size();
+          std::vector<int> own;
+          own.push_back(J.a);
+          for (int o : J.N) own.push_back(o);
+          for (int s1 = 0; s1 < fr.ns; ++s1)
+            for (int s2 = 0; s2 < fr.ns; ++s2) ftab.push_back(cur.off(own[s1], own[s2]));
+          fr.bld_off = (int)fbld.size();
+          for (int s1 = 0; s1 < fr.ns; ++s1) fbld.push_back((int)cur.act[own[s1]].size());
+          frames.push_back(fr);
+        }
+        if (maps.empty()) maps.push_back(0);
+        if (fslot.empty()) { fslot.push_back(0); fpos.push_back(0); }
+        if (ftab.empty()) ftab.push_back(-1);
+        if (fbld.empty()) fbld.push_back(0);
+        Stage s;
+        size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_fs = s.add(fslot),
+               o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
+               o_rec = s.add(recs);
+        s.upload(st);
+        launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), Wp, st);
+        launch_copy(s.ptr<CopyTask>(o_ct), (int)cpsT.size(), s.ptr<int>(o_m), Tb.as<cplx>(), F, st);
+        // E: W_B[R,:] −= Tᵀ W_B[S,:]
+        std::vector<GemmProblem> gp;
+        std::vector<GemmTile> gt;
+        const cplx m1 = cmk(-1.0, 0.0), p1 = cmk(1.0, 0.0);
+        for (size_t e = 0; e < el.size(); ++e) {
+          BoxJob& J = jobs[el[e]];
+          BoxRec& R = recs[e];
+          GemmProblem P{};
+          P.m = R.r;
+          P.n = J.b + J.nN;
+          P.k = R.k;
+          P.opA = kOpT;
+          P.opB = kOpN;
+          P.A = F + R.T;
+          P.lda = std::max(R.k, 1);
+          P.B = Wp + WBoff[el[e]] + R.r;
+          P.ldb = J.b;
+          P.C = Wp + WBoff[el[e]];
+          P.ldc = J.b;
+          add_gemm(gp, gt, P);
+        }
+        run_gemms(gp, gt, m1, 0, nullptr, st, keep);
+        // F: W_B[:,R] −= W_B[:,S] T ;  W_N[:,R] −= W_N[:,S] T
+        for (size_t e = 0; e < el.size(); ++e) {
+          BoxJob& J = jobs[el[e]];
+          BoxRec& R = recs[e];
+          GemmProblem P{};
+          P.m = J.b;
+          P.n = R.r;
+          P.k = R.k;
+          P.opA = kOpN;
+          P.opB = kOpN;
+          P.A = Wp + WBoff[el[e]] + (long long)R.r * J.b;
+          P.lda = J.b;
+          P.B = F + R.T;
+          P.ldb = std::max(R.k, 1);
+          P.C = Wp + WBoff[el[e]];
+          P.ldc = J.b;
+          add_gemm(gp, gt, P);
+          if (J.nN > 0) {
+            GemmProblem Q = P;
+            Q.m = J.nN;
+            Q.A = Wp + WNoff[el[e]] + (long long)R.r * J.nN;
+            Q.lda = J.nN;
+            Q.C = Wp + WNoff[el[e]];
+            Q.ldc = J.nN;
+            add_gemm(gp, gt, Q);
+          }
+        }
+        run_gemms(gp, gt, m1, 0, nullptr, st, keep);
+        // X_RR⁻¹ (Gauss-Jordan with partial pivoting)
+        launch_copy(s.ptr<CopyTask>(o_cx), (int)cpsX.size(), s.ptr<int>(o_m), Wp, F, st);
+        launch_gj_inverse(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
+                          ph.rmax);
+        // Up = X_RR⁻¹ X_{R(S∪N)} ;  Lp = X_{(S∪N)R} X_RR⁻¹
+        for (size_t e = 0; e < el.size(); ++e) {
+          BoxJob& J = jobs[el[e]];
+          BoxRec& R = recs[e];
+          const int kn = R.k + J.nN;
+          GemmProblem P{};
+          P.m = R.r;
+          P.n = kn;
+          P.k = R.r;
+          P.opA = kOpN;
+          P.opB = kOpN;
+          P.A = F + R.Xi;
+          P.lda = R.r;
+          P.B = Wp + WBoff[el[e]] + (long long)R.r * J.b;
+          P.ldb = J.b;
+          P.C = F + R.Up;
+          P.ldc = R.r;
+          add_gemm(gp, gt, P);
+          if (R.k > 0) {
+            GemmProblem Q{};
+            Q.m = R.k;
+            Q.n = R.r;
+            Q.k = R.r;
+            Q.opA = kOpN;
+            Q.opB = kOpN;
+            Q.A = Wp + WBoff[el[e]] + R.r;
+            Q.lda = J.b;
+            Q.B = F + R.Xi;
+            Q.ldb = R.r;
+            Q.C = F + R.Lp;
+            Q.ldc = kn;
+            add_gemm(gp, gt, Q);
+          }
+          if (J.nN > 0) {
+            GemmProblem Q{};
+            Q.m = J.nN;
+            Q.n = R.r;
+            Q.k = R.r;
+            Q.opA = kOpN;
+            Q.opB = kOpN;
+            Q.A = Wp + WNoff[el[e]];
+            Q.lda = J.nN;
+            Q.B = F + R.Xi;
+            Q.ldb = R.r;
+            Q.C = F + R.Lp + R.k;
+            Q.ldc = kn;
+            add_gemm(gp, gt, Q);
+          }
+        }
+        run_gemms(gp, gt, p1, 0, nullptr, st, keep);
+        // Schur complement: Δ_{(S∪N)²} −= Lp · X_{R(S∪N)}, scattered into the level BSR
+        for (size_t e = 0; e < el.size(); ++e) {
+          BoxJob& J = jobs[el[e]];
+          BoxRec& R = recs[e];
+          const int kn = R.k + J.nN;
+          const FrameRef& fr = frames[e];
+          GemmProblem P{};
+          P.m = kn;
+          P.n = kn;
+          P.k = R.r;
+          P.opA = kOpN;
+          P.opB = kOpN;
+          P.A = F + R.Lp;
+          P.lda = kn;
+          P.B = Wp + WBoff[el[e]] + (long long)R.r * J.b;
+          P.ldb = J.b;
+          P.C = nullptr;
+          P.ldc = 0;
+          P.row0 = 0;
+          P.col0 = 0;
+          P.ns = fr.ns;
+          P.slot = s.ptr<int>(o_fs) + fr.slot_off;
+          P.pos = s.ptr<int>(o_fp) + fr.slot_off;
+          P.tab = s.ptr<long long>(o_ft) + fr.tab_off;
+          P.bld = s.ptr<int>(o_fb) + fr.bld_off;
+          add_gemm(gp, gt, P);
+        }
+        run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep);
+        // index arena + records
+        FMMLU_CUDA(cudaMemcpyAsync(ph.idx.p, hidx.data(), hidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        ph.recs.alloc(recs.size() * sizeof(BoxRec), st);
+        FMMLU_CUDA(cudaMemcpyAsync(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), cudaMemcpyHostToDevice, st));
+        ph.nrec = (int)recs.size();
+        FMMLU_CUDA(cudaStreamSynchronize(st));
+        keep.clear();
+        keep.push_back(std::move(s.dev));
+        track(h, -(long long)W.bytes);
+        W.release();
+        h->phases.push_back(std::move(ph));
+      }
+      // update current actives: B keeps its skeleton S (sorted)
+      for (int j = 0; j < nj; ++j) {
+        BoxJob& J = jobs[j];
+        if (J.k == J.b) continue;
+        const int* pm = &hperm[J.permoff];
+        std::vector<int> sk(pm, pm + J.k);
+        std::sort(sk.begin(), sk.end());
+        total_active -= (J.b - J.k);
+        curpos[J.a] = sk;
+      }
+      track(h, -(long long)Tb.bytes);
+      Tb.release();
+      keep.clear();
+    }
+    // carry state to the next (coarser) level
+    for (int a = 0; a < no; ++a) {
+      std::vector<int> na;
+      for (int p : curpos[a]) na.push_back(cur.act[a][p]);
+      act[cur.owners[a]] = na;
+    }
+    std::fill(prevOwner.begin(), prevOwner.end(), -1);
+    for (int a = 0; a < no; ++a)
+      for (size_t i = 0; i < cur.act[a].size(); ++i) {
+        prevOwner[cur.act[a][i]] = a;
+        prevPos[cur.act[a][i]] = (int)i;
+      }
+    prev = std::move(cur);
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    S.t_levels_ms[lvl] = now_ms() - tl0;
+  }
+
+  // ------------------------------------------------------------------ root
+  double tr0 = now_ms();
+  std::vector<int> Bt;
+  if (prev.level >= 0) {
+    for (size_t a = 0; a < prev.owners.size(); ++a)
+      for (int g : act[prev.owners[a]]) Bt.push_back(g);
+  } else {
+    for (int i = 0; i < n; ++i) Bt.push_back(i);
+  }
+  std::sort(Bt.begin(), Bt.end());
+  const int n0 = (int)Bt.size();
+  h->n0 = n0;
+  S.n0 = n0;
+  if (n0 > 0) {
+    h->root.alloc((size_t)n0 * n0 * sizeof(cplx), st);
+    track(h, h->root.bytes);
+    S.factor_bytes += h->root.bytes;
+    std::vector<int> slot(n0), pos(n0), bld;
+    std::vector<long long> tab;
+    int ns = 1;
+    if (prev.level >= 0) {
+      ns = (int)prev.owners.size();
+      for (int i = 0; i < n0; ++i) {
+        slot[i] = prevOwner[Bt[i]];
+        pos[i] = prevPos[Bt[i]];
+      }
+      tab.assign((size_t)ns * ns, -1);
+      for (int a = 0; a < ns; ++a)
+        for (int b = 0; b < ns; ++b) tab[(size_t)a * ns + b] = prev.off(a, b);
+      for (int a = 0; a < ns; ++a) bld.push_back((int)prev.act[a].size());
+    } else {
+      std::fill(slot.begin(), slot.end(), -1);
+      tab.push_back(-1);
+      bld.push_back(0);
+    }
+    std::vector<BuildTask> tasks;
+    for (int i0 = 0; i0 < n0; i0 += kTile)
+      for (int j0 = 0; j0 < n0; j0 += kTile) {
+        BuildTask t{};
+        t.dst = 0;
+        t.ldd = n0;
+        t.rows_off = 0;
+        t.cols_off = 0;
+        t.i0 = i0;
+        t.j0 = j0;
+        t.ni = std::min(kTile, n0 - i0);
+        t.nj = std::min(kTile, n0 - j0);
+        t.ns = ns;
+        t.tab_off = 0;
+        t.bld_off = 0;
+        tasks.push_back(t);
+      }
+    Stage s;
+    size_t o_t = s.add(tasks), o_g = s.add(Bt), o_s = s.add(slot), o_p = s.add(pos), o_tab = s.add(tab),
+           o_b = s.add(bld);
+    s.upload(st);
+    launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
+                 s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), h->root.as<cplx>(), h->g, k, st);
+    DBuf scratch;
+    scratch.alloc(((size_t)n0 * n0 + 3 * (size_t)n0 + 8) * sizeof(cplx), st);
+    launch_gj_inverse_coop(h->root.as<cplx>(), n0, scratch.as<cplx>(), status.as<int>(), st);
+    h->root_rows.alloc((size_t)n0 * sizeof(int), st);
+    FMMLU_CUDA(cudaMemcpyAsync(h->root_rows.p, Bt.data(), n0 * sizeof(int), cudaMemcpyHostToDevice, st));
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+  }
+  if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
+  prev.bsr.release();
+  int hstatus = 0;
+  FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMMLU_CUDA(cudaStreamSynchronize(st));
+  S.t_root_ms = now_ms() - tr0;
+  if (hstatus) throw Error(FMMLU_ESINGULAR, "exactly singular pivot block (X_RR or root)");
+  h->k = k;
+  h->eps = eps;
+  h->factored = true;
+}
+
+void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
+  cudaStream_t st = h->stream;
+  const int n = (int)h->n;
+  const bool dev = is_device_ptr(rhs);
+  DBuf io, y;
+  cplx* b = reinterpret_cast<cplx*>(rhs);
+  if (!dev) {
+    io.alloc((size_t)n * nrhs * sizeof(cplx), st);
+    FMMLU_CUDA(cudaMemcpyAsync(io.p, rhs, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    b = io.as<cplx>();
+  }
+  y.alloc((size_t)n * nrhs * sizeof(cplx), st);
+  cplx* yp = y.as<cplx>();
+  launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
+  for (auto& ph : h->phases)
+    launch_solve_up(ph.recs.as<BoxRec>(), ph.nrec, ph.fac.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs, st, ph.kmax,
+                    ph.rmax);
+  DBuf tmp;
+  if (h->n0 > 0) {
+    tmp.alloc((size_t)h->n0 * nrhs * sizeof(cplx), st);
+    launch_root_apply(h->root.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), yp, n, nrhs, tmp.as<cplx>(), st);
+  }
+  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it)
+    launch_solve_down(it->recs.as<BoxRec>(), it->nrec, it->fac.as<cplx>(), it->idx.as<int>(), yp, n, nrhs, st,
+                      it->rmax);
+  launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
+  if (!dev)
+    FMMLU_CUDA(cudaMemcpyAsync(rhs, io.p, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  FMMLU_CUDA(cudaStreamSynchronize(st));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FMMLU_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(FMMLU_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(FMMLU_ECUDA, e.what());
+  }
+}
+
+void ensure_device() {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw Error(FMMLU_ECUDA, "no CUDA device available (libfmmlu has no CPU fallback)");
+  }
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int fmmlu_tree(const double* points, const double* normals, const double* weights, int64_t n,
+               int leaf_max, fmmlu_handle** out) {
+  if (out) *out = nullptr;
+  if (!out || !points || !normals || !weights) return fail(FMMLU_EINVAL, "NULL argument");
+  if (n < 1) return fail(FMMLU_EINVAL, "n must be >= 1");
+  if (n > (int64_t)INT32_MAX / 4) return fail(FMMLU_EINVAL, "n too large");
+  if (leaf_max < 1) return fail(FMMLU_EINVAL, "leaf_max must be >= 1");
+  fmmlu_handle* h = nullptr;
+  int rc = guarded([&] {
+    ensure_device();
+    double t0 = now_ms();
+    h = new fmmlu_handle();
+    FMMLU_CUDA(cudaGetDevice(&h->dev));
+    FMMLU_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    h->n = n;
+    std::vector<double> P(3 * n), N(3 * n), W(n);
+    auto fetch = [&](const double* src, double* dst, size_t cnt) {
+      if (is_device_ptr(src))
+        FMMLU_CUDA(cudaMemcpy(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+      else
+        std::memcpy(dst, src, cnt * sizeof(double));
+    };
+    fetch(points, P.data(), 3 * n);
+    fetch(normals, N.data(), 3 * n);
+    fetch(weights, W.data(), n);
+    for (int64_t i = 0; i < n; ++i) {
+      if (!(W[i] > 0.0) || !std::isfinite(W[i])) throw Error(FMMLU_EINVAL, "weights must be finite and > 0");
+      double nn = std::sqrt(N[3 * i] * N[3 * i] + N[3 * i + 1] * N[3 * i + 1] + N[3 * i + 2] * N[3 * i + 2]);
+      if (!(std::fabs(nn - 1.0) <= 1e-10)) throw Error(FMMLU_EINVAL, "normals must be unit vectors");
+      for (int a = 0; a < 3; ++a)
+        if (!std::isfinite(P[3 * i + a])) throw Error(FMMLU_EINVAL, "points must be finite");
+    }
+    h->tree.build(P.data(), n, leaf_max);
+    // geometry in tree order, SoA
+    std::vector<double> G(7 * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t p = h->tree.perm[i];
+      for (int a = 0; a < 3; ++a) {
+        G[a * n + i] = P[3 * p + a];
+        G[(3 + a) * n + i] = N[3 * p + a];
+      }
+      G[6 * n + i] = std::sqrt(W[p]);
+    }
+    h->geo.alloc(G.size() * sizeof(double), h->stream);
+    FMMLU_CUDA(cudaMemcpyAsync(h->geo.p, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    h->perm.alloc(n * sizeof(long long), h->stream);
+    FMMLU_CUDA(cudaMemcpyAsync(h->perm.p, h->tree.perm.data(), n * sizeof(long long), cudaMemcpyHostToDevice,
+                               h->stream));
+    FMMLU_CUDA(cudaStreamSynchronize(h->stream));
+    double* gp = h->geo.as<double>();
+    h->g = Geo{gp, gp + n, gp + 2 * n, gp + 3 * n, gp + 4 * n, gp + 5 * n, gp + 6 * n};
+    track(h, h->geo.bytes + h->perm.bytes);
+    fmmlu_stats_t& S = h->stats;
+    S.n = n;
+    S.nlevels = h->tree.nlevels;
+    S.nboxes = (int)h->tree.boxes.size();
+    S.nleaves = 0;
+    for (auto& b : h->tree.boxes) S.nleaves += b.leaf();
+    S.t_tree_ms = now_ms() - t0;
+  });
+  if (rc != FMMLU_OK) {
+    if (h) fmmlu_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return FMMLU_OK;
+}
+
+int fmmlu_factor(fmmlu_handle* h, double k, double eps) {
+  if (!h) return fail(FMMLU_EINVAL, "NULL handle");
+  if (!(k > 0.0) || !std::isfinite(k)) return fail(FMMLU_EINVAL, "k must be finite and > 0");
+  if (!(eps > 0.0 && eps < 1.0)) return fail(FMMLU_EINVAL, "eps must lie in (0, 1)");
+  return guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    double t0 = now_ms();
+    factor_impl(h, k, eps);
+    h->stats.t_factor_ms = now_ms() - t0;
+    h->stats.peak_bytes = (int64_t)h->peak_bytes;
+  });
+}
+
+int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs) {
+  if (!h) return fail(FMMLU_EINVAL, "NULL handle");
+  if (!rhs) return fail(FMMLU_EINVAL, "NULL rhs");
+  if (nrhs < 1) return fail(FMMLU_EINVAL, "nrhs must be >= 1");
+  if (!h->factored) return fail(FMMLU_ESTATE, "fmmlu_solve called before a successful fmmlu_factor");
+  return guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    double t0 = now_ms();
+    solve_impl(h, rhs, nrhs);
+    h->stats.t_solve_ms = now_ms() - t0;
+  });
+}
+
+int fmmlu_matvec(fmmlu_handle* h, double k, const void* x, void* y, int nrhs) {
+  if (!h) return fail(FMMLU_EINVAL, "NULL handle");
+  if (!x || !y || nrhs < 1) return fail(FMMLU_EINVAL, "bad x/y/nrhs");
+  if (!std::isfinite(k) || k < 0) return fail(FMMLU_EINVAL, "k must be finite and >= 0");
+  return guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    cudaStream_t st = h->stream;
+    const int n = (int)h->n;
+    size_t bytes = (size_t)n * nrhs * sizeof(cplx);
+    DBuf xi, xt, yt;
+    const cplx* xs = reinterpret_cast<const cplx*>(x);
+    if (!is_device_ptr(x)) {
+      xi.alloc(bytes, st);
+      FMMLU_CUDA(cudaMemcpyAsync(xi.p, x, bytes, cudaMemcpyHostToDevice, st));
+      xs = xi.as<cplx>();
+    }
+    xt.alloc(bytes, st);
+    yt.alloc(bytes, st);
+    launch_permute_in(xs, n, xt.as<cplx>(), n, nrhs, h->perm.as<long long>(), h->g.sw, 0, st);
+    launch_matvec(h->g, k, n, xt.as<cplx>(), yt.as<cplx>(), nrhs, st);
+    if (is_device_ptr(y)) {
+      launch_permute_out(yt.as<cplx>(), reinterpret_cast<cplx*>(y), n, n, nrhs, h->perm.as<long long>(), h->g.sw, 0,
+                         st);
+    } else {
+      launch_permute_out(yt.as<cplx>(), xt.as<cplx>(), n, n, nrhs, h->perm.as<long long>(), h->g.sw, 0, st);
+      FMMLU_CUDA(cudaMemcpyAsync(y, xt.p, bytes, cudaMemcpyDeviceToHost, st));
+    }
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int fmmlu_destroy(fmmlu_handle* h) {
+  if (!h) return FMMLU_OK;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->phases.clear();
+  h->root.release();
+  h->root_rows.release();
+  h->geo.release();
+  h->perm.release();
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return FMMLU_OK;
+}
+
+const char* fmmlu_last_error(void) { return g_last_error.c_str(); }
+
+int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out) {
+  if (!h || !out) return fail(FMMLU_EINVAL, "NULL argument");
+  *out = h->stats;
+  out->peak_bytes = (int64_t)h->peak_bytes;
+  return FMMLU_OK;
+}
+
+int fmmlu_set_stream(fmmlu_handle* h, void* s) {
+  if (!h) return fail(FMMLU_EINVAL, "NULL handle");
+  h->stream = s ? reinterpret_cast<cudaStream_t>(s) : h->own_stream;
+  return FMMLU_OK;
+}
+
+int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm) {
+  if (!h || !perm) return fail(FMMLU_EINVAL, "NULL argument");
+  std::memcpy(perm, h->tree.perm.data(), h->n * sizeof(int64_t));
+  return FMMLU_OK;
+}
+
+int fmmlu_probe_fp64(int kind, double* tflops) {
+  if (!tflops || (kind != 0 && kind != 1)) return fail(FMMLU_EINVAL, "bad argument");
+  return guarded([&] {
+    ensure_device();
+    *tflops = probe_fp64(kind);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,175 @@
+// Batched complex128 GEMM on DMMA (mma.sync.aligned.m8n8k4.f64) for sm_100a.
+// 64×64 output tile per CTA, 8 warps (2×4), warp tile 32×16, K-step 16 complex,
+// cp.async double-buffered shared-memory staging with zero-fill at the edges.
+// Complex product as 4 real DMMAs: Re += ArBr − AiBi, Im += ArBi + AiBr.
+#include "gemm.cuh"
+
+namespace fmmlu {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int PADA = BM + 2, PADB = BN + 2;  // +2 complex: conflict-free fragment loads
+constexpr int NT = 256;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int src = pred ? 16 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
+
+__device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0, int k0, cplx* As,
+                                           cplx* Bs, int tid) {
+#pragma unroll
+  for (int e = 0; e < (BM * BK) / NT; ++e) {
+    int idx = tid + e * NT;
+    int mm, kk;
+    if (P.opA == kOpN) {
+      mm = idx % BM;
+      kk = idx / BM;
+    } else {
+      kk = idx % BK;
+      mm = idx / BK;
+    }
+    int gm = m0 + mm, gk = k0 + kk;
+    bool ok = gm < P.m && gk < P.k;
+    const cplx* src = ok ? (P.opA == kOpN ? P.A + gm + (size_t)gk * P.lda
+                                          : P.A + gk + (size_t)gm * P.lda)
+                         : P.A;
+    cp_async16(&As[kk * PADA + mm], src, ok);
+  }
+#pragma unroll
+  for (int e = 0; e < (BN * BK) / NT; ++e) {
+    int idx = tid + e * NT;
+    int nn, kk;
+    if (P.opB == kOpN) {
+      kk = idx % BK;
+      nn = idx / BK;
+    } else {
+      nn = idx % BN;
+      kk = idx / BN;
+    }
+    int gn = n0 + nn, gk = k0 + kk;
+    bool ok = gn < P.n && gk < P.k;
+    const cplx* src = ok ? (P.opB == kOpN ? P.B + gk + (size_t)gn * P.ldb
+                                          : P.B + gn + (size_t)gk * P.ldb)
+                         : P.B;
+    cp_async16(&Bs[kk * PADB + nn], src, ok);
+  }
+}
+
+template <int SCATTER>
+__global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ probs,
+                                             const GemmTile* __restrict__ tiles, cplx alpha,
+                                             cplx* __restrict__ bsr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);      // [2][BK][PADA]
+  cplx* Bs = As + 2 * BK * PADA;                     // [2][BK][PADB]
+  const GemmTile T = tiles[blockIdx.x];
+  const GemmProblem P = probs[T.p];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 × 4 warps
+  const int m0 = T.tm * BM, n0 = T.tn * BN;
+
+  double accr[4][2][2], acci[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
+
+  const int nk = (P.k + BK - 1) / BK;
+  if (nk > 0) {
+    load_tiles(P, m0, n0, 0, As, Bs, tid);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait_all();
+    __syncthreads();
+    if (kt + 1 < nk) {
+      int s = (kt + 1) & 1;
+      load_tiles(P, m0, n0, (kt + 1) * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
+      cp_async_commit();
+    }
+    const cplx* as = As + (kt & 1) * BK * PADA;
+    const cplx* bs = Bs + (kt & 1) * BK * PADB;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int kk = ks * 4 + t;
+      cplx a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[kk * PADA + wm * 32 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = bs[kk * PADB + wn * 16 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(accr[i][j][0], accr[i][j][1], a[i].x, b[j].x);
+          dmma(accr[i][j][0], accr[i][j][1], a[i].y, -b[j].y);
+          dmma(acci[i][j][0], acci[i][j][1], a[i].x, b[j].y);
+          dmma(acci[i][j][0], acci[i][j][1], a[i].y, b[j].x);
+        }
+    }
+  }
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= P.m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn * 16 + j * 8 + 2 * t + h;
+        if (col >= P.n) continue;
+        cplx v = cmk(alpha.x * accr[i][j][h] - alpha.y * acci[i][j][h],
+                     alpha.x * acci[i][j][h] + alpha.y * accr[i][j][h]);
+        if (SCATTER) {
+          const int fr = P.row0 + row, fc = P.col0 + col;
+          const int s = P.slot[fr], q = P.slot[fc];
+          const long long off = P.tab[s * P.ns + q];
+          if (off >= 0) {
+            cplx* d = bsr + off + P.pos[fr] + (size_t)P.pos[fc] * P.bld[s];
+            atomicAdd(&d->x, v.x);
+            atomicAdd(&d->y, v.y);
+          }
+        } else {
+          cplx* d = P.C + row + (size_t)col * P.ldc;
+          cplx c = *d;
+          *d = cadd(c, v);
+        }
+      }
+  }
+}
+
+}  // namespace
+
+void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
+                  int scatter, cplx* bsr_base, cudaStream_t st) {
+  if (ntiles <= 0) return;
+  const size_t smem = 2 * BK * (PADA + PADB) * sizeof(cplx);
+  static bool init = false;
+  if (!init) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    init = true;
+  }
+  // grid.x limit is 2^31-1; tiles are enumerated explicitly
+  if (scatter)
+    k_gemm<1><<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
+  else
+    k_gemm<0><<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
+  FMMLU_LAUNCH();
+}
+
+}  // namespace fmmlu

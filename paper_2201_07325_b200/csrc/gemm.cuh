@@ -1,0 +1,44 @@
+// Batched variable-size complex128 GEMM on the FP64 tensor path (DMMA
+// mma.sync.m8n8k4.f64 — tcgen05 has no f64 kind), with two
+// epilogues:
+//   kStore      : C = C + alpha * op(A) op(B)                  (E/F transforms, LU updates)
+//   kScatterAdd : Δ[(S∪N) frame] += alpha * op(A) op(B), scattered with fp64 atomics
+//                 into the level's block-sparse "current matrix" store (the Schur
+//                 complement update −X_{(S∪N)R} X_RR⁻¹ X_{R(S∪N)}, PAPER.md L676-680,
+//                 L813-825).
+#pragma once
+#include "common.cuh"
+
+namespace fmmlu {
+
+enum : int { kOpN = 0, kOpT = 1 };
+
+struct GemmProblem {
+  int m, n, k;
+  int opA, opB;
+  int lda, ldb, ldc;
+  const cplx* A;
+  const cplx* B;
+  cplx* C;  // kStore: C itself; kScatterAdd: unused
+  // scatter epilogue: output row i (col j) of the problem maps to frame index
+  // row0 + i (col0 + j); frame index f -> (slot[f], pos[f]); block pointer for
+  // slot pair (s, t) is tab[s * ns + t] (complex offset into the BSR arena, -1 = absent),
+  // block leading dimension is ld[s].
+  int row0, col0, ns;
+  const int* slot;
+  const int* pos;
+  const long long* tab;
+  const int* bld;
+};
+
+struct GemmTile {
+  int p;   // problem index
+  int tm;  // tile row
+  int tn;  // tile col
+};
+
+// C = C + alpha * op(A) op(B) for each problem; `tiles` enumerates 64×64 output tiles.
+void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
+                  int scatter, cplx* bsr_base, cudaStream_t st);
+
+}  // namespace fmmlu

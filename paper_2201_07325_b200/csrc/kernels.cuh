@@ -1,0 +1,91 @@
+// Task descriptors and launchers for the libfmmlu device kernels.
+#pragma once
+#include "common.cuh"
+
+namespace fmmlu {
+
+// Gather-or-generate one dense block of the current scaled matrix Ã.
+// Entry (i, j): global indices gi = gidx[rows_off+i], gj = gidx[cols_off+j]; if the pair of
+// their previous-level owners (slot[...]) has a stored block (tab[si*ns+sj] >= 0) the value is
+// copied from it at (pos_i, pos_j) with leading dimension bld[si], else it is the pure kernel
+// entry √w_i K √w_j (½ on the diagonal).  dst is column-major with ld = rows.
+struct BuildTask {
+  long long dst;           // complex offset of the block's (0,0) in the destination arena
+  int ldd;                 // destination leading dimension (= block rows)
+  int rows_off, cols_off;  // offsets into gidx/slot/pos for the block's rows / cols
+  int i0, j0, ni, nj;      // the sub-tile of the block this task fills
+  int ns;                  // slot table dimension
+  int tab_off;             // offset into tab (ns*ns entries)
+  int bld_off;             // offset into bld (ns entries, row-slot leading dims)
+};
+
+// Copy a (possibly index-mapped / transposed) block.
+//   !trans: dst(i,j) = src(rm(i), cm(j));   trans: dst(i,j) = src(cm(j), rm(i))
+// rm(i) = rmap ? rmap[i] : i (rmap_off < 0 means identity), same for cm.
+struct CopyTask {
+  long long src, dst;  // complex offsets into src / dst arenas
+  int lds, ldd;
+  int rows, cols;      // dst dims
+  int trans;
+  int rmap_off, cmap_off;
+};
+
+// Proxy rows of M (§5.1.3; readings C3-C5): rows row0 .. row0+nγ-1 hold
+// s_γ K(y_ℓ, x_j) √w_j (outgoing, combined field with the box normals), rows row0+nγ ..
+// row0+2nγ-1 hold s_γ G(x_j, y_ℓ) √w_j (incoming single layer, transposed).
+struct ProxyTask {
+  long long dst;  // complex offset of M
+  int ld, row0, b, idx_off, ngamma;
+  double cx, cy, cz, rho, sg;
+};
+
+// Per-box ID on M (m × b, ld = m): CPQR with stopping rule |R_jj| ≤ eps·|R_00| (reading C9).
+struct IdTask {
+  long long M;    // complex offset of M in the workspace
+  int m, b;
+  int out_off;    // offset into perm output (b ints)
+  long long T;    // complex offset of T (k × (b-k)) in the T arena (capacity b*b)
+};
+
+// Elimination record of one box (offsets in the factor arena, complex units, and index arena).
+struct BoxRec {
+  long long T, Xi, Up, Lp;  // T: k×r, Xinv: r×r, Up: r×(k+nN), Lp: (k+nN)×r
+  int k, r, nN;
+  int idxS, idxR, idxN;     // offsets into the index arena (global tree-order indices)
+};
+
+void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const int* slot,
+                  const int* pos, const long long* tab, const int* bld, const cplx* src_arena,
+                  cplx* dst_arena, const Geo& g, double k, cudaStream_t st);
+void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cplx* src_arena,
+                 cplx* dst_arena, cudaStream_t st);
+void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
+                  double k, cudaStream_t st);
+void launch_cpqr(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out,
+                 double eps, cudaStream_t st, int bmax);
+void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
+                   cplx* tarena, cudaStream_t st);
+// in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
+void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx* arena,
+                       int* d_status, cudaStream_t st, int nmax);
+// cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
+void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
+// solve sweeps for one (level, colour) phase
+void launch_solve_up(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
+                     int ldy, int nrhs, cudaStream_t st, int kmax, int rmax);
+void launch_solve_down(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
+                       int ldy, int nrhs, cudaStream_t st, int rmax);
+// y[rows] = Xinv (n0×n0) · y[rows] for the root block
+void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
+                       cplx* tmp, cudaStream_t st);
+// elementwise helpers (caller order <-> tree order, √w scaling)
+void launch_permute_in(const cplx* src, int ld_src, cplx* dst, int n, int nrhs,
+                       const long long* perm, const double* sw, int mode, cudaStream_t st);
+void launch_permute_out(const cplx* src, cplx* dst, int ld_dst, int n, int nrhs,
+                        const long long* perm, const double* sw, int mode, cudaStream_t st);
+// brute-force y = A x (unscaled, tree order; w = sw²)
+void launch_matvec(const Geo& g, double k, int n, const cplx* x, cplx* y, int nrhs,
+                   cudaStream_t st);
+double probe_fp64(int kind);
+
+}  // namespace fmmlu

@@ -1,0 +1,182 @@
+"""Thin ctypes binding over libfmmlu.so (include/fmmlu.h).  Argument marshalling only:
+every step of the method runs in the library's CUDA kernels.  There is no CPU fallback —
+if the shared library or a CUDA device is missing, calls raise.
+
+Arrays may be NumPy arrays (host memory: the library copies in/out inside the call) or
+CUDA torch tensors (device memory, used in place).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_LIB = None
+
+FMMLU_ERRORS = {
+    -1: "EINVAL", -2: "EDEPTH", -3: "ESINGULAR", -4: "ENOMEM", -5: "ESTATE", -6: "ENOTIMPL", -7: "ECUDA",
+}
+
+
+class FmmluError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fmmlu error {code} ({FMMLU_ERRORS.get(code, '?')}): {msg}")
+        self.code = code
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("nlevels", ctypes.c_int32), ("nboxes", ctypes.c_int32),
+        ("nleaves", ctypes.c_int32), ("n_eliminated", ctypes.c_int32), ("n0", ctypes.c_int64),
+        ("max_rank", ctypes.c_int32), ("max_b", ctypes.c_int32), ("factor_bytes", ctypes.c_int64),
+        ("peak_bytes", ctypes.c_int64), ("t_tree_ms", ctypes.c_double), ("t_factor_ms", ctypes.c_double),
+        ("t_solve_ms", ctypes.c_double), ("t_root_ms", ctypes.c_double), ("t_levels_ms", ctypes.c_double * 24),
+        ("n_singular_warn", ctypes.c_int32), ("ranks_sum", ctypes.c_int32 * 24), ("boxes", ctypes.c_int32 * 24),
+    ]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if hasattr(v, "__len__") else v
+        return d
+
+
+EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_matvec", "fmmlu_destroy",
+           "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64")
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = False):
+    """Load libfmmlu.so (in-tree).  Raises if it is missing (no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise FmmluError(-7, f"{path} not built (run python -m paper_2201_07325_b200.build)")
+        _build.build()
+    L = ctypes.CDLL(path)
+    vp, i64, ci, cd = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.fmmlu_tree.argtypes = [vp, vp, vp, i64, ci, ctypes.POINTER(vp)]
+    L.fmmlu_factor.argtypes = [vp, cd, cd]
+    L.fmmlu_solve.argtypes = [vp, vp, ci]
+    L.fmmlu_matvec.argtypes = [vp, cd, vp, vp, ci]
+    L.fmmlu_destroy.argtypes = [vp]
+    L.fmmlu_last_error.restype = ctypes.c_char_p
+    L.fmmlu_last_error.argtypes = []
+    L.fmmlu_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+    L.fmmlu_set_stream.argtypes = [vp, vp]
+    L.fmmlu_tree_perm.argtypes = [vp, vp]
+    L.fmmlu_probe_fp64.argtypes = [ci, ctypes.POINTER(cd)]
+    for f in EXPORTS:
+        getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
+    _LIB = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FmmluError(rc, load().fmmlu_last_error().decode())
+
+
+def _ptr(a):
+    """Data pointer of a NumPy array (host) or a torch tensor (host or device)."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    raise TypeError(type(a))
+
+
+def _f64_rows3(a):
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.float64)
+    assert a.dtype.is_floating_point and a.element_size() == 8 and a.is_contiguous()
+    return a
+
+
+class FmmLu:
+    """One handle = one point set; factor() may be called repeatedly (new k / eps)."""
+
+    def __init__(self, points, normals, weights, leaf_max: int = 64):
+        L = load()
+        self._keep = [_f64_rows3(points), _f64_rows3(normals), _f64_rows3(weights)]
+        n = int(self._keep[2].shape[0])
+        h = ctypes.c_void_p()
+        _check(L.fmmlu_tree(_ptr(self._keep[0]), _ptr(self._keep[1]), _ptr(self._keep[2]), n, int(leaf_max),
+                            ctypes.byref(h)))
+        self.h = h
+        self.n = n
+        self._keep = None
+
+    def factor(self, k: float, eps: float):
+        _check(load().fmmlu_factor(self.h, float(k), float(eps)))
+        return self
+
+    def solve(self, rhs, nrhs: int | None = None):
+        """In place: rhs (n×nrhs column-major complex128, i.e. a Fortran-order NumPy array or a
+        transposed-contiguous torch tensor) is overwritten with A⁻¹ rhs.  Returns rhs."""
+        if nrhs is None:
+            nrhs = 1 if rhs.ndim == 1 else int(rhs.shape[1])
+        if isinstance(rhs, np.ndarray):
+            assert rhs.dtype == np.complex128 and (rhs.ndim == 1 or rhs.flags.f_contiguous)
+        _check(load().fmmlu_solve(self.h, _ptr(rhs), int(nrhs)))
+        return rhs
+
+    def matvec(self, k: float, x, y=None):
+        nrhs = 1 if x.ndim == 1 else int(x.shape[1])
+        if y is None:
+            y = np.empty_like(x, order="F") if isinstance(x, np.ndarray) else x.clone()
+        _check(load().fmmlu_matvec(self.h, float(k), _ptr(x), _ptr(y), nrhs))
+        return y
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(load().fmmlu_stats(self.h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def tree_perm(self) -> np.ndarray:
+        p = np.empty(self.n, dtype=np.int64)
+        _check(load().fmmlu_tree_perm(self.h, p.ctypes.data))
+        return p
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(load().fmmlu_set_stream(self.h, stream_ptr or None))
+
+    def close(self):
+        if getattr(self, "h", None):
+            load().fmmlu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# module-level names mirroring the C ABI
+def fmmlu_tree(points, normals, weights, leaf_max: int = 64) -> FmmLu:
+    return FmmLu(points, normals, weights, leaf_max)
+
+
+def fmmlu_factor(h: FmmLu, k: float, eps: float) -> FmmLu:
+    return h.factor(k, eps)
+
+
+def fmmlu_solve(h: FmmLu, rhs, nrhs: int | None = None):
+    return h.solve(rhs, nrhs)
+
+
+def probe_fp64(kind: int) -> float:
+    v = ctypes.c_double()
+    _check(load().fmmlu_probe_fp64(int(kind), ctypes.byref(v)))
+    return v.value

@@ -1,0 +1,147 @@
+"""GPU parity: libfmmlu (CUDA, through the C ABI) against the CPU oracle on the same
+seeded inputs (BASELINE.json north_star: solution relative difference ≤ 10ε and
+residual ‖Ax−b‖/‖b‖ ≤ 10ε against a brute-force matvec)."""
+import math
+
+import numpy as np
+import pytest
+
+import fmmlu_inputs as fi
+from oracle import dense, kernel as okern, rss
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2201_07325_b200 import fmmlu
+    fmmlu.load()
+    return fmmlu
+
+
+def _gpu_solve(F, g, k, eps, leaf, b):
+    h = F.FmmLu(g.points, g.normals, g.weights, leaf).factor(k, eps)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    return h, x
+
+
+def test_tree_order_matches_oracle(F):
+    g = fi.bump_sphere(n_base=3000, n_cap=1500, theta_c=0.05, height=0.02)
+    h = F.FmmLu(g.points, g.normals, g.weights, 16)
+    from oracle.tree import Tree
+    t = Tree(g.points, 16)
+    assert np.array_equal(h.tree_perm(), t.perm)
+    s = h.stats()
+    assert s["nlevels"] == t.nlevels and s["nboxes"] == len(t.level)
+
+
+def test_matvec_kernel_parity(F):
+    g = fi.ellipsoid(1500)
+    k = 2 * math.pi
+    x = np.asfortranarray(fi.gaussian_rhs(g.n, 3, 5))
+    h = F.FmmLu(g.points, g.normals, g.weights, 64)
+    y = h.matvec(k, x)
+    yo = okern.matvec_unscaled(k, g.points, g.normals, g.weights, x)
+    assert np.max(np.abs(y - yo)) <= 1e-13 * np.max(np.abs(yo))
+
+
+def test_single_leaf_equals_dense_lu(F):
+    g = fi.fibonacci_sphere(60)
+    b = fi.gaussian_rhs(g.n, 2, 1)
+    h, x = _gpu_solve(F, g, 1.0, 1e-6, 64, b)
+    xd = dense.dense_solve(g.points, g.normals, g.weights, 1.0, b)
+    assert h.stats()["n0"] == 60
+    assert dense.rel_diff(x, xd) < 1e-12
+
+
+@pytest.mark.parametrize("case", ["cfg1", "ellipsoid3000", "cube1500"])
+def test_parity_vs_oracle(F, case):
+    eps = 1e-6
+    if case == "cfg1":
+        g, k, leaf, nrhs = fi.config_geometry("cfg1"), 1.0, 64, 1
+    elif case == "ellipsoid3000":
+        g, k, leaf, nrhs = fi.ellipsoid(3000), 2 * math.pi, 32, 3
+    else:
+        g, k, leaf, nrhs = fi.random_cube(1500, seed=2), 3.0, 16, 2
+    b = fi.gaussian_rhs(g.n, nrhs, 0)
+    h, x = _gpu_solve(F, g, k, eps, leaf, b)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf)
+    xo = rss.solve(f, b)
+    st = h.stats()
+    assert st["n0"] > 0
+    assert dense.rel_diff(x, xo) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
+    # structural parity (P8): same tree, comparable root size
+    assert abs(st["n0"] - f.stats["n0"]) <= 0.05 * f.stats["n0"] + 2
+
+
+def test_tight_eps_matches_dense(F):
+    g = fi.ellipsoid(2000)
+    k = 2 * math.pi
+    b = fi.gaussian_rhs(g.n, 2, 3)
+    h, x = _gpu_solve(F, g, k, 1e-12, 32, b)
+    xd = dense.dense_solve(g.points, g.normals, g.weights, k, b)
+    assert h.stats()["n_eliminated"] > 0
+    assert dense.rel_diff(x, xd) < 1e-9
+
+
+def test_device_pointers_equal_host(F):
+    import torch
+    g = fi.ellipsoid(2500)
+    k = 2 * math.pi
+    b = fi.gaussian_rhs(g.n, 4, 7)
+    h, x = _gpu_solve(F, g, k, 1e-6, 32, b)
+    bt = torch.from_numpy(np.ascontiguousarray(b.T)).cuda()   # (nrhs, n) C-order = n×nrhs col-major
+    h.solve(bt, nrhs=4)
+    xt = bt.cpu().numpy().T
+    assert np.max(np.abs(xt - x)) <= 1e-12 * np.max(np.abs(x))
+    # geometry from device tensors gives the same tree and factorization
+    P = torch.from_numpy(g.points).cuda()
+    N = torch.from_numpy(g.normals).cuda()
+    W = torch.from_numpy(g.weights).cuda()
+    h2 = F.FmmLu(P, N, W, 32).factor(k, 1e-6)
+    assert h2.stats()["n0"] == h.stats()["n0"]
+
+
+def test_edge_errors(F):
+    g = fi.fibonacci_sphere(200)
+    h = F.FmmLu(g.points, g.normals, g.weights, 16)
+    x = np.asfortranarray(fi.gaussian_rhs(g.n, 1, 0))
+    with pytest.raises(F.FmmluError) as e:
+        h.solve(x)
+    assert e.value.code == -5          # ESTATE: solve before factor
+    with pytest.raises(F.FmmluError) as e:
+        h.factor(-1.0, 1e-6)
+    assert e.value.code == -1
+    with pytest.raises(F.FmmluError) as e:
+        h.factor(1.0, 1.5)
+    assert e.value.code == -1
+    pts = np.zeros((10, 3))
+    pts[:, 0] = 1.0
+    pts[0, 0] = 0.0
+    nrm = np.tile([0.0, 0.0, 1.0], (10, 1))
+    with pytest.raises(F.FmmluError) as e:
+        F.FmmLu(pts, nrm, np.ones(10), 2)
+    assert e.value.code == -2          # EDEPTH: duplicate points
+
+
+def test_cfg2_full_size_residual(F):
+    """BASELINE configs[1] at full size: residual ≤ 10ε with the GPU brute-force matvec,
+    whose rows are themselves checked one by one against the oracle kernel."""
+    c = fi.CONFIGS["cfg2"]
+    g = fi.config_geometry("cfg2")
+    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    h, x = _gpu_solve(F, g, c["k"], c["eps"], c["leaf_max"], b)
+    Ax = h.matvec(c["k"], x)
+    res = np.max(np.linalg.norm(Ax - b, axis=0) / np.linalg.norm(b, axis=0))
+    assert res <= 10 * c["eps"]
+    rows = np.random.default_rng(0).choice(g.n, 40, replace=False)
+    for i in rows:
+        Ki = okern.combined_field(c["k"], g.points[i:i + 1], g.points, g.normals)[0]
+        Ki[i] = 0.0
+        yi = (Ki * g.weights) @ x + 0.5 * x[i]
+        assert np.max(np.abs(yi - Ax[i])) <= 1e-11 * np.max(np.abs(yi)) + 1e-13
