@@ -30,7 +30,7 @@ b = np.asfortranarray(fi.gaussian_rhs(g.n, 4, 0))
 for rep in range(3):
     t = time.time(); h = F.FmmLu(g.points, g.normals, g.weights, 64); t1 = time.time()
     h.factor(c["k"], c["eps"]); t2 = time.time()
-    xg = b.copy(); h.solve(xg); t3 = time.time()
+    xg = b.copy(order="F"); h.solve(xg); t3 = time.time()
     st = h.stats()
     print("cfg2 tree %.1f ms factor %.1f ms solve %.1f ms" % ((t1-t)*1e3, (t2-t1)*1e3, (t3-t2)*1e3),
           "n0", st["n0"], "levels ms", [round(v,1) for v in st["t_levels_ms"][:6]], "root ms", round(st["t_root_ms"],1), flush=True)
