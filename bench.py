@@ -1,0 +1,324 @@
+"""bench.py — FMM-LU hot path on B200 (BASELINE.json metric: factor unknowns/s and solve
+ms/RHS at ε = 1e-6, complex128, 1 B200).
+
+Workload (N=1): BASELINE.json configs[1] = "cfg2": ellipsoid (0.5, 1, 2), n = 20,000,
+k = 2π, leaf ≤ 64, ε = 1e-6, 4 Gaussian RHS (seed 0).  One STEP = the whole hot path
+(every SURVEY §8(a) row): fmmlu_tree + fmmlu_factor + fmmlu_solve through the C ABI.
+value = unknowns processed per second of step time (tree + factor + solve), summed over
+ranks ("replicas only"); factor-only unknowns/s and solve ms/RHS are extra keys.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+`--impl reference` times the CPU oracle (oracle/, plain NumPy/SciPy) on a bounded sample of
+the same workload family, on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fmmlu_inputs as fi  # noqa: E402
+
+METRIC = "FMM-LU factor unknowns/s and solve ms/RHS at eps=1e-6 (complex128, 1 B200)"
+UNIT = "unknowns/s"
+CFG = "cfg2"
+ORACLE_SAMPLE_N = 4000  # bounded CPU sample (same geometry family / k / leaf / eps)
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """Samples nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args):
+    """CPU oracle arm (test-infrastructure oracle, untuned) on a bounded sample."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import rss
+    c = fi.CONFIGS[CFG]
+    g = fi.ellipsoid(ORACLE_SAMPLE_N)
+    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        f = rss.factor(g.points, g.normals, g.weights, c["k"], c["eps"], c["leaf_max"])
+        rss.solve(f, b)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    cores = os.cpu_count()
+    value = g.n / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"{CFG} family sample: ellipsoid n={g.n}, k=2pi, leaf 64, eps 1e-6, 4 RHS",
+                   "sample_of": CFG},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"oracle tree+factor+solve of the cfg2-family ellipsoid at n={g.n} "
+                                   f"(full cfg2 n=20000 takes ~200 s on 8 cores)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_sample():
+    from oracle import rss
+    c = fi.CONFIGS[CFG]
+    g = fi.ellipsoid(ORACLE_SAMPLE_N)
+    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    t0 = time.perf_counter()
+    f = rss.factor(g.points, g.normals, g.weights, c["k"], c["eps"], c["leaf_max"])
+    rss.solve(f, b)
+    dt = time.perf_counter() - t0
+    return {"value": g.n / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"oracle (NumPy/SciPy, untuned) tree+factor+solve of the cfg2-family ellipsoid at "
+                      f"n={g.n} ({dt:.1f} s); full cfg2 is ~200 s on 8 cores"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    from paper_2201_07325_b200 import fmmlu as F
+    F.load()
+
+    c = fi.CONFIGS[CFG]
+    g = fi.config_geometry(CFG)
+    n, nrhs = g.n, c["nrhs"]
+    b_host = np.asfortranarray(fi.gaussian_rhs(n, nrhs, 0))
+    # inputs resident in HBM for the device-timed leg
+    P = torch.from_numpy(g.points).to(dev)
+    N = torch.from_numpy(g.normals).to(dev)
+    W = torch.from_numpy(g.weights).to(dev)
+    B = torch.from_numpy(np.ascontiguousarray(b_host.T)).to(dev)  # (nrhs, n) C = n×nrhs col-major
+    X = torch.empty_like(B)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+
+    def step_device():
+        h = F.FmmLu(P, N, W, c["leaf_max"])
+        h.set_stream(stream.cuda_stream)
+        h.factor(c["k"], c["eps"])
+        X.copy_(B)
+        h.solve(X, nrhs=nrhs)
+        return h
+
+    def step_e2e():
+        pts, nrm, wts = g.points.copy(), g.normals.copy(), g.weights.copy()  # host buffers
+        h = F.FmmLu(pts, nrm, wts, c["leaf_max"])
+        h.set_stream(stream.cuda_stream)
+        h.factor(c["k"], c["eps"])
+        x = b_host.copy(order="F")
+        h.solve(x)           # H2D of rhs and D2H of the result inside the call
+        return h, x
+
+    for _ in range(args.warmup):
+        h = step_device()
+    torch.cuda.synchronize()
+
+    # ---- device-timed leg (CUDA events on the launch stream, L2 flushed between steps)
+    ev = []
+    stats = []
+    with Clocks(torch.cuda.current_device()) as clk:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            h = step_device()
+            e1.record(stream)
+            ev.append((e0, e1))
+            stats.append(h.stats())
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t_step = float(np.mean(ms))
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    st = stats[-1]
+    t_fac = float(np.mean([s["t_factor_ms"] for s in stats]))
+    t_sol = float(np.mean([s["t_solve_ms"] for s in stats]))
+    t_tree = float(np.mean([s["t_tree_ms"] for s in stats]))
+
+    # ---- end-to-end leg through the public API with host buffers
+    e2e_ms = []
+    resid = None
+    for _ in range(max(2, min(3, args.steps))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h2, x = step_e2e()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    # residual of the last e2e solve with the GPU brute-force matvec
+    Ax = h2.matvec(c["k"], x)
+    resid = float(np.max(np.linalg.norm(Ax - b_host, axis=0) / np.linalg.norm(b_host, axis=0)))
+    t_e2e = float(np.mean(e2e_ms))
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+
+    # ---- roofline of the dominant kernel class (events recorded inside libfmmlu)
+    cls = F.KERNEL_CLASSES
+    cms = st["class_ms"][:len(cls)]
+    dom = int(np.argmax(cms))
+    dmma_tf = F.probe_fp64(1)
+    peaks = _peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    fl, by, t = st["class_flops"][dom], st["class_bytes"][dom], cms[dom]
+    per_launch = max(1, st["class_launches"][dom])
+    if cls[dom] in ("schur", "ef", "panel", "qr"):
+        achieved = fl / (t * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": dmma_tf, "unit": "TFLOP/s",
+                "frac": achieved / dmma_tf, "traffic": None, "kernel": cls[dom],
+                "peak_source": "FP64 DMMA m8n8k4 probe measured in this run (MEASURED_PEAKS has no FP64 entry)",
+                "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch}
+    elif cls[dom] in ("build", "gather", "solve"):
+        achieved = by / (t * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "kernel": cls[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "bytes_per_launch": by / per_launch, "ms_per_launch": t / per_launch}
+    else:
+        dfma_tf = F.probe_fp64(0)
+        achieved = fl / (t * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": dfma_tf, "unit": "TFLOP/s",
+                "frac": achieved / dfma_tf, "traffic": None, "kernel": cls[dom],
+                "peak_source": "FP64 DFMA probe measured in this run",
+                "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch}
+    breakdown = {cls[i]: {"ms": round(cms[i], 3), "share": round(cms[i] / max(1e-9, sum(cms)), 4),
+                          "tflops": round(st["class_flops"][i] / max(1e-9, cms[i]) / 1e9, 3),
+                          "gbs": round(st["class_bytes"][i] / max(1e-9, cms[i]) / 1e6, 1)}
+                 for i in range(len(cls))}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample()
+    h2d = g.points.nbytes + g.normals.nbytes + g.weights.nbytes + b_host.nbytes
+    d2h = b_host.nbytes
+    line = {
+        "metric": METRIC, "value": world * n / (t_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"{CFG}: ellipsoid (0.5,1,2) n={n}, k=2pi, leaf 64, eps 1e-6, {nrhs} RHS",
+                   "step": "fmmlu_tree + fmmlu_factor + fmmlu_solve (device-resident inputs)",
+                   "parallelism": f"replicas x{world}", "l2": "flushed (256 MB write) between steps"},
+        "factor_unknowns_per_s": n / (t_fac * 1e-3),
+        "solve_ms_per_rhs": t_sol / nrhs,
+        "tree_ms": t_tree, "factor_ms": t_fac, "solve_ms": t_sol,
+        "n0": st["n0"], "peak_mem_bytes": st["peak_bytes"], "factor_bytes": st["factor_bytes"],
+        "residual": resid,
+        "e2e": {"value": world * n / (t_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e},
+        "gpu_launches": int(st["n_launches"]),
+        "roofline": roof,
+        "kernel_breakdown": breakdown,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

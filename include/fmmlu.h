@@ -73,7 +73,28 @@ typedef struct fmmlu_stats_t {
   int32_t n_singular_warn;/* near-singular pivot warnings                         */
   int32_t ranks_sum[24];  /* Σ|S| per level                                       */
   int32_t boxes[24];      /* skeletonized boxes per level                         */
+  int64_t n_launches;     /* kernels launched by the last factor + solve          */
+  /* Per kernel class (FMMLU_K_* below), accumulated over the last factor and the
+   * last solve: device time from CUDA events recorded on the launch stream, and the
+   * ALGORITHMIC real flops / bytes of the launches in that class.                 */
+  double class_ms[16];
+  double class_flops[16];
+  double class_bytes[16];
+  int64_t class_launches[16];
 } fmmlu_stats_t;
+
+/* kernel classes for fmmlu_stats_t.class_* */
+#define FMMLU_K_BUILD 0   /* level block store: kernel generation + carry-over      */
+#define FMMLU_K_GATHER 1  /* M / W gathers, proxy rows                              */
+#define FMMLU_K_QR 2      /* ID: Householder QR of M                                */
+#define FMMLU_K_CPQR 3    /* ID: column-pivoted QR + T = R11^-1 R12                 */
+#define FMMLU_K_EF 4      /* E/F transforms (GEMM)                                  */
+#define FMMLU_K_INV 5     /* X_RR^-1 (Gauss-Jordan)                                 */
+#define FMMLU_K_PANEL 6   /* Up / Lp panels (GEMM)                                  */
+#define FMMLU_K_SCHUR 7   /* Schur-complement GEMM + scatter-add                    */
+#define FMMLU_K_ROOT 8    /* root block build + inverse                             */
+#define FMMLU_K_SOLVE 9   /* solve sweeps + root apply                              */
+#define FMMLU_K_NCLASS 10
 
 /* Build the adaptive level-restricted octree over the n points
  * (readings C14, C6-C8 of SURVEY.md §8(c)).

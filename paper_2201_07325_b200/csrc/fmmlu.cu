@@ -124,6 +124,57 @@ double now_ms() {
       .count();
 }
 
+// Per-kernel-class device timing with CUDA events recorded on the launch stream;
+// resolved at the driver's existing synchronisation points.
+struct Prof {
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  double ms[16] = {}, flops[16] = {}, bytes[16] = {};
+  long long launches[16] = {};
+  long long total_launches = 0;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      FMMLU_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  int begin(int cls, cudaStream_t st) {
+    Rec r{cls, ev(), ev()};
+    FMMLU_CUDA(cudaEventRecord(r.a, st));
+    pending.push_back(r);
+    return (int)pending.size() - 1;
+  }
+  void end(int id, cudaStream_t st) { FMMLU_CUDA(cudaEventRecord(pending[id].b, st)); }
+  void add(int cls, double fl, double by, long long nl) {
+    flops[cls] += fl;
+    bytes[cls] += by;
+    launches[cls] += nl;
+    total_launches += nl;
+  }
+  void resolve() {  // call after the stream has been synchronised
+    for (auto& r : pending) {
+      float t = 0.f;
+      FMMLU_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      ms[r.cls] += t;
+    }
+    pending.clear();
+    used = 0;
+  }
+  void reset() {
+    pending.clear();
+    used = 0;
+    for (int i = 0; i < 16; ++i) ms[i] = flops[i] = bytes[i] = 0, launches[i] = 0;
+    total_launches = 0;
+  }
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 }  // namespace
 
 struct fmmlu_handle {
@@ -144,6 +195,7 @@ struct fmmlu_handle {
   int64_t n0 = 0;
   fmmlu_stats_t stats{};
   size_t cur_bytes = 0, peak_bytes = 0;
+  Prof prof;
 };
 
 namespace {
@@ -171,16 +223,244 @@ void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, con
     for (int tn = 0; tn < (p.n + kTile - 1) / kTile; ++tn) tiles.push_back({id, tm, tn});
 }
 
+// Algorithmic work of a batch: 8mnk real flops per complex GEMM; bytes = read A and B once,
+// read-modify-write C once (16 B per complex element).
+void gemm_work(const std::vector<GemmProblem>& probs, double& fl, double& by) {
+  fl = by = 0;
+  for (auto& p : probs) {
+    fl += 8.0 * p.m * (double)p.n * p.k;
+    by += 16.0 * ((double)p.m * p.k + (double)p.k * p.n) + 32.0 * (double)p.m * p.n;
+  }
+}
+
 void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cplx alpha,
-               int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep) {
+               int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep, Prof& P, int cls) {
   if (tiles.empty()) return;
   Stage s;
   size_t op = s.add(probs), ot = s.add(tiles);
   s.upload(st);
+  double fl, by;
+  gemm_work(probs, fl, by);
+  int id = P.begin(cls, st);
   gemm_batched(s.ptr<GemmProblem>(op), s.ptr<GemmTile>(ot), (int)tiles.size(), alpha, scatter, bsr, st);
+  P.end(id, st);
+  P.add(cls, fl, by, 1);
   keep.push_back(std::move(s.dev));
   probs.clear();
   tiles.clear();
+}
+
+// ---------------------------------------------------------------------------- TSQR + blocked QR
+// R0_j = triu(R) of M_j = Q R for each box j (only R is needed: CPQR(R0) selects the same
+// pivots and T as CPQR(M) because Qᴴ preserves column norms and inner products).  Rows of M
+// are split into chunks of ≤ H rows (H ≥ 2b), each chunk is QR-factored by the blocked
+// Householder method (panel in shared memory, WY trailing update on the DMMA GEMM), the
+// chunks' R factors are stacked, and the process repeats until one chunk remains (TSQR).
+struct R0Out {
+  DBuf R;                    // compact R0 matrices (ld = rows)
+  std::vector<long long> off;
+  std::vector<int> rows;
+};
+
+void tsqr_R0(fmmlu_handle* h, cplx* Mbase, const std::vector<long long>& moff,
+             const std::vector<int>& mrows, const std::vector<int>& bcol, R0Out& out) {
+  cudaStream_t st = h->stream;
+  Prof& P = h->prof;
+  const int nbx = (int)moff.size();
+  int bmax = 0;
+  for (int b : bcol) bmax = std::max(bmax, b);
+  int NB = 16, H = 800;
+  if (2 * bmax >= H) { NB = 8; H = 1600; }
+  if (2 * bmax >= H) throw Error(FMMLU_ENOTIMPL, "box with more than 799 actives: TSQR chunking not built");
+  long long r0tot = 0;
+  out.off.assign(nbx, 0);
+  out.rows.assign(nbx, 0);
+  for (int j = 0; j < nbx; ++j) {
+    out.off[j] = r0tot;
+    r0tot += (long long)bcol[j] * bcol[j];
+  }
+  out.R.alloc((size_t)std::max<long long>(r0tot, 1) * sizeof(cplx), st);
+  std::vector<cplx*> base(nbx, Mbase);
+  std::vector<long long> off = moff;
+  std::vector<int> rows = mrows, ld = mrows;
+  std::vector<char> done(nbx, 0);
+  DBuf arena;  // stacked matrices of the current round (owns them after round 0)
+  for (int round = 0;; ++round) {
+    struct Ch { int box; int h; long long r0; };
+    std::vector<Ch> chs;
+    long long qws = 0;
+    for (int j = 0; j < nbx; ++j) {
+      if (done[j]) continue;
+      int nch = rows[j] <= H ? 1 : (rows[j] + H - 1) / H;
+      int bh = rows[j] / nch, ex = rows[j] % nch;
+      long long r0 = 0;
+      for (int c = 0; c < nch; ++c) {
+        int hc = bh + (c < ex ? 1 : 0);
+        chs.push_back({j, hc, r0});
+        r0 += hc;
+        qws += 2LL * hc * NB + (long long)NB * bcol[j];
+      }
+    }
+    DBuf qw;
+    qw.alloc((size_t)qws * sizeof(cplx), st);
+    std::vector<QrChunk> qc;
+    long long q = 0;
+    int jmax = 0;
+    for (auto& c : chs) {
+      QrChunk x{};
+      x.A = base[c.box] + off[c.box] + c.r0;
+      x.lda = ld[c.box];
+      x.h = c.h;
+      x.b = bcol[c.box];
+      x.V = qw.as<cplx>() + q;
+      q += (long long)c.h * NB;
+      x.Z = qw.as<cplx>() + q;
+      q += (long long)c.h * NB;
+      x.W = qw.as<cplx>() + q;
+      q += (long long)NB * x.b;
+      qc.push_back(x);
+      jmax = std::max(jmax, std::min(c.h, x.b));
+    }
+    // all panels' GEMM batches, uploaded once
+    std::vector<GemmProblem> gp;
+    std::vector<GemmTile> gt;
+    struct Launch { size_t p0, t0, nt; };
+    std::vector<Launch> l1, l2;
+    double fl = 0, by = 0;
+    for (int j0 = 0; j0 < jmax; j0 += NB) {
+      for (int pass = 0; pass < 2; ++pass) {
+        std::vector<GemmProblem> pp;
+        std::vector<GemmTile> tt;
+        for (auto& x : qc) {
+          int kmax = std::min(x.h, x.b);
+          if (j0 >= kmax) continue;
+          int jb = std::min(NB, kmax - j0), nt = x.b - j0 - jb, hr = x.h - j0;
+          if (nt <= 0) continue;
+          GemmProblem g{};
+          cplx* At = x.A + j0 + (size_t)(j0 + jb) * x.lda;
+          if (pass == 0) {  // W = Vᴴ A_t
+            g.m = jb; g.n = nt; g.k = hr;
+            g.opA = kOpC; g.opB = kOpN;
+            g.A = x.V; g.lda = x.h;
+            g.B = At; g.ldb = x.lda;
+            g.C = x.W; g.ldc = NB;
+          } else {          // A_t −= Z W
+            g.m = hr; g.n = nt; g.k = jb;
+            g.opA = kOpN; g.opB = kOpN;
+            g.A = x.Z; g.lda = x.h;
+            g.B = x.W; g.ldb = NB;
+            g.C = At; g.ldc = x.lda;
+          }
+          add_gemm(pp, tt, g);
+        }
+        double f1, b1;
+        gemm_work(pp, f1, b1);
+        fl += f1;
+        by += b1;
+        Launch L{gp.size(), gt.size(), tt.size()};
+        for (auto& t : tt) t.p += (int)gp.size() - (int)0;  // local → global index fixed below
+        gp.insert(gp.end(), pp.begin(), pp.end());
+        gt.insert(gt.end(), tt.begin(), tt.end());
+        (pass == 0 ? l1 : l2).push_back(L);
+      }
+    }
+    // tile problem indices are global; pass the full problem array to every launch
+    Stage s;
+    size_t o_c = s.add(qc), o_p = s.add(gp), o_t = s.add(gt);
+    s.upload(st);
+    int id = P.begin(FMMLU_K_QR, st);
+    int pi = 0;
+    for (int j0 = 0; j0 < jmax; j0 += NB, ++pi) {
+      launch_qr_panel(s.ptr<QrChunk>(o_c), (int)qc.size(), j0, NB, st);
+      P.add(FMMLU_K_QR, 0, 0, 1);
+      const Launch& a = l1[pi];
+      const Launch& b = l2[pi];
+      if (a.nt) {
+        gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_t) + a.t0, (int)a.nt, cmk(1.0, 0.0), 0, nullptr, st);
+        P.add(FMMLU_K_QR, 0, 0, 1);
+      }
+      if (b.nt) {
+        gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_t) + b.t0, (int)b.nt, cmk(-1.0, 0.0), 0, nullptr, st);
+        P.add(FMMLU_K_QR, 0, 0, 1);
+      }
+    }
+    P.end(id, st);
+    // panel flops (Householder on h×jb panels) + GEMM flops
+    for (auto& x : qc) {
+      double m_ = x.h, n_ = std::min(x.h, x.b);
+      fl += 8.0 * (m_ * n_ * NB);  // panel BLAS-2 part (upper bound)
+    }
+    P.add(FMMLU_K_QR, fl, by, 0);
+    // collect: finished boxes → R0; others → stacked matrices for the next round
+    std::vector<CopyTask> fin, stk;
+    std::vector<long long> noff(nbx, 0);
+    std::vector<int> nrows(nbx, 0);
+    long long ntot = 0;
+    size_t ci = 0;
+    for (int j = 0; j < nbx; ++j) {
+      if (done[j]) continue;
+      size_t c0 = ci;
+      while (ci < chs.size() && chs[ci].box == j) ++ci;
+      const int b = bcol[j];
+      if (ci - c0 == 1) {
+        int r = std::min(chs[c0].h, b);
+        CopyTask t{};
+        t.src = off[j];
+        t.lds = ld[j];
+        t.dst = out.off[j];
+        t.ldd = std::max(r, 1);
+        t.rows = r;
+        t.cols = b;
+        t.rmap_off = t.cmap_off = -1;
+        t.tri = 1;
+        fin.push_back(t);
+        out.rows[j] = r;
+        done[j] = 1;
+      } else {
+        int rr = 0;
+        for (size_t c = c0; c < ci; ++c) rr += std::min(chs[c].h, b);
+        noff[j] = ntot;
+        nrows[j] = rr;
+        ntot += (long long)rr * b;
+        int r0 = 0;
+        for (size_t c = c0; c < ci; ++c) {
+          int r = std::min(chs[c].h, b);
+          CopyTask t{};
+          t.src = off[j] + chs[c].r0;
+          t.lds = ld[j];
+          t.dst = noff[j] + r0;
+          t.ldd = rr;
+          t.rows = r;
+          t.cols = b;
+          t.rmap_off = t.cmap_off = -1;
+          t.tri = 1;
+          stk.push_back(t);
+          r0 += r;
+        }
+      }
+    }
+    DBuf next;
+    if (!stk.empty()) next.alloc((size_t)ntot * sizeof(cplx), st);
+    {
+      std::vector<int> nomap{0};
+      Stage s2;
+      size_t o_f = s2.add(fin), o_s = s2.add(stk), o_m = s2.add(nomap);
+      s2.upload(st);
+      cplx* src = round == 0 ? Mbase : arena.as<cplx>();
+      launch_copy(s2.ptr<CopyTask>(o_f), (int)fin.size(), s2.ptr<int>(o_m), src, out.R.as<cplx>(), st);
+      launch_copy(s2.ptr<CopyTask>(o_s), (int)stk.size(), s2.ptr<int>(o_m), src, next.as<cplx>(), st);
+      P.add(FMMLU_K_QR, 0, 0, (fin.empty() ? 0 : 1) + (stk.empty() ? 0 : 1));
+    }
+    if (stk.empty()) break;
+    arena = std::move(next);
+    for (int j = 0; j < nbx; ++j)
+      if (!done[j]) {
+        base[j] = arena.as<cplx>();
+        off[j] = noff[j];
+        rows[j] = nrows[j];
+        ld[j] = nrows[j];
+      }
+  }
 }
 
 // ---------------------------------------------------------------------------- factorization
@@ -334,8 +614,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       size_t o_t = s.add(tasks), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_tab = s.add(tab),
              o_b = s.add(bld);
       s.upload(st);
+      int bid = h->prof.begin(FMMLU_K_BUILD, st);
       launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
                    s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), cur.bsr.as<cplx>(), h->g, k, st);
+      h->prof.end(bid, st);
+      h->prof.add(FMMLU_K_BUILD, 60.0 * cur.size, 16.0 * cur.size, 1);
       keep.push_back(std::move(s.dev));
     }
     if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
@@ -486,18 +769,52 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (maps.empty()) maps.push_back(0);
         if (gidx.empty()) gidx.push_back(0);
         Stage s;
-        size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_i = s.add(ids), o_g = s.add(gidx);
+        size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_g = s.add(gidx);
         s.upload(st);
+        int pid = h->prof.begin(FMMLU_K_GATHER, st);
         launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), M.as<cplx>(), st);
         launch_proxy(s.ptr<ProxyTask>(o_p), (int)pts.size(), s.ptr<int>(o_g), M.as<cplx>(), h->g, k, st);
-        launch_cpqr(s.ptr<IdTask>(o_i), nj, M.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st, bmax);
-        launch_trsm_T(s.ptr<IdTask>(o_i), kd.as<int>(), nj, M.as<cplx>(), Tb.as<cplx>(), st);
+        h->prof.end(pid, st);
+        {
+          double by = 0, fl = 0;
+          for (auto& c : cps) by += 32.0 * c.rows * c.cols;
+          for (auto& p : pts) {
+            by += 32.0 * p.ngamma * p.b;
+            fl += 2.0 * p.ngamma * p.b * 60.0;  // ~60 flops per kernel entry (estimate)
+          }
+          h->prof.add(FMMLU_K_GATHER, fl, by, (cps.empty() ? 0 : 1) + (pts.empty() ? 0 : 1));
+        }
         keep.push_back(std::move(s.dev));
+        // TSQR/blocked-QR → R0, then CPQR(R0) and T = R11⁻¹R12
+        std::vector<long long> moff;
+        std::vector<int> mrows, bcol;
+        for (auto& J : jobs) {
+          moff.push_back(J.Moff);
+          mrows.push_back(J.m);
+          bcol.push_back(J.b);
+        }
+        R0Out r0;
+        tsqr_R0(h, M.as<cplx>(), moff, mrows, bcol, r0);
+        for (int j = 0; j < nj; ++j) {
+          ids[j].M = r0.off[j];
+          ids[j].m = r0.rows[j];
+        }
+        Stage s2;
+        size_t o_i = s2.add(ids);
+        s2.upload(st);
+        int cid = h->prof.begin(FMMLU_K_CPQR, st);
+        launch_cpqr(s2.ptr<IdTask>(o_i), nj, r0.R.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st, bmax);
+        launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, r0.R.as<cplx>(), Tb.as<cplx>(), st);
+        h->prof.end(cid, st);
+        h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
+        keep.push_back(std::move(s2.dev));
+        keep.push_back(std::move(r0.R));
       }
       std::vector<int> hk(nj), hperm(permtot);
       FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
       FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
       FMMLU_CUDA(cudaStreamSynchronize(st));
+      h->prof.resolve();
       keep.clear();
       track(h, -(long long)M.bytes);
       M.release();
@@ -507,6 +824,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       for (int j = 0; j < nj; ++j) {
         jobs[j].k = hk[j];
         int r = jobs[j].b - hk[j];
+        {  // CPQR(R0) + T algorithmic flops: 8(b²k − bk² + k³/3) + 4k²r
+          double b_ = jobs[j].b, k_ = hk[j];
+          h->prof.add(FMMLU_K_CPQR, 8.0 * (b_ * b_ * k_ - b_ * k_ * k_ + k_ * k_ * k_ / 3.0) + 4.0 * k_ * k_ * r,
+                      16.0 * b_ * b_, 0);
+        }
         S.ranks_sum[lvl] += hk[j];
         S.boxes[lvl] += 1;
         S.max_rank = std::max(S.max_rank, hk[j]);
@@ -685,8 +1007,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
                o_rec = s.add(recs);
         s.upload(st);
+        int gid = h->prof.begin(FMMLU_K_GATHER, st);
         launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), Wp, st);
         launch_copy(s.ptr<CopyTask>(o_ct), (int)cpsT.size(), s.ptr<int>(o_m), Tb.as<cplx>(), F, st);
+        h->prof.end(gid, st);
+        {
+          double by = 0;
+          for (auto& c : cps) by += 32.0 * c.rows * c.cols;
+          for (auto& c : cpsT) by += 32.0 * c.rows * c.cols;
+          h->prof.add(FMMLU_K_GATHER, 0, by, 1 + (cpsT.empty() ? 0 : 1));
+        }
         // E: W_B[R,:] −= Tᵀ W_B[S,:]
         std::vector<GemmProblem> gp;
         std::vector<GemmTile> gt;
@@ -708,7 +1038,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.ldc = J.b;
           add_gemm(gp, gt, P);
         }
-        run_gemms(gp, gt, m1, 0, nullptr, st, keep);
+        run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_EF);
         // F: W_B[:,R] −= W_B[:,S] T ;  W_N[:,R] −= W_N[:,S] T
         for (size_t e = 0; e < el.size(); ++e) {
           BoxJob& J = jobs[el[e]];
@@ -736,11 +1066,21 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             add_gemm(gp, gt, Q);
           }
         }
-        run_gemms(gp, gt, m1, 0, nullptr, st, keep);
+        run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_EF);
         // X_RR⁻¹ (Gauss-Jordan with partial pivoting)
+        int iid = h->prof.begin(FMMLU_K_INV, st);
         launch_copy(s.ptr<CopyTask>(o_cx), (int)cpsX.size(), s.ptr<int>(o_m), Wp, F, st);
         launch_gj_inverse(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
                           ph.rmax);
+        h->prof.end(iid, st);
+        {
+          double fl = 0, by = 0;
+          for (int d : gjdim) {
+            fl += 8.0 * (double)d * d * d;
+            by += 32.0 * (double)d * d;
+          }
+          h->prof.add(FMMLU_K_INV, fl, by, 2);
+        }
         // Up = X_RR⁻¹ X_{R(S∪N)} ;  Lp = X_{(S∪N)R} X_RR⁻¹
         for (size_t e = 0; e < el.size(); ++e) {
           BoxJob& J = jobs[el[e]];
@@ -790,7 +1130,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             add_gemm(gp, gt, Q);
           }
         }
-        run_gemms(gp, gt, p1, 0, nullptr, st, keep);
+        run_gemms(gp, gt, p1, 0, nullptr, st, keep, h->prof, FMMLU_K_PANEL);
         // Schur complement: Δ_{(S∪N)²} −= Lp · X_{R(S∪N)}, scattered into the level BSR
         for (size_t e = 0; e < el.size(); ++e) {
           BoxJob& J = jobs[el[e]];
@@ -818,13 +1158,14 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.bld = s.ptr<int>(o_fb) + fr.bld_off;
           add_gemm(gp, gt, P);
         }
-        run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep);
+        run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep, h->prof, FMMLU_K_SCHUR);
         // index arena + records
         FMMLU_CUDA(cudaMemcpyAsync(ph.idx.p, hidx.data(), hidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
         ph.recs.alloc(recs.size() * sizeof(BoxRec), st);
         FMMLU_CUDA(cudaMemcpyAsync(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), cudaMemcpyHostToDevice, st));
         ph.nrec = (int)recs.size();
         FMMLU_CUDA(cudaStreamSynchronize(st));
+        h->prof.resolve();
         keep.clear();
         keep.push_back(std::move(s.dev));
         track(h, -(long long)W.bytes);
@@ -859,6 +1200,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       }
     prev = std::move(cur);
     FMMLU_CUDA(cudaStreamSynchronize(st));
+    h->prof.resolve();
     S.t_levels_ms[lvl] = now_ms() - tl0;
   }
 
@@ -918,11 +1260,14 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     size_t o_t = s.add(tasks), o_g = s.add(Bt), o_s = s.add(slot), o_p = s.add(pos), o_tab = s.add(tab),
            o_b = s.add(bld);
     s.upload(st);
+    int rid = h->prof.begin(FMMLU_K_ROOT, st);
     launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
                  s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), h->root.as<cplx>(), h->g, k, st);
     DBuf scratch;
     scratch.alloc(((size_t)n0 * n0 + 3 * (size_t)n0 + 8) * sizeof(cplx), st);
     launch_gj_inverse_coop(h->root.as<cplx>(), n0, scratch.as<cplx>(), status.as<int>(), st);
+    h->prof.end(rid, st);
+    h->prof.add(FMMLU_K_ROOT, 8.0 * (double)n0 * n0 * n0, 32.0 * (double)n0 * n0, 3);
     h->root_rows.alloc((size_t)n0 * sizeof(int), st);
     FMMLU_CUDA(cudaMemcpyAsync(h->root_rows.p, Bt.data(), n0 * sizeof(int), cudaMemcpyHostToDevice, st));
     FMMLU_CUDA(cudaStreamSynchronize(st));
@@ -932,6 +1277,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   int hstatus = 0;
   FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FMMLU_CUDA(cudaStreamSynchronize(st));
+  h->prof.resolve();
   S.t_root_ms = now_ms() - tr0;
   if (hstatus) throw Error(FMMLU_ESINGULAR, "exactly singular pivot block (X_RR or root)");
   h->k = k;
@@ -952,6 +1298,8 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   }
   y.alloc((size_t)n * nrhs * sizeof(cplx), st);
   cplx* yp = y.as<cplx>();
+  Prof& P = h->prof;
+  int sid = P.begin(FMMLU_K_SOLVE, st);
   launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
   for (auto& ph : h->phases)
     launch_solve_up(ph.recs.as<BoxRec>(), ph.nrec, ph.fac.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs, st, ph.kmax,
@@ -965,9 +1313,18 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
     launch_solve_down(it->recs.as<BoxRec>(), it->nrec, it->fac.as<cplx>(), it->idx.as<int>(), yp, n, nrhs, st,
                       it->rmax);
   launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
+  P.end(sid, st);
+  {
+    // algorithmic: every stored factor entry read once, 8 flops per entry per RHS
+    double entries = (double)h->n0 * h->n0;
+    for (auto& ph : h->phases) entries += (double)ph.fac_bytes / 16.0;
+    P.add(FMMLU_K_SOLVE, 8.0 * entries * nrhs, 16.0 * entries + 64.0 * n * nrhs,
+          3 + 2 * (long long)h->phases.size() + (h->n0 > 0 ? 2 : 0));
+  }
   if (!dev)
     FMMLU_CUDA(cudaMemcpyAsync(rhs, io.p, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyDeviceToHost, st));
   FMMLU_CUDA(cudaStreamSynchronize(st));
+  P.resolve();
 }
 
 template <class F>
@@ -1079,6 +1436,7 @@ int fmmlu_factor(fmmlu_handle* h, double k, double eps) {
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
     double t0 = now_ms();
+    h->prof.reset();
     factor_impl(h, k, eps);
     h->stats.t_factor_ms = now_ms() - t0;
     h->stats.peak_bytes = (int64_t)h->peak_bytes;
@@ -1149,6 +1507,13 @@ int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out) {
   if (!h || !out) return fail(FMMLU_EINVAL, "NULL argument");
   *out = h->stats;
   out->peak_bytes = (int64_t)h->peak_bytes;
+  out->n_launches = h->prof.total_launches;
+  for (int i = 0; i < 16; ++i) {
+    out->class_ms[i] = h->prof.ms[i];
+    out->class_flops[i] = h->prof.flops[i];
+    out->class_bytes[i] = h->prof.bytes[i];
+    out->class_launches[i] = h->prof.launches[i];
+  }
   return FMMLU_OK;
 }
 

@@ -35,7 +35,7 @@ __device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0,
     if (P.opA == kOpN) {
       mm = idx % BM;
       kk = idx / BM;
-    } else {
+    } else {  // T or C
       kk = idx % BK;
       mm = idx / BK;
     }
@@ -53,7 +53,7 @@ __device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0,
     if (P.opB == kOpN) {
       kk = idx % BK;
       nn = idx / BK;
-    } else {
+    } else {  // T or C
       nn = idx % BN;
       kk = idx / BN;
     }
@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // 2 × 4 warps
   const int m0 = T.tm * BM, n0 = T.tn * BN;
+  const double sa = P.opA == kOpC ? -1.0 : 1.0;  // conjugation of A / B at fragment load
+  const double sb = P.opB == kOpC ? -1.0 : 1.0;
 
   double accr[4][2][2], acci[4][2][2];
 #pragma unroll
@@ -106,9 +108,15 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
       const int kk = ks * 4 + t;
       cplx a[4], b[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[kk * PADA + wm * 32 + i * 8 + g];
+      for (int i = 0; i < 4; ++i) {
+        a[i] = as[kk * PADA + wm * 32 + i * 8 + g];
+        a[i].y *= sa;
+      }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) b[j] = bs[kk * PADB + wn * 16 + j * 8 + g];
+      for (int j = 0; j < 2; ++j) {
+        b[j] = bs[kk * PADB + wn * 16 + j * 8 + g];
+        b[j].y *= sb;
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll

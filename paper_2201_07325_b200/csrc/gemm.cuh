@@ -11,7 +11,7 @@
 
 namespace fmmlu {
 
-enum : int { kOpN = 0, kOpT = 1 };
+enum : int { kOpN = 0, kOpT = 1, kOpC = 2 };  // C = conjugate transpose
 
 struct GemmProblem {
   int m, n, k;

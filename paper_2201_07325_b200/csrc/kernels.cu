@@ -120,7 +120,8 @@ __global__ void k_copy(const CopyTask* __restrict__ tasks, const int* __restrict
     const int i = e % t.rows, j = e / t.rows;
     const int ri = t.rmap_off >= 0 ? maps[t.rmap_off + i] : i;
     const int cj = t.cmap_off >= 0 ? maps[t.cmap_off + j] : j;
-    const cplx v = t.trans ? src[t.src + cj + (size_t)ri * t.lds] : src[t.src + ri + (size_t)cj * t.lds];
+    cplx v = t.trans ? src[t.src + cj + (size_t)ri * t.lds] : src[t.src + ri + (size_t)cj * t.lds];
+    if (t.tri && i > j) v = cmk(0.0, 0.0);
     dst[t.dst + i + (size_t)j * t.ldd] = v;
   }
 }
@@ -150,6 +151,165 @@ __global__ void k_proxy(const ProxyTask* __restrict__ tasks, const int* __restri
     ws[t.dst + (t.row0 + l) + (size_t)j * t.ld] = cscale(Ko, scl);
     ws[t.dst + (t.row0 + t.ngamma + l) + (size_t)j * t.ld] = cscale(Gi, scl);
   }
+}
+
+// ------------------------------------------------------------------ blocked Householder QR panel
+// Hermitian reflectors H = I − τ v vᴴ (τ real, v_0 = 1) with H x = β e1, β = −(α/|α|)‖x‖.
+constexpr int QP_NT = 512;
+constexpr int QP_NBMAX = 16;
+
+__global__ void __launch_bounds__(QP_NT) k_qr_panel(const QrChunk* __restrict__ chunks, int j0, int NB) {
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ cplx sred[QP_NT / 32][QP_NBMAX];
+  __shared__ cplx dots[QP_NBMAX];
+  __shared__ double tau[QP_NBMAX];
+  __shared__ cplx G[QP_NBMAX][QP_NBMAX];
+  __shared__ cplx Tm[QP_NBMAX][QP_NBMAX];
+  const QrChunk c = chunks[blockIdx.x];
+  const int kmax = min(c.h, c.b);
+  if (j0 >= kmax) return;
+  const int jb = min(NB, kmax - j0);
+  const int hr = c.h - j0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  cplx* P = reinterpret_cast<cplx*>(shm);  // hr × jb, ld hr
+  cplx* A = c.A;
+  for (int e = tid; e < hr * jb; e += QP_NT) {
+    const int i = e % hr, jj = e / hr;
+    P[e] = A[(j0 + i) + (size_t)(j0 + jj) * c.lda];
+  }
+  __syncthreads();
+  for (int jj = 0; jj < jb; ++jj) {
+    double xs = 0.0;
+    for (int i = jj + 1 + tid; i < hr; i += QP_NT) xs += cabs2(P[i + jj * hr]);
+    const double xn2 = block_sum<QP_NT>(xs, red_v);
+    const cplx alpha = P[jj + jj * hr];
+    const double aa = sqrt(cabs2(alpha));
+    const double nrm = sqrt(aa * aa + xn2);
+    __syncthreads();
+    if (nrm == 0.0) {  // zero column: identity reflector
+      if (tid == 0) tau[jj] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    const cplx beta = aa > 0.0 ? cmk(-alpha.x / aa * nrm, -alpha.y / aa * nrm) : cmk(-nrm, 0.0);
+    const cplx u0 = csub(alpha, beta);
+    const double u02 = cabs2(u0);
+    const cplx inv_u0 = cmk(u0.x / u02, -u0.y / u02);
+    for (int i = jj + 1 + tid; i < hr; i += QP_NT) P[i + jj * hr] = cmul(P[i + jj * hr], inv_u0);
+    if (tid == 0) {
+      tau[jj] = 2.0 * u02 / (u02 + xn2);
+      P[jj + jj * hr] = beta;
+    }
+    __syncthreads();
+    const int nrest = jb - jj - 1;
+    if (nrest > 0) {
+      // d_c = vᴴ P[jj:, c] for the remaining panel columns (v_jj = 1)
+      cplx d[QP_NBMAX];
+#pragma unroll
+      for (int q = 0; q < QP_NBMAX; ++q) d[q] = cmk(0.0, 0.0);
+      for (int i = jj + tid; i < hr; i += QP_NT) {
+        const cplx v = i == jj ? cmk(1.0, 0.0) : P[i + jj * hr];
+#pragma unroll
+        for (int q = 0; q < QP_NBMAX; ++q)
+          if (q < nrest) d[q] = cadd(d[q], cmulc(v, P[i + (jj + 1 + q) * hr]));
+      }
+#pragma unroll
+      for (int q = 0; q < QP_NBMAX; ++q) {
+        if (q < nrest) {
+          cplx s = warp_csum(d[q]);
+          if (lane == 0) sred[warp][q] = s;
+        }
+      }
+      __syncthreads();
+      if (tid < nrest) {
+        cplx s = cmk(0.0, 0.0);
+        for (int w = 0; w < QP_NT / 32; ++w) s = cadd(s, sred[w][tid]);
+        dots[tid] = cscale(s, tau[jj]);
+      }
+      __syncthreads();
+      for (int e = tid; e < (hr - jj) * nrest; e += QP_NT) {
+        const int i = jj + e % (hr - jj), q = e / (hr - jj);
+        const cplx v = i == jj ? cmk(1.0, 0.0) : P[i + jj * hr];
+        P[i + (jj + 1 + q) * hr] = cfms(dots[q], v, P[i + (jj + 1 + q) * hr]);
+      }
+      __syncthreads();
+    }
+  }
+  // R rows back to A (upper triangle of the panel's top jb rows)
+  for (int e = tid; e < jb * jb; e += QP_NT) {
+    const int i = e % jb, jj = e / jb;
+    if (i <= jj) A[(j0 + i) + (size_t)(j0 + jj) * c.lda] = P[i + jj * hr];
+  }
+  // explicit V (unit diagonal, zeros above) and G = Vᴴ V
+  cplx* V = c.V;
+  for (int e = tid; e < hr * jb; e += QP_NT) {
+    const int i = e % hr, jj = e / hr;
+    V[i + (size_t)jj * c.h] = i < jj ? cmk(0.0, 0.0) : (i == jj ? cmk(1.0, 0.0) : P[i + jj * hr]);
+  }
+  {
+    // 4 threads per (p, q) pair with p < q; rows strided
+    const int pair = tid >> 2, part = tid & 3;
+    const int npairs = jb * (jb - 1) / 2;
+    for (int pb = 0; pb < npairs; pb += QP_NT / 4) {
+      const int pr = pb + pair;
+      cplx s = cmk(0.0, 0.0);
+      int p = 0, q = 0;
+      if (pr < npairs) {
+        // decode pr -> (p, q), p < q
+        int rem = pr;
+        q = 1;
+        while (rem >= q) {
+          rem -= q;
+          ++q;
+        }
+        p = rem;
+        for (int i = q + part; i < hr; i += 4) {
+          const cplx vp = i == p ? cmk(1.0, 0.0) : (i < p ? cmk(0.0, 0.0) : P[i + p * hr]);
+          const cplx vq = i == q ? cmk(1.0, 0.0) : P[i + q * hr];
+          s = cadd(s, cmulc(vp, vq));
+        }
+      }
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
+      if (pr < npairs && part == 0) G[p][q] = s;
+    }
+  }
+  __syncthreads();
+  // T (upper triangular): T_ii = τ_i, T(0:i, i) = −τ_i T(0:i,0:i) G(0:i, i)
+  if (warp == 0) {
+    for (int i = 0; i < jb; ++i) {
+      cplx t = cmk(0.0, 0.0);
+      if (lane < i) {
+        for (int q = lane; q < i; ++q) t = cfma(Tm[lane][q], G[q][i], t);
+        t = cscale(t, -tau[i]);
+      }
+      __syncwarp();
+      if (lane < i) Tm[lane][i] = t;
+      if (lane == i) Tm[i][i] = cmk(tau[i], 0.0);
+      if (lane > i && lane < jb) Tm[lane][i] = cmk(0.0, 0.0);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // Z = V Tᴴ :  Z[i][cc] = Σ_{p ≥ cc} V[i][p] conj(T[cc][p])
+  cplx* Z = c.Z;
+  for (int e = tid; e < hr * jb; e += QP_NT) {
+    const int i = e % hr, cc = e / hr;
+    cplx s = cmk(0.0, 0.0);
+    for (int p = cc; p < jb && p <= i; ++p) {
+      const cplx v = i == p ? cmk(1.0, 0.0) : P[i + p * hr];
+      const cplx tc = cmk(Tm[cc][p].x, -Tm[cc][p].y);
+      s = cfma(v, tc, s);
+    }
+    Z[i + (size_t)cc * c.h] = s;
+  }
+  // zero W (jb × (b − j0 − jb)) for the next GEMM's accumulation
+  cplx* W = c.W;
+  const int nt = c.b - j0 - jb;
+  for (int e = tid; e < NB * nt; e += QP_NT) W[e] = cmk(0.0, 0.0);
 }
 
 // ------------------------------------------------------------------ CPQR
@@ -707,6 +867,17 @@ void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* w
   if (ntasks <= 0) return;
   dim3 grid(ntasks, 8);
   k_proxy<<<grid, 256, 0, st>>>(d_tasks, gidx, ws, g, k);
+  FMMLU_LAUNCH();
+}
+
+void launch_qr_panel(const QrChunk* d_chunks, int nchunks, int j0, int nb, cudaStream_t st) {
+  if (nchunks <= 0) return;
+  static bool init = false;
+  if (!init) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    init = true;
+  }
+  k_qr_panel<<<nchunks, QP_NT, 200 * 1024, st>>>(d_chunks, j0, nb);
   FMMLU_LAUNCH();
 }
 

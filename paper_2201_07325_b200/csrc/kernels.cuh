@@ -28,6 +28,14 @@ struct CopyTask {
   int rows, cols;      // dst dims
   int trans;
   int rmap_off, cmap_off;
+  int tri;             // 1: zero the strictly-lower part of dst (upper-triangular R copies)
+};
+
+// One row-chunk of a box's ID matrix for the blocked Householder QR (TSQR leaves).
+// A: h × b (ld lda) in the workspace arena; V, Z: h × NB (ld h); W: NB × b (ld NB).
+struct QrChunk {
+  cplx *A, *V, *Z, *W;
+  int lda, h, b, pad;
 };
 
 // Proxy rows of M (§5.1.3; readings C3-C5): rows row0 .. row0+nγ-1 hold
@@ -61,6 +69,10 @@ void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cpl
                  cplx* dst_arena, cudaStream_t st);
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
                   double k, cudaStream_t st);
+// Householder panel of every chunk: columns j0 .. j0+jb-1 factored in shared memory; writes R
+// rows back, the explicit reflectors V (unit diagonal) and Z = V Tᴴ of the compact WY form
+// H_1⋯H_jb = I − V T Vᴴ, and zeroes W.  One CTA per chunk.
+void launch_qr_panel(const QrChunk* d_chunks, int nchunks, int j0, int nb, cudaStream_t st);
 void launch_cpqr(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out,
                  double eps, cudaStream_t st, int bmax);
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,

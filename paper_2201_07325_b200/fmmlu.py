@@ -35,6 +35,8 @@ class Stats(ctypes.Structure):
         ("peak_bytes", ctypes.c_int64), ("t_tree_ms", ctypes.c_double), ("t_factor_ms", ctypes.c_double),
         ("t_solve_ms", ctypes.c_double), ("t_root_ms", ctypes.c_double), ("t_levels_ms", ctypes.c_double * 24),
         ("n_singular_warn", ctypes.c_int32), ("ranks_sum", ctypes.c_int32 * 24), ("boxes", ctypes.c_int32 * 24),
+        ("n_launches", ctypes.c_int64), ("class_ms", ctypes.c_double * 16), ("class_flops", ctypes.c_double * 16),
+        ("class_bytes", ctypes.c_double * 16), ("class_launches", ctypes.c_int64 * 16),
     ]
 
     def as_dict(self):
@@ -44,6 +46,8 @@ class Stats(ctypes.Structure):
             d[name] = list(v) if hasattr(v, "__len__") else v
         return d
 
+
+KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve"]
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64")
