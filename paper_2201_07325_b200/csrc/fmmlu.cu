@@ -114,7 +114,9 @@ struct Phase {  // one (level, colour) elimination phase
   DBuf fac;    // complex: T | Xinv | Up | Lp per box
   DBuf idx;    // int: S | R | N per box
   DBuf recs;   // BoxRec[nrec]
-  int nrec = 0, kmax = 0, rmax = 0;
+  DBuf items;  // SolveItem[nitems] (row/column chunks of Lp/Up)
+  int nrec = 0, kmax = 0, rmax = 0, nitems = 0;
+  int tmp_rows = 0;  // Σ r over the phase's boxes (solve scratch)
   size_t fac_bytes = 0;
 };
 
@@ -219,8 +221,10 @@ void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, con
   if (p.m <= 0 || p.n <= 0 || p.k <= 0) return;
   int id = (int)probs.size();
   probs.push_back(p);
+  const int nks = p.kchunk > 0 ? (p.k + p.kchunk - 1) / p.kchunk : 1;
   for (int tm = 0; tm < (p.m + kTile - 1) / kTile; ++tm)
-    for (int tn = 0; tn < (p.n + kTile - 1) / kTile; ++tn) tiles.push_back({id, tm, tn});
+    for (int tn = 0; tn < (p.n + kTile - 1) / kTile; ++tn)
+      for (int ks = 0; ks < nks; ++ks) tiles.push_back({id, tm, tn, ks});
 }
 
 // Algorithmic work of a batch: 8mnk real flops per complex GEMM; bytes = read A and B once,
@@ -338,12 +342,13 @@ void tsqr_R0(fmmlu_handle* h, cplx* Mbase, const std::vector<long long>& moff,
           if (nt <= 0) continue;
           GemmProblem g{};
           cplx* At = x.A + j0 + (size_t)(j0 + jb) * x.lda;
-          if (pass == 0) {  // W = Vᴴ A_t
+          if (pass == 0) {  // W = Vᴴ A_t  (split-K over the tall dimension, atomic accumulate)
             g.m = jb; g.n = nt; g.k = hr;
             g.opA = kOpC; g.opB = kOpN;
             g.A = x.V; g.lda = x.h;
             g.B = At; g.ldb = x.lda;
             g.C = x.W; g.ldc = NB;
+            g.kchunk = hr > 128 ? 64 : 0;
           } else {          // A_t −= Z W
             g.m = hr; g.n = nt; g.k = jb;
             g.opA = kOpN; g.opB = kOpN;
@@ -803,7 +808,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         size_t o_i = s2.add(ids);
         s2.upload(st);
         int cid = h->prof.begin(FMMLU_K_CPQR, st);
-        launch_cpqr(s2.ptr<IdTask>(o_i), nj, r0.R.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st, bmax);
+        int mmax0 = 1;
+        for (int j = 0; j < nj; ++j) mmax0 = std::max(mmax0, r0.rows[j]);
+        if (!launch_cpqr_cluster(s2.ptr<IdTask>(o_i), nj, r0.R.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st,
+                                 mmax0, bmax))
+          launch_cpqr(s2.ptr<IdTask>(o_i), nj, r0.R.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st, bmax);
         launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, r0.R.as<cplx>(), Tb.as<cplx>(), st);
         h->prof.end(cid, st);
         h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
@@ -869,6 +878,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           idxsz += r;
           R.idxN = idxsz;
           idxsz += J.nN;
+          R.tmp = ph.tmp_rows;
+          ph.tmp_rows += r;
           recs.push_back(R);
           ph.kmax = std::max(ph.kmax, kk);
           ph.rmax = std::max(ph.rmax, r);
@@ -1070,8 +1081,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         // X_RR⁻¹ (Gauss-Jordan with partial pivoting)
         int iid = h->prof.begin(FMMLU_K_INV, st);
         launch_copy(s.ptr<CopyTask>(o_cx), (int)cpsX.size(), s.ptr<int>(o_m), Wp, F, st);
-        launch_gj_inverse(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
-                          ph.rmax);
+        if (!launch_gj_cluster(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
+                               ph.rmax))
+          launch_gj_inverse(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
+                            ph.rmax);
         h->prof.end(iid, st);
         {
           double fl = 0, by = 0;
@@ -1164,6 +1177,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         ph.recs.alloc(recs.size() * sizeof(BoxRec), st);
         FMMLU_CUDA(cudaMemcpyAsync(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), cudaMemcpyHostToDevice, st));
         ph.nrec = (int)recs.size();
+        {
+          std::vector<SolveItem> items;
+          for (size_t e = 0; e < recs.size(); ++e)
+            for (int c0 = 0; c0 < recs[e].k + recs[e].nN; c0 += kSolveChunk) items.push_back({(int)e, c0});
+          ph.nitems = (int)items.size();
+          ph.items.alloc(std::max<size_t>(1, items.size()) * sizeof(SolveItem), st);
+          if (!items.empty())
+            FMMLU_CUDA(cudaMemcpyAsync(ph.items.p, items.data(), items.size() * sizeof(SolveItem),
+                                       cudaMemcpyHostToDevice, st));
+        }
         FMMLU_CUDA(cudaStreamSynchronize(st));
         h->prof.resolve();
         keep.clear();
@@ -1301,17 +1324,23 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   Prof& P = h->prof;
   int sid = P.begin(FMMLU_K_SOLVE, st);
   launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
+  size_t scr_rows = 1;
+  for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
+  DBuf scr;
+  scr.alloc(scr_rows * nrhs * sizeof(cplx), st);
   for (auto& ph : h->phases)
-    launch_solve_up(ph.recs.as<BoxRec>(), ph.nrec, ph.fac.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs, st, ph.kmax,
-                    ph.rmax);
+    launch_solve_up2(ph.recs.as<BoxRec>(), ph.nrec, ph.items.as<SolveItem>(), ph.nitems, ph.fac.as<cplx>(),
+                     ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.kmax, ph.rmax);
   DBuf tmp;
   if (h->n0 > 0) {
-    tmp.alloc((size_t)h->n0 * nrhs * sizeof(cplx), st);
+    tmp.alloc(2 * (size_t)h->n0 * nrhs * sizeof(cplx), st);
     launch_root_apply(h->root.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), yp, n, nrhs, tmp.as<cplx>(), st);
   }
-  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it)
-    launch_solve_down(it->recs.as<BoxRec>(), it->nrec, it->fac.as<cplx>(), it->idx.as<int>(), yp, n, nrhs, st,
-                      it->rmax);
+  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
+    FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
+    launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
+                       it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax);
+  }
   launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
   P.end(sid, st);
   {

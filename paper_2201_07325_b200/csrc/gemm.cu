@@ -88,9 +88,12 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
 #pragma unroll
     for (int j = 0; j < 2; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
 
-  const int nk = (P.k + BK - 1) / BK;
+  // K range of this tile (split-K); the range is BK-aligned, P.k bounds the loads
+  const int kbeg = P.kchunk > 0 ? T.ks * P.kchunk : 0;
+  const int kend = P.kchunk > 0 ? min(P.k, kbeg + P.kchunk) : P.k;
+  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   if (nk > 0) {
-    load_tiles(P, m0, n0, 0, As, Bs, tid);
+    load_tiles(P, m0, n0, kbeg, As, Bs, tid);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
     __syncthreads();
     if (kt + 1 < nk) {
       int s = (kt + 1) & 1;
-      load_tiles(P, m0, n0, (kt + 1) * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
+      load_tiles(P, m0, n0, kbeg + (kt + 1) * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
       cp_async_commit();
     }
     const cplx* as = As + (kt & 1) * BK * PADA;
@@ -151,6 +154,10 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
             atomicAdd(&d->x, v.x);
             atomicAdd(&d->y, v.y);
           }
+        } else if (P.kchunk > 0) {
+          cplx* d = P.C + row + (size_t)col * P.ldc;
+          atomicAdd(&d->x, v.x);
+          atomicAdd(&d->y, v.y);
         } else {
           cplx* d = P.C + row + (size_t)col * P.ldc;
           cplx c = *d;

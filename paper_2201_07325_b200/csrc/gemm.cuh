@@ -29,12 +29,15 @@ struct GemmProblem {
   const int* pos;
   const long long* tab;
   const int* bld;
+  int kchunk;  // split-K: each tile covers K range [ks*kchunk, (ks+1)*kchunk); 0 = whole K.
+               // With split-K the kStore epilogue accumulates with fp64 atomics.
 };
 
 struct GemmTile {
   int p;   // problem index
   int tm;  // tile row
   int tn;  // tile col
+  int ks;  // K split index
 };
 
 // C = C + alpha * op(A) op(B) for each problem; `tiles` enumerates 64×64 output tiles.

@@ -160,10 +160,8 @@ constexpr int QP_NBMAX = 16;
 
 __global__ void __launch_bounds__(QP_NT) k_qr_panel(const QrChunk* __restrict__ chunks, int j0, int NB) {
   extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ cplx sred[QP_NT / 32][QP_NBMAX];
-  __shared__ cplx dots[QP_NBMAX];
   __shared__ double tau[QP_NBMAX];
+  __shared__ cplx betas[QP_NBMAX];
   __shared__ cplx G[QP_NBMAX][QP_NBMAX];
   __shared__ cplx Tm[QP_NBMAX][QP_NBMAX];
   const QrChunk c = chunks[blockIdx.x];
@@ -174,68 +172,97 @@ __global__ void __launch_bounds__(QP_NT) k_qr_panel(const QrChunk* __restrict__ 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   cplx* P = reinterpret_cast<cplx*>(shm);  // hr × jb, ld hr
   cplx* A = c.A;
+  // rows are owned by threads (i ≡ tid mod QP_NT) for the whole factorization, so the only
+  // barriers per column are the norm reduction and the two-step dot reduction.
+  double xs = 0.0;  // this thread's part of ‖P[jj+1:, jj]‖² for the current column
   for (int e = tid; e < hr * jb; e += QP_NT) {
     const int i = e % hr, jj = e / hr;
-    P[e] = A[(j0 + i) + (size_t)(j0 + jj) * c.lda];
+    const cplx v = A[(j0 + i) + (size_t)(j0 + jj) * c.lda];
+    P[e] = v;
   }
-  __syncthreads();
+  for (int i = 1 + tid; i < hr; i += QP_NT) {
+    const cplx v = A[(j0 + i) + (size_t)j0 * c.lda];
+    xs += cabs2(v);
+  }
+  __shared__ double nred[2][QP_NT / 32];
+  __shared__ cplx dred[2][QP_NT / 32][QP_NBMAX];
+  __shared__ cplx dots2[2][QP_NBMAX];
   for (int jj = 0; jj < jb; ++jj) {
-    double xs = 0.0;
-    for (int i = jj + 1 + tid; i < hr; i += QP_NT) xs += cabs2(P[i + jj * hr]);
-    const double xn2 = block_sum<QP_NT>(xs, red_v);
+    const int par = jj & 1;
+    double ws_ = warp_sum(xs);
+    if (lane == 0) nred[par][warp] = ws_;
+    __syncthreads();  // (1) column jj final after the previous update; norm partials visible
+    double xn2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < QP_NT / 32; ++w) xn2 += nred[par][w];
     const cplx alpha = P[jj + jj * hr];
     const double aa = sqrt(cabs2(alpha));
     const double nrm = sqrt(aa * aa + xn2);
-    __syncthreads();
-    if (nrm == 0.0) {  // zero column: identity reflector
-      if (tid == 0) tau[jj] = 0.0;
-      __syncthreads();
+    const int nrest = jb - jj - 1;
+    xs = 0.0;
+    if (nrm == 0.0) {  // zero column: identity reflector (uniform branch)
+      if (tid == 0) {
+        tau[jj] = 0.0;
+        betas[jj] = cmk(0.0, 0.0);
+      }
+      if (nrest > 0)
+        for (int i = jj + 2 + tid; i < hr; i += QP_NT) xs += cabs2(P[i + (jj + 1) * hr]);
       continue;
     }
     const cplx beta = aa > 0.0 ? cmk(-alpha.x / aa * nrm, -alpha.y / aa * nrm) : cmk(-nrm, 0.0);
     const cplx u0 = csub(alpha, beta);
     const double u02 = cabs2(u0);
     const cplx inv_u0 = cmk(u0.x / u02, -u0.y / u02);
-    for (int i = jj + 1 + tid; i < hr; i += QP_NT) P[i + jj * hr] = cmul(P[i + jj * hr], inv_u0);
-    if (tid == 0) {
-      tau[jj] = 2.0 * u02 / (u02 + xn2);
-      P[jj + jj * hr] = beta;
+    const double tj = 2.0 * u02 / (u02 + xn2);
+    // v (v_jj = 1) written in place, partial dots d_q = vᴴ P[jj:, jj+1+q]
+    cplx d[QP_NBMAX];
+#pragma unroll
+    for (int q = 0; q < QP_NBMAX; ++q) d[q] = cmk(0.0, 0.0);
+    for (int i = jj + tid; i < hr; i += QP_NT) {
+      cplx v;
+      if (i == jj) {
+        v = cmk(1.0, 0.0);  // β goes to the diagonal after the loop (others may still read α)
+      } else {
+        v = cmul(P[i + jj * hr], inv_u0);
+        P[i + jj * hr] = v;
+      }
+#pragma unroll
+      for (int q = 0; q < QP_NBMAX; ++q)
+        if (q < nrest) d[q] = cadd(d[q], cmulc(v, P[i + (jj + 1 + q) * hr]));
     }
-    __syncthreads();
-    const int nrest = jb - jj - 1;
-    if (nrest > 0) {
-      // d_c = vᴴ P[jj:, c] for the remaining panel columns (v_jj = 1)
-      cplx d[QP_NBMAX];
+    if (tid == 0) {
+      tau[jj] = tj;
+      betas[jj] = beta;
+    }
+    if (nrest == 0) continue;
 #pragma unroll
-      for (int q = 0; q < QP_NBMAX; ++q) d[q] = cmk(0.0, 0.0);
-      for (int i = jj + tid; i < hr; i += QP_NT) {
-        const cplx v = i == jj ? cmk(1.0, 0.0) : P[i + jj * hr];
-#pragma unroll
-        for (int q = 0; q < QP_NBMAX; ++q)
-          if (q < nrest) d[q] = cadd(d[q], cmulc(v, P[i + (jj + 1 + q) * hr]));
+    for (int q = 0; q < QP_NBMAX; ++q)
+      if (q < nrest) {
+        const cplx s = warp_csum(d[q]);
+        if (lane == 0) dred[par][warp][q] = s;
       }
+    __syncthreads();  // (2)
+    if (tid < nrest) {
+      cplx s = cmk(0.0, 0.0);
 #pragma unroll
-      for (int q = 0; q < QP_NBMAX; ++q) {
+      for (int w = 0; w < QP_NT / 32; ++w) s = cadd(s, dred[par][w][tid]);
+      dots2[par][tid] = cscale(s, tj);
+    }
+    __syncthreads();  // (3)
+    for (int i = jj + tid; i < hr; i += QP_NT) {
+      const cplx v = i == jj ? cmk(1.0, 0.0) : P[i + jj * hr];
+#pragma unroll
+      for (int q = 0; q < QP_NBMAX; ++q)
         if (q < nrest) {
-          cplx s = warp_csum(d[q]);
-          if (lane == 0) sred[warp][q] = s;
+          const cplx nv = cfms(dots2[par][q], v, P[i + (jj + 1 + q) * hr]);
+          P[i + (jj + 1 + q) * hr] = nv;
+          if (q == 0 && i > jj + 1) xs += cabs2(nv);
         }
-      }
-      __syncthreads();
-      if (tid < nrest) {
-        cplx s = cmk(0.0, 0.0);
-        for (int w = 0; w < QP_NT / 32; ++w) s = cadd(s, sred[w][tid]);
-        dots[tid] = cscale(s, tau[jj]);
-      }
-      __syncthreads();
-      for (int e = tid; e < (hr - jj) * nrest; e += QP_NT) {
-        const int i = jj + e % (hr - jj), q = e / (hr - jj);
-        const cplx v = i == jj ? cmk(1.0, 0.0) : P[i + jj * hr];
-        P[i + (jj + 1 + q) * hr] = cfms(dots[q], v, P[i + (jj + 1 + q) * hr]);
-      }
-      __syncthreads();
     }
   }
+  __syncthreads();
+  if (tid < jb) P[tid + tid * hr] = betas[tid];
+  __syncthreads();
   // R rows back to A (upper triangle of the panel's top jb rows)
   for (int e = tid; e < jb * jb; e += QP_NT) {
     const int i = e % jb, jj = e / jb;
@@ -494,6 +521,257 @@ __global__ void __launch_bounds__(GJ_NT) k_gj(const long long* __restrict__ offs
   }
 }
 
+// ------------------------------------------------------------------ cluster kernels (DSMEM)
+// Columns of an n×n (or m×b) matrix are distributed cyclically over the CL CTAs of a
+// thread-block cluster (global column g lives in CTA g % CL, local slot g / CL) and held in
+// shared memory for the whole factorization; the pivot column / Householder vector of each
+// step is published in the owner's shared memory and read by the others through DSMEM.
+constexpr int CK_NT = 256;
+
+// Gauss-Jordan inverse with partial pivoting (X_RR⁻¹ of each eliminated box): grid (CL, nmat).
+__global__ void __launch_bounds__(CK_NT) k_gj_cluster(const long long* __restrict__ offs,
+                                                      const int* __restrict__ dims, cplx* arena,
+                                                      int* status) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int meta[2][2];  // [parity] {pivot row, singular flag}
+  const int n = dims[blockIdx.y];
+  cplx* A = arena + offs[blockIdx.y];
+  const int ncl = (n - rank + CL - 1) / CL;  // local columns
+  cplx* Al = reinterpret_cast<cplx*>(shm);   // n × ncl
+  cplx* buf = Al + (size_t)n * ((n + CL - 1) / CL);  // [2][n] published pivot column (rows swapped)
+  cplx* colsw = buf + 2 * n;                  // local copy of the pivot column
+  int* piv = reinterpret_cast<int*>(colsw + n);  // n
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * ncl; e += CK_NT) {
+    const int i = e % n, l = e / n;
+    Al[e] = A[i + (size_t)(rank + l * CL) * n];
+  }
+  cl.sync();
+  for (int j = 0; j < n; ++j) {
+    const int o = j % CL, lj = j / CL, par = j & 1;
+    if (rank == o) {
+      double pv = -1.0;
+      int p = INT_MAX;
+      for (int i = j + tid; i < n; i += CK_NT) argmax_merge(pv, p, cabs2(Al[i + (size_t)lj * n]), i);
+      block_argmax<CK_NT>(pv, p, red_v, red_i);
+      const bool sing = !(pv > 0.0);
+      if (tid == 0) {
+        meta[par][0] = sing ? j : p;
+        meta[par][1] = sing ? 1 : 0;
+      }
+      if (!sing)
+        for (int i = tid; i < n; i += CK_NT) {
+          const int src = i == j ? p : (i == p ? j : i);
+          buf[par * n + i] = Al[src + (size_t)lj * n];
+        }
+    }
+    cl.sync();
+    const int* rmeta = cl.map_shared_rank(&meta[par][0], o);
+    const int p = rmeta[0];
+    if (rmeta[1]) {
+      if (rank == 0 && tid == 0) atomicExch(status, 1);
+      return;  // uniform across the cluster
+    }
+    const cplx* rb = cl.map_shared_rank(buf + par * n, o);
+    for (int i = tid; i < n; i += CK_NT) colsw[i] = rb[i];
+    if (tid == 0) piv[j] = p;
+    __syncthreads();
+    const cplx dinv = cdiv(cmk(1.0, 0.0), colsw[j]);
+    for (int l = 0; l < ncl; ++l) {
+      const int g = rank + l * CL;
+      cplx* Ac = Al + (size_t)l * n;
+      cplx aj = Ac[j], ap = Ac[p];
+      __syncthreads();
+      if (g == j) {
+        for (int i = tid; i < n; i += CK_NT)
+          Ac[i] = i == j ? dinv : cmk(-(colsw[i].x * dinv.x - colsw[i].y * dinv.y),
+                                      -(colsw[i].x * dinv.y + colsw[i].y * dinv.x));
+      } else {
+        // swap rows j, p of this column, then eliminate
+        const cplx rj = cmul(p == j ? aj : ap, dinv);
+        for (int i = tid; i < n; i += CK_NT) {
+          cplx v = i == p ? aj : (i == j ? ap : Ac[i]);
+          if (p == j) v = Ac[i];
+          Ac[i] = i == j ? rj : cfms(colsw[i], rj, v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // undo the interchanges: output column c = column L[c], L = swaps applied in reverse
+  int* L = piv + n;  // n ints (smem sized for it)
+  __syncthreads();
+  if (tid == 0) {
+    for (int c = 0; c < n; ++c) L[c] = c;
+    for (int j = n - 1; j >= 0; --j) {
+      int a = L[j];
+      L[j] = L[piv[j]];
+      L[piv[j]] = a;
+    }
+  }
+  __syncthreads();
+  cl.sync();  // every CTA has loaded its input columns long ago; safe to overwrite A
+  for (int c = 0; c < n; ++c) {
+    const int g = L[c];
+    if (g % CL != rank) continue;
+    const cplx* src = Al + (size_t)(g / CL) * n;
+    for (int i = tid; i < n; i += CK_NT) A[i + (size_t)c * n] = src[i];
+  }
+}
+
+// Column-pivoted Householder QR of R0 (m × b, ld m) with the stopping rule of reading C9;
+// columns are never moved: the pivot order is recorded and R' (k × b, pivot columns first,
+// then the redundant columns in ascending index) is written back in place.  grid (CL, ntasks).
+__global__ void __launch_bounds__(CK_NT) k_cpqr_cluster(const IdTask* __restrict__ tasks, cplx* ws,
+                                                        int* __restrict__ perm_out, int* __restrict__ k_out,
+                                                        double eps) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ double cand_v;
+  __shared__ int cand_i;
+  __shared__ double hmeta[2][4];  // [parity] {tau, beta.re, beta.im, -}
+  const IdTask t = tasks[blockIdx.y];
+  cplx* M = ws + t.M;
+  const int m = t.m, b = t.b;
+  const int ncl = (b - rank + CL - 1) / CL;
+  const int nclmax = (b + CL - 1) / CL;
+  cplx* Al = reinterpret_cast<cplx*>(shm);          // m × ncl
+  cplx* ub = Al + (size_t)m * nclmax;               // [2][m] published Householder vector
+  cplx* u = ub + 2 * m;                             // local copy
+  double* vn1 = reinterpret_cast<double*>(u + m);   // ncl
+  double* vn2 = vn1 + nclmax;
+  int* piv = reinterpret_cast<int*>(vn2 + nclmax);  // b: pivot columns in order
+  int* done = piv + b;                              // b flags (global column pivoted?)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CK_NT / 32;
+  const double tol3z = sqrt(DBL_EPSILON);
+  for (int e = tid; e < m * ncl; e += CK_NT) {
+    const int i = e % m, l = e / m;
+    Al[e] = M[i + (size_t)(rank + l * CL) * m];
+  }
+  for (int g = tid; g < b; g += CK_NT) done[g] = 0;
+  __syncthreads();
+  for (int l = warp; l < ncl; l += nw) {
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s += cabs2(Al[i + (size_t)l * m]);
+    s = warp_sum(s);
+    if (lane == 0) vn1[l] = vn2[l] = sqrt(s);
+  }
+  __syncthreads();
+  const int kmax = min(m, b);
+  int kk = kmax;
+  double norm0 = 0.0;
+  for (int j = 0; j < kmax; ++j) {
+    const int par = j & 1;
+    // local candidate, then cluster-wide argmax (ties → lowest global column)
+    double pv = -1.0;
+    int p = INT_MAX;
+    for (int l = tid; l < ncl; l += CK_NT) {
+      const int g = rank + l * CL;
+      if (!done[g]) argmax_merge(pv, p, vn1[l], g);
+    }
+    block_argmax<CK_NT>(pv, p, red_v, red_i);
+    if (tid == 0) {
+      cand_v = pv;
+      cand_i = p;
+    }
+    cl.sync();  // (A) candidates published
+    pv = -1.0;
+    p = INT_MAX;
+    for (int r = 0; r < CL; ++r) {
+      const double* rv = cl.map_shared_rank(&cand_v, r);
+      const int* ri = cl.map_shared_rank(&cand_i, r);
+      argmax_merge(pv, p, *rv, *ri);
+    }
+    if (j == 0) norm0 = pv;
+    if (!(pv > eps * norm0) || pv == 0.0) {
+      kk = j;
+      break;  // uniform
+    }
+    const int o = p % CL, lp = p / CL;
+    if (rank == o) {
+      cplx* x = Al + (size_t)lp * m;
+      double xs = 0.0;
+      for (int i = j + 1 + tid; i < m; i += CK_NT) xs += cabs2(x[i]);
+      const double xn2 = block_sum<CK_NT>(xs, red_v);
+      const cplx alpha = x[j];
+      const double aa = sqrt(cabs2(alpha));
+      const double nrm = sqrt(aa * aa + xn2);
+      const cplx beta = aa > 0.0 ? cmk(-alpha.x / aa * nrm, -alpha.y / aa * nrm) : cmk(-nrm, 0.0);
+      const cplx u0 = csub(alpha, beta);
+      for (int i = j + tid; i < m; i += CK_NT) ub[par * m + i] = i == j ? u0 : x[i];
+      if (tid == 0) {
+        hmeta[par][0] = 2.0 / (cabs2(u0) + xn2);
+        hmeta[par][1] = beta.x;
+        hmeta[par][2] = beta.y;
+      }
+      __syncthreads();
+      for (int i = j + tid; i < m; i += CK_NT) x[i] = i == j ? beta : cmk(0.0, 0.0);
+    }
+    cl.sync();  // (B) reflector published
+    const cplx* ru = cl.map_shared_rank(ub + par * m, o);
+    const double tau = *cl.map_shared_rank(&hmeta[par][0], o);
+    for (int i = j + tid; i < m; i += CK_NT) u[i] = ru[i];
+    if (tid == 0) {
+      piv[j] = p;
+      done[p] = 1;
+    }
+    __syncthreads();
+    for (int l = warp; l < ncl; l += nw) {
+      const int g = rank + l * CL;
+      if (done[g]) continue;
+      cplx* Mc = Al + (size_t)l * m;
+      cplx d = cmk(0.0, 0.0);
+      for (int i = j + lane; i < m; i += 32) d = cadd(d, cmulc(u[i], Mc[i]));
+      d = warp_csum(d);
+      const cplx f = cscale(d, tau);
+      for (int i = j + lane; i < m; i += 32) Mc[i] = cfms(f, u[i], Mc[i]);
+      __syncwarp();
+      int recompute = 0;
+      if (lane == 0 && vn1[l] != 0.0) {
+        const double r = sqrt(cabs2(Mc[j])) / vn1[l];
+        const double temp = fmax(0.0, 1.0 - r * r);
+        const double q = vn1[l] / vn2[l];
+        if (temp * q * q <= tol3z) recompute = 1;
+        else vn1[l] *= sqrt(temp);
+      }
+      recompute = __shfl_sync(0xffffffffu, recompute, 0);
+      if (recompute) {
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) s += cabs2(Mc[i]);
+        s = warp_sum(s);
+        if (lane == 0) vn1[l] = vn2[l] = sqrt(s);
+      }
+    }
+    __syncthreads();
+  }
+  // output order: pivots, then the redundant columns in ascending index
+  int* posmap = done;  // reuse: position of global column g in the output
+  __syncthreads();
+  if (tid == 0) {
+    for (int g = 0; g < b; ++g) posmap[g] = -1;
+    for (int q = 0; q < kk; ++q) posmap[piv[q]] = q;
+    int c = kk;
+    for (int g = 0; g < b; ++g)
+      if (posmap[g] < 0) posmap[g] = c++;
+  }
+  __syncthreads();
+  cl.sync();  // all loads of M are long done; write R' in place (rows 0..k-1)
+  for (int l = 0; l < ncl; ++l) {
+    const int g = rank + l * CL;
+    const int c = posmap[g];
+    for (int i = tid; i < kk; i += CK_NT) M[i + (size_t)c * m] = Al[i + (size_t)l * m];
+    if (tid == 0) perm_out[t.out_off + c] = g;
+  }
+  if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+}
+
 // Cooperative Gauss-Jordan inverse (root block D_t⁻¹): columns are
 // owned round-robin by the CTAs; one grid barrier per elimination step.  Output to B
 // (column permutation undone out-of-place).
@@ -713,6 +991,162 @@ __global__ void __launch_bounds__(SV_NT) k_solve_down(const BoxRec* __restrict__
   }
 }
 
+// ---- split solve kernels (more CTAs per box; the factor store is streamed once)
+__global__ void __launch_bounds__(SV_NT) k_su_a(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
+                                                const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                                                cplx* __restrict__ tmp) {
+  extern __shared__ double shm[];
+  const BoxRec R = recs[blockIdx.x];
+  const int k = R.k, r = R.r;
+  cplx* yS = reinterpret_cast<cplx*>(shm);  // k × Q
+  cplx* yR = yS + k * SV_Q;                // r × Q
+  const int* S = idx + R.idxS;
+  const int* Ri = idx + R.idxR;
+  const cplx* T = fac + R.T;
+  const cplx* Xi = fac + R.Xi;
+  cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {
+      int i = e % k, q = e / k;
+      yS[i + q * k] = y[S[i] + (size_t)(q0 + q) * ldy];
+    }
+    __syncthreads();
+    // E: y_R' = y_R − Tᵀ y_S
+    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
+      int i = e % r, q = e / r;
+      cplx v = y[Ri[i] + (size_t)(q0 + q) * ldy];
+      for (int l = 0; l < k; ++l) v = cfms(T[l + (size_t)i * k], yS[l + q * k], v);
+      yR[i + q * r] = v;
+      tb[i + (size_t)(q0 + q) * r] = v;
+    }
+    __syncthreads();
+    // D⁻¹: y_R ← X_RR⁻¹ y_R'
+    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
+      int i = e % r, q = e / r;
+      cplx v = cmk(0.0, 0.0);
+      for (int l = 0; l < r; ++l) v = cfma(Xi[i + (size_t)l * r], yR[l + q * r], v);
+      y[Ri[i] + (size_t)(q0 + q) * ldy] = v;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kSolveChunk) k_su_b(const BoxRec* __restrict__ recs,
+                                                      const SolveItem* __restrict__ items,
+                                                      const cplx* __restrict__ fac, const int* __restrict__ idx,
+                                                      cplx* y, int ldy, int nrhs, const cplx* __restrict__ tmp) {
+  extern __shared__ double shm[];
+  const SolveItem it = items[blockIdx.x];
+  const BoxRec R = recs[it.rec];
+  const int k = R.k, r = R.r, kn = R.k + R.nN;
+  const int f = it.c0 + threadIdx.x;
+  cplx* tr = reinterpret_cast<cplx*>(shm);  // r × Q
+  const cplx* Lp = fac + R.Lp;
+  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < r * nq; e += kSolveChunk) {
+      int i = e % r, q = e / r;
+      tr[i + q * r] = tb[i + (size_t)(q0 + q) * r];
+    }
+    __syncthreads();
+    if (f < kn) {
+      cplx acc[SV_Q];
+#pragma unroll
+      for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
+      for (int i = 0; i < r; ++i) {
+        const cplx l = Lp[f + (size_t)i * kn];
+#pragma unroll
+        for (int q = 0; q < SV_Q; ++q)
+          if (q < nq) acc[q] = cfma(l, tr[i + q * r], acc[q]);
+      }
+      for (int q = 0; q < nq; ++q) {
+        if (f < k) {
+          cplx* d = y + idx[R.idxS + f] + (size_t)(q0 + q) * ldy;
+          *d = csub(*d, acc[q]);
+        } else {
+          cplx* d = y + idx[R.idxN + f - k] + (size_t)(q0 + q) * ldy;
+          atomicAdd(&d->x, -acc[q].x);
+          atomicAdd(&d->y, -acc[q].y);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SV_NT) k_sd_a(const BoxRec* __restrict__ recs, const SolveItem* __restrict__ items,
+                                                const cplx* __restrict__ fac, const int* __restrict__ idx,
+                                                const cplx* y, int ldy, int nrhs, cplx* __restrict__ tmp) {
+  extern __shared__ double shm[];
+  const SolveItem it = items[blockIdx.x];
+  const BoxRec R = recs[it.rec];
+  const int k = R.k, r = R.r, kn = R.k + R.nN;
+  const int fn = min(kSolveChunk, kn - it.c0);
+  cplx* ys = reinterpret_cast<cplx*>(shm);  // kSolveChunk × Q
+  const cplx* Up = fac + R.Up;
+  cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < fn * nq; e += SV_NT) {
+      const int f = e % fn, q = e / fn, ff = it.c0 + f;
+      const int gi = ff < k ? idx[R.idxS + ff] : idx[R.idxN + ff - k];
+      ys[f + q * kSolveChunk] = y[gi + (size_t)(q0 + q) * ldy];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < r; i += SV_NT) {
+      cplx acc[SV_Q];
+#pragma unroll
+      for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
+      for (int f = 0; f < fn; ++f) {
+        const cplx u = Up[i + (size_t)(it.c0 + f) * r];
+#pragma unroll
+        for (int q = 0; q < SV_Q; ++q)
+          if (q < nq) acc[q] = cfma(u, ys[f + q * kSolveChunk], acc[q]);
+      }
+      for (int q = 0; q < nq; ++q) {
+        cplx* d = tb + i + (size_t)(q0 + q) * r;
+        atomicAdd(&d->x, acc[q].x);
+        atomicAdd(&d->y, acc[q].y);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SV_NT) k_sd_b(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
+                                                const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                                                const cplx* __restrict__ tmp) {
+  extern __shared__ double shm[];
+  const BoxRec R = recs[blockIdx.x];
+  const int k = R.k, r = R.r;
+  cplx* yR = reinterpret_cast<cplx*>(shm);  // r × Q
+  const int* S = idx + R.idxS;
+  const int* Ri = idx + R.idxR;
+  const cplx* T = fac + R.T;
+  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
+      int i = e % r, q = e / r;
+      cplx* d = y + Ri[i] + (size_t)(q0 + q) * ldy;
+      const cplx v = csub(*d, tb[i + (size_t)(q0 + q) * r]);  // U: y_R −= Up y_{S∪N}
+      *d = v;
+      yR[i + q * r] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {  // F: y_S −= T y_R
+      int l = e % k, q = e / k;
+      cplx* d = y + S[l] + (size_t)(q0 + q) * ldy;
+      cplx v = *d;
+      for (int i = 0; i < r; ++i) v = cfms(T[l + (size_t)i * k], yR[i + q * r], v);
+      *d = v;
+    }
+    __syncthreads();
+  }
+}
+
 // root: tmp = y[rows]; y[rows] = Xinv · tmp   (one thread per row, column-major Xinv)
 __global__ void k_root_gather(const int* rows, const cplx* y, int ldy, cplx* tmp, int n0, int nrhs) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n0 * nrhs; e += gridDim.x * blockDim.x) {
@@ -720,23 +1154,36 @@ __global__ void k_root_gather(const int* rows, const cplx* y, int ldy, cplx* tmp
     tmp[e] = y[rows[i] + (size_t)q * ldy];
   }
 }
-__global__ void k_root_apply(const cplx* __restrict__ Xi, int n0, const int* __restrict__ rows,
-                             cplx* y, int ldy, int nrhs, const cplx* __restrict__ tmp) {
+// out += Xinv[:, column chunk] · tmp[column chunk]  (grid: row blocks × column chunks, atomics)
+constexpr int RA_COLS = 64;
+__global__ void k_root_apply(const cplx* __restrict__ Xi, int n0, const cplx* __restrict__ tmp, int nrhs,
+                             cplx* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l0 = blockIdx.y * RA_COLS, l1 = min(n0, l0 + RA_COLS);
   for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
     const int nq = min(SV_Q, nrhs - q0);
     if (i < n0) {
       cplx acc[SV_Q];
 #pragma unroll
       for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
-      for (int l = 0; l < n0; ++l) {
+      for (int l = l0; l < l1; ++l) {
         const cplx a = Xi[i + (size_t)l * n0];
 #pragma unroll
         for (int q = 0; q < SV_Q; ++q)
           if (q < nq) acc[q] = cfma(a, tmp[l + (size_t)(q0 + q) * n0], acc[q]);
       }
-      for (int q = 0; q < nq; ++q) y[rows[i] + (size_t)(q0 + q) * ldy] = acc[q];
+      for (int q = 0; q < nq; ++q) {
+        cplx* d = out + i + (size_t)(q0 + q) * n0;
+        atomicAdd(&d->x, acc[q].x);
+        atomicAdd(&d->y, acc[q].y);
+      }
     }
+  }
+}
+__global__ void k_root_scatter(const int* rows, cplx* y, int ldy, const cplx* out, int n0, int nrhs) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n0 * nrhs; e += gridDim.x * blockDim.x) {
+    int i = e % n0, q = e / n0;
+    y[rows[i] + (size_t)q * ldy] = out[e];
   }
 }
 
@@ -881,6 +1328,63 @@ void launch_qr_panel(const QrChunk* d_chunks, int nchunks, int j0, int nb, cudaS
   FMMLU_LAUNCH();
 }
 
+namespace {
+constexpr size_t kClusterSmemCap = 220 * 1024;
+size_t gj_smem(int n, int CL) {
+  return (size_t)n * ((n + CL - 1) / CL) * sizeof(cplx) + 3 * (size_t)n * sizeof(cplx) + 2 * (size_t)n * sizeof(int) + 64;
+}
+size_t cpqr_smem(int m, int b, int CL) {
+  const int ncl = (b + CL - 1) / CL;
+  return (size_t)m * ncl * sizeof(cplx) + 3 * (size_t)m * sizeof(cplx) + 2 * (size_t)ncl * sizeof(double) +
+         2 * (size_t)b * sizeof(int) + 64;
+}
+template <class K>
+void cluster_attrs(K kern, size_t smem, int CL) {
+  FMMLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+template <class K, class... Args>
+void launch_cluster(K kern, int CL, int ny, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL, ny, 1);
+  cfg.blockDim = dim3(CK_NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FMMLU_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+}  // namespace
+
+bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,
+                       cudaStream_t st, int nmax) {
+  if (nmat <= 0) return true;
+  int CL = 1;
+  while (CL <= 16 && gj_smem(nmax, CL) > kClusterSmemCap) CL *= 2;
+  if (CL > 16) return false;
+  const size_t smem = gj_smem(nmax, CL);
+  cluster_attrs(k_gj_cluster, smem, CL);
+  launch_cluster(k_gj_cluster, CL, nmat, smem, st, d_off, d_dim, arena, d_status);
+  return true;
+}
+
+bool launch_cpqr_cluster(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out, double eps,
+                         cudaStream_t st, int mmax, int bmax) {
+  if (ntasks <= 0) return true;
+  int CL = 1;
+  while (CL <= 16 && cpqr_smem(mmax, bmax, CL) > kClusterSmemCap) CL *= 2;
+  if (CL > 16) return false;
+  const size_t smem = cpqr_smem(mmax, bmax, CL);
+  cluster_attrs(k_cpqr_cluster, smem, CL);
+  launch_cluster(k_cpqr_cluster, CL, ntasks, smem, st, d_tasks, ws, perm_out, k_out, eps);
+  return true;
+}
+
 void launch_cpqr(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out,
                  double eps, cudaStream_t st, int bmax) {
   if (ntasks <= 0) return;
@@ -964,12 +1468,58 @@ void launch_solve_down(const BoxRec* d_recs, int nrec, const cplx* fac, const in
 }
 
 
+void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                      const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax) {
+  if (nrec <= 0) return;
+  size_t sa = (size_t)(kmax + rmax) * SV_Q * sizeof(cplx) + 16;
+  size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
+  static size_t ca = 0, cb = 0;
+  if (sa > 48 * 1024 && sa > ca) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_su_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa));
+    ca = sa;
+  }
+  if (sb > 48 * 1024 && sb > cb) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_su_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    cb = sb;
+  }
+  k_su_a<<<nrec, SV_NT, sa, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp);
+  FMMLU_LAUNCH();
+  if (nitems > 0) {
+    k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
+    FMMLU_LAUNCH();
+  }
+}
+
+void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                        const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax) {
+  if (nrec <= 0) return;
+  size_t sa = (size_t)kSolveChunk * SV_Q * sizeof(cplx) + 16;
+  size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
+  static size_t cb = 0;
+  if (sb > 48 * 1024 && sb > cb) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_sd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+    cb = sb;
+  }
+  if (nitems > 0) {
+    k_sd_a<<<nitems, SV_NT, sa, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
+    FMMLU_LAUNCH();
+  }
+  k_sd_b<<<nrec, SV_NT, sb, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp);
+  FMMLU_LAUNCH();
+}
+
 void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
                        cplx* tmp, cudaStream_t st) {
   if (n0 <= 0) return;
+  // tmp holds 2·n0·nrhs: [gathered input | output accumulator]
+  cplx* out = tmp + (size_t)n0 * nrhs;
+  FMMLU_CUDA(cudaMemsetAsync(out, 0, (size_t)n0 * nrhs * sizeof(cplx), st));
   k_root_gather<<<256, 256, 0, st>>>(d_rows, y, ldy, tmp, n0, nrhs);
   FMMLU_LAUNCH();
-  k_root_apply<<<(n0 + 127) / 128, 128, 0, st>>>(Xinv, n0, d_rows, y, ldy, nrhs, tmp);
+  dim3 grid((n0 + 127) / 128, (n0 + RA_COLS - 1) / RA_COLS);
+  k_root_apply<<<grid, 128, 0, st>>>(Xinv, n0, tmp, nrhs, out);
+  FMMLU_LAUNCH();
+  k_root_scatter<<<256, 256, 0, st>>>(d_rows, y, ldy, out, n0, nrhs);
   FMMLU_LAUNCH();
 }
 

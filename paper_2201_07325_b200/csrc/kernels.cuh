@@ -60,6 +60,13 @@ struct BoxRec {
   long long T, Xi, Up, Lp;  // T: k×r, Xinv: r×r, Up: r×(k+nN), Lp: (k+nN)×r
   int k, r, nN;
   int idxS, idxR, idxN;     // offsets into the index arena (global tree-order indices)
+  int tmp;                  // offset (in units of r·nrhs rows) of the box's solve scratch
+};
+
+// (box, chunk) work items of the split solve kernels
+struct SolveItem {
+  int rec;    // BoxRec index
+  int c0;     // first row (upward, rows of Lp) or first column (downward, columns of Up)
 };
 
 void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const int* slot,
@@ -80,6 +87,14 @@ void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx
 // in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
 void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx* arena,
                        int* d_status, cudaStream_t st, int nmax);
+// Thread-block-cluster versions (matrix resident in distributed shared memory); return false
+// when the matrix is too large for a 16-CTA cluster (caller falls back to the kernels above).
+bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,
+                       cudaStream_t st, int nmax);
+// CPQR of R0 with the columns left in place: writes R' = [R11 R12] (pivot columns first, then
+// the redundant ones in ascending index) over rows 0..k-1 and perm = that column order.
+bool launch_cpqr_cluster(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out, double eps,
+                         cudaStream_t st, int mmax, int bmax);
 // cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
 void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
 // solve sweeps for one (level, colour) phase
@@ -87,6 +102,14 @@ void launch_solve_up(const BoxRec* d_recs, int nrec, const cplx* fac, const int*
                      int ldy, int nrhs, cudaStream_t st, int kmax, int rmax);
 void launch_solve_down(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
                        int ldy, int nrhs, cudaStream_t st, int rmax);
+// Split solve sweeps for one phase:
+//   up:   [a] y_R' = y_R − Tᵀy_S → tmp, y_R ← X_RR⁻¹ y_R'   [b] y_{S∪N} −= Lp tmp (row chunks)
+//   down: [a] acc = Up y_{S∪N} (column chunks, atomics)    [b] y_R −= acc, y_S −= T y_R
+constexpr int kSolveChunk = 128;
+void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                      const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax);
+void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                        const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax);
 // y[rows] = Xinv (n0×n0) · y[rows] for the root block
 void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
                        cplx* tmp, cudaStream_t st);
