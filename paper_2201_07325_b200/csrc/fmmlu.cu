@@ -254,217 +254,71 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cp
   tiles.clear();
 }
 
-// ---------------------------------------------------------------------------- TSQR + blocked QR
-// R0_j = triu(R) of M_j = Q R for each box j (only R is needed: CPQR(R0) selects the same
-// pivots and T as CPQR(M) because Qᴴ preserves column norms and inner products).  Rows of M
-// are split into chunks of ≤ H rows (H ≥ 2b), each chunk is QR-factored by the blocked
-// Householder method (panel in shared memory, WY trailing update on the DMMA GEMM), the
-// chunks' R factors are stacked, and the process repeats until one chunk remains (TSQR).
-struct R0Out {
-  DBuf R;                    // compact R0 matrices (ld = rows)
-  std::vector<long long> off;
-  std::vector<int> rows;
-};
-
-void tsqr_R0(fmmlu_handle* h, cplx* Mbase, const std::vector<long long>& moff,
-             const std::vector<int>& mrows, const std::vector<int>& bcol, R0Out& out) {
+// ---------------------------------------------------------------------------- cluster TSQR
+// Only R of M = Q R is needed (CPQR(R) selects the same pivots and T as CPQR(M): Qᴴ preserves
+// column norms and inner products).  Each round splits every box matrix that does not fit one
+// 16-CTA cluster into row chunks that do, factors them with the cluster Householder kernel
+// (chunk resident in distributed shared memory), and stacks the triangular factors; repeat
+// until the box matrix fits a cluster for the pivoted pass.  mp/mrows are updated (ld = rows).
+void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mrows, const std::vector<int>& bcol,
+                  std::vector<DBuf>& keep) {
   cudaStream_t st = h->stream;
   Prof& P = h->prof;
-  const int nbx = (int)moff.size();
-  int bmax = 0;
-  for (int b : bcol) bmax = std::max(bmax, b);
-  int NB = 16, H = 800;
-  if (2 * bmax >= H) { NB = 8; H = 1600; }
-  if (2 * bmax >= H) throw Error(FMMLU_ENOTIMPL, "box with more than 799 actives: TSQR chunking not built");
-  long long r0tot = 0;
-  out.off.assign(nbx, 0);
-  out.rows.assign(nbx, 0);
-  for (int j = 0; j < nbx; ++j) {
-    out.off[j] = r0tot;
-    r0tot += (long long)bcol[j] * bcol[j];
-  }
-  out.R.alloc((size_t)std::max<long long>(r0tot, 1) * sizeof(cplx), st);
-  std::vector<cplx*> base(nbx, Mbase);
-  std::vector<long long> off = moff;
-  std::vector<int> rows = mrows, ld = mrows;
-  std::vector<char> done(nbx, 0);
-  DBuf arena;  // stacked matrices of the current round (owns them after round 0)
-  for (int round = 0;; ++round) {
-    struct Ch { int box; int h; long long r0; };
-    std::vector<Ch> chs;
-    long long qws = 0;
-    for (int j = 0; j < nbx; ++j) {
-      if (done[j]) continue;
-      int nch = rows[j] <= H ? 1 : (rows[j] + H - 1) / H;
-      int bh = rows[j] / nch, ex = rows[j] % nch;
-      long long r0 = 0;
-      for (int c = 0; c < nch; ++c) {
-        int hc = bh + (c < ex ? 1 : 0);
-        chs.push_back({j, hc, r0});
-        r0 += hc;
-        qws += 2LL * hc * NB + (long long)NB * bcol[j];
+  const int nbx = (int)mp.size();
+  for (;;) {
+    std::vector<int> todo;
+    int bmax = 0;
+    for (int j = 0; j < nbx; ++j)
+      if (hqr_cluster_size(mrows[j], bcol[j]) == 0) {
+        todo.push_back(j);
+        bmax = std::max(bmax, bcol[j]);
       }
-    }
-    DBuf qw;
-    qw.alloc((size_t)qws * sizeof(cplx), st);
-    std::vector<QrChunk> qc;
-    long long q = 0;
-    int jmax = 0;
-    for (auto& c : chs) {
-      QrChunk x{};
-      x.A = base[c.box] + off[c.box] + c.r0;
-      x.lda = ld[c.box];
-      x.h = c.h;
-      x.b = bcol[c.box];
-      x.V = qw.as<cplx>() + q;
-      q += (long long)c.h * NB;
-      x.Z = qw.as<cplx>() + q;
-      q += (long long)c.h * NB;
-      x.W = qw.as<cplx>() + q;
-      q += (long long)NB * x.b;
-      qc.push_back(x);
-      jmax = std::max(jmax, std::min(c.h, x.b));
-    }
-    // all panels' GEMM batches, uploaded once
-    std::vector<GemmProblem> gp;
-    std::vector<GemmTile> gt;
-    struct Launch { size_t p0, t0, nt; };
-    std::vector<Launch> l1, l2;
-    double fl = 0, by = 0;
-    for (int j0 = 0; j0 < jmax; j0 += NB) {
-      for (int pass = 0; pass < 2; ++pass) {
-        std::vector<GemmProblem> pp;
-        std::vector<GemmTile> tt;
-        for (auto& x : qc) {
-          int kmax = std::min(x.h, x.b);
-          if (j0 >= kmax) continue;
-          int jb = std::min(NB, kmax - j0), nt = x.b - j0 - jb, hr = x.h - j0;
-          if (nt <= 0) continue;
-          GemmProblem g{};
-          cplx* At = x.A + j0 + (size_t)(j0 + jb) * x.lda;
-          if (pass == 0) {  // W = Vᴴ A_t  (split-K over the tall dimension, atomic accumulate)
-            g.m = jb; g.n = nt; g.k = hr;
-            g.opA = kOpC; g.opB = kOpN;
-            g.A = x.V; g.lda = x.h;
-            g.B = At; g.ldb = x.lda;
-            g.C = x.W; g.ldc = NB;
-            g.kchunk = hr > 128 ? 64 : 0;
-          } else {          // A_t −= Z W
-            g.m = hr; g.n = nt; g.k = jb;
-            g.opA = kOpN; g.opB = kOpN;
-            g.A = x.Z; g.lda = x.h;
-            g.B = x.W; g.ldb = NB;
-            g.C = At; g.ldc = x.lda;
-          }
-          add_gemm(pp, tt, g);
-        }
-        double f1, b1;
-        gemm_work(pp, f1, b1);
-        fl += f1;
-        by += b1;
-        Launch L{gp.size(), gt.size(), tt.size()};
-        for (auto& t : tt) t.p += (int)gp.size() - (int)0;  // local → global index fixed below
-        gp.insert(gp.end(), pp.begin(), pp.end());
-        gt.insert(gt.end(), tt.begin(), tt.end());
-        (pass == 0 ? l1 : l2).push_back(L);
-      }
-    }
-    // tile problem indices are global; pass the full problem array to every launch
-    Stage s;
-    size_t o_c = s.add(qc), o_p = s.add(gp), o_t = s.add(gt);
-    s.upload(st);
-    int id = P.begin(FMMLU_K_QR, st);
-    int pi = 0;
-    for (int j0 = 0; j0 < jmax; j0 += NB, ++pi) {
-      launch_qr_panel(s.ptr<QrChunk>(o_c), (int)qc.size(), j0, NB, st);
-      P.add(FMMLU_K_QR, 0, 0, 1);
-      const Launch& a = l1[pi];
-      const Launch& b = l2[pi];
-      if (a.nt) {
-        gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_t) + a.t0, (int)a.nt, cmk(1.0, 0.0), 0, nullptr, st);
-        P.add(FMMLU_K_QR, 0, 0, 1);
-      }
-      if (b.nt) {
-        gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_t) + b.t0, (int)b.nt, cmk(-1.0, 0.0), 0, nullptr, st);
-        P.add(FMMLU_K_QR, 0, 0, 1);
-      }
-    }
-    P.end(id, st);
-    // panel flops (Householder on h×jb panels) + GEMM flops
-    for (auto& x : qc) {
-      double m_ = x.h, n_ = std::min(x.h, x.b);
-      fl += 8.0 * (m_ * n_ * NB);  // panel BLAS-2 part (upper bound)
-    }
-    P.add(FMMLU_K_QR, fl, by, 0);
-    // collect: finished boxes → R0; others → stacked matrices for the next round
-    std::vector<CopyTask> fin, stk;
+    if (todo.empty()) return;
+    const int H = hqr_max_rows(bmax, 16);
+    if (H <= bmax) throw Error(FMMLU_ENOTIMPL, "box with too many actives for the cluster TSQR");
     std::vector<long long> noff(nbx, 0);
     std::vector<int> nrows(nbx, 0);
-    long long ntot = 0;
-    size_t ci = 0;
-    for (int j = 0; j < nbx; ++j) {
-      if (done[j]) continue;
-      size_t c0 = ci;
-      while (ci < chs.size() && chs[ci].box == j) ++ci;
-      const int b = bcol[j];
-      if (ci - c0 == 1) {
-        int r = std::min(chs[c0].h, b);
-        CopyTask t{};
-        t.src = off[j];
-        t.lds = ld[j];
-        t.dst = out.off[j];
-        t.ldd = std::max(r, 1);
-        t.rows = r;
-        t.cols = b;
-        t.rmap_off = t.cmap_off = -1;
-        t.tri = 1;
-        fin.push_back(t);
-        out.rows[j] = r;
-        done[j] = 1;
-      } else {
-        int rr = 0;
-        for (size_t c = c0; c < ci; ++c) rr += std::min(chs[c].h, b);
-        noff[j] = ntot;
-        nrows[j] = rr;
-        ntot += (long long)rr * b;
-        int r0 = 0;
-        for (size_t c = c0; c < ci; ++c) {
-          int r = std::min(chs[c].h, b);
-          CopyTask t{};
-          t.src = off[j] + chs[c].r0;
-          t.lds = ld[j];
-          t.dst = noff[j] + r0;
-          t.ldd = rr;
-          t.rows = r;
-          t.cols = b;
-          t.rmap_off = t.cmap_off = -1;
-          t.tri = 1;
-          stk.push_back(t);
-          r0 += r;
-        }
-      }
+    long long tot = 0;
+    for (int j : todo) {
+      const int nch = (mrows[j] + H - 1) / H, bh = mrows[j] / nch, ex = mrows[j] % nch;
+      int rr = 0;
+      for (int c = 0; c < nch; ++c) rr += std::min(bh + (c < ex ? 1 : 0), bcol[j]);
+      noff[j] = tot;
+      nrows[j] = rr;
+      tot += (long long)rr * bcol[j];
     }
     DBuf next;
-    if (!stk.empty()) next.alloc((size_t)ntot * sizeof(cplx), st);
-    {
-      std::vector<int> nomap{0};
-      Stage s2;
-      size_t o_f = s2.add(fin), o_s = s2.add(stk), o_m = s2.add(nomap);
-      s2.upload(st);
-      cplx* src = round == 0 ? Mbase : arena.as<cplx>();
-      launch_copy(s2.ptr<CopyTask>(o_f), (int)fin.size(), s2.ptr<int>(o_m), src, out.R.as<cplx>(), st);
-      launch_copy(s2.ptr<CopyTask>(o_s), (int)stk.size(), s2.ptr<int>(o_m), src, next.as<cplx>(), st);
-      P.add(FMMLU_K_QR, 0, 0, (fin.empty() ? 0 : 1) + (stk.empty() ? 0 : 1));
-    }
-    if (stk.empty()) break;
-    arena = std::move(next);
-    for (int j = 0; j < nbx; ++j)
-      if (!done[j]) {
-        base[j] = arena.as<cplx>();
-        off[j] = noff[j];
-        rows[j] = nrows[j];
-        ld[j] = nrows[j];
+    next.alloc((size_t)tot * sizeof(cplx), st);
+    std::vector<ClusterQrTask> tasks;
+    int hmax = 1;
+    double fl = 0, by = 0;
+    for (int j : todo) {
+      const int nch = (mrows[j] + H - 1) / H, bh = mrows[j] / nch, ex = mrows[j] % nch, b = bcol[j];
+      int r0 = 0, ro = 0;
+      for (int c = 0; c < nch; ++c) {
+        const int hc = bh + (c < ex ? 1 : 0);
+        tasks.push_back(ClusterQrTask{mp[j] + r0, next.as<cplx>() + noff[j] + ro, mrows[j], hc, b, nrows[j], 0, 0});
+        r0 += hc;
+        ro += std::min(hc, b);
+        hmax = std::max(hmax, hc);
+        const double kq = std::min(hc, b);
+        fl += 8.0 * ((double)hc * b * kq - 0.5 * (hc + b) * kq * kq + kq * kq * kq / 3.0);
+        by += 16.0 * hc * b + 16.0 * kq * b;
       }
+    }
+    Stage s;
+    size_t o_t = s.add(tasks);
+    s.upload(st);
+    int id = P.begin(FMMLU_K_QR, st);
+    launch_hqr_cluster(s.ptr<ClusterQrTask>(o_t), (int)tasks.size(), 0, nullptr, nullptr, 0.0, st, hmax, bmax);
+    P.end(id, st);
+    P.add(FMMLU_K_QR, fl, by, 1);
+    for (int j : todo) {
+      mp[j] = next.as<cplx>() + noff[j];
+      mrows[j] = nrows[j];
+    }
+    keep.push_back(std::move(s.dev));
+    keep.push_back(std::move(next));
   }
 }
 
@@ -654,6 +508,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         long long Moff = 0, Toff = 0;
         int permoff = 0;
         int k = 0;
+        int mfin = 0;  // rows of the matrix the pivoted pass ran on
       };
       std::vector<BoxJob> jobs;
       for (int bx : T.levels[lvl]) {
@@ -764,7 +619,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             pts.push_back(p);
           }
           IdTask it{};
-          it.M = J.Moff;
+          it.Mp = nullptr;
           it.m = J.m;
           it.b = J.b;
           it.out_off = J.permoff;
@@ -790,34 +645,34 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           h->prof.add(FMMLU_K_GATHER, fl, by, (cps.empty() ? 0 : 1) + (pts.empty() ? 0 : 1));
         }
         keep.push_back(std::move(s.dev));
-        // TSQR/blocked-QR → R0, then CPQR(R0) and T = R11⁻¹R12
-        std::vector<long long> moff;
-        std::vector<int> mrows, bcol;
-        for (auto& J : jobs) {
-          moff.push_back(J.Moff);
-          mrows.push_back(J.m);
-          bcol.push_back(J.b);
-        }
-        R0Out r0;
-        tsqr_R0(h, M.as<cplx>(), moff, mrows, bcol, r0);
+        // TSQR rounds (cluster QR) until each box's matrix fits one cluster, then cluster CPQR
+        // on it and T = R11⁻¹R12
+        std::vector<cplx*> mp(nj);
+        std::vector<int> mrows(nj), bcol(nj);
         for (int j = 0; j < nj; ++j) {
-          ids[j].M = r0.off[j];
-          ids[j].m = r0.rows[j];
+          mp[j] = M.as<cplx>() + jobs[j].Moff;
+          mrows[j] = jobs[j].m;
+          bcol[j] = jobs[j].b;
+        }
+        tsqr_cluster(h, mp, mrows, bcol, keep);
+        std::vector<ClusterQrTask> cq(nj);
+        int mmax0 = 1;
+        for (int j = 0; j < nj; ++j) {
+          ids[j].Mp = mp[j];
+          ids[j].m = mrows[j];
+          cq[j] = ClusterQrTask{mp[j], nullptr, mrows[j], mrows[j], bcol[j], 0, jobs[j].permoff, 0};
+          jobs[j].mfin = mrows[j];
+          mmax0 = std::max(mmax0, mrows[j]);
         }
         Stage s2;
-        size_t o_i = s2.add(ids);
+        size_t o_i = s2.add(ids), o_q = s2.add(cq);
         s2.upload(st);
         int cid = h->prof.begin(FMMLU_K_CPQR, st);
-        int mmax0 = 1;
-        for (int j = 0; j < nj; ++j) mmax0 = std::max(mmax0, r0.rows[j]);
-        if (!launch_cpqr_cluster(s2.ptr<IdTask>(o_i), nj, r0.R.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st,
-                                 mmax0, bmax))
-          launch_cpqr(s2.ptr<IdTask>(o_i), nj, r0.R.as<cplx>(), permd.as<int>(), kd.as<int>(), eps, st, bmax);
-        launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, r0.R.as<cplx>(), Tb.as<cplx>(), st);
+        launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st, mmax0, bmax);
+        launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
         h->prof.end(cid, st);
         h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
         keep.push_back(std::move(s2.dev));
-        keep.push_back(std::move(r0.R));
       }
       std::vector<int> hk(nj), hperm(permtot);
       FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -833,10 +688,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       for (int j = 0; j < nj; ++j) {
         jobs[j].k = hk[j];
         int r = jobs[j].b - hk[j];
-        {  // CPQR(R0) + T algorithmic flops: 8(b²k − bk² + k³/3) + 4k²r
-          double b_ = jobs[j].b, k_ = hk[j];
-          h->prof.add(FMMLU_K_CPQR, 8.0 * (b_ * b_ * k_ - b_ * k_ * k_ + k_ * k_ * k_ / 3.0) + 4.0 * k_ * k_ * r,
-                      16.0 * b_ * b_, 0);
+        {  // CPQR on m'×b + T: 8(m'bk − (m'+b)k²/2 + k³/3) + 4k²r real flops
+          double b_ = jobs[j].b, k_ = hk[j], m_ = jobs[j].mfin;
+          h->prof.add(FMMLU_K_CPQR,
+                      8.0 * (m_ * b_ * k_ - 0.5 * (m_ + b_) * k_ * k_ + k_ * k_ * k_ / 3.0) + 4.0 * k_ * k_ * r,
+                      16.0 * m_ * b_, 0);
         }
         S.ranks_sum[lvl] += hk[j];
         S.boxes[lvl] += 1;

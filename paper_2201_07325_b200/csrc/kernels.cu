@@ -153,291 +153,7 @@ __global__ void k_proxy(const ProxyTask* __restrict__ tasks, const int* __restri
   }
 }
 
-// ------------------------------------------------------------------ blocked Householder QR panel
-// Hermitian reflectors H = I − τ v vᴴ (τ real, v_0 = 1) with H x = β e1, β = −(α/|α|)‖x‖.
-constexpr int QP_NT = 512;
-constexpr int QP_NBMAX = 16;
-
-__global__ void __launch_bounds__(QP_NT) k_qr_panel(const QrChunk* __restrict__ chunks, int j0, int NB) {
-  extern __shared__ double shm[];
-  __shared__ double tau[QP_NBMAX];
-  __shared__ cplx betas[QP_NBMAX];
-  __shared__ cplx G[QP_NBMAX][QP_NBMAX];
-  __shared__ cplx Tm[QP_NBMAX][QP_NBMAX];
-  const QrChunk c = chunks[blockIdx.x];
-  const int kmax = min(c.h, c.b);
-  if (j0 >= kmax) return;
-  const int jb = min(NB, kmax - j0);
-  const int hr = c.h - j0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  cplx* P = reinterpret_cast<cplx*>(shm);  // hr × jb, ld hr
-  cplx* A = c.A;
-  // rows are owned by threads (i ≡ tid mod QP_NT) for the whole factorization, so the only
-  // barriers per column are the norm reduction and the two-step dot reduction.
-  double xs = 0.0;  // this thread's part of ‖P[jj+1:, jj]‖² for the current column
-  for (int e = tid; e < hr * jb; e += QP_NT) {
-    const int i = e % hr, jj = e / hr;
-    const cplx v = A[(j0 + i) + (size_t)(j0 + jj) * c.lda];
-    P[e] = v;
-  }
-  for (int i = 1 + tid; i < hr; i += QP_NT) {
-    const cplx v = A[(j0 + i) + (size_t)j0 * c.lda];
-    xs += cabs2(v);
-  }
-  __shared__ double nred[2][QP_NT / 32];
-  __shared__ cplx dred[2][QP_NT / 32][QP_NBMAX];
-  __shared__ cplx dots2[2][QP_NBMAX];
-  for (int jj = 0; jj < jb; ++jj) {
-    const int par = jj & 1;
-    double ws_ = warp_sum(xs);
-    if (lane == 0) nred[par][warp] = ws_;
-    __syncthreads();  // (1) column jj final after the previous update; norm partials visible
-    double xn2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < QP_NT / 32; ++w) xn2 += nred[par][w];
-    const cplx alpha = P[jj + jj * hr];
-    const double aa = sqrt(cabs2(alpha));
-    const double nrm = sqrt(aa * aa + xn2);
-    const int nrest = jb - jj - 1;
-    xs = 0.0;
-    if (nrm == 0.0) {  // zero column: identity reflector (uniform branch)
-      if (tid == 0) {
-        tau[jj] = 0.0;
-        betas[jj] = cmk(0.0, 0.0);
-      }
-      if (nrest > 0)
-        for (int i = jj + 2 + tid; i < hr; i += QP_NT) xs += cabs2(P[i + (jj + 1) * hr]);
-      continue;
-    }
-    const cplx beta = aa > 0.0 ? cmk(-alpha.x / aa * nrm, -alpha.y / aa * nrm) : cmk(-nrm, 0.0);
-    const cplx u0 = csub(alpha, beta);
-    const double u02 = cabs2(u0);
-    const cplx inv_u0 = cmk(u0.x / u02, -u0.y / u02);
-    const double tj = 2.0 * u02 / (u02 + xn2);
-    // v (v_jj = 1) written in place, partial dots d_q = vᴴ P[jj:, jj+1+q]
-    cplx d[QP_NBMAX];
-#pragma unroll
-    for (int q = 0; q < QP_NBMAX; ++q) d[q] = cmk(0.0, 0.0);
-    for (int i = jj + tid; i < hr; i += QP_NT) {
-      cplx v;
-      if (i == jj) {
-        v = cmk(1.0, 0.0);  // β goes to the diagonal after the loop (others may still read α)
-      } else {
-        v = cmul(P[i + jj * hr], inv_u0);
-        P[i + jj * hr] = v;
-      }
-#pragma unroll
-      for (int q = 0; q < QP_NBMAX; ++q)
-        if (q < nrest) d[q] = cadd(d[q], cmulc(v, P[i + (jj + 1 + q) * hr]));
-    }
-    if (tid == 0) {
-      tau[jj] = tj;
-      betas[jj] = beta;
-    }
-    if (nrest == 0) continue;
-#pragma unroll
-    for (int q = 0; q < QP_NBMAX; ++q)
-      if (q < nrest) {
-        const cplx s = warp_csum(d[q]);
-        if (lane == 0) dred[par][warp][q] = s;
-      }
-    __syncthreads();  // (2)
-    if (tid < nrest) {
-      cplx s = cmk(0.0, 0.0);
-#pragma unroll
-      for (int w = 0; w < QP_NT / 32; ++w) s = cadd(s, dred[par][w][tid]);
-      dots2[par][tid] = cscale(s, tj);
-    }
-    __syncthreads();  // (3)
-    for (int i = jj + tid; i < hr; i += QP_NT) {
-      const cplx v = i == jj ? cmk(1.0, 0.0) : P[i + jj * hr];
-#pragma unroll
-      for (int q = 0; q < QP_NBMAX; ++q)
-        if (q < nrest) {
-          const cplx nv = cfms(dots2[par][q], v, P[i + (jj + 1 + q) * hr]);
-          P[i + (jj + 1 + q) * hr] = nv;
-          if (q == 0 && i > jj + 1) xs += cabs2(nv);
-        }
-    }
-  }
-  __syncthreads();
-  if (tid < jb) P[tid + tid * hr] = betas[tid];
-  __syncthreads();
-  // R rows back to A (upper triangle of the panel's top jb rows)
-  for (int e = tid; e < jb * jb; e += QP_NT) {
-    const int i = e % jb, jj = e / jb;
-    if (i <= jj) A[(j0 + i) + (size_t)(j0 + jj) * c.lda] = P[i + jj * hr];
-  }
-  // explicit V (unit diagonal, zeros above) and G = Vᴴ V
-  cplx* V = c.V;
-  for (int e = tid; e < hr * jb; e += QP_NT) {
-    const int i = e % hr, jj = e / hr;
-    V[i + (size_t)jj * c.h] = i < jj ? cmk(0.0, 0.0) : (i == jj ? cmk(1.0, 0.0) : P[i + jj * hr]);
-  }
-  {
-    // 4 threads per (p, q) pair with p < q; rows strided
-    const int pair = tid >> 2, part = tid & 3;
-    const int npairs = jb * (jb - 1) / 2;
-    for (int pb = 0; pb < npairs; pb += QP_NT / 4) {
-      const int pr = pb + pair;
-      cplx s = cmk(0.0, 0.0);
-      int p = 0, q = 0;
-      if (pr < npairs) {
-        // decode pr -> (p, q), p < q
-        int rem = pr;
-        q = 1;
-        while (rem >= q) {
-          rem -= q;
-          ++q;
-        }
-        p = rem;
-        for (int i = q + part; i < hr; i += 4) {
-          const cplx vp = i == p ? cmk(1.0, 0.0) : (i < p ? cmk(0.0, 0.0) : P[i + p * hr]);
-          const cplx vq = i == q ? cmk(1.0, 0.0) : P[i + q * hr];
-          s = cadd(s, cmulc(vp, vq));
-        }
-      }
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
-      if (pr < npairs && part == 0) G[p][q] = s;
-    }
-  }
-  __syncthreads();
-  // T (upper triangular): T_ii = τ_i, T(0:i, i) = −τ_i T(0:i,0:i) G(0:i, i)
-  if (warp == 0) {
-    for (int i = 0; i < jb; ++i) {
-      cplx t = cmk(0.0, 0.0);
-      if (lane < i) {
-        for (int q = lane; q < i; ++q) t = cfma(Tm[lane][q], G[q][i], t);
-        t = cscale(t, -tau[i]);
-      }
-      __syncwarp();
-      if (lane < i) Tm[lane][i] = t;
-      if (lane == i) Tm[i][i] = cmk(tau[i], 0.0);
-      if (lane > i && lane < jb) Tm[lane][i] = cmk(0.0, 0.0);
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  // Z = V Tᴴ :  Z[i][cc] = Σ_{p ≥ cc} V[i][p] conj(T[cc][p])
-  cplx* Z = c.Z;
-  for (int e = tid; e < hr * jb; e += QP_NT) {
-    const int i = e % hr, cc = e / hr;
-    cplx s = cmk(0.0, 0.0);
-    for (int p = cc; p < jb && p <= i; ++p) {
-      const cplx v = i == p ? cmk(1.0, 0.0) : P[i + p * hr];
-      const cplx tc = cmk(Tm[cc][p].x, -Tm[cc][p].y);
-      s = cfma(v, tc, s);
-    }
-    Z[i + (size_t)cc * c.h] = s;
-  }
-  // zero W (jb × (b − j0 − jb)) for the next GEMM's accumulation
-  cplx* W = c.W;
-  const int nt = c.b - j0 - jb;
-  for (int e = tid; e < NB * nt; e += QP_NT) W[e] = cmk(0.0, 0.0);
-}
-
-// ------------------------------------------------------------------ CPQR
 constexpr int QR_NT = 512;
-
-__global__ void __launch_bounds__(QR_NT) k_cpqr(const IdTask* __restrict__ tasks, cplx* ws,
-                                                int* __restrict__ perm_out, int* __restrict__ k_out,
-                                                double eps) {
-  extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  const IdTask t = tasks[blockIdx.x];
-  cplx* M = ws + t.M;
-  const int m = t.m, b = t.b;
-  double* vn1 = shm;
-  double* vn2 = shm + b;
-  int* perm = reinterpret_cast<int*>(shm + 2 * b);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = QR_NT / 32;
-  const double tol3z = sqrt(DBL_EPSILON);
-
-  for (int c = warp; c < b; c += nw) {
-    double s = 0.0;
-    for (int i = lane; i < m; i += 32) s += cabs2(M[i + (size_t)c * m]);
-    s = warp_sum(s);
-    if (lane == 0) {
-      vn1[c] = vn2[c] = sqrt(s);
-      perm[c] = c;
-    }
-  }
-  __syncthreads();
-  const int kmax = min(m, b);
-  int kk = kmax;
-  double norm0 = 0.0;
-  for (int j = 0; j < kmax; ++j) {
-    double pv = -1.0;
-    int p = INT_MAX;
-    for (int c = j + tid; c < b; c += QR_NT) argmax_merge(pv, p, vn1[c], c);
-    block_argmax<QR_NT>(pv, p, red_v, red_i);
-    if (j == 0) norm0 = pv;
-    if (!(pv > eps * norm0) || pv == 0.0) {
-      kk = j;
-      break;
-    }
-    if (p != j) {
-      for (int i = tid; i < m; i += QR_NT) {
-        cplx a = M[i + (size_t)j * m];
-        M[i + (size_t)j * m] = M[i + (size_t)p * m];
-        M[i + (size_t)p * m] = a;
-      }
-      if (tid == 0) {
-        double x = vn1[j]; vn1[j] = vn1[p]; vn1[p] = x;
-        x = vn2[j]; vn2[j] = vn2[p]; vn2[p] = x;
-        int q = perm[j]; perm[j] = perm[p]; perm[p] = q;
-      }
-      __syncthreads();
-    }
-    // Householder reflector H = I − τ u uᴴ with H x = β e1, β = −(α/|α|)‖x‖
-    double xs = 0.0;
-    for (int i = j + 1 + tid; i < m; i += QR_NT) xs += cabs2(M[i + (size_t)j * m]);
-    const double xn2 = block_sum<QR_NT>(xs, red_v);
-    const cplx alpha = M[j + (size_t)j * m];
-    const double aa = sqrt(cabs2(alpha));
-    const double nrm = sqrt(aa * aa + xn2);
-    const cplx beta = aa > 0.0 ? cmk(-alpha.x / aa * nrm, -alpha.y / aa * nrm) : cmk(-nrm, 0.0);
-    const cplx u0 = csub(alpha, beta);
-    const double tau = 2.0 / (cabs2(u0) + xn2);
-    for (int c = j + 1 + warp; c < b; c += nw) {
-      cplx* Mc = M + (size_t)c * m;
-      const cplx* u = M + (size_t)j * m;
-      cplx d = lane == 0 ? cmulc(u0, Mc[j]) : cmk(0.0, 0.0);
-      for (int i = j + 1 + lane; i < m; i += 32) d = cadd(d, cmulc(u[i], Mc[i]));
-      d = warp_csum(d);
-      const cplx f = cscale(d, tau);
-      if (lane == 0) Mc[j] = cfms(f, u0, Mc[j]);
-      for (int i = j + 1 + lane; i < m; i += 32) Mc[i] = cfms(f, u[i], Mc[i]);
-      __syncwarp();
-      // LAPACK-style norm downdate with recomputation on cancellation (zlaqp2)
-      int recompute = 0;
-      if (lane == 0 && vn1[c] != 0.0) {
-        double r = sqrt(cabs2(Mc[j])) / vn1[c];
-        double temp = fmax(0.0, 1.0 - r * r);
-        double q = vn1[c] / vn2[c];
-        double temp2 = temp * q * q;
-        if (temp2 <= tol3z) recompute = 1;
-        else vn1[c] *= sqrt(temp);
-      }
-      recompute = __shfl_sync(0xffffffffu, recompute, 0);
-      if (recompute) {
-        double s = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) s += cabs2(Mc[i]);
-        s = warp_sum(s);
-        if (lane == 0) vn1[c] = vn2[c] = sqrt(s);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) M[j + (size_t)j * m] = beta;
-    __syncthreads();
-  }
-  for (int c = tid; c < b; c += QR_NT) perm_out[t.out_off + c] = perm[c];
-  if (tid == 0) k_out[blockIdx.x] = kk;
-}
 
 // T = R11⁻¹ R12, warp per column, back substitution.
 __global__ void k_trsm_T(const IdTask* __restrict__ tasks, const int* __restrict__ kv,
@@ -445,7 +161,7 @@ __global__ void k_trsm_T(const IdTask* __restrict__ tasks, const int* __restrict
   const IdTask t = tasks[blockIdx.x];
   const int kk = kv[blockIdx.x];
   const int r = t.b - kk, m = t.m;
-  const cplx* M = ws + t.M;
+  const cplx* M = t.Mp;
   cplx* T = tarena + t.T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = warp; c < r; c += nw) {
@@ -544,7 +260,9 @@ __global__ void __launch_bounds__(CK_NT) k_gj_cluster(const long long* __restric
   cplx* Al = reinterpret_cast<cplx*>(shm);   // n × ncl
   cplx* buf = Al + (size_t)n * ((n + CL - 1) / CL);  // [2][n] published pivot column (rows swapped)
   cplx* colsw = buf + 2 * n;                  // local copy of the pivot column
-  int* piv = reinterpret_cast<int*>(colsw + n);  // n
+  cplx* rowj = colsw + n;                     // ncl: row j of the local columns
+  cplx* rowp = rowj + (n + CL - 1) / CL;      // ncl: row p
+  int* piv = reinterpret_cast<int*>(rowp + (n + CL - 1) / CL);  // n
   const int tid = threadIdx.x;
   for (int e = tid; e < n * ncl; e += CK_NT) {
     const int i = e % n, l = e / n;
@@ -581,24 +299,27 @@ __global__ void __launch_bounds__(CK_NT) k_gj_cluster(const long long* __restric
     if (tid == 0) piv[j] = p;
     __syncthreads();
     const cplx dinv = cdiv(cmk(1.0, 0.0), colsw[j]);
-    for (int l = 0; l < ncl; ++l) {
+    // rows j and p of every local column (read before anyone writes)
+    for (int l = tid; l < ncl; l += CK_NT) {
+      rowj[l] = Al[j + (size_t)l * n];
+      rowp[l] = Al[p + (size_t)l * n];
+    }
+    __syncthreads();
+    for (int e = tid; e < n * ncl; e += CK_NT) {
+      const int i = e % n, l = e / n;
       const int g = rank + l * CL;
-      cplx* Ac = Al + (size_t)l * n;
-      cplx aj = Ac[j], ap = Ac[p];
-      __syncthreads();
+      cplx v;
       if (g == j) {
-        for (int i = tid; i < n; i += CK_NT)
-          Ac[i] = i == j ? dinv : cmk(-(colsw[i].x * dinv.x - colsw[i].y * dinv.y),
-                                      -(colsw[i].x * dinv.y + colsw[i].y * dinv.x));
+        v = i == j ? dinv : cmk(-(colsw[i].x * dinv.x - colsw[i].y * dinv.y),
+                                -(colsw[i].x * dinv.y + colsw[i].y * dinv.x));
       } else {
-        // swap rows j, p of this column, then eliminate
-        const cplx rj = cmul(p == j ? aj : ap, dinv);
-        for (int i = tid; i < n; i += CK_NT) {
-          cplx v = i == p ? aj : (i == j ? ap : Ac[i]);
-          if (p == j) v = Ac[i];
-          Ac[i] = i == j ? rj : cfms(colsw[i], rj, v);
-        }
+        // rows j and p swapped, row j scaled by 1/d, others eliminated
+        const cplx aj = rowj[l], ap = rowp[l];
+        const cplx rj = cmul(ap, dinv);  // (p == j ⇒ ap == aj)
+        const cplx old = i == p ? aj : (i == j ? ap : Al[e]);
+        v = i == j ? rj : cfms(colsw[i], rj, old);
       }
+      Al[e] = v;
     }
     __syncthreads();
   }
@@ -623,12 +344,18 @@ __global__ void __launch_bounds__(CK_NT) k_gj_cluster(const long long* __restric
   }
 }
 
-// Column-pivoted Householder QR of R0 (m × b, ld m) with the stopping rule of reading C9;
-// columns are never moved: the pivot order is recorded and R' (k × b, pivot columns first,
-// then the redundant columns in ascending index) is written back in place.  grid (CL, ntasks).
-__global__ void __launch_bounds__(CK_NT) k_cpqr_cluster(const IdTask* __restrict__ tasks, cplx* ws,
-                                                        int* __restrict__ perm_out, int* __restrict__ k_out,
-                                                        double eps) {
+// Householder QR on a matrix resident in cluster shared memory (columns cyclic over the CL
+// CTAs).  PIVOT = 1: column-pivoted QR with the stopping rule of reading C9 (largest residual
+// column norm ≤ ε · largest initial norm; ties → lowest column), norms downdated LAPACK-style
+// with recomputation on cancellation.  PIVOT = 0: plain QR (TSQR round), all min(m, b) steps.
+// The reflector H = I − τ u uᴴ of step j is published through the owner's own column
+// (u_i = x_i below row j; u_j, τ, β in a double-buffered meta record).
+// Output: PIVOT=1 writes R' = [R11 R12] (pivot columns first, then the redundant columns in
+// ascending index) over rows 0..k-1 of the input, perm and k;  PIVOT=0 writes triu(R)
+// (min(m,b) × b) to t.out (ld t.ldo).  grid (CL, ntasks).
+template <int PIVOT>
+__global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __restrict__ tasks, int* __restrict__ perm_out,
+                                                       int* __restrict__ k_out, double eps) {
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ double shm[];
@@ -636,63 +363,62 @@ __global__ void __launch_bounds__(CK_NT) k_cpqr_cluster(const IdTask* __restrict
   __shared__ int red_i[32];
   __shared__ double cand_v;
   __shared__ int cand_i;
-  __shared__ double hmeta[2][4];  // [parity] {tau, beta.re, beta.im, -}
-  const IdTask t = tasks[blockIdx.y];
-  cplx* M = ws + t.M;
+  __shared__ double hmeta[2][4];  // [parity] {u0.re, u0.im, tau, -}
+  const ClusterQrTask t = tasks[blockIdx.y];
   const int m = t.m, b = t.b;
   const int ncl = (b - rank + CL - 1) / CL;
   const int nclmax = (b + CL - 1) / CL;
-  cplx* Al = reinterpret_cast<cplx*>(shm);          // m × ncl
-  cplx* ub = Al + (size_t)m * nclmax;               // [2][m] published Householder vector
-  cplx* u = ub + 2 * m;                             // local copy
+  cplx* Al = reinterpret_cast<cplx*>(shm);          // m × ncl (ld m)
+  cplx* u = Al + (size_t)m * nclmax;                // m: local copy of the current reflector
   double* vn1 = reinterpret_cast<double*>(u + m);   // ncl
   double* vn2 = vn1 + nclmax;
-  int* piv = reinterpret_cast<int*>(vn2 + nclmax);  // b: pivot columns in order
-  int* done = piv + b;                              // b flags (global column pivoted?)
+  int* piv = reinterpret_cast<int*>(vn2 + nclmax);  // b: column chosen at each step
+  int* done = piv + b;                              // b flags
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CK_NT / 32;
   const double tol3z = sqrt(DBL_EPSILON);
   for (int e = tid; e < m * ncl; e += CK_NT) {
     const int i = e % m, l = e / m;
-    Al[e] = M[i + (size_t)(rank + l * CL) * m];
+    Al[e] = t.A[i + (size_t)(rank + l * CL) * t.lda];
   }
   for (int g = tid; g < b; g += CK_NT) done[g] = 0;
   __syncthreads();
-  for (int l = warp; l < ncl; l += nw) {
-    double s = 0.0;
-    for (int i = lane; i < m; i += 32) s += cabs2(Al[i + (size_t)l * m]);
-    s = warp_sum(s);
-    if (lane == 0) vn1[l] = vn2[l] = sqrt(s);
+  if (PIVOT) {
+    for (int l = warp; l < ncl; l += nw) {
+      double s = 0.0;
+      for (int i = lane; i < m; i += 32) s += cabs2(Al[i + (size_t)l * m]);
+      s = warp_sum(s);
+      if (lane == 0) vn1[l] = vn2[l] = sqrt(s);
+    }
   }
-  __syncthreads();
+  cl.sync();
   const int kmax = min(m, b);
   int kk = kmax;
   double norm0 = 0.0;
   for (int j = 0; j < kmax; ++j) {
     const int par = j & 1;
-    // local candidate, then cluster-wide argmax (ties → lowest global column)
-    double pv = -1.0;
-    int p = INT_MAX;
-    for (int l = tid; l < ncl; l += CK_NT) {
-      const int g = rank + l * CL;
-      if (!done[g]) argmax_merge(pv, p, vn1[l], g);
-    }
-    block_argmax<CK_NT>(pv, p, red_v, red_i);
-    if (tid == 0) {
-      cand_v = pv;
-      cand_i = p;
-    }
-    cl.sync();  // (A) candidates published
-    pv = -1.0;
-    p = INT_MAX;
-    for (int r = 0; r < CL; ++r) {
-      const double* rv = cl.map_shared_rank(&cand_v, r);
-      const int* ri = cl.map_shared_rank(&cand_i, r);
-      argmax_merge(pv, p, *rv, *ri);
-    }
-    if (j == 0) norm0 = pv;
-    if (!(pv > eps * norm0) || pv == 0.0) {
-      kk = j;
-      break;  // uniform
+    int p = j;
+    if (PIVOT) {
+      double pv = -1.0;
+      p = INT_MAX;
+      for (int l = tid; l < ncl; l += CK_NT) {
+        const int g = rank + l * CL;
+        if (!done[g]) argmax_merge(pv, p, vn1[l], g);
+      }
+      block_argmax<CK_NT>(pv, p, red_v, red_i);
+      if (tid == 0) {
+        cand_v = pv;
+        cand_i = p;
+      }
+      cl.sync();  // (A) candidates published
+      pv = -1.0;
+      p = INT_MAX;
+      for (int r = 0; r < CL; ++r)
+        argmax_merge(pv, p, *cl.map_shared_rank(&cand_v, r), *cl.map_shared_rank(&cand_i, r));
+      if (j == 0) norm0 = pv;
+      if (!(pv > eps * norm0) || pv == 0.0) {
+        kk = j;
+        break;  // uniform across the cluster
+      }
     }
     const int o = p % CL, lp = p / CL;
     if (rank == o) {
@@ -705,54 +431,60 @@ __global__ void __launch_bounds__(CK_NT) k_cpqr_cluster(const IdTask* __restrict
       const double nrm = sqrt(aa * aa + xn2);
       const cplx beta = aa > 0.0 ? cmk(-alpha.x / aa * nrm, -alpha.y / aa * nrm) : cmk(-nrm, 0.0);
       const cplx u0 = csub(alpha, beta);
-      for (int i = j + tid; i < m; i += CK_NT) ub[par * m + i] = i == j ? u0 : x[i];
+      const double den = cabs2(u0) + xn2;
+      __syncthreads();  // everyone has read α
       if (tid == 0) {
-        hmeta[par][0] = 2.0 / (cabs2(u0) + xn2);
-        hmeta[par][1] = beta.x;
-        hmeta[par][2] = beta.y;
+        hmeta[par][0] = u0.x;
+        hmeta[par][1] = u0.y;
+        hmeta[par][2] = den > 0.0 ? 2.0 / den : 0.0;
+        x[j] = beta;  // R_jj; rows below keep u (frozen: the column is done)
       }
-      __syncthreads();
-      for (int i = j + tid; i < m; i += CK_NT) x[i] = i == j ? beta : cmk(0.0, 0.0);
     }
     cl.sync();  // (B) reflector published
-    const cplx* ru = cl.map_shared_rank(ub + par * m, o);
-    const double tau = *cl.map_shared_rank(&hmeta[par][0], o);
-    for (int i = j + tid; i < m; i += CK_NT) u[i] = ru[i];
+    const double* rm = cl.map_shared_rank(&hmeta[par][0], o);
+    const cplx u0 = cmk(rm[0], rm[1]);
+    const double tau = rm[2];
+    const cplx* rx = cl.map_shared_rank(Al + (size_t)lp * m, o);
+    for (int i = j + tid; i < m; i += CK_NT) u[i] = i == j ? u0 : rx[i];
     if (tid == 0) {
       piv[j] = p;
       done[p] = 1;
     }
     __syncthreads();
-    for (int l = warp; l < ncl; l += nw) {
-      const int g = rank + l * CL;
-      if (done[g]) continue;
-      cplx* Mc = Al + (size_t)l * m;
-      cplx d = cmk(0.0, 0.0);
-      for (int i = j + lane; i < m; i += 32) d = cadd(d, cmulc(u[i], Mc[i]));
-      d = warp_csum(d);
-      const cplx f = cscale(d, tau);
-      for (int i = j + lane; i < m; i += 32) Mc[i] = cfms(f, u[i], Mc[i]);
-      __syncwarp();
-      int recompute = 0;
-      if (lane == 0 && vn1[l] != 0.0) {
-        const double r = sqrt(cabs2(Mc[j])) / vn1[l];
-        const double temp = fmax(0.0, 1.0 - r * r);
-        const double q = vn1[l] / vn2[l];
-        if (temp * q * q <= tol3z) recompute = 1;
-        else vn1[l] *= sqrt(temp);
-      }
-      recompute = __shfl_sync(0xffffffffu, recompute, 0);
-      if (recompute) {
-        double s = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) s += cabs2(Mc[i]);
-        s = warp_sum(s);
-        if (lane == 0) vn1[l] = vn2[l] = sqrt(s);
+    if (tau != 0.0) {
+      for (int l = warp; l < ncl; l += nw) {
+        const int g = rank + l * CL;
+        if (done[g]) continue;
+        cplx* Mc = Al + (size_t)l * m;
+        cplx d = cmk(0.0, 0.0);
+        for (int i = j + lane; i < m; i += 32) d = cadd(d, cmulc(u[i], Mc[i]));
+        d = warp_csum(d);
+        const cplx f = cscale(d, tau);
+        for (int i = j + lane; i < m; i += 32) Mc[i] = cfms(f, u[i], Mc[i]);
+        if (PIVOT) {
+          __syncwarp();
+          int recompute = 0;
+          if (lane == 0 && vn1[l] != 0.0) {
+            const double r = sqrt(cabs2(Mc[j])) / vn1[l];
+            const double temp = fmax(0.0, 1.0 - r * r);
+            const double q = vn1[l] / vn2[l];
+            if (temp * q * q <= tol3z) recompute = 1;
+            else vn1[l] *= sqrt(temp);
+          }
+          recompute = __shfl_sync(0xffffffffu, recompute, 0);
+          if (recompute) {
+            double s = 0.0;
+            for (int i = j + 1 + lane; i < m; i += 32) s += cabs2(Mc[i]);
+            s = warp_sum(s);
+            if (lane == 0) vn1[l] = vn2[l] = sqrt(s);
+          }
+        }
       }
     }
     __syncthreads();
   }
-  // output order: pivots, then the redundant columns in ascending index
-  int* posmap = done;  // reuse: position of global column g in the output
+  // output
+  int* posmap = done;  // position (output column) of global column g
   __syncthreads();
   if (tid == 0) {
     for (int g = 0; g < b; ++g) posmap[g] = -1;
@@ -762,14 +494,25 @@ __global__ void __launch_bounds__(CK_NT) k_cpqr_cluster(const IdTask* __restrict
       if (posmap[g] < 0) posmap[g] = c++;
   }
   __syncthreads();
-  cl.sync();  // all loads of M are long done; write R' in place (rows 0..k-1)
-  for (int l = 0; l < ncl; ++l) {
+  cl.sync();  // all CTAs have loaded their input columns; in-place output is safe
+  cplx* out = PIVOT ? t.A : t.out;
+  const int ldo = PIVOT ? t.lda : t.ldo;
+  const int rows = kk;
+  for (int e = tid; e < rows * ncl; e += CK_NT) {
+    const int i = e % rows, l = e / rows;
     const int g = rank + l * CL;
     const int c = posmap[g];
-    for (int i = tid; i < kk; i += CK_NT) M[i + (size_t)c * m] = Al[i + (size_t)l * m];
-    if (tid == 0) perm_out[t.out_off + c] = g;
+    // a column pivoted at step c holds R rows 0..c; below that it stores its reflector
+    const cplx v = (c < kk && i > c) ? cmk(0.0, 0.0) : Al[i + (size_t)l * m];
+    out[i + (size_t)c * ldo] = v;
   }
-  if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+  if (PIVOT) {
+    for (int l = tid; l < ncl; l += CK_NT) {
+      const int g = rank + l * CL;
+      perm_out[t.out_off + posmap[g]] = g;
+    }
+    if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+  }
 }
 
 // Cooperative Gauss-Jordan inverse (root block D_t⁻¹): columns are
@@ -1317,26 +1060,12 @@ void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* w
   FMMLU_LAUNCH();
 }
 
-void launch_qr_panel(const QrChunk* d_chunks, int nchunks, int j0, int nb, cudaStream_t st) {
-  if (nchunks <= 0) return;
-  static bool init = false;
-  if (!init) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_qr_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    init = true;
-  }
-  k_qr_panel<<<nchunks, QP_NT, 200 * 1024, st>>>(d_chunks, j0, nb);
-  FMMLU_LAUNCH();
-}
-
 namespace {
 constexpr size_t kClusterSmemCap = 220 * 1024;
 size_t gj_smem(int n, int CL) {
-  return (size_t)n * ((n + CL - 1) / CL) * sizeof(cplx) + 3 * (size_t)n * sizeof(cplx) + 2 * (size_t)n * sizeof(int) + 64;
-}
-size_t cpqr_smem(int m, int b, int CL) {
-  const int ncl = (b + CL - 1) / CL;
-  return (size_t)m * ncl * sizeof(cplx) + 3 * (size_t)m * sizeof(cplx) + 2 * (size_t)ncl * sizeof(double) +
-         2 * (size_t)b * sizeof(int) + 64;
+  const size_t ncl = (n + CL - 1) / CL;
+  return (size_t)n * ncl * sizeof(cplx) + 3 * (size_t)n * sizeof(cplx) + 2 * ncl * sizeof(cplx) +
+         2 * (size_t)n * sizeof(int) + 64;
 }
 template <class K>
 void cluster_attrs(K kern, size_t smem, int CL) {
@@ -1373,31 +1102,38 @@ bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx*
   return true;
 }
 
-bool launch_cpqr_cluster(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out, double eps,
-                         cudaStream_t st, int mmax, int bmax) {
-  if (ntasks <= 0) return true;
+size_t hqr_cluster_smem(int m, int b, int CL) {
+  const size_t ncl = (b + CL - 1) / CL;
+  return (size_t)m * (ncl + 1) * sizeof(cplx) + 2 * ncl * sizeof(double) + 2 * (size_t)b * sizeof(int) + 64;
+}
+
+int hqr_cluster_size(int m, int b) {
   int CL = 1;
-  while (CL <= 16 && cpqr_smem(mmax, bmax, CL) > kClusterSmemCap) CL *= 2;
-  if (CL > 16) return false;
-  const size_t smem = cpqr_smem(mmax, bmax, CL);
-  cluster_attrs(k_cpqr_cluster, smem, CL);
-  launch_cluster(k_cpqr_cluster, CL, ntasks, smem, st, d_tasks, ws, perm_out, k_out, eps);
-  return true;
+  while (CL <= 16 && hqr_cluster_smem(m, b, CL) > kClusterSmemCap) CL *= 2;
+  return CL <= 16 ? CL : 0;
 }
 
-void launch_cpqr(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out,
-                 double eps, cudaStream_t st, int bmax) {
+int hqr_max_rows(int b, int CL) {
+  const size_t ncl = (b + CL - 1) / CL;
+  const size_t fixed = 2 * ncl * sizeof(double) + 2 * (size_t)b * sizeof(int) + 64;
+  if (fixed >= kClusterSmemCap) return 0;
+  return (int)((kClusterSmemCap - fixed) / ((ncl + 1) * sizeof(cplx)));
+}
+
+void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
+                        cudaStream_t st, int mmax, int bmax) {
   if (ntasks <= 0) return;
-  size_t smem = (size_t)bmax * (2 * sizeof(double) + sizeof(int)) + 16;
-  static size_t cur = 0;
-  if (smem > 48 * 1024 && smem > cur) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_cpqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cur = smem;
+  const int CL = hqr_cluster_size(mmax, bmax);
+  if (CL == 0) throw Error(-6, "ID matrix too large for a 16-CTA cluster");
+  const size_t smem = hqr_cluster_smem(mmax, bmax, CL);
+  if (pivot) {
+    cluster_attrs(k_hqr_cluster<1>, smem, CL);
+    launch_cluster(k_hqr_cluster<1>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps);
+  } else {
+    cluster_attrs(k_hqr_cluster<0>, smem, CL);
+    launch_cluster(k_hqr_cluster<0>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps);
   }
-  k_cpqr<<<ntasks, QR_NT, smem, st>>>(d_tasks, ws, perm_out, k_out, eps);
-  FMMLU_LAUNCH();
 }
-
 
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st) {

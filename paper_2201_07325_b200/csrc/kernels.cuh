@@ -31,13 +31,6 @@ struct CopyTask {
   int tri;             // 1: zero the strictly-lower part of dst (upper-triangular R copies)
 };
 
-// One row-chunk of a box's ID matrix for the blocked Householder QR (TSQR leaves).
-// A: h × b (ld lda) in the workspace arena; V, Z: h × NB (ld h); W: NB × b (ld NB).
-struct QrChunk {
-  cplx *A, *V, *Z, *W;
-  int lda, h, b, pad;
-};
-
 // Proxy rows of M (§5.1.3; readings C3-C5): rows row0 .. row0+nγ-1 hold
 // s_γ K(y_ℓ, x_j) √w_j (outgoing, combined field with the box normals), rows row0+nγ ..
 // row0+2nγ-1 hold s_γ G(x_j, y_ℓ) √w_j (incoming single layer, transposed).
@@ -49,7 +42,7 @@ struct ProxyTask {
 
 // Per-box ID on M (m × b, ld = m): CPQR with stopping rule |R_jj| ≤ eps·|R_00| (reading C9).
 struct IdTask {
-  long long M;    // complex offset of M in the workspace
+  cplx* Mp;       // the (m × b, ld m) matrix holding R' = [R11 R12] in rows 0..k-1
   int m, b;
   int out_off;    // offset into perm output (b ints)
   long long T;    // complex offset of T (k × (b-k)) in the T arena (capacity b*b)
@@ -76,12 +69,6 @@ void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cpl
                  cplx* dst_arena, cudaStream_t st);
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
                   double k, cudaStream_t st);
-// Householder panel of every chunk: columns j0 .. j0+jb-1 factored in shared memory; writes R
-// rows back, the explicit reflectors V (unit diagonal) and Z = V Tᴴ of the compact WY form
-// H_1⋯H_jb = I − V T Vᴴ, and zeroes W.  One CTA per chunk.
-void launch_qr_panel(const QrChunk* d_chunks, int nchunks, int j0, int nb, cudaStream_t st);
-void launch_cpqr(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out,
-                 double eps, cudaStream_t st, int bmax);
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st);
 // in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
@@ -91,10 +78,21 @@ void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx*
 // when the matrix is too large for a 16-CTA cluster (caller falls back to the kernels above).
 bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,
                        cudaStream_t st, int nmax);
-// CPQR of R0 with the columns left in place: writes R' = [R11 R12] (pivot columns first, then
-// the redundant ones in ascending index) over rows 0..k-1 and perm = that column order.
-bool launch_cpqr_cluster(const IdTask* d_tasks, int ntasks, cplx* ws, int* perm_out, int* k_out, double eps,
-                         cudaStream_t st, int mmax, int bmax);
+// Householder QR (pivot = 0: TSQR round, writes triu(R) to out) or CPQR with the reading-C9
+// stopping rule (pivot = 1: writes R' = [R11 R12], pivot columns first then the redundant ones
+// in ascending index, over rows 0..k-1 of A, plus perm and k) on matrices resident in the
+// distributed shared memory of a thread-block cluster of ≤ 16 CTAs.
+struct ClusterQrTask {
+  cplx* A;
+  cplx* out;
+  int lda, m, b, ldo;
+  int out_off;  // perm output offset (pivot = 1)
+  int pad;
+};
+int hqr_cluster_size(int m, int b);  // CTAs needed to hold m × b (0 = too large)
+int hqr_max_rows(int b, int CL);     // largest m that fits a CL-CTA cluster with b columns
+void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
+                        cudaStream_t st, int mmax, int bmax);
 // cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
 void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
 // solve sweeps for one (level, colour) phase
