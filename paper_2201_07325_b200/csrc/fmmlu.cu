@@ -309,8 +309,14 @@ void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mro
     Stage s;
     size_t o_t = s.add(tasks);
     s.upload(st);
+    std::vector<int> tm, tb;
+    for (auto& t : tasks) {
+      tm.push_back(t.m);
+      tb.push_back(t.b);
+    }
     int id = P.begin(FMMLU_K_QR, st);
-    launch_hqr_cluster(s.ptr<ClusterQrTask>(o_t), (int)tasks.size(), 0, nullptr, nullptr, 0.0, st, hmax, bmax);
+    launch_hqr_cluster(s.ptr<ClusterQrTask>(o_t), (int)tasks.size(), 0, nullptr, nullptr, 0.0, st, tm.data(),
+                       tb.data());
     P.end(id, st);
     P.add(FMMLU_K_QR, fl, by, 1);
     for (int j : todo) {
@@ -668,7 +674,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         size_t o_i = s2.add(ids), o_q = s2.add(cq);
         s2.upload(st);
         int cid = h->prof.begin(FMMLU_K_CPQR, st);
-        launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st, mmax0, bmax);
+        launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st, mrows.data(),
+                           bcol.data());
         launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
         h->prof.end(cid, st);
         h->prof.add(FMMLU_K_CPQR, 0, 0, 2);

@@ -1121,11 +1121,17 @@ int hqr_max_rows(int b, int CL) {
 }
 
 void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
-                        cudaStream_t st, int mmax, int bmax) {
+                        cudaStream_t st, const int* m_of, const int* b_of) {
   if (ntasks <= 0) return;
-  const int CL = hqr_cluster_size(mmax, bmax);
-  if (CL == 0) throw Error(-6, "ID matrix too large for a 16-CTA cluster");
-  const size_t smem = hqr_cluster_smem(mmax, bmax, CL);
+  // smallest cluster in which every task's (m, b) fits; smem = the largest task's need
+  int CL = 1;
+  size_t smem = 0;
+  for (; CL <= 16; CL *= 2) {
+    smem = 0;
+    for (int i = 0; i < ntasks; ++i) smem = std::max(smem, hqr_cluster_smem(m_of[i], b_of[i], CL));
+    if (smem <= kClusterSmemCap) break;
+  }
+  if (CL > 16) throw Error(-6, "ID matrix too large for a 16-CTA cluster");
   if (pivot) {
     cluster_attrs(k_hqr_cluster<1>, smem, CL);
     launch_cluster(k_hqr_cluster<1>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps);

@@ -91,8 +91,9 @@ struct ClusterQrTask {
 };
 int hqr_cluster_size(int m, int b);  // CTAs needed to hold m × b (0 = too large)
 int hqr_max_rows(int b, int CL);     // largest m that fits a CL-CTA cluster with b columns
+// m_of / b_of: host arrays with each task's (m, b) (they size the cluster and its shared memory)
 void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
-                        cudaStream_t st, int mmax, int bmax);
+                        cudaStream_t st, const int* m_of, const int* b_of);
 // cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
 void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
 // solve sweeps for one (level, colour) phase
