@@ -140,6 +140,15 @@ int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out);
  * own stream).  The caller keeps ownership of the stream. */
 int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
 
+/* Tuning parameters (apply to the next fmmlu_factor):
+ *   "id_mode"   0 = auto (Gram path for eps >= 1e-7, Householder below; default),
+ *               1 = Householder TSQR + column-pivoted QR on the ID matrix,
+ *               2 = Gram matrix + pivoted Cholesky (same pivots/rank/T as CPQR in exact
+ *                   arithmetic; accurate while eps^2 >> unit roundoff)
+ *   "proxy_rho" proxy-sphere radius / box side, in (sqrt(3)/2, 5/2) (reading C5; default 2.0)
+ * Errors: EINVAL (unknown name or value out of range). */
+int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);
+
 /* Tree order: perm[i] = caller index of the i-th point in tree (Morton) order.
  * perm: int64[n] host buffer. */
 int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm);

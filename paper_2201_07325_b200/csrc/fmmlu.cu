@@ -198,6 +198,8 @@ struct fmmlu_handle {
   fmmlu_stats_t stats{};
   size_t cur_bytes = 0, peak_bytes = 0;
   Prof prof;
+  int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
+  double rho_factor = 2.0;   // proxy radius / box side (reading C5)
 };
 
 namespace {
@@ -498,7 +500,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     long long total_active = 0;
     for (int a = 0; a < no; ++a) total_active += (long long)cur.act[a].size();
     const double side = T.box_side(lvl);
-    const double rho = 2.0 * side;
+    const double rho = h->rho_factor * side;
     const int ngamma = proxy_count(k, rho, eps);
     const double sg = std::sqrt(4.0 * M_PI * rho * rho / ngamma);
 
@@ -660,26 +662,82 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           mrows[j] = jobs[j].m;
           bcol[j] = jobs[j].b;
         }
-        tsqr_cluster(h, mp, mrows, bcol, keep);
+        // ID mode: at ε ≥ 1e-7 the pivoted Cholesky of G = MᴴM gives the
+        // CPQR pivots/rank/T to ~u·cond accuracy (ε² ≫ u); tighter ε uses Householder TSQR.
+        const bool gram = h->id_mode == 2 || (h->id_mode == 0 && eps >= 1e-7);
         std::vector<ClusterQrTask> cq(nj);
-        int mmax0 = 1;
-        for (int j = 0; j < nj; ++j) {
-          ids[j].Mp = mp[j];
-          ids[j].m = mrows[j];
-          cq[j] = ClusterQrTask{mp[j], nullptr, mrows[j], mrows[j], bcol[j], 0, jobs[j].permoff, 0};
-          jobs[j].mfin = mrows[j];
-          mmax0 = std::max(mmax0, mrows[j]);
+        DBuf G;
+        bool done_id = false;
+        if (gram) {
+          long long gsz = 0;
+          std::vector<long long> goff(nj);
+          for (int j = 0; j < nj; ++j) {
+            goff[j] = gsz;
+            gsz += (long long)bcol[j] * bcol[j];
+          }
+          G.alloc((size_t)gsz * sizeof(cplx), st);
+          FMMLU_CUDA(cudaMemsetAsync(G.p, 0, G.bytes, st));
+          std::vector<GemmProblem> gp;
+          std::vector<GemmTile> gt;
+          for (int j = 0; j < nj; ++j) {
+            GemmProblem P{};
+            P.m = bcol[j];
+            P.n = bcol[j];
+            P.k = mrows[j];
+            P.opA = kOpC;
+            P.opB = kOpN;
+            P.A = mp[j];
+            P.lda = mrows[j];
+            P.B = mp[j];
+            P.ldb = mrows[j];
+            P.C = G.as<cplx>() + goff[j];
+            P.ldc = bcol[j];
+            P.kchunk = mrows[j] > 512 ? 256 : 0;
+            add_gemm(gp, gt, P);
+          }
+          run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR);
+          for (int j = 0; j < nj; ++j) {
+            cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], nullptr, bcol[j], bcol[j], bcol[j], 0, jobs[j].permoff, 0};
+            ids[j].Mp = G.as<cplx>() + goff[j];
+            ids[j].m = bcol[j];
+            jobs[j].mfin = bcol[j];
+          }
+          Stage s2;
+          size_t o_i = s2.add(ids), o_q = s2.add(cq);
+          s2.upload(st);
+          int cid = h->prof.begin(FMMLU_K_CPQR, st);
+          done_id = launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd.as<int>(), kd.as<int>(), eps, st, bmax);
+          if (done_id) launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
+          h->prof.end(cid, st);
+          h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
+          keep.push_back(std::move(s2.dev));
+          if (!done_id) {  // b too large for a cluster: fall back to the Householder path
+            for (int j = 0; j < nj; ++j) {
+              mp[j] = M.as<cplx>() + jobs[j].Moff;
+              mrows[j] = jobs[j].m;
+            }
+          }
         }
-        Stage s2;
-        size_t o_i = s2.add(ids), o_q = s2.add(cq);
-        s2.upload(st);
-        int cid = h->prof.begin(FMMLU_K_CPQR, st);
-        launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st, mrows.data(),
-                           bcol.data());
-        launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
-        h->prof.end(cid, st);
-        h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
-        keep.push_back(std::move(s2.dev));
+        if (!done_id) {
+          tsqr_cluster(h, mp, mrows, bcol, keep);
+          for (int j = 0; j < nj; ++j) {
+            ids[j].Mp = mp[j];
+            ids[j].m = mrows[j];
+            cq[j] = ClusterQrTask{mp[j], nullptr, mrows[j], mrows[j], bcol[j], 0, jobs[j].permoff, 0};
+            jobs[j].mfin = mrows[j];
+          }
+          Stage s2;
+          size_t o_i = s2.add(ids), o_q = s2.add(cq);
+          s2.upload(st);
+          int cid = h->prof.begin(FMMLU_K_CPQR, st);
+          launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st,
+                             mrows.data(), bcol.data());
+          launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
+          h->prof.end(cid, st);
+          h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
+          keep.push_back(std::move(s2.dev));
+        }
+        keep.push_back(std::move(G));
       }
       std::vector<int> hk(nj), hperm(permtot);
       FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1412,6 +1470,21 @@ int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out) {
 int fmmlu_set_stream(fmmlu_handle* h, void* s) {
   if (!h) return fail(FMMLU_EINVAL, "NULL handle");
   h->stream = s ? reinterpret_cast<cudaStream_t>(s) : h->own_stream;
+  return FMMLU_OK;
+}
+
+int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
+  if (!h || !name) return fail(FMMLU_EINVAL, "NULL argument");
+  std::string k(name);
+  if (k == "id_mode") {
+    if (value != 0 && value != 1 && value != 2) return fail(FMMLU_EINVAL, "id_mode must be 0, 1 or 2");
+    h->id_mode = (int)value;
+  } else if (k == "proxy_rho") {
+    if (!(value > 0.87 && value < 2.5)) return fail(FMMLU_EINVAL, "proxy_rho must lie in (0.87, 2.5)");
+    h->rho_factor = value;
+  } else {
+    return fail(FMMLU_EINVAL, "unknown parameter " + k);
+  }
   return FMMLU_OK;
 }
 

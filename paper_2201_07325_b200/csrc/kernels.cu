@@ -515,6 +515,109 @@ __global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __re
   }
 }
 
+// Pivoted Cholesky of the Gram matrix G = MᴴM (b × b, Hermitian, ld b) in cluster shared memory:
+// the Gram-side form of the same greedy column pivoting (diagonal of the Schur complement =
+// squared residual column norms; pivot = largest, ties → lowest column; stop when it is
+// ≤ (ε·max initial column norm)², reading C9).  Writes R' = [R11 R12] (k × b, ld b; pivot
+// columns first, then the redundant ones in ascending index) over G, plus perm and k.
+// grid (CL, ntasks); task.A = G, task.lda = b, task.m = b.
+__global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __restrict__ tasks,
+                                                         int* __restrict__ perm_out, int* __restrict__ k_out,
+                                                         double eps) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ double cand_v;
+  __shared__ int cand_i;
+  const ClusterQrTask t = tasks[blockIdx.y];
+  const int b = t.b;
+  const int ncl = (b - rank + CL - 1) / CL;
+  const int nclmax = (b + CL - 1) / CL;
+  cplx* Sl = reinterpret_cast<cplx*>(shm);          // b × ncl: local columns of the Schur complement
+  cplx* Rl = Sl + (size_t)b * nclmax;               // b × ncl: rows of R for the local columns (row = step)
+  cplx* pc = Rl + (size_t)b * nclmax;               // b: copy of the pivot column
+  cplx* rowp = pc + b;                              // ncl: row p of the local columns
+  int* piv = reinterpret_cast<int*>(rowp + nclmax); // b
+  int* done = piv + b;                              // b
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * ncl; e += CK_NT) {
+    const int i = e % b, l = e / b;
+    Sl[e] = t.A[i + (size_t)(rank + l * CL) * t.lda];
+    Rl[e] = cmk(0.0, 0.0);
+  }
+  for (int g = tid; g < b; g += CK_NT) done[g] = 0;
+  cl.sync();
+  int kk = b;
+  double d0 = 0.0;
+  for (int j = 0; j < b; ++j) {
+    double pv = -1.0;
+    int p = INT_MAX;
+    for (int l = tid; l < ncl; l += CK_NT) {
+      const int g = rank + l * CL;
+      if (!done[g]) argmax_merge(pv, p, Sl[g + (size_t)l * b].x, g);
+    }
+    block_argmax<CK_NT>(pv, p, red_v, red_i);
+    if (tid == 0) {
+      cand_v = pv;
+      cand_i = p;
+    }
+    cl.sync();  // (A)
+    pv = -1.0;
+    p = INT_MAX;
+    for (int r = 0; r < CL; ++r)
+      argmax_merge(pv, p, *cl.map_shared_rank(&cand_v, r), *cl.map_shared_rank(&cand_i, r));
+    if (j == 0) d0 = pv;
+    if (!(pv > eps * eps * d0) || !(pv > 0.0)) {
+      kk = j;
+      break;  // uniform
+    }
+    const int o = p % CL, lp = p / CL;
+    const cplx* rcol = cl.map_shared_rank(Sl + (size_t)lp * b, o);
+    for (int i = tid; i < b; i += CK_NT) pc[i] = rcol[i];
+    if (tid == 0) {
+      piv[j] = p;
+      done[p] = 1;
+    }
+    for (int l = tid; l < ncl; l += CK_NT) rowp[l] = Sl[p + (size_t)l * b];
+    cl.sync();  // (B) column p and row p copied everywhere; candidates of step j consumed
+    const double sd = sqrt(pv), inv = 1.0 / pv;
+    // R_{j,c} = S_{p,c}/√S_pp ;  S_{a,c} −= S_{a,p} S_{p,c} / S_pp  (remaining columns c)
+    for (int e = tid; e < b * ncl; e += CK_NT) {
+      const int a = e % b, l = e / b;
+      const int g = rank + l * CL;
+      if (g == p) {
+        if (a == j) Rl[j + (size_t)l * b] = cmk(sd, 0.0);
+        continue;
+      }
+      if (done[g]) continue;
+      const cplx spc = rowp[l];
+      if (a == j) Rl[j + (size_t)l * b] = cscale(spc, 1.0 / sd);
+      Sl[e] = cfms(cscale(pc[a], inv), spc, Sl[e]);
+    }
+    __syncthreads();
+  }
+  int* posmap = done;
+  __syncthreads();
+  if (tid == 0) {
+    for (int g = 0; g < b; ++g) posmap[g] = -1;
+    for (int q = 0; q < kk; ++q) posmap[piv[q]] = q;
+    int c = kk;
+    for (int g = 0; g < b; ++g)
+      if (posmap[g] < 0) posmap[g] = c++;
+  }
+  __syncthreads();
+  cl.sync();  // all CTAs loaded G; write R' over it
+  for (int e = tid; e < kk * ncl; e += CK_NT) {
+    const int i = e % kk, l = e / kk;
+    const int g = rank + l * CL;
+    t.A[i + (size_t)posmap[g] * t.lda] = Rl[i + (size_t)l * b];
+  }
+  for (int l = tid; l < ncl; l += CK_NT) perm_out[t.out_off + posmap[rank + l * CL]] = rank + l * CL;
+  if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+}
+
 // Cooperative Gauss-Jordan inverse (root block D_t⁻¹): columns are
 // owned round-robin by the CTAs; one grid barrier per elimination step.  Output to B
 // (column permutation undone out-of-place).
@@ -1118,6 +1221,24 @@ int hqr_max_rows(int b, int CL) {
   const size_t fixed = 2 * ncl * sizeof(double) + 2 * (size_t)b * sizeof(int) + 64;
   if (fixed >= kClusterSmemCap) return 0;
   return (int)((kClusterSmemCap - fixed) / ((ncl + 1) * sizeof(cplx)));
+}
+
+size_t pchol_smem(int b, int CL) {
+  const size_t ncl = (b + CL - 1) / CL;
+  return 2 * (size_t)b * ncl * sizeof(cplx) + (size_t)b * sizeof(cplx) + ncl * sizeof(cplx) +
+         2 * (size_t)b * sizeof(int) + 64;
+}
+
+bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
+                          cudaStream_t st, int bmax) {
+  if (ntasks <= 0) return true;
+  int CL = 1;
+  while (CL <= 16 && pchol_smem(bmax, CL) > kClusterSmemCap) CL *= 2;
+  if (CL > 16) return false;
+  const size_t smem = pchol_smem(bmax, CL);
+  cluster_attrs(k_pchol_cluster, smem, CL);
+  launch_cluster(k_pchol_cluster, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps);
+  return true;
 }
 
 void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,

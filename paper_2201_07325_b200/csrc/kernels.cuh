@@ -94,6 +94,10 @@ int hqr_max_rows(int b, int CL);     // largest m that fits a CL-CTA cluster wit
 // m_of / b_of: host arrays with each task's (m, b) (they size the cluster and its shared memory)
 void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
                         cudaStream_t st, const int* m_of, const int* b_of);
+// Pivoted Cholesky of G = MᴴM (b × b) in a cluster, same outputs as the pivoted launch above
+// (R' over G with ld b).  false if b is too large for a 16-CTA cluster.
+bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
+                          cudaStream_t st, int bmax);
 // cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
 void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
 // solve sweeps for one (level, colour) phase

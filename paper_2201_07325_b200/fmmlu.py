@@ -50,7 +50,8 @@ class Stats(ctypes.Structure):
 KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve"]
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_matvec", "fmmlu_destroy",
-           "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64")
+           "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
+           "fmmlu_set_param")
 
 
 def lib_path() -> str:
@@ -80,6 +81,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_set_stream.argtypes = [vp, vp]
     L.fmmlu_tree_perm.argtypes = [vp, vp]
     L.fmmlu_probe_fp64.argtypes = [ci, ctypes.POINTER(cd)]
+    L.fmmlu_set_param.argtypes = [vp, ctypes.c_char_p, cd]
     for f in EXPORTS:
         getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
     _LIB = L
@@ -151,6 +153,10 @@ class FmmLu:
         p = np.empty(self.n, dtype=np.int64)
         _check(load().fmmlu_tree_perm(self.h, p.ctypes.data))
         return p
+
+    def set_param(self, name: str, value: float):
+        _check(load().fmmlu_set_param(self.h, name.encode(), float(value)))
+        return self
 
     def set_stream(self, stream_ptr: int | None):
         _check(load().fmmlu_set_stream(self.h, stream_ptr or None))

@@ -145,3 +145,23 @@ def test_cfg2_full_size_residual(F):
         Ki[i] = 0.0
         yi = (Ki * g.weights) @ x + 0.5 * x[i]
         assert np.max(np.abs(yi - Ax[i])) <= 1e-11 * np.max(np.abs(yi)) + 1e-13
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_id_modes_parity(F, mode):
+    """Both ID paths (1: Householder TSQR + CPQR, 2: Gram + pivoted Cholesky) match the oracle."""
+    g = fi.ellipsoid(3000)
+    k, eps = 2 * math.pi, 1e-6
+    b = fi.gaussian_rhs(g.n, 2, 4)
+    h = F.FmmLu(g.points, g.normals, g.weights, 32).set_param("id_mode", mode).factor(k, eps)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, 32)
+    xo = rss.solve(f, b)
+    assert dense.rel_diff(x, xo) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
+    st = h.stats()
+    # ranks per level within a few percent of the oracle's (pivot near-ties may differ)
+    for lvl, s in f.stats["levels"].items():
+        ro = int(s["ranks"].sum())
+        assert abs(st["ranks_sum"][lvl] - ro) <= 0.03 * ro + 2
