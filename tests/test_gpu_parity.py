@@ -104,7 +104,13 @@ def test_device_pointers_equal_host(F):
     N = torch.from_numpy(g.normals).cuda()
     W = torch.from_numpy(g.weights).cuda()
     h2 = F.FmmLu(P, N, W, 32).factor(k, 1e-6)
-    assert h2.stats()["n0"] == h.stats()["n0"]
+    assert np.array_equal(h2.tree_perm(), h.tree_perm())
+    # fp64 atomics (Schur scatter, split-K Gram) make pivot near-ties run-dependent: the root
+    # size may move by a few DOFs, the solution only at the ε level
+    assert abs(h2.stats()["n0"] - h.stats()["n0"]) <= 0.01 * h.stats()["n0"] + 2
+    x2 = np.asfortranarray(b.copy())
+    h2.solve(x2)
+    assert dense.rel_diff(x2, x) <= 10 * 1e-6
 
 
 def test_edge_errors(F):
