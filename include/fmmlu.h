@@ -81,6 +81,7 @@ typedef struct fmmlu_stats_t {
   double class_flops[16];
   double class_bytes[16];
   int64_t class_launches[16];
+  double t_sync_wait_ms;  /* part of t_factor_ms the host spent blocked on the stream */
 } fmmlu_stats_t;
 
 /* kernel classes for fmmlu_stats_t.class_* */

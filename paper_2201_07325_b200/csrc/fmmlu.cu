@@ -204,6 +204,13 @@ struct fmmlu_handle {
 
 namespace {
 
+// cudaStreamSynchronize with the blocked time accounted (stats: host vs device-wait split)
+void wait_stream(fmmlu_handle* h, cudaStream_t st) {
+  double t0 = now_ms();
+  FMMLU_CUDA(cudaStreamSynchronize(st));
+  h->stats.t_sync_wait_ms += now_ms() - t0;
+}
+
 void track(fmmlu_handle* h, long long delta) {
   h->cur_bytes += delta;
   h->peak_bytes = std::max(h->peak_bytes, h->cur_bytes);
@@ -742,7 +749,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       std::vector<int> hk(nj), hperm(permtot);
       FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
       FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
-      FMMLU_CUDA(cudaStreamSynchronize(st));
+      wait_stream(h, st);
       h->prof.resolve();
       keep.clear();
       track(h, -(long long)M.bytes);
@@ -1108,7 +1115,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             FMMLU_CUDA(cudaMemcpyAsync(ph.items.p, items.data(), items.size() * sizeof(SolveItem),
                                        cudaMemcpyHostToDevice, st));
         }
-        FMMLU_CUDA(cudaStreamSynchronize(st));
+        wait_stream(h, st);
         h->prof.resolve();
         keep.clear();
         keep.push_back(std::move(s.dev));
@@ -1143,7 +1150,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         prevPos[cur.act[a][i]] = (int)i;
       }
     prev = std::move(cur);
-    FMMLU_CUDA(cudaStreamSynchronize(st));
+    wait_stream(h, st);
     h->prof.resolve();
     S.t_levels_ms[lvl] = now_ms() - tl0;
   }
@@ -1214,13 +1221,13 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     h->prof.add(FMMLU_K_ROOT, 8.0 * (double)n0 * n0 * n0, 32.0 * (double)n0 * n0, 3);
     h->root_rows.alloc((size_t)n0 * sizeof(int), st);
     FMMLU_CUDA(cudaMemcpyAsync(h->root_rows.p, Bt.data(), n0 * sizeof(int), cudaMemcpyHostToDevice, st));
-    FMMLU_CUDA(cudaStreamSynchronize(st));
+    wait_stream(h, st);
   }
   if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
   prev.bsr.release();
   int hstatus = 0;
   FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FMMLU_CUDA(cudaStreamSynchronize(st));
+  wait_stream(h, st);
   h->prof.resolve();
   S.t_root_ms = now_ms() - tr0;
   if (hstatus) throw Error(FMMLU_ESINGULAR, "exactly singular pivot block (X_RR or root)");
@@ -1387,6 +1394,7 @@ int fmmlu_factor(fmmlu_handle* h, double k, double eps) {
     FMMLU_CUDA(cudaSetDevice(h->dev));
     double t0 = now_ms();
     h->prof.reset();
+    h->stats.t_sync_wait_ms = 0;
     factor_impl(h, k, eps);
     h->stats.t_factor_ms = now_ms() - t0;
     h->stats.peak_bytes = (int64_t)h->peak_bytes;

@@ -37,6 +37,7 @@ class Stats(ctypes.Structure):
         ("n_singular_warn", ctypes.c_int32), ("ranks_sum", ctypes.c_int32 * 24), ("boxes", ctypes.c_int32 * 24),
         ("n_launches", ctypes.c_int64), ("class_ms", ctypes.c_double * 16), ("class_flops", ctypes.c_double * 16),
         ("class_bytes", ctypes.c_double * 16), ("class_launches", ctypes.c_int64 * 16),
+        ("t_sync_wait_ms", ctypes.c_double),
     ]
 
     def as_dict(self):
