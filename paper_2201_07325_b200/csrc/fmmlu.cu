@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -384,7 +386,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   LevelBSR prev;
   std::vector<DBuf> keep;  // per-phase temporaries kept alive until the phase syncs
 
+  // host-time trace (FMMLU_TRACE=1): sections exclusive of stream waits
+  static const bool trace = getenv("FMMLU_TRACE") != nullptr;
+  double tr[8] = {0};
+  double tmark = now_ms(), wmark = S.t_sync_wait_ms;
+  auto lap = [&](int sec) {
+    double t = now_ms(), w = S.t_sync_wait_ms;
+    tr[sec] += (t - tmark) - (w - wmark);
+    tmark = t;
+    wmark = w;
+  };
   for (int lvl = L - 1; lvl >= 2; --lvl) {
+    lap(7);
     double tl0 = now_ms();
     LevelBSR cur;
     cur.level = lvl;
@@ -423,6 +436,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     cur.bsr.alloc((size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
     track(h, cur.bsr.bytes);
 
+    lap(0);
     // ---- build the level's BSR (kernel entries, or carried-over Schur-updated values)
     {
       std::vector<int> gidx, slot, pos, bld, rowoff(no);
@@ -511,7 +525,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     const int ngamma = proxy_count(k, rho, eps);
     const double sg = std::sqrt(4.0 * M_PI * rho * rho / ngamma);
 
+    lap(1);
     for (int colour = 0; colour < 8; ++colour) {
+      lap(7);
       // ------------------------------------------------ boxes of this phase
       struct BoxJob {
         int a;  // local owner index of B
@@ -555,6 +571,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       if (jobs.empty()) continue;
       const int nj = (int)jobs.size();
 
+      lap(2);
       // ------------------------------------------------ ID stage
       long long wsM = 0, wsT = 0;
       int permtot = 0, bmax = 0;
@@ -755,6 +772,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       track(h, -(long long)M.bytes);
       M.release();
 
+      lap(3);
       // ------------------------------------------------ elimination stage
       std::vector<int> el;  // jobs with r > 0
       for (int j = 0; j < nj; ++j) {
@@ -1123,6 +1141,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         W.release();
         h->phases.push_back(std::move(ph));
       }
+      lap(4);
       // update current actives: B keeps its skeleton S (sorted)
       for (int j = 0; j < nj; ++j) {
         BoxJob& J = jobs[j];
@@ -1137,6 +1156,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       Tb.release();
       keep.clear();
     }
+    lap(5);
     // carry state to the next (coarser) level
     for (int a = 0; a < no; ++a) {
       std::vector<int> na;
@@ -1155,6 +1175,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     S.t_levels_ms[lvl] = now_ms() - tl0;
   }
 
+  lap(6);
+  if (trace)
+    fprintf(stderr, "[fmmlu] host ms: level-setup %.1f build-tasks %.1f phase-jobs %.1f id %.1f elim %.1f "
+                    "update %.1f carry %.1f other %.1f | wait %.1f\n",
+            tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root
   double tr0 = now_ms();
   std::vector<int> Bt;
