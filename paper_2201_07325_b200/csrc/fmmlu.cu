@@ -93,6 +93,44 @@ struct DBuf {
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// Pinned host staging for H2D uploads: cudaMemcpyAsync from pageable memory synchronises the
+// stream first, pinned memory keeps uploads asynchronous.  Reset only after a stream sync.
+struct PinnedArena {
+  std::vector<std::pair<char*, size_t>> chunks;
+  size_t used = 0;
+  char* get(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (chunks.empty() || used + bytes > chunks.back().second) {
+      size_t cap = std::max<size_t>(bytes, chunks.empty() ? (64u << 20) : 2 * chunks.back().second);
+      void* p = nullptr;
+      FMMLU_CUDA(cudaMallocHost(&p, cap));
+      chunks.push_back({(char*)p, cap});
+      used = 0;
+    }
+    char* r = chunks.back().first + used;
+    used += bytes;
+    return r;
+  }
+  void reset() {  // keep the largest (last) chunk
+    while (chunks.size() > 1) {
+      cudaFreeHost(chunks.front().first);
+      chunks.erase(chunks.begin());
+    }
+    used = 0;
+  }
+  ~PinnedArena() {
+    for (auto& c : chunks) cudaFreeHost(c.first);
+  }
+};
+thread_local PinnedArena tl_pin;
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  char* hp = tl_pin.get(bytes);
+  std::memcpy(hp, src, bytes);
+  FMMLU_CUDA(cudaMemcpyAsync(dst, hp, bytes, cudaMemcpyHostToDevice, st));
+}
+
 // Collects host arrays and uploads them in one H2D copy.
 struct Stage {
   std::vector<char> host;
@@ -105,8 +143,7 @@ struct Stage {
   }
   void upload(cudaStream_t s) {
     dev.alloc(host.size() + 16, s);
-    if (!host.empty())
-      FMMLU_CUDA(cudaMemcpyAsync(dev.p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+    h2d(dev.p, host.data(), host.size(), s);
   }
   template <class T> T* ptr(size_t off) const { return reinterpret_cast<T*>(dev.as<char>() + off); }
 };
@@ -181,6 +218,16 @@ struct Prof {
 
 }  // namespace
 
+// Per-level owner topology (tree-only; cached per handle): owners = level-ℓ boxes (Morton order)
+// then the leaves of coarser levels (reading C7); nb[a] = owners at Chebyshev separation ≤ 2
+// of owner a, including a, sorted; sep[a][i] = that separation (≤ 1: near field N, 2: Q; C6).
+struct LevelTopo {
+  std::vector<int> owners;
+  std::vector<int> local;
+  std::vector<std::vector<int>> nb;
+  std::vector<std::vector<signed char>> sep;
+};
+
 struct fmmlu_handle {
   int dev = 0;
   cudaStream_t stream = nullptr;
@@ -200,6 +247,8 @@ struct fmmlu_handle {
   fmmlu_stats_t stats{};
   size_t cur_bytes = 0, peak_bytes = 0;
   Prof prof;
+  std::vector<LevelTopo> topo;    // per-level owner topology (tree-only, cached)
+  std::vector<char> topo_ready;
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
 };
@@ -211,6 +260,7 @@ void wait_stream(fmmlu_handle* h, cudaStream_t st) {
   double t0 = now_ms();
   FMMLU_CUDA(cudaStreamSynchronize(st));
   h->stats.t_sync_wait_ms += now_ms() - t0;
+  tl_pin.reset();
 }
 
 void track(fmmlu_handle* h, long long delta) {
@@ -340,18 +390,72 @@ void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mro
 }
 
 // ---------------------------------------------------------------------------- factorization
+void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
+  tp.owners.clear();
+  for (int b : T.levels[lvl]) tp.owners.push_back(b);
+  for (int m = 0; m < lvl; ++m)
+    for (int b : T.levels[m])
+      if (T.boxes[b].leaf()) tp.owners.push_back(b);
+  const int no = (int)tp.owners.size();
+  tp.local.assign(T.boxes.size(), -1);
+  for (int i = 0; i < no; ++i) tp.local[tp.owners[i]] = i;
+  const int64_t side = (int64_t)1 << lvl;
+  const bool dense = lvl <= 7;
+  std::vector<int> grid;
+  if (dense) {
+    grid.assign((size_t)side * side * side, -1);
+    for (int a = 0; a < no; ++a) {
+      int64_t lo[3], hi[3];
+      T.extent(tp.owners[a], lvl, lo, hi);
+      for (int64_t x = lo[0]; x <= hi[0]; ++x)
+        for (int64_t y = lo[1]; y <= hi[1]; ++y)
+          for (int64_t z = lo[2]; z <= hi[2]; ++z) grid[(x * side + y) * side + z] = a;
+    }
+  }
+  tp.nb.assign(no, {});
+  tp.sep.assign(no, {});
+  std::vector<int> tmp;
+  for (int a = 0; a < no; ++a) {
+    const int box = tp.owners[a];
+    int64_t lo[3], hi[3];
+    T.extent(box, lvl, lo, hi);
+    tmp.clear();
+    tmp.push_back(a);
+    for (int64_t x = std::max<int64_t>(lo[0] - 2, 0); x <= std::min<int64_t>(hi[0] + 2, side - 1); ++x)
+      for (int64_t y = std::max<int64_t>(lo[1] - 2, 0); y <= std::min<int64_t>(hi[1] + 2, side - 1); ++y)
+        for (int64_t z = std::max<int64_t>(lo[2] - 2, 0); z <= std::min<int64_t>(hi[2] + 2, side - 1); ++z) {
+          if (x >= lo[0] && x <= hi[0] && y >= lo[1] && y <= hi[1] && z >= lo[2] && z <= hi[2]) continue;
+          int o;
+          if (dense) {
+            o = grid[(x * side + y) * side + z];
+          } else {
+            int ob = T.owner_of_cell(lvl, (int)x, (int)y, (int)z);
+            o = ob >= 0 ? tp.local[ob] : -1;
+          }
+          if (o >= 0) tmp.push_back(o);
+        }
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    tp.nb[a] = tmp;
+    tp.sep[a].resize(tmp.size());
+    for (size_t i = 0; i < tmp.size(); ++i)
+      tp.sep[a][i] = (signed char)(tmp[i] == a ? 0 : T.sep(box, tp.owners[tmp[i]], lvl));
+  }
+}
+
 struct LevelBSR {
   int level = -1;
-  std::vector<int> owners;                 // box ids
-  std::unordered_map<int, int> local;      // box id -> local owner index
-  std::vector<std::vector<int>> act;       // actives at level start (sorted)
-  std::unordered_map<long long, long long> pairoff;  // a*no+b -> complex offset
+  const LevelTopo* tp = nullptr;
+  std::vector<std::vector<int>> act;        // actives at level start (sorted), per local owner
+  std::vector<std::vector<long long>> poff; // complex offset of block (a, nb[a][i])
   DBuf bsr;
   long long size = 0;
-  long long key(int a, int b) const { return (long long)a * (long long)owners.size() + b; }
+  const std::vector<int>& owners() const { return tp->owners; }
+  int local(int box) const { return tp->local[box]; }
   long long off(int a, int b) const {
-    auto it = pairoff.find(key(a, b));
-    return it == pairoff.end() ? -1 : it->second;
+    const std::vector<int>& v = tp->nb[a];
+    auto it = std::lower_bound(v.begin(), v.end(), b);
+    return (it == v.end() || *it != b) ? -1 : poff[a][it - v.begin()];
   }
 };
 
@@ -401,6 +505,13 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     double tl0 = now_ms();
     LevelBSR cur;
     cur.level = lvl;
+    if ((int)h->topo.size() < L) h->topo.resize(L);
+    if (h->topo_ready.size() < (size_t)L) h->topo_ready.resize(L, 0);
+    if (!h->topo_ready[lvl]) {
+      build_topo(T, lvl, h->topo[lvl]);
+      h->topo_ready[lvl] = 1;
+    }
+    cur.tp = &h->topo[lvl];
     for (int b : T.levels[lvl]) {
       if (!T.boxes[b].leaf()) {
         std::vector<int> u;
@@ -409,27 +520,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::sort(u.begin(), u.end());
         act[b] = u;
       }
-      cur.owners.push_back(b);
     }
-    for (int m = 0; m < lvl; ++m)
-      for (int b : T.levels[m])
-        if (T.boxes[b].leaf()) cur.owners.push_back(b);
-    const int no = (int)cur.owners.size();
-    for (int i = 0; i < no; ++i) cur.local[cur.owners[i]] = i;
+    const int no = (int)cur.owners().size();
     cur.act.resize(no);
-    for (int i = 0; i < no; ++i) cur.act[i] = act[cur.owners[i]];
-    // neighbour lists (sep ≤ 2) and BSR layout
-    std::vector<std::vector<int>> nb(no);
-    std::vector<int> tmp;
+    for (int i = 0; i < no; ++i) cur.act[i] = act[cur.owners()[i]];
+    const std::vector<std::vector<int>>& nb = cur.tp->nb;
     long long off = 0;
+    cur.poff.resize(no);
     for (int a = 0; a < no; ++a) {
-      T.neighbours2(cur.owners[a], lvl, tmp);
-      nb[a].push_back(a);
-      for (int o : tmp) nb[a].push_back(cur.local.at(o));
-      std::sort(nb[a].begin(), nb[a].end());
-      for (int b : nb[a]) {
-        cur.pairoff[cur.key(a, b)] = off;
-        off += (long long)cur.act[a].size() * cur.act[b].size();
+      cur.poff[a].resize(nb[a].size());
+      for (size_t i = 0; i < nb[a].size(); ++i) {
+        cur.poff[a][i] = off;
+        off += (long long)cur.act[a].size() * cur.act[nb[a][i]].size();
       }
     }
     cur.size = off;
@@ -479,7 +581,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           for (size_t i = 0; i < slots_of[a].size(); ++i)
             for (size_t j = 0; j < slots_of[b].size(); ++j)
               tab[toff + i * ns + j] = prev.off(slots_of[a][i], slots_of[b][j]);
-          long long dst = cur.pairoff[cur.key(a, b)];
+          long long dst = cur.off(a, b);
           for (int i0 = 0; i0 < ra; i0 += kTile)
             for (int j0 = 0; j0 < cb; j0 += kTile) {
               BuildTask t;
@@ -544,15 +646,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       std::vector<BoxJob> jobs;
       for (int bx : T.levels[lvl]) {
         if (T.colour(bx) != colour) continue;
-        int a = cur.local.at(bx);
+        int a = cur.local(bx);
         int b = (int)curpos[a].size();
         if (b == 0) continue;
         BoxJob J;
         J.a = a;
         J.b = b;
-        for (int o : nb[a]) {
+        for (size_t ii = 0; ii < nb[a].size(); ++ii) {
+          const int o = nb[a][ii];
           if (o == a || curpos[o].empty()) continue;
-          int sp = T.sep(bx, cur.owners[o], lvl);
+          const int sp = cur.tp->sep[a][ii];
           if (sp <= 1) {
             J.N.push_back(o);
             J.nN += (int)curpos[o].size();
@@ -598,8 +701,6 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::vector<int> gidx;
         for (auto& J : jobs) {
           int row = 0;
-          long long bb = cur.pairoff[cur.key(J.a, J.a)];
-          (void)bb;
           for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
             int mo = (int)maps.size();
             maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
@@ -642,7 +743,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             gidx.insert(gidx.end(), cur.act[J.a].begin(), cur.act[J.a].end());
             p.ngamma = ngamma;
             double c3[3];
-            T.box_centre(cur.owners[J.a], c3);
+            T.box_centre(cur.owners()[J.a], c3);
             p.cx = c3[0];
             p.cy = c3[1];
             p.cz = c3[2];
@@ -1119,9 +1220,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         }
         run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep, h->prof, FMMLU_K_SCHUR);
         // index arena + records
-        FMMLU_CUDA(cudaMemcpyAsync(ph.idx.p, hidx.data(), hidx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        h2d(ph.idx.p, hidx.data(), hidx.size() * sizeof(int), st);
         ph.recs.alloc(recs.size() * sizeof(BoxRec), st);
-        FMMLU_CUDA(cudaMemcpyAsync(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), cudaMemcpyHostToDevice, st));
+        h2d(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), st);
         ph.nrec = (int)recs.size();
         {
           std::vector<SolveItem> items;
@@ -1130,8 +1231,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           ph.nitems = (int)items.size();
           ph.items.alloc(std::max<size_t>(1, items.size()) * sizeof(SolveItem), st);
           if (!items.empty())
-            FMMLU_CUDA(cudaMemcpyAsync(ph.items.p, items.data(), items.size() * sizeof(SolveItem),
-                                       cudaMemcpyHostToDevice, st));
+            h2d(ph.items.p, items.data(), items.size() * sizeof(SolveItem), st);
         }
         wait_stream(h, st);
         h->prof.resolve();
@@ -1161,7 +1261,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     for (int a = 0; a < no; ++a) {
       std::vector<int> na;
       for (int p : curpos[a]) na.push_back(cur.act[a][p]);
-      act[cur.owners[a]] = na;
+      act[cur.owners()[a]] = na;
     }
     std::fill(prevOwner.begin(), prevOwner.end(), -1);
     for (int a = 0; a < no; ++a)
@@ -1184,8 +1284,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   double tr0 = now_ms();
   std::vector<int> Bt;
   if (prev.level >= 0) {
-    for (size_t a = 0; a < prev.owners.size(); ++a)
-      for (int g : act[prev.owners[a]]) Bt.push_back(g);
+    for (size_t a = 0; a < prev.owners().size(); ++a)
+      for (int g : act[prev.owners()[a]]) Bt.push_back(g);
   } else {
     for (int i = 0; i < n; ++i) Bt.push_back(i);
   }
@@ -1201,7 +1301,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     std::vector<long long> tab;
     int ns = 1;
     if (prev.level >= 0) {
-      ns = (int)prev.owners.size();
+      ns = (int)prev.owners().size();
       for (int i = 0; i < n0; ++i) {
         slot[i] = prevOwner[Bt[i]];
         pos[i] = prevPos[Bt[i]];
@@ -1245,7 +1345,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     h->prof.end(rid, st);
     h->prof.add(FMMLU_K_ROOT, 8.0 * (double)n0 * n0 * n0, 32.0 * (double)n0 * n0, 3);
     h->root_rows.alloc((size_t)n0 * sizeof(int), st);
-    FMMLU_CUDA(cudaMemcpyAsync(h->root_rows.p, Bt.data(), n0 * sizeof(int), cudaMemcpyHostToDevice, st));
+    h2d(h->root_rows.p, Bt.data(), n0 * sizeof(int), st);
     wait_stream(h, st);
   }
   if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
@@ -1418,6 +1518,7 @@ int fmmlu_factor(fmmlu_handle* h, double k, double eps) {
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
     double t0 = now_ms();
+    tl_pin.reset();
     h->prof.reset();
     h->stats.t_sync_wait_ms = 0;
     factor_impl(h, k, eps);
