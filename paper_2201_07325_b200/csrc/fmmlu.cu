@@ -492,7 +492,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
 
   // host-time trace (FMMLU_TRACE=1): sections exclusive of stream waits
   static const bool trace = getenv("FMMLU_TRACE") != nullptr;
-  double tr[8] = {0};
+  double tr[16] = {0};
   double tmark = now_ms(), wmark = S.t_sync_wait_ms;
   auto lap = [&](int sec) {
     double t = now_ms(), w = S.t_sync_wait_ms;
@@ -764,6 +764,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         Stage s;
         size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_g = s.add(gidx);
         s.upload(st);
+        lap(8);
         int pid = h->prof.begin(FMMLU_K_GATHER, st);
         launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), M.as<cplx>(), st);
         launch_proxy(s.ptr<ProxyTask>(o_p), (int)pts.size(), s.ptr<int>(o_g), M.as<cplx>(), h->g, k, st);
@@ -789,6 +790,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         }
         // ID mode: at ε ≥ 1e-7 the pivoted Cholesky of G = MᴴM gives the
         // CPQR pivots/rank/T to ~u·cond accuracy (ε² ≫ u); tighter ε uses Householder TSQR.
+        lap(9);
         const bool gram = h->id_mode == 2 || (h->id_mode == 0 && eps >= 1e-7);
         std::vector<ClusterQrTask> cq(nj);
         DBuf G;
@@ -821,6 +823,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             add_gemm(gp, gt, P);
           }
           run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR);
+          lap(10);
           for (int j = 0; j < nj; ++j) {
             cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], nullptr, bcol[j], bcol[j], bcol[j], 0, jobs[j].permoff, 0};
             ids[j].Mp = G.as<cplx>() + goff[j];
@@ -831,7 +834,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           size_t o_i = s2.add(ids), o_q = s2.add(cq);
           s2.upload(st);
           int cid = h->prof.begin(FMMLU_K_CPQR, st);
+          lap(11);
           done_id = launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd.as<int>(), kd.as<int>(), eps, st, bmax);
+          lap(12);
           if (done_id) launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
           h->prof.end(cid, st);
           h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
@@ -863,6 +868,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           keep.push_back(std::move(s2.dev));
         }
         keep.push_back(std::move(G));
+        lap(13);
       }
       std::vector<int> hk(nj), hperm(permtot);
       FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1278,8 +1284,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   lap(6);
   if (trace)
     fprintf(stderr, "[fmmlu] host ms: level-setup %.1f build-tasks %.1f phase-jobs %.1f id %.1f elim %.1f "
-                    "update %.1f carry %.1f other %.1f | wait %.1f\n",
-            tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], S.t_sync_wait_ms);
+                    "update %.1f carry %.1f other %.1f | id: tasks %.1f gatherlaunch %.1f gram %.1f prep %.1f "
+                    "pchol %.1f rest %.1f | wait %.1f\n",
+            tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8], tr[9], tr[10], tr[11], tr[12], tr[13],
+            S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root
   double tr0 = now_ms();
   std::vector<int> Bt;
