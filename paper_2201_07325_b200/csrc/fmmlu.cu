@@ -315,6 +315,102 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cp
   tiles.clear();
 }
 
+// ---------------------------------------------------------------------------- blocked GJ inverse
+// In-place inverse (Gauss-Jordan, partial pivoting) of every (A, n) with lda = n: panels of nb
+// columns factored in shared memory, rank-nb updates of the other columns on the DMMA GEMM.
+void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats, int* d_status,
+                std::vector<DBuf>& keep, int cls) {
+  cudaStream_t st = h->stream;
+  if (mats.empty()) return;
+  int nmax = 1;
+  for (auto& m : mats) nmax = std::max(nmax, m.second);
+  const int nb = gj_panel_width(nmax);
+  long long csz = 0, isz = 0;
+  for (auto& m : mats) {
+    csz += 2LL * m.second * nb + (long long)m.second * m.second;
+    isz += m.second;
+  }
+  DBuf cb, ib;
+  cb.alloc((size_t)csz * sizeof(cplx), st);
+  ib.alloc((size_t)std::max<long long>(isz, 1) * sizeof(int), st);
+  std::vector<GjTask> tasks;
+  std::vector<long long> soff;
+  long long co = 0, io = 0;
+  double fl = 0, by = 0;
+  for (auto& m : mats) {
+    GjTask t{};
+    t.A = m.first;
+    t.lda = m.second;
+    t.n = m.second;
+    t.Am = cb.as<cplx>() + co;
+    co += (long long)m.second * nb;
+    t.Y = cb.as<cplx>() + co;
+    co += (long long)m.second * nb;
+    soff.push_back(co);
+    co += (long long)m.second * m.second;
+    t.piv = ib.as<int>() + io;
+    io += m.second;
+    tasks.push_back(t);
+    fl += 8.0 * (double)m.second * m.second * m.second;
+    by += 32.0 * (double)m.second * m.second;
+  }
+  std::vector<GemmProblem> gp;
+  std::vector<GemmTile> gt;
+  std::vector<std::pair<size_t, size_t>> launches;  // (tile offset, tile count) per panel
+  for (int j0 = 0; j0 < nmax; j0 += nb) {
+    std::vector<GemmProblem> pp;
+    std::vector<GemmTile> tt;
+    for (auto& t : tasks) {
+      if (j0 >= t.n) continue;
+      const int jb = std::min(nb, t.n - j0);
+      GemmProblem L{};
+      L.m = t.n;
+      L.n = j0;
+      L.k = jb;
+      L.opA = kOpN;
+      L.opB = kOpN;
+      L.A = t.Am;
+      L.lda = t.n;
+      L.B = t.Y;
+      L.ldb = nb;
+      L.C = t.A;
+      L.ldc = t.lda;
+      add_gemm(pp, tt, L);
+      GemmProblem R = L;
+      R.n = t.n - j0 - jb;
+      R.B = t.Y + (size_t)(j0 + jb) * nb;
+      R.C = t.A + (size_t)(j0 + jb) * t.lda;
+      add_gemm(pp, tt, R);
+    }
+    for (auto& x : tt) x.p += (int)gp.size();
+    launches.push_back({gt.size(), tt.size()});
+    gp.insert(gp.end(), pp.begin(), pp.end());
+    gt.insert(gt.end(), tt.begin(), tt.end());
+  }
+  Stage s;
+  size_t o_t = s.add(tasks), o_s = s.add(soff), o_p = s.add(gp), o_g = s.add(gt);
+  s.upload(st);
+  int id = h->prof.begin(cls, st);
+  int pi = 0;
+  long long nl = 0;
+  for (int j0 = 0; j0 < nmax; j0 += nb, ++pi) {
+    launch_gj_panel(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, st, nmax);
+    launch_gj_swap(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, st, nmax);
+    nl += 2;
+    if (launches[pi].second) {
+      gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_g) + launches[pi].first, (int)launches[pi].second,
+                   cmk(1.0, 0.0), 0, nullptr, st);
+      ++nl;
+    }
+  }
+  launch_gj_unscramble(s.ptr<GjTask>(o_t), (int)tasks.size(), cb.as<cplx>(), s.ptr<long long>(o_s), st, nmax);
+  h->prof.end(id, st);
+  h->prof.add(cls, fl, by, nl + 2);
+  keep.push_back(std::move(s.dev));
+  keep.push_back(std::move(cb));
+  keep.push_back(std::move(ib));
+}
+
 // ---------------------------------------------------------------------------- cluster TSQR
 // Only R of M = Q R is needed (CPQR(R) selects the same pivots and T as CPQR(M): Qᴴ preserves
 // column norms and inner products).  Each round splits every box matrix that does not fit one
@@ -1132,20 +1228,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         }
         run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_EF);
         // X_RR⁻¹ (Gauss-Jordan with partial pivoting)
-        int iid = h->prof.begin(FMMLU_K_INV, st);
         launch_copy(s.ptr<CopyTask>(o_cx), (int)cpsX.size(), s.ptr<int>(o_m), Wp, F, st);
-        if (!launch_gj_cluster(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
-                               ph.rmax))
-          launch_gj_inverse(s.ptr<long long>(o_go), s.ptr<int>(o_gd), (int)gjdim.size(), F, status.as<int>(), st,
-                            ph.rmax);
-        h->prof.end(iid, st);
         {
-          double fl = 0, by = 0;
-          for (int d : gjdim) {
-            fl += 8.0 * (double)d * d * d;
-            by += 32.0 * (double)d * d;
-          }
-          h->prof.add(FMMLU_K_INV, fl, by, 2);
+          std::vector<std::pair<cplx*, int>> mats;
+          for (size_t e = 0; e < gjdim.size(); ++e) mats.push_back({F + gjoff[e], gjdim[e]});
+          gj_blocked(h, mats, status.as<int>(), keep, FMMLU_K_INV);
         }
         // Up = X_RR⁻¹ X_{R(S∪N)} ;  Lp = X_{(S∪N)R} X_RR⁻¹
         for (size_t e = 0; e < el.size(); ++e) {
@@ -1347,11 +1434,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     int rid = h->prof.begin(FMMLU_K_ROOT, st);
     launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
                  s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), h->root.as<cplx>(), h->g, k, st);
-    DBuf scratch;
-    scratch.alloc(((size_t)n0 * n0 + 3 * (size_t)n0 + 8) * sizeof(cplx), st);
-    launch_gj_inverse_coop(h->root.as<cplx>(), n0, scratch.as<cplx>(), status.as<int>(), st);
     h->prof.end(rid, st);
-    h->prof.add(FMMLU_K_ROOT, 8.0 * (double)n0 * n0 * n0, 32.0 * (double)n0 * n0, 3);
+    h->prof.add(FMMLU_K_ROOT, 60.0 * (double)n0 * n0, 16.0 * (double)n0 * n0, 1);
+    std::vector<DBuf> rkeep;
+    gj_blocked(h, {{h->root.as<cplx>(), n0}}, status.as<int>(), rkeep, FMMLU_K_ROOT);
     h->root_rows.alloc((size_t)n0 * sizeof(int), st);
     h2d(h->root_rows.p, Bt.data(), n0 * sizeof(int), st);
     wait_stream(h, st);

@@ -237,6 +237,136 @@ __global__ void __launch_bounds__(GJ_NT) k_gj(const long long* __restrict__ offs
   }
 }
 
+// ------------------------------------------------------------------ blocked Gauss-Jordan
+// In-place Gauss-Jordan with partial pivoting, blocked by column panels J = [j0, j0+jb):
+// the steps of a panel, as a transform of every column outside J, are  x ← G P x  with P the
+// panel's row interchanges and G = I + (Gp − E_J) E_Jᵀ, where Gp = the panel's own in-place GJ
+// output (computable from the panel alone).  So: [panel] GJ of the n×jb panel in shared memory
+// → Gp, pivots;  [swap] apply the interchanges to the other columns and copy their rows J → Y;
+// [GEMM] C_out += (Gp − E_J) · Y.  After the last panel the column interchanges are undone.
+constexpr int GJP_NT = 512;
+
+__global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ tasks, int j0, int nb,
+                                                     int* status) {
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ cplx rowj[64];
+  const GjTask t = tasks[blockIdx.x];
+  const int n = t.n;
+  if (j0 >= n) return;
+  const int jb = min(nb, n - j0);
+  cplx* P = reinterpret_cast<cplx*>(shm);  // n × jb (ld n)
+  cplx* colf = P + (size_t)n * jb;         // n: multipliers of the current step
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * jb; e += GJP_NT) {
+    const int i = e % n, c = e / n;
+    P[e] = t.A[i + (size_t)(j0 + c) * t.lda];
+  }
+  __syncthreads();
+  for (int s = 0; s < jb; ++s) {
+    const int j = j0 + s;
+    cplx* Pc = P + (size_t)s * n;
+    double pv = -1.0;
+    int p = INT_MAX;
+    for (int i = j + tid; i < n; i += GJP_NT) argmax_merge(pv, p, cabs2(Pc[i]), i);
+    block_argmax<GJP_NT>(pv, p, red_v, red_i);
+    if (!(pv > 0.0)) {  // exactly singular: flag it and continue with a harmless identity step
+      if (tid == 0) atomicExch(status, 1);
+      p = j;
+    }
+    if (tid == 0) t.piv[j] = p;
+    if (p != j)
+      for (int c = tid; c < jb; c += GJP_NT) {
+        const cplx a = P[j + (size_t)c * n];
+        P[j + (size_t)c * n] = P[p + (size_t)c * n];
+        P[p + (size_t)c * n] = a;
+      }
+    __syncthreads();
+    const cplx d = Pc[j];
+    const cplx dinv = pv > 0.0 ? cdiv(cmk(1.0, 0.0), d) : cmk(1.0, 0.0);
+    for (int c = tid; c < jb; c += GJP_NT) rowj[c] = c == s ? dinv : cmul(P[j + (size_t)c * n], dinv);
+    for (int i = tid; i < n; i += GJP_NT) colf[i] = Pc[i];
+    __syncthreads();
+    for (int e = tid; e < n * jb; e += GJP_NT) {
+      const int i = e % n, c = e / n;
+      cplx v;
+      if (i == j) v = rowj[c];
+      else if (c == s) v = cmk(-(colf[i].x * dinv.x - colf[i].y * dinv.y), -(colf[i].x * dinv.y + colf[i].y * dinv.x));
+      else v = cfms(colf[i], rowj[c], P[e]);
+      P[e] = v;
+    }
+    __syncthreads();
+  }
+  // write the panel back and Am = Gp − E_J (n × jb, ld n)
+  for (int e = tid; e < n * jb; e += GJP_NT) {
+    const int i = e % n, c = e / n;
+    const cplx v = P[e];
+    t.A[i + (size_t)(j0 + c) * t.lda] = v;
+    t.Am[e] = i == j0 + c ? cmk(v.x - 1.0, v.y) : v;
+  }
+}
+
+// Apply the panel's interchanges to every column outside J and gather their rows J into Y
+// (jb × n, ld nb).  grid (ceil(n/128), ntasks).
+__global__ void k_gj_swap(const GjTask* __restrict__ tasks, int j0, int nb) {
+  const GjTask t = tasks[blockIdx.y];
+  const int n = t.n;
+  if (j0 >= n) return;
+  const int jb = min(nb, n - j0);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n || (c >= j0 && c < j0 + jb)) return;
+  cplx* col = t.A + (size_t)c * t.lda;
+  for (int s = 0; s < jb; ++s) {
+    const int j = j0 + s, p = t.piv[j];
+    if (p != j) {
+      cplx a = col[j];
+      col[j] = col[p];
+      col[p] = a;
+    }
+  }
+  for (int s = 0; s < jb; ++s) t.Y[s + (size_t)c * nb] = col[j0 + s];
+}
+
+// Undo the column interchanges: column c of the inverse = column L[c], L = swaps in reverse.
+// grid (ceil(n/32), ntasks): every CTA rebuilds L in shared memory, copies its 32 columns to
+// scratch; k_gj_copyback then copies scratch back over A.
+__global__ void k_gj_unscramble(const GjTask* __restrict__ tasks, cplx* __restrict__ scratch,
+                                const long long* __restrict__ soff) {
+  extern __shared__ int Lsh[];
+  const GjTask t = tasks[blockIdx.y];
+  const int n = t.n;
+  const int c0 = blockIdx.x * 32;
+  if (c0 >= n) return;
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < n; ++c) Lsh[c] = c;
+    for (int j = n - 1; j >= 0; --j) {
+      const int p = t.piv[j];
+      const int a = Lsh[j];
+      Lsh[j] = Lsh[p];
+      Lsh[p] = a;
+    }
+  }
+  __syncthreads();
+  cplx* B = scratch + soff[blockIdx.y];
+  const int c1 = min(n, c0 + 32);
+  for (int e = threadIdx.x; e < n * (c1 - c0); e += blockDim.x) {
+    const int i = e % n, c = c0 + e / n;
+    B[i + (size_t)c * n] = t.A[i + (size_t)Lsh[c] * t.lda];
+  }
+}
+__global__ void k_gj_copyback(const GjTask* __restrict__ tasks, const cplx* __restrict__ scratch,
+                              const long long* __restrict__ soff) {
+  const GjTask t = tasks[blockIdx.y];
+  const int n = t.n;
+  const cplx* B = scratch + soff[blockIdx.y];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), c = (int)(e / n);
+    t.A[i + (size_t)c * t.lda] = B[e];
+  }
+}
+
 // ------------------------------------------------------------------ cluster kernels (DSMEM)
 // Columns of an n×n (or m×b) matrix are distributed cyclically over the CL CTAs of a
 // thread-block cluster (global column g lives in CTA g % CL, local slot g / CL) and held in
@@ -1160,6 +1290,48 @@ void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* w
   if (ntasks <= 0) return;
   dim3 grid(ntasks, 8);
   k_proxy<<<grid, 256, 0, st>>>(d_tasks, gidx, ws, g, k);
+  FMMLU_LAUNCH();
+}
+
+int gj_panel_width(int nmax) {
+  const size_t cap = 200 * 1024;
+  int nb = (int)(cap / (16 * (size_t)std::max(nmax, 1))) - 1;
+  return std::max(1, std::min(nb, 32));
+}
+
+void launch_gj_panel(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st, int nmax) {
+  if (ntasks <= 0) return;
+  const size_t smem = (size_t)nmax * (nb + 1) * sizeof(cplx) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gj_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  k_gj_panel<<<ntasks, GJP_NT, smem, st>>>(d_tasks, j0, nb, d_status);
+  FMMLU_LAUNCH();
+}
+
+void launch_gj_swap(const GjTask* d_tasks, int ntasks, int j0, int nb, cudaStream_t st, int nmax) {
+  if (ntasks <= 0) return;
+  dim3 grid((nmax + 127) / 128, ntasks);
+  k_gj_swap<<<grid, 128, 0, st>>>(d_tasks, j0, nb);
+  FMMLU_LAUNCH();
+}
+
+void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, const long long* d_soff, cudaStream_t st,
+                          int nmax) {
+  if (ntasks <= 0) return;
+  const size_t smem = (size_t)nmax * sizeof(int) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gj_unscramble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  dim3 g1((nmax + 31) / 32, ntasks);
+  k_gj_unscramble<<<g1, 256, smem, st>>>(d_tasks, scratch, d_soff);
+  FMMLU_LAUNCH();
+  dim3 g2(std::min(1024, (int)(((long long)nmax * nmax + 255) / 256)), ntasks);
+  k_gj_copyback<<<g2, 256, 0, st>>>(d_tasks, scratch, d_soff);
   FMMLU_LAUNCH();
 }
 

@@ -71,6 +71,19 @@ void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* w
                   double k, cudaStream_t st);
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st);
+// Blocked in-place Gauss-Jordan inverse (partial pivoting) of a batch of matrices.
+struct GjTask {
+  cplx* A;   // n × n, ld lda, inverted in place
+  cplx* Am;  // n × nb scratch (panel minus identity)
+  cplx* Y;   // nb × n scratch (rows J of the other columns)
+  int* piv;  // n pivot rows
+  int lda, n;
+};
+int gj_panel_width(int nmax);  // panel width nb whose n×nb panel fits shared memory
+void launch_gj_panel(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st, int nmax);
+void launch_gj_swap(const GjTask* d_tasks, int ntasks, int j0, int nb, cudaStream_t st, int nmax);
+void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, const long long* d_soff, cudaStream_t st,
+                          int nmax);
 // in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
 void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx* arena,
                        int* d_status, cudaStream_t st, int nmax);
