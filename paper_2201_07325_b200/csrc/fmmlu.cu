@@ -248,6 +248,18 @@ struct fmmlu_handle {
   size_t cur_bytes = 0, peak_bytes = 0;
   Prof prof;
   std::vector<LevelTopo> topo;    // per-level owner topology (tree-only, cached)
+  int* d2h_buf = nullptr;         // pinned landing buffer for ranks / pivots
+  size_t d2h_cap = 0;
+  int* d2h(size_t n) {
+    if (n > d2h_cap) {
+      if (d2h_buf) cudaFreeHost(d2h_buf);
+      d2h_cap = std::max<size_t>(n, 2 * d2h_cap + 4096);
+      void* p = nullptr;
+      FMMLU_CUDA(cudaMallocHost(&p, d2h_cap * sizeof(int)));
+      d2h_buf = (int*)p;
+    }
+    return d2h_buf;
+  }
   std::vector<char> topo_ready;
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
@@ -967,9 +979,12 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         lap(13);
       }
       std::vector<int> hk(nj), hperm(permtot);
-      FMMLU_CUDA(cudaMemcpyAsync(hk.data(), kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
-      FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
+      int* pin = h->d2h(nj + permtot);
+      FMMLU_CUDA(cudaMemcpyAsync(pin, kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FMMLU_CUDA(cudaMemcpyAsync(pin + nj, permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
       wait_stream(h, st);
+      std::memcpy(hk.data(), pin, nj * sizeof(int));
+      std::memcpy(hperm.data(), pin + nj, permtot * sizeof(int));
       h->prof.resolve();
       keep.clear();
       track(h, -(long long)M.bytes);
@@ -1326,9 +1341,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           if (!items.empty())
             h2d(ph.items.p, items.data(), items.size() * sizeof(SolveItem), st);
         }
-        wait_stream(h, st);
-        h->prof.resolve();
-        keep.clear();
+        // no sync here: the next phase's ID preparation overlaps with this elimination on the GPU
         keep.push_back(std::move(s.dev));
         track(h, -(long long)W.bytes);
         W.release();
@@ -1363,9 +1376,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         prevPos[cur.act[a][i]] = (int)i;
       }
     prev = std::move(cur);
-    wait_stream(h, st);
-    h->prof.resolve();
-    S.t_levels_ms[lvl] = now_ms() - tl0;
+    S.t_levels_ms[lvl] = now_ms() - tl0;  // host-side span of the level (GPU work may still drain)
   }
 
   lap(6);
@@ -1675,6 +1686,7 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->perm.release();
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  if (h->d2h_buf) cudaFreeHost(h->d2h_buf);
   delete h;
   return FMMLU_OK;
 }
