@@ -780,6 +780,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         jobs.push_back(std::move(J));
       }
       if (jobs.empty()) continue;
+      if (trace) {
+        int bmx = 0, mmx = 0, nmx = 0;
+        for (auto& J : jobs) {
+          bmx = std::max(bmx, J.b);
+          mmx = std::max(mmx, J.m);
+          nmx = std::max(nmx, J.nN);
+        }
+        fprintf(stderr, "[fmmlu] L%d c%d boxes %zu bmax %d mmax %d nNmax %d ngamma %d mem %.2f GB t %.1f ms\n", lvl,
+                colour, jobs.size(), bmx, mmx, nmx, ngamma, h->cur_bytes / 1e9, now_ms() - tl0);
+      }
       const int nj = (int)jobs.size();
 
       lap(2);
@@ -1050,6 +1060,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           S.n_eliminated += 1;
         }
         DBuf W;
+        if (trace)
+          fprintf(stderr, "[fmmlu]   elim: boxes %zu W %.2f GB factor %.2f GB\n", el.size(), wsW * 16e-9,
+                  facsz * 16e-9);
         W.alloc((size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
         ph.fac.alloc((size_t)std::max<long long>(facsz, 1) * sizeof(cplx), st);
         FMMLU_CUDA(cudaMemsetAsync(ph.fac.p, 0, ph.fac.bytes, st));
