@@ -224,8 +224,8 @@ struct Prof {
 struct LevelTopo {
   std::vector<int> owners;
   std::vector<int> local;
-  std::vector<std::vector<int>> nb;
-  std::vector<std::vector<signed char>> sep;
+  std::vector<std::vector<int>> boxN, boxQ;  // per level-ℓ box (local ids 0..nbox-1): N and Q owners
+  std::vector<std::vector<int>> nb;          // per owner: block partners (pair set, sorted)
 };
 
 struct fmmlu_handle {
@@ -452,6 +452,9 @@ void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mro
       const int nch = (mrows[j] + H - 1) / H, bh = mrows[j] / nch, ex = mrows[j] % nch;
       int rr = 0;
       for (int c = 0; c < nch; ++c) rr += std::min(bh + (c < ex ? 1 : 0), bcol[j]);
+      if (rr >= mrows[j])
+        throw Error(FMMLU_ENOTIMPL, "cluster TSQR cannot reduce a " + std::to_string(mrows[j]) + "x" +
+                                        std::to_string(bcol[j]) + " ID matrix (box too large for id_mode 1)");
       noff[j] = tot;
       nrows[j] = rr;
       tot += (long long)rr * bcol[j];
@@ -498,56 +501,56 @@ void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mro
 }
 
 // ---------------------------------------------------------------------------- factorization
+// N/Q lists of the level-ℓ boxes from 5×5×5 cell lookups (coarser owners found through their
+// ancestors), and the block-pair set = all pairs (x, y) with x, y ∈ {B} ∪ N(B) plus (B, q), (q, B),
+// q ∈ Q(B), over the level-ℓ boxes B: exactly the blocks the level can read or modify (and every
+// block modified at level ℓ+1 maps into it, since both owners touch the parent box).
 void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
   tp.owners.clear();
   for (int b : T.levels[lvl]) tp.owners.push_back(b);
+  const int nlb = (int)tp.owners.size();
   for (int m = 0; m < lvl; ++m)
     for (int b : T.levels[m])
       if (T.boxes[b].leaf()) tp.owners.push_back(b);
   const int no = (int)tp.owners.size();
   tp.local.assign(T.boxes.size(), -1);
   for (int i = 0; i < no; ++i) tp.local[tp.owners[i]] = i;
-  const int64_t side = (int64_t)1 << lvl;
-  const bool dense = lvl <= 7;
-  std::vector<int> grid;
-  if (dense) {
-    grid.assign((size_t)side * side * side, -1);
-    for (int a = 0; a < no; ++a) {
-      int64_t lo[3], hi[3];
-      T.extent(tp.owners[a], lvl, lo, hi);
-      for (int64_t x = lo[0]; x <= hi[0]; ++x)
-        for (int64_t y = lo[1]; y <= hi[1]; ++y)
-          for (int64_t z = lo[2]; z <= hi[2]; ++z) grid[(x * side + y) * side + z] = a;
+  const int lim = (1 << lvl) - 1;
+  tp.boxN.assign(nlb, {});
+  tp.boxQ.assign(nlb, {});
+  std::vector<std::vector<int>> pairs(no);
+  std::vector<int> cand, grp;
+  for (int i = 0; i < nlb; ++i) {
+    const int box = tp.owners[i];
+    const Box& B = T.boxes[box];
+    cand.clear();
+    for (int dx = -2; dx <= 2; ++dx)
+      for (int dy = -2; dy <= 2; ++dy)
+        for (int dz = -2; dz <= 2; ++dz) {
+          const int x = B.c[0] + dx, y = B.c[1] + dy, z = B.c[2] + dz;
+          if (x < 0 || y < 0 || z < 0 || x > lim || y > lim || z > lim) continue;
+          const int ob = T.owner_of_cell(lvl, x, y, z);
+          if (ob < 0 || ob == box) continue;
+          const int o = tp.local[ob];
+          if (o >= 0) cand.push_back(o);
+        }
+    std::sort(cand.begin(), cand.end());
+    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+    for (int o : cand) (T.sep(box, tp.owners[o], lvl) <= 1 ? tp.boxN[i] : tp.boxQ[i]).push_back(o);
+    grp.assign(1, i);
+    grp.insert(grp.end(), tp.boxN[i].begin(), tp.boxN[i].end());
+    for (int x : grp)
+      for (int y : grp) pairs[x].push_back(y);
+    for (int q : tp.boxQ[i]) {
+      pairs[i].push_back(q);
+      pairs[q].push_back(i);
     }
   }
   tp.nb.assign(no, {});
-  tp.sep.assign(no, {});
-  std::vector<int> tmp;
   for (int a = 0; a < no; ++a) {
-    const int box = tp.owners[a];
-    int64_t lo[3], hi[3];
-    T.extent(box, lvl, lo, hi);
-    tmp.clear();
-    tmp.push_back(a);
-    for (int64_t x = std::max<int64_t>(lo[0] - 2, 0); x <= std::min<int64_t>(hi[0] + 2, side - 1); ++x)
-      for (int64_t y = std::max<int64_t>(lo[1] - 2, 0); y <= std::min<int64_t>(hi[1] + 2, side - 1); ++y)
-        for (int64_t z = std::max<int64_t>(lo[2] - 2, 0); z <= std::min<int64_t>(hi[2] + 2, side - 1); ++z) {
-          if (x >= lo[0] && x <= hi[0] && y >= lo[1] && y <= hi[1] && z >= lo[2] && z <= hi[2]) continue;
-          int o;
-          if (dense) {
-            o = grid[(x * side + y) * side + z];
-          } else {
-            int ob = T.owner_of_cell(lvl, (int)x, (int)y, (int)z);
-            o = ob >= 0 ? tp.local[ob] : -1;
-          }
-          if (o >= 0) tmp.push_back(o);
-        }
-    std::sort(tmp.begin(), tmp.end());
-    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-    tp.nb[a] = tmp;
-    tp.sep[a].resize(tmp.size());
-    for (size_t i = 0; i < tmp.size(); ++i)
-      tp.sep[a][i] = (signed char)(tmp[i] == a ? 0 : T.sep(box, tp.owners[tmp[i]], lvl));
+    std::sort(pairs[a].begin(), pairs[a].end());
+    pairs[a].erase(std::unique(pairs[a].begin(), pairs[a].end()), pairs[a].end());
+    tp.nb[a] = std::move(pairs[a]);
   }
 }
 
@@ -760,18 +763,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         BoxJob J;
         J.a = a;
         J.b = b;
-        for (size_t ii = 0; ii < nb[a].size(); ++ii) {
-          const int o = nb[a][ii];
-          if (o == a || curpos[o].empty()) continue;
-          const int sp = cur.tp->sep[a][ii];
-          if (sp <= 1) {
+        for (int o : cur.tp->boxN[a])
+          if (!curpos[o].empty()) {
             J.N.push_back(o);
             J.nN += (int)curpos[o].size();
-          } else {
+          }
+        for (int o : cur.tp->boxQ[a])
+          if (!curpos[o].empty()) {
             J.Q.push_back(o);
             J.nQ += (int)curpos[o].size();
           }
-        }
         long long nF = total_active - b - J.nN;
         if (nF == 0) continue;  // F = ∅ → S = B (reading C12)
         long long nP = nF - J.nQ;
@@ -920,8 +921,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             goff[j] = gsz;
             gsz += (long long)bcol[j] * bcol[j];
           }
-          G.alloc((size_t)gsz * sizeof(cplx), st);
-          FMMLU_CUDA(cudaMemsetAsync(G.p, 0, G.bytes, st));
+          G.alloc(2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
+          FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
           std::vector<GemmProblem> gp;
           std::vector<GemmTile> gt;
           for (int j = 0; j < nj; ++j) {
@@ -943,7 +944,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR);
           lap(10);
           for (int j = 0; j < nj; ++j) {
-            cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], nullptr, bcol[j], bcol[j], bcol[j], 0, jobs[j].permoff, 0};
+            cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], G.as<cplx>() + gsz + goff[j], bcol[j], bcol[j], bcol[j],
+                                  bcol[j], jobs[j].permoff, 0};
             ids[j].Mp = G.as<cplx>() + goff[j];
             ids[j].m = bcol[j];
             jobs[j].mfin = bcol[j];

@@ -666,16 +666,15 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   const int ncl = (b - rank + CL - 1) / CL;
   const int nclmax = (b + CL - 1) / CL;
   cplx* Sl = reinterpret_cast<cplx*>(shm);          // b × ncl: local columns of the Schur complement
-  cplx* Rl = Sl + (size_t)b * nclmax;               // b × ncl: rows of R for the local columns (row = step)
-  cplx* pc = Rl + (size_t)b * nclmax;               // b: copy of the pivot column
+  cplx* pc = Sl + (size_t)b * nclmax;               // b: copy of the pivot column
   cplx* rowp = pc + b;                              // ncl: row p of the local columns
   int* piv = reinterpret_cast<int*>(rowp + nclmax); // b
   int* done = piv + b;                              // b
+  cplx* Rg = t.out;                                 // b × b (ld b): R rows by natural column
   const int tid = threadIdx.x;
   for (int e = tid; e < b * ncl; e += CK_NT) {
     const int i = e % b, l = e / b;
     Sl[e] = t.A[i + (size_t)(rank + l * CL) * t.lda];
-    Rl[e] = cmk(0.0, 0.0);
   }
   for (int g = tid; g < b; g += CK_NT) done[g] = 0;
   cl.sync();
@@ -712,19 +711,18 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
     }
     for (int l = tid; l < ncl; l += CK_NT) rowp[l] = Sl[p + (size_t)l * b];
     cl.sync();  // (B) column p and row p copied everywhere; candidates of step j consumed
-    const double sd = sqrt(pv), inv = 1.0 / pv;
+    const double sd = sqrt(pv), inv = 1.0 / pv, isd = 1.0 / sd;
     // R_{j,c} = S_{p,c}/√S_pp ;  S_{a,c} −= S_{a,p} S_{p,c} / S_pp  (remaining columns c)
+    for (int l = tid; l < ncl; l += CK_NT) {
+      const int g = rank + l * CL;
+      if (g == p) Rg[j + (size_t)g * b] = cmk(sd, 0.0);
+      else if (!done[g]) Rg[j + (size_t)g * b] = cscale(rowp[l], isd);
+    }
     for (int e = tid; e < b * ncl; e += CK_NT) {
       const int a = e % b, l = e / b;
       const int g = rank + l * CL;
-      if (g == p) {
-        if (a == j) Rl[j + (size_t)l * b] = cmk(sd, 0.0);
-        continue;
-      }
       if (done[g]) continue;
-      const cplx spc = rowp[l];
-      if (a == j) Rl[j + (size_t)l * b] = cscale(spc, 1.0 / sd);
-      Sl[e] = cfms(cscale(pc[a], inv), spc, Sl[e]);
+      Sl[e] = cfms(cscale(pc[a], inv), rowp[l], Sl[e]);
     }
     __syncthreads();
   }
@@ -738,11 +736,12 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
       if (posmap[g] < 0) posmap[g] = c++;
   }
   __syncthreads();
-  cl.sync();  // all CTAs loaded G; write R' over it
+  cl.sync();  // all CTAs loaded G and wrote their R rows; write R' over G
   for (int e = tid; e < kk * ncl; e += CK_NT) {
     const int i = e % kk, l = e / kk;
     const int g = rank + l * CL;
-    t.A[i + (size_t)posmap[g] * t.lda] = Rl[i + (size_t)l * b];
+    const int c = posmap[g];
+    t.A[i + (size_t)c * t.lda] = (c < kk && i > c) ? cmk(0.0, 0.0) : Rg[i + (size_t)g * b];
   }
   for (int l = tid; l < ncl; l += CK_NT) perm_out[t.out_off + posmap[rank + l * CL]] = rank + l * CL;
   if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
@@ -1397,7 +1396,7 @@ int hqr_max_rows(int b, int CL) {
 
 size_t pchol_smem(int b, int CL) {
   const size_t ncl = (b + CL - 1) / CL;
-  return 2 * (size_t)b * ncl * sizeof(cplx) + (size_t)b * sizeof(cplx) + ncl * sizeof(cplx) +
+  return (size_t)b * ncl * sizeof(cplx) + (size_t)b * sizeof(cplx) + ncl * sizeof(cplx) +
          2 * (size_t)b * sizeof(int) + 64;
 }
 
