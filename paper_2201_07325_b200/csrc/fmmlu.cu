@@ -336,7 +336,16 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   if (mats.empty()) return;
   int nmax = 1;
   for (auto& m : mats) nmax = std::max(nmax, m.second);
-  const int nb = gj_panel_width(nmax);
+  int nb = gj_panel_width(nmax);
+  bool cluster_panel = false;
+  if (nb < 32 && nmax > 64) {  // tall blocks (root): panel rows spread over a cluster, nb up to 32
+    for (int w = 32; w >= 8; w /= 2)
+      if (gj_panel_cluster_size(nmax, w) > 0) {
+        nb = w;
+        cluster_panel = true;
+        break;
+      }
+  }
   long long csz = 0, isz = 0;
   for (auto& m : mats) {
     csz += 2LL * m.second * nb + (long long)m.second * m.second;
@@ -406,7 +415,10 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   int pi = 0;
   long long nl = 0;
   for (int j0 = 0; j0 < nmax; j0 += nb, ++pi) {
-    launch_gj_panel(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, st, nmax);
+    if (cluster_panel)
+      launch_gj_panel_cluster(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, st, nmax);
+    else
+      launch_gj_panel(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, st, nmax);
     launch_gj_swap(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, st, nmax);
     nl += 2;
     if (launches[pi].second) {

@@ -307,6 +307,91 @@ __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ 
   }
 }
 
+// Same panel step with the n × jb panel's ROWS distributed over a thread-block cluster (CTA r
+// owns rows [r·rc, (r+1)·rc)): for large blocks (the root, n_0 in the thousands).  Per column:
+// (A) cluster argmax of the pivot, (B) everybody has read the old rows j and p; the owners then
+// swap, and every CTA eliminates its own rows.  grid (CL, ntasks).
+__global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __restrict__ tasks, int j0, int nb,
+                                                            int* status) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ double cand_v;
+  __shared__ int cand_i;
+  __shared__ cplx rj_old[64], rp_old[64], rowj[64];
+  const GjTask t = tasks[blockIdx.y];
+  const int n = t.n;
+  if (j0 >= n) return;  // uniform across the cluster
+  const int jb = min(nb, n - j0);
+  const int rc = (n + CL - 1) / CL;
+  const int r0 = rank * rc, r1 = min(n, r0 + rc), nr = max(0, r1 - r0);
+  cplx* P = reinterpret_cast<cplx*>(shm);  // nr × jb (ld rc): own rows of the panel
+  cplx* fcol = P + (size_t)rc * jb;        // rc: multipliers of the current column
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nr * jb; e += CK_NT) {
+    const int i = e % nr, c = e / nr;
+    P[i + (size_t)c * rc] = t.A[(r0 + i) + (size_t)(j0 + c) * t.lda];
+  }
+  cl.sync();
+  for (int s = 0; s < jb; ++s) {
+    const int j = j0 + s;
+    double pv = -1.0;
+    int p = INT_MAX;
+    for (int i = max(j, r0) + tid; i < r1; i += CK_NT) argmax_merge(pv, p, cabs2(P[(i - r0) + (size_t)s * rc]), i);
+    block_argmax<CK_NT>(pv, p, red_v, red_i);
+    if (tid == 0) {
+      cand_v = pv;
+      cand_i = p;
+    }
+    cl.sync();  // (A)
+    pv = -1.0;
+    p = INT_MAX;
+    for (int r = 0; r < CL; ++r)
+      argmax_merge(pv, p, *cl.map_shared_rank(&cand_v, r), *cl.map_shared_rank(&cand_i, r));
+    const bool sing = !(pv > 0.0);
+    if (sing) p = j;
+    if (rank == 0 && tid == 0) {
+      t.piv[j] = p;
+      if (sing) atomicExch(status, 1);
+    }
+    const int oj = j / rc, op = p / rc;
+    const cplx* Rj = cl.map_shared_rank(P, oj) + (j - oj * rc);
+    const cplx* Rp = cl.map_shared_rank(P, op) + (p - op * rc);
+    for (int c = tid; c < jb; c += CK_NT) {
+      rj_old[c] = Rj[(size_t)c * rc];
+      rp_old[c] = Rp[(size_t)c * rc];
+    }
+    cl.sync();  // (B) rows j and p read everywhere
+    const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), rp_old[s]);
+    if (rank == op && p != j)
+      for (int c = tid; c < jb; c += CK_NT) P[(p - r0) + (size_t)c * rc] = rj_old[c];
+    for (int c = tid; c < jb; c += CK_NT) rowj[c] = c == s ? dinv : cmul(rp_old[c], dinv);
+    __syncthreads();
+    for (int i = tid; i < nr; i += CK_NT) fcol[i] = P[i + (size_t)s * rc];
+    __syncthreads();
+    for (int e = tid; e < nr * jb; e += CK_NT) {
+      const int i = e % nr, c = e / nr;
+      const int gi = r0 + i;
+      cplx* x = P + i + (size_t)c * rc;
+      if (gi == j) {
+        *x = rowj[c];
+      } else {
+        const cplx f = fcol[i];
+        *x = c == s ? cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x)) : cfms(f, rowj[c], *x);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nr * jb; e += CK_NT) {
+    const int i = e % nr, c = e / nr, gi = r0 + i;
+    const cplx v = P[i + (size_t)c * rc];
+    t.A[gi + (size_t)(j0 + c) * t.lda] = v;
+    t.Am[gi + (size_t)c * n] = gi == j0 + c ? cmk(v.x - 1.0, v.y) : v;
+  }
+}
+
 // Apply the panel's interchanges to every column outside J and gather their rows J into Y
 // (jb × n, ld nb).  grid (ceil(n/128), ntasks).
 __global__ void k_gj_swap(const GjTask* __restrict__ tasks, int j0, int nb) {
@@ -1310,6 +1395,17 @@ void launch_gj_panel(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_s
   FMMLU_LAUNCH();
 }
 
+int gj_panel_cluster_size(int nmax, int nb) {
+  for (int CL = 1; CL <= 16; CL *= 2) {
+    const size_t rc = (nmax + CL - 1) / CL;
+    if (rc * (nb + 1) * sizeof(cplx) + 64 <= 200 * 1024) return CL;
+  }
+  return 0;
+}
+
+void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st,
+                             int nmax);
+
 void launch_gj_swap(const GjTask* d_tasks, int ntasks, int j0, int nb, cudaStream_t st, int nmax) {
   if (ntasks <= 0) return;
   dim3 grid((nmax + 127) / 128, ntasks);
@@ -1363,6 +1459,17 @@ void launch_cluster(K kern, int CL, int ny, size_t smem, cudaStream_t st, Args..
   FMMLU_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 }  // namespace
+
+void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st,
+                             int nmax) {
+  if (ntasks <= 0) return;
+  const int CL = gj_panel_cluster_size(nmax, nb);
+  if (CL == 0) throw Error(-6, "root block too large for the cluster Gauss-Jordan panel");
+  const size_t rc = (nmax + CL - 1) / CL;
+  const size_t smem = rc * (nb + 1) * sizeof(cplx) + 64;
+  cluster_attrs(k_gj_panel_cluster, smem, CL);
+  launch_cluster(k_gj_panel_cluster, CL, ntasks, smem, st, d_tasks, j0, nb, d_status);
+}
 
 bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,
                        cudaStream_t st, int nmax) {

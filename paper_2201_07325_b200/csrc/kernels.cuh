@@ -82,6 +82,10 @@ struct GjTask {
 int gj_panel_width(int nmax);  // panel width nb whose n×nb panel fits shared memory
 void launch_gj_panel(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st, int nmax);
 void launch_gj_swap(const GjTask* d_tasks, int ntasks, int j0, int nb, cudaStream_t st, int nmax);
+// cluster-distributed panel (rows over ≤ 16 CTAs) for blocks too tall for one CTA's smem
+int gj_panel_cluster_size(int nmax, int nb);  // 0 = does not fit
+void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st,
+                             int nmax);
 void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, const long long* d_soff, cudaStream_t st,
                           int nmax);
 // in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
