@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(GJ_NT) k_gj(const long long* __restrict__ offs
 // → Gp, pivots;  [swap] apply the interchanges to the other columns and copy their rows J → Y;
 // [GEMM] C_out += (Gp − E_J) · Y.  After the last panel the column interchanges are undone.
 constexpr int GJP_NT = 512;
+constexpr int CK_NT = 256;  // threads per CTA of the cluster kernels
 
 __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ tasks, int j0, int nb,
                                                      int* status) {
@@ -457,7 +458,6 @@ __global__ void k_gj_copyback(const GjTask* __restrict__ tasks, const cplx* __re
 // thread-block cluster (global column g lives in CTA g % CL, local slot g / CL) and held in
 // shared memory for the whole factorization; the pivot column / Householder vector of each
 // step is published in the owner's shared memory and read by the others through DSMEM.
-constexpr int CK_NT = 256;
 
 // Gauss-Jordan inverse with partial pivoting (X_RR⁻¹ of each eliminated box): grid (CL, nmat).
 __global__ void __launch_bounds__(CK_NT) k_gj_cluster(const long long* __restrict__ offs,
