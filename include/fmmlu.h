@@ -146,6 +146,8 @@ int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
  *               1 = Householder TSQR + column-pivoted QR on the ID matrix,
  *               2 = Gram matrix + pivoted Cholesky (same pivots/rank/T as CPQR in exact
  *                   arithmetic; accurate while eps^2 >> unit roundoff)
+ *               3 = as 2 but always with the global-memory blocked pivoted Cholesky
+ *                   (the path used automatically for boxes beyond the cluster capacity)
  *   "proxy_rho" proxy-sphere radius / box side, in (sqrt(3)/2, 5/2) (reading C5; default 2.0)
  * Errors: EINVAL (unknown name or value out of range). */
 int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);

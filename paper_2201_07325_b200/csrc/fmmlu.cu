@@ -435,6 +435,85 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   keep.push_back(std::move(ib));
 }
 
+// ---------------------------------------------------------------------------- large-box pivoted Cholesky
+void pchol_big(fmmlu_handle* h, cplx* G, const std::vector<long long>& goff, long long gsz,
+               const std::vector<int>& bcol, const std::vector<int>& permoff, int* d_perm, int* d_k, double eps,
+               std::vector<DBuf>& keep) {
+  cudaStream_t st = h->stream;
+  const int nbx = (int)bcol.size();
+  const int NB = 32;
+  int bmax = 1;
+  long long cs = 0, ds = 0, is = 0;
+  for (int b : bcol) {
+    bmax = std::max(bmax, b);
+    cs += (long long)b * b + (long long)NB * b;
+    ds += b;
+    is += 2LL * b;
+  }
+  DBuf cb, db, ib, sb;
+  cb.alloc((size_t)cs * sizeof(cplx), st);
+  db.alloc((size_t)ds * sizeof(double), st);
+  ib.alloc((size_t)is * sizeof(int), st);
+  sb.alloc((size_t)nbx * sizeof(PcholState), st);
+  std::vector<PcholState> states(nbx, PcholState{0, 1, 0.0});
+  h2d(sb.p, states.data(), states.size() * sizeof(PcholState), st);
+  std::vector<PcholBig> tasks(nbx);
+  long long co = 0, dof = 0, io = 0;
+  for (int j = 0; j < nbx; ++j) {
+    PcholBig& t = tasks[j];
+    t.G = G + goff[j];
+    t.R = cb.as<cplx>() + co;
+    co += (long long)bcol[j] * bcol[j];
+    t.Rp = cb.as<cplx>() + co;
+    co += (long long)NB * bcol[j];
+    t.d = db.as<double>() + dof;
+    dof += bcol[j];
+    t.done = ib.as<int>() + io;
+    io += bcol[j];
+    t.piv = ib.as<int>() + io;
+    io += bcol[j];
+    t.state = sb.as<PcholState>() + j;
+    t.b = bcol[j];
+    t.out_off = permoff[j];
+    t.kslot = j;
+  }
+  std::vector<GemmProblem> gp;
+  std::vector<GemmTile> gt;
+  for (int j = 0; j < nbx; ++j) {
+    GemmProblem P{};
+    P.m = bcol[j];
+    P.n = bcol[j];
+    P.k = NB;
+    P.opA = kOpC;
+    P.opB = kOpN;
+    P.A = tasks[j].Rp;
+    P.lda = NB;
+    P.B = tasks[j].Rp;
+    P.ldb = NB;
+    P.C = tasks[j].G;
+    P.ldc = bcol[j];
+    P.active = &tasks[j].state->active;
+    add_gemm(gp, gt, P);
+  }
+  Stage s;
+  size_t o_t = s.add(tasks), o_p = s.add(gp), o_g = s.add(gt);
+  s.upload(st);
+  int id = h->prof.begin(FMMLU_K_CPQR, st);
+  for (int j0 = 0; j0 < bmax; j0 += NB) {
+    launch_pchol_big_panel(s.ptr<PcholBig>(o_t), nbx, NB, eps, st, bmax);
+    gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_g), (int)gt.size(), cmk(-1.0, 0.0), 0, nullptr, st);
+  }
+  launch_pchol_big_finish(s.ptr<PcholBig>(o_t), nbx, d_perm, d_k, st, bmax);
+  h->prof.end(id, st);
+  h->prof.add(FMMLU_K_CPQR, 0, 0, 2 * ((bmax + NB - 1) / NB) + 1);
+  keep.push_back(std::move(s.dev));
+  keep.push_back(std::move(cb));
+  keep.push_back(std::move(db));
+  keep.push_back(std::move(ib));
+  keep.push_back(std::move(sb));
+  (void)gsz;
+}
+
 // ---------------------------------------------------------------------------- cluster TSQR
 // Only R of M = Q R is needed (CPQR(R) selects the same pivots and T as CPQR(M): Qᴴ preserves
 // column norms and inner products).  Each round splits every box matrix that does not fit one
@@ -581,6 +660,13 @@ struct LevelBSR {
     return (it == v.end() || *it != b) ? -1 : poff[a][it - v.begin()];
   }
 };
+
+template <class J>
+std::vector<int> jobs_permoff(const std::vector<J>& jobs) {
+  std::vector<int> v;
+  for (auto& x : jobs) v.push_back(x.permoff);
+  return v;
+}
 
 void factor_impl(fmmlu_handle* h, double k, double eps) {
   cudaStream_t st = h->stream;
@@ -922,7 +1008,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         // ID mode: at ε ≥ 1e-7 the pivoted Cholesky of G = MᴴM gives the
         // CPQR pivots/rank/T to ~u·cond accuracy (ε² ≫ u); tighter ε uses Householder TSQR.
         lap(9);
-        const bool gram = h->id_mode == 2 || (h->id_mode == 0 && eps >= 1e-7);
+        const bool gram = h->id_mode >= 2 || (h->id_mode == 0 && eps >= 1e-7);
         std::vector<ClusterQrTask> cq(nj);
         DBuf G;
         bool done_id = false;
@@ -967,7 +1053,12 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           s2.upload(st);
           int cid = h->prof.begin(FMMLU_K_CPQR, st);
           lap(11);
-          done_id = launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd.as<int>(), kd.as<int>(), eps, st, bmax);
+          done_id = h->id_mode != 3 &&
+                    launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd.as<int>(), kd.as<int>(), eps, st, bmax);
+          if (!done_id) {  // boxes too large for a cluster: global-memory blocked pivoted Cholesky
+            pchol_big(h, G.as<cplx>(), goff, gsz, bcol, jobs_permoff(jobs), permd.as<int>(), kd.as<int>(), eps, keep);
+            done_id = true;
+          }
           lap(12);
           if (done_id) launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
           h->prof.end(cid, st);
@@ -1744,7 +1835,8 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
   if (!h || !name) return fail(FMMLU_EINVAL, "NULL argument");
   std::string k(name);
   if (k == "id_mode") {
-    if (value != 0 && value != 1 && value != 2) return fail(FMMLU_EINVAL, "id_mode must be 0, 1 or 2");
+    if (value != 0 && value != 1 && value != 2 && value != 3)
+      return fail(FMMLU_EINVAL, "id_mode must be 0, 1, 2 or 3");
     h->id_mode = (int)value;
   } else if (k == "proxy_rho") {
     if (!(value > 0.87 && value < 2.5)) return fail(FMMLU_EINVAL, "proxy_rho must lie in (0.87, 2.5)");

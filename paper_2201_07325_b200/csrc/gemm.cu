@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
   cplx* Bs = As + 2 * BK * PADA;                     // [2][BK][PADB]
   const GemmTile T = tiles[blockIdx.x];
   const GemmProblem P = probs[T.p];
+  if (P.active != nullptr && *P.active == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // 2 × 4 warps

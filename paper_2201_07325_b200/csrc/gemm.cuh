@@ -31,6 +31,7 @@ struct GemmProblem {
   const int* bld;
   int kchunk;  // split-K: each tile covers K range [ks*kchunk, (ks+1)*kchunk); 0 = whole K.
                // With split-K the kStore epilogue accumulates with fp64 atomics.
+  const int* active;  // optional device flag: tile is skipped when *active == 0
 };
 
 struct GemmTile {

@@ -832,6 +832,109 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
 }
 
+// Pivoted Cholesky for large boxes (b beyond the cluster capacity), G and R in global memory.
+// Per panel of nb pivots (one CTA per box, left-looking within the panel):
+//   p = argmax of the Schur-complement diagonal d over unpivoted columns (ties → lowest),
+//   stop when d_p ≤ ε²·d0 (reading C9);  s = G[:, p] − Σ_{panel rows i<jj} conj(Rp[i,:]) Rp[i,p];
+//   R_{j,c} = s_c / √d_p,  d_c −= |R_{j,c}|².
+// The host then applies G −= Rpᴴ Rp (rank-nb, DMMA GEMM, skipped once the box has stopped).
+__global__ void __launch_bounds__(1024) k_pchol_big_panel(const PcholBig* __restrict__ tasks, int nb, double eps) {
+  extern __shared__ double shm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  const PcholBig t = tasks[blockIdx.x];
+  PcholState* S = t.state;
+  if (!S->active) return;
+  const int b = t.b;
+  double* d = shm;                                   // b
+  int* done = reinterpret_cast<int*>(d + b);         // b
+  const int tid = threadIdx.x;
+  int j = S->j;
+  if (j == 0) {  // first panel: diagonal of G
+    for (int c = tid; c < b; c += 1024) {
+      t.d[c] = t.G[c + (size_t)c * b].x;
+      t.done[c] = 0;
+    }
+    __syncthreads();
+  }
+  for (int c = tid; c < b; c += 1024) {
+    d[c] = t.d[c];
+    done[c] = t.done[c];
+  }
+  for (int e = tid; e < nb * b; e += 1024) t.Rp[e] = cmk(0.0, 0.0);
+  __syncthreads();
+  double d0 = S->d0;
+  int stopped = 0;
+  for (int jj = 0; jj < nb && j < b; ++jj, ++j) {
+    double pv = -1.0;
+    int p = INT_MAX;
+    for (int c = tid; c < b; c += 1024)
+      if (!done[c]) argmax_merge(pv, p, d[c], c);
+    block_argmax<1024>(pv, p, red_v, red_i);
+    if (j == 0) d0 = pv;
+    if (!(pv > eps * eps * d0) || !(pv > 0.0)) {
+      stopped = 1;
+      break;
+    }
+    const double sd = sqrt(pv), isd = 1.0 / sd;
+    for (int c = tid; c < b; c += 1024) {
+      if (c == p) {
+        t.R[j + (size_t)c * b] = cmk(sd, 0.0);
+        t.Rp[jj + (size_t)c * nb] = cmk(sd, 0.0);
+        continue;
+      }
+      if (done[c]) continue;
+      // S_{c,p} = G[c,p] − Σ_i conj(R_ic) R_ip ;  R_{j,c} = S_{p,c}/√S_pp = conj(S_{c,p})/√S_pp
+      cplx s = t.G[c + (size_t)p * b];
+      for (int i = 0; i < jj; ++i) s = cfms(cmk(t.Rp[i + (size_t)c * nb].x, -t.Rp[i + (size_t)c * nb].y),
+                                            t.Rp[i + (size_t)p * nb], s);
+      const cplx r = cmk(s.x * isd, -s.y * isd);
+      t.R[j + (size_t)c * b] = r;
+      t.Rp[jj + (size_t)c * nb] = r;
+      d[c] -= cabs2(r);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      done[p] = 1;
+      t.piv[j] = p;
+    }
+    __syncthreads();
+  }
+  for (int c = tid; c < b; c += 1024) {
+    t.d[c] = d[c];
+    t.done[c] = done[c];
+  }
+  if (tid == 0) {
+    S->j = j;
+    S->d0 = d0;
+    if (stopped || j >= b) S->active = 0;
+  }
+}
+
+// R' (pivot columns first, then the redundant ones ascending; zeros below the diagonal of the
+// pivot block) over G, perm and k.  One CTA per box.
+__global__ void k_pchol_big_finish(const PcholBig* __restrict__ tasks, int* __restrict__ perm_out,
+                                   int* __restrict__ k_out) {
+  extern __shared__ int pm[];  // posmap, b
+  const PcholBig t = tasks[blockIdx.x];
+  const int b = t.b, kk = t.state->j;
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < b; ++g) pm[g] = -1;
+    for (int q = 0; q < kk; ++q) pm[t.piv[q]] = q;
+    int c = kk;
+    for (int g = 0; g < b; ++g)
+      if (pm[g] < 0) pm[g] = c++;
+  }
+  __syncthreads();
+  for (long long e = threadIdx.x; e < (long long)kk * b; e += blockDim.x) {
+    const int i = (int)(e % kk), g = (int)(e / kk);
+    const int c = pm[g];
+    t.G[i + (size_t)c * b] = (c < kk && i > c) ? cmk(0.0, 0.0) : t.R[i + (size_t)g * b];
+  }
+  for (int g = threadIdx.x; g < b; g += blockDim.x) perm_out[t.out_off + pm[g]] = g;
+  if (threadIdx.x == 0) k_out[t.kslot] = kk;
+}
+
 // Cooperative Gauss-Jordan inverse (root block D_t⁻¹): columns are
 // owned round-robin by the CTAs; one grid barrier per elimination step.  Output to B
 // (column permutation undone out-of-place).
@@ -1469,6 +1572,31 @@ void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, 
   const size_t smem = rc * (nb + 1) * sizeof(cplx) + 64;
   cluster_attrs(k_gj_panel_cluster, smem, CL);
   launch_cluster(k_gj_panel_cluster, CL, ntasks, smem, st, d_tasks, j0, nb, d_status);
+}
+
+void launch_pchol_big_panel(const PcholBig* d_tasks, int ntasks, int nb, double eps, cudaStream_t st, int bmax) {
+  if (ntasks <= 0) return;
+  const size_t smem = (size_t)bmax * (sizeof(double) + sizeof(int)) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_big_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  k_pchol_big_panel<<<ntasks, 1024, smem, st>>>(d_tasks, nb, eps);
+  FMMLU_LAUNCH();
+}
+
+void launch_pchol_big_finish(const PcholBig* d_tasks, int ntasks, int* perm_out, int* k_out, cudaStream_t st,
+                             int bmax) {
+  if (ntasks <= 0) return;
+  const size_t smem = (size_t)bmax * sizeof(int) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_big_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  k_pchol_big_finish<<<ntasks, 512, smem, st>>>(d_tasks, perm_out, k_out);
+  FMMLU_LAUNCH();
 }
 
 bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,

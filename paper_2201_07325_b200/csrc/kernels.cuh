@@ -115,6 +115,25 @@ void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int
 // (R' over G with ld b).  false if b is too large for a 16-CTA cluster.
 bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
                           cudaStream_t st, int bmax);
+// Global-memory blocked pivoted Cholesky for boxes beyond the cluster capacity.
+struct PcholState {
+  int j;       // pivots taken so far
+  int active;  // 0 once the ε stop rule fired (or all columns pivoted)
+  double d0;   // largest initial diagonal (‖M_c‖² max)
+};
+struct PcholBig {
+  cplx* G;     // b × b Gram matrix (ld b); receives R' at the end
+  cplx* R;     // b × b: R rows by natural column
+  cplx* Rp;    // nb × b: the current panel's R rows
+  double* d;   // b: Schur-complement diagonal
+  int* done;   // b
+  int* piv;    // b
+  PcholState* state;
+  int b, out_off, kslot, pad;
+};
+void launch_pchol_big_panel(const PcholBig* d_tasks, int ntasks, int nb, double eps, cudaStream_t st, int bmax);
+void launch_pchol_big_finish(const PcholBig* d_tasks, int ntasks, int* perm_out, int* k_out, cudaStream_t st,
+                             int bmax);
 // cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
 void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
 // solve sweeps for one (level, colour) phase

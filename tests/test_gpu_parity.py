@@ -153,9 +153,10 @@ def test_cfg2_full_size_residual(F):
         assert np.max(np.abs(yi - Ax[i])) <= 1e-11 * np.max(np.abs(yi)) + 1e-13
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_id_modes_parity(F, mode):
-    """Both ID paths (1: Householder TSQR + CPQR, 2: Gram + pivoted Cholesky) match the oracle."""
+    """All ID paths (1: Householder TSQR + CPQR, 2: Gram + cluster pivoted Cholesky, 3: Gram + global-memory
+    blocked pivoted Cholesky) match the oracle."""
     g = fi.ellipsoid(3000)
     k, eps = 2 * math.pi, 1e-6
     b = fi.gaussian_rhs(g.n, 2, 4)
