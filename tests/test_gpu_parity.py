@@ -172,3 +172,24 @@ def test_id_modes_parity(F, mode):
     for lvl, s in f.stats["levels"].items():
         ro = int(s["ranks"].sum())
         assert abs(st["ranks_sum"][lvl] - ro) <= 0.03 * ro + 2
+
+
+@pytest.mark.parametrize("name,nrhs", [("cfg3", 16), ("cfg5", 4)])
+def test_large_configs_full_size_residual(F, name, nrhs):
+    """BASELINE configs[2] (multiscale bump sphere, 100k, 12 levels) and configs[4] (wavy torus,
+    10⁶): residual ‖Ax−b‖/‖b‖ ≤ 10ε with the GPU brute-force matvec, whose rows are checked
+    one by one against the oracle kernel (the dense oracle cannot run at these sizes)."""
+    c = fi.CONFIGS[name]
+    g = fi.config_geometry(name)
+    b = fi.gaussian_rhs(g.n, nrhs, 0)
+    h, x = _gpu_solve(F, g, c["k"], c["eps"], c["leaf_max"], b)
+    st = h.stats()
+    assert st["n_eliminated"] > 0 and st["n0"] < g.n // 10
+    Ax = h.matvec(c["k"], x)
+    res = np.max(np.linalg.norm(Ax - b, axis=0) / np.linalg.norm(b, axis=0))
+    assert res <= 10 * c["eps"], res
+    for i in np.random.default_rng(2).choice(g.n, 6, replace=False):
+        Ki = okern.combined_field(c["k"], g.points[i:i + 1], g.points, g.normals)[0]
+        Ki[i] = 0.0
+        yi = (Ki * g.weights) @ x + 0.5 * x[i]
+        assert np.max(np.abs(yi - Ax[i])) <= 1e-11 * np.max(np.abs(yi)) + 1e-13
