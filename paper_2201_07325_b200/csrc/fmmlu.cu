@@ -979,6 +979,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (maps.empty()) maps.push_back(0);
         if (gidx.empty()) gidx.push_back(0);
         Stage s;
+        split_copy_tasks(cps);
         size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_g = s.add(gidx);
         s.upload(st);
         lap(8);
@@ -1060,7 +1061,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             done_id = true;
           }
           lap(12);
-          if (done_id) launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
+          if (done_id) launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st, bmax);
           h->prof.end(cid, st);
           h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
           keep.push_back(std::move(s2.dev));
@@ -1085,7 +1086,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           int cid = h->prof.begin(FMMLU_K_CPQR, st);
           launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st,
                              mrows.data(), bcol.data());
-          launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st);
+          launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st, bmax);
           h->prof.end(cid, st);
           h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
           keep.push_back(std::move(s2.dev));
@@ -1296,6 +1297,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (ftab.empty()) ftab.push_back(-1);
         if (fbld.empty()) fbld.push_back(0);
         Stage s;
+        split_copy_tasks(cps);
+        split_copy_tasks(cpsT);
+        split_copy_tasks(cpsX);
         size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_fs = s.add(fslot),
                o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
                o_rec = s.add(recs);

@@ -88,6 +88,34 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Cluster-wide argmax of the per-CTA candidates (cand_v, cand_i live in every CTA's shared
+// memory): lane r of warp 0 reads rank r's candidate through DSMEM, warp-reduces (ties → lowest
+// index), and broadcasts through (ov, oi).  Call after the cluster barrier that publishes them.
+__device__ __forceinline__ void cluster_argmax(cg::cluster_group& cl, int CL, double* cand_v, int* cand_i,
+                                               double* ov, int* oi, double& pv, int& p) {
+  if (threadIdx.x < 32) {
+    double v = -1.0;
+    int i = INT_MAX;
+    if ((int)threadIdx.x < CL) {
+      v = *cl.map_shared_rank(cand_v, threadIdx.x);
+      i = *cl.map_shared_rank(cand_i, threadIdx.x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+      argmax_merge(v, i, v2, i2);
+    }
+    if (threadIdx.x == 0) {
+      *ov = v;
+      *oi = i;
+    }
+  }
+  __syncthreads();
+  pv = *ov;
+  p = *oi;
+}
+
 // ------------------------------------------------------------------ block builder
 __global__ void k_build(const BuildTask* __restrict__ tasks, const int* __restrict__ gidx,
                         const int* __restrict__ slot, const int* __restrict__ pos,
@@ -121,7 +149,7 @@ __global__ void k_copy(const CopyTask* __restrict__ tasks, const int* __restrict
     const int ri = t.rmap_off >= 0 ? maps[t.rmap_off + i] : i;
     const int cj = t.cmap_off >= 0 ? maps[t.cmap_off + j] : j;
     cplx v = t.trans ? src[t.src + cj + (size_t)ri * t.lds] : src[t.src + ri + (size_t)cj * t.lds];
-    if (t.tri && i > j) v = cmk(0.0, 0.0);
+    if (t.tri && i + t.ti > j + t.tj) v = cmk(0.0, 0.0);
     dst[t.dst + i + (size_t)j * t.ldd] = v;
   }
 }
@@ -156,26 +184,29 @@ __global__ void k_proxy(const ProxyTask* __restrict__ tasks, const int* __restri
 constexpr int QR_NT = 512;
 
 // T = R11⁻¹ R12, warp per column, back substitution.
-__global__ void k_trsm_T(const IdTask* __restrict__ tasks, const int* __restrict__ kv,
-                         const cplx* __restrict__ ws, cplx* __restrict__ tarena) {
+// grid (ntasks, ceil(bmax / 16)), 16 warps: one redundant column per warp, x staged in shared memory.
+__global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks, const int* __restrict__ kv,
+                                                const cplx* __restrict__ ws, cplx* __restrict__ tarena) {
+  extern __shared__ double shm[];
   const IdTask t = tasks[blockIdx.x];
   const int kk = kv[blockIdx.x];
   const int r = t.b - kk, m = t.m;
   const cplx* M = t.Mp;
   cplx* T = tarena + t.T;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = warp; c < r; c += nw) {
-    cplx* x = T + (size_t)c * kk;
-    for (int i = lane; i < kk; i += 32) x[i] = M[i + (size_t)(kk + c) * m];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y * 16 + warp;
+  if (c >= r) return;
+  cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)warp * kk;
+  for (int i = lane; i < kk; i += 32) x[i] = M[i + (size_t)(kk + c) * m];
+  __syncwarp();
+  for (int l = kk - 1; l >= 0; --l) {
+    const cplx xl = cdiv(x[l], M[l + (size_t)l * m]);
     __syncwarp();
-    for (int l = kk - 1; l >= 0; --l) {
-      const cplx xl = cdiv(x[l], M[l + (size_t)l * m]);
-      __syncwarp();
-      if (lane == 0) x[l] = xl;
-      for (int i = lane; i < l; i += 32) x[i] = cfms(M[i + (size_t)l * m], xl, x[i]);
-      __syncwarp();
-    }
+    if (lane == 0) x[l] = xl;
+    for (int i = lane; i < l; i += 32) x[i] = cfms(M[i + (size_t)l * m], xl, x[i]);
+    __syncwarp();
   }
+  for (int i = lane; i < kk; i += 32) T[i + (size_t)c * kk] = x[i];
 }
 
 // ------------------------------------------------------------------ Gauss-Jordan inverse
@@ -319,8 +350,8 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
   extern __shared__ double shm[];
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  __shared__ double cand_v;
-  __shared__ int cand_i;
+  __shared__ double cand_v, cres_v;
+  __shared__ int cand_i, cres_i;
   __shared__ cplx rj_old[64], rp_old[64], rowj[64];
   const GjTask t = tasks[blockIdx.y];
   const int n = t.n;
@@ -347,10 +378,7 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
       cand_i = p;
     }
     cl.sync();  // (A)
-    pv = -1.0;
-    p = INT_MAX;
-    for (int r = 0; r < CL; ++r)
-      argmax_merge(pv, p, *cl.map_shared_rank(&cand_v, r), *cl.map_shared_rank(&cand_i, r));
+    cluster_argmax(cl, CL, &cand_v, &cand_i, &cres_v, &cres_i, pv, p);
     const bool sing = !(pv > 0.0);
     if (sing) p = j;
     if (rank == 0 && tid == 0) {
@@ -576,8 +604,8 @@ __global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __re
   extern __shared__ double shm[];
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  __shared__ double cand_v;
-  __shared__ int cand_i;
+  __shared__ double cand_v, cres_v;
+  __shared__ int cand_i, cres_i;
   __shared__ double hmeta[2][4];  // [parity] {u0.re, u0.im, tau, -}
   const ClusterQrTask t = tasks[blockIdx.y];
   const int m = t.m, b = t.b;
@@ -625,10 +653,7 @@ __global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __re
         cand_i = p;
       }
       cl.sync();  // (A) candidates published
-      pv = -1.0;
-      p = INT_MAX;
-      for (int r = 0; r < CL; ++r)
-        argmax_merge(pv, p, *cl.map_shared_rank(&cand_v, r), *cl.map_shared_rank(&cand_i, r));
+      cluster_argmax(cl, CL, &cand_v, &cand_i, &cres_v, &cres_i, pv, p);
       if (j == 0) norm0 = pv;
       if (!(pv > eps * norm0) || pv == 0.0) {
         kk = j;
@@ -744,8 +769,8 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   extern __shared__ double shm[];
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  __shared__ double cand_v;
-  __shared__ int cand_i;
+  __shared__ double cand_v, cres_v;
+  __shared__ int cand_i, cres_i;
   const ClusterQrTask t = tasks[blockIdx.y];
   const int b = t.b;
   const int ncl = (b - rank + CL - 1) / CL;
@@ -778,10 +803,7 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
       cand_i = p;
     }
     cl.sync();  // (A)
-    pv = -1.0;
-    p = INT_MAX;
-    for (int r = 0; r < CL; ++r)
-      argmax_merge(pv, p, *cl.map_shared_rank(&cand_v, r), *cl.map_shared_rank(&cand_i, r));
+    cluster_argmax(cl, CL, &cand_v, &cand_i, &cres_v, &cres_i, pv, p);
     if (j == 0) d0 = pv;
     if (!(pv > eps * eps * d0) || !(pv > 0.0)) {
       kk = j;
@@ -1465,6 +1487,35 @@ void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const i
   FMMLU_LAUNCH();
 }
 
+void split_copy_tasks(std::vector<CopyTask>& v) {
+  std::vector<CopyTask> out;
+  out.reserve(v.size());
+  for (const CopyTask& t : v) {
+    if ((long long)t.rows * t.cols <= 4096) {
+      out.push_back(t);
+      continue;
+    }
+    for (int i0 = 0; i0 < t.rows; i0 += 64)
+      for (int j0 = 0; j0 < t.cols; j0 += 64) {
+        CopyTask u = t;
+        u.rows = std::min(64, t.rows - i0);
+        u.cols = std::min(64, t.cols - j0);
+        u.dst = t.dst + i0 + (long long)j0 * t.ldd;
+        u.ti = t.ti + i0;
+        u.tj = t.tj + j0;
+        if (!t.trans) {
+          if (t.rmap_off >= 0) u.rmap_off = t.rmap_off + i0; else u.src += i0;
+          if (t.cmap_off >= 0) u.cmap_off = t.cmap_off + j0; else u.src += (long long)j0 * t.lds;
+        } else {
+          if (t.rmap_off >= 0) u.rmap_off = t.rmap_off + i0; else u.src += (long long)i0 * t.lds;
+          if (t.cmap_off >= 0) u.cmap_off = t.cmap_off + j0; else u.src += j0;
+        }
+        out.push_back(u);
+      }
+  }
+  v.swap(out);
+}
+
 void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cplx* src_arena,
                  cplx* dst_arena, cudaStream_t st) {
   if (ntasks <= 0) return;
@@ -1669,9 +1720,16 @@ void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int
 }
 
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
-                   cplx* tarena, cudaStream_t st) {
+                   cplx* tarena, cudaStream_t st, int bmax) {
   if (ntasks <= 0) return;
-  k_trsm_T<<<ntasks, 512, 0, st>>>(d_tasks, d_k, ws, tarena);
+  const size_t smem = 16 * (size_t)bmax * sizeof(cplx) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_trsm_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  dim3 grid(ntasks, (bmax + 15) / 16);
+  k_trsm_T<<<grid, 512, smem, st>>>(d_tasks, d_k, ws, tarena);
   FMMLU_LAUNCH();
 }
 

@@ -2,6 +2,8 @@
 #pragma once
 #include "common.cuh"
 
+#include <vector>
+
 namespace fmmlu {
 
 // Gather-or-generate one dense block of the current scaled matrix Ã.
@@ -29,7 +31,10 @@ struct CopyTask {
   int trans;
   int rmap_off, cmap_off;
   int tri;             // 1: zero the strictly-lower part of dst (upper-triangular R copies)
+  int ti, tj;          // tile origin within the original block (for the tri test)
 };
+// Split copy tasks larger than 64×64 into 64×64 tiles (load balance across CTAs).
+void split_copy_tasks(std::vector<CopyTask>& v);
 
 // Proxy rows of M (§5.1.3; readings C3-C5): rows row0 .. row0+nγ-1 hold
 // s_γ K(y_ℓ, x_j) √w_j (outgoing, combined field with the box normals), rows row0+nγ ..
@@ -70,7 +75,7 @@ void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cpl
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
                   double k, cudaStream_t st);
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
-                   cplx* tarena, cudaStream_t st);
+                   cplx* tarena, cudaStream_t st, int bmax);
 // Blocked in-place Gauss-Jordan inverse (partial pivoting) of a batch of matrices.
 struct GjTask {
   cplx* A;   // n × n, ld lda, inverted in place
