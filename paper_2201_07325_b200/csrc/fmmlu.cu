@@ -648,6 +648,8 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
 struct LevelBSR {
   int level = -1;
   const LevelTopo* tp = nullptr;
+  LevelMeta meta{};   // device CSR of the level (kept for the next level's carry-over lookups)
+  DBuf meta_buf;
   std::vector<std::vector<int>> act;        // actives at level start (sorted), per local owner
   std::vector<std::vector<long long>> poff; // complex offset of block (a, nb[a][i])
   DBuf bsr;
@@ -750,80 +752,69 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     lap(0);
     // ---- build the level's BSR (kernel entries, or carried-over Schur-updated values)
     {
-      std::vector<int> gidx, slot, pos, bld, rowoff(no);
-      std::vector<long long> tab;
-      std::vector<std::vector<int>> slots_of(no);  // prev-level owners (local) per slot
+      // host: flatten the level into CSR arrays (no per-pair tables; lookups happen on the device)
+      std::vector<int> actoff(no + 1, 0), gidx, slot, pos, nbptr(no + 1, 0), nbidx, slptr(no + 1, 0), sllist, pair_a;
+      std::vector<long long> poffv;
+      std::vector<int2> tasks;
+      for (int a = 0; a < no; ++a) actoff[a + 1] = actoff[a] + (int)cur.act[a].size();
+      gidx.reserve(actoff[no]);
+      slot.reserve(actoff[no]);
+      pos.reserve(actoff[no]);
       for (int a = 0; a < no; ++a) {
-        rowoff[a] = (int)gidx.size();
+        const int s0 = (int)sllist.size();
         for (int g : cur.act[a]) {
           gidx.push_back(g);
-          int po = prev.level >= 0 ? prevOwner[g] : -1;
-          int s = -1;
+          const int po = prev.level >= 0 ? prevOwner[g] : -1;
+          int sidx = -1;
           if (po >= 0) {
-            auto& sl = slots_of[a];
-            auto it = std::find(sl.begin(), sl.end(), po);
-            if (it == sl.end()) {
-              sl.push_back(po);
-              s = (int)sl.size() - 1;
-            } else {
-              s = (int)(it - sl.begin());
+            for (int q = s0; q < (int)sllist.size(); ++q)
+              if (sllist[q] == po) {
+                sidx = q - s0;
+                break;
+              }
+            if (sidx < 0) {
+              sllist.push_back(po);
+              sidx = (int)sllist.size() - 1 - s0;
             }
           }
-          slot.push_back(s);
+          slot.push_back(sidx);
           pos.push_back(po >= 0 ? prevPos[g] : 0);
         }
-      }
-      std::vector<int> bldoff(no);
-      for (int a = 0; a < no; ++a) {
-        bldoff[a] = (int)bld.size();
-        for (int po : slots_of[a]) bld.push_back((int)prev.act[po].size());
-        if (slots_of[a].empty()) bld.push_back(0);
-      }
-      std::vector<BuildTask> tasks;
-      for (int a = 0; a < no; ++a)
-        for (int b : nb[a]) {
-          int ra = (int)cur.act[a].size(), cb = (int)cur.act[b].size();
-          if (ra == 0 || cb == 0) continue;
-          int ns = std::max<int>(1, (int)std::max(slots_of[a].size(), slots_of[b].size()));
-          int toff = (int)tab.size();
-          tab.resize(tab.size() + (size_t)ns * ns, -1);
-          for (size_t i = 0; i < slots_of[a].size(); ++i)
-            for (size_t j = 0; j < slots_of[b].size(); ++j)
-              tab[toff + i * ns + j] = prev.off(slots_of[a][i], slots_of[b][j]);
-          long long dst = cur.off(a, b);
-          for (int i0 = 0; i0 < ra; i0 += kTile)
-            for (int j0 = 0; j0 < cb; j0 += kTile) {
-              BuildTask t;
-              t.dst = dst;
-              t.ldd = ra;
-              t.rows_off = rowoff[a];
-              t.cols_off = rowoff[b];
-              t.i0 = i0;
-              t.j0 = j0;
-              t.ni = std::min(kTile, ra - i0);
-              t.nj = std::min(kTile, cb - j0);
-              t.ns = ns;
-              t.tab_off = toff;
-              t.bld_off = bldoff[a];
-              tasks.push_back(t);
-            }
+        slptr[a + 1] = (int)sllist.size();
+        for (size_t i = 0; i < nb[a].size(); ++i) {
+          const int b = nb[a][i];
+          const int p = (int)nbidx.size();
+          nbidx.push_back(b);
+          poffv.push_back(cur.poff[a][i]);
+          pair_a.push_back(a);
+          const int ra = (int)cur.act[a].size(), cb = (int)cur.act[b].size();
+          const int nt = ((ra + 63) / 64) * ((cb + 63) / 64);
+          for (int q = 0; q < nt; ++q) tasks.push_back(make_int2(p, q));
         }
-      if (tab.empty()) tab.push_back(-1);
+        nbptr[a + 1] = (int)nbidx.size();
+      }
+      for (std::vector<int>* v : {&gidx, &slot, &pos, &nbidx, &sllist, &pair_a})
+        if (v->empty()) v->push_back(0);
+      if (poffv.empty()) poffv.push_back(0);
       Stage s;
-      size_t o_t = s.add(tasks), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_tab = s.add(tab),
-             o_b = s.add(bld);
+      size_t o_ao = s.add(actoff), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_np = s.add(nbptr),
+             o_ni = s.add(nbidx), o_po = s.add(poffv), o_sp = s.add(slptr), o_sl = s.add(sllist),
+             o_pa = s.add(pair_a), o_t = s.add(tasks);
       s.upload(st);
+      cur.meta = LevelMeta{s.ptr<int>(o_ao), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p), s.ptr<int>(o_np),
+                           s.ptr<int>(o_ni), s.ptr<long long>(o_po), s.ptr<int>(o_sp), s.ptr<int>(o_sl)};
       int bid = h->prof.begin(FMMLU_K_BUILD, st);
-      launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
-                   s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), cur.bsr.as<cplx>(), h->g, k, st);
+      launch_build_level(s.ptr<int2>(o_t), (int)tasks.size(), s.ptr<int>(o_pa), cur.meta, prev.meta,
+                         prev.level >= 0 ? 1 : 0, prev.bsr.as<cplx>(), cur.bsr.as<cplx>(), h->g, k, st);
       h->prof.end(bid, st);
       h->prof.add(FMMLU_K_BUILD, 60.0 * cur.size, 16.0 * cur.size, 1);
-      keep.push_back(std::move(s.dev));
+      cur.meta_buf = std::move(s.dev);
     }
     if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
     prev.bsr.release();
 
-    // current actives (positions within the level-start actives)
+    // current actives (positions within the level-start actives); ident[a]: still all of them
+    std::vector<char> ident(no, 1);
     std::vector<std::vector<int>> curpos(no);
     for (int a = 0; a < no; ++a) {
       curpos[a].resize(cur.act[a].size());
@@ -919,8 +910,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         for (auto& J : jobs) {
           int row = 0;
           for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
-            int mo = (int)maps.size();
-            maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+            int mo = -1;
+            if (!ident[q]) {
+              mo = (int)maps.size();
+              maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+            }
             CopyTask c{};
             c.src = cur.off(q, J.a);
             c.lds = (int)cur.act[q].size();
@@ -935,8 +929,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             row += c.rows;
           }
           for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
-            int mo = (int)maps.size();
-            maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+            int mo = -1;
+            if (!ident[q]) {
+              mo = (int)maps.size();
+              maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+            }
             CopyTask c{};
             c.src = cur.off(J.a, q);
             c.lds = J.b;
@@ -1213,8 +1210,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           cps.push_back(c);
           int noff = 0;
           for (int o : J.N) {
-            int mo = (int)maps.size();
-            maps.insert(maps.end(), curpos[o].begin(), curpos[o].end());
+            int mo = -1;
+            if (!ident[o]) {
+              mo = (int)maps.size();
+              maps.insert(maps.end(), curpos[o].begin(), curpos[o].end());
+            }
             int no_ = (int)curpos[o].size();
             for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
             CopyTask a{};
@@ -1479,6 +1479,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::sort(sk.begin(), sk.end());
         total_active -= (J.b - J.k);
         curpos[J.a] = sk;
+        ident[J.a] = 0;
       }
       track(h, -(long long)Tb.bytes);
       Tb.release();

@@ -139,6 +139,57 @@ __global__ void k_build(const BuildTask* __restrict__ tasks, const int* __restri
   }
 }
 
+__global__ void __launch_bounds__(256) k_build_level(const int2* __restrict__ tasks, const int* __restrict__ pair_a,
+                                                     LevelMeta cur, LevelMeta prev, int has_prev,
+                                                     const cplx* __restrict__ src, cplx* __restrict__ dst, Geo g,
+                                                     double k) {
+  __shared__ long long tab[64];
+  __shared__ int bld[8];
+  const int2 t = tasks[blockIdx.x];
+  const int p = t.x;
+  const int a = pair_a[p], b = cur.nbidx[p];
+  const int ra0 = cur.actoff[a], rb0 = cur.actoff[b];
+  const int ra = cur.actoff[a + 1] - ra0, cb = cur.actoff[b + 1] - rb0;
+  const int ntr = (ra + 63) / 64;
+  const int i0 = (t.y % ntr) * 64, j0 = (t.y / ntr) * 64;
+  const int ni = min(64, ra - i0), nj = min(64, cb - j0);
+  const int sa0 = cur.slptr[a], sb0 = cur.slptr[b];
+  const int na = has_prev ? cur.slptr[a + 1] - sa0 : 0, nbs = has_prev ? cur.slptr[b + 1] - sb0 : 0;
+  for (int e = threadIdx.x; e < na * nbs; e += blockDim.x) {
+    const int si = e / nbs, sj = e % nbs;
+    const int pa = cur.sllist[sa0 + si], pb = cur.sllist[sb0 + sj];
+    int lo = prev.nbptr[pa], hi = prev.nbptr[pa + 1];
+    long long off = -1;
+    while (lo < hi) {  // partner lists are sorted
+      const int mid = (lo + hi) >> 1;
+      const int v = prev.nbidx[mid];
+      if (v == pb) {
+        off = prev.poff[mid];
+        break;
+      }
+      if (v < pb) lo = mid + 1; else hi = mid;
+    }
+    tab[si * 8 + sj] = off;
+  }
+  for (int si = threadIdx.x; si < na; si += blockDim.x) {
+    const int pa = cur.sllist[sa0 + si];
+    bld[si] = prev.actoff[pa + 1] - prev.actoff[pa];
+  }
+  __syncthreads();
+  cplx* out = dst + cur.poff[p];
+  for (int e = threadIdx.x; e < ni * nj; e += blockDim.x) {
+    const int i = i0 + e % ni, j = j0 + e / ni;
+    const int ri = ra0 + i, cj = rb0 + j;
+    const int si = cur.slot[ri], sj = cur.slot[cj];
+    long long off = -1;
+    if (has_prev && si >= 0 && sj >= 0) off = tab[si * 8 + sj];
+    cplx v;
+    if (off >= 0) v = src[off + cur.pos[ri] + (size_t)cur.pos[cj] * bld[si]];
+    else v = entry_scaled(g, k, cur.gidx[ri], cur.gidx[cj]);
+    out[i + (size_t)j * ra] = v;
+  }
+}
+
 // ------------------------------------------------------------------ copies
 __global__ void k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ maps,
                        const cplx* __restrict__ src, cplx* __restrict__ dst) {
@@ -1514,6 +1565,14 @@ void split_copy_tasks(std::vector<CopyTask>& v) {
       }
   }
   v.swap(out);
+}
+
+void launch_build_level(const int2* d_tasks, int ntasks, const int* d_pair_a, const LevelMeta& cur,
+                        const LevelMeta& prev, int has_prev, const cplx* src_arena, cplx* dst_arena, const Geo& g,
+                        double k, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  k_build_level<<<ntasks, 256, 0, st>>>(d_tasks, d_pair_a, cur, prev, has_prev, src_arena, dst_arena, g, k);
+  FMMLU_LAUNCH();
 }
 
 void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cplx* src_arena,

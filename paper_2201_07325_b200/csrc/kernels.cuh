@@ -21,6 +21,25 @@ struct BuildTask {
   int bld_off;             // offset into bld (ns entries, row-slot leading dims)
 };
 
+// Device-side description of one level's block store (CSR over owners).
+struct LevelMeta {
+  const int* actoff;     // no+1: prefix of active counts (rows of owner a = actoff[a+1]-actoff[a])
+  const int* gidx;       // Σ act: global tree-order index of each active
+  const int* slot;       // Σ act: slot of the active's previous-level owner in a's slot list (-1: none)
+  const int* pos;        // Σ act: position in that previous-level owner's active list
+  const int* nbptr;      // no+1: CSR row pointers of the block-pair set
+  const int* nbidx;      // #pairs: partner owner
+  const long long* poff; // #pairs: complex offset of the block in the level arena
+  const int* slptr;      // no+1: CSR of the previous-level owners each owner is made of
+  const int* sllist;
+};
+// Build every block of the level store: task = (pair, tile) with 64×64 tiles.  Each entry is the
+// carried-over value when the previous level stored the owners' child pair, else the kernel
+// entry √w_i K √w_j (½ on the diagonal).
+void launch_build_level(const int2* d_tasks, int ntasks, const int* d_pair_a, const LevelMeta& cur,
+                        const LevelMeta& prev, int has_prev, const cplx* src_arena, cplx* dst_arena, const Geo& g,
+                        double k, cudaStream_t st);
+
 // Copy a (possibly index-mapped / transposed) block.
 //   !trans: dst(i,j) = src(rm(i), cm(j));   trans: dst(i,j) = src(cm(j), rm(i))
 // rm(i) = rmap ? rmap[i] : i (rmap_off < 0 means identity), same for cm.
