@@ -607,6 +607,20 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
   tp.local.assign(T.boxes.size(), -1);
   for (int i = 0; i < no; ++i) tp.local[tp.owners[i]] = i;
   const int lim = (1 << lvl) - 1;
+  // dense cell → owner grid for moderate levels (hash lookups through the ancestors otherwise)
+  const bool dense = lvl <= 7;
+  std::vector<int> grid;
+  const int64_t side = (int64_t)1 << lvl;
+  if (dense) {
+    grid.assign((size_t)(side * side * side), -1);
+    for (int a = 0; a < no; ++a) {
+      int64_t lo[3], hi[3];
+      T.extent(tp.owners[a], lvl, lo, hi);
+      for (int64_t x = lo[0]; x <= hi[0]; ++x)
+        for (int64_t y = lo[1]; y <= hi[1]; ++y)
+          for (int64_t z = lo[2]; z <= hi[2]; ++z) grid[(size_t)((x * side + y) * side + z)] = a;
+    }
+  }
   tp.boxN.assign(nlb, {});
   tp.boxQ.assign(nlb, {});
   std::vector<std::vector<int>> pairs(no);
@@ -620,10 +634,14 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
         for (int dz = -2; dz <= 2; ++dz) {
           const int x = B.c[0] + dx, y = B.c[1] + dy, z = B.c[2] + dz;
           if (x < 0 || y < 0 || z < 0 || x > lim || y > lim || z > lim) continue;
-          const int ob = T.owner_of_cell(lvl, x, y, z);
-          if (ob < 0 || ob == box) continue;
-          const int o = tp.local[ob];
-          if (o >= 0) cand.push_back(o);
+          int o;
+          if (dense) {
+            o = grid[(size_t)(((int64_t)x * side + y) * side + z)];
+          } else {
+            const int ob = T.owner_of_cell(lvl, x, y, z);
+            o = ob >= 0 ? tp.local[ob] : -1;
+          }
+          if (o >= 0 && o != i) cand.push_back(o);
         }
     std::sort(cand.begin(), cand.end());
     cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
