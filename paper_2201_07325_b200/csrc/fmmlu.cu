@@ -741,6 +741,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       h->topo_ready[lvl] = 1;
     }
     cur.tp = &h->topo[lvl];
+    lap(14);
     for (int b : T.levels[lvl]) {
       if (!T.boxes[b].leaf()) {
         std::vector<int> u;
@@ -764,6 +765,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       }
     }
     cur.size = off;
+    lap(15);
     cur.bsr.alloc((size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
     track(h, cur.bsr.bytes);
 
@@ -1524,9 +1526,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   if (trace)
     fprintf(stderr, "[fmmlu] host ms: level-setup %.1f build-tasks %.1f phase-jobs %.1f id %.1f elim %.1f "
                     "update %.1f carry %.1f other %.1f | id: tasks %.1f gatherlaunch %.1f gram %.1f prep %.1f "
-                    "pchol %.1f rest %.1f | wait %.1f\n",
+                    "pchol %.1f rest %.1f | topo %.1f acts %.1f | wait %.1f\n",
             tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8], tr[9], tr[10], tr[11], tr[12], tr[13],
-            S.t_sync_wait_ms);
+            tr[14], tr[15], S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root
   double tr0 = now_ms();
   std::vector<int> Bt;
