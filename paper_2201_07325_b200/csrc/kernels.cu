@@ -399,11 +399,12 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  __shared__ double cand_v, cres_v;
-  __shared__ int cand_i, cres_i;
-  __shared__ cplx rj_old[64], rp_old[64], rowj[64];
+  // every CTA publishes its pivot candidate (value, row index, row values) and the owner of row
+  // j publishes old row j, all double-buffered by parity: one cluster barrier per column
+  __shared__ double cand_v[2], cres_v;
+  __shared__ int cand_i[2], cres_i;
+  __shared__ cplx pubc[2][64], pubj[2][64];
+  __shared__ cplx rowj[64], rowp_old[64], rowj_old[64];
   const GjTask t = tasks[blockIdx.y];
   const int n = t.n;
   if (j0 >= n) return;  // uniform across the cluster
@@ -417,37 +418,48 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
     const int i = e % nr, c = e / nr;
     P[i + (size_t)c * rc] = t.A[(r0 + i) + (size_t)(j0 + c) * t.lda];
   }
-  cl.sync();
+  __syncthreads();
   for (int s = 0; s < jb; ++s) {
-    const int j = j0 + s;
-    double pv = -1.0;
-    int p = INT_MAX;
-    for (int i = max(j, r0) + tid; i < r1; i += CK_NT) argmax_merge(pv, p, cabs2(P[(i - r0) + (size_t)s * rc]), i);
-    block_argmax<CK_NT>(pv, p, red_v, red_i);
-    if (tid == 0) {
-      cand_v = pv;
-      cand_i = p;
+    const int j = j0 + s, par = s & 1;
+    if (tid < 32) {
+      double pv = -1.0;
+      int p = INT_MAX;
+      for (int i = max(j, r0) + tid; i < r1; i += 32) argmax_merge(pv, p, cabs2(P[(i - r0) + (size_t)s * rc]), i);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, pv, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, p, o);
+        argmax_merge(pv, p, v2, i2);
+      }
+      if (tid == 0) {
+        cand_v[par] = pv;
+        cand_i[par] = p;
+      }
+      if (p != INT_MAX)
+        for (int c = tid; c < jb; c += 32) pubc[par][c] = P[(p - r0) + (size_t)c * rc];
+      if (j >= r0 && j < r1)
+        for (int c = tid; c < jb; c += 32) pubj[par][c] = P[(j - r0) + (size_t)c * rc];
     }
     cl.sync();  // (A)
-    cluster_argmax(cl, CL, &cand_v, &cand_i, &cres_v, &cres_i, pv, p);
+    double pv;
+    int p;
+    cluster_argmax(cl, CL, &cand_v[par], &cand_i[par], &cres_v, &cres_i, pv, p);
     const bool sing = !(pv > 0.0);
     if (sing) p = j;
     if (rank == 0 && tid == 0) {
       t.piv[j] = p;
       if (sing) atomicExch(status, 1);
     }
-    const int oj = j / rc, op = p / rc;
-    const cplx* Rj = cl.map_shared_rank(P, oj) + (j - oj * rc);
-    const cplx* Rp = cl.map_shared_rank(P, op) + (p - op * rc);
-    for (int c = tid; c < jb; c += CK_NT) {
-      rj_old[c] = Rj[(size_t)c * rc];
-      rp_old[c] = Rp[(size_t)c * rc];
+    const int oj = j / rc, op = sing ? oj : p / rc;
+    if (tid < jb) {
+      rowj_old[tid] = *(cl.map_shared_rank(&pubj[par][0], oj) + tid);
+      rowp_old[tid] = sing ? rowj_old[tid] : *(cl.map_shared_rank(&pubc[par][0], op) + tid);
     }
-    cl.sync();  // (B) rows j and p read everywhere
-    const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), rp_old[s]);
+    __syncthreads();
+    const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), rowp_old[s]);
     if (rank == op && p != j)
-      for (int c = tid; c < jb; c += CK_NT) P[(p - r0) + (size_t)c * rc] = rj_old[c];
-    for (int c = tid; c < jb; c += CK_NT) rowj[c] = c == s ? dinv : cmul(rp_old[c], dinv);
+      for (int c = tid; c < jb; c += CK_NT) P[(p - r0) + (size_t)c * rc] = rowj_old[c];
+    for (int c = tid; c < jb; c += CK_NT) rowj[c] = c == s ? dinv : cmul(rowp_old[c], dinv);
     __syncthreads();
     for (int i = tid; i < nr; i += CK_NT) fcol[i] = P[i + (size_t)s * rc];
     __syncthreads();
@@ -464,6 +476,7 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
     }
     __syncthreads();
   }
+  cl.sync();  // no CTA may exit while others still read its published buffers
   for (int e = tid; e < nr * jb; e += CK_NT) {
     const int i = e % nr, c = e / nr, gi = r0 + i;
     const cplx v = P[i + (size_t)c * rc];
@@ -820,8 +833,9 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   extern __shared__ double shm[];
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  __shared__ double cand_v, cres_v;
-  __shared__ int cand_i, cres_i;
+  __shared__ double cand_v[2], cres_v;  // candidates double-buffered by step parity: one
+  __shared__ int cand_i[2], cres_i;     // cluster barrier per step suffices
+
   const ClusterQrTask t = tasks[blockIdx.y];
   const int b = t.b;
   const int ncl = (b - rank + CL - 1) / CL;
@@ -842,19 +856,27 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   int kk = b;
   double d0 = 0.0;
   for (int j = 0; j < b; ++j) {
+    const int par = j & 1;
     double pv = -1.0;
     int p = INT_MAX;
-    for (int l = tid; l < ncl; l += CK_NT) {
-      const int g = rank + l * CL;
-      if (!done[g]) argmax_merge(pv, p, Sl[g + (size_t)l * b].x, g);
+    if (tid < 32) {  // local candidate (≤ a few dozen columns per CTA): one warp
+      for (int l = tid; l < ncl; l += 32) {
+        const int g = rank + l * CL;
+        if (!done[g]) argmax_merge(pv, p, Sl[g + (size_t)l * b].x, g);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, pv, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, p, o);
+        argmax_merge(pv, p, v2, i2);
+      }
+      if (tid == 0) {
+        cand_v[par] = pv;
+        cand_i[par] = p;
+      }
     }
-    block_argmax<CK_NT>(pv, p, red_v, red_i);
-    if (tid == 0) {
-      cand_v = pv;
-      cand_i = p;
-    }
-    cl.sync();  // (A)
-    cluster_argmax(cl, CL, &cand_v, &cand_i, &cres_v, &cres_i, pv, p);
+    cl.sync();  // (A) the only cluster barrier of the step
+    cluster_argmax(cl, CL, &cand_v[par], &cand_i[par], &cres_v, &cres_i, pv, p);
     if (j == 0) d0 = pv;
     if (!(pv > eps * eps * d0) || !(pv > 0.0)) {
       kk = j;
@@ -868,7 +890,9 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
       done[p] = 1;
     }
     for (int l = tid; l < ncl; l += CK_NT) rowp[l] = Sl[p + (size_t)l * b];
-    cl.sync();  // (B) column p and row p copied everywhere; candidates of step j consumed
+    // column p is never modified again (it is pivoted), so no second cluster barrier is needed;
+    // the local barrier orders the copies before this CTA's update
+    __syncthreads();
     const double sd = sqrt(pv), inv = 1.0 / pv, isd = 1.0 / sd;
     // R_{j,c} = S_{p,c}/√S_pp ;  S_{a,c} −= S_{a,p} S_{p,c} / S_pp  (remaining columns c)
     for (int l = tid; l < ncl; l += CK_NT) {
