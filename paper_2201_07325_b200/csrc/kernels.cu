@@ -369,15 +369,19 @@ __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ 
     const cplx d = Pc[j];
     const cplx dinv = pv > 0.0 ? cdiv(cmk(1.0, 0.0), d) : cmk(1.0, 0.0);
     for (int c = tid; c < jb; c += GJP_NT) rowj[c] = c == s ? dinv : cmul(P[j + (size_t)c * n], dinv);
-    for (int i = tid; i < n; i += GJP_NT) colf[i] = Pc[i];
     __syncthreads();
-    for (int e = tid; e < n * jb; e += GJP_NT) {
-      const int i = e % n, c = e / n;
-      cplx v;
-      if (i == j) v = rowj[c];
-      else if (c == s) v = cmk(-(colf[i].x * dinv.x - colf[i].y * dinv.y), -(colf[i].x * dinv.y + colf[i].y * dinv.x));
-      else v = cfms(colf[i], rowj[c], P[e]);
-      P[e] = v;
+    // each thread owns whole rows: reads its multiplier before overwriting it (no copy, no div/mod)
+    for (int i = tid; i < n; i += GJP_NT) {
+      if (i == j) {
+        for (int c = 0; c < jb; ++c) P[i + (size_t)c * n] = rowj[c];
+      } else {
+        const cplx f = Pc[i];
+        const cplx fs = cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x));
+        for (int c = 0; c < jb; ++c) {
+          cplx* x = P + i + (size_t)c * n;
+          *x = c == s ? fs : cfms(f, rowj[c], *x);
+        }
+      }
     }
     __syncthreads();
   }
@@ -461,17 +465,16 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
       for (int c = tid; c < jb; c += CK_NT) P[(p - r0) + (size_t)c * rc] = rowj_old[c];
     for (int c = tid; c < jb; c += CK_NT) rowj[c] = c == s ? dinv : cmul(rowp_old[c], dinv);
     __syncthreads();
-    for (int i = tid; i < nr; i += CK_NT) fcol[i] = P[i + (size_t)s * rc];
-    __syncthreads();
-    for (int e = tid; e < nr * jb; e += CK_NT) {
-      const int i = e % nr, c = e / nr;
-      const int gi = r0 + i;
-      cplx* x = P + i + (size_t)c * rc;
-      if (gi == j) {
-        *x = rowj[c];
+    for (int i = tid; i < nr; i += CK_NT) {  // own rows, whole rows per thread
+      if (r0 + i == j) {
+        for (int c = 0; c < jb; ++c) P[i + (size_t)c * rc] = rowj[c];
       } else {
-        const cplx f = fcol[i];
-        *x = c == s ? cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x)) : cfms(f, rowj[c], *x);
+        const cplx f = P[i + (size_t)s * rc];
+        const cplx fs = cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x));
+        for (int c = 0; c < jb; ++c) {
+          cplx* x = P + i + (size_t)c * rc;
+          *x = c == s ? fs : cfms(f, rowj[c], *x);
+        }
       }
     }
     __syncthreads();
@@ -835,6 +838,7 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   __shared__ int red_i[32];
   __shared__ double cand_v[2], cres_v;  // candidates double-buffered by step parity: one
   __shared__ int cand_i[2], cres_i;     // cluster barrier per step suffices
+  __shared__ char lact[128];             // local column still unpivoted (ncl ≤ 117 by the smem cap)
 
   const ClusterQrTask t = tasks[blockIdx.y];
   const int b = t.b;
@@ -900,11 +904,12 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
       if (g == p) Rg[j + (size_t)g * b] = cmk(sd, 0.0);
       else if (!done[g]) Rg[j + (size_t)g * b] = cscale(rowp[l], isd);
     }
-    for (int e = tid; e < b * ncl; e += CK_NT) {
-      const int a = e % b, l = e / b;
-      const int g = rank + l * CL;
-      if (done[g]) continue;
-      Sl[e] = cfms(cscale(pc[a], inv), rowp[l], Sl[e]);
+    for (int l = tid; l < ncl; l += CK_NT) lact[l] = done[rank + l * CL] ? 0 : 1;
+    __syncthreads();
+    for (int a = tid; a < b; a += CK_NT) {  // whole rows per thread, no div/mod
+      const cplx pa = cscale(pc[a], inv);
+      for (int l = 0; l < ncl; ++l)
+        if (lact[l]) Sl[a + (size_t)l * b] = cfms(pa, rowp[l], Sl[a + (size_t)l * b]);
     }
     __syncthreads();
   }
