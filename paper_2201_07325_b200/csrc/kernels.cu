@@ -347,29 +347,39 @@ __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ 
     P[e] = t.A[i + (size_t)(j0 + c) * t.lda];
   }
   __syncthreads();
+  __shared__ cplx sdinv;
   for (int s = 0; s < jb; ++s) {
     const int j = j0 + s;
     cplx* Pc = P + (size_t)s * n;
-    double pv = -1.0;
-    int p = INT_MAX;
-    for (int i = j + tid; i < n; i += GJP_NT) argmax_merge(pv, p, cabs2(Pc[i]), i);
-    block_argmax<GJP_NT>(pv, p, red_v, red_i);
-    if (!(pv > 0.0)) {  // exactly singular: flag it and continue with a harmless identity step
-      if (tid == 0) atomicExch(status, 1);
-      p = j;
-    }
-    if (tid == 0) t.piv[j] = p;
-    if (p != j)
-      for (int c = tid; c < jb; c += GJP_NT) {
-        const cplx a = P[j + (size_t)c * n];
-        P[j + (size_t)c * n] = P[p + (size_t)c * n];
-        P[p + (size_t)c * n] = a;
+    if (tid < 32) {  // warp 0: pivot search, row interchange, scaled pivot row
+      double pv = -1.0;
+      int p = INT_MAX;
+      for (int i = j + tid; i < n; i += 32) argmax_merge(pv, p, cabs2(Pc[i]), i);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, pv, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, p, o);
+        argmax_merge(pv, p, v2, i2);
       }
+      const bool sing = !(pv > 0.0);
+      if (sing) p = j;  // exactly singular: flag it and continue with a harmless identity step
+      if (tid == 0) {
+        t.piv[j] = p;
+        if (sing) atomicExch(status, 1);
+      }
+      if (p != j)
+        for (int c = tid; c < jb; c += 32) {
+          const cplx a = P[j + (size_t)c * n];
+          P[j + (size_t)c * n] = P[p + (size_t)c * n];
+          P[p + (size_t)c * n] = a;
+        }
+      __syncwarp();
+      const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), Pc[j]);
+      for (int c = tid; c < jb; c += 32) rowj[c] = c == s ? dinv : cmul(P[j + (size_t)c * n], dinv);
+      if (tid == 0) sdinv = dinv;
+    }
     __syncthreads();
-    const cplx d = Pc[j];
-    const cplx dinv = pv > 0.0 ? cdiv(cmk(1.0, 0.0), d) : cmk(1.0, 0.0);
-    for (int c = tid; c < jb; c += GJP_NT) rowj[c] = c == s ? dinv : cmul(P[j + (size_t)c * n], dinv);
-    __syncthreads();
+    const cplx dinv = sdinv;
     // each thread owns whole rows: reads its multiplier before overwriting it (no copy, no div/mod)
     for (int i = tid; i < n; i += GJP_NT) {
       if (i == j) {
@@ -838,7 +848,6 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   __shared__ int red_i[32];
   __shared__ double cand_v[2], cres_v;  // candidates double-buffered by step parity: one
   __shared__ int cand_i[2], cres_i;     // cluster barrier per step suffices
-  __shared__ char lact[128];             // local column still unpivoted (ncl ≤ 117 by the smem cap)
 
   const ClusterQrTask t = tasks[blockIdx.y];
   const int b = t.b;
@@ -904,12 +913,14 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
       if (g == p) Rg[j + (size_t)g * b] = cmk(sd, 0.0);
       else if (!done[g]) Rg[j + (size_t)g * b] = cscale(rowp[l], isd);
     }
-    for (int l = tid; l < ncl; l += CK_NT) lact[l] = done[rank + l * CL] ? 0 : 1;
-    __syncthreads();
-    for (int a = tid; a < b; a += CK_NT) {  // whole rows per thread, no div/mod
-      const cplx pa = cscale(pc[a], inv);
-      for (int l = 0; l < ncl; ++l)
-        if (lact[l]) Sl[a + (size_t)l * b] = cfms(pa, rowp[l], Sl[a + (size_t)l * b]);
+    {  // warp per local column (balanced; the skip of pivoted columns is warp-uniform)
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int l = warp; l < ncl; l += CK_NT / 32) {
+        if (done[rank + l * CL]) continue;
+        const cplx rp = cscale(rowp[l], inv);
+        cplx* col = Sl + (size_t)l * b;
+        for (int a = lane; a < b; a += 32) col[a] = cfms(pc[a], rp, col[a]);
+      }
     }
     __syncthreads();
   }
