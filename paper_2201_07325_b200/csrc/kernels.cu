@@ -376,20 +376,21 @@ __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ 
       __syncwarp();
       const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), Pc[j]);
       for (int c = tid; c < jb; c += 32) rowj[c] = c == s ? dinv : cmul(P[j + (size_t)c * n], dinv);
+      for (int i = tid; i < n; i += 32) colf[i] = Pc[i];
       if (tid == 0) sdinv = dinv;
     }
     __syncthreads();
     const cplx dinv = sdinv;
-    // each thread owns whole rows: reads its multiplier before overwriting it (no copy, no div/mod)
-    for (int i = tid; i < n; i += GJP_NT) {
-      if (i == j) {
-        for (int c = 0; c < jb; ++c) P[i + (size_t)c * n] = rowj[c];
-      } else {
-        const cplx f = Pc[i];
-        const cplx fs = cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x));
-        for (int c = 0; c < jb; ++c) {
-          cplx* x = P + i + (size_t)c * n;
-          *x = c == s ? fs : cfms(f, rowj[c], *x);
+    {  // warp per column, lanes over rows (balanced, coalesced, no div/mod)
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int c = warp; c < jb; c += GJP_NT / 32) {
+        cplx* col = P + (size_t)c * n;
+        const cplx rc = rowj[c];
+        if (c == s) {
+          const cplx nd = cmk(-dinv.x, -dinv.y);
+          for (int i = lane; i < n; i += 32) col[i] = i == j ? rc : cmul(colf[i], nd);
+        } else {
+          for (int i = lane; i < n; i += 32) col[i] = i == j ? rc : cfms(colf[i], rc, col[i]);
         }
       }
     }
@@ -475,15 +476,19 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
       for (int c = tid; c < jb; c += CK_NT) P[(p - r0) + (size_t)c * rc] = rowj_old[c];
     for (int c = tid; c < jb; c += CK_NT) rowj[c] = c == s ? dinv : cmul(rowp_old[c], dinv);
     __syncthreads();
-    for (int i = tid; i < nr; i += CK_NT) {  // own rows, whole rows per thread
-      if (r0 + i == j) {
-        for (int c = 0; c < jb; ++c) P[i + (size_t)c * rc] = rowj[c];
-      } else {
-        const cplx f = P[i + (size_t)s * rc];
-        const cplx fs = cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x));
-        for (int c = 0; c < jb; ++c) {
-          cplx* x = P + i + (size_t)c * rc;
-          *x = c == s ? fs : cfms(f, rowj[c], *x);
+    for (int i = tid; i < nr; i += CK_NT) fcol[i] = P[i + (size_t)s * rc];
+    __syncthreads();
+    {  // warp per column over the own rows
+      const int warp = tid >> 5, lane = tid & 31;
+      const int jl = j - r0;  // local index of row j (may be outside [0, nr))
+      for (int c = warp; c < jb; c += CK_NT / 32) {
+        cplx* col = P + (size_t)c * rc;
+        const cplx rcj = rowj[c];
+        if (c == s) {
+          const cplx nd = cmk(-dinv.x, -dinv.y);
+          for (int i = lane; i < nr; i += 32) col[i] = i == jl ? rcj : cmul(fcol[i], nd);
+        } else {
+          for (int i = lane; i < nr; i += 32) col[i] = i == jl ? rcj : cfms(fcol[i], rcj, col[i]);
         }
       }
     }
