@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(objdir, f + ".o")
         _run([CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", os.path.join(CSRC, f), "-o", o])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+    _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-Xcompiler", "-pthread"])
     return LIB
 
 

@@ -16,6 +16,7 @@
 //   root: B_t dense block → X⁻¹ (L894-918)                        [k_build, k_gj_coop]
 // Solve: upward sweep over phases, root apply, downward sweep.
 #include <cuda_runtime.h>
+#include <malloc.h>
 
 #include <algorithm>
 #include <chrono>
@@ -25,6 +26,7 @@
 #include <cstring>
 #include <string>
 #include <unordered_map>
+#include <future>
 #include <vector>
 
 #include "../../include/fmmlu.h"
@@ -290,13 +292,15 @@ int proxy_count(double k, double rho, double eps) {
 
 constexpr int kTile = 64;
 
-void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, const GemmProblem& p) {
+// upper = true: only output tiles with tile-row ≤ tile-column (Hermitian results)
+void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, const GemmProblem& p,
+              bool upper = false) {
   if (p.m <= 0 || p.n <= 0 || p.k <= 0) return;
   int id = (int)probs.size();
   probs.push_back(p);
   const int nks = p.kchunk > 0 ? (p.k + p.kchunk - 1) / p.kchunk : 1;
   for (int tm = 0; tm < (p.m + kTile - 1) / kTile; ++tm)
-    for (int tn = 0; tn < (p.n + kTile - 1) / kTile; ++tn)
+    for (int tn = upper ? tm : 0; tn < (p.n + kTile - 1) / kTile; ++tn)
       for (int ks = 0; ks < nks; ++ks) tiles.push_back({id, tm, tn, ks});
 }
 
@@ -311,13 +315,16 @@ void gemm_work(const std::vector<GemmProblem>& probs, double& fl, double& by) {
 }
 
 void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cplx alpha,
-               int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep, Prof& P, int cls) {
+               int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep, Prof& P, int cls,
+               double work_scale = 1.0) {
   if (tiles.empty()) return;
   Stage s;
   size_t op = s.add(probs), ot = s.add(tiles);
   s.upload(st);
   double fl, by;
   gemm_work(probs, fl, by);
+  fl *= work_scale;  // e.g. 0.5 for Hermitian products computed on upper tiles only
+  by *= work_scale;
   int id = P.begin(cls, st);
   gemm_batched(s.ptr<GemmProblem>(op), s.ptr<GemmTile>(ot), (int)tiles.size(), alpha, scatter, bsr, st);
   P.end(id, st);
@@ -729,17 +736,20 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     tmark = t;
     wmark = w;
   };
+  // per-level topologies depend only on the tree: build the not-yet-cached ones concurrently
+  if ((int)h->topo.size() < L) h->topo.resize(L);
+  if (h->topo_ready.size() < (size_t)L) h->topo_ready.resize(L, 0);
+  std::vector<std::future<void>> topo_fut(std::max(L, 1));
+  for (int lvl = L - 1; lvl >= 2; --lvl)
+    if (!h->topo_ready[lvl])
+      topo_fut[lvl] = std::async(std::launch::async, [&T, h, lvl] { build_topo(T, lvl, h->topo[lvl]); });
   for (int lvl = L - 1; lvl >= 2; --lvl) {
     lap(7);
     double tl0 = now_ms();
     LevelBSR cur;
     cur.level = lvl;
-    if ((int)h->topo.size() < L) h->topo.resize(L);
-    if (h->topo_ready.size() < (size_t)L) h->topo_ready.resize(L, 0);
-    if (!h->topo_ready[lvl]) {
-      build_topo(T, lvl, h->topo[lvl]);
-      h->topo_ready[lvl] = 1;
-    }
+    if (topo_fut[lvl].valid()) topo_fut[lvl].get();  // built on a worker thread (tree-only work)
+    h->topo_ready[lvl] = 1;
     cur.tp = &h->topo[lvl];
     lap(14);
     for (int b : T.levels[lvl]) {
@@ -1055,9 +1065,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             P.C = G.as<cplx>() + goff[j];
             P.ldc = bcol[j];
             P.kchunk = mrows[j] > 512 ? 256 : 0;
-            add_gemm(gp, gt, P);
+            add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
           }
-          run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR);
+          run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
+          {
+            std::vector<cplx*> gptr(nj);
+            for (int j = 0; j < nj; ++j) gptr[j] = G.as<cplx>() + goff[j];
+            Stage sm;
+            size_t o_gp = sm.add(gptr), o_gd = sm.add(bcol);
+            sm.upload(st);
+            launch_herm_mirror(sm.ptr<cplx* const>(o_gp), sm.ptr<int>(o_gd), nj, bmax, st);
+            keep.push_back(std::move(sm.dev));
+          }
           lap(10);
           for (int j = 0; j < nj; ++j) {
             cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], G.as<cplx>() + gsz + goff[j], bcol[j], bcol[j], bcol[j],
@@ -1671,7 +1690,17 @@ int guarded(F&& f) {
   }
 }
 
+void tune_malloc() {  // keep large host temporaries off the mmap/munmap (page-fault) path
+  static bool done = false;
+  if (!done) {
+    mallopt(M_MMAP_THRESHOLD, 256 << 20);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+    done = true;
+  }
+}
+
 void ensure_device() {
+  tune_malloc();
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {

@@ -190,6 +190,19 @@ __global__ void __launch_bounds__(256) k_build_level(const int2* __restrict__ ta
   }
 }
 
+// Fill the strictly-lower triangle of Hermitian matrices from the upper one (Gram matrices
+// computed tile-upper only).  grid (ceil(b/32), nmats); mats[i] = (ptr, b) with ld b.
+__global__ void k_herm_mirror(cplx* const* __restrict__ ptrs, const int* __restrict__ dims) {
+  cplx* G = ptrs[blockIdx.y];
+  const int b = dims[blockIdx.y];
+  const int j = blockIdx.x * 32 + (threadIdx.x >> 3);  // column
+  if (j >= b) return;
+  for (int i = j + 1 + (threadIdx.x & 7); i < b; i += 8) {
+    const cplx v = G[j + (size_t)i * b];
+    G[i + (size_t)j * b] = cmk(v.x, -v.y);
+  }
+}
+
 // ------------------------------------------------------------------ copies
 __global__ void k_copy(const CopyTask* __restrict__ tasks, const int* __restrict__ maps,
                        const cplx* __restrict__ src, cplx* __restrict__ dst) {
@@ -1580,6 +1593,13 @@ void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const i
                   cplx* dst_arena, const Geo& g, double k, cudaStream_t st) {
   if (ntasks <= 0) return;
   k_build<<<ntasks, 256, 0, st>>>(d_tasks, gidx, slot, pos, tab, bld, src_arena, dst_arena, g, k);
+  FMMLU_LAUNCH();
+}
+
+void launch_herm_mirror(cplx* const* d_ptrs, const int* d_dims, int nmats, int bmax, cudaStream_t st) {
+  if (nmats <= 0) return;
+  dim3 grid((bmax + 31) / 32, nmats);
+  k_herm_mirror<<<grid, 256, 0, st>>>(d_ptrs, d_dims);
   FMMLU_LAUNCH();
 }
 

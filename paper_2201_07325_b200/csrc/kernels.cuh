@@ -52,6 +52,8 @@ struct CopyTask {
   int tri;             // 1: zero the strictly-lower part of dst (upper-triangular R copies)
   int ti, tj;          // tile origin within the original block (for the tri test)
 };
+// Mirror the upper triangle of Hermitian b×b matrices (ld b) into the lower one.
+void launch_herm_mirror(cplx* const* d_ptrs, const int* d_dims, int nmats, int bmax, cudaStream_t st);
 // Split copy tasks larger than 64×64 into 64×64 tiles (load balance across CTAs).
 void split_copy_tasks(std::vector<CopyTask>& v);
 
