@@ -133,7 +133,34 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
     }
   }
 
-  // epilogue
+  // epilogue.  Scatter: stage the tile's frame rows/columns (slot, position) and the owner-pair
+  // table in shared memory (reusing the operand buffers) so each element costs 2 atomics only.
+  int* rs = reinterpret_cast<int*>(smem_raw);  // [64] row slots
+  int* rp = rs + BM;                           // [64] row positions
+  int* cs = rp + BM;                           // [64] col slots
+  int* cp = cs + BN;                           // [64] col positions
+  int* bl = cp + BN;                           // [ns] block leading dims
+  long long* tb = reinterpret_cast<long long*>(bl + 64);  // [ns*ns] pair offsets (if it fits)
+  bool tab_in_smem = false;
+  if (SCATTER) {
+    tab_in_smem = P.ns <= 64 && P.ns * P.ns <= 2048;
+    __syncthreads();  // operand buffers are free
+    for (int e = tid; e < BM; e += NT) {
+      const int r = m0 + e;
+      rs[e] = r < P.m ? P.slot[P.row0 + r] : 0;
+      rp[e] = r < P.m ? P.pos[P.row0 + r] : 0;
+    }
+    for (int e = tid; e < BN; e += NT) {
+      const int c = n0 + e;
+      cs[e] = c < P.n ? P.slot[P.col0 + c] : 0;
+      cp[e] = c < P.n ? P.pos[P.col0 + c] : 0;
+    }
+    if (tab_in_smem) {
+      for (int e = tid; e < P.ns; e += NT) bl[e] = P.bld[e];
+      for (int e = tid; e < P.ns * P.ns; e += NT) tb[e] = P.tab[e];
+    }
+    __syncthreads();
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + wm * 32 + i * 8 + g;
@@ -147,11 +174,12 @@ __global__ void __launch_bounds__(NT) k_gemm(const GemmProblem* __restrict__ pro
         cplx v = cmk(alpha.x * accr[i][j][h] - alpha.y * acci[i][j][h],
                      alpha.x * acci[i][j][h] + alpha.y * accr[i][j][h]);
         if (SCATTER) {
-          const int fr = P.row0 + row, fc = P.col0 + col;
-          const int s = P.slot[fr], q = P.slot[fc];
-          const long long off = P.tab[s * P.ns + q];
+          const int lr = row - m0, lc = col - n0;
+          const int s = rs[lr], q = cs[lc];
+          const long long off = tab_in_smem ? tb[s * P.ns + q] : P.tab[s * P.ns + q];
           if (off >= 0) {
-            cplx* d = bsr + off + P.pos[fr] + (size_t)P.pos[fc] * P.bld[s];
+            const int ld = tab_in_smem ? bl[s] : P.bld[s];
+            cplx* d = bsr + off + rp[lr] + (size_t)cp[lc] * ld;
             atomicAdd(&d->x, v.x);
             atomicAdd(&d->y, v.y);
           }
