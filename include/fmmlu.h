@@ -148,6 +148,9 @@ int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
  *                   arithmetic; accurate while eps^2 >> unit roundoff)
  *               3 = as 2 but always with the global-memory blocked pivoted Cholesky
  *                   (the path used automatically for boxes beyond the cluster capacity)
+ *   "gj_mode"   X_RR inverse (Gauss-Jordan, partial pivoting): 0 = auto (whole matrix resident
+ *               in one CTA's or one <=16-CTA cluster's shared memory when it fits, blocked
+ *               panel path otherwise; default), 1 = blocked panel path always
  *   "proxy_rho" proxy-sphere radius / box side, in (sqrt(3)/2, 5/2) (reading C5; default 2.0)
  * Errors: EINVAL (unknown name or value out of range). */
 int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);
@@ -155,6 +158,15 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);
 /* Tree order: perm[i] = caller index of the i-th point in tree (Morton) order.
  * perm: int64[n] host buffer. */
 int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm);
+
+/* Batched in-place inverse of the X_RR blocks' kind (the elimination applies
+ * X_RR^-1; reading R3: explicit inverse by Gauss-Jordan with partial pivoting), exposed for
+ * kernel-level tests and timing.  A: DEVICE pointer to `count` n x n complex128 matrices,
+ * column-major, contiguous (matrix c at A + c*n*n*16 bytes), inverted in place on the
+ * handle's stream with the handle's "gj_mode".  ms (optional, may be NULL): device time of the
+ * inversion (CUDA events).  Synchronises the stream.
+ * Errors: EINVAL (NULL, host pointer, n < 1, count < 1), ESINGULAR (an exactly zero pivot). */
+int fmmlu_inverse_batch(fmmlu_handle* h, void* A, int n, int count, double* ms);
 
 /* Measure FP64 peak on this device: DFMA (kind=0) or DMMA m8n8k4 (kind=1)
  * throughput in TFLOP/s (roofline denominator; not part of the method). */

@@ -264,6 +264,7 @@ struct fmmlu_handle {
   }
   std::vector<char> topo_ready;
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
+  int gj_mode = 0;           // 0 auto (shared-memory GJ when it fits), 1 blocked panel GJ always
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
 };
 
@@ -343,6 +344,37 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   if (mats.empty()) return;
   int nmax = 1;
   for (auto& m : mats) nmax = std::max(nmax, m.second);
+  if (h->gj_mode == 0 && gj_dsm_cluster_size(nmax) > 0) {
+    // whole matrices resident in (cluster) shared memory: one launch for the batch
+    std::vector<GjTask> tasks;
+    double fl = 0, by = 0;
+    long long xs = 0;
+    for (auto& m : mats) xs += 2LL * m.second + 64;  // per-task exchange scratch (cluster path)
+    DBuf xb;
+    xb.alloc((size_t)xs * sizeof(cplx), st);
+    xs = 0;
+    for (auto& m : mats) {
+      GjTask t{};
+      t.A = m.first;
+      t.lda = m.second;
+      t.n = m.second;
+      t.Am = xb.as<cplx>() + xs;
+      xs += 2LL * m.second + 64;
+      tasks.push_back(t);
+      fl += 8.0 * (double)m.second * m.second * m.second;
+      by += 32.0 * (double)m.second * m.second;
+    }
+    Stage s;
+    size_t o_t = s.add(tasks);
+    s.upload(st);
+    int id = h->prof.begin(cls, st);
+    launch_gj_dsm(s.ptr<GjTask>(o_t), (int)tasks.size(), d_status, st, nmax);
+    h->prof.end(id, st);
+    h->prof.add(cls, fl, by, 1);
+    keep.push_back(std::move(s.dev));
+    keep.push_back(std::move(xb));
+    return;
+  }
   int nb = gj_panel_width(nmax);
   bool cluster_panel = false;
   if (nb < 32 && nmax > 64) {  // tall blocks (root): panel rows spread over a cluster, nb up to 32
@@ -1137,7 +1169,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       wait_stream(h, st);
       std::memcpy(hk.data(), pin, nj * sizeof(int));
       std::memcpy(hperm.data(), pin + nj, permtot * sizeof(int));
-      h->prof.resolve();
+      if (trace) {
+        double before[16];
+        std::memcpy(before, h->prof.ms, sizeof(before));
+        h->prof.resolve();
+        fprintf(stderr, "[fmmlu]   gpu ms since last sync (prev elim + this ID):");
+        static const char* nm[10] = {"build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve"};
+        for (int c = 0; c < 10; ++c)
+          if (h->prof.ms[c] - before[c] > 0.005) fprintf(stderr, " %s %.3f", nm[c], h->prof.ms[c] - before[c]);
+        fprintf(stderr, "\n");
+      } else {
+        h->prof.resolve();
+      }
       keep.clear();
       track(h, -(long long)M.bytes);
       M.release();
@@ -1202,9 +1245,20 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           S.n_eliminated += 1;
         }
         DBuf W;
-        if (trace)
-          fprintf(stderr, "[fmmlu]   elim: boxes %zu W %.2f GB factor %.2f GB\n", el.size(), wsW * 16e-9,
+        if (trace) {
+          int hist[5] = {0, 0, 0, 0, 0}, kmx = 0, nnmx = 0;
+          for (int j : el) {
+            const int r = jobs[j].b - jobs[j].k;
+            hist[r <= 32 ? 0 : r <= 64 ? 1 : r <= 119 ? 2 : r <= 200 ? 3 : 4]++;
+            kmx = std::max(kmx, jobs[j].k);
+            nnmx = std::max(nnmx, jobs[j].nN);
+          }
+          fprintf(stderr,
+                  "[fmmlu]   elim: boxes %zu rmax %d kmax %d nNmax %d r-hist[<=32,<=64,<=119,<=200,>200] %d %d %d %d %d "
+                  "W %.2f GB factor %.2f GB\n",
+                  el.size(), ph.rmax, kmx, nnmx, hist[0], hist[1], hist[2], hist[3], hist[4], wsW * 16e-9,
                   facsz * 16e-9);
+        }
         W.alloc((size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
         ph.fac.alloc((size_t)std::max<long long>(facsz, 1) * sizeof(cplx), st);
         FMMLU_CUDA(cudaMemsetAsync(ph.fac.p, 0, ph.fac.bytes, st));
@@ -1848,6 +1902,33 @@ int fmmlu_matvec(fmmlu_handle* h, double k, const void* x, void* y, int nrhs) {
   });
 }
 
+int fmmlu_inverse_batch(fmmlu_handle* h, void* A, int n, int count, double* ms) {
+  if (!h || !A) return fail(FMMLU_EINVAL, "NULL argument");
+  if (n < 1 || count < 1) return fail(FMMLU_EINVAL, "n and count must be >= 1");
+  if (!is_device_ptr(A)) return fail(FMMLU_EINVAL, "A must be a device pointer");
+  int sing = 0;
+  int rc = guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    cudaStream_t st = h->stream;
+    DBuf status;
+    status.alloc(16, st);
+    FMMLU_CUDA(cudaMemsetAsync(status.p, 0, 16, st));
+    std::vector<std::pair<cplx*, int>> mats;
+    for (int c = 0; c < count; ++c) mats.push_back({reinterpret_cast<cplx*>(A) + (size_t)c * n * n, n});
+    std::vector<DBuf> keep;
+    h->prof.resolve();
+    const double before = h->prof.ms[FMMLU_K_INV];
+    gj_blocked(h, mats, status.as<int>(), keep, FMMLU_K_INV);  // events bracket the kernels only
+    FMMLU_CUDA(cudaMemcpyAsync(&sing, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    h->prof.resolve();
+    if (ms) *ms = h->prof.ms[FMMLU_K_INV] - before;
+  });
+  if (rc != FMMLU_OK) return rc;
+  if (sing) return fail(FMMLU_ESINGULAR, "exactly singular pivot in fmmlu_inverse_batch");
+  return FMMLU_OK;
+}
+
 int fmmlu_destroy(fmmlu_handle* h) {
   if (!h) return FMMLU_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
@@ -1892,6 +1973,9 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
     if (value != 0 && value != 1 && value != 2 && value != 3)
       return fail(FMMLU_EINVAL, "id_mode must be 0, 1, 2 or 3");
     h->id_mode = (int)value;
+  } else if (k == "gj_mode") {
+    if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "gj_mode must be 0 or 1");
+    h->gj_mode = (int)value;
   } else if (k == "proxy_rho") {
     if (!(value > 0.87 && value < 2.5)) return fail(FMMLU_EINVAL, "proxy_rho must lie in (0.87, 2.5)");
     h->rho_factor = value;

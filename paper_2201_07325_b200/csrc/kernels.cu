@@ -582,103 +582,208 @@ __global__ void k_gj_copyback(const GjTask* __restrict__ tasks, const cplx* __re
 // shared memory for the whole factorization; the pivot column / Householder vector of each
 // step is published in the owner's shared memory and read by the others through DSMEM.
 
-// Gauss-Jordan inverse with partial pivoting (X_RR⁻¹ of each eliminated box): grid (CL, nmat).
-__global__ void __launch_bounds__(CK_NT) k_gj_cluster(const long long* __restrict__ offs,
-                                                      const int* __restrict__ dims, cplx* arena,
-                                                      int* status) {
+// Gauss-Jordan inverse with partial pivoting (X_RR⁻¹ of each eliminated box), the whole matrix
+// resident in REGISTERS for all n steps, in the swap-free "sweep" form: step j takes the pivot
+// row p_j = argmax over the not-yet-pivoted rows of |m_ij| (ties → lowest row), then
+//   m_pc ← m_pc / d  (c ≠ j),   m_ic ← m_ic − m_ij m_pc  (i ≠ p, c ≠ j),
+//   m_pj ← 1/d,   m_ij ← −m_ij / d  (i ≠ p),                         d = m_pj,
+// and at the end X⁻¹[j, p_j'] = M[p_j, j'].  The same arithmetic as GJ with row interchanges,
+// without moving rows.  Every element of a non-pivot column takes the same update
+// m_ic ← m_ic − cs_i·(m_pc/d) with cs = column j and cs_p := d − 1 (which yields m_pc/d in row
+// p), so the inner loop is 4 DFMA per complex element with no selects.
+// Layout: columns cyclic over the CL CTAs of a cluster (CL = 1: a single CTA); inside a CTA the
+// 16 warps form RG row groups × CG column groups; warp (rg, cg) holds rows
+// rg·32·MR + 32 r + lane (r < MR) of the local columns cg + CG q (q < MC).
+// Per step: [P1] the RG warps holding column j write it to a parity double-buffer and their
+// argmax candidates; barrier B1 (cluster barrier if CL > 1); [P2] everybody reduces the
+// candidates (DSMEM) → p, d; the lanes holding row p publish m_pc/d for their columns;
+// CTA barrier B2; [P3] register update.  grid (CL, ntasks), 512 threads.
+constexpr int GJR_NT = 512, GJR_NW = GJR_NT / 32, GJR_NMAX = 512;
+
+// Exchange record of one row group's pivot candidate: |x|², row, x.
+struct GjCand {
+  double v;
+  int i, pad;
+  cplx x;
+};
+
+template <int MR, int MC, bool MULTI>
+__global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__ tasks, int* status) {
   cg::cluster_group cl = cg::this_cluster();
-  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
-  extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  __shared__ int meta[2][2];  // [parity] {pivot row, singular flag}
-  const int n = dims[blockIdx.y];
-  cplx* A = arena + offs[blockIdx.y];
-  const int ncl = (n - rank + CL - 1) / CL;  // local columns
-  cplx* Al = reinterpret_cast<cplx*>(shm);   // n × ncl
-  cplx* buf = Al + (size_t)n * ((n + CL - 1) / CL);  // [2][n] published pivot column (rows swapped)
-  cplx* colsw = buf + 2 * n;                  // local copy of the pivot column
-  cplx* rowj = colsw + n;                     // ncl: row j of the local columns
-  cplx* rowp = rowj + (n + CL - 1) / CL;      // ncl: row p
-  int* piv = reinterpret_cast<int*>(rowp + (n + CL - 1) / CL);  // n
-  const int tid = threadIdx.x;
-  for (int e = tid; e < n * ncl; e += CK_NT) {
-    const int i = e % n, l = e / n;
-    Al[e] = A[i + (size_t)(rank + l * CL) * n];
-  }
-  cl.sync();
+  const int CL = MULTI ? (int)cl.num_blocks() : 1, rank = MULTI ? (int)cl.block_rank() : 0;
+  // single CTA: exchange through shared memory.  Cluster: through global memory / L2 (t.Am is
+  // this task's scratch: [2][n] column + [2][16] candidates) — DSMEM reads of one owner CTA by
+  // every thread of 16 CTAs would serialise on the owner's shared-memory port.
+  __shared__ cplx pbs[MULTI ? 1 : 2][MULTI ? 1 : GJR_NMAX];
+  __shared__ GjCand cands[MULTI ? 1 : 2][GJR_NW];
+  __shared__ cplx rowp[GJR_NW * MC];       // m_pc / d, [column group][slot]
+  __shared__ int piv[GJR_NMAX], pinv[GJR_NMAX];
+  const GjTask t = tasks[blockIdx.y];
+  const int n = t.n;
+  const int ncl = (n - rank + CL - 1) / CL;
+  const int RG = (n + 32 * MR - 1) / (32 * MR), CG = GJR_NW / RG;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rg = warp % RG, cgp = warp / RG;
+  cplx* const xg = t.Am;                                        // [2][n]
+  GjCand* const cg_ = reinterpret_cast<GjCand*>(t.Am + 2 * n);  // [2][16]
+  // this warp's local columns are cgp + CG q for q < nq
+  const int nq = cgp < CG ? min(MC, (ncl - cgp + CG - 1) / CG) : 0;
+  const int row0 = rg * 32 * MR + lane;
+  cplx a[MC][MR];
+  unsigned used = 0;  // bit r: row row0 + 32 r already pivoted
+#pragma unroll
+  for (int q = 0; q < MC; ++q)
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int i = row0 + 32 * r;
+      a[q][r] = (q < nq && i < n) ? t.A[i + (size_t)(rank + (cgp + CG * q) * CL) * t.lda] : cmk(0.0, 0.0);
+    }
+  if (MULTI) cl.sync(); else __syncthreads();  // all inputs loaded before anyone writes output
+  cplx* const rpw = rowp + cgp * MC;
   for (int j = 0; j < n; ++j) {
     const int o = j % CL, lj = j / CL, par = j & 1;
-    if (rank == o) {
+    cplx* const pcol = MULTI ? xg + par * n : &pbs[par & (MULTI ? 0 : 1)][0];
+    GjCand* const pcand = MULTI ? cg_ + par * GJR_NW : &cands[par & (MULTI ? 0 : 1)][0];
+    // slot of column j in this warp (-1: not here)
+    const int dq = lj - cgp;
+    const int qj = (rank == o && nq > 0 && dq >= 0 && dq % CG == 0) ? dq / CG : -1;
+    // ---- P1: the warps holding column j publish it and their pivot candidates
+    if (qj >= 0) {
       double pv = -1.0;
       int p = INT_MAX;
-      for (int i = j + tid; i < n; i += CK_NT) argmax_merge(pv, p, cabs2(Al[i + (size_t)lj * n]), i);
-      block_argmax<CK_NT>(pv, p, red_v, red_i);
-      const bool sing = !(pv > 0.0);
-      if (tid == 0) {
-        meta[par][0] = sing ? j : p;
-        meta[par][1] = sing ? 1 : 0;
-      }
-      if (!sing)
-        for (int i = tid; i < n; i += CK_NT) {
-          const int src = i == j ? p : (i == p ? j : i);
-          buf[par * n + i] = Al[src + (size_t)lj * n];
+      cplx px = cmk(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < MR; ++r) {
+        cplx x = a[0][r];
+#pragma unroll
+        for (int q = 1; q < MC; ++q)
+          if (q == qj) x = a[q][r];
+        const int i = row0 + 32 * r;
+        if (i < n) {
+          if (MULTI) __stcg(reinterpret_cast<double2*>(pcol + i), x);
+          else pcol[i] = x;
+          if (!((used >> r) & 1u)) {
+            const double v = cabs2(x);
+            if (v > pv || (v == pv && i < p)) {
+              pv = v;
+              p = i;
+              px = x;
+            }
+          }
         }
-    }
-    cl.sync();
-    const int* rmeta = cl.map_shared_rank(&meta[par][0], o);
-    const int p = rmeta[0];
-    if (rmeta[1]) {
-      if (rank == 0 && tid == 0) atomicExch(status, 1);
-      return;  // uniform across the cluster
-    }
-    const cplx* rb = cl.map_shared_rank(buf + par * n, o);
-    for (int i = tid; i < n; i += CK_NT) colsw[i] = rb[i];
-    if (tid == 0) piv[j] = p;
-    __syncthreads();
-    const cplx dinv = cdiv(cmk(1.0, 0.0), colsw[j]);
-    // rows j and p of every local column (read before anyone writes)
-    for (int l = tid; l < ncl; l += CK_NT) {
-      rowj[l] = Al[j + (size_t)l * n];
-      rowp[l] = Al[p + (size_t)l * n];
-    }
-    __syncthreads();
-    for (int e = tid; e < n * ncl; e += CK_NT) {
-      const int i = e % n, l = e / n;
-      const int g = rank + l * CL;
-      cplx v;
-      if (g == j) {
-        v = i == j ? dinv : cmk(-(colsw[i].x * dinv.x - colsw[i].y * dinv.y),
-                                -(colsw[i].x * dinv.y + colsw[i].y * dinv.x));
-      } else {
-        // rows j and p swapped, row j scaled by 1/d, others eliminated
-        const cplx aj = rowj[l], ap = rowp[l];
-        const cplx rj = cmul(ap, dinv);  // (p == j ⇒ ap == aj)
-        const cplx old = i == p ? aj : (i == j ? ap : Al[e]);
-        v = i == j ? rj : cfms(colsw[i], rj, old);
       }
-      Al[e] = v;
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
+        const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
+        const double x2 = __shfl_xor_sync(0xffffffffu, px.x, s), y2 = __shfl_xor_sync(0xffffffffu, px.y, s);
+        if (v2 > pv || (v2 == pv && i2 < p)) {
+          pv = v2;
+          p = i2;
+          px = cmk(x2, y2);
+        }
+      }
+      if (lane == 0) {
+        GjCand cd;
+        cd.v = pv;
+        cd.i = p;
+        cd.pad = 0;
+        cd.x = px;
+        pcand[rg] = cd;
+      }
     }
-    __syncthreads();
-  }
-  // undo the interchanges: output column c = column L[c], L = swaps applied in reverse
-  int* L = piv + n;  // n ints (smem sized for it)
-  __syncthreads();
-  if (tid == 0) {
-    for (int c = 0; c < n; ++c) L[c] = c;
-    for (int j = n - 1; j >= 0; --j) {
-      int a = L[j];
-      L[j] = L[piv[j]];
-      L[piv[j]] = a;
+    if (MULTI) cl.sync(); else __syncthreads();  // B1 (release/acquire: global writes visible)
+    // ---- P2: pivot row p and d (every warp reduces the RG candidates itself)
+    double pv = -1.0;
+    int p = INT_MAX;
+    cplx d = cmk(1.0, 0.0);
+    if (lane < RG) {
+      if (MULTI) {
+        const double* cp = reinterpret_cast<const double*>(pcand + lane);
+        pv = __ldcg(cp);
+        p = __ldcg(reinterpret_cast<const int*>(cp + 1));
+        d = __ldcg(reinterpret_cast<const double2*>(cp + 2));
+      } else {
+        pv = pcand[lane].v;
+        p = pcand[lane].i;
+        d = pcand[lane].x;
+      }
+    }
+    cplx c[MR];  // issue the column loads early (they do not depend on p)
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int i = row0 + 32 * r;
+      c[r] = i < n ? (MULTI ? __ldcg(reinterpret_cast<const double2*>(pcol + i)) : pcol[i]) : cmk(0.0, 0.0);
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
+      const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
+      const double x2 = __shfl_xor_sync(0xffffffffu, d.x, s), y2 = __shfl_xor_sync(0xffffffffu, d.y, s);
+      if (v2 > pv || (v2 == pv && i2 < p)) {
+        pv = v2;
+        p = i2;
+        d = cmk(x2, y2);
+      }
+    }
+    const bool sing = !(pv > 0.0);
+    if (p == INT_MAX) p = j;  // NaN column: keep indices in range (flagged below, result invalid)
+    if (sing) d = cmk(1.0, 0.0);
+    const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), d);
+    if (rg == p / (32 * MR) && lane == (p & 31)) {
+      const int pr = (p / 32) % MR;
+#pragma unroll
+      for (int r = 0; r < MR; ++r)
+        if (r == pr) used |= 1u << r;
+#pragma unroll
+      for (int q = 0; q < MC; ++q) {
+        cplx x = a[q][0];
+#pragma unroll
+        for (int r = 1; r < MR; ++r)
+          if (r == pr) x = a[q][r];
+        if (q < nq) rpw[q] = cmul(x, dinv);
+      }
+    }
+    if (tid == 0) {
+      piv[j] = p;
+      if (sing && rank == 0) atomicExch(status, 1);
+    }
+    __syncthreads();  // B2
+    // ---- P3: register update
+#pragma unroll
+    for (int r = 0; r < MR; ++r)
+      if (row0 + 32 * r == p) c[r] = cmk(d.x - 1.0, d.y);
+#pragma unroll
+    for (int q = 0; q < MC; ++q) {
+      if (q >= nq) break;
+      if (q == qj) {  // the pivot column: −cs/d, and 1/d in row p
+#pragma unroll
+        for (int r = 0; r < MR; ++r) {
+          const int i = row0 + 32 * r;
+          a[q][r] = i == p ? dinv : cmk(-(c[r].x * dinv.x - c[r].y * dinv.y), -(c[r].x * dinv.y + c[r].y * dinv.x));
+        }
+      } else {
+        const cplx rp = rpw[q];
+#pragma unroll
+        for (int r = 0; r < MR; ++r) a[q][r] = cfms(c[r], rp, a[q][r]);
+      }
     }
   }
+  // ---- output X⁻¹[j, p_j'] = M[p_j, j']: element (row i, column g) → (pinv[i], piv[g])
+  for (int j = tid; j < n; j += GJR_NT) pinv[j] = j;
   __syncthreads();
-  cl.sync();  // every CTA has loaded its input columns long ago; safe to overwrite A
-  for (int c = 0; c < n; ++c) {
-    const int g = L[c];
-    if (g % CL != rank) continue;
-    const cplx* src = Al + (size_t)(g / CL) * n;
-    for (int i = tid; i < n; i += CK_NT) A[i + (size_t)c * n] = src[i];
+  if (tid == 0)
+    for (int j = 0; j < n; ++j) pinv[piv[j]] = j;  // serial: well-defined even if a flagged step repeated a row
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < MC; ++q) {
+    if (q >= nq) break;
+    const int c = piv[rank + (cgp + CG * q) * CL];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int i = row0 + 32 * r;
+      if (i < n) t.A[pinv[i] + (size_t)c * t.lda] = a[q][r];
+    }
   }
 }
 
@@ -1710,11 +1815,6 @@ void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, cons
 
 namespace {
 constexpr size_t kClusterSmemCap = 220 * 1024;
-size_t gj_smem(int n, int CL) {
-  const size_t ncl = (n + CL - 1) / CL;
-  return (size_t)n * ncl * sizeof(cplx) + 3 * (size_t)n * sizeof(cplx) + 2 * ncl * sizeof(cplx) +
-         2 * (size_t)n * sizeof(int) + 64;
-}
 template <class K>
 void cluster_attrs(K kern, size_t smem, int CL) {
   FMMLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1774,15 +1874,55 @@ void launch_pchol_big_finish(const PcholBig* d_tasks, int ntasks, int* perm_out,
   FMMLU_LAUNCH();
 }
 
-bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,
-                       cudaStream_t st, int nmax) {
-  if (nmat <= 0) return true;
-  int CL = 1;
-  while (CL <= 16 && gj_smem(nmax, CL) > kClusterSmemCap) CL *= 2;
-  if (CL > 16) return false;
-  const size_t smem = gj_smem(nmax, CL);
-  cluster_attrs(k_gj_cluster, smem, CL);
-  launch_cluster(k_gj_cluster, CL, nmat, smem, st, d_off, d_dim, arena, d_status);
+// register-resident GJ configurations: rows per lane MR, columns per warp MC, cluster size CL
+namespace {
+struct GjrCfg { int MR, MC, CL; };
+GjrCfg gjr_cfg(int nmax) {  // RG = ceil(n/(32 MR)) row groups, CG = 16/RG column groups
+  if (nmax <= 32) return {1, 2, 1};
+  if (nmax <= 64) return {1, 8, 1};
+  if (nmax <= 128) return {1, 32, 1};
+  if (nmax <= 256) return {1, 16, 8};
+  if (nmax <= 384) return {1, 24, 16};
+  return {2, 16, 16};  // ≤ 512
+}
+constexpr int GJR_NCAP = 512;
+template <int MR, int MC, bool MULTI>
+void launch_gjr(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t st, int CL) {
+  if constexpr (!MULTI) {
+    k_gj_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, d_status);
+    FMMLU_LAUNCH();
+    return;
+  } else {
+  if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(k_gj_reg<MR, MC, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL, ntasks, 1);
+  cfg.blockDim = dim3(GJR_NT, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_gj_reg<MR, MC, true>, d_tasks, d_status));
+  }
+}
+}  // namespace
+
+int gj_dsm_cluster_size(int nmax) { return nmax <= GJR_NCAP ? gjr_cfg(nmax).CL : 0; }
+
+bool launch_gj_dsm(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t st, int nmax) {
+  if (ntasks <= 0) return true;
+  if (nmax > GJR_NCAP) return false;
+  const GjrCfg c = gjr_cfg(nmax);
+  if (nmax <= 32) launch_gjr<1, 2, false>(d_tasks, ntasks, d_status, st, 1);
+  else if (nmax <= 64) launch_gjr<1, 8, false>(d_tasks, ntasks, d_status, st, 1);
+  else if (nmax <= 128) launch_gjr<1, 32, false>(d_tasks, ntasks, d_status, st, 1);
+  else if (nmax <= 256) launch_gjr<1, 16, true>(d_tasks, ntasks, d_status, st, c.CL);
+  else if (nmax <= 384) launch_gjr<1, 24, true>(d_tasks, ntasks, d_status, st, c.CL);
+  else launch_gjr<2, 16, true>(d_tasks, ntasks, d_status, st, c.CL);
   return true;
 }
 

@@ -100,7 +100,7 @@ void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx
 // Blocked in-place Gauss-Jordan inverse (partial pivoting) of a batch of matrices.
 struct GjTask {
   cplx* A;   // n × n, ld lda, inverted in place
-  cplx* Am;  // n × nb scratch (panel minus identity)
+  cplx* Am;  // blocked path: n × nb scratch (panel minus identity); register path: exchange scratch
   cplx* Y;   // nb × n scratch (rows J of the other columns)
   int* piv;  // n pivot rows
   int lda, n;
@@ -117,10 +117,11 @@ void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, cons
 // in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
 void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx* arena,
                        int* d_status, cudaStream_t st, int nmax);
-// Thread-block-cluster versions (matrix resident in distributed shared memory); return false
-// when the matrix is too large for a 16-CTA cluster (caller falls back to the kernels above).
-bool launch_gj_cluster(const long long* d_off, const int* d_dim, int nmat, cplx* arena, int* d_status,
-                       cudaStream_t st, int nmax);
+// Whole-matrix Gauss-Jordan inverse resident in (distributed) shared memory: one CTA, or a
+// cluster of ≤ 16 CTAs holding the columns cyclically.  Returns false when nmax is too large
+// (the caller uses the blocked panel path).
+int gj_dsm_cluster_size(int nmax);  // 0 = does not fit
+bool launch_gj_dsm(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t st, int nmax);
 // Householder QR (pivot = 0: TSQR round, writes triu(R) to out) or CPQR with the reading-C9
 // stopping rule (pivot = 1: writes R' = [R11 R12], pivot columns first then the redundant ones
 // in ascending index, over rows 0..k-1 of A, plus perm and k) on matrices resident in the

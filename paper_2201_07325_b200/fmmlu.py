@@ -52,7 +52,7 @@ KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur"
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
-           "fmmlu_set_param")
+           "fmmlu_set_param", "fmmlu_inverse_batch")
 
 
 def lib_path() -> str:
@@ -83,6 +83,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_tree_perm.argtypes = [vp, vp]
     L.fmmlu_probe_fp64.argtypes = [ci, ctypes.POINTER(cd)]
     L.fmmlu_set_param.argtypes = [vp, ctypes.c_char_p, cd]
+    L.fmmlu_inverse_batch.argtypes = [vp, vp, ci, ci, ctypes.POINTER(cd)]
     for f in EXPORTS:
         getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
     _LIB = L
@@ -158,6 +159,13 @@ class FmmLu:
     def set_param(self, name: str, value: float):
         _check(load().fmmlu_set_param(self.h, name.encode(), float(value)))
         return self
+
+    def inverse_batch(self, A, n: int, count: int) -> float:
+        """In-place inverse of `count` n×n complex128 matrices (device tensor, column-major,
+        contiguous) with the handle's gj_mode; returns the device time in ms."""
+        ms = ctypes.c_double(0.0)
+        _check(load().fmmlu_inverse_batch(self.h, _ptr(A), int(n), int(count), ctypes.byref(ms)))
+        return ms.value
 
     def set_stream(self, stream_ptr: int | None):
         _check(load().fmmlu_set_stream(self.h, stream_ptr or None))

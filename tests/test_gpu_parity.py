@@ -193,3 +193,19 @@ def test_large_configs_full_size_residual(F, name, nrhs):
         Ki[i] = 0.0
         yi = (Ki * g.weights) @ x + 0.5 * x[i]
         assert np.max(np.abs(yi - Ax[i])) <= 1e-11 * np.max(np.abs(yi)) + 1e-13
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_gj_modes_parity(F, mode):
+    """X_RR⁻¹ paths (0: whole matrix in one CTA's / one cluster's shared memory; 1: blocked panel
+    Gauss-Jordan) both match the oracle on a case whose X_RR span one-CTA and cluster sizes."""
+    g = fi.ellipsoid(6000)
+    k, eps = 2 * math.pi, 1e-6
+    b = fi.gaussian_rhs(g.n, 2, 6)
+    h = F.FmmLu(g.points, g.normals, g.weights, 64).set_param("gj_mode", mode).factor(k, eps)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, 64)
+    xo = rss.solve(f, b)
+    assert dense.rel_diff(x, xo) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
