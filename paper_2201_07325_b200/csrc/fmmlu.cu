@@ -27,6 +27,7 @@
 #include <string>
 #include <unordered_map>
 #include <future>
+#include <mutex>
 #include <vector>
 
 #include "../../include/fmmlu.h"
@@ -56,6 +57,67 @@ bool is_device_ptr(const void* p) {
 }
 
 // --------------------------------------------------------------------------- device memory
+// host-side time spent in allocator calls (FMMLU_TRACE diagnostics)
+struct AllocClock {
+  double alloc_ms = 0, free_ms = 0, pin_ms = 0, alloc_max = 0;
+  long long nalloc = 0;
+};
+AllocClock g_ac;
+double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Process-wide cache of large device blocks.  Repeated factorizations ask for the same large
+// buffers (level block stores, workspaces); returning them to cudaMallocAsync's pool and
+// re-requesting them occasionally stalls the host for hundreds of ms (pool growth / reclaim),
+// so blocks ≥ kBigBlock are kept here.  Reuse is stream-ordered: an event recorded at release
+// is waited on by the next user's stream.  A failed allocation flushes the cache and retries.
+constexpr size_t kBigBlock = 32u << 20;
+struct BigCache {
+  struct Blk {
+    void* p;
+    size_t bytes;
+    cudaEvent_t ev;
+  };
+  std::mutex mu;
+  std::vector<Blk> free_;
+  void* take(size_t b, cudaStream_t st, size_t* got) {
+    std::lock_guard<std::mutex> lk(mu);
+    int best = -1;
+    for (int i = 0; i < (int)free_.size(); ++i)
+      if (free_[i].bytes >= b && free_[i].bytes <= 2 * b + kBigBlock &&
+          (best < 0 || free_[i].bytes < free_[best].bytes))
+        best = i;
+    if (best < 0) return nullptr;
+    Blk k = free_[best];
+    free_.erase(free_.begin() + best);
+    cudaStreamWaitEvent(st, k.ev, 0);
+    cudaEventDestroy(k.ev);
+    *got = k.bytes;
+    return k.p;
+  }
+  void give(void* p, size_t bytes, cudaStream_t st) {
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, st);
+    std::lock_guard<std::mutex> lk(mu);
+    free_.push_back({p, bytes, ev});
+  }
+  void flush() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& k : free_) {
+      cudaEventSynchronize(k.ev);
+      cudaEventDestroy(k.ev);
+      cudaFree(k.p);
+    }
+    free_.clear();
+  }
+};
+BigCache& big_cache() {
+  static BigCache* c = new BigCache();  // never destroyed: blocks live until process exit
+  return *c;
+}
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -63,29 +125,66 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), big(o.big), cap(o.cap) {
+    o.p = nullptr;
+    o.bytes = 0;
+    o.big = false;
+  }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
       p = o.p;
       bytes = o.bytes;
       st = o.st;
+      big = o.big;
+      cap = o.cap;
       o.p = nullptr;
       o.bytes = 0;
+      o.big = false;
     }
     return *this;
   }
   ~DBuf() { release(); }
+  bool big = false;  // from / back to the big-block cache (plain cudaMalloc memory)
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) {
+      const double t0 = wall_ms();
+      if (big) big_cache().give(p, cap, st);
+      else cudaFreeAsync(p, st);
+      g_ac.free_ms += wall_ms() - t0;
+    }
     p = nullptr;
     bytes = 0;
+    big = false;
   }
+  size_t cap = 0;
   void alloc(size_t b, cudaStream_t s) {
     release();
     st = s;
     if (b == 0) b = 16;
-    cudaError_t e = cudaMallocAsync(&p, b, s);
+    const double t0 = wall_ms();
+    cudaError_t e = cudaSuccess;
+    if (b >= kBigBlock) {
+      size_t got = 0;
+      p = big_cache().take(b, s, &got);
+      if (!p) {
+        got = (b + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+        e = cudaMalloc(&p, got);
+        if (e != cudaSuccess) {  // give the cached blocks back and retry once
+          cudaGetLastError();
+          big_cache().flush();
+          e = cudaMalloc(&p, got);
+        }
+      }
+      big = e == cudaSuccess;
+      cap = got;
+    } else {
+      e = cudaMallocAsync(&p, b, s);
+    }
+    const double dt = wall_ms() - t0;
+    g_ac.alloc_ms += dt;
+    g_ac.alloc_max = std::max(g_ac.alloc_max, dt);
+    ++g_ac.nalloc;
     if (e != cudaSuccess) {
       cudaGetLastError();
       throw Error(FMMLU_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed");
@@ -105,7 +204,9 @@ struct PinnedArena {
     if (chunks.empty() || used + bytes > chunks.back().second) {
       size_t cap = std::max<size_t>(bytes, chunks.empty() ? (64u << 20) : 2 * chunks.back().second);
       void* p = nullptr;
+      const double t0 = wall_ms();
       FMMLU_CUDA(cudaMallocHost(&p, cap));
+      g_ac.pin_ms += wall_ms() - t0;
       chunks.push_back({(char*)p, cap});
       used = 0;
     }
@@ -250,17 +351,20 @@ struct fmmlu_handle {
   size_t cur_bytes = 0, peak_bytes = 0;
   Prof prof;
   std::vector<LevelTopo> topo;    // per-level owner topology (tree-only, cached)
-  int* d2h_buf = nullptr;         // pinned landing buffer for ranks / pivots
-  size_t d2h_cap = 0;
+  // pinned landing buffer for ranks / pivots: per thread, grow-only, never freed (pinned
+  // allocations and frees per handle stalled the host for hundreds of ms)
   int* d2h(size_t n) {
-    if (n > d2h_cap) {
-      if (d2h_buf) cudaFreeHost(d2h_buf);
-      d2h_cap = std::max<size_t>(n, 2 * d2h_cap + 4096);
+    thread_local int* buf = nullptr;
+    thread_local size_t cap = 0;
+    if (n > cap) {
+      const size_t c = std::max<size_t>(n, 2 * cap + (1u << 20));
       void* p = nullptr;
-      FMMLU_CUDA(cudaMallocHost(&p, d2h_cap * sizeof(int)));
-      d2h_buf = (int*)p;
+      FMMLU_CUDA(cudaMallocHost(&p, c * sizeof(int)));
+      if (buf) cudaFreeHost(buf);  // only while growing (the stream was synchronised by the caller)
+      buf = (int*)p;
+      cap = c;
     }
-    return d2h_buf;
+    return buf;
   }
   std::vector<char> topo_ready;
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
@@ -662,8 +766,10 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
   }
   tp.boxN.assign(nlb, {});
   tp.boxQ.assign(nlb, {});
-  std::vector<std::vector<int>> pairs(no);
-  std::vector<int> cand, grp;
+  // pair set: nb[a] = ∪ { grp(i) : a ∈ grp(i) } ∪ Q-relations, grp(i) = {i} ∪ N(i).  Built as
+  // per-owner lists of the groups containing it, then one stamped union per owner.
+  std::vector<std::vector<int>> ingrp(no), qrel(no);
+  std::vector<int> cand;
   for (int i = 0; i < nlb; ++i) {
     const int box = tp.owners[i];
     const Box& B = T.boxes[box];
@@ -685,20 +791,29 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
     std::sort(cand.begin(), cand.end());
     cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
     for (int o : cand) (T.sep(box, tp.owners[o], lvl) <= 1 ? tp.boxN[i] : tp.boxQ[i]).push_back(o);
-    grp.assign(1, i);
-    grp.insert(grp.end(), tp.boxN[i].begin(), tp.boxN[i].end());
-    for (int x : grp)
-      for (int y : grp) pairs[x].push_back(y);
+    ingrp[i].push_back(i);
+    for (int x : tp.boxN[i]) ingrp[x].push_back(i);
     for (int q : tp.boxQ[i]) {
-      pairs[i].push_back(q);
-      pairs[q].push_back(i);
+      qrel[i].push_back(q);
+      qrel[q].push_back(i);
     }
   }
   tp.nb.assign(no, {});
+  std::vector<int> stamp(no, -1);
   for (int a = 0; a < no; ++a) {
-    std::sort(pairs[a].begin(), pairs[a].end());
-    pairs[a].erase(std::unique(pairs[a].begin(), pairs[a].end()), pairs[a].end());
-    tp.nb[a] = std::move(pairs[a]);
+    std::vector<int>& v = tp.nb[a];
+    auto add = [&](int b) {
+      if (stamp[b] != a) {
+        stamp[b] = a;
+        v.push_back(b);
+      }
+    };
+    for (int i : ingrp[a]) {
+      add(i);
+      for (int x : tp.boxN[i]) add(x);
+    }
+    for (int q : qrel[a]) add(q);
+    std::sort(v.begin(), v.end());
   }
 }
 
@@ -760,7 +875,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
 
   // host-time trace (FMMLU_TRACE=1): sections exclusive of stream waits
   static const bool trace = getenv("FMMLU_TRACE") != nullptr;
-  double tr[16] = {0};
+  double tr[24] = {0};
   double tmark = now_ms(), wmark = S.t_sync_wait_ms;
   auto lap = [&](int sec) {
     double t = now_ms(), w = S.t_sync_wait_ms;
@@ -1244,6 +1359,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           ph.rmax = std::max(ph.rmax, r);
           S.n_eliminated += 1;
         }
+        lap(16);
         DBuf W;
         if (trace) {
           int hist[5] = {0, 0, 0, 0, 0}, kmx = 0, nnmx = 0;
@@ -1268,6 +1384,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         S.factor_bytes += ph.fac.bytes + ph.idx.bytes;
         cplx* Wp = W.as<cplx>();
         cplx* F = ph.fac.as<cplx>();
+        lap(17);
 
         std::vector<CopyTask> cps, cpsT, cpsX;
         std::vector<int> maps, hidx(idxsz);
@@ -1389,6 +1506,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (fslot.empty()) { fslot.push_back(0); fpos.push_back(0); }
         if (ftab.empty()) ftab.push_back(-1);
         if (fbld.empty()) fbld.push_back(0);
+        lap(18);
         Stage s;
         split_copy_tasks(cps);
         split_copy_tasks(cpsT);
@@ -1407,6 +1525,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           for (auto& c : cpsT) by += 32.0 * c.rows * c.cols;
           h->prof.add(FMMLU_K_GATHER, 0, by, 1 + (cpsT.empty() ? 0 : 1));
         }
+        lap(19);
         // E: W_B[R,:] −= Tᵀ W_B[S,:]
         std::vector<GemmProblem> gp;
         std::vector<GemmTile> gt;
@@ -1457,6 +1576,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           }
         }
         run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_EF);
+        lap(20);
         // X_RR⁻¹ (Gauss-Jordan with partial pivoting)
         launch_copy(s.ptr<CopyTask>(o_cx), (int)cpsX.size(), s.ptr<int>(o_m), Wp, F, st);
         {
@@ -1542,6 +1662,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           add_gemm(gp, gt, P);
         }
         run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep, h->prof, FMMLU_K_SCHUR);
+        lap(21);
         // index arena + records
         h2d(ph.idx.p, hidx.data(), hidx.size() * sizeof(int), st);
         ph.recs.alloc(recs.size() * sizeof(BoxRec), st);
@@ -1596,12 +1717,19 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   }
 
   lap(6);
+  if (trace) {
+    fprintf(stderr, "[fmmlu] allocator host ms: cudaMallocAsync %.1f (%lld calls, max %.1f) cudaFreeAsync %.1f "
+                    "cudaMallocHost %.1f\n",
+            g_ac.alloc_ms, g_ac.nalloc, g_ac.alloc_max, g_ac.free_ms, g_ac.pin_ms);
+    g_ac = AllocClock{};
+  }
   if (trace)
     fprintf(stderr, "[fmmlu] host ms: level-setup %.1f build-tasks %.1f phase-jobs %.1f id %.1f elim %.1f "
                     "update %.1f carry %.1f other %.1f | id: tasks %.1f gatherlaunch %.1f gram %.1f prep %.1f "
-                    "pchol %.1f rest %.1f | topo %.1f acts %.1f | wait %.1f\n",
+                    "pchol %.1f rest %.1f | topo %.1f acts %.1f | elim: sizes %.1f alloc %.1f tasks %.1f "
+                    "upload %.1f EF %.1f inv-panel-schur %.1f recs %.1f | wait %.1f\n",
             tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8], tr[9], tr[10], tr[11], tr[12], tr[13],
-            tr[14], tr[15], S.t_sync_wait_ms);
+            tr[14], tr[15], tr[16], tr[17], tr[18], tr[19], tr[20], tr[21], tr[4], S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root
   double tr0 = now_ms();
   std::vector<int> Bt;
@@ -1939,7 +2067,6 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->perm.release();
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
-  if (h->d2h_buf) cudaFreeHost(h->d2h_buf);
   delete h;
   return FMMLU_OK;
 }

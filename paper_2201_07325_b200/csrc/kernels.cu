@@ -607,28 +607,40 @@ struct GjCand {
   cplx x;
 };
 
-template <int MR, int MC, bool MULTI>
+template <int MR, int MC, bool MULTI, bool TIMING = false>
 __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__ tasks, int* status) {
+  static_assert(MR == 1 || MR == 2, "rows per lane");
+  long long tph[5] = {0, 0, 0, 0, 0}, tc = 0;  // TIMING: cycles in P1 | B1 | P2 | B2 | P3
+#define GJ_TICK(k)                     \
+  if (TIMING) {                        \
+    const long long now = clock64();   \
+    tph[k] += now - tc;                \
+    tc = now;                          \
+  }
+  constexpr int LGMR = MR == 1 ? 0 : 1;
   cg::cluster_group cl = cg::this_cluster();
   const int CL = MULTI ? (int)cl.num_blocks() : 1, rank = MULTI ? (int)cl.block_rank() : 0;
+  const int lgCL = __ffs(CL) - 1;  // CL is a power of two
   // single CTA: exchange through shared memory.  Cluster: through global memory / L2 (t.Am is
   // this task's scratch: [2][n] column + [2][16] candidates) — DSMEM reads of one owner CTA by
   // every thread of 16 CTAs would serialise on the owner's shared-memory port.
   __shared__ cplx pbs[MULTI ? 1 : 2][MULTI ? 1 : GJR_NMAX];
   __shared__ GjCand cands[MULTI ? 1 : 2][GJR_NW];
-  __shared__ cplx rowp[GJR_NW * MC];       // m_pc / d, [column group][slot]
+  __shared__ cplx rowp[GJR_NW * MC];  // m_pc / d, [column group][slot]
   __shared__ int piv[GJR_NMAX], pinv[GJR_NMAX];
   const GjTask t = tasks[blockIdx.y];
   const int n = t.n;
-  const int ncl = (n - rank + CL - 1) / CL;
-  const int RG = (n + 32 * MR - 1) / (32 * MR), CG = GJR_NW / RG;
+  const int ncl = (n - rank + CL - 1) >> lgCL;
+  const int RG = (n + 32 * MR - 1) >> (5 + LGMR), CG = GJR_NW / RG;
+  int rgp2 = 1;  // rounds of the cross-row-group candidate reduction: log2(next pow2 ≥ RG)
+  while (rgp2 < RG) rgp2 <<= 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rg = warp % RG, cgp = warp / RG;
   cplx* const xg = t.Am;                                        // [2][n]
   GjCand* const cg_ = reinterpret_cast<GjCand*>(t.Am + 2 * n);  // [2][16]
   // this warp's local columns are cgp + CG q for q < nq
   const int nq = cgp < CG ? min(MC, (ncl - cgp + CG - 1) / CG) : 0;
-  const int row0 = rg * 32 * MR + lane;
+  const int row0 = (rg << (5 + LGMR)) + lane;
   cplx a[MC][MR];
   unsigned used = 0;  // bit r: row row0 + 32 r already pivoted
 #pragma unroll
@@ -636,17 +648,22 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int i = row0 + 32 * r;
-      a[q][r] = (q < nq && i < n) ? t.A[i + (size_t)(rank + (cgp + CG * q) * CL) * t.lda] : cmk(0.0, 0.0);
+      a[q][r] = (q < nq && i < n) ? t.A[i + (size_t)(rank + ((cgp + CG * q) << lgCL)) * t.lda] : cmk(0.0, 0.0);
     }
   if (MULTI) cl.sync(); else __syncthreads();  // all inputs loaded before anyone writes output
   cplx* const rpw = rowp + cgp * MC;
+  int qn = 0, nextl = cgp;  // next own slot and its local column index (columns come in order)
   for (int j = 0; j < n; ++j) {
-    const int o = j % CL, lj = j / CL, par = j & 1;
+    if (TIMING) tc = clock64();
+    const int o = j & (CL - 1), lj = j >> lgCL, par = j & 1;
     cplx* const pcol = MULTI ? xg + par * n : &pbs[par & (MULTI ? 0 : 1)][0];
     GjCand* const pcand = MULTI ? cg_ + par * GJR_NW : &cands[par & (MULTI ? 0 : 1)][0];
-    // slot of column j in this warp (-1: not here)
-    const int dq = lj - cgp;
-    const int qj = (rank == o && nq > 0 && dq >= 0 && dq % CG == 0) ? dq / CG : -1;
+    int qj = -1;  // slot of column j in this warp
+    if (rank == o && lj == nextl && qn < nq) {
+      qj = qn;
+      ++qn;
+      nextl += CG;
+    }
     // ---- P1: the warps holding column j publish it and their pivot candidates
     if (qj >= 0) {
       double pv = -1.0;
@@ -662,13 +679,11 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
         if (i < n) {
           if (MULTI) __stcg(reinterpret_cast<double2*>(pcol + i), x);
           else pcol[i] = x;
-          if (!((used >> r) & 1u)) {
-            const double v = cabs2(x);
-            if (v > pv || (v == pv && i < p)) {
-              pv = v;
-              p = i;
-              px = x;
-            }
+          const double v = cabs2(x);
+          if (!((used >> r) & 1u) && v > pv) {  // rows ascend with r: strict > keeps the lowest
+            pv = v;
+            p = i;
+            px = x;
           }
         }
       }
@@ -676,11 +691,15 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
       for (int s = 16; s > 0; s >>= 1) {
         const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
         const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
-        const double x2 = __shfl_xor_sync(0xffffffffu, px.x, s), y2 = __shfl_xor_sync(0xffffffffu, px.y, s);
+        double x2 = 0.0, y2 = 0.0;
+        if (MULTI) {
+          x2 = __shfl_xor_sync(0xffffffffu, px.x, s);
+          y2 = __shfl_xor_sync(0xffffffffu, px.y, s);
+        }
         if (v2 > pv || (v2 == pv && i2 < p)) {
           pv = v2;
           p = i2;
-          px = cmk(x2, y2);
+          if (MULTI) px = cmk(x2, y2);
         }
       }
       if (lane == 0) {
@@ -692,7 +711,9 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
         pcand[rg] = cd;
       }
     }
+    GJ_TICK(0);
     if (MULTI) cl.sync(); else __syncthreads();  // B1 (release/acquire: global writes visible)
+    GJ_TICK(1);
     // ---- P2: pivot row p and d (every warp reduces the RG candidates itself)
     double pv = -1.0;
     int p = INT_MAX;
@@ -706,7 +727,6 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
       } else {
         pv = pcand[lane].v;
         p = pcand[lane].i;
-        d = pcand[lane].x;
       }
     }
     cplx c[MR];  // issue the column loads early (they do not depend on p)
@@ -715,23 +735,31 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
       const int i = row0 + 32 * r;
       c[r] = i < n ? (MULTI ? __ldcg(reinterpret_cast<const double2*>(pcol + i)) : pcol[i]) : cmk(0.0, 0.0);
     }
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
+    for (int s = rgp2 >> 1; s > 0; s >>= 1) {
       const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
       const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
-      const double x2 = __shfl_xor_sync(0xffffffffu, d.x, s), y2 = __shfl_xor_sync(0xffffffffu, d.y, s);
+      double x2 = 0.0, y2 = 0.0;
+      if (MULTI) {
+        x2 = __shfl_xor_sync(0xffffffffu, d.x, s);
+        y2 = __shfl_xor_sync(0xffffffffu, d.y, s);
+      }
       if (v2 > pv || (v2 == pv && i2 < p)) {
         pv = v2;
         p = i2;
-        d = cmk(x2, y2);
+        if (MULTI) d = cmk(x2, y2);
       }
     }
+    pv = __shfl_sync(0xffffffffu, pv, 0);
+    p = __shfl_sync(0xffffffffu, p, 0);
     const bool sing = !(pv > 0.0);
     if (p == INT_MAX) p = j;  // NaN column: keep indices in range (flagged below, result invalid)
+    if (MULTI) d = cmk(__shfl_sync(0xffffffffu, d.x, 0), __shfl_sync(0xffffffffu, d.y, 0));
+    else d = pcol[p];
     if (sing) d = cmk(1.0, 0.0);
-    const cplx dinv = sing ? cmk(1.0, 0.0) : cdiv(cmk(1.0, 0.0), d);
-    if (rg == p / (32 * MR) && lane == (p & 31)) {
-      const int pr = (p / 32) % MR;
+    const double rn = __drcp_rn(d.x * d.x + d.y * d.y);
+    const cplx dinv = cmk(d.x * rn, -d.y * rn);
+    if ((p >> (5 + LGMR)) == rg && lane == (p & 31)) {
+      const int pr = (p >> 5) & (MR - 1);
 #pragma unroll
       for (int r = 0; r < MR; ++r)
         if (r == pr) used |= 1u << r;
@@ -748,7 +776,9 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
       piv[j] = p;
       if (sing && rank == 0) atomicExch(status, 1);
     }
+    GJ_TICK(2);
     __syncthreads();  // B2
+    GJ_TICK(3);
     // ---- P3: register update
 #pragma unroll
     for (int r = 0; r < MR; ++r)
@@ -768,7 +798,12 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
         for (int r = 0; r < MR; ++r) a[q][r] = cfms(c[r], rp, a[q][r]);
       }
     }
+    GJ_TICK(4);
   }
+#undef GJ_TICK
+  if (TIMING && blockIdx.x == 0 && blockIdx.y == 0 && (tid == 0 || tid == 32 * (GJR_NW - 1)))
+    printf("[gj timing] n %d CL %d warp %d cycles/step: P1 %lld B1 %lld P2 %lld B2 %lld P3 %lld\n", n, CL, warp,
+           tph[0] / n, tph[1] / n, tph[2] / n, tph[3] / n, tph[4] / n);
   // ---- output X⁻¹[j, p_j'] = M[p_j, j']: element (row i, column g) → (pinv[i], piv[g])
   for (int j = tid; j < n; j += GJR_NT) pinv[j] = j;
   __syncthreads();
@@ -778,7 +813,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
 #pragma unroll
   for (int q = 0; q < MC; ++q) {
     if (q >= nq) break;
-    const int c = piv[rank + (cgp + CG * q) * CL];
+    const int c = piv[rank + ((cgp + CG * q) << lgCL)];
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int i = row0 + 32 * r;
@@ -1880,7 +1915,7 @@ struct GjrCfg { int MR, MC, CL; };
 GjrCfg gjr_cfg(int nmax) {  // RG = ceil(n/(32 MR)) row groups, CG = 16/RG column groups
   if (nmax <= 32) return {1, 2, 1};
   if (nmax <= 64) return {1, 8, 1};
-  if (nmax <= 128) return {1, 32, 1};
+  if (nmax <= 128) return {1, 16, 2};
   if (nmax <= 256) return {1, 16, 8};
   if (nmax <= 384) return {1, 24, 16};
   return {2, 16, 16};  // ≤ 512
@@ -1888,11 +1923,29 @@ GjrCfg gjr_cfg(int nmax) {  // RG = ceil(n/(32 MR)) row groups, CG = 16/RG colum
 constexpr int GJR_NCAP = 512;
 template <int MR, int MC, bool MULTI>
 void launch_gjr(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t st, int CL) {
+  static const bool timing = getenv("FMMLU_GJ_TIMING") != nullptr;
   if constexpr (!MULTI) {
-    k_gj_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, d_status);
+    if (timing) k_gj_reg<MR, MC, false, true><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, d_status);
+    else k_gj_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, d_status);
     FMMLU_LAUNCH();
     return;
   } else {
+  if (timing) {
+    if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(k_gj_reg<MR, MC, true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, ntasks, 1);
+    cfg.blockDim = dim3(GJR_NT, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_gj_reg<MR, MC, true, true>, d_tasks, d_status));
+    return;
+  }
   if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(k_gj_reg<MR, MC, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL, ntasks, 1);
@@ -1919,7 +1972,6 @@ bool launch_gj_dsm(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_
   const GjrCfg c = gjr_cfg(nmax);
   if (nmax <= 32) launch_gjr<1, 2, false>(d_tasks, ntasks, d_status, st, 1);
   else if (nmax <= 64) launch_gjr<1, 8, false>(d_tasks, ntasks, d_status, st, 1);
-  else if (nmax <= 128) launch_gjr<1, 32, false>(d_tasks, ntasks, d_status, st, 1);
   else if (nmax <= 256) launch_gjr<1, 16, true>(d_tasks, ntasks, d_status, st, c.CL);
   else if (nmax <= 384) launch_gjr<1, 24, true>(d_tasks, ntasks, d_status, st, c.CL);
   else launch_gjr<2, 16, true>(d_tasks, ntasks, d_status, st, c.CL);
