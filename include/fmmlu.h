@@ -168,6 +168,28 @@ int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm);
  * Errors: EINVAL (NULL, host pointer, n < 1, count < 1), ESINGULAR (an exactly zero pivot). */
 int fmmlu_inverse_batch(fmmlu_handle* h, void* A, int n, int count, double* ms);
 
+/* Config-4 workload (BASELINE.json configs[3], readings C21/C22): ID and
+ * elimination of nbox INDEPENDENT boxes (one level, nothing modified yet, Q = ∅).
+ *   pts, nrm   : nbox × b × 3 doubles (row-major xyz per point): box points, unit normals
+ *   npts, nnrm : nbox × nnear × 3: the near set N of each box (Schur-update targets, C22)
+ *   w          : uniform quadrature weight; k: wavenumber; eps: ID tolerance (0,1)
+ *   n_gamma, rho: proxy points (Fibonacci directions, R2) on the sphere of radius rho about
+ *               the origin (every box is centred at 0); ID rows = 2 n_gamma proxy rows (C21)
+ * Per box: M = [s_γ K(y_ℓ,x_j)√w ; s_γ G(x_j,y_ℓ)√w], ID (L606-638,
+ * C9), E/F transforms, X_RR^-1, panels, and Δ = −X_{(S∪N)R} X_RR^-1 X_{R(S∪N)} (L753-825).
+ * Outputs (host or device pointers):
+ *   ranks  int32[nbox]: k of each box
+ *   perm   int32[nbox × b] or NULL: skeleton columns first (pivot order), then the redundant
+ *          ones ascending
+ *   keep[nkeep], delta: for box keep[j], Δ ((k+nnear) × (k+nnear), column-major, frame
+ *          [S in pivot order | N]) is written at delta + j·(b+nnear)² complex128 elements
+ *   timing double[3] or NULL: device ms of the whole batch, model GFLOP (SURVEY §8(d) cost
+ *          model with the measured ranks), boxes per wave.
+ * Errors: EINVAL, ENOMEM, ESINGULAR (exactly singular X_RR), ECUDA. */
+int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const double* nnrm, int nbox, int b,
+                int nnear, double w, double k, double eps, int n_gamma, double rho, int* ranks, int* perm,
+                int nkeep, const int* keep, void* delta, double* timing);
+
 /* Measure FP64 peak on this device: DFMA (kind=0) or DMMA m8n8k4 (kind=1)
  * throughput in TFLOP/s (roofline denominator; not part of the method). */
 int fmmlu_probe_fp64(int kind, double* tflops);

@@ -835,6 +835,110 @@ struct LevelBSR {
   }
 };
 
+// ID of a batch of m×b matrices M (column-major, ld m, reading C9, R4):
+// perm (b ints per box at pofs[j]: skeleton first in pivot order, then the redundant columns
+// ascending), k per box, T = R11⁻¹R12 (k × (b−k), ld k) at tofs[j] in Tb.  ε ≥ 1e-7 (auto):
+// Gram G = MᴴM (DMMA, upper tiles + mirror) + pivoted Cholesky (cluster, or global-memory
+// blocked for big b); otherwise Householder TSQR rounds + cluster CPQR.  mfin[j] = rows of the
+// matrix the pivoted pass ran on (flop accounting).  May overwrite M.
+void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, const std::vector<int>& bcol,
+              const std::vector<int>& pofs, const std::vector<long long>& tofs, double eps, int* permd, int* kd,
+              cplx* Tb, std::vector<DBuf>& keep, std::vector<int>& mfin) {
+  cudaStream_t st = h->stream;
+  const int nj = (int)mp.size();
+  int bmax = 1;
+  for (int b : bcol) bmax = std::max(bmax, b);
+  std::vector<IdTask> ids(nj);
+  for (int j = 0; j < nj; ++j) {
+    ids[j].Mp = nullptr;
+    ids[j].m = mrows[j];
+    ids[j].b = bcol[j];
+    ids[j].out_off = pofs[j];
+    ids[j].T = tofs[j];
+  }
+  const bool gram = h->id_mode >= 2 || (h->id_mode == 0 && eps >= 1e-7);
+  std::vector<ClusterQrTask> cq(nj);
+  DBuf G;
+  bool done_id = false;
+  if (gram) {
+    long long gsz = 0;
+    std::vector<long long> goff(nj);
+    for (int j = 0; j < nj; ++j) {
+      goff[j] = gsz;
+      gsz += (long long)bcol[j] * bcol[j];
+    }
+    G.alloc(2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
+    FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
+    std::vector<GemmProblem> gp;
+    std::vector<GemmTile> gt;
+    for (int j = 0; j < nj; ++j) {
+      GemmProblem P{};
+      P.m = bcol[j];
+      P.n = bcol[j];
+      P.k = mrows[j];
+      P.opA = kOpC;
+      P.opB = kOpN;
+      P.A = mp[j];
+      P.lda = mrows[j];
+      P.B = mp[j];
+      P.ldb = mrows[j];
+      P.C = G.as<cplx>() + goff[j];
+      P.ldc = bcol[j];
+      P.kchunk = mrows[j] > 512 ? 256 : 0;
+      add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
+    }
+    run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
+    {
+      std::vector<cplx*> gptr(nj);
+      for (int j = 0; j < nj; ++j) gptr[j] = G.as<cplx>() + goff[j];
+      Stage sm;
+      size_t o_gp = sm.add(gptr), o_gd = sm.add(bcol);
+      sm.upload(st);
+      launch_herm_mirror(sm.ptr<cplx* const>(o_gp), sm.ptr<int>(o_gd), nj, bmax, st);
+      keep.push_back(std::move(sm.dev));
+    }
+    for (int j = 0; j < nj; ++j) {
+      cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], G.as<cplx>() + gsz + goff[j], bcol[j], bcol[j], bcol[j],
+                            bcol[j], pofs[j], 0};
+      ids[j].Mp = G.as<cplx>() + goff[j];
+      ids[j].m = bcol[j];
+      mfin[j] = bcol[j];
+    }
+    Stage s2;
+    size_t o_i = s2.add(ids), o_q = s2.add(cq);
+    s2.upload(st);
+    int cid = h->prof.begin(FMMLU_K_CPQR, st);
+    done_id = h->id_mode != 3 && launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
+    if (!done_id) {  // boxes too large for a cluster: global-memory blocked pivoted Cholesky
+      pchol_big(h, G.as<cplx>(), goff, gsz, bcol, pofs, permd, kd, eps, keep);
+      done_id = true;
+    }
+    launch_trsm_T(s2.ptr<IdTask>(o_i), kd, nj, nullptr, Tb, st, bmax);
+    h->prof.end(cid, st);
+    h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
+    keep.push_back(std::move(s2.dev));
+  }
+  if (!done_id) {
+    tsqr_cluster(h, mp, mrows, bcol, keep);
+    for (int j = 0; j < nj; ++j) {
+      ids[j].Mp = mp[j];
+      ids[j].m = mrows[j];
+      cq[j] = ClusterQrTask{mp[j], nullptr, mrows[j], mrows[j], bcol[j], 0, pofs[j], 0};
+      mfin[j] = mrows[j];
+    }
+    Stage s2;
+    size_t o_i = s2.add(ids), o_q = s2.add(cq);
+    s2.upload(st);
+    int cid = h->prof.begin(FMMLU_K_CPQR, st);
+    launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd, kd, eps, st, mrows.data(), bcol.data());
+    launch_trsm_T(s2.ptr<IdTask>(o_i), kd, nj, nullptr, Tb, st, bmax);
+    h->prof.end(cid, st);
+    h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
+    keep.push_back(std::move(s2.dev));
+  }
+  keep.push_back(std::move(G));
+}
+
 template <class J>
 std::vector<int> jobs_permoff(const std::vector<J>& jobs) {
   std::vector<int> v;
@@ -1171,110 +1275,21 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           h->prof.add(FMMLU_K_GATHER, fl, by, (cps.empty() ? 0 : 1) + (pts.empty() ? 0 : 1));
         }
         keep.push_back(std::move(s.dev));
-        // TSQR rounds (cluster QR) until each box's matrix fits one cluster, then cluster CPQR
-        // on it and T = R11⁻¹R12
-        std::vector<cplx*> mp(nj);
-        std::vector<int> mrows(nj), bcol(nj);
-        for (int j = 0; j < nj; ++j) {
-          mp[j] = M.as<cplx>() + jobs[j].Moff;
-          mrows[j] = jobs[j].m;
-          bcol[j] = jobs[j].b;
+        {
+          std::vector<cplx*> mp(nj);
+          std::vector<int> mrows(nj), bcol(nj), pofs(nj), mfin(nj);
+          std::vector<long long> tofs(nj);
+          for (int j = 0; j < nj; ++j) {
+            mp[j] = M.as<cplx>() + jobs[j].Moff;
+            mrows[j] = jobs[j].m;
+            bcol[j] = jobs[j].b;
+            pofs[j] = jobs[j].permoff;
+            tofs[j] = jobs[j].Toff;
+          }
+          lap(9);
+          id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin);
+          for (int j = 0; j < nj; ++j) jobs[j].mfin = mfin[j];
         }
-        // ID mode: at ε ≥ 1e-7 the pivoted Cholesky of G = MᴴM gives the
-        // CPQR pivots/rank/T to ~u·cond accuracy (ε² ≫ u); tighter ε uses Householder TSQR.
-        lap(9);
-        const bool gram = h->id_mode >= 2 || (h->id_mode == 0 && eps >= 1e-7);
-        std::vector<ClusterQrTask> cq(nj);
-        DBuf G;
-        bool done_id = false;
-        if (gram) {
-          long long gsz = 0;
-          std::vector<long long> goff(nj);
-          for (int j = 0; j < nj; ++j) {
-            goff[j] = gsz;
-            gsz += (long long)bcol[j] * bcol[j];
-          }
-          G.alloc(2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
-          FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
-          std::vector<GemmProblem> gp;
-          std::vector<GemmTile> gt;
-          for (int j = 0; j < nj; ++j) {
-            GemmProblem P{};
-            P.m = bcol[j];
-            P.n = bcol[j];
-            P.k = mrows[j];
-            P.opA = kOpC;
-            P.opB = kOpN;
-            P.A = mp[j];
-            P.lda = mrows[j];
-            P.B = mp[j];
-            P.ldb = mrows[j];
-            P.C = G.as<cplx>() + goff[j];
-            P.ldc = bcol[j];
-            P.kchunk = mrows[j] > 512 ? 256 : 0;
-            add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
-          }
-          run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
-          {
-            std::vector<cplx*> gptr(nj);
-            for (int j = 0; j < nj; ++j) gptr[j] = G.as<cplx>() + goff[j];
-            Stage sm;
-            size_t o_gp = sm.add(gptr), o_gd = sm.add(bcol);
-            sm.upload(st);
-            launch_herm_mirror(sm.ptr<cplx* const>(o_gp), sm.ptr<int>(o_gd), nj, bmax, st);
-            keep.push_back(std::move(sm.dev));
-          }
-          lap(10);
-          for (int j = 0; j < nj; ++j) {
-            cq[j] = ClusterQrTask{G.as<cplx>() + goff[j], G.as<cplx>() + gsz + goff[j], bcol[j], bcol[j], bcol[j],
-                                  bcol[j], jobs[j].permoff, 0};
-            ids[j].Mp = G.as<cplx>() + goff[j];
-            ids[j].m = bcol[j];
-            jobs[j].mfin = bcol[j];
-          }
-          Stage s2;
-          size_t o_i = s2.add(ids), o_q = s2.add(cq);
-          s2.upload(st);
-          int cid = h->prof.begin(FMMLU_K_CPQR, st);
-          lap(11);
-          done_id = h->id_mode != 3 &&
-                    launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd.as<int>(), kd.as<int>(), eps, st, bmax);
-          if (!done_id) {  // boxes too large for a cluster: global-memory blocked pivoted Cholesky
-            pchol_big(h, G.as<cplx>(), goff, gsz, bcol, jobs_permoff(jobs), permd.as<int>(), kd.as<int>(), eps, keep);
-            done_id = true;
-          }
-          lap(12);
-          if (done_id) launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st, bmax);
-          h->prof.end(cid, st);
-          h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
-          keep.push_back(std::move(s2.dev));
-          if (!done_id) {  // b too large for a cluster: fall back to the Householder path
-            for (int j = 0; j < nj; ++j) {
-              mp[j] = M.as<cplx>() + jobs[j].Moff;
-              mrows[j] = jobs[j].m;
-            }
-          }
-        }
-        if (!done_id) {
-          tsqr_cluster(h, mp, mrows, bcol, keep);
-          for (int j = 0; j < nj; ++j) {
-            ids[j].Mp = mp[j];
-            ids[j].m = mrows[j];
-            cq[j] = ClusterQrTask{mp[j], nullptr, mrows[j], mrows[j], bcol[j], 0, jobs[j].permoff, 0};
-            jobs[j].mfin = mrows[j];
-          }
-          Stage s2;
-          size_t o_i = s2.add(ids), o_q = s2.add(cq);
-          s2.upload(st);
-          int cid = h->prof.begin(FMMLU_K_CPQR, st);
-          launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd.as<int>(), kd.as<int>(), eps, st,
-                             mrows.data(), bcol.data());
-          launch_trsm_T(s2.ptr<IdTask>(o_i), kd.as<int>(), nj, nullptr, Tb.as<cplx>(), st, bmax);
-          h->prof.end(cid, st);
-          h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
-          keep.push_back(std::move(s2.dev));
-        }
-        keep.push_back(std::move(G));
         lap(13);
       }
       std::vector<int> hk(nj), hperm(permtot);
@@ -1891,6 +1906,398 @@ void ensure_device() {
   }
 }
 
+// ---------------------------------------------------------------------------- cfg4: independent boxes
+// BASELINE.json configs[3] (readings C21/C22): for each box, M = the 2n_γ proxy rows (Q = ∅),
+// ID (id_stage), then the elimination of its redundant DOFs against its near set N, writing the
+// box's Schur update Δ_{(S∪N)²} = −X_{(S∪N)R} X_RR⁻¹ X_{R(S∪N)} into a private buffer.  The same
+// kernels as the tree path (k_proxy, Gram/pivoted Cholesky or TSQR/CPQR, k_trsm_T, k_build,
+// DMMA GEMMs, Gauss-Jordan), processed in waves sized to free device memory.
+double box_model_flops(int b, int kk, int nn, int m) {  // SURVEY §8(d) per-box cost model
+  const double r = b - kk, K = kk, N = nn, B = b, Mr = m;
+  const double kgen = 70.0 * (Mr * B + B * B + 2.0 * B * N);
+  const double qr = 8.0 * Mr * B * B - (8.0 / 3.0) * B * B * B;
+  const double cpqr = 8.0 * (B * B * K - B * K * K + K * K * K / 3.0) + 4.0 * K * K * r;
+  const double ef = 8.0 * (3.0 * r * r * K + K * K * r) + 8.0 * r * K * K + 16.0 * r * K * N;
+  const double pan = (8.0 / 3.0) * r * r * r + 16.0 * r * r * (K + N);
+  const double schur = 8.0 * (K + N) * (K + N) * r;
+  return kgen + qr + cpqr + (r > 0 ? ef + pan + schur : 0.0);
+}
+
+void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const double* npts, const double* nnrm,
+                int nbox, int b, int nnear, double w, double k, double eps, int ngamma, double rho, int* ranks,
+                int* perm, int nkeep, const int* keep_ids, void* delta, double* timing) {
+  cudaStream_t st = h->stream;
+  const int npb = b + nnear, m = 2 * ngamma;
+  const double sg = std::sqrt(4.0 * M_PI * rho * rho / ngamma);
+  std::unordered_map<int, int> kslot;
+  for (int j = 0; j < nkeep; ++j) kslot[keep_ids[j]] = j;
+  const bool in_dev = is_device_ptr(pts);
+  const bool rk_dev = is_device_ptr(ranks), pm_dev = perm && is_device_ptr(perm),
+             dl_dev = delta && is_device_ptr(delta);
+  const long long tcap = (long long)(b / 2 + 1) * (b - b / 2 + 1);
+  // per-box device bytes (upper bounds: k ≤ b for the factor pieces and Δ)
+  const double per_box = 16.0 * ((double)m * b + 2.0 * b * b + (double)b * npb + (double)nnear * b + tcap +
+                                 (double)npb * npb + (double)b * b + 2.0 * b * npb) +
+                         8.0 * 13.0 * npb + 64.0 * b;
+  size_t fr = 0, tot = 0;
+  FMMLU_CUDA(cudaMemGetInfo(&fr, &tot));
+  const int wave = (int)std::max(1.0, std::min<double>({(double)nbox, 2048.0, 0.6 * fr / per_box}));
+  cudaEvent_t e0, e1;
+  FMMLU_CUDA(cudaEventCreate(&e0));
+  FMMLU_CUDA(cudaEventCreate(&e1));
+  FMMLU_CUDA(cudaEventRecord(e0, st));
+  double model = 0.0;
+  DBuf status;
+  status.alloc(16, st);
+  FMMLU_CUDA(cudaMemsetAsync(status.p, 0, 16, st));
+  const cplx m1 = cmk(-1.0, 0.0), p1 = cmk(1.0, 0.0);
+  for (int w0 = 0; w0 < nbox; w0 += wave) {
+    const int nw = std::min(wave, nbox - w0);
+    const long long np = (long long)nw * npb;
+    std::vector<DBuf> keep;
+    // ---- geometry (SoA) of the wave
+    DBuf gin, geo;
+    const double *dp = pts + (size_t)w0 * b * 3, *dn = nrm + (size_t)w0 * b * 3,
+                 *dq = npts + (size_t)w0 * nnear * 3, *dr = nnrm + (size_t)w0 * nnear * 3;
+    if (!in_dev) {
+      const size_t sb = (size_t)nw * b * 3 * sizeof(double), sn = (size_t)nw * nnear * 3 * sizeof(double);
+      gin.alloc(2 * sb + 2 * sn, st);
+      char* base = gin.as<char>();
+      h2d(base, dp, sb, st);
+      h2d(base + sb, dn, sb, st);
+      h2d(base + 2 * sb, dq, sn, st);
+      h2d(base + 2 * sb + sn, dr, sn, st);
+      dp = (const double*)base;
+      dn = (const double*)(base + sb);
+      dq = (const double*)(base + 2 * sb);
+      dr = (const double*)(base + 2 * sb + sn);
+    }
+    geo.alloc((size_t)7 * np * sizeof(double), st);
+    double* G7 = geo.as<double>();
+    launch_box_geo(dp, dn, dq, dr, nw, b, nnear, std::sqrt(w), G7, st);
+    const Geo g{G7, G7 + np, G7 + 2 * np, G7 + 3 * np, G7 + 4 * np, G7 + 5 * np, G7 + 6 * np};
+    // ---- M (proxy rows) and the ID
+    DBuf M, Tb, permd, kd;
+    M.alloc((size_t)nw * m * b * sizeof(cplx), st);
+    Tb.alloc((size_t)nw * tcap * sizeof(cplx), st);
+    permd.alloc((size_t)nw * b * sizeof(int), st);
+    kd.alloc((size_t)nw * sizeof(int), st);
+    {
+      std::vector<int> gidx((size_t)nw * b);
+      std::vector<ProxyTask> pt(nw);
+      for (int j = 0; j < nw; ++j) {
+        for (int t = 0; t < b; ++t) gidx[(size_t)j * b + t] = j * npb + t;
+        ProxyTask q{};
+        q.dst = (long long)j * m * b;
+        q.ld = m;
+        q.row0 = 0;
+        q.b = b;
+        q.idx_off = j * b;
+        q.ngamma = ngamma;
+        q.cx = q.cy = q.cz = 0.0;
+        q.rho = rho;
+        q.sg = sg;
+        pt[j] = q;
+      }
+      Stage sg_;
+      size_t o_p = sg_.add(pt), o_g = sg_.add(gidx);
+      sg_.upload(st);
+      int pid = h->prof.begin(FMMLU_K_GATHER, st);
+      launch_proxy(sg_.ptr<ProxyTask>(o_p), nw, sg_.ptr<int>(o_g), M.as<cplx>(), g, k, st);
+      h->prof.end(pid, st);
+      h->prof.add(FMMLU_K_GATHER, 120.0 * m * b * nw, 16.0 * m * b * nw, 1);
+      keep.push_back(std::move(sg_.dev));
+      std::vector<cplx*> mp(nw);
+      std::vector<int> mrows(nw, m), bcol(nw, b), pofs(nw), mfin(nw);
+      std::vector<long long> tofs(nw);
+      for (int j = 0; j < nw; ++j) {
+        mp[j] = M.as<cplx>() + (size_t)j * m * b;
+        pofs[j] = j * b;
+        tofs[j] = (long long)j * tcap;
+      }
+      id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin);
+    }
+    std::vector<int> hk(nw), hp((size_t)nw * b);
+    int* pin = h->d2h(nw + (size_t)nw * b);
+    FMMLU_CUDA(cudaMemcpyAsync(pin, kd.p, nw * sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMMLU_CUDA(cudaMemcpyAsync(pin + nw, permd.p, (size_t)nw * b * sizeof(int), cudaMemcpyDeviceToHost, st));
+    wait_stream(h, st);
+    std::memcpy(hk.data(), pin, nw * sizeof(int));
+    std::memcpy(hp.data(), pin + nw, (size_t)nw * b * sizeof(int));
+    if (const char* dump = getenv("FMMLU_DEBUG_DUMP_T")) {  // diagnostics: T of the wave's first box
+      std::vector<cplx> t0((size_t)hk[0] * (b - hk[0]));
+      FMMLU_CUDA(cudaMemcpy(t0.data(), Tb.p, t0.size() * sizeof(cplx), cudaMemcpyDeviceToHost));
+      if (FILE* f = fopen(dump, "wb")) {
+        fwrite(t0.data(), sizeof(cplx), t0.size(), f);
+        fclose(f);
+      }
+    }
+    h->prof.resolve();
+    M.release();
+    // ---- elimination
+    std::vector<int> el;
+    long long wsW = 0, wsF = 0, wsD = 0;
+    std::vector<long long> oWB(nw), oWN(nw), oT(nw), oXi(nw), oUp(nw), oLp(nw), oD(nw);
+    for (int j = 0; j < nw; ++j) {
+      const int kk = hk[j], r = b - kk, kn = kk + nnear;
+      model += box_model_flops(b, kk, nnear, m);
+      if (r <= 0) continue;
+      el.push_back(j);
+      oWB[j] = wsW;
+      wsW += (long long)b * npb;
+      oWN[j] = wsW;
+      wsW += (long long)nnear * b;
+      oT[j] = wsF;
+      wsF += (long long)kk * r;
+      oXi[j] = wsF;
+      wsF += (long long)r * r;
+      oUp[j] = wsF;
+      wsF += (long long)r * kn;
+      oLp[j] = wsF;
+      wsF += (long long)kn * r;
+      oD[j] = wsD;
+      wsD += (long long)kn * kn;
+    }
+    DBuf Wb, Fb, Db;
+    Wb.alloc((size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
+    Fb.alloc((size_t)std::max<long long>(wsF, 1) * sizeof(cplx), st);
+    Db.alloc((size_t)std::max<long long>(wsD, 1) * sizeof(cplx), st);
+    // the GEMM store epilogue accumulates (C += αAB): Up/Lp and Δ start from zero
+    FMMLU_CUDA(cudaMemsetAsync(Fb.p, 0, (size_t)std::max<long long>(wsF, 1) * sizeof(cplx), st));
+    FMMLU_CUDA(cudaMemsetAsync(Db.p, 0, (size_t)std::max<long long>(wsD, 1) * sizeof(cplx), st));
+    cplx *W = Wb.as<cplx>(), *Fp = Fb.as<cplx>(), *D = Db.as<cplx>();
+    if (!el.empty()) {
+      // W_B = Ã[B_RS, B_RS ∪ N] and W_N = Ã[N, B_RS] generated directly in [R | S] order
+      std::vector<int> gl, slot, pos;
+      std::vector<BuildTask> bt;
+      std::vector<CopyTask> cpT, cpX;
+      auto tiles = [&](long long dst, int ldd, int ro, int co, int ni, int nj) {
+        for (int i0 = 0; i0 < ni; i0 += kTile)
+          for (int j0 = 0; j0 < nj; j0 += kTile) {
+            BuildTask t{};
+            t.dst = dst;
+            t.ldd = ldd;
+            t.rows_off = ro;
+            t.cols_off = co;
+            t.i0 = i0;
+            t.j0 = j0;
+            t.ni = std::min(kTile, ni - i0);
+            t.nj = std::min(kTile, nj - j0);
+            t.ns = 1;
+            bt.push_back(t);
+          }
+      };
+      for (int j : el) {
+        const int kk = hk[j], r = b - kk;
+        const int* pm = &hp[(size_t)j * b];
+        const int ro = (int)gl.size();  // [R | S] then N
+        for (int i = kk; i < b; ++i) gl.push_back(j * npb + pm[i]);
+        for (int i = 0; i < kk; ++i) gl.push_back(j * npb + pm[i]);
+        for (int t = 0; t < nnear; ++t) gl.push_back(j * npb + b + t);
+        tiles(oWB[j], b, ro, ro, b, npb);            // W_B: rows B_RS, cols [B_RS | N]
+        tiles(oWN[j], nnear, ro + b, ro, nnear, b);  // W_N: rows N, cols B_RS
+        CopyTask c{};
+        c.src = (long long)j * tcap;
+        c.lds = std::max(kk, 1);
+        c.dst = oT[j];
+        c.ldd = std::max(kk, 1);
+        c.rows = kk;
+        c.cols = r;
+        c.rmap_off = c.cmap_off = -1;
+        if (kk > 0) cpT.push_back(c);
+        CopyTask x{};
+        x.src = oWB[j];
+        x.lds = b;
+        x.dst = oXi[j];
+        x.ldd = r;
+        x.rows = r;
+        x.cols = r;
+        x.rmap_off = x.cmap_off = -1;
+        cpX.push_back(x);
+      }
+      slot.assign(gl.size(), -1);
+      pos.assign(gl.size(), 0);
+      std::vector<long long> tab(1, -1);
+      std::vector<int> bld(1, 0), maps(1, 0);
+      split_copy_tasks(cpT);
+      split_copy_tasks(cpX);
+      Stage sb;
+      size_t o_t = sb.add(bt), o_g = sb.add(gl), o_s = sb.add(slot), o_p = sb.add(pos), o_tb = sb.add(tab),
+             o_bl = sb.add(bld), o_ct = sb.add(cpT), o_cx = sb.add(cpX), o_m = sb.add(maps);
+      sb.upload(st);
+      int bid = h->prof.begin(FMMLU_K_BUILD, st);
+      launch_build(sb.ptr<BuildTask>(o_t), (int)bt.size(), sb.ptr<int>(o_g), sb.ptr<int>(o_s), sb.ptr<int>(o_p),
+                   sb.ptr<long long>(o_tb), sb.ptr<int>(o_bl), nullptr, W, g, k, st);
+      h->prof.end(bid, st);
+      h->prof.add(FMMLU_K_BUILD, 70.0 * (double)wsW, 16.0 * (double)wsW, 1);
+      launch_copy(sb.ptr<CopyTask>(o_ct), (int)cpT.size(), sb.ptr<int>(o_m), Tb.as<cplx>(), Fp, st);
+      std::vector<GemmProblem> gp;
+      std::vector<GemmTile> gt;
+      for (int j : el) {  // E: W_B[R,:] −= Tᵀ W_B[S,:]
+        const int kk = hk[j], r = b - kk;
+        GemmProblem P{};
+        P.m = r;
+        P.n = npb;
+        P.k = kk;
+        P.opA = kOpT;
+        P.opB = kOpN;
+        P.A = Fp + oT[j];
+        P.lda = std::max(kk, 1);
+        P.B = W + oWB[j] + r;
+        P.ldb = b;
+        P.C = W + oWB[j];
+        P.ldc = b;
+        add_gemm(gp, gt, P);
+      }
+      run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_EF);
+      for (int j : el) {  // F: W_B[:,R] −= W_B[:,S] T ;  W_N[:,R] −= W_N[:,S] T
+        const int kk = hk[j], r = b - kk;
+        GemmProblem P{};
+        P.m = b;
+        P.n = r;
+        P.k = kk;
+        P.opA = kOpN;
+        P.opB = kOpN;
+        P.A = W + oWB[j] + (long long)r * b;
+        P.lda = b;
+        P.B = Fp + oT[j];
+        P.ldb = std::max(kk, 1);
+        P.C = W + oWB[j];
+        P.ldc = b;
+        add_gemm(gp, gt, P);
+        GemmProblem Q = P;
+        Q.m = nnear;
+        Q.A = W + oWN[j] + (long long)r * nnear;
+        Q.lda = nnear;
+        Q.C = W + oWN[j];
+        Q.ldc = nnear;
+        add_gemm(gp, gt, Q);
+      }
+      run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_EF);
+      launch_copy(sb.ptr<CopyTask>(o_cx), (int)cpX.size(), sb.ptr<int>(o_m), W, Fp, st);
+      {
+        std::vector<std::pair<cplx*, int>> mats;
+        for (int j : el) mats.push_back({Fp + oXi[j], b - hk[j]});
+        gj_blocked(h, mats, status.as<int>(), keep, FMMLU_K_INV);
+      }
+      for (int j : el) {  // Up = X_RR⁻¹ X_{R(S∪N)} ;  Lp = X_{(S∪N)R} X_RR⁻¹
+        const int kk = hk[j], r = b - kk, kn = kk + nnear;
+        GemmProblem P{};
+        P.m = r;
+        P.n = kn;
+        P.k = r;
+        P.opA = kOpN;
+        P.opB = kOpN;
+        P.A = Fp + oXi[j];
+        P.lda = r;
+        P.B = W + oWB[j] + (long long)r * b;
+        P.ldb = b;
+        P.C = Fp + oUp[j];
+        P.ldc = r;
+        add_gemm(gp, gt, P);
+        if (kk > 0) {
+          GemmProblem Q{};
+          Q.m = kk;
+          Q.n = r;
+          Q.k = r;
+          Q.opA = kOpN;
+          Q.opB = kOpN;
+          Q.A = W + oWB[j] + r;
+          Q.lda = b;
+          Q.B = Fp + oXi[j];
+          Q.ldb = r;
+          Q.C = Fp + oLp[j];
+          Q.ldc = kn;
+          add_gemm(gp, gt, Q);
+        }
+        GemmProblem R{};
+        R.m = nnear;
+        R.n = r;
+        R.k = r;
+        R.opA = kOpN;
+        R.opB = kOpN;
+        R.A = W + oWN[j];
+        R.lda = nnear;
+        R.B = Fp + oXi[j];
+        R.ldb = r;
+        R.C = Fp + oLp[j] + kk;
+        R.ldc = kn;
+        add_gemm(gp, gt, R);
+      }
+      run_gemms(gp, gt, p1, 0, nullptr, st, keep, h->prof, FMMLU_K_PANEL);
+      for (int j : el) {  // Δ = −Lp · X_{R(S∪N)}  (private per-box buffer, C21)
+        const int kk = hk[j], r = b - kk, kn = kk + nnear;
+        GemmProblem P{};
+        P.m = kn;
+        P.n = kn;
+        P.k = r;
+        P.opA = kOpN;
+        P.opB = kOpN;
+        P.A = Fp + oLp[j];
+        P.lda = kn;
+        P.B = W + oWB[j] + (long long)r * b;
+        P.ldb = b;
+        P.C = D + oD[j];
+        P.ldc = kn;
+        add_gemm(gp, gt, P);
+      }
+      run_gemms(gp, gt, m1, 0, nullptr, st, keep, h->prof, FMMLU_K_SCHUR);
+      keep.push_back(std::move(sb.dev));
+      if (const char* dump = getenv("FMMLU_DEBUG_DUMP_W")) {  // diagnostics: W_B | W_N | Xi of el[0]
+        const int j = el[0], r = b - hk[j];
+        std::vector<cplx> t0((size_t)b * npb + (size_t)nnear * b + (size_t)r * r);
+        FMMLU_CUDA(cudaStreamSynchronize(st));
+        FMMLU_CUDA(cudaMemcpy(t0.data(), W + oWB[j], ((size_t)b * npb + (size_t)nnear * b) * sizeof(cplx),
+                              cudaMemcpyDeviceToHost));
+        FMMLU_CUDA(cudaMemcpy(t0.data() + (size_t)b * npb + (size_t)nnear * b, Fp + oXi[j], (size_t)r * r * sizeof(cplx),
+                              cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(dump, "wb")) {
+          fwrite(t0.data(), sizeof(cplx), t0.size(), f);
+          fclose(f);
+        }
+      }
+    }
+    // ---- outputs of the wave
+    if (rk_dev) h2d(ranks + w0, hk.data(), nw * sizeof(int), st);
+    else std::memcpy(ranks + w0, hk.data(), nw * sizeof(int));
+    if (perm) {
+      if (pm_dev) FMMLU_CUDA(cudaMemcpyAsync(perm + (size_t)w0 * b, permd.p, (size_t)nw * b * sizeof(int),
+                                             cudaMemcpyDeviceToDevice, st));
+      else std::memcpy(perm + (size_t)w0 * b, hp.data(), (size_t)nw * b * sizeof(int));
+    }
+    if (delta)
+      for (int j = 0; j < nw; ++j) {
+        auto it = kslot.find(w0 + j);
+        if (it == kslot.end()) continue;
+        const int kk = hk[j], kn = kk + nnear;
+        cplx* out = reinterpret_cast<cplx*>(delta) + (size_t)it->second * npb * npb;
+        if (b - kk <= 0) {  // nothing eliminated: Δ = 0
+          if (dl_dev) FMMLU_CUDA(cudaMemsetAsync(out, 0, (size_t)kn * kn * sizeof(cplx), st));
+          else std::memset(out, 0, (size_t)kn * kn * sizeof(cplx));
+          continue;
+        }
+        FMMLU_CUDA(cudaMemcpyAsync(out, D + oD[j], (size_t)kn * kn * sizeof(cplx),
+                                   dl_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+      }
+    wait_stream(h, st);
+    h->prof.resolve();
+  }
+  FMMLU_CUDA(cudaEventRecord(e1, st));
+  int sing = 0;
+  FMMLU_CUDA(cudaMemcpyAsync(&sing, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FMMLU_CUDA(cudaStreamSynchronize(st));
+  float t = 0.f;
+  FMMLU_CUDA(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (timing) {
+    timing[0] = t;
+    timing[1] = model * 1e-9;
+    timing[2] = wave;
+  }
+  if (sing) throw Error(FMMLU_ESINGULAR, "exactly singular X_RR pivot in fmmlu_boxes");
+}
+
 }  // namespace
 
 // ============================================================================ C ABI
@@ -2055,6 +2462,38 @@ int fmmlu_inverse_batch(fmmlu_handle* h, void* A, int n, int count, double* ms) 
   if (rc != FMMLU_OK) return rc;
   if (sing) return fail(FMMLU_ESINGULAR, "exactly singular pivot in fmmlu_inverse_batch");
   return FMMLU_OK;
+}
+
+int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const double* nnrm, int nbox, int b,
+                int nnear, double w, double k, double eps, int n_gamma, double rho, int* ranks, int* perm,
+                int nkeep, const int* keep, void* delta, double* timing) {
+  if (!pts || !nrm || !npts || !nnrm || !ranks) return fail(FMMLU_EINVAL, "NULL argument");
+  if (nbox < 1 || b < 1 || nnear < 0 || n_gamma < 1) return fail(FMMLU_EINVAL, "bad sizes");
+  if (!(w > 0) || !(rho > 0) || !std::isfinite(k) || k < 0) return fail(FMMLU_EINVAL, "bad w / rho / k");
+  if (!(eps > 0 && eps < 1)) return fail(FMMLU_EINVAL, "eps must lie in (0, 1)");
+  if (nkeep < 0 || (nkeep > 0 && (!keep || !delta))) return fail(FMMLU_EINVAL, "bad keep / delta");
+  for (int j = 0; j < nkeep; ++j)
+    if (keep[j] < 0 || keep[j] >= nbox) return fail(FMMLU_EINVAL, "keep id out of range");
+  fmmlu_handle* h = nullptr;
+  int rc = guarded([&] {
+    ensure_device();
+    h = new fmmlu_handle();
+    FMMLU_CUDA(cudaGetDevice(&h->dev));
+    FMMLU_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    // Δ is this workload's output, and it multiplies T by A_SS: use the backward-stable
+    // Householder ID (T accurate to u·cond(M_S)) rather than the Gram path (u·cond(M_S)²)
+    h->id_mode = 1;
+    if (const char* e = getenv("FMMLU_BOXES_ID_MODE")) h->id_mode = atoi(e);
+    boxes_impl(h, pts, nrm, npts, nnrm, nbox, b, nnear, w, k, eps, n_gamma, rho, ranks, perm, nkeep, keep, delta,
+               timing);
+  });
+  if (h) {
+    cudaStreamSynchronize(h->stream);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    delete h;
+  }
+  return rc;
 }
 
 int fmmlu_destroy(fmmlu_handle* h) {

@@ -1728,6 +1728,35 @@ __global__ void k_probe_dmma(double* out, int iters) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+// cfg4 geometry (readings C21/C22): box i's points are [b box points | nnear near points]
+// at global index i·(b+nnear) + t; SoA out = x | y | z | nx | ny | nz | √w (7 × np doubles).
+__global__ void k_box_geo(const double* __restrict__ pts, const double* __restrict__ nrm,
+                          const double* __restrict__ npts, const double* __restrict__ nnrm, int nbox, int b,
+                          int nnear, double sw, double* __restrict__ out) {
+  const long long np = (long long)nbox * (b + nnear);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < np; e += (long long)gridDim.x * blockDim.x) {
+    const long long box = e / (b + nnear);
+    const int t = (int)(e - box * (b + nnear));
+    const double* p = t < b ? pts + (box * b + t) * 3 : npts + (box * nnear + (t - b)) * 3;
+    const double* q = t < b ? nrm + (box * b + t) * 3 : nnrm + (box * nnear + (t - b)) * 3;
+    out[e] = p[0];
+    out[np + e] = p[1];
+    out[2 * np + e] = p[2];
+    out[3 * np + e] = q[0];
+    out[4 * np + e] = q[1];
+    out[5 * np + e] = q[2];
+    out[6 * np + e] = sw;
+  }
+}
+
+void launch_box_geo(const double* pts, const double* nrm, const double* npts, const double* nnrm, int nbox, int b,
+                    int nnear, double sw, double* out, cudaStream_t st) {
+  const long long np = (long long)nbox * (b + nnear);
+  const int grid = (int)std::min<long long>((np + 255) / 256, 148 * 16);
+  k_box_geo<<<grid, 256, 0, st>>>(pts, nrm, npts, nnrm, nbox, b, nnear, sw, out);
+  FMMLU_LAUNCH();
+}
+
 void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const int* slot,
                   const int* pos, const long long* tab, const int* bld, const cplx* src_arena,
                   cplx* dst_arena, const Geo& g, double k, cudaStream_t st) {

@@ -188,5 +188,8 @@ void launch_permute_out(const cplx* src, cplx* dst, int ld_dst, int n, int nrhs,
 void launch_matvec(const Geo& g, double k, int n, const cplx* x, cplx* y, int nrhs,
                    cudaStream_t st);
 double probe_fp64(int kind);
+// cfg4: row-major per-box geometry → SoA (x|y|z|nx|ny|nz|√w), box i at [i·(b+nnear), (i+1)·(b+nnear))
+void launch_box_geo(const double* pts, const double* nrm, const double* npts, const double* nnrm, int nbox, int b,
+                    int nnear, double sw, double* out, cudaStream_t st);
 
 }  // namespace fmmlu

@@ -52,7 +52,7 @@ KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur"
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
-           "fmmlu_set_param", "fmmlu_inverse_batch")
+           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes")
 
 
 def lib_path() -> str:
@@ -84,6 +84,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_probe_fp64.argtypes = [ci, ctypes.POINTER(cd)]
     L.fmmlu_set_param.argtypes = [vp, ctypes.c_char_p, cd]
     L.fmmlu_inverse_batch.argtypes = [vp, vp, ci, ci, ctypes.POINTER(cd)]
+    L.fmmlu_boxes.argtypes = [vp, vp, vp, vp, ci, ci, ci, cd, cd, cd, ci, cd, vp, vp, ci, vp, vp, vp]
     for f in EXPORTS:
         getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
     _LIB = L
@@ -199,3 +200,30 @@ def probe_fp64(kind: int) -> float:
     v = ctypes.c_double()
     _check(load().fmmlu_probe_fp64(int(kind), ctypes.byref(v)))
     return v.value
+
+
+def boxes(pts, nrm, npts, nnrm, w: float, k: float, eps: float, n_gamma: int, rho: float,
+          keep=(), want_perm: bool = True):
+    """cfg4 batched ID + elimination of independent boxes (fmmlu_boxes).  Arrays (NumPy or torch,
+    host or device): pts/nrm (nbox, b, 3), npts/nnrm (nbox, nnear, 3).  Returns dict(ranks, perm,
+    delta: {box id: Δ (k+nnear)²}, ms, gflop, wave)."""
+    L = load()
+    arrs = [_f64_rows3(a) for a in (pts, nrm, npts, nnrm)]
+    nbox, b = int(arrs[0].shape[0]), int(arrs[0].shape[1])
+    nnear = int(arrs[2].shape[1])
+    ranks = np.zeros(nbox, dtype=np.int32)
+    perm = np.zeros((nbox, b), dtype=np.int32) if want_perm else None
+    keep = np.asarray(list(keep), dtype=np.int32)
+    npb = b + nnear
+    delta = np.zeros((max(1, keep.size), npb * npb), dtype=np.complex128)
+    timing = (ctypes.c_double * 3)()
+    _check(L.fmmlu_boxes(_ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), _ptr(arrs[3]), nbox, b, nnear, float(w),
+                         float(k), float(eps), int(n_gamma), float(rho), ranks.ctypes.data,
+                         perm.ctypes.data if perm is not None else None, int(keep.size),
+                         keep.ctypes.data if keep.size else None, delta.ctypes.data if keep.size else None,
+                         timing))
+    out = {}
+    for j, bid in enumerate(keep.tolist()):
+        kn = int(ranks[bid]) + nnear
+        out[bid] = delta[j, :kn * kn].reshape(kn, kn, order="F")
+    return dict(ranks=ranks, perm=perm, delta=out, ms=timing[0], gflop=timing[1], wave=int(timing[2]))
