@@ -68,10 +68,12 @@ double wall_ms() {
 }
 
 // Process-wide cache of large device blocks.  Repeated factorizations ask for the same large
-// buffers (level block stores, workspaces); returning them to cudaMallocAsync's pool and
+// buffers (level block stores, workspaces); handing them back to cudaMallocAsync's pool and
 // re-requesting them occasionally stalls the host for hundreds of ms (pool growth / reclaim),
-// so blocks ≥ kBigBlock are kept here.  Reuse is stream-ordered: an event recorded at release
-// is waited on by the next user's stream.  A failed allocation flushes the cache and retries.
+// so blocks ≥ kBigBlock are kept here (allocated from, and evicted to, the async pool).  Reuse
+// is stream-ordered: an event recorded at release is waited on by the next user's stream.  The
+// cache holds at most kBigCap bytes (oldest blocks are evicted first); a failed allocation
+// evicts everything and retries.
 constexpr size_t kBigBlock = 32u << 20;
 struct BigCache {
   struct Blk {
@@ -79,8 +81,10 @@ struct BigCache {
     size_t bytes;
     cudaEvent_t ev;
   };
+  size_t cap = 0;  // 60 % of device memory (set on first use)
   std::mutex mu;
-  std::vector<Blk> free_;
+  std::vector<Blk> free_;  // oldest first
+  size_t held = 0;
   void* take(size_t b, cudaStream_t st, size_t* got) {
     std::lock_guard<std::mutex> lk(mu);
     int best = -1;
@@ -91,26 +95,42 @@ struct BigCache {
     if (best < 0) return nullptr;
     Blk k = free_[best];
     free_.erase(free_.begin() + best);
+    held -= k.bytes;
     cudaStreamWaitEvent(st, k.ev, 0);
     cudaEventDestroy(k.ev);
     *got = k.bytes;
     return k.p;
+  }
+  // caller holds mu; st = a live stream of the caller (the releasing stream may be gone)
+  void evict_front(cudaStream_t st) {
+    Blk k = free_.front();
+    free_.erase(free_.begin());
+    held -= k.bytes;
+    cudaStreamWaitEvent(st, k.ev, 0);
+    cudaFreeAsync(k.p, st);
+    cudaEventDestroy(k.ev);
   }
   void give(void* p, size_t bytes, cudaStream_t st) {
     cudaEvent_t ev;
     cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     cudaEventRecord(ev, st);
     std::lock_guard<std::mutex> lk(mu);
-    free_.push_back({p, bytes, ev});
-  }
-  void flush() {
-    std::lock_guard<std::mutex> lk(mu);
-    for (auto& k : free_) {
-      cudaEventSynchronize(k.ev);
-      cudaEventDestroy(k.ev);
-      cudaFree(k.p);
+    if (cap == 0) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      cap = tot / 10 * 6;
     }
-    free_.clear();
+    free_.push_back({p, bytes, ev});
+    held += bytes;
+    while (held > cap && free_.size() > 1) evict_front(st);
+  }
+  void flush(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(mu);
+    while (!free_.empty()) evict_front(st);
+  }
+  size_t cached() {
+    std::lock_guard<std::mutex> lk(mu);
+    return held;
   }
 };
 BigCache& big_cache() {
@@ -145,7 +165,7 @@ struct DBuf {
     return *this;
   }
   ~DBuf() { release(); }
-  bool big = false;  // from / back to the big-block cache (plain cudaMalloc memory)
+  bool big = false;  // from / back to the big-block cache
   void release() {
     if (p) {
       const double t0 = wall_ms();
@@ -169,11 +189,11 @@ struct DBuf {
       p = big_cache().take(b, s, &got);
       if (!p) {
         got = (b + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
-        e = cudaMalloc(&p, got);
+        e = cudaMallocAsync(&p, got, s);
         if (e != cudaSuccess) {  // give the cached blocks back and retry once
           cudaGetLastError();
-          big_cache().flush();
-          e = cudaMalloc(&p, got);
+          big_cache().flush(s);
+          e = cudaMallocAsync(&p, got, s);
         }
       }
       big = e == cudaSuccess;
@@ -369,6 +389,7 @@ struct fmmlu_handle {
   std::vector<char> topo_ready;
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
   int gj_mode = 0;           // 0 auto (shared-memory GJ when it fits), 1 blocked panel GJ always
+  int id_refine = 0;         // 1: one corrected-seminormal-equations step on the Gram-path T
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
 };
 
@@ -841,9 +862,15 @@ struct LevelBSR {
 // Gram G = MᴴM (DMMA, upper tiles + mirror) + pivoted Cholesky (cluster, or global-memory
 // blocked for big b); otherwise Householder TSQR rounds + cluster CPQR.  mfin[j] = rows of the
 // matrix the pivoted pass ran on (flop accounting).  May overwrite M.
+struct IdAux {  // Gram path: R' = [R11 R12] over G (ld b) per box, for the refinement step
+  bool gram = false;
+  DBuf G;
+  std::vector<long long> goff;
+};
+
 void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, const std::vector<int>& bcol,
               const std::vector<int>& pofs, const std::vector<long long>& tofs, double eps, int* permd, int* kd,
-              cplx* Tb, std::vector<DBuf>& keep, std::vector<int>& mfin) {
+              cplx* Tb, std::vector<DBuf>& keep, std::vector<int>& mfin, IdAux* aux = nullptr) {
   cudaStream_t st = h->stream;
   const int nj = (int)mp.size();
   int bmax = 1;
@@ -936,7 +963,134 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
     keep.push_back(std::move(s2.dev));
   }
-  keep.push_back(std::move(G));
+  if (aux && gram && done_id && h->id_mode != 1) {
+    aux->gram = true;
+    aux->G = std::move(G);
+    aux->goff.clear();
+    long long o = 0;
+    for (int j = 0; j < nj; ++j) {
+      aux->goff.push_back(o);
+      o += (long long)bcol[j] * bcol[j];
+    }
+  } else {
+    keep.push_back(std::move(G));
+  }
+}
+
+// One corrected-seminormal-equations step for the Gram-path T (R4): E = M_R − M_S T from M
+// itself (columns gathered into [S | R] order), Z = M_Sᴴ E, T += R11⁻¹ R11⁻ᴴ Z.  Brings T from
+// u·cond(M_S)² to ≈ u·cond(M_S) accuracy.  Called after the ranks/pivots reached the host.
+void refine_T(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<int>& mrows,
+              const std::vector<int>& bcol, const std::vector<int>& kv, const std::vector<int>& hperm,
+              const std::vector<int>& pofs, cplx* Tb, const std::vector<long long>& tofs, const IdAux& aux,
+              std::vector<DBuf>& keep) {
+  cudaStream_t st = h->stream;
+  std::vector<int> sel;
+  long long mg = 0, zs = 0;
+  int kmax = 1, rmax = 0;
+  for (int j = 0; j < (int)mp.size(); ++j) {
+    const int kk = kv[j], r = bcol[j] - kk;
+    if (kk <= 0 || r <= 0) continue;
+    sel.push_back(j);
+    mg += (long long)mrows[j] * bcol[j];
+    zs += (long long)kk * r;
+    kmax = std::max(kmax, kk);
+    rmax = std::max(rmax, r);
+  }
+  if (sel.empty()) return;
+  DBuf Mg, Zb;
+  Mg.alloc((size_t)mg * sizeof(cplx), st);
+  Zb.alloc((size_t)zs * sizeof(cplx), st);
+  FMMLU_CUDA(cudaMemsetAsync(Zb.p, 0, (size_t)zs * sizeof(cplx), st));
+  std::vector<CopyTask> cps;
+  std::vector<int> maps;
+  std::vector<long long> omg(mp.size()), oz(mp.size());
+  long long a = 0, z = 0;
+  for (int j : sel) {
+    omg[j] = a;
+    a += (long long)mrows[j] * bcol[j];
+    oz[j] = z;
+    z += (long long)kv[j] * (bcol[j] - kv[j]);
+    CopyTask c{};
+    c.src = mp[j] - mp[sel[0]];  // offsets relative to the first matrix (one M arena)
+    c.lds = mrows[j];
+    c.dst = omg[j];
+    c.ldd = mrows[j];
+    c.rows = mrows[j];
+    c.cols = bcol[j];
+    c.rmap_off = -1;
+    c.cmap_off = (int)maps.size();
+    maps.insert(maps.end(), hperm.begin() + pofs[j], hperm.begin() + pofs[j] + bcol[j]);
+    cps.push_back(c);
+  }
+  split_copy_tasks(cps);
+  Stage s;
+  size_t o_c = s.add(cps), o_m = s.add(maps);
+  s.upload(st);
+  int id = h->prof.begin(FMMLU_K_CPQR, st);
+  launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), mp[sel[0]], Mg.as<cplx>(), st);
+  h->prof.end(id, st);
+  std::vector<GemmProblem> gp;
+  std::vector<GemmTile> gt;
+  cplx* MG = Mg.as<cplx>();
+  for (int j : sel) {  // E = M_R − M_S T (in place over the gathered M_R)
+    const int kk = kv[j], r = bcol[j] - kk, m = mrows[j];
+    GemmProblem P{};
+    P.m = m;
+    P.n = r;
+    P.k = kk;
+    P.opA = kOpN;
+    P.opB = kOpN;
+    P.A = MG + omg[j];
+    P.lda = m;
+    P.B = Tb + tofs[j];
+    P.ldb = kk;
+    P.C = MG + omg[j] + (long long)kk * m;
+    P.ldc = m;
+    add_gemm(gp, gt, P);
+  }
+  run_gemms(gp, gt, cmk(-1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR);
+  for (int j : sel) {  // Z = M_Sᴴ E
+    const int kk = kv[j], r = bcol[j] - kk, m = mrows[j];
+    GemmProblem P{};
+    P.m = kk;
+    P.n = r;
+    P.k = m;
+    P.opA = kOpC;
+    P.opB = kOpN;
+    P.A = MG + omg[j];
+    P.lda = m;
+    P.B = MG + omg[j] + (long long)kk * m;
+    P.ldb = m;
+    P.C = Zb.as<cplx>() + oz[j];
+    P.ldc = kk;
+    P.kchunk = m > 512 ? 256 : 0;
+    add_gemm(gp, gt, P);
+  }
+  run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR);
+  std::vector<RefineTask> rt;
+  for (int j : sel) {
+    RefineTask t{};
+    t.R = aux.G.as<cplx>() + aux.goff[j];
+    t.ldr = bcol[j];
+    t.Z = Zb.as<cplx>() + oz[j];
+    t.T = Tb + tofs[j];
+    t.k = kv[j];
+    t.r = bcol[j] - kv[j];
+    t.kmax = kmax;
+    rt.push_back(t);
+  }
+  Stage s2;
+  size_t o_r = s2.add(rt);
+  s2.upload(st);
+  int id2 = h->prof.begin(FMMLU_K_CPQR, st);
+  launch_refine_T(s2.ptr<RefineTask>(o_r), (int)rt.size(), kmax, rmax, st);
+  h->prof.end(id2, st);
+  h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
+  keep.push_back(std::move(s.dev));
+  keep.push_back(std::move(s2.dev));
+  keep.push_back(std::move(Mg));
+  keep.push_back(std::move(Zb));
 }
 
 template <class J>
@@ -1941,7 +2095,8 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
                          8.0 * 13.0 * npb + 64.0 * b;
   size_t fr = 0, tot = 0;
   FMMLU_CUDA(cudaMemGetInfo(&fr, &tot));
-  const int wave = (int)std::max(1.0, std::min<double>({(double)nbox, 2048.0, 0.6 * fr / per_box}));
+  fr += big_cache().cached();  // cached blocks are reusable (or evicted on demand)
+  const int wave = (int)std::max(1.0, std::min<double>({(double)nbox, 1024.0, 0.45 * fr / per_box}));
   cudaEvent_t e0, e1;
   FMMLU_CUDA(cudaEventCreate(&e0));
   FMMLU_CUDA(cudaEventCreate(&e1));
@@ -1951,7 +2106,9 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
   status.alloc(16, st);
   FMMLU_CUDA(cudaMemsetAsync(status.p, 0, 16, st));
   const cplx m1 = cmk(-1.0, 0.0), p1 = cmk(1.0, 0.0);
+  static const bool trace = getenv("FMMLU_TRACE") != nullptr;
   for (int w0 = 0; w0 < nbox; w0 += wave) {
+    const double tw0 = now_ms(), ww0 = h->stats.t_sync_wait_ms;
     const int nw = std::min(wave, nbox - w0);
     const long long np = (long long)nw * npb;
     std::vector<DBuf> keep;
@@ -1978,6 +2135,10 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
     const Geo g{G7, G7 + np, G7 + 2 * np, G7 + 3 * np, G7 + 4 * np, G7 + 5 * np, G7 + 6 * np};
     // ---- M (proxy rows) and the ID
     DBuf M, Tb, permd, kd;
+    IdAux aux;
+    std::vector<cplx*> mp_keep;
+    std::vector<int> pofs_keep;
+    std::vector<long long> tofs_keep;
     M.alloc((size_t)nw * m * b * sizeof(cplx), st);
     Tb.alloc((size_t)nw * tcap * sizeof(cplx), st);
     permd.alloc((size_t)nw * b * sizeof(int), st);
@@ -2015,7 +2176,10 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
         pofs[j] = j * b;
         tofs[j] = (long long)j * tcap;
       }
-      id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin);
+      id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin, &aux);
+      mp_keep = mp;
+      pofs_keep = pofs;
+      tofs_keep = tofs;
     }
     std::vector<int> hk(nw), hp((size_t)nw * b);
     int* pin = h->d2h(nw + (size_t)nw * b);
@@ -2033,7 +2197,9 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
       }
     }
     h->prof.resolve();
-    M.release();
+    if (aux.gram && h->id_refine)
+      refine_T(h, mp_keep, std::vector<int>(nw, m), std::vector<int>(nw, b), hk, hp, pofs_keep, Tb.as<cplx>(),
+               tofs_keep, aux, keep);
     // ---- elimination
     std::vector<int> el;
     long long wsW = 0, wsF = 0, wsD = 0;
@@ -2281,6 +2447,20 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
       }
     wait_stream(h, st);
     h->prof.resolve();
+    if (trace) {
+      fprintf(stderr, "[fmmlu boxes] wave %d (%d boxes): %.1f ms (host %.1f, wait %.1f) | allocator: %.1f ms in %lld "
+                      "calls (max %.1f), cached %.1f GB\n",
+              w0 / wave, nw, now_ms() - tw0, now_ms() - tw0 - (h->stats.t_sync_wait_ms - ww0),
+              h->stats.t_sync_wait_ms - ww0, g_ac.alloc_ms, g_ac.nalloc, g_ac.alloc_max, big_cache().cached() / 1e9);
+      g_ac = AllocClock{};
+    }
+  }
+  if (trace) {
+    fprintf(stderr, "[fmmlu boxes] gpu ms by class:");
+    static const char* nm[10] = {"build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve"};
+    for (int c = 0; c < 10; ++c)
+      if (h->prof.ms[c] > 0.005) fprintf(stderr, " %s %.1f", nm[c], h->prof.ms[c]);
+    fprintf(stderr, "\n");
   }
   FMMLU_CUDA(cudaEventRecord(e1, st));
   int sing = 0;
@@ -2481,10 +2661,13 @@ int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const 
     FMMLU_CUDA(cudaGetDevice(&h->dev));
     FMMLU_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
-    // Δ is this workload's output, and it multiplies T by A_SS: use the backward-stable
-    // Householder ID (T accurate to u·cond(M_S)) rather than the Gram path (u·cond(M_S)²)
-    h->id_mode = 1;
+    // Δ is this workload's output and multiplies T by A_SS: T must be accurate to ≈ u·cond(M_S).
+    // Gram path (ε ≥ 1e-7) + one corrected-seminormal-equations step gives that at GEMM speed;
+    // the Householder path (ε < 1e-7) has it by construction.
+    h->id_mode = 0;
+    h->id_refine = 1;
     if (const char* e = getenv("FMMLU_BOXES_ID_MODE")) h->id_mode = atoi(e);
+    if (const char* e = getenv("FMMLU_BOXES_REFINE")) h->id_refine = atoi(e);
     boxes_impl(h, pts, nrm, npts, nnrm, nbox, b, nnear, w, k, eps, n_gamma, rho, ranks, perm, nkeep, keep, delta,
                timing);
   });
@@ -2539,6 +2722,9 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
     if (value != 0 && value != 1 && value != 2 && value != 3)
       return fail(FMMLU_EINVAL, "id_mode must be 0, 1, 2 or 3");
     h->id_mode = (int)value;
+  } else if (k == "id_refine") {
+    if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "id_refine must be 0 or 1");
+    h->id_refine = (int)value;
   } else if (k == "gj_mode") {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "gj_mode must be 0 or 1");
     h->gj_mode = (int)value;

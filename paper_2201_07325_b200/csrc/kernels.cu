@@ -2064,6 +2064,56 @@ void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int
   }
 }
 
+// One corrected-seminormal-equations step for the Gram-path ID (R4): with
+// R11ᴴR11 = G_SS from the pivoted Cholesky and Z = M_Sᴴ(M_R − M_S T) formed from M itself,
+// T ← T + R11⁻¹ R11⁻ᴴ Z.  grid (ntasks, ceil(rmax/16)), one warp per column of T.
+__global__ void __launch_bounds__(512) k_refine_T(const RefineTask* __restrict__ tasks) {
+  extern __shared__ double shm[];
+  const RefineTask t = tasks[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y * 16 + warp;
+  if (c >= t.r) return;
+  const int kk = t.k;
+  cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)warp * t.kmax;
+  for (int i = lane; i < kk; i += 32) x[i] = t.Z[i + (size_t)c * kk];
+  __syncwarp();
+  for (int l = 0; l < kk; ++l) {  // R11ᴴ y = z  (forward; (R11ᴴ)_{il} = conj(R11_{li}))
+    const cplx d = t.R[l + (size_t)l * t.ldr];
+    const cplx yl = cdiv(x[l], cmk(d.x, -d.y));
+    __syncwarp();
+    if (lane == 0) x[l] = yl;
+    for (int i = l + 1 + lane; i < kk; i += 32) {
+      const cplx rli = t.R[l + (size_t)i * t.ldr];
+      x[i] = cfms(cmk(rli.x, -rli.y), yl, x[i]);
+    }
+    __syncwarp();
+  }
+  for (int l = kk - 1; l >= 0; --l) {  // R11 δ = y  (backward)
+    const cplx xl = cdiv(x[l], t.R[l + (size_t)l * t.ldr]);
+    __syncwarp();
+    if (lane == 0) x[l] = xl;
+    for (int i = lane; i < l; i += 32) x[i] = cfms(t.R[i + (size_t)l * t.ldr], xl, x[i]);
+    __syncwarp();
+  }
+  for (int i = lane; i < kk; i += 32) {
+    cplx* d = t.T + i + (size_t)c * kk;
+    *d = cadd(*d, x[i]);
+  }
+}
+
+void launch_refine_T(const RefineTask* d_tasks, int ntasks, int kmax, int rmax, cudaStream_t st) {
+  if (ntasks <= 0 || rmax <= 0) return;
+  const size_t smem = 16 * (size_t)std::max(kmax, 1) * sizeof(cplx) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_refine_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  dim3 grid(ntasks, (rmax + 15) / 16);
+  k_refine_T<<<grid, 512, smem, st>>>(d_tasks);
+  FMMLU_LAUNCH();
+}
+
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st, int bmax) {
   if (ntasks <= 0) return;

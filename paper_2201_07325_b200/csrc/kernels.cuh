@@ -95,6 +95,14 @@ void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cpl
                  cplx* dst_arena, cudaStream_t st);
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
                   double k, cudaStream_t st);
+// One corrected-seminormal-equations refinement of T (Gram-path ID): T += R11⁻¹R11⁻ᴴ Z.
+struct RefineTask {
+  const cplx* R;  // R11 (k × k upper, ld ldr) from the pivoted Cholesky (R' layout over G)
+  const cplx* Z;  // M_Sᴴ (M_R − M_S T)  (k × r, ld k)
+  cplx* T;        // k × r, ld k, updated in place
+  int ldr, k, r, kmax;
+};
+void launch_refine_T(const RefineTask* d_tasks, int ntasks, int kmax, int rmax, cudaStream_t st);
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st, int bmax);
 // Blocked in-place Gauss-Jordan inverse (partial pivoting) of a batch of matrices.

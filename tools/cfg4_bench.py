@@ -11,7 +11,7 @@ d = fi.box_batch(nbox)
 print(f"inputs {time.perf_counter()-t:.1f} s", flush=True)
 rho = 1.5 * math.sqrt(3) / 2 * d["h"]
 for eps in epss:
-    F.boxes(d["pts"][:64], d["nrm"][:64], d["npts"][:64], d["nnrm"][:64], d["w"], 10.0, eps, 512, rho, want_perm=False)
+    F.boxes(d["pts"], d["nrm"], d["npts"], d["nnrm"], d["w"], 10.0, eps, 512, rho, want_perm=False)  # warm-up
     out = F.boxes(d["pts"], d["nrm"], d["npts"], d["nnrm"], d["w"], 10.0, eps, 512, rho, want_perm=False)
     r = out["ranks"]
     print(f"eps {eps:g}: {out['ms']:.1f} ms  {nbox/(out['ms']*1e-3):.0f} boxes/s  model {out['gflop']:.0f} GFLOP "
