@@ -148,6 +148,10 @@ int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
  *                   arithmetic; accurate while eps^2 >> unit roundoff)
  *               3 = as 2 but always with the global-memory blocked pivoted Cholesky
  *                   (the path used automatically for boxes beyond the cluster capacity)
+ *   "id_refine" 1 = one corrected-seminormal-equations step on the Gram-path T (T accurate to
+ *               u*cond(M_S) instead of u*cond(M_S)^2; R4); default 0
+ *   "pchol_mode" Gram-path pivoted Cholesky: 0 = register-resident kernel (b <= 512; default),
+ *               1 = shared-memory cluster kernel
  *   "gj_mode"   X_RR inverse (Gauss-Jordan, partial pivoting): 0 = auto (whole matrix resident
  *               in one CTA's or one <=16-CTA cluster's shared memory when it fits, blocked
  *               panel path otherwise; default), 1 = blocked panel path always

@@ -390,6 +390,7 @@ struct fmmlu_handle {
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
   int gj_mode = 0;           // 0 auto (shared-memory GJ when it fits), 1 blocked panel GJ always
   int id_refine = 0;         // 1: one corrected-seminormal-equations step on the Gram-path T
+  int pchol_mode = 0;        // 0 register-resident pivoted Cholesky (b ≤ 512), 1 shared-memory cluster kernel
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
 };
 
@@ -502,7 +503,13 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   }
   int nb = gj_panel_width(nmax);
   bool cluster_panel = false;
-  if (nb < 32 && nmax > 64) {  // tall blocks (root): panel rows spread over a cluster, nb up to 32
+  static const int panel_env = getenv("FMMLU_GJ_PANEL") ? atoi(getenv("FMMLU_GJ_PANEL")) : 0;
+  bool reg_panel = false;
+  if (panel_env == 0 && nb < 32 && nmax > 512 && gj_panel_reg_width(nmax) >= 32) {
+    // tall blocks (root): register-resident panel rows over a 16-CTA cluster, L2 exchange
+    nb = gj_panel_reg_width(nmax);
+    reg_panel = true;
+  } else if (panel_env <= 2 && panel_env != 1 && nb < 32 && nmax > 64) {  // shared-memory cluster panel
     for (int w = 32; w >= 8; w /= 2)
       if (gj_panel_cluster_size(nmax, w) > 0) {
         nb = w;
@@ -575,11 +582,15 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   Stage s;
   size_t o_t = s.add(tasks), o_s = s.add(soff), o_p = s.add(gp), o_g = s.add(gt);
   s.upload(st);
+  DBuf xsb;
+  if (reg_panel) xsb.alloc((size_t)tasks.size() * gj_panel_reg_scratch(nb) * sizeof(cplx), st);
   int id = h->prof.begin(cls, st);
   int pi = 0;
   long long nl = 0;
   for (int j0 = 0; j0 < nmax; j0 += nb, ++pi) {
-    if (cluster_panel)
+    if (reg_panel)
+      launch_gj_panel_reg(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, xsb.as<cplx>(), st, nmax);
+    else if (cluster_panel)
       launch_gj_panel_cluster(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, st, nmax);
     else
       launch_gj_panel(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, d_status, st, nmax);
@@ -597,6 +608,7 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   keep.push_back(std::move(s.dev));
   keep.push_back(std::move(cb));
   keep.push_back(std::move(ib));
+  keep.push_back(std::move(xsb));
 }
 
 // ---------------------------------------------------------------------------- large-box pivoted Cholesky
@@ -935,7 +947,16 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     size_t o_i = s2.add(ids), o_q = s2.add(cq);
     s2.upload(st);
     int cid = h->prof.begin(FMMLU_K_CPQR, st);
-    done_id = h->id_mode != 3 && launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
+    if (h->id_mode != 3) {
+      if (h->pchol_mode == 0 && pchol_reg_scratch(bmax) > 0) {  // register-resident pivoted Cholesky
+        DBuf xs;
+        xs.alloc((size_t)nj * pchol_reg_scratch(bmax) * sizeof(cplx), st);
+        done_id = launch_pchol_reg(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, xs.as<cplx>(), st, bmax);
+        keep.push_back(std::move(xs));
+      } else {
+        done_id = launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
+      }
+    }
     if (!done_id) {  // boxes too large for a cluster: global-memory blocked pivoted Cholesky
       pchol_big(h, G.as<cplx>(), goff, gsz, bcol, pofs, permd, kd, eps, keep);
       done_id = true;
@@ -2722,6 +2743,9 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
     if (value != 0 && value != 1 && value != 2 && value != 3)
       return fail(FMMLU_EINVAL, "id_mode must be 0, 1, 2 or 3");
     h->id_mode = (int)value;
+  } else if (k == "pchol_mode") {
+    if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "pchol_mode must be 0 or 1");
+    h->pchol_mode = (int)value;
   } else if (k == "id_refine") {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "id_refine must be 0 or 1");
     h->id_refine = (int)value;

@@ -341,6 +341,18 @@ __global__ void __launch_bounds__(GJ_NT) k_gj(const long long* __restrict__ offs
 // [GEMM] C_out += (Gp − E_J) · Y.  After the last panel the column interchanges are undone.
 constexpr int GJP_NT = 512;
 constexpr int CK_NT = 256;  // threads per CTA of the cluster kernels
+constexpr int GJR_NT = 512, GJR_NW = GJR_NT / 32, GJR_NMAX = 512;
+
+struct GjrCfg { int MR, MC, CL; };
+GjrCfg gjr_cfg(int nmax) {  // RG = ceil(n/(32 MR)) row groups, CG = 16/RG column groups
+  if (nmax <= 32) return {1, 2, 1};
+  if (nmax <= 64) return {1, 8, 1};
+  if (nmax <= 128) return {1, 16, 2};
+  if (nmax <= 256) return {1, 16, 8};
+  if (nmax <= 384) return {1, 24, 16};
+  return {2, 16, 16};  // ≤ 512
+}
+constexpr int GJR_NCAP = 512;
 
 __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ tasks, int j0, int nb,
                                                      int* status) {
@@ -516,6 +528,170 @@ __global__ void __launch_bounds__(CK_NT) k_gj_panel_cluster(const GjTask* __rest
   }
 }
 
+// Register-resident cluster version of the GJ panel step for tall blocks (the root): the n × jb
+// panel's rows are split over the CL CTAs (CTA c owns rows [c·rc, (c+1)·rc)), inside a CTA rows go
+// over (row group, lane) and panel columns over (column group, slot) as in k_gj_reg.  Per column:
+// [P1a] the warps holding column s take per-warp argmax candidates and publish the column values
+// of their rows; CTA barrier; [P1b] the CTA-local winner row and, if owned here, the old row j are
+// published to L2 (speculatively) with the candidate; ONE cluster barrier; [P2] every CTA reduces
+// the CL candidates and loads the pivot row and old row j; CTA barrier; [P3] interchange, scale,
+// eliminate in registers.  Same outputs as k_gj_panel_cluster.  grid (CL, ntasks), 512 threads;
+// xs = exchange scratch per task (xstride complex): [2][CL] candidates, [2][CL][nb] rows, [2][nb].
+template <int MC>
+__global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __restrict__ tasks, int j0, int nb,
+                                                           int* status, cplx* __restrict__ xs, long long xstride) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  __shared__ double wcv[2][GJR_NW];
+  __shared__ int wci[2][GJR_NW];
+  __shared__ cplx fcol[2][GJR_NMAX];   // column s of the own rows (by local row)
+  __shared__ cplx prow[64], orow[64];  // pivot row, old row j
+  __shared__ int sp[2];
+  const GjTask t = tasks[blockIdx.y];
+  const int n = t.n;
+  if (j0 >= n) return;  // uniform across the cluster
+  const int jb = min(nb, n - j0);
+  const int rc = (n + CL - 1) / CL;
+  const int r0 = rank * rc, r1 = min(n, r0 + rc);
+  const int RG = (rc + 31) >> 5, CG = GJR_NW / RG;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rg = warp % RG, cgp = warp / RG;
+  const int nq = cgp < CG ? min(MC, (jb - cgp + CG - 1) / CG) : 0;
+  const int il = rg * 32 + lane;      // local row
+  const int i = r0 + il;              // global row
+  const bool rowok = il < rc && i < r1;
+  cplx* const X = xs + blockIdx.y * xstride;
+  double* const xc = reinterpret_cast<double*>(X);          // [2][CL][2]
+  cplx* const xrow = X + 2 * CL;                            // [2][CL][nb]
+  cplx* const xold = xrow + 2 * (size_t)CL * nb;            // [2][nb]
+  cplx a[MC];
+#pragma unroll
+  for (int q = 0; q < MC; ++q) {
+    const int c = cgp + CG * q;
+    a[q] = (q < nq && rowok) ? t.A[i + (size_t)(j0 + c) * t.lda] : cmk(0.0, 0.0);
+  }
+  for (int s = 0; s < jb; ++s) {
+    const int j = j0 + s, par = s & 1;
+    // ---- P1a: the warps holding panel column s: per-warp candidates, column values to smem
+    if (cgp < CG && cgp == s % CG) {
+      const int qs = s / CG;
+      cplx x = a[0];
+#pragma unroll
+      for (int q = 1; q < MC; ++q)
+        if (q == qs) x = a[q];
+      if (rowok) fcol[par][il] = x;
+      double v = (rowok && i >= j) ? cabs2(x) : -1.0;
+      int ix = (rowok && i >= j) ? i : INT_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (v2 > v || (v2 == v && i2 < ix)) {
+          v = v2;
+          ix = i2;
+        }
+      }
+      if (lane == 0) {
+        wcv[par][rg] = v;
+        wci[par][rg] = ix;
+      }
+    }
+    __syncthreads();  // B0
+    // ---- P1b: CTA-local winner; publish its row, old row j (if here) and the candidate
+    double lv = lane < RG ? wcv[par][lane] : -1.0;
+    int li = lane < RG ? wci[par][lane] : INT_MAX;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, lv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, li, o);
+      if (v2 > lv || (v2 == lv && i2 < li)) {
+        lv = v2;
+        li = i2;
+      }
+    }
+    lv = __shfl_sync(0xffffffffu, lv, 0);
+    li = __shfl_sync(0xffffffffu, li, 0);
+    if (rowok && (i == li || i == j)) {
+#pragma unroll
+      for (int q = 0; q < MC; ++q) {
+        if (q >= nq) break;
+        const int c = cgp + CG * q;
+        if (i == li) __stcg(reinterpret_cast<double2*>(xrow + ((size_t)par * CL + rank) * nb + c), a[q]);
+        if (i == j) __stcg(reinterpret_cast<double2*>(xold + (size_t)par * nb + c), a[q]);
+      }
+    }
+    if (tid == 0) {
+      __stcg(xc + ((size_t)par * CL + rank) * 2, lv);
+      __stcg(reinterpret_cast<long long*>(xc + ((size_t)par * CL + rank) * 2 + 1), (long long)li);
+    }
+    cl.sync();  // B1
+    // ---- P2: global pivot row p (ties → lowest row), pivot row and old row j to smem
+    if (warp == 0) {
+      double pv = lane < CL ? __ldcg(xc + ((size_t)par * CL + lane) * 2) : -1.0;
+      int p = lane < CL ? (int)__ldcg(reinterpret_cast<const long long*>(xc + ((size_t)par * CL + lane) * 2 + 1))
+                        : INT_MAX;
+      int po = lane;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, pv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, p, o);
+        const int o2 = __shfl_xor_sync(0xffffffffu, po, o);
+        if (v2 > pv || (v2 == pv && i2 < p)) {
+          pv = v2;
+          p = i2;
+          po = o2;
+        }
+      }
+      if (lane == 0) {
+        const bool sing = !(pv > 0.0) || p == INT_MAX;
+        sp[0] = sing ? j : p;
+        sp[1] = sing ? -1 : po;
+        if (rank == 0) {
+          t.piv[j] = sing ? j : p;
+          if (sing) atomicExch(status, 1);
+        }
+      }
+    }
+    __syncthreads();
+    const int p = sp[0], po = sp[1];
+    for (int c = tid; c < jb; c += GJR_NT) {
+      orow[c] = __ldcg(reinterpret_cast<const double2*>(xold + (size_t)par * nb + c));
+      prow[c] = po >= 0 ? __ldcg(reinterpret_cast<const double2*>(xrow + ((size_t)par * CL + po) * nb + c))
+                        : orow[c];
+    }
+    __syncthreads();  // B2
+    // ---- P3: interchange rows j and p, scale row j, eliminate
+    const cplx d = prow[s];
+    const double rn = __drcp_rn(d.x * d.x + d.y * d.y);
+    const cplx dinv = po >= 0 ? cmk(d.x * rn, -d.y * rn) : cmk(1.0, 0.0);
+    if (rowok) {
+      const bool isj = i == j, isp = i == p && p != j;
+      const cplx f = isp ? orow[s] : fcol[par][il];
+#pragma unroll
+      for (int q = 0; q < MC; ++q) {
+        if (q >= nq) break;
+        const int c = cgp + CG * q;
+        const cplx rc_ = c == s ? dinv : cmul(prow[c], dinv);  // new row j
+        if (isj) {
+          a[q] = rc_;
+        } else {
+          const cplx old = isp ? orow[c] : a[q];
+          a[q] = c == s ? cmk(-(f.x * dinv.x - f.y * dinv.y), -(f.x * dinv.y + f.y * dinv.x)) : cfms(f, rc_, old);
+        }
+      }
+    }
+  }
+  // ---- write the panel back and Am = Gp − E_J (n × jb, ld n)
+#pragma unroll
+  for (int q = 0; q < MC; ++q) {
+    if (q >= nq || !rowok) break;
+    const int c = cgp + CG * q;
+    const cplx v = a[q];
+    t.A[i + (size_t)(j0 + c) * t.lda] = v;
+    t.Am[i + (size_t)c * n] = i == j0 + c ? cmk(v.x - 1.0, v.y) : v;
+  }
+}
+
 // Apply the panel's interchanges to every column outside J and gather their rows J into Y
 // (jb × n, ld nb).  grid (ceil(n/128), ntasks).
 __global__ void k_gj_swap(const GjTask* __restrict__ tasks, int j0, int nb) {
@@ -598,7 +774,6 @@ __global__ void k_gj_copyback(const GjTask* __restrict__ tasks, const cplx* __re
 // argmax candidates; barrier B1 (cluster barrier if CL > 1); [P2] everybody reduces the
 // candidates (DSMEM) → p, d; the lanes holding row p publish m_pc/d for their columns;
 // CTA barrier B2; [P3] register update.  grid (CL, ntasks), 512 threads.
-constexpr int GJR_NT = 512, GJR_NW = GJR_NT / 32, GJR_NMAX = 512;
 
 // Exchange record of one row group's pivot candidate: |x|², row, x.
 struct GjCand {
@@ -1100,6 +1275,204 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
     t.A[i + (size_t)c * t.lda] = (c < kk && i > c) ? cmk(0.0, 0.0) : Rg[i + (size_t)g * b];
   }
   for (int l = tid; l < ncl; l += CK_NT) perm_out[t.out_off + posmap[rank + l * CL]] = rank + l * CL;
+  if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+}
+
+// Pivoted Cholesky of the Gram matrix G = MᴴM (same semantics and outputs as k_pchol_cluster)
+// with the Schur complement S resident in REGISTERS: columns cyclic over the CL CTAs of a cluster
+// (CL = 1: a single CTA), inside a CTA the same (row group × column group) warp layout as
+// k_gj_reg.  Step j: every warp takes the CTA-local argmax of the diagonal (an O(ncl) shared
+// array); the warps holding that local candidate column publish it (speculatively) together with
+// the candidate; ONE barrier (cluster barrier + L2 exchange if CL > 1); every CTA reduces the CL
+// candidates, copies the winner's column p into shared memory, writes R_{j,c} = conj(S_cp)/√S_pp
+// for its columns and updates S_ac −= S_ap conj(S_cp)/S_pp in registers.  Stop rule C9 on the
+// diagonal (≤ ε²·initial max).  grid (CL, ntasks), 512 threads; xs = exchange scratch
+// ([2][CL][b] columns + [2][CL] candidates per task, task stride xstride complex).
+template <int MR, int MC, bool MULTI, bool TIMING = false>
+__global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __restrict__ tasks,
+                                                        int* __restrict__ perm_out, int* __restrict__ k_out,
+                                                        double eps, cplx* __restrict__ xs, long long xstride) {
+  constexpr int LGMR = MR == 1 ? 0 : 1;
+  long long tph[4] = {0, 0, 0, 0}, tc = 0;  // TIMING: P1 | B1+P2 (until p known) | colp+B2 | P3+B3
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = MULTI ? (int)cl.num_blocks() : 1, rank = MULTI ? (int)cl.block_rank() : 0;
+  const int lgCL = __ffs(CL) - 1;
+  __shared__ cplx colp[GJR_NMAX];                          // the pivot column (all b rows)
+  __shared__ cplx colx[MULTI ? 1 : 2][MULTI ? 1 : GJR_NMAX];  // single CTA: published column
+  __shared__ double dg[GJR_NMAX / 2 + 16];                 // diagonal of S, local columns
+  __shared__ int dn[GJR_NMAX / 2 + 16];                    // local column pivoted
+  __shared__ int piv[GJR_NMAX];
+  __shared__ int posmap[GJR_NMAX];
+  __shared__ double cvs[2];
+  __shared__ int cis[2];
+  const ClusterQrTask t = tasks[blockIdx.y];
+  const int b = t.b;
+  const int ncl = (b - rank + CL - 1) >> lgCL;
+  const int RG = (b + 32 * MR - 1) >> (5 + LGMR), CG = GJR_NW / RG;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rg = warp % RG, cgp = warp / RG;
+  const int nq = cgp < CG ? min(MC, (ncl - cgp + CG - 1) / CG) : 0;
+  const int row0 = (rg << (5 + LGMR)) + lane;
+  cplx* const xcol = MULTI ? xs + blockIdx.y * xstride : nullptr;                          // [2][CL][b]
+  double* const xcand = MULTI ? reinterpret_cast<double*>(xcol + 2 * (size_t)CL * b) : nullptr;  // [2][CL][2]
+  cplx* const Rg = t.out;  // b × b (ld b): R rows by natural column
+  cplx a[MC][MR];
+#pragma unroll
+  for (int q = 0; q < MC; ++q)
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int i = row0 + 32 * r;
+      a[q][r] = (q < nq && i < b) ? t.A[i + (size_t)(rank + ((cgp + CG * q) << lgCL)) * t.lda] : cmk(0.0, 0.0);
+    }
+  for (int l = tid; l < ncl; l += GJR_NT) {
+    const int g = rank + (l << lgCL);
+    dg[l] = t.A[g + (size_t)g * t.lda].x;
+    dn[l] = 0;
+  }
+  if (MULTI) cl.sync(); else __syncthreads();  // inputs loaded (G is overwritten at the end)
+  int kk = b;
+  double d0 = 0.0;
+  int jdone = 0;
+  for (int j = 0; j < b; ++j) {
+    if (TIMING) tc = clock64();
+    const int par = j & 1;
+    // ---- P1: CTA-local candidate (every warp computes it), its column published
+    double lv = -1.0;
+    int ll = INT_MAX;
+    for (int l = lane; l < ncl; l += 32)
+      if (!dn[l] && dg[l] > lv) {  // ascending l within a lane: strict > keeps the lowest
+        lv = dg[l];
+        ll = l;
+      }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, lv, s);
+      const int i2 = __shfl_xor_sync(0xffffffffu, ll, s);
+      if (v2 > lv || (v2 == lv && i2 < ll)) {
+        lv = v2;
+        ll = i2;
+      }
+    }
+    const int lg_ = ll == INT_MAX ? INT_MAX : rank + (ll << lgCL);  // global column of the candidate
+    if (ll != INT_MAX && cgp == ll % CG && cgp < CG) {
+      const int qs = ll / CG;
+      cplx* dst = MULTI ? xcol + ((size_t)par * CL + rank) * b : &colx[par & (MULTI ? 0 : 1)][0];
+#pragma unroll
+      for (int r = 0; r < MR; ++r) {
+        cplx x = a[0][r];
+#pragma unroll
+        for (int q = 1; q < MC; ++q)
+          if (q == qs) x = a[q][r];
+        const int i = row0 + 32 * r;
+        if (i < b) {
+          if (MULTI) __stcg(reinterpret_cast<double2*>(dst + i), x);
+          else dst[i] = x;
+        }
+      }
+    }
+    if (tid == 0) {
+      if (MULTI) {
+        __stcg(xcand + ((size_t)par * CL + rank) * 2, lv);
+        __stcg(reinterpret_cast<long long*>(xcand + ((size_t)par * CL + rank) * 2 + 1), (long long)lg_);
+      } else {
+        cvs[par] = lv;
+        cis[par] = lg_;
+      }
+    }
+    if (TIMING) { const long long n_ = clock64(); tph[0] += n_ - tc; tc = n_; }
+    if (MULTI) cl.sync(); else __syncthreads();  // B1
+    // ---- P2: global pivot (ties → lowest column) and its column into shared memory
+    double pv = -1.0;
+    int p = INT_MAX, po = 0;
+    if (MULTI) {
+      if (lane < CL) {
+        pv = __ldcg(xcand + ((size_t)par * CL + lane) * 2);
+        p = (int)__ldcg(reinterpret_cast<const long long*>(xcand + ((size_t)par * CL + lane) * 2 + 1));
+        po = lane;
+      }
+#pragma unroll
+      for (int s = 8; s > 0; s >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
+        const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
+        const int o2 = __shfl_xor_sync(0xffffffffu, po, s);
+        if (v2 > pv || (v2 == pv && i2 < p)) {
+          pv = v2;
+          p = i2;
+          po = o2;
+        }
+      }
+      pv = __shfl_sync(0xffffffffu, pv, 0);
+      p = __shfl_sync(0xffffffffu, p, 0);
+      po = __shfl_sync(0xffffffffu, po, 0);
+    } else {
+      pv = cvs[par];
+      p = cis[par];
+    }
+    if (TIMING) { const long long n_ = clock64() + (p & 0); tph[1] += n_ - tc; tc = n_; }
+    if (j == 0) d0 = pv;
+    if (!(pv > eps * eps * d0) || !(pv > 0.0) || p == INT_MAX) {
+      kk = j;
+      break;  // uniform: every CTA reads the same candidates
+    }
+    jdone = j + 1;
+    const cplx* src = MULTI ? xcol + ((size_t)par * CL + po) * b : &colx[par & (MULTI ? 0 : 1)][0];
+    for (int i = tid; i < b; i += GJR_NT) colp[i] = MULTI ? __ldcg(reinterpret_cast<const double2*>(src + i)) : src[i];
+    if (tid == 0) piv[j] = p;
+    __syncthreads();  // B2
+    if (TIMING) { const long long n_ = clock64() + (int)colp[0].x * 0; tph[2] += n_ - tc; tc = n_; }
+    // ---- P3: R row j for the local columns, diagonal and register updates
+    const double isd = rsqrt(pv), ipv = 1.0 / pv;
+    for (int l = tid; l < ncl; l += GJR_NT) {
+      const int g = rank + (l << lgCL);
+      if (dn[l]) continue;
+      if (g == p) {
+        Rg[j + (size_t)g * b] = cmk(pv * isd, 0.0);
+        dn[l] = 1;
+      } else {
+        const cplx u = colp[g];  // S_gp;  R_{j,g} = conj(S_gp)/√S_pp
+        Rg[j + (size_t)g * b] = cmk(u.x * isd, -u.y * isd);
+        dg[l] -= (u.x * u.x + u.y * u.y) * ipv;
+      }
+    }
+    cplx c[MR];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int i = row0 + 32 * r;
+      c[r] = i < b ? cmk(colp[i].x * ipv, colp[i].y * ipv) : cmk(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < MC; ++q) {
+      if (q >= nq) break;
+      const int g = rank + ((cgp + CG * q) << lgCL);
+      const cplx u = colp[g];
+      const cplx uc = cmk(u.x, -u.y);  // conj(S_gp) = S_pg
+#pragma unroll
+      for (int r = 0; r < MR; ++r) a[q][r] = cfms(c[r], uc, a[q][r]);
+    }
+    __syncthreads();  // B3: dg / dn / colp reuse
+    if (TIMING) { const long long n_ = clock64() + (int)dg[0] * 0; tph[3] += n_ - tc; }
+  }
+  if (TIMING && blockIdx.y == 0 && (tid == 0 || tid == 32 * (GJR_NW - 1)))
+    printf("[pchol timing] b %d CL %d rank %d warp %d steps %d cycles/step: P1 %lld B1+P2 %lld colp+B2 %lld P3+B3 %lld\n",
+           b, CL, rank, warp, jdone, tph[0] / max(jdone, 1), tph[1] / max(jdone, 1), tph[2] / max(jdone, 1),
+           tph[3] / max(jdone, 1));
+  // ---- output: R' = [R11 R12] over G (pivot columns first, then the rest ascending), perm, k
+  if (tid == 0) {
+    for (int g = 0; g < b; ++g) posmap[g] = -1;
+    for (int q = 0; q < kk; ++q) posmap[piv[q]] = q;
+    int cpos = kk;
+    for (int g = 0; g < b; ++g)
+      if (posmap[g] < 0) posmap[g] = cpos++;
+  }
+  __syncthreads();
+  if (MULTI) cl.sync();  // every CTA loaded G long ago; Rg rows of the own columns are complete
+  for (int e = tid; e < kk * ncl; e += GJR_NT) {
+    const int i = e % kk, l = e / kk;
+    const int g = rank + (l << lgCL);
+    const int cpos = posmap[g];
+    t.A[i + (size_t)cpos * t.lda] = (cpos < kk && i > cpos) ? cmk(0.0, 0.0) : Rg[i + (size_t)g * b];
+  }
+  for (int l = tid; l < ncl; l += GJR_NT) perm_out[t.out_off + posmap[rank + (l << lgCL)]] = rank + (l << lgCL);
   if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
 }
 
@@ -1902,6 +2275,46 @@ void launch_cluster(K kern, int CL, int ny, size_t smem, cudaStream_t st, Args..
 }
 }  // namespace
 
+// register panel: panel width for an n-row block (columns per warp ≤ 24, width ≤ 64)
+int gj_panel_reg_width(int nmax) {
+  const int CL = 16, rc = (nmax + CL - 1) / CL, RG = (rc + 31) / 32;
+  if (RG > GJR_NW) return 0;
+  const int CG = GJR_NW / RG;
+  return std::min(64, 8 * CG);  // ≤ 8 panel columns per warp (registers)
+}
+long long gj_panel_reg_scratch(int nb) { return 2LL * 16 + 2LL * 16 * nb + 2LL * nb + 8; }
+
+namespace {
+template <int MC>
+void launch_gpr(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cplx* xs, long long xstride,
+                cudaStream_t st) {
+  const int CL = 16;
+  FMMLU_CUDA(cudaFuncSetAttribute(k_gj_panel_reg<MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL, ntasks, 1);
+  cfg.blockDim = dim3(GJR_NT, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_gj_panel_reg<MC>, d_tasks, j0, nb, d_status, xs, xstride));
+}
+}  // namespace
+
+void launch_gj_panel_reg(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cplx* xs,
+                         cudaStream_t st, int nmax) {
+  if (ntasks <= 0) return;
+  const int rc = (nmax + 15) / 16, RG = (rc + 31) / 32, CG = GJR_NW / RG;
+  const int mc = (nb + CG - 1) / CG;
+  const long long xstride = gj_panel_reg_scratch(nb);
+  if (mc > 8) throw Error(-6, "register GJ panel: width beyond 8 columns per warp");
+  launch_gpr<8>(d_tasks, ntasks, j0, nb, d_status, xs, xstride, st);
+}
+
 void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st,
                              int nmax) {
   if (ntasks <= 0) return;
@@ -1940,16 +2353,6 @@ void launch_pchol_big_finish(const PcholBig* d_tasks, int ntasks, int* perm_out,
 
 // register-resident GJ configurations: rows per lane MR, columns per warp MC, cluster size CL
 namespace {
-struct GjrCfg { int MR, MC, CL; };
-GjrCfg gjr_cfg(int nmax) {  // RG = ceil(n/(32 MR)) row groups, CG = 16/RG column groups
-  if (nmax <= 32) return {1, 2, 1};
-  if (nmax <= 64) return {1, 8, 1};
-  if (nmax <= 128) return {1, 16, 2};
-  if (nmax <= 256) return {1, 16, 8};
-  if (nmax <= 384) return {1, 24, 16};
-  return {2, 16, 16};  // ≤ 512
-}
-constexpr int GJR_NCAP = 512;
 template <int MR, int MC, bool MULTI>
 void launch_gjr(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t st, int CL) {
   static const bool timing = getenv("FMMLU_GJ_TIMING") != nullptr;
@@ -2029,6 +2432,75 @@ size_t pchol_smem(int b, int CL) {
   const size_t ncl = (b + CL - 1) / CL;
   return (size_t)b * ncl * sizeof(cplx) + (size_t)b * sizeof(cplx) + ncl * sizeof(cplx) +
          2 * (size_t)b * sizeof(int) + 64;
+}
+
+namespace {
+template <int MR, int MC, bool MULTI>
+void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
+                long long xstride, cudaStream_t st, int CL) {
+  static const bool timing = getenv("FMMLU_PCHOL_TIMING") != nullptr;
+  if (timing && MULTI) {
+    if (CL > 8)
+      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_reg<MR, MC, true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, ntasks, 1);
+    cfg.blockDim = dim3(GJR_NT, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_pchol_reg<MR, MC, true, true>, d_tasks, perm_out, k_out, eps, xs, xstride));
+    return;
+  }
+  if (timing && !MULTI) {
+    k_pchol_reg<MR, MC, false, true><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride);
+    FMMLU_LAUNCH();
+    return;
+  }
+  if constexpr (!MULTI) {
+    k_pchol_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride);
+    FMMLU_LAUNCH();
+  } else {
+    if (CL > 8)
+      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_reg<MR, MC, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, ntasks, 1);
+    cfg.blockDim = dim3(GJR_NT, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_pchol_reg<MR, MC, true>, d_tasks, perm_out, k_out, eps, xs, xstride));
+  }
+}
+}  // namespace
+
+long long pchol_reg_scratch(int bmax) {  // complex elements of exchange scratch per task
+  if (bmax > GJR_NCAP) return 0;
+  const int CL = gjr_cfg(bmax).CL;
+  return 2LL * CL * bmax + 2LL * CL + 8;
+}
+
+bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
+                      cudaStream_t st, int bmax) {
+  if (ntasks <= 0) return true;
+  if (bmax > GJR_NCAP) return false;
+  const GjrCfg c = gjr_cfg(bmax);
+  const long long xstride = pchol_reg_scratch(bmax);
+  if (bmax <= 32) launch_pcr<1, 2, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
+  else if (bmax <= 64) launch_pcr<1, 8, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
+  else if (bmax <= 256) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
+  else if (bmax <= 384) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
+  else launch_pcr<2, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
+  return true;
 }
 
 bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,

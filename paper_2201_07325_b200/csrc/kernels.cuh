@@ -120,6 +120,12 @@ void launch_gj_swap(const GjTask* d_tasks, int ntasks, int j0, int nb, cudaStrea
 int gj_panel_cluster_size(int nmax, int nb);  // 0 = does not fit
 void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cudaStream_t st,
                              int nmax);
+// register-resident cluster panel (16 CTAs, L2 exchange): width for nmax (0 = not usable) and
+// exchange scratch per task (complex elements) for panel width nb
+int gj_panel_reg_width(int nmax);
+long long gj_panel_reg_scratch(int nb);
+void launch_gj_panel_reg(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cplx* xs,
+                         cudaStream_t st, int nmax);
 void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, const long long* d_soff, cudaStream_t st,
                           int nmax);
 // in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
@@ -150,6 +156,11 @@ void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int
 // (R' over G with ld b).  false if b is too large for a 16-CTA cluster.
 bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
                           cudaStream_t st, int bmax);
+// Register-resident pivoted Cholesky (b ≤ 512; same outputs as launch_pchol_cluster).  xs: exchange
+// scratch of pchol_reg_scratch(bmax) complex elements per task.  false if bmax is too large.
+long long pchol_reg_scratch(int bmax);
+bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
+                      cudaStream_t st, int bmax);
 // Global-memory blocked pivoted Cholesky for boxes beyond the cluster capacity.
 struct PcholState {
   int j;       // pivots taken so far

@@ -209,3 +209,22 @@ def test_gj_modes_parity(F, mode):
     xo = rss.solve(f, b)
     assert dense.rel_diff(x, xo) <= 10 * eps
     assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_pchol_modes_parity(F, mode):
+    """Pivoted-Cholesky kernels (0: register-resident, 1: shared-memory cluster) match the oracle
+    and pick the same ranks (pivot near-ties aside)."""
+    g = fi.ellipsoid(6000)
+    k, eps = 2 * math.pi, 1e-6
+    b = fi.gaussian_rhs(g.n, 2, 8)
+    h = F.FmmLu(g.points, g.normals, g.weights, 64).set_param("pchol_mode", mode).factor(k, eps)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, 64)
+    xo = rss.solve(f, b)
+    assert dense.rel_diff(x, xo) <= 10 * eps
+    st = h.stats()
+    for lvl, s in f.stats["levels"].items():
+        ro = int(s["ranks"].sum())
+        assert abs(st["ranks_sum"][lvl] - ro) <= 0.03 * ro + 2
