@@ -15,7 +15,7 @@ LIB = os.path.join(LIBDIR, "libfmmlu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-          "-I", os.path.join(HERE, "..", "include")]
+          "-I", os.path.join(HERE, "..", "include")] + os.environ.get("FMMLU_NVCC_EXTRA", "").split()
 CU = ["fmmlu.cu", "kernels.cu", "gemm.cu"]
 CPP = ["tree.cpp"]
 CXX = os.environ.get("CXX", "g++")

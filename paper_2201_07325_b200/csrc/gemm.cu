@@ -66,7 +66,7 @@ __device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0,
   }
 }
 
-template <int SCATTER>
+template <int SCATTER, bool THREEM>
 __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
                                           const GemmTile* __restrict__ tiles, cplx alpha,
                                           cplx* __restrict__ bsr) {
@@ -83,11 +83,17 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
   const double sa = P.opA == kOpC ? -1.0 : 1.0;  // conjugation of A / B at fragment load
   const double sb = P.opB == kOpC ? -1.0 : 1.0;
 
+  // THREEM: 3-multiplication complex product (P1 = ArBr, P2 = AiBi, P3 = (Ar+Ai)(Br+Bi);
+  // Re = P1 − P2, Im = P3 − P1 − P2): 24 instead of 32 DMMAs per k-step on the tensor pipe.
   double accr[4][2][2], acci[4][2][2];
+  double acc3[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
+    for (int j = 0; j < 2; ++j) {
+      accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
+      acc3[i][j][0] = acc3[i][j][1] = 0.0;
+    }
 
   // K range of this tile (split-K); the range is BK-aligned, P.k bounds the loads
   const int kbeg = P.kchunk > 0 ? T.ks * P.kchunk : 0;
@@ -121,6 +127,21 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
         b[j] = bs[kk * PADB + wn * 16 + j * 8 + g];
         b[j].y *= sb;
       }
+      if constexpr (THREEM) {
+      double as_[4], bs_[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) as_[i] = a[i].x + a[i].y;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bs_[j] = b[j].x + b[j].y;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(accr[i][j][0], accr[i][j][1], a[i].x, b[j].x);  // P1
+          dmma(acci[i][j][0], acci[i][j][1], a[i].y, b[j].y);  // P2
+          dmma(acc3[i][j][0], acc3[i][j][1], as_[i], bs_[j]);  // P3
+        }
+      } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -130,8 +151,20 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
           dmma(acci[i][j][0], acci[i][j][1], a[i].x, b[j].y);
           dmma(acci[i][j][0], acci[i][j][1], a[i].y, b[j].x);
         }
+      }
     }
   }
+  if constexpr (THREEM)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double p1 = accr[i][j][h], p2 = acci[i][j][h];
+        accr[i][j][h] = p1 - p2;
+        acci[i][j][h] = acc3[i][j][h] - p1 - p2;
+      }
 
   // epilogue.  Scatter: stage the tile's frame rows/columns (slot, position) and the owner-pair
   // table in shared memory (reusing the operand buffers) so each element costs 2 atomics only.
@@ -197,15 +230,15 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
 }
 
 // distinct names so profilers can tell the Schur-complement GEMM from the others
-__global__ void __launch_bounds__(NT) k_gemm_store(const GemmProblem* __restrict__ probs,
+__global__ void __launch_bounds__(NT, 2) k_gemm_store(const GemmProblem* __restrict__ probs,
                                                    const GemmTile* __restrict__ tiles, cplx alpha,
                                                    cplx* __restrict__ bsr) {
-  gemm_body<0>(probs, tiles, alpha, bsr);
+  gemm_body<0, true>(probs, tiles, alpha, bsr);
 }
 __global__ void __launch_bounds__(NT) k_gemm_schur(const GemmProblem* __restrict__ probs,
                                                    const GemmTile* __restrict__ tiles, cplx alpha,
                                                    cplx* __restrict__ bsr) {
-  gemm_body<1>(probs, tiles, alpha, bsr);
+  gemm_body<1, false>(probs, tiles, alpha, bsr);
 }
 
 }  // namespace
