@@ -2031,7 +2031,7 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
     FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
     launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
-                       it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax);
+                       it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax, it->kmax);
   }
   launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
   P.end(sid, st);
@@ -2040,7 +2040,7 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
     double entries = (double)h->n0 * h->n0;
     for (auto& ph : h->phases) entries += (double)ph.fac_bytes / 16.0;
     P.add(FMMLU_K_SOLVE, 8.0 * entries * nrhs, 16.0 * entries + 64.0 * n * nrhs,
-          3 + 2 * (long long)h->phases.size() + (h->n0 > 0 ? 2 : 0));
+          2 + 6 * (long long)h->phases.size() + (h->n0 > 0 ? 3 : 0));
   }
   if (!dev)
     FMMLU_CUDA(cudaMemcpyAsync(rhs, io.p, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyDeviceToHost, st));

@@ -1954,6 +1954,136 @@ __global__ void __launch_bounds__(SV_NT) k_sd_b(const BoxRec* __restrict__ recs,
   }
 }
 
+// ---- parallel split of the per-box solve products
+// up [e]:   t = y_R − Tᵀ y_S → tmp; y_R ← 0            (one warp per row i of Tᵀ; lanes over l)
+// up [dinv]: y_R += X_RR⁻¹[rows, l-chunk] · t[l-chunk]   (thread per row, 32-column chunks, atomics)
+// down [b1]: y_R −= acc (acc = Up y_{S∪N} from k_sd_a)    (elementwise)
+// down [b2]: y_S −= T[:, i-chunk] y_R[i-chunk]            (thread per row l of T, atomics)
+constexpr int SV_CH = 32;
+__global__ void __launch_bounds__(256) k_su_e(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
+                                             const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                                             cplx* __restrict__ tmp) {
+  const BoxRec R = recs[blockIdx.x];
+  const int lane = threadIdx.x & 31, i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= R.r) return;
+  const int k = R.k, r = R.r;
+  const int* S = idx + R.idxS;
+  const cplx* T = fac + R.T + (size_t)i * k;  // column i of T = row i of Tᵀ
+  cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  const int gi = idx[R.idxR + i];
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    cplx acc[SV_Q];
+#pragma unroll
+    for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
+    for (int l = lane; l < k; l += 32) {
+      const cplx tv = T[l];
+      const int gs = S[l];
+#pragma unroll
+      for (int q = 0; q < SV_Q; ++q)
+        if (q < nq) acc[q] = cfma(tv, y[gs + (size_t)(q0 + q) * ldy], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < SV_Q; ++q) acc[q] = warp_csum(acc[q]);
+    if (lane < nq) {
+      cplx a = acc[0];
+#pragma unroll
+      for (int q = 1; q < SV_Q; ++q)
+        if (q == lane) a = acc[q];
+      cplx* d = y + gi + (size_t)(q0 + lane) * ldy;
+      tb[i + (size_t)(q0 + lane) * r] = csub(*d, a);
+      *d = cmk(0.0, 0.0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_su_dinv(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
+                                                const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                                                const cplx* __restrict__ tmp) {
+  const BoxRec R = recs[blockIdx.x];
+  const int r = R.r;
+  const int i = blockIdx.y * 128 + threadIdx.x, l0 = blockIdx.z * SV_CH;
+  if (l0 >= r) return;
+  const int l1 = min(r, l0 + SV_CH);
+  __shared__ cplx ts[SV_CH * SV_Q];
+  const cplx* Xi = fac + R.Xi;
+  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < (l1 - l0) * nq; e += 128) {
+      const int l = e % (l1 - l0), q = e / (l1 - l0);
+      ts[l + q * SV_CH] = tb[l0 + l + (size_t)(q0 + q) * r];
+    }
+    __syncthreads();
+    if (i < r) {
+      cplx acc[SV_Q];
+#pragma unroll
+      for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
+      for (int l = l0; l < l1; ++l) {
+        const cplx a = Xi[i + (size_t)l * r];
+#pragma unroll
+        for (int q = 0; q < SV_Q; ++q)
+          if (q < nq) acc[q] = cfma(a, ts[(l - l0) + q * SV_CH], acc[q]);
+      }
+      const int gi = idx[R.idxR + i];
+      for (int q = 0; q < nq; ++q) {
+        cplx* d = y + gi + (size_t)(q0 + q) * ldy;
+        atomicAdd(&d->x, acc[q].x);
+        atomicAdd(&d->y, acc[q].y);
+      }
+    }
+  }
+}
+
+__global__ void k_sd_b1(const BoxRec* __restrict__ recs, const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                        const cplx* __restrict__ tmp) {
+  const BoxRec R = recs[blockIdx.x];
+  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int e = threadIdx.x; e < R.r * nrhs; e += blockDim.x) {
+    const int i = e % R.r, q = e / R.r;
+    cplx* d = y + idx[R.idxR + i] + (size_t)q * ldy;
+    *d = csub(*d, tb[i + (size_t)q * R.r]);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_sd_b2(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
+                                              const int* __restrict__ idx, cplx* y, int ldy, int nrhs) {
+  const BoxRec R = recs[blockIdx.x];
+  const int k = R.k, r = R.r;
+  const int l = blockIdx.y * 128 + threadIdx.x, i0 = blockIdx.z * SV_CH;
+  if (i0 >= r) return;
+  const int i1 = min(r, i0 + SV_CH);
+  __shared__ cplx ys[SV_CH * SV_Q];
+  const cplx* T = fac + R.T;
+  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
+    const int nq = min(SV_Q, nrhs - q0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < (i1 - i0) * nq; e += 128) {
+      const int i = e % (i1 - i0), q = e / (i1 - i0);
+      ys[i + q * SV_CH] = y[idx[R.idxR + i0 + i] + (size_t)(q0 + q) * ldy];
+    }
+    __syncthreads();
+    if (l < k) {
+      cplx acc[SV_Q];
+#pragma unroll
+      for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
+      for (int i = i0; i < i1; ++i) {
+        const cplx tv = T[l + (size_t)i * k];
+#pragma unroll
+        for (int q = 0; q < SV_Q; ++q)
+          if (q < nq) acc[q] = cfma(tv, ys[(i - i0) + q * SV_CH], acc[q]);
+      }
+      const int gs = idx[R.idxS + l];
+      for (int q = 0; q < nq; ++q) {
+        cplx* d = y + gs + (size_t)(q0 + q) * ldy;
+        atomicAdd(&d->x, -acc[q].x);
+        atomicAdd(&d->y, -acc[q].y);
+      }
+    }
+  }
+}
+
 // root: tmp = y[rows]; y[rows] = Xinv · tmp   (one thread per row, column-major Xinv)
 __global__ void k_root_gather(const int* rows, const cplx* y, int ldy, cplx* tmp, int n0, int nrhs) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n0 * nrhs; e += gridDim.x * blockDim.x) {
@@ -2676,7 +2806,11 @@ void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, 
     FMMLU_CUDA(cudaFuncSetAttribute(k_su_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     cb = sb;
   }
-  k_su_a<<<nrec, SV_NT, sa, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp);
+  (void)sa;
+  k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp);
+  FMMLU_LAUNCH();
+  k_su_dinv<<<dim3(nrec, (rmax + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
+                                                                                       nrhs, tmp);
   FMMLU_LAUNCH();
   if (nitems > 0) {
     k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
@@ -2685,7 +2819,8 @@ void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, 
 }
 
 void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
-                        const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax) {
+                        const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax,
+                        int kmax_down) {
   if (nrec <= 0) return;
   size_t sa = (size_t)kSolveChunk * SV_Q * sizeof(cplx) + 16;
   size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
@@ -2698,7 +2833,11 @@ void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items
     k_sd_a<<<nitems, SV_NT, sa, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
     FMMLU_LAUNCH();
   }
-  k_sd_b<<<nrec, SV_NT, sb, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp);
+  (void)sb;
+  k_sd_b1<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp);
+  FMMLU_LAUNCH();
+  k_sd_b2<<<dim3(nrec, (kmax_down + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
+                                                                                          nrhs);
   FMMLU_LAUNCH();
 }
 

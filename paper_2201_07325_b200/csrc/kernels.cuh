@@ -194,7 +194,8 @@ constexpr int kSolveChunk = 128;
 void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                       const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax);
 void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
-                        const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax);
+                        const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax,
+                        int kmax);
 // y[rows] = Xinv (n0×n0) · y[rows] for the root block
 void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
                        cplx* tmp, cudaStream_t st);
