@@ -1438,7 +1438,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         lap(8);
         int pid = h->prof.begin(FMMLU_K_GATHER, st);
         launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), M.as<cplx>(), st);
-        launch_proxy(s.ptr<ProxyTask>(o_p), (int)pts.size(), s.ptr<int>(o_g), M.as<cplx>(), h->g, k, st);
+        launch_proxy(s.ptr<ProxyTask>(o_p), (int)pts.size(), s.ptr<int>(o_g), M.as<cplx>(), h->g, k, st, ngamma);
         h->prof.end(pid, st);
         {
           double by = 0, fl = 0;
@@ -2185,7 +2185,7 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
       size_t o_p = sg_.add(pt), o_g = sg_.add(gidx);
       sg_.upload(st);
       int pid = h->prof.begin(FMMLU_K_GATHER, st);
-      launch_proxy(sg_.ptr<ProxyTask>(o_p), nw, sg_.ptr<int>(o_g), M.as<cplx>(), g, k, st);
+      launch_proxy(sg_.ptr<ProxyTask>(o_p), nw, sg_.ptr<int>(o_g), M.as<cplx>(), g, k, st, ngamma);
       h->prof.end(pid, st);
       h->prof.add(FMMLU_K_GATHER, 120.0 * m * b * nw, 16.0 * m * b * nw, 1);
       keep.push_back(std::move(sg_.dev));

@@ -217,29 +217,44 @@ __global__ void k_copy(const CopyTask* __restrict__ tasks, const int* __restrict
     dst[t.dst + i + (size_t)j * t.ldd] = v;
   }
 }
-
-// ------------------------------------------------------------------ proxy rows
-__global__ void k_proxy(const ProxyTask* __restrict__ tasks, const int* __restrict__ gidx,
-                        cplx* __restrict__ ws, Geo g, double k) {
+__global__ void __launch_bounds__(256) k_proxy(const ProxyTask* __restrict__ tasks, const int* __restrict__ gidx,
+                                              cplx* __restrict__ ws, Geo g, double k) {
+  extern __shared__ double ysh[];  // proxy points of the task: x | y | z (3 × ngamma)
   const ProxyTask t = tasks[blockIdx.x];
   const double ga = M_PI * (3.0 - sqrt(5.0));
+  for (int l = threadIdx.x; l < t.ngamma; l += blockDim.x) {  // Fibonacci direction u_l (R2)
+    const double zl = 1.0 - (2.0 * l + 1.0) / t.ngamma;
+    const double phi = l * ga;
+    const double sl = sqrt(fmax(0.0, 1.0 - zl * zl));
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    ysh[l] = t.cx + t.rho * sl * cp;
+    ysh[t.ngamma + l] = t.cy + t.rho * sl * sp;
+    ysh[2 * t.ngamma + l] = t.cz + t.rho * zl;
+  }
+  __syncthreads();
   const int n = t.ngamma * t.b;
   for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < n; e += blockDim.x * gridDim.y) {
     const int l = e % t.ngamma, j = e / t.ngamma;
-    // Fibonacci direction u_l (reading C5)
-    const double zl = 1.0 - (2.0 * l + 1.0) / t.ngamma;
-    const double phi = l * ga;
-    const double s = sqrt(fmax(0.0, 1.0 - zl * zl));
-    double sp, cp;
-    sincos(phi, &sp, &cp);
-    const double yx = t.cx + t.rho * s * cp, yy = t.cy + t.rho * s * sp, yz = t.cz + t.rho * zl;
     const int gj = gidx[t.idx_off + j];
-    const double xx = g.x[gj], xy = g.y[gj], xz = g.z[gj];
+    const double dx = ysh[l] - g.x[gj], dy = ysh[t.ngamma + l] - g.y[gj], dz = ysh[2 * t.ngamma + l] - g.z[gj];
     const double scl = t.sg * g.sw[gj];
-    // outgoing: K(y_l, x_j) with source normal n(x_j)
-    cplx Ko = kernel_K(k, yx - xx, yy - xy, yz - xz, g.nx[gj], g.ny[gj], g.nz[gj]);
-    // incoming: G(x_j, y_l)
-    cplx Gi = kernel_G(k, xx - yx, xy - yy, xz - yz);
+    // r, e^{ikr} once for both rows (same arithmetic as kernel_K / kernel_G)
+    const double r2 = dx * dx + dy * dy + dz * dz;
+    double rinv = rsqrt(r2);
+    rinv = rinv * (1.5 - 0.5 * r2 * rinv * rinv);
+    const double r = r2 * rinv;
+    double sn, c;
+    sincos(k * r, &sn, &c);
+    const double gg = kInv4Pi * rinv;
+    // outgoing K(y_l, x_j) with the source normal n(x_j)
+    const double dn = dx * g.nx[gj] + dy * g.ny[gj] + dz * g.nz[gj];
+    const double f = dn * rinv * rinv;
+    const double kr = k * r;
+    const double dre = (c + sn * kr) * f * gg, dim = (sn - c * kr) * f * gg;
+    const cplx Ko = cmk(dre + k * sn * gg, dim - k * c * gg);
+    // incoming G(x_j, y_l)
+    const cplx Gi = cmk(c * gg, sn * gg);
     ws[t.dst + (t.row0 + l) + (size_t)j * t.ld] = cscale(Ko, scl);
     ws[t.dst + (t.row0 + t.ngamma + l) + (size_t)j * t.ld] = cscale(Gi, scl);
   }
@@ -2320,10 +2335,16 @@ void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cpl
 }
 
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
-                  double k, cudaStream_t st) {
+                  double k, cudaStream_t st, int ngmax) {
   if (ntasks <= 0) return;
+  const size_t smem = 3 * (size_t)std::max(ngmax, 1) * sizeof(double);  // proxy points x | y | z
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_proxy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
   dim3 grid(ntasks, 8);
-  k_proxy<<<grid, 256, 0, st>>>(d_tasks, gidx, ws, g, k);
+  k_proxy<<<grid, 256, smem, st>>>(d_tasks, gidx, ws, g, k);
   FMMLU_LAUNCH();
 }
 

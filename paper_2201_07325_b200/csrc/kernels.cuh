@@ -94,7 +94,7 @@ void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const i
 void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cplx* src_arena,
                  cplx* dst_arena, cudaStream_t st);
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
-                  double k, cudaStream_t st);
+                  double k, cudaStream_t st, int ngmax);
 // One corrected-seminormal-equations refinement of T (Gram-path ID): T += R11⁻¹R11⁻ᴴ Z.
 struct RefineTask {
   const cplx* R;  // R11 (k × k upper, ld ldr) from the pivoted Cholesky (R' layout over G)
