@@ -274,12 +274,16 @@ __global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks
   cplx* T = tarena + t.T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.y * 16 + warp;
+  if (blockIdx.y * 16 >= r) return;  // uniform per block
+  cplx* rd = reinterpret_cast<cplx*>(shm) + (size_t)16 * kk;  // 1 / R_ll (shared by the block's warps)
+  for (int l = threadIdx.x; l < kk; l += blockDim.x) rd[l] = cdiv(cmk(1.0, 0.0), M[l + (size_t)l * m]);
+  __syncthreads();
   if (c >= r) return;
   cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)warp * kk;
   for (int i = lane; i < kk; i += 32) x[i] = M[i + (size_t)(kk + c) * m];
   __syncwarp();
   for (int l = kk - 1; l >= 0; --l) {
-    const cplx xl = cdiv(x[l], M[l + (size_t)l * m]);
+    const cplx xl = cmul(x[l], rd[l]);
     __syncwarp();
     if (lane == 0) x[l] = xl;
     for (int i = lane; i < l; i += 32) x[i] = cfms(M[i + (size_t)l * m], xl, x[i]);
@@ -2740,7 +2744,7 @@ void launch_refine_T(const RefineTask* d_tasks, int ntasks, int kmax, int rmax, 
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st, int bmax) {
   if (ntasks <= 0) return;
-  const size_t smem = 16 * (size_t)bmax * sizeof(cplx) + 16;
+  const size_t smem = 17 * (size_t)bmax * sizeof(cplx) + 16;
   static size_t cur = 0;
   if (smem > 48 * 1024 && smem > cur) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_trsm_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
