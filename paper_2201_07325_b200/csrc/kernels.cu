@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __rest
   const int RG = (rc + 31) >> 5, CG = GJR_NW / RG;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rg = warp % RG, cgp = warp / RG;
+  if ((jb + CG - 1) / CG > MC || RG > GJR_NW || nb > 64) __trap();  // configuration mismatch
   const int nq = cgp < CG ? min(MC, (jb - cgp + CG - 1) / CG) : 0;
   const int il = rg * 32 + lane;      // local row
   const int i = r0 + il;              // global row
@@ -833,6 +834,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
   cplx* const xg = t.Am;                                        // [2][n]
   GjCand* const cg_ = reinterpret_cast<GjCand*>(t.Am + 2 * n);  // [2][16]
   // this warp's local columns are cgp + CG q for q < nq
+  if ((ncl + CG - 1) / CG > MC || RG > GJR_NW) __trap();  // launch configuration / template mismatch
   const int nq = cgp < CG ? min(MC, (ncl - cgp + CG - 1) / CG) : 0;
   const int row0 = (rg << (5 + LGMR)) + lane;
   cplx a[MC][MR];
@@ -1330,6 +1332,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
   const int RG = (b + 32 * MR - 1) >> (5 + LGMR), CG = GJR_NW / RG;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rg = warp % RG, cgp = warp / RG;
+  if ((ncl + CG - 1) / CG > MC || RG > GJR_NW) __trap();  // launch configuration / template mismatch
   const int nq = cgp < CG ? min(MC, (ncl - cgp + CG - 1) / CG) : 0;
   const int row0 = (rg << (5 + LGMR)) + lane;
   cplx* const xcol = MULTI ? xs + blockIdx.y * xstride : nullptr;                          // [2][CL][b]
@@ -2638,9 +2641,14 @@ void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_
 }
 }  // namespace
 
+GjrCfg pchol_cfg(int bmax) {  // must match the launch_pcr instantiations below
+  if (bmax > 128 && bmax <= 192) return {1, 24, 4};
+  return gjr_cfg(bmax);
+}
+
 long long pchol_reg_scratch(int bmax) {  // complex elements of exchange scratch per task
   if (bmax > GJR_NCAP) return 0;
-  const int CL = gjr_cfg(bmax).CL;
+  const int CL = pchol_cfg(bmax).CL;
   return 2LL * CL * bmax + 2LL * CL + 8;
 }
 
@@ -2648,10 +2656,12 @@ bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, i
                       cudaStream_t st, int bmax) {
   if (ntasks <= 0) return true;
   if (bmax > GJR_NCAP) return false;
-  const GjrCfg c = gjr_cfg(bmax);
+  const GjrCfg c = pchol_cfg(bmax);
   const long long xstride = pchol_reg_scratch(bmax);
   if (bmax <= 32) launch_pcr<1, 2, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
   else if (bmax <= 64) launch_pcr<1, 8, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
+  else if (bmax <= 128) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
+  else if (bmax <= 192) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
   else if (bmax <= 256) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
   else if (bmax <= 384) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
   else launch_pcr<2, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
