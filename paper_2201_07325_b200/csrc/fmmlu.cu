@@ -28,6 +28,7 @@
 #include <unordered_map>
 #include <future>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/fmmlu.h"
@@ -800,30 +801,49 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
   tp.boxN.assign(nlb, {});
   tp.boxQ.assign(nlb, {});
   // pair set: nb[a] = ∪ { grp(i) : a ∈ grp(i) } ∪ Q-relations, grp(i) = {i} ∪ N(i).  Built as
-  // per-owner lists of the groups containing it, then one stamped union per owner.
-  std::vector<std::vector<int>> ingrp(no), qrel(no);
-  std::vector<int> cand;
-  for (int i = 0; i < nlb; ++i) {
-    const int box = tp.owners[i];
-    const Box& B = T.boxes[box];
-    cand.clear();
-    for (int dx = -2; dx <= 2; ++dx)
-      for (int dy = -2; dy <= 2; ++dy)
-        for (int dz = -2; dz <= 2; ++dz) {
-          const int x = B.c[0] + dx, y = B.c[1] + dy, z = B.c[2] + dz;
-          if (x < 0 || y < 0 || z < 0 || x > lim || y > lim || z > lim) continue;
-          int o;
-          if (dense) {
-            o = grid[(size_t)(((int64_t)x * side + y) * side + z)];
-          } else {
-            const int ob = T.owner_of_cell(lvl, x, y, z);
-            o = ob >= 0 ? tp.local[ob] : -1;
+  // per-owner lists of the groups containing it, then one stamped union per owner.  The
+  // per-box classification and the per-owner unions run on a few host threads.
+  const int nth = std::max(1, std::min<int>(8, (int)std::thread::hardware_concurrency() / 2));
+  auto par = [&](int count, auto&& fn) {
+    if (nth == 1 || count < 256) {
+      fn(0, count);
+      return;
+    }
+    std::vector<std::thread> th;
+    const int chunk = (count + nth - 1) / nth;
+    for (int w = 0; w < nth; ++w) {
+      const int lo = w * chunk, hi = std::min(count, lo + chunk);
+      if (lo < hi) th.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+    }
+    for (auto& t : th) t.join();
+  };
+  par(nlb, [&](int lo, int hi) {
+    std::vector<int> cand;
+    for (int i = lo; i < hi; ++i) {
+      const int box = tp.owners[i];
+      const Box& B = T.boxes[box];
+      cand.clear();
+      for (int dx = -2; dx <= 2; ++dx)
+        for (int dy = -2; dy <= 2; ++dy)
+          for (int dz = -2; dz <= 2; ++dz) {
+            const int x = B.c[0] + dx, y = B.c[1] + dy, z = B.c[2] + dz;
+            if (x < 0 || y < 0 || z < 0 || x > lim || y > lim || z > lim) continue;
+            int o;
+            if (dense) {
+              o = grid[(size_t)(((int64_t)x * side + y) * side + z)];
+            } else {
+              const int ob = T.owner_of_cell(lvl, x, y, z);
+              o = ob >= 0 ? tp.local[ob] : -1;
+            }
+            if (o >= 0 && o != i) cand.push_back(o);
           }
-          if (o >= 0 && o != i) cand.push_back(o);
-        }
-    std::sort(cand.begin(), cand.end());
-    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-    for (int o : cand) (T.sep(box, tp.owners[o], lvl) <= 1 ? tp.boxN[i] : tp.boxQ[i]).push_back(o);
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      for (int o : cand) (T.sep(box, tp.owners[o], lvl) <= 1 ? tp.boxN[i] : tp.boxQ[i]).push_back(o);
+    }
+  });
+  std::vector<std::vector<int>> ingrp(no), qrel(no);
+  for (int i = 0; i < nlb; ++i) {
     ingrp[i].push_back(i);
     for (int x : tp.boxN[i]) ingrp[x].push_back(i);
     for (int q : tp.boxQ[i]) {
@@ -832,22 +852,24 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
     }
   }
   tp.nb.assign(no, {});
-  std::vector<int> stamp(no, -1);
-  for (int a = 0; a < no; ++a) {
-    std::vector<int>& v = tp.nb[a];
-    auto add = [&](int b) {
-      if (stamp[b] != a) {
-        stamp[b] = a;
-        v.push_back(b);
+  par(no, [&](int lo, int hi) {
+    std::vector<int> stamp(no, -1);
+    for (int a = lo; a < hi; ++a) {
+      std::vector<int>& v = tp.nb[a];
+      auto add = [&](int b2) {
+        if (stamp[b2] != a) {
+          stamp[b2] = a;
+          v.push_back(b2);
+        }
+      };
+      for (int i : ingrp[a]) {
+        add(i);
+        for (int x : tp.boxN[i]) add(x);
       }
-    };
-    for (int i : ingrp[a]) {
-      add(i);
-      for (int x : tp.boxN[i]) add(x);
+      for (int q : qrel[a]) add(q);
+      std::sort(v.begin(), v.end());
     }
-    for (int q : qrel[a]) add(q);
-    std::sort(v.begin(), v.end());
-  }
+  });
 }
 
 struct LevelBSR {
