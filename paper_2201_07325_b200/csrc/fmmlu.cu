@@ -146,10 +146,11 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), big(o.big), cap(o.cap) {
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), big(o.big), borrowed(o.borrowed), cap(o.cap) {
     o.p = nullptr;
     o.bytes = 0;
     o.big = false;
+    o.borrowed = false;
   }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
@@ -158,16 +159,25 @@ struct DBuf {
       bytes = o.bytes;
       st = o.st;
       big = o.big;
+      borrowed = o.borrowed;
       cap = o.cap;
       o.p = nullptr;
       o.bytes = 0;
       o.big = false;
+      o.borrowed = false;
     }
     return *this;
   }
   ~DBuf() { release(); }
-  bool big = false;  // from / back to the big-block cache
+  bool big = false;       // from / back to the big-block cache
+  bool borrowed = false;  // points into a staging arena (released with the arena)
   void release() {
+    if (borrowed) {
+      p = nullptr;
+      bytes = 0;
+      borrowed = false;
+      return;
+    }
     if (p) {
       const double t0 = wall_ms();
       if (big) big_cache().give(p, cap, st);
@@ -255,6 +265,39 @@ void h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   FMMLU_CUDA(cudaMemcpyAsync(dst, hp, bytes, cudaMemcpyHostToDevice, st));
 }
 
+// Device staging arena for task/descriptor uploads: grow-only chunks per (thread, stream), bump
+// allocation, reset after the stream has been synchronised (wait_stream) — replaces one
+// cudaMallocAsync/cudaFreeAsync pair per upload (≈ 10 per elimination phase).
+struct DevArena {
+  std::vector<DBuf> chunks;
+  size_t used = 0;
+  char* get(size_t bytes, cudaStream_t st) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (chunks.empty() || used + bytes > chunks.back().bytes) {
+      const size_t cap = std::max<size_t>(bytes, chunks.empty() ? (16u << 20) : 2 * chunks.back().bytes);
+      chunks.emplace_back();
+      chunks.back().alloc(cap, st);
+      used = 0;
+    }
+    char* r = chunks.back().as<char>() + used;
+    used += bytes;
+    return r;
+  }
+  void reset() {  // the stream is idle: keep the largest (last) chunk
+    while (chunks.size() > 1) chunks.erase(chunks.begin());
+    used = 0;
+  }
+};
+// per thread, never destroyed (no CUDA calls from static destructors at process exit)
+thread_local std::unordered_map<cudaStream_t, DevArena>& tl_devarena = *new std::unordered_map<cudaStream_t, DevArena>();
+void drop_arena(cudaStream_t st) {  // before destroying a stream: free its chunks on it while it is alive
+  auto it = tl_devarena.find(st);
+  if (it == tl_devarena.end()) return;
+  cudaStreamSynchronize(st);
+  it->second.chunks.clear();
+  tl_devarena.erase(it);
+}
+
 // Collects host arrays and uploads them in one H2D copy.
 struct Stage {
   std::vector<char> host;
@@ -266,6 +309,14 @@ struct Stage {
     return off;
   }
   void upload(cudaStream_t s) {
+    dev.release();
+    dev.p = tl_devarena[s].get(host.size() + 16, s);
+    dev.bytes = host.size() + 16;
+    dev.st = s;
+    dev.borrowed = true;
+    h2d(dev.p, host.data(), host.size(), s);
+  }
+  void upload_owned(cudaStream_t s) {  // own allocation: for data that outlives the next sync
     dev.alloc(host.size() + 16, s);
     h2d(dev.p, host.data(), host.size(), s);
   }
@@ -403,6 +454,8 @@ void wait_stream(fmmlu_handle* h, cudaStream_t st) {
   FMMLU_CUDA(cudaStreamSynchronize(st));
   h->stats.t_sync_wait_ms += now_ms() - t0;
   tl_pin.reset();
+  auto it = tl_devarena.find(st);
+  if (it != tl_devarena.end()) it->second.reset();
 }
 
 void track(fmmlu_handle* h, long long delta) {
@@ -1278,7 +1331,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       size_t o_ao = s.add(actoff), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_np = s.add(nbptr),
              o_ni = s.add(nbidx), o_po = s.add(poffv), o_sp = s.add(slptr), o_sl = s.add(sllist),
              o_pa = s.add(pair_a), o_t = s.add(tasks);
-      s.upload(st);
+      s.upload_owned(st);  // the level CSR is read again by the next level's build
       cur.meta = LevelMeta{s.ptr<int>(o_ao), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p), s.ptr<int>(o_np),
                            s.ptr<int>(o_ni), s.ptr<long long>(o_po), s.ptr<int>(o_sp), s.ptr<int>(o_sl)};
       int bid = h->prof.begin(FMMLU_K_BUILD, st);
@@ -2716,7 +2769,10 @@ int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const 
   });
   if (h) {
     cudaStreamSynchronize(h->stream);
-    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    if (h->own_stream) {
+      drop_arena(h->own_stream);
+      cudaStreamDestroy(h->own_stream);
+    }
     delete h;
   }
   return rc;
@@ -2731,7 +2787,10 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->geo.release();
   h->perm.release();
   if (h->stream) cudaStreamSynchronize(h->stream);
-  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  if (h->own_stream) {
+    drop_arena(h->own_stream);
+    cudaStreamDestroy(h->own_stream);
+  }
   delete h;
   return FMMLU_OK;
 }
