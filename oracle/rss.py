@@ -17,6 +17,10 @@ Follows, step by step and in the paper's notation:
 * Order within a level (reading C8): colours 0..7, Morton order inside a colour,
   and the snapshot rule — N/Q/P membership and Q rows use the actives as of the
   start of the colour phase.
+* PAPER.md L907-918 (forward form):
+  A ≈ (V₁V₂⋯V_M) P_t D P_tᵀ (W_M⋯W₁) with V = P E⁻¹ L⁻¹, W = U⁻¹ F⁻¹ Pᵀ and
+  D = diag(X_{R₁R₁}, …, X_{R_MR_M}, A_{B_tB_t}); the inverses E⁻¹, F⁻¹, L⁻¹, U⁻¹
+  toggle the sign of the off-diagonal blocks (L851-853).  ``apply`` follows it.
 * Reading C1: the √w-scaled matrix Ã = W^{½} A W^{-½} is factorized;
   solve returns x = W^{-½} Ã⁻¹ (W^{½} b) in the caller's ordering.
 
@@ -53,6 +57,7 @@ class BoxRecord:
     lu: tuple        # scipy lu_factor of X_RR
     Lp: np.ndarray   # X_{(S∪N)R} X_RR⁻¹   ((k+|N|) × r)
     Up: np.ndarray   # X_RR⁻¹ X_{R(S∪N)}   (r × (k+|N|))
+    X_RR: np.ndarray  # the pivot block itself (the D factor of the forward form)
 
 
 @dataclasses.dataclass
@@ -65,6 +70,7 @@ class Factorization:
     Bt: np.ndarray          # root actives (tree order, ascending)
     root_lu: tuple
     stats: dict
+    A_t: np.ndarray = None  # A_{B_t B_t} (root block of D)
 
 
 def _gen(A, rows, cols):
@@ -164,7 +170,7 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 A[np.ix_(SN, SN)] -= X_cR @ Up         # Schur complement update
                 if hook is not None:
                     hook("post", ctx)
-                records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up))
+                records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up, X_RR))
                 active[B] = np.sort(Bs)
         lst["ranks"] = np.asarray(lst["ranks"])
         stats["levels"][lvl] = lst
@@ -176,9 +182,10 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
     for r in records:
         alive[r.Br] = False
     Bt = np.nonzero(alive)[0]
-    root_lu = sla.lu_factor(_gen(A, Bt, Bt), check_finite=False)
+    A_t = _gen(A, Bt, Bt)
+    root_lu = sla.lu_factor(A_t, check_finite=False)
     stats["n0"] = int(Bt.size)
-    f = Factorization(tree, k, eps, sw, records, Bt, root_lu, stats)
+    f = Factorization(tree, k, eps, sw, records, Bt, root_lu, stats, A_t)
     if keep_dense:
         f.A_final = A
     return f
@@ -203,3 +210,29 @@ def solve(f: Factorization, b: np.ndarray) -> np.ndarray:
     x = np.empty_like(y)
     x[perm] = y / f.sw[:, None]
     return x[:, 0] if vec else x
+
+
+def apply(f: Factorization, x: np.ndarray) -> np.ndarray:
+    """y ≈ A x from the stored factors, for BASELINE.json's
+    unscaled A; x is n or n×nrhs in caller order.  Rightmost factor first:
+    W₁ … W_M (F⁻¹ then U⁻¹ per box, boxes in elimination order), then D, then
+    V_M … V₁ (L⁻¹ then E⁻¹ per box, boxes in reverse order).  Exactly inverse to
+    ``solve`` up to rounding; within ε of A x."""
+    x = np.asarray(x, dtype=np.complex128)
+    vec = x.ndim == 1
+    xx = x[:, None] if vec else x
+    perm = f.tree.perm
+    y = xx[perm] * f.sw[:, None]                    # Ã acts on W^{½} x (C1)
+    for r in f.records:                             # W_j = U⁻¹ F⁻¹ Pᵀ
+        y[r.Bs] += r.T @ y[r.Br]                    # F⁻¹
+        y[r.Br] += r.Up @ y[r.SN]                   # U⁻¹
+    for r in f.records:                             # D on the R blocks
+        y[r.Br] = r.X_RR @ y[r.Br]
+    if f.Bt.size:
+        y[f.Bt] = f.A_t @ y[f.Bt]                   # P_t A_{B_tB_t} P_tᵀ
+    for r in reversed(f.records):                   # V_j = P E⁻¹ L⁻¹
+        y[r.SN] += r.Lp @ y[r.Br]                   # L⁻¹
+        y[r.Br] += r.T.T @ y[r.Bs]                  # E⁻¹
+    out = np.empty_like(y)
+    out[perm] = y / f.sw[:, None]                   # back to A = W^{-½} Ã W^{½}
+    return out[:, 0] if vec else out

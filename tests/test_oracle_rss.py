@@ -108,3 +108,32 @@ def test_literal_strong_skel_elim_and_proxy_completeness():
 
     rss.factor(g.points, g.normals, g.weights, k, eps, 24, hook=hook)
     assert checked["n"] >= 12 and checked["proxy"] >= 4, checked
+
+
+# ---- forward form A ≈ V₁⋯V_M P_t D P_tᵀ W_M⋯W₁
+def test_apply_single_leaf_is_exact_matvec():
+    # no skeletonized box: the forward form is P_t A P_tᵀ itself
+    g = fi.fibonacci_sphere(60)
+    f = rss.factor(g.points, g.normals, g.weights, 1.0, 1e-6, 64)
+    x = fi.gaussian_rhs(g.n, 2, 3)
+    y = rss.apply(f, x)
+    ye = kern.matvec_unscaled(1.0, g.points, g.normals, g.weights, x)
+    assert dense.rel_diff(y, ye) < 1e-13
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-12])
+def test_apply_approximates_A_and_inverts_solve(eps):
+    g = fi.ellipsoid(3000)
+    k = 2 * math.pi
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, 32)
+    assert len(f.records) > 0
+    x = fi.gaussian_rhs(g.n, 2, 5)
+    y = rss.apply(f, x)
+    ye = kern.matvec_unscaled(k, g.points, g.normals, g.weights, x)   # brute-force A x
+    assert dense.rel_diff(y, ye) <= (10 * eps if eps > 1e-9 else 1e-9)
+    # apply and solve are exact inverses of each other (same factors, sign-toggled)
+    assert dense.rel_diff(rss.solve(f, y), x) < 1e-12
+    assert dense.rel_diff(rss.apply(f, rss.solve(f, x)), x) < 1e-12
+    # linearity
+    a = 0.3 - 1.7j
+    assert dense.rel_diff(rss.apply(f, a * x[:, :1] + x[:, 1:]), a * y[:, :1] + y[:, 1:]) < 1e-12
