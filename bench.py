@@ -278,7 +278,7 @@ def main():
                 "frac": achieved / dmma_tf, "traffic": None, "kernel": cls[dom],
                 "peak_source": "FP64 DMMA m8n8k4 probe measured in this run (MEASURED_PEAKS has no FP64 entry)",
                 "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch}
-    elif cls[dom] in ("build", "gather", "solve"):
+    elif cls[dom] in ("build", "gather", "solve", "apply"):
         achieved = by / (t * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": None, "kernel": cls[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs",

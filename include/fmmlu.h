@@ -95,7 +95,8 @@ typedef struct fmmlu_stats_t {
 #define FMMLU_K_SCHUR 7   /* Schur-complement GEMM + scatter-add                    */
 #define FMMLU_K_ROOT 8    /* root block build + inverse                             */
 #define FMMLU_K_SOLVE 9   /* solve sweeps + root apply                              */
-#define FMMLU_K_NCLASS 10
+#define FMMLU_K_APPLY 10  /* forward apply sweeps (+ one-time re-inversion of D)    */
+#define FMMLU_K_NCLASS 11
 
 /* Build the adaptive level-restricted octree over the n points
  * (readings C14, C6-C8 of SURVEY.md §8(c)).
@@ -121,6 +122,17 @@ int fmmlu_factor(fmmlu_handle* h, double k, double eps);
  *   nrhs : ≥ 1
  * Errors: EINVAL (NULL rhs, nrhs < 1), ESTATE (no factorization), ENOMEM, ECUDA. */
 int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs);
+
+/* Forward factored apply, in place: x ← Â x with the stored factors
+ * Â = V₁⋯V_M P_t D P_tᵀ W_M⋯W₁ ≈ A  (V = P E⁻¹ L⁻¹, W = U⁻¹ F⁻¹ Pᵀ
+ * with sign-toggled inverses L851-853; D = diag(X_{R_jR_j}, A_{B_tB_t})).  Exactly
+ * inverse to fmmlu_solve up to rounding, and within the factorization's ε of A x.
+ * The first call after a factorization re-inverts the stored X_RR⁻¹ / X_t⁻¹
+ * blocks (reading R3) into a cache of the same size, held until the next factor.
+ *   x    : n×nrhs column-major complex128 (host or device), caller ordering
+ *   nrhs : ≥ 1
+ * Errors: EINVAL (NULL x, nrhs < 1), ESTATE (no factorization), ESINGULAR, ENOMEM, ECUDA. */
+int fmmlu_apply(fmmlu_handle* h, void* x, int nrhs);
 
 /* Apply the (unfactored) matrix: y = A x by brute-force O(n²) summation on the
  * GPU (test/measurement infrastructure for residuals; reading C17).

@@ -332,6 +332,7 @@ struct Phase {  // one (level, colour) elimination phase
   int nrec = 0, kmax = 0, rmax = 0, nitems = 0;
   int tmp_rows = 0;  // Σ r over the phase's boxes (solve scratch)
   size_t fac_bytes = 0;
+  DBuf ap_xs, ap_recs;  // fmmlu_apply: X_RR blocks (re-inverted X_RR⁻¹) and records pointing at them
 };
 
 double now_ms() {
@@ -418,6 +419,8 @@ struct fmmlu_handle {
   std::vector<Phase> phases;
   DBuf root;       // n0 × n0 complex: X_t⁻¹
   DBuf root_rows;  // int n0
+  DBuf root_fwd;   // n0 × n0 complex: A_{B_tB_t} for fmmlu_apply (built on first use)
+  bool apply_ready = false;
   int64_t n0 = 0;
   fmmlu_stats_t stats{};
   size_t cur_bytes = 0, peak_bytes = 0;
@@ -1204,6 +1207,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   h->phases.clear();
   h->root.release();
   h->root_rows.release();
+  h->root_fwd.release();
+  h->apply_ready = false;
   h->factored = false;
   fmmlu_stats_t& S = h->stats;
   std::memset(S.t_levels_ms, 0, sizeof(S.t_levels_ms));
@@ -2123,6 +2128,107 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   P.resolve();
 }
 
+// ---- forward factored apply
+// A ≈ V₁⋯V_M P_t D P_tᵀ W_M⋯W₁ with D = diag(X_{R_jR_j}, A_{B_tB_t}).  The factor store keeps
+// X_RR⁻¹ and X_t⁻¹ (reading R3); their inverses are formed once, on the first apply, by the same
+// batched Gauss-Jordan kernels and cached until the next factorization.
+void apply_prepare(fmmlu_handle* h) {
+  cudaStream_t st = h->stream;
+  DBuf status;
+  status.alloc(16, st);
+  FMMLU_CUDA(cudaMemsetAsync(status.p, 0, 16, st));
+  std::vector<DBuf> keep;
+  for (auto& ph : h->phases) {
+    if (ph.nrec <= 0) continue;
+    std::vector<BoxRec> recs(ph.nrec);
+    FMMLU_CUDA(cudaMemcpyAsync(recs.data(), ph.recs.p, recs.size() * sizeof(BoxRec), cudaMemcpyDeviceToHost, st));
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    long long off = 0;
+    std::vector<std::pair<long long, int>> mats;
+    for (auto& R : recs) {
+      R.Xi = off;
+      mats.push_back({off, R.r});
+      off += (long long)R.r * R.r;
+    }
+    ph.ap_xs.alloc(std::max<long long>(1, off) * sizeof(cplx), st);
+    ph.ap_recs.alloc(recs.size() * sizeof(BoxRec), st);
+    FMMLU_CUDA(cudaMemcpyAsync(ph.ap_recs.p, recs.data(), recs.size() * sizeof(BoxRec), cudaMemcpyHostToDevice, st));
+    track(h, ph.ap_xs.bytes);
+    launch_apply_copyX(ph.recs.as<BoxRec>(), ph.ap_recs.as<BoxRec>(), ph.nrec, ph.fac.as<cplx>(),
+                       ph.ap_xs.as<cplx>(), st);
+    std::vector<std::pair<cplx*, int>> mp;
+    for (auto& m : mats)
+      if (m.second > 0) mp.push_back({ph.ap_xs.as<cplx>() + m.first, m.second});
+    gj_blocked(h, mp, status.as<int>(), keep, FMMLU_K_APPLY);
+    FMMLU_CUDA(cudaStreamSynchronize(st));  // recs (host) and the staging arena are reused next phase
+    keep.clear();
+  }
+  if (h->n0 > 0) {
+    const size_t bytes = (size_t)h->n0 * h->n0 * sizeof(cplx);
+    h->root_fwd.alloc(bytes, st);
+    track(h, bytes);
+    FMMLU_CUDA(cudaMemcpyAsync(h->root_fwd.p, h->root.p, bytes, cudaMemcpyDeviceToDevice, st));
+    gj_blocked(h, {{h->root_fwd.as<cplx>(), (int)h->n0}}, status.as<int>(), keep, FMMLU_K_APPLY);
+  }
+  int hstatus = 0;
+  FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  wait_stream(h, st);
+  h->prof.resolve();
+  if (hstatus) throw Error(FMMLU_ESINGULAR, "singular stored inverse while preparing fmmlu_apply");
+  h->apply_ready = true;
+}
+
+void apply_impl(fmmlu_handle* h, void* xio, int nrhs) {
+  cudaStream_t st = h->stream;
+  if (!h->apply_ready) apply_prepare(h);
+  const int n = (int)h->n;
+  const bool dev = is_device_ptr(xio);
+  DBuf io, y;
+  cplx* b = reinterpret_cast<cplx*>(xio);
+  if (!dev) {
+    io.alloc((size_t)n * nrhs * sizeof(cplx), st);
+    FMMLU_CUDA(cudaMemcpyAsync(io.p, xio, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    b = io.as<cplx>();
+  }
+  y.alloc((size_t)n * nrhs * sizeof(cplx), st);
+  cplx* yp = y.as<cplx>();
+  Prof& P = h->prof;
+  int sid = P.begin(FMMLU_K_APPLY, st);
+  launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);  // W^{½} x, tree order
+  size_t scr_rows = 1;
+  for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
+  DBuf scr;
+  scr.alloc(scr_rows * nrhs * sizeof(cplx), st);
+  for (auto& ph : h->phases) {  // W_M⋯W₁ x: W₁ first
+    FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)ph.tmp_rows * nrhs * sizeof(cplx), st));
+    launch_apply_w(ph.recs.as<BoxRec>(), ph.nrec, ph.items.as<SolveItem>(), ph.nitems, ph.fac.as<cplx>(),
+                   ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.rmax, ph.kmax);
+  }
+  for (auto& ph : h->phases)  // D on the R blocks
+    launch_apply_d(ph.ap_recs.as<BoxRec>(), ph.nrec, ph.ap_xs.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs,
+                   scr.as<cplx>(), st, ph.rmax);
+  DBuf tmp;
+  if (h->n0 > 0) {  // P_t A_{B_tB_t} P_tᵀ
+    tmp.alloc(2 * (size_t)h->n0 * nrhs * sizeof(cplx), st);
+    launch_root_apply(h->root_fwd.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), yp, n, nrhs, tmp.as<cplx>(), st);
+  }
+  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it)  // V₁⋯V_M: V_M first
+    launch_apply_v(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
+                   it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax);
+  launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);  // W^{-½}, caller order
+  P.end(sid, st);
+  {
+    double entries = 2.0 * (double)h->n0 * h->n0;
+    for (auto& ph : h->phases) entries += (double)ph.fac_bytes / 16.0;
+    P.add(FMMLU_K_APPLY, 8.0 * entries * nrhs, 16.0 * entries + 64.0 * n * nrhs,
+          2 + 8 * (long long)h->phases.size() + (h->n0 > 0 ? 3 : 0));
+  }
+  if (!dev)
+    FMMLU_CUDA(cudaMemcpyAsync(xio, io.p, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  FMMLU_CUDA(cudaStreamSynchronize(st));
+  P.resolve();
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -2682,6 +2788,17 @@ int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs) {
   });
 }
 
+int fmmlu_apply(fmmlu_handle* h, void* x, int nrhs) {
+  if (!h) return fail(FMMLU_EINVAL, "NULL handle");
+  if (!x) return fail(FMMLU_EINVAL, "NULL x");
+  if (nrhs < 1) return fail(FMMLU_EINVAL, "nrhs must be >= 1");
+  if (!h->factored) return fail(FMMLU_ESTATE, "fmmlu_apply called before a successful fmmlu_factor");
+  return guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    apply_impl(h, x, nrhs);
+  });
+}
+
 int fmmlu_matvec(fmmlu_handle* h, double k, const void* x, void* y, int nrhs) {
   if (!h) return fail(FMMLU_EINVAL, "NULL handle");
   if (!x || !y || nrhs < 1) return fail(FMMLU_EINVAL, "bad x/y/nrhs");
@@ -2784,6 +2901,7 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->phases.clear();
   h->root.release();
   h->root_rows.release();
+  h->root_fwd.release();
   h->geo.release();
   h->perm.release();
   if (h->stream) cudaStreamSynchronize(h->stream);

@@ -979,19 +979,25 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
 #pragma unroll
     for (int r = 0; r < MR; ++r)
       if (row0 + 32 * r == p) c[r] = cmk(d.x - 1.0, d.y);
+    // Branch-free update of every register column (columns q ≥ nq are never read back, so their
+    // garbage is harmless); the pivot column is replaced by select.  A branch per column kept
+    // each column's DFMA chain in its own basic block and the update latency-bound.
+    cplx pc[MR];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int i = row0 + 32 * r;
+      pc[r] = i == p ? dinv : cmk(-(c[r].x * dinv.x - c[r].y * dinv.y), -(c[r].x * dinv.y + c[r].y * dinv.x));
+    }
 #pragma unroll
     for (int q = 0; q < MC; ++q) {
-      if (q >= nq) break;
-      if (q == qj) {  // the pivot column: −cs/d, and 1/d in row p
+      if ((q & 3) == 0 && q >= nq) break;  // branch only every 4 columns
+      const cplx rp = rpw[q];
+      const bool isp = q == qj;
 #pragma unroll
-        for (int r = 0; r < MR; ++r) {
-          const int i = row0 + 32 * r;
-          a[q][r] = i == p ? dinv : cmk(-(c[r].x * dinv.x - c[r].y * dinv.y), -(c[r].x * dinv.y + c[r].y * dinv.x));
-        }
-      } else {
-        const cplx rp = rpw[q];
-#pragma unroll
-        for (int r = 0; r < MR; ++r) a[q][r] = cfms(c[r], rp, a[q][r]);
+      for (int r = 0; r < MR; ++r) {
+        const cplx u = cfms(c[r], rp, a[q][r]);
+        a[q][r].x = isp ? pc[r].x : u.x;
+        a[q][r].y = isp ? pc[r].y : u.y;
       }
     }
     GJ_TICK(4);
@@ -1463,9 +1469,9 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
       c[r] = i < b ? cmk(colp[i].x * ipv, colp[i].y * ipv) : cmk(0.0, 0.0);
     }
 #pragma unroll
-    for (int q = 0; q < MC; ++q) {
-      if (q >= nq) break;
-      const int g = rank + ((cgp + CG * q) << lgCL);
+    for (int q = 0; q < MC; ++q) {  // branch only every 4 columns (see k_gj_reg)
+      if ((q & 3) == 0 && q >= nq) break;
+      const int g = min(rank + ((cgp + CG * q) << lgCL), b - 1);
       const cplx u = colp[g];
       const cplx uc = cmk(u.x, -u.y);  // conj(S_gp) = S_pg
 #pragma unroll
@@ -1864,7 +1870,8 @@ __global__ void __launch_bounds__(SV_NT) k_su_a(const BoxRec* __restrict__ recs,
 __global__ void __launch_bounds__(kSolveChunk) k_su_b(const BoxRec* __restrict__ recs,
                                                       const SolveItem* __restrict__ items,
                                                       const cplx* __restrict__ fac, const int* __restrict__ idx,
-                                                      cplx* y, int ldy, int nrhs, const cplx* __restrict__ tmp) {
+                                                      cplx* y, int ldy, int nrhs, const cplx* __restrict__ tmp,
+                                                      double sg) {
   extern __shared__ double shm[];
   const SolveItem it = items[blockIdx.x];
   const BoxRec R = recs[it.rec];
@@ -1894,11 +1901,11 @@ __global__ void __launch_bounds__(kSolveChunk) k_su_b(const BoxRec* __restrict__
       for (int q = 0; q < nq; ++q) {
         if (f < k) {
           cplx* d = y + idx[R.idxS + f] + (size_t)(q0 + q) * ldy;
-          *d = csub(*d, acc[q]);
+          *d = cmk(d->x + sg * acc[q].x, d->y + sg * acc[q].y);
         } else {
           cplx* d = y + idx[R.idxN + f - k] + (size_t)(q0 + q) * ldy;
-          atomicAdd(&d->x, -acc[q].x);
-          atomicAdd(&d->y, -acc[q].y);
+          atomicAdd(&d->x, sg * acc[q].x);
+          atomicAdd(&d->y, sg * acc[q].y);
         }
       }
     }
@@ -1982,9 +1989,11 @@ __global__ void __launch_bounds__(SV_NT) k_sd_b(const BoxRec* __restrict__ recs,
 // down [b1]: y_R −= acc (acc = Up y_{S∪N} from k_sd_a)    (elementwise)
 // down [b2]: y_S −= T[:, i-chunk] y_R[i-chunk]            (thread per row l of T, atomics)
 constexpr int SV_CH = 32;
+// apply = 0 (solve, E):  t = y_R − Tᵀ y_S → tmp, y_R ← 0
+// apply = 1 (forward, E⁻¹): y_R += Tᵀ y_S
 __global__ void __launch_bounds__(256) k_su_e(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
                                              const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
-                                             cplx* __restrict__ tmp) {
+                                             cplx* __restrict__ tmp, int apply) {
   const BoxRec R = recs[blockIdx.x];
   const int lane = threadIdx.x & 31, i = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (i >= R.r) return;
@@ -2013,8 +2022,12 @@ __global__ void __launch_bounds__(256) k_su_e(const BoxRec* __restrict__ recs, c
       for (int q = 1; q < SV_Q; ++q)
         if (q == lane) a = acc[q];
       cplx* d = y + gi + (size_t)(q0 + lane) * ldy;
-      tb[i + (size_t)(q0 + lane) * r] = csub(*d, a);
-      *d = cmk(0.0, 0.0);
+      if (apply) {
+        *d = cadd(*d, a);
+      } else {
+        tb[i + (size_t)(q0 + lane) * r] = csub(*d, a);
+        *d = cmk(0.0, 0.0);
+      }
     }
   }
 }
@@ -2059,18 +2072,19 @@ __global__ void __launch_bounds__(128) k_su_dinv(const BoxRec* __restrict__ recs
 }
 
 __global__ void k_sd_b1(const BoxRec* __restrict__ recs, const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
-                        const cplx* __restrict__ tmp) {
+                        const cplx* __restrict__ tmp, double sg) {
   const BoxRec R = recs[blockIdx.x];
   const cplx* tb = tmp + (size_t)R.tmp * nrhs;
   for (int e = threadIdx.x; e < R.r * nrhs; e += blockDim.x) {
     const int i = e % R.r, q = e / R.r;
     cplx* d = y + idx[R.idxR + i] + (size_t)q * ldy;
-    *d = csub(*d, tb[i + (size_t)q * R.r]);
+    const cplx t = tb[i + (size_t)q * R.r];
+    *d = cmk(d->x + sg * t.x, d->y + sg * t.y);
   }
 }
 
 __global__ void __launch_bounds__(128) k_sd_b2(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
-                                              const int* __restrict__ idx, cplx* y, int ldy, int nrhs) {
+                                              const int* __restrict__ idx, cplx* y, int ldy, int nrhs, double sg) {
   const BoxRec R = recs[blockIdx.x];
   const int k = R.k, r = R.r;
   const int l = blockIdx.y * 128 + threadIdx.x, i0 = blockIdx.z * SV_CH;
@@ -2099,8 +2113,8 @@ __global__ void __launch_bounds__(128) k_sd_b2(const BoxRec* __restrict__ recs, 
       const int gs = idx[R.idxS + l];
       for (int q = 0; q < nq; ++q) {
         cplx* d = y + gs + (size_t)(q0 + q) * ldy;
-        atomicAdd(&d->x, -acc[q].x);
-        atomicAdd(&d->y, -acc[q].y);
+        atomicAdd(&d->x, sg * acc[q].x);
+        atomicAdd(&d->y, sg * acc[q].y);
       }
     }
   }
@@ -2842,13 +2856,13 @@ void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, 
     cb = sb;
   }
   (void)sa;
-  k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp);
+  k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp, 0);
   FMMLU_LAUNCH();
   k_su_dinv<<<dim3(nrec, (rmax + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
                                                                                        nrhs, tmp);
   FMMLU_LAUNCH();
   if (nitems > 0) {
-    k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
+    k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, -1.0);
     FMMLU_LAUNCH();
   }
 }
@@ -2869,10 +2883,87 @@ void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items
     FMMLU_LAUNCH();
   }
   (void)sb;
-  k_sd_b1<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp);
+  k_sd_b1<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp, -1.0);
   FMMLU_LAUNCH();
   k_sd_b2<<<dim3(nrec, (kmax_down + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
-                                                                                          nrhs);
+                                                                                          nrhs, -1.0);
+  FMMLU_LAUNCH();
+}
+
+// ---- forward factored apply A ≈ V₁⋯V_M P_t D P_tᵀ W_M⋯W₁
+// tmp[R rows] = y_R (and y_R ← 0 when zero)
+__global__ void k_ap_gather(const BoxRec* __restrict__ recs, const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                            cplx* __restrict__ tmp, int zero) {
+  const BoxRec R = recs[blockIdx.x];
+  cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int e = threadIdx.x; e < R.r * nrhs; e += blockDim.x) {
+    const int i = e % R.r, q = e / R.r;
+    cplx* d = y + idx[R.idxR + i] + (size_t)q * ldy;
+    tb[i + (size_t)q * R.r] = *d;
+    if (zero) *d = cmk(0.0, 0.0);
+  }
+}
+// dst[recsX.Xi] = fac[recs.Xi]  (r × r per box; the stored X_RR⁻¹ blocks, to be re-inverted)
+__global__ void k_ap_copyX(const BoxRec* __restrict__ recs, const BoxRec* __restrict__ recsX,
+                           const cplx* __restrict__ fac, cplx* __restrict__ dst) {
+  const BoxRec R = recs[blockIdx.x];
+  const cplx* s = fac + R.Xi;
+  cplx* d = dst + recsX[blockIdx.x].Xi;
+  const long long m = (long long)R.r * R.r;
+  for (long long e = threadIdx.x; e < m; e += blockDim.x) d[e] = s[e];
+}
+
+void launch_apply_copyX(const BoxRec* d_recs, const BoxRec* d_recsX, int nrec, const cplx* fac, cplx* dst,
+                        cudaStream_t st) {
+  if (nrec <= 0) return;
+  k_ap_copyX<<<nrec, 256, 0, st>>>(d_recs, d_recsX, fac, dst);
+  FMMLU_LAUNCH();
+}
+
+// W_j = U⁻¹ F⁻¹ Pᵀ for the phase's boxes: y_S += T y_R, then y_R += Up y_{S∪N}  (tmp zeroed by the caller)
+void launch_apply_w(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                    const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax, int kmax) {
+  if (nrec <= 0) return;
+  k_sd_b2<<<dim3(nrec, (kmax + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
+                                                                                     nrhs, 1.0);
+  FMMLU_LAUNCH();
+  if (nitems > 0) {
+    const size_t sa = (size_t)kSolveChunk * SV_Q * sizeof(cplx) + 16;
+    k_sd_a<<<nitems, SV_NT, sa, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
+    FMMLU_LAUNCH();
+  }
+  k_sd_b1<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp, 1.0);
+  FMMLU_LAUNCH();
+}
+
+// D on the phase's R blocks: y_R ← X_RR y_R  (recsX/xs: re-inverted blocks)
+void launch_apply_d(const BoxRec* d_recsX, int nrec, const cplx* xs, const int* idx, cplx* y, int ldy, int nrhs,
+                    cplx* tmp, cudaStream_t st, int rmax) {
+  if (nrec <= 0) return;
+  k_ap_gather<<<nrec, 256, 0, st>>>(d_recsX, idx, y, ldy, nrhs, tmp, 1);
+  FMMLU_LAUNCH();
+  k_su_dinv<<<dim3(nrec, (rmax + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recsX, xs, idx, y, ldy,
+                                                                                       nrhs, tmp);
+  FMMLU_LAUNCH();
+}
+
+// V_j = P E⁻¹ L⁻¹: y_{S∪N} += Lp y_R, then y_R += Tᵀ y_S
+void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                    const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax) {
+  if (nrec <= 0) return;
+  k_ap_gather<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp, 0);
+  FMMLU_LAUNCH();
+  if (nitems > 0) {
+    const size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
+    static size_t cb = 0;
+    if (sb > 48 * 1024 && sb > cb) {
+      FMMLU_CUDA(cudaFuncSetAttribute(k_su_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+      cb = sb;
+    }
+    k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, 1.0);
+    FMMLU_LAUNCH();
+  }
+  k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp, 1);
   FMMLU_LAUNCH();
 }
 

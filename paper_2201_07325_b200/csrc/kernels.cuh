@@ -196,6 +196,15 @@ void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, 
 void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                         const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax,
                         int kmax);
+// forward factored apply: per-phase W, D and V sweeps (see kernels.cu)
+void launch_apply_copyX(const BoxRec* d_recs, const BoxRec* d_recsX, int nrec, const cplx* fac, cplx* dst,
+                        cudaStream_t st);
+void launch_apply_w(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                    const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax, int kmax);
+void launch_apply_d(const BoxRec* d_recsX, int nrec, const cplx* xs, const int* idx, cplx* y, int ldy, int nrhs,
+                    cplx* tmp, cudaStream_t st, int rmax);
+void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
+                    const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax);
 // y[rows] = Xinv (n0×n0) · y[rows] for the root block
 void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
                        cplx* tmp, cudaStream_t st);

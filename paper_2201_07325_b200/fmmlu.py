@@ -48,9 +48,9 @@ class Stats(ctypes.Structure):
         return d
 
 
-KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve"]
+KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve", "apply"]
 
-EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_matvec", "fmmlu_destroy",
+EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
            "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes")
 
@@ -74,6 +74,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_tree.argtypes = [vp, vp, vp, i64, ci, ctypes.POINTER(vp)]
     L.fmmlu_factor.argtypes = [vp, cd, cd]
     L.fmmlu_solve.argtypes = [vp, vp, ci]
+    L.fmmlu_apply.argtypes = [vp, vp, ci]
     L.fmmlu_matvec.argtypes = [vp, cd, vp, vp, ci]
     L.fmmlu_destroy.argtypes = [vp]
     L.fmmlu_last_error.restype = ctypes.c_char_p
@@ -140,6 +141,16 @@ class FmmLu:
         _check(load().fmmlu_solve(self.h, _ptr(rhs), int(nrhs)))
         return rhs
 
+    def apply(self, x, nrhs: int | None = None):
+        """In place: x (n×nrhs column-major complex128) is overwritten with Â x, the forward
+        factored operator V₁⋯V_M P_t D P_tᵀ W_M⋯W₁ ≈ A.  Returns x."""
+        if nrhs is None:
+            nrhs = 1 if x.ndim == 1 else int(x.shape[1])
+        if isinstance(x, np.ndarray):
+            assert x.dtype == np.complex128 and (x.ndim == 1 or x.flags.f_contiguous)
+        _check(load().fmmlu_apply(self.h, _ptr(x), int(nrhs)))
+        return x
+
     def matvec(self, k: float, x, y=None):
         nrhs = 1 if x.ndim == 1 else int(x.shape[1])
         if y is None:
@@ -194,6 +205,10 @@ def fmmlu_factor(h: FmmLu, k: float, eps: float) -> FmmLu:
 
 def fmmlu_solve(h: FmmLu, rhs, nrhs: int | None = None):
     return h.solve(rhs, nrhs)
+
+
+def fmmlu_apply(h: FmmLu, x, nrhs: int | None = None):
+    return h.apply(x, nrhs)
 
 
 def probe_fp64(kind: int) -> float:

@@ -228,3 +228,32 @@ def test_pchol_modes_parity(F, mode):
     for lvl, s in f.stats["levels"].items():
         ro = int(s["ranks"].sum())
         assert abs(st["ranks_sum"][lvl] - ro) <= 0.03 * ro + 2
+
+
+# ---- forward factored apply
+@pytest.mark.parametrize("case", ["ellipsoid3000", "cube1500", "single_leaf"])
+def test_apply_parity(F, case):
+    eps = 1e-6
+    if case == "ellipsoid3000":
+        g, k, leaf = fi.ellipsoid(3000), 2 * math.pi, 32
+    elif case == "cube1500":
+        g, k, leaf = fi.random_cube(1500, seed=2), 3.0, 16
+    else:
+        g, k, leaf = fi.fibonacci_sphere(60), 1.0, 64
+    x = fi.gaussian_rhs(g.n, 3, 7)
+    h = F.FmmLu(g.points, g.normals, g.weights, leaf).factor(k, eps)
+    y = np.asfortranarray(x.copy())
+    h.apply(y)
+    ye = okern.matvec_unscaled(k, g.points, g.normals, g.weights, x)   # brute-force A x
+    tol = 1e-12 if case == "single_leaf" else 10 * eps
+    assert dense.rel_diff(y, ye) <= tol
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf)
+    assert dense.rel_diff(y, rss.apply(f, x)) <= tol
+    # solve ∘ apply = identity on the GPU's own factors (second apply reuses the cached D)
+    z = np.asfortranarray(y.copy())
+    h.solve(z)
+    assert dense.rel_diff(z, x) < 1e-10
+    w = np.asfortranarray(x.copy())
+    h.solve(w)
+    h.apply(w)
+    assert dense.rel_diff(w, x) < 1e-10
