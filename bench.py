@@ -91,6 +91,47 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+# ncu --set full summaries committed under profiles/ (tools/ncu_summary.py full): DRAM traffic
+# per launch of the kernel behind each class, for the roofline's "traffic" field
+NCU_FULL = {"schur": "k_gemm_schur", "ef": "k_gemm_store", "panel": "k_gemm_store", "qr": "k_gemm_store",
+            "inv": "k_gj_panel", "cpqr": "k_pchol_cluster", "gather": "k_proxy", "build": "k_build_level"}
+
+
+def ncu_traffic(cls: str):
+    """(bytes per launch, source file) from the newest committed ncu full capture, or (None, None)."""
+    kern = NCU_FULL.get(cls)
+    if not kern:
+        return None, None
+    pdir = os.path.join(ROOT, "profiles")
+    cands = sorted(f for f in os.listdir(pdir) if f.endswith(f"ncu_full_{kern}.json")) if os.path.isdir(pdir) else []
+    if not cands:
+        return None, None
+    try:
+        d = json.load(open(os.path.join(pdir, cands[-1])))
+        big = [l for l in d["launches"] if l.get("dram_read") is not None]
+        # launches of one factorization (ncu -c caps the list; the summary is over the same set)
+        return float(d["summary"]["traffic_per_launch"]), f"profiles/{cands[-1]} ({len(big)} launches)"
+    except Exception:
+        return None, None
+
+
+def max_over_ranks(t_ms: float, world: int, device=None) -> float:
+    """Max of a per-rank time over all ranks (all_reduce MAX; a no-op at world = 1).  Works on
+    any backend: the tensor lives on `device` (cuda under NCCL, cpu under gloo)."""
+    if world <= 1:
+        return float(t_ms)
+    import torch
+    tt = torch.tensor([float(t_ms)], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def job_throughput(n_per_rank: int, world: int, t_step_ms: float) -> float:
+    """Whole-job unknowns/s: every rank factors its own replica (weak scaling),
+    timed as the slowest rank."""
+    return world * n_per_rank / (t_step_ms * 1e-3)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -232,11 +273,7 @@ def main():
         if world > 1:
             torch.distributed.barrier()
     ms = [a.elapsed_time(b) for a, b in ev]
-    t_step = float(np.mean(ms))
-    if world > 1:
-        tt = torch.tensor([t_step], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_step = float(tt.item())
+    t_step = max_over_ranks(float(np.mean(ms)), world, dev)
     st = stats[-1]
     t_fac = float(np.mean([s["t_factor_ms"] for s in stats]))
     t_sol = float(np.mean([s["t_solve_ms"] for s in stats]))
@@ -257,11 +294,7 @@ def main():
     x = np.asfortranarray(x)
     Ax = h2.matvec(c["k"], x)
     resid = float(np.max(np.linalg.norm(Ax - b_host, axis=0) / np.linalg.norm(b_host, axis=0)))
-    t_e2e = float(np.mean(e2e_ms))
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_e2e = float(tt.item())
+    t_e2e = max_over_ranks(float(np.mean(e2e_ms)), world, dev)
 
     # ---- roofline of the dominant kernel class (events recorded inside libfmmlu)
     cls = F.KERNEL_CLASSES
@@ -272,22 +305,25 @@ def main():
     hbm = peaks.get("hbm_gbs", 6650.0)
     fl, by, t = st["class_flops"][dom], st["class_bytes"][dom], cms[dom]
     per_launch = max(1, st["class_launches"][dom])
+    traffic, traffic_src = ncu_traffic(cls[dom])
     if cls[dom] in ("schur", "ef", "panel", "qr"):
         achieved = fl / (t * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": dmma_tf, "unit": "TFLOP/s",
-                "frac": achieved / dmma_tf, "traffic": None, "kernel": cls[dom],
+                "frac": achieved / dmma_tf, "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": by / per_launch, "kernel": cls[dom],
                 "peak_source": "FP64 DMMA m8n8k4 probe measured in this run (MEASURED_PEAKS has no FP64 entry)",
                 "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch}
     elif cls[dom] in ("build", "gather", "solve", "apply"):
         achieved = by / (t * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "kernel": cls[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": cls[dom], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "bytes_per_launch": by / per_launch, "ms_per_launch": t / per_launch}
     else:
         dfma_tf = F.probe_fp64(0)
         achieved = fl / (t * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": dfma_tf, "unit": "TFLOP/s",
-                "frac": achieved / dfma_tf, "traffic": None, "kernel": cls[dom],
+                "frac": achieved / dfma_tf, "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": cls[dom],
                 "peak_source": "FP64 DFMA probe measured in this run",
                 "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch}
     breakdown = {cls[i]: {"ms": round(cms[i], 3), "share": round(cms[i] / max(1e-9, sum(cms)), 4),
@@ -305,7 +341,7 @@ def main():
     h2d = g.points.nbytes + g.normals.nbytes + g.weights.nbytes + b_host.nbytes
     d2h = b_host.nbytes
     line = {
-        "metric": METRIC, "value": world * n / (t_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": job_throughput(n, world, t_step), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": f"{CFG}: ellipsoid (0.5,1,2) n={n}, k=2pi, leaf 64, eps 1e-6, {nrhs} RHS",
@@ -316,7 +352,7 @@ def main():
         "tree_ms": t_tree, "factor_ms": t_fac, "solve_ms": t_sol,
         "n0": st["n0"], "peak_mem_bytes": st["peak_bytes"], "factor_bytes": st["factor_bytes"],
         "residual": resid,
-        "e2e": {"value": world * n / (t_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        "e2e": {"value": job_throughput(n, world, t_e2e), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e, "ms_steps": [round(v, 2) for v in e2e_ms],
                 "host_buffers": "pinned",
                 "timing": "host wall clock around tree+factor+solve incl. H2D/D2H, mean of K steps"},
