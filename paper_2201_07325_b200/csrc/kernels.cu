@@ -795,6 +795,20 @@ __global__ void k_gj_copyback(const GjTask* __restrict__ tasks, const cplx* __re
 // candidates (DSMEM) → p, d; the lanes holding row p publish m_pc/d for their columns;
 // CTA barrier B2; [P3] register update.  grid (CL, ntasks), 512 threads.
 
+// Warp argmax of (v, idx) with ties → lowest idx, by three redux.sync steps on the IEEE bit
+// pattern (monotone for v ≥ 0) instead of five shuffle rounds.  Lanes without a candidate pass
+// idx = INT_MAX.  Non-positive v compare as 0 (only reached when every candidate is ≤ 0, where the
+// callers stop or flag); the result v is then 0 (or -1 with idx INT_MAX if nobody had one).
+__device__ __forceinline__ void warp_argmax_redux(double& v, int& idx) {
+  const unsigned long long key = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned bi = __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)idx : 0xffffffffu);
+  idx = (int)bi;
+  v = idx == INT_MAX ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+}
+
 // Exchange record of one row group's pivot candidate: |x|², row, x.
 struct GjCand {
   double v;
@@ -827,8 +841,6 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
   const int n = t.n;
   const int ncl = (n - rank + CL - 1) >> lgCL;
   const int RG = (n + 32 * MR - 1) >> (5 + LGMR), CG = GJR_NW / RG;
-  int rgp2 = 1;  // rounds of the cross-row-group candidate reduction: log2(next pow2 ≥ RG)
-  while (rgp2 < RG) rgp2 <<= 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rg = warp % RG, cgp = warp / RG;
   cplx* const xg = t.Am;                                        // [2][n]
@@ -883,20 +895,10 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
           }
         }
       }
-#pragma unroll
-      for (int s = 16; s > 0; s >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
-        const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
-        double x2 = 0.0, y2 = 0.0;
-        if (MULTI) {
-          x2 = __shfl_xor_sync(0xffffffffu, px.x, s);
-          y2 = __shfl_xor_sync(0xffffffffu, px.y, s);
-        }
-        if (v2 > pv || (v2 == pv && i2 < p)) {
-          pv = v2;
-          p = i2;
-          if (MULTI) px = cmk(x2, y2);
-        }
+      warp_argmax_redux(pv, p);
+      if (MULTI) {  // the winning row's value, from the lane that holds it
+        const int src = p == INT_MAX ? 0 : (p & 31);
+        px = cmk(__shfl_sync(0xffffffffu, px.x, src), __shfl_sync(0xffffffffu, px.y, src));
       }
       if (lane == 0) {
         GjCand cd;
@@ -931,26 +933,15 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
       const int i = row0 + 32 * r;
       c[r] = i < n ? (MULTI ? __ldcg(reinterpret_cast<const double2*>(pcol + i)) : pcol[i]) : cmk(0.0, 0.0);
     }
-    for (int s = rgp2 >> 1; s > 0; s >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
-      const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
-      double x2 = 0.0, y2 = 0.0;
-      if (MULTI) {
-        x2 = __shfl_xor_sync(0xffffffffu, d.x, s);
-        y2 = __shfl_xor_sync(0xffffffffu, d.y, s);
-      }
-      if (v2 > pv || (v2 == pv && i2 < p)) {
-        pv = v2;
-        p = i2;
-        if (MULTI) d = cmk(x2, y2);
-      }
-    }
-    pv = __shfl_sync(0xffffffffu, pv, 0);
-    p = __shfl_sync(0xffffffffu, p, 0);
+    warp_argmax_redux(pv, p);  // every lane gets the result (redux.sync is warp-uniform)
     const bool sing = !(pv > 0.0);
     if (p == INT_MAX) p = j;  // NaN column: keep indices in range (flagged below, result invalid)
-    if (MULTI) d = cmk(__shfl_sync(0xffffffffu, d.x, 0), __shfl_sync(0xffffffffu, d.y, 0));
-    else d = pcol[p];
+    if (MULTI) {  // d from the lane holding the winning row group's candidate
+      const int src = p >> (5 + LGMR);
+      d = cmk(__shfl_sync(0xffffffffu, d.x, src), __shfl_sync(0xffffffffu, d.y, src));
+    } else {
+      d = pcol[p];
+    }
     if (sing) d = cmk(1.0, 0.0);
     const double rn = __drcp_rn(d.x * d.x + d.y * d.y);
     const cplx dinv = cmk(d.x * rn, -d.y * rn);
@@ -1332,6 +1323,8 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
   __shared__ int posmap[GJR_NMAX];
   __shared__ double cvs[2];
   __shared__ int cis[2];
+  __shared__ double ccv[2][16];  // cluster: candidates pushed by every CTA (DSMEM), [parity][rank]
+  __shared__ int cci[2][16];
   const ClusterQrTask t = tasks[blockIdx.y];
   const int b = t.b;
   const int ncl = (b - rank + CL - 1) >> lgCL;
@@ -1342,7 +1335,6 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
   const int nq = cgp < CG ? min(MC, (ncl - cgp + CG - 1) / CG) : 0;
   const int row0 = (rg << (5 + LGMR)) + lane;
   cplx* const xcol = MULTI ? xs + blockIdx.y * xstride : nullptr;                          // [2][CL][b]
-  double* const xcand = MULTI ? reinterpret_cast<double*>(xcol + 2 * (size_t)CL * b) : nullptr;  // [2][CL][2]
   cplx* const Rg = t.out;  // b × b (ld b): R rows by natural column
   cplx a[MC][MR];
 #pragma unroll
@@ -1372,15 +1364,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
         lv = dg[l];
         ll = l;
       }
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, lv, s);
-      const int i2 = __shfl_xor_sync(0xffffffffu, ll, s);
-      if (v2 > lv || (v2 == lv && i2 < ll)) {
-        lv = v2;
-        ll = i2;
-      }
-    }
+    warp_argmax_redux(lv, ll);
     const int lg_ = ll == INT_MAX ? INT_MAX : rank + (ll << lgCL);  // global column of the candidate
     if (ll != INT_MAX && cgp == ll % CG && cgp < CG) {
       const int qs = ll / CG;
@@ -1398,14 +1382,16 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
         }
       }
     }
-    if (tid == 0) {
-      if (MULTI) {
-        __stcg(xcand + ((size_t)par * CL + rank) * 2, lv);
-        __stcg(reinterpret_cast<long long*>(xcand + ((size_t)par * CL + rank) * 2 + 1), (long long)lg_);
-      } else {
-        cvs[par] = lv;
-        cis[par] = lg_;
+    if (MULTI) {  // push the candidate into every CTA's shared memory (read locally after B1)
+      if (tid < CL) {
+        double* dv = cl.map_shared_rank(&ccv[par][rank], tid);
+        int* di = cl.map_shared_rank(&cci[par][rank], tid);
+        *dv = lv;
+        *di = lg_;
       }
+    } else if (tid == 0) {
+      cvs[par] = lv;
+      cis[par] = lg_;
     }
     if (TIMING) { const long long n_ = clock64(); tph[0] += n_ - tc; tc = n_; }
     if (MULTI) cl.sync(); else __syncthreads();  // B1
@@ -1414,24 +1400,11 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
     int p = INT_MAX, po = 0;
     if (MULTI) {
       if (lane < CL) {
-        pv = __ldcg(xcand + ((size_t)par * CL + lane) * 2);
-        p = (int)__ldcg(reinterpret_cast<const long long*>(xcand + ((size_t)par * CL + lane) * 2 + 1));
-        po = lane;
+        pv = ccv[par][lane];
+        p = cci[par][lane];
       }
-#pragma unroll
-      for (int s = 8; s > 0; s >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, pv, s);
-        const int i2 = __shfl_xor_sync(0xffffffffu, p, s);
-        const int o2 = __shfl_xor_sync(0xffffffffu, po, s);
-        if (v2 > pv || (v2 == pv && i2 < p)) {
-          pv = v2;
-          p = i2;
-          po = o2;
-        }
-      }
-      pv = __shfl_sync(0xffffffffu, pv, 0);
-      p = __shfl_sync(0xffffffffu, p, 0);
-      po = __shfl_sync(0xffffffffu, po, 0);
+      warp_argmax_redux(pv, p);              // global column; its owner CTA is p mod CL
+      po = p == INT_MAX ? 0 : (p & (CL - 1));
     } else {
       pv = cvs[par];
       p = cis[par];
