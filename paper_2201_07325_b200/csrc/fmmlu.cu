@@ -988,6 +988,16 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
     std::vector<GemmProblem> gp;
     std::vector<GemmTile> gt;
+    // split-K: as few chunks as keep ≈ 4 CTAs per SM busy (each chunk ends in an atomic
+    // read-modify-write of its 64×64 tile, so short chunks are epilogue-bound)
+    long long utiles = 0;
+    for (int j = 0; j < nj; ++j) {
+      const long long t = (bcol[j] + kTile - 1) / kTile;
+      utiles += t * (t + 1) / 2;
+    }
+    static const int g_cps = getenv("FMMLU_GRAM_CPS") ? atoi(getenv("FMMLU_GRAM_CPS")) : 8;
+    static const int g_minch = getenv("FMMLU_GRAM_MINCH") ? atoi(getenv("FMMLU_GRAM_MINCH")) : 128;
+    const long long want = std::max<long long>(1, ((long long)g_cps * 148 + utiles - 1) / std::max<long long>(utiles, 1));
     for (int j = 0; j < nj; ++j) {
       GemmProblem P{};
       P.m = bcol[j];
@@ -1001,7 +1011,11 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
       P.ldb = mrows[j];
       P.C = G.as<cplx>() + goff[j];
       P.ldc = bcol[j];
-      P.kchunk = mrows[j] > 512 ? 256 : 0;
+      {
+        long long ch = (mrows[j] + want - 1) / want;
+        ch = std::max<long long>(g_minch, (ch + 15) / 16 * 16);
+        P.kchunk = mrows[j] > ch ? (int)ch : 0;
+      }
       add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
     }
     run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);

@@ -88,6 +88,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Warp argmax of (v, idx) with ties → lowest idx, by three redux.sync steps on the IEEE bit
+// pattern (monotone for v ≥ 0) instead of five shuffle rounds.  Lanes without a candidate pass
+// idx = INT_MAX.  Non-positive v compare as 0 (only reached when every candidate is ≤ 0, where the
+// callers stop or flag); the result v is then 0 (or -1 with idx INT_MAX if nobody had one).
+__device__ __forceinline__ void warp_argmax_redux(double& v, int& idx) {
+  const unsigned long long key = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned bi = __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)idx : 0xffffffffu);
+  idx = (int)bi;
+  v = idx == INT_MAX ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+}
+
 // Cluster-wide argmax of the per-CTA candidates (cand_v, cand_i live in every CTA's shared
 // memory): lane r of warp 0 reads rank r's candidate through DSMEM, warp-reduces (ties → lowest
 // index), and broadcasts through (ov, oi).  Call after the cluster barrier that publishes them.
@@ -561,11 +575,15 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __rest
                                                            int* status, cplx* __restrict__ xs, long long xstride) {
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ __align__(16) unsigned char gpr_dyn[];
+  cplx* const crow = reinterpret_cast<cplx*>(gpr_dyn);  // [2][CL][nb]: every CTA's candidate row (DSMEM)
   __shared__ double wcv[2][GJR_NW];
   __shared__ int wci[2][GJR_NW];
-  __shared__ cplx fcol[2][GJR_NMAX];   // column s of the own rows (by local row)
-  __shared__ cplx prow[64], orow[64];  // pivot row, old row j
-  __shared__ int sp[2];
+  __shared__ cplx fcol[2][GJR_NMAX];  // column s of the own rows (by local row)
+  __shared__ cplx mrow[64], mold[64];  // this CTA's candidate row / old row j (before pushing)
+  __shared__ cplx cold[2][64];         // old row j, pushed by its owner (DSMEM)
+  __shared__ double ccv[2][16];        // candidates of every CTA (DSMEM), [parity][rank]
+  __shared__ int cci[2][16];
   const GjTask t = tasks[blockIdx.y];
   const int n = t.n;
   if (j0 >= n) return;  // uniform across the cluster
@@ -575,21 +593,21 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __rest
   const int RG = (rc + 31) >> 5, CG = GJR_NW / RG;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rg = warp % RG, cgp = warp / RG;
-  if ((jb + CG - 1) / CG > MC || RG > GJR_NW || nb > 64) __trap();  // configuration mismatch
+  if ((jb + CG - 1) / CG > MC || RG > GJR_NW || nb > 64 || CL > 16) __trap();  // configuration mismatch
   const int nq = cgp < CG ? min(MC, (jb - cgp + CG - 1) / CG) : 0;
   const int il = rg * 32 + lane;      // local row
   const int i = r0 + il;              // global row
   const bool rowok = il < rc && i < r1;
-  cplx* const X = xs + blockIdx.y * xstride;
-  double* const xc = reinterpret_cast<double*>(X);          // [2][CL][2]
-  cplx* const xrow = X + 2 * CL;                            // [2][CL][nb]
-  cplx* const xold = xrow + 2 * (size_t)CL * nb;            // [2][nb]
+  (void)xs;
+  (void)xstride;
   cplx a[MC];
 #pragma unroll
   for (int q = 0; q < MC; ++q) {
     const int c = cgp + CG * q;
     a[q] = (q < nq && rowok) ? t.A[i + (size_t)(j0 + c) * t.lda] : cmk(0.0, 0.0);
   }
+  // Per step: one cluster barrier; every exchange is pushed into the consumers' shared memory
+  // before it (candidate, candidate row, old row j), so nothing is read through L2 after it.
   for (int s = 0; s < jb; ++s) {
     const int j = j0 + s, par = s & 1;
     // ---- P1a: the warps holding panel column s: per-warp candidates, column values to smem
@@ -602,84 +620,52 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __rest
       if (rowok) fcol[par][il] = x;
       double v = (rowok && i >= j) ? cabs2(x) : -1.0;
       int ix = (rowok && i >= j) ? i : INT_MAX;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
-        if (v2 > v || (v2 == v && i2 < ix)) {
-          v = v2;
-          ix = i2;
-        }
-      }
+      warp_argmax_redux(v, ix);
       if (lane == 0) {
         wcv[par][rg] = v;
         wci[par][rg] = ix;
       }
     }
     __syncthreads();  // B0
-    // ---- P1b: CTA-local winner; publish its row, old row j (if here) and the candidate
+    // ---- P1b: CTA-local winner; its row and (if here) old row j to smem
     double lv = lane < RG ? wcv[par][lane] : -1.0;
     int li = lane < RG ? wci[par][lane] : INT_MAX;
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, lv, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, li, o);
-      if (v2 > lv || (v2 == lv && i2 < li)) {
-        lv = v2;
-        li = i2;
-      }
-    }
-    lv = __shfl_sync(0xffffffffu, lv, 0);
-    li = __shfl_sync(0xffffffffu, li, 0);
+    warp_argmax_redux(lv, li);
     if (rowok && (i == li || i == j)) {
 #pragma unroll
       for (int q = 0; q < MC; ++q) {
         if (q >= nq) break;
         const int c = cgp + CG * q;
-        if (i == li) __stcg(reinterpret_cast<double2*>(xrow + ((size_t)par * CL + rank) * nb + c), a[q]);
-        if (i == j) __stcg(reinterpret_cast<double2*>(xold + (size_t)par * nb + c), a[q]);
+        if (i == li) mrow[c] = a[q];
+        if (i == j) mold[c] = a[q];
       }
     }
-    if (tid == 0) {
-      __stcg(xc + ((size_t)par * CL + rank) * 2, lv);
-      __stcg(reinterpret_cast<long long*>(xc + ((size_t)par * CL + rank) * 2 + 1), (long long)li);
+    __syncthreads();  // B0b
+    // ---- push: candidate and candidate row to every CTA; old row j from its owner
+    const bool ownj = j >= r0 && j < r1;
+    for (int e = tid; e < CL * jb; e += GJR_NT) {
+      const int dst = e / jb, c = e - dst * jb;
+      *cl.map_shared_rank(&crow[((size_t)par * CL + rank) * nb + c], dst) = mrow[c];
+      if (ownj) *cl.map_shared_rank(&cold[par][c], dst) = mold[c];
+    }
+    if (tid < CL) {
+      *cl.map_shared_rank(&ccv[par][rank], tid) = lv;
+      *cl.map_shared_rank(&cci[par][rank], tid) = li;
     }
     cl.sync();  // B1
-    // ---- P2: global pivot row p (ties → lowest row), pivot row and old row j to smem
-    if (warp == 0) {
-      double pv = lane < CL ? __ldcg(xc + ((size_t)par * CL + lane) * 2) : -1.0;
-      int p = lane < CL ? (int)__ldcg(reinterpret_cast<const long long*>(xc + ((size_t)par * CL + lane) * 2 + 1))
-                        : INT_MAX;
-      int po = lane;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, pv, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, p, o);
-        const int o2 = __shfl_xor_sync(0xffffffffu, po, o);
-        if (v2 > pv || (v2 == pv && i2 < p)) {
-          pv = v2;
-          p = i2;
-          po = o2;
-        }
-      }
-      if (lane == 0) {
-        const bool sing = !(pv > 0.0) || p == INT_MAX;
-        sp[0] = sing ? j : p;
-        sp[1] = sing ? -1 : po;
-        if (rank == 0) {
-          t.piv[j] = sing ? j : p;
-          if (sing) atomicExch(status, 1);
-        }
-      }
+    // ---- P2: global pivot row p (ties → lowest row); every warp reduces the CL candidates itself
+    double pv = lane < CL ? ccv[par][lane] : -1.0;
+    int p = lane < CL ? cci[par][lane] : INT_MAX;
+    warp_argmax_redux(pv, p);
+    const bool sing = !(pv > 0.0) || p == INT_MAX;
+    const int po = sing ? -1 : p / rc;  // owner CTA of the pivot row (contiguous row blocks)
+    if (sing) p = j;
+    if (rank == 0 && tid == 0) {
+      t.piv[j] = p;
+      if (sing) atomicExch(status, 1);
     }
-    __syncthreads();
-    const int p = sp[0], po = sp[1];
-    for (int c = tid; c < jb; c += GJR_NT) {
-      orow[c] = __ldcg(reinterpret_cast<const double2*>(xold + (size_t)par * nb + c));
-      prow[c] = po >= 0 ? __ldcg(reinterpret_cast<const double2*>(xrow + ((size_t)par * CL + po) * nb + c))
-                        : orow[c];
-    }
-    __syncthreads();  // B2
+    const cplx* const orow = cold[par];
+    const cplx* const prow = po >= 0 ? crow + ((size_t)par * CL + po) * nb : orow;
     // ---- P3: interchange rows j and p, scale row j, eliminate
     const cplx d = prow[s];
     const double rn = __drcp_rn(d.x * d.x + d.y * d.y);
@@ -701,6 +687,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __rest
       }
     }
   }
+  cl.sync();  // no CTA exits while others may still push into its shared memory
   // ---- write the panel back and Am = Gp − E_J (n × jb, ld n)
 #pragma unroll
   for (int q = 0; q < MC; ++q) {
@@ -794,20 +781,6 @@ __global__ void k_gj_copyback(const GjTask* __restrict__ tasks, const cplx* __re
 // argmax candidates; barrier B1 (cluster barrier if CL > 1); [P2] everybody reduces the
 // candidates (DSMEM) → p, d; the lanes holding row p publish m_pc/d for their columns;
 // CTA barrier B2; [P3] register update.  grid (CL, ntasks), 512 threads.
-
-// Warp argmax of (v, idx) with ties → lowest idx, by three redux.sync steps on the IEEE bit
-// pattern (monotone for v ≥ 0) instead of five shuffle rounds.  Lanes without a candidate pass
-// idx = INT_MAX.  Non-positive v compare as 0 (only reached when every candidate is ≤ 0, where the
-// callers stop or flag); the result v is then 0 (or -1 with idx INT_MAX if nobody had one).
-__device__ __forceinline__ void warp_argmax_redux(double& v, int& idx) {
-  const unsigned long long key = v > 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
-  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-  const unsigned bi = __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)idx : 0xffffffffu);
-  idx = (int)bi;
-  v = idx == INT_MAX ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-}
 
 // Exchange record of one row group's pivot candidate: |x|², row, x.
 struct GjCand {
@@ -2436,8 +2409,15 @@ void launch_gpr(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status
   const int CL = 16;
   FMMLU_CUDA(cudaFuncSetAttribute(k_gj_panel_reg<MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
+  const size_t dyn = 2 * (size_t)CL * nb * sizeof(cplx);
+  static size_t cur = 0;
+  if (dyn > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gj_panel_reg<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    cur = dyn;
+  }
   cfg.gridDim = dim3(CL, ntasks, 1);
   cfg.blockDim = dim3(GJR_NT, 1, 1);
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
