@@ -281,6 +281,7 @@ def main():
 
     # ---- end-to-end leg through the public API with host buffers
     e2e_ms = []
+    e2e_detail = []  # per step: library-reported tree / factor / factor-wait / solve ms
     resid = None
     for _ in range(2):  # untimed warm-up of the host-buffer path (first calls pay one-time setup)
         step_e2e()
@@ -290,6 +291,9 @@ def main():
         t0 = time.perf_counter()
         h2, x = step_e2e()  # returns after the D2H of the solution (the call synchronises)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        s2 = h2.stats()
+        e2e_detail.append([round(s2["t_tree_ms"], 1), round(s2["t_factor_ms"], 1), round(s2["t_sync_wait_ms"], 1),
+                           round(s2["t_solve_ms"], 1)])
     # residual of the last e2e solve with the GPU brute-force matvec
     x = np.asfortranarray(x)
     Ax = h2.matvec(c["k"], x)
@@ -354,6 +358,7 @@ def main():
         "residual": resid,
         "e2e": {"value": job_throughput(n, world, t_e2e), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e, "ms_steps": [round(v, 2) for v in e2e_ms],
+                "lib_tree_factor_wait_solve_ms": e2e_detail,
                 "host_buffers": "pinned",
                 "timing": "host wall clock around tree+factor+solve incl. H2D/D2H, mean of K steps"},
         "gpu_launches": int(st["n_launches"]),

@@ -1639,6 +1639,7 @@ __global__ void __launch_bounds__(GJC_NT) k_gj_coop(cplx* A, cplx* B, int n, cpl
 // ------------------------------------------------------------------ solve sweeps
 constexpr int SV_NT = 256;
 constexpr int SV_Q = 4;  // RHS processed per pass
+constexpr int SV_U = 8;  // factor loads in flight per thread in the solve products
 
 __global__ void __launch_bounds__(SV_NT) k_solve_up(const BoxRec* __restrict__ recs,
                                                     const cplx* __restrict__ fac,
@@ -1813,7 +1814,11 @@ __global__ void __launch_bounds__(SV_NT) k_su_a(const BoxRec* __restrict__ recs,
   }
 }
 
-__global__ void __launch_bounds__(kSolveChunk) k_su_b(const BoxRec* __restrict__ recs,
+// y_{S∪N} += sg · Lp t for one item (kSolveChunk rows of Lp); SB_P threads per row split the
+// r-loop (interleaved batches of SV_U loads) and combine by shuffles: the per-row dot product
+// was HBM-latency-bound with one thread per row.
+constexpr int SB_P = 4;
+__global__ void __launch_bounds__(kSolveChunk * SB_P) k_su_b(const BoxRec* __restrict__ recs,
                                                       const SolveItem* __restrict__ items,
                                                       const cplx* __restrict__ fac, const int* __restrict__ idx,
                                                       cplx* y, int ldy, int nrhs, const cplx* __restrict__ tmp,
@@ -1822,28 +1827,44 @@ __global__ void __launch_bounds__(kSolveChunk) k_su_b(const BoxRec* __restrict__
   const SolveItem it = items[blockIdx.x];
   const BoxRec R = recs[it.rec];
   const int k = R.k, r = R.r, kn = R.k + R.nN;
-  const int f = it.c0 + threadIdx.x;
+  const int part = threadIdx.x & (SB_P - 1);
+  const int f = it.c0 + (threadIdx.x / SB_P);
   cplx* tr = reinterpret_cast<cplx*>(shm);  // r × Q
   const cplx* Lp = fac + R.Lp;
   const cplx* tb = tmp + (size_t)R.tmp * nrhs;
   for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
     const int nq = min(SV_Q, nrhs - q0);
     __syncthreads();
-    for (int e = threadIdx.x; e < r * nq; e += kSolveChunk) {
+    for (int e = threadIdx.x; e < r * nq; e += kSolveChunk * SB_P) {
       int i = e % r, q = e / r;
       tr[i + q * r] = tb[i + (size_t)(q0 + q) * r];
     }
     __syncthreads();
+    cplx acc[SV_Q];
+#pragma unroll
+    for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
     if (f < kn) {
-      cplx acc[SV_Q];
+      for (int i0 = part * SV_U; i0 < r; i0 += SB_P * SV_U) {
+        cplx l[SV_U];
 #pragma unroll
-      for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
-      for (int i = 0; i < r; ++i) {
-        const cplx l = Lp[f + (size_t)i * kn];
+        for (int u = 0; u < SV_U; ++u) l[u] = i0 + u < r ? Lp[f + (size_t)(i0 + u) * kn] : cmk(0.0, 0.0);
 #pragma unroll
-        for (int q = 0; q < SV_Q; ++q)
-          if (q < nq) acc[q] = cfma(l, tr[i + q * r], acc[q]);
+        for (int u = 0; u < SV_U; ++u) {
+          const int i = min(i0 + u, r - 1);
+#pragma unroll
+          for (int q = 0; q < SV_Q; ++q)
+            if (q < nq) acc[q] = cfma(l[u], tr[i + q * r], acc[q]);
+        }
       }
+    }
+#pragma unroll
+    for (int q = 0; q < SV_Q; ++q)
+#pragma unroll
+      for (int o = 1; o < SB_P; o <<= 1) {
+        acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+        acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+      }
+    if (f < kn && part == 0)
       for (int q = 0; q < nq; ++q) {
         if (f < k) {
           cplx* d = y + idx[R.idxS + f] + (size_t)(q0 + q) * ldy;
@@ -1854,7 +1875,6 @@ __global__ void __launch_bounds__(kSolveChunk) k_su_b(const BoxRec* __restrict__
           atomicAdd(&d->y, sg * acc[q].y);
         }
       }
-    }
   }
 }
 
@@ -1867,6 +1887,7 @@ __global__ void __launch_bounds__(SV_NT) k_sd_a(const BoxRec* __restrict__ recs,
   const int k = R.k, r = R.r, kn = R.k + R.nN;
   const int fn = min(kSolveChunk, kn - it.c0);
   cplx* ys = reinterpret_cast<cplx*>(shm);  // kSolveChunk × Q
+  __shared__ cplx sda_red[SV_NT * SV_Q];
   const cplx* Up = fac + R.Up;
   cplx* tb = tmp + (size_t)R.tmp * nrhs;
   for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
@@ -1878,15 +1899,37 @@ __global__ void __launch_bounds__(SV_NT) k_sd_a(const BoxRec* __restrict__ recs,
       ys[f + q * kSolveChunk] = y[gi + (size_t)(q0 + q) * ldy];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < r; i += SV_NT) {
+    // rows over RW threads; for small r the fn columns are split over P = SV_NT / RW parts whose
+    // partial sums meet in shared memory before the one atomic per element
+    const int RW = min(SV_NT, (r + 31) & ~31), P = SV_NT / RW;
+    const int part = threadIdx.x / RW;
+    for (int i = threadIdx.x % RW; i < (P > 1 ? RW : r); i += RW) {
       cplx acc[SV_Q];
 #pragma unroll
       for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
-      for (int f = 0; f < fn; ++f) {
-        const cplx u = Up[i + (size_t)(it.c0 + f) * r];
+      if (i < r && part < P)
+        for (int f0 = part * SV_U; f0 < fn; f0 += P * SV_U) {
+          cplx uu[SV_U];
 #pragma unroll
-        for (int q = 0; q < SV_Q; ++q)
-          if (q < nq) acc[q] = cfma(u, ys[f + q * kSolveChunk], acc[q]);
+          for (int w = 0; w < SV_U; ++w) uu[w] = f0 + w < fn ? Up[i + (size_t)(it.c0 + f0 + w) * r] : cmk(0.0, 0.0);
+#pragma unroll
+          for (int w = 0; w < SV_U; ++w) {
+            const int f = min(f0 + w, fn - 1);
+#pragma unroll
+            for (int q = 0; q < SV_Q; ++q)
+              if (q < nq) acc[q] = cfma(uu[w], ys[f + q * kSolveChunk], acc[q]);
+          }
+        }
+      if (P > 1) {  // uniform per CTA
+        if (part < P)
+#pragma unroll
+          for (int q = 0; q < SV_Q; ++q) sda_red[(part * RW + i) * SV_Q + q] = acc[q];
+        __syncthreads();
+        if (part == 0 && i < r)
+          for (int pp = 1; pp < P; ++pp)
+#pragma unroll
+            for (int q = 0; q < SV_Q; ++q) acc[q] = cadd(acc[q], sda_red[(pp * RW + i) * SV_Q + q]);
+        if (part != 0 || i >= r) continue;
       }
       for (int q = 0; q < nq; ++q) {
         cplx* d = tb + i + (size_t)(q0 + q) * r;
@@ -2001,11 +2044,17 @@ __global__ void __launch_bounds__(128) k_su_dinv(const BoxRec* __restrict__ recs
       cplx acc[SV_Q];
 #pragma unroll
       for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
-      for (int l = l0; l < l1; ++l) {
-        const cplx a = Xi[i + (size_t)l * r];
+      for (int la = l0; la < l1; la += SV_U) {
+        cplx av[SV_U];
 #pragma unroll
-        for (int q = 0; q < SV_Q; ++q)
-          if (q < nq) acc[q] = cfma(a, ts[(l - l0) + q * SV_CH], acc[q]);
+        for (int u = 0; u < SV_U; ++u) av[u] = la + u < l1 ? Xi[i + (size_t)(la + u) * r] : cmk(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < SV_U; ++u) {
+          const int l = min(la + u, l1 - 1);
+#pragma unroll
+          for (int q = 0; q < SV_Q; ++q)
+            if (q < nq) acc[q] = cfma(av[u], ts[(l - l0) + q * SV_CH], acc[q]);
+        }
       }
       const int gi = idx[R.idxR + i];
       for (int q = 0; q < nq; ++q) {
@@ -2050,11 +2099,17 @@ __global__ void __launch_bounds__(128) k_sd_b2(const BoxRec* __restrict__ recs, 
       cplx acc[SV_Q];
 #pragma unroll
       for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
-      for (int i = i0; i < i1; ++i) {
-        const cplx tv = T[l + (size_t)i * k];
+      for (int ia = i0; ia < i1; ia += SV_U) {
+        cplx tv[SV_U];
 #pragma unroll
-        for (int q = 0; q < SV_Q; ++q)
-          if (q < nq) acc[q] = cfma(tv, ys[(i - i0) + q * SV_CH], acc[q]);
+        for (int u = 0; u < SV_U; ++u) tv[u] = ia + u < i1 ? T[l + (size_t)(ia + u) * k] : cmk(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < SV_U; ++u) {
+          const int i = min(ia + u, i1 - 1);
+#pragma unroll
+          for (int q = 0; q < SV_Q; ++q)
+            if (q < nq) acc[q] = cfma(tv[u], ys[(i - i0) + q * SV_CH], acc[q]);
+        }
       }
       const int gs = idx[R.idxS + l];
       for (int q = 0; q < nq; ++q) {
@@ -2815,7 +2870,7 @@ void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, 
                                                                                        nrhs, tmp);
   FMMLU_LAUNCH();
   if (nitems > 0) {
-    k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, -1.0);
+    k_su_b<<<nitems, kSolveChunk * SB_P, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, -1.0);
     FMMLU_LAUNCH();
   }
 }
@@ -2913,7 +2968,7 @@ void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, in
       FMMLU_CUDA(cudaFuncSetAttribute(k_su_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
       cb = sb;
     }
-    k_su_b<<<nitems, kSolveChunk, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, 1.0);
+    k_su_b<<<nitems, kSolveChunk * SB_P, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, 1.0);
     FMMLU_LAUNCH();
   }
   k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp, 1);
