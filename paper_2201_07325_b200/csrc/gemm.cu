@@ -4,6 +4,8 @@
 // Complex product as 4 real DMMAs: Re += ArBr − AiBi, Im += ArBi + AiBr.
 #include "gemm.cuh"
 
+#include <cstdlib>
+
 namespace fmmlu {
 
 namespace {
@@ -240,6 +242,11 @@ __global__ void __launch_bounds__(NT) k_gemm_schur(const GemmProblem* __restrict
                                                    cplx* __restrict__ bsr) {
   gemm_body<1, false>(probs, tiles, alpha, bsr);
 }
+__global__ void __launch_bounds__(NT) k_gemm_schur3(const GemmProblem* __restrict__ probs,
+                                                    const GemmTile* __restrict__ tiles, cplx alpha,
+                                                    cplx* __restrict__ bsr) {
+  gemm_body<1, true>(probs, tiles, alpha, bsr);
+}
 
 }  // namespace
 
@@ -251,10 +258,14 @@ void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntile
   if (!init) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_store, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_schur3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     init = true;
   }
   // grid.x limit is 2^31-1; tiles are enumerated explicitly
-  if (scatter)
+  static const bool schur3 = getenv("FMMLU_SCHUR_3M") && atoi(getenv("FMMLU_SCHUR_3M"));
+  if (scatter && schur3)
+    k_gemm_schur3<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
+  else if (scatter)
     k_gemm_schur<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
   else
     k_gemm_store<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
