@@ -190,7 +190,7 @@ void launch_solve_down(const BoxRec* d_recs, int nrec, const cplx* fac, const in
 // Split solve sweeps for one phase:
 //   up:   [a] y_R' = y_R − Tᵀy_S → tmp, y_R ← X_RR⁻¹ y_R'   [b] y_{S∪N} −= Lp tmp (row chunks)
 //   down: [a] acc = Up y_{S∪N} (column chunks, atomics)    [b] y_R −= acc, y_S −= T y_R
-constexpr int kSolveChunk = 128;
+constexpr int kSolveChunk = 32;
 void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                       const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax);
 void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
