@@ -134,6 +134,15 @@ int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs);
  * Errors: EINVAL (NULL x, nrhs < 1), ESTATE (no factorization), ESINGULAR, ENOMEM, ECUDA. */
 int fmmlu_apply(fmmlu_handle* h, void* x, int nrhs);
 
+/* Azimuthal monostatic sonar cross section of the sound-soft scatterer (§6.3,
+ * L2755-2794): for each φ_a, d = (cos φ_a, sin φ_a, 0), solve A σ = −e^{ik x·d}
+ * with the stored factors (k = the factorization's wavenumber) and return
+ *   R(φ_a) = (−ik/4π) Σ_j w_j (1 − n_j·d) e^{+ik x_j·d} σ_j     (reading R8 of DESIGN.md).
+ * Right-hand sides are generated on the device; ≥ 32 angles run the sweeps as batched DMMA GEMMs.
+ *   phis : nphi azimuths (radians), host or device;  R : nphi complex128 out, host or device
+ * Errors: EINVAL (NULL, nphi < 1), ESTATE (no factorization), ENOMEM, ECUDA. */
+int fmmlu_monostatic_rcs(fmmlu_handle* h, const double* phis, int nphi, void* R);
+
 /* Apply the (unfactored) matrix: y = A x by brute-force O(n²) summation on the
  * GPU (test/measurement infrastructure for residuals; reading C17).
  *   x, y : n×nrhs column-major complex128 (host or device; y may not alias x)

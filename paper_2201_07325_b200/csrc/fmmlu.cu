@@ -333,6 +333,7 @@ struct Phase {  // one (level, colour) elimination phase
   int tmp_rows = 0;  // Σ r over the phase's boxes (solve scratch)
   size_t fac_bytes = 0;
   DBuf ap_xs, ap_recs;  // fmmlu_apply: X_RR blocks (re-inverted X_RR⁻¹) and records pointing at them
+  std::vector<BoxRec> hrecs;  // host copy of recs (multi-RHS GEMM sweeps build their problems from it)
 };
 
 double now_ms() {
@@ -1952,6 +1953,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         ph.recs.alloc(recs.size() * sizeof(BoxRec), st);
         h2d(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), st);
         ph.nrec = (int)recs.size();
+        ph.hrecs = recs;
         {
           std::vector<SolveItem> items;
           for (size_t e = 0; e < recs.size(); ++e)
@@ -2094,6 +2096,151 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   h->factored = true;
 }
 
+// ---- multi-RHS sweeps on the DMMA GEMM (the same operators as the
+// per-box kernels below): y (tree order, W^{½}-scaled, ld ldy) ← Ã⁻¹ y for
+// Q columns.  Per phase the boxes' rows are gathered into dense blocks, the products run as
+// batched GEMMs (C += α op(A) B), and the results are scattered back (atomics on shared N rows).
+constexpr int kGemmSolveMin = 32;  // nrhs from which the GEMM sweeps replace the per-box kernels
+
+void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
+  cudaStream_t st = h->stream;
+  Prof& P = h->prof;
+  std::vector<DBuf> keep;
+  std::vector<GemmProblem> gp;
+  std::vector<GemmTile> gt;
+  const cplx m1 = cmk(-1.0, 0.0), p1 = cmk(1.0, 0.0);
+  size_t wsmax = 1;
+  for (auto& ph : h->phases) {
+    size_t w = 0;
+    for (auto& R : ph.hrecs) w += (size_t)(2 * (R.k + R.nN) + 2 * R.r) * Q;
+    wsmax = std::max(wsmax, w);
+  }
+  DBuf ws;
+  ws.alloc(wsmax * sizeof(cplx), st);
+  cplx* W = ws.as<cplx>();
+  // per phase: gathered blocks (YSN, YR of every box) first, then the accumulators (Z, DSN)
+  // in one contiguous region [z0, tot) that a single memset clears
+  auto layout = [&](const Phase& ph, std::vector<SweepWs>& L, long long& z0) {
+    long long o = 0;
+    L.resize(ph.hrecs.size());
+    for (size_t e = 0; e < ph.hrecs.size(); ++e) {
+      const BoxRec& R = ph.hrecs[e];
+      L[e].ysn = o;
+      o += (long long)(R.k + R.nN) * Q;
+      L[e].yr = o;
+      o += (long long)R.r * Q;
+    }
+    z0 = o;
+    for (size_t e = 0; e < ph.hrecs.size(); ++e) {
+      const BoxRec& R = ph.hrecs[e];
+      L[e].z = o;
+      o += (long long)R.r * Q;
+      L[e].dsn = o;
+      o += (long long)(R.k + R.nN) * Q;
+    }
+    return o;
+  };
+  auto prob = [&](int m, int n, int k, int opA, const cplx* A, int lda, const cplx* B, int ldb, cplx* C, int ldc) {
+    GemmProblem g{};
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.opA = opA;
+    g.opB = kOpN;
+    g.A = A;
+    g.lda = std::max(lda, 1);
+    g.B = B;
+    g.ldb = std::max(ldb, 1);
+    g.C = C;
+    g.ldc = std::max(ldc, 1);
+    add_gemm(gp, gt, g);
+  };
+  const int id = P.begin(FMMLU_K_SOLVE, st);
+  // ---- upward: E (t = y_R − Tᵀ y_S), then Lp t and X_RR⁻¹ t
+  for (auto& ph : h->phases) {
+    if (ph.nrec <= 0) continue;
+    std::vector<SweepWs> L;
+    long long z0 = 0;
+    const long long tot = layout(ph, L, z0);
+    Stage s;
+    const size_t oL = s.add(L);
+    s.upload(st);
+    const SweepWs* dL = s.ptr<SweepWs>(oL);
+    const cplx* F = ph.fac.as<cplx>();
+    FMMLU_CUDA(cudaMemsetAsync(W + z0, 0, (size_t)(tot - z0) * sizeof(cplx), st));
+    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 0, st);
+    for (size_t e = 0; e < L.size(); ++e) {
+      const BoxRec& R = ph.hrecs[e];
+      if (R.k > 0) prob(R.r, Q, R.k, kOpT, F + R.T, R.k, W + L[e].ysn, R.k + R.nN, W + L[e].yr, R.r);
+    }
+    run_gemms(gp, gt, m1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
+    for (size_t e = 0; e < L.size(); ++e) {
+      const BoxRec& R = ph.hrecs[e];
+      const int kn = R.k + R.nN;
+      prob(R.r, Q, R.r, kOpN, F + R.Xi, R.r, W + L[e].yr, R.r, W + L[e].z, R.r);
+      prob(kn, Q, R.r, kOpN, F + R.Lp, kn, W + L[e].yr, R.r, W + L[e].dsn, kn);
+    }
+    run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
+    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 1, st);
+    keep.push_back(std::move(s.dev));
+  }
+  // ---- root: y[B_t] ← X_t⁻¹ y[B_t]
+  DBuf r0;
+  if (h->n0 > 0) {
+    const int n0 = (int)h->n0;
+    r0.alloc(2 * (size_t)n0 * Q * sizeof(cplx), st);
+    cplx* Y0 = r0.as<cplx>();
+    cplx* Z0 = Y0 + (size_t)n0 * Q;
+    launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, Y0, Q, 0, st);
+    FMMLU_CUDA(cudaMemsetAsync(Z0, 0, (size_t)n0 * Q * sizeof(cplx), st));
+    prob(n0, Q, n0, kOpN, h->root.as<cplx>(), n0, Y0, n0, Z0, n0);
+    run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
+    launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, Z0, Q, 1, st);
+  }
+  // ---- downward (reverse order): U (y_R −= Up y_{S∪N}), then F (y_S −= T y_R)
+  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
+    Phase& ph = *it;
+    if (ph.nrec <= 0) continue;
+    std::vector<SweepWs> L;
+    long long z0 = 0;
+    const long long tot = layout(ph, L, z0);
+    Stage s;
+    const size_t oL = s.add(L);
+    s.upload(st);
+    const SweepWs* dL = s.ptr<SweepWs>(oL);
+    const cplx* F = ph.fac.as<cplx>();
+    FMMLU_CUDA(cudaMemsetAsync(W + z0, 0, (size_t)(tot - z0) * sizeof(cplx), st));
+    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 0, st);
+    for (size_t e = 0; e < L.size(); ++e) {
+      const BoxRec& R = ph.hrecs[e];
+      const int kn = R.k + R.nN;
+      prob(R.r, Q, kn, kOpN, F + R.Up, R.r, W + L[e].ysn, kn, W + L[e].yr, R.r);
+    }
+    run_gemms(gp, gt, m1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
+    for (size_t e = 0; e < L.size(); ++e) {
+      const BoxRec& R = ph.hrecs[e];
+      if (R.k > 0) prob(R.k, Q, R.r, kOpN, F + R.T, R.k, W + L[e].yr, R.r, W + L[e].dsn, R.k);
+    }
+    run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
+    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 2, st);
+    keep.push_back(std::move(s.dev));
+  }
+  P.end(id, st);
+  wait_stream(h, st);  // keep (staging, workspace) outlives the launches; resets the staging arenas
+}
+
+// RHS columns per GEMM-sweep pass: bounded so the phase workspace stays ≤ ~2 GB
+int sweep_chunk(const fmmlu_handle* h, int nrhs) {
+  size_t per = 1;
+  for (auto& ph : h->phases) {
+    size_t w = 0;
+    for (auto& R : ph.hrecs) w += (size_t)(2 * (R.k + R.nN) + 2 * R.r);
+    per = std::max(per, w);
+  }
+  const size_t cap = (size_t)2e9 / (per * sizeof(cplx));
+  return (int)std::max<size_t>(kGemmSolveMin, std::min<size_t>({(size_t)nrhs, cap, (size_t)1024}));
+}
+
 void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   cudaStream_t st = h->stream;
   const int n = (int)h->n;
@@ -2110,6 +2257,19 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   Prof& P = h->prof;
   int sid = P.begin(FMMLU_K_SOLVE, st);
   launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
+  if (nrhs >= kGemmSolveMin) {  // many right-hand sides: the sweeps as batched DMMA GEMMs
+    P.end(sid, st);
+    const int qc = sweep_chunk(h, nrhs);
+    for (int q0 = 0; q0 < nrhs; q0 += qc) sweeps_gemm(h, yp + (size_t)q0 * n, n, std::min(qc, nrhs - q0));
+    sid = P.begin(FMMLU_K_SOLVE, st);
+    launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
+    P.end(sid, st);
+    if (!dev)
+      FMMLU_CUDA(cudaMemcpyAsync(rhs, io.p, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    P.resolve();
+    return;
+  }
   size_t scr_rows = 1;
   for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
   DBuf scr;
@@ -2810,6 +2970,81 @@ int fmmlu_apply(fmmlu_handle* h, void* x, int nrhs) {
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
     apply_impl(h, x, nrhs);
+  });
+}
+
+// Monostatic sonar cross section (§6.3, reading R8): for each azimuth φ_a the
+// plane-wave system A σ = −e^{ik x·d_a} is solved with the stored factors and
+// R(φ_a) = (−ik/4π) Σ_j w_j (1 − n_j·d_a) e^{ik x_j·d_a} σ_j.  Everything stays in tree order on the
+// device: the RHS is generated already W^{½}-scaled and R is reduced from y = W^{½}σ directly.
+void rcs_impl(fmmlu_handle* h, const double* phis, int nphi, void* Rout) {
+  cudaStream_t st = h->stream;
+  const int n = (int)h->n;
+  DBuf dphi, dR;
+  const double* ph = phis;
+  if (!is_device_ptr(phis)) {
+    dphi.alloc((size_t)nphi * sizeof(double), st);
+    FMMLU_CUDA(cudaMemcpyAsync(dphi.p, phis, (size_t)nphi * sizeof(double), cudaMemcpyHostToDevice, st));
+    ph = dphi.as<double>();
+  }
+  const bool rdev = is_device_ptr(Rout);
+  cplx* R = reinterpret_cast<cplx*>(Rout);
+  if (!rdev) {
+    dR.alloc((size_t)nphi * sizeof(cplx), st);
+    R = dR.as<cplx>();
+  }
+  FMMLU_CUDA(cudaMemsetAsync(R, 0, (size_t)nphi * sizeof(cplx), st));
+  const int qc = nphi >= kGemmSolveMin ? sweep_chunk(h, nphi) : nphi;
+  DBuf yb;
+  yb.alloc((size_t)n * qc * sizeof(cplx), st);
+  cplx* y = yb.as<cplx>();
+  for (int a0 = 0; a0 < nphi; a0 += qc) {
+    const int q = std::min(qc, nphi - a0);
+    int id = h->prof.begin(FMMLU_K_SOLVE, st);
+    launch_plane_wave(h->g, n, h->k, ph + a0, q, y, n, st);
+    h->prof.end(id, st);
+    if (q >= kGemmSolveMin) {
+      sweeps_gemm(h, y, n, q);
+    } else {  // few angles: the per-box solve kernels (the same path as fmmlu_solve)
+      size_t scr_rows = 1;
+      for (auto& p : h->phases) scr_rows = std::max(scr_rows, (size_t)p.tmp_rows);
+      DBuf scr, tmp;
+      scr.alloc(scr_rows * q * sizeof(cplx), st);
+      id = h->prof.begin(FMMLU_K_SOLVE, st);
+      for (auto& p : h->phases)
+        launch_solve_up2(p.recs.as<BoxRec>(), p.nrec, p.items.as<SolveItem>(), p.nitems, p.fac.as<cplx>(),
+                         p.idx.as<int>(), y, n, q, scr.as<cplx>(), st, p.kmax, p.rmax);
+      if (h->n0 > 0) {
+        tmp.alloc(2 * (size_t)h->n0 * q * sizeof(cplx), st);
+        launch_root_apply(h->root.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), y, n, q, tmp.as<cplx>(), st);
+      }
+      for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
+        FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * q * sizeof(cplx), st));
+        launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems,
+                           it->fac.as<cplx>(), it->idx.as<int>(), y, n, q, scr.as<cplx>(), st, it->rmax, it->kmax);
+      }
+      h->prof.end(id, st);
+      wait_stream(h, st);
+    }
+    id = h->prof.begin(FMMLU_K_SOLVE, st);
+    launch_rcs_reduce(h->g, n, h->k, ph + a0, q, y, n, R + a0, st);
+    h->prof.end(id, st);
+  }
+  if (!rdev) FMMLU_CUDA(cudaMemcpyAsync(Rout, R, (size_t)nphi * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  wait_stream(h, st);
+  h->prof.resolve();
+}
+
+int fmmlu_monostatic_rcs(fmmlu_handle* h, const double* phis, int nphi, void* R) {
+  if (!h) return fail(FMMLU_EINVAL, "NULL handle");
+  if (!phis || !R) return fail(FMMLU_EINVAL, "NULL phis / R");
+  if (nphi < 1) return fail(FMMLU_EINVAL, "nphi must be >= 1");
+  if (!h->factored) return fail(FMMLU_ESTATE, "fmmlu_monostatic_rcs called before a successful fmmlu_factor");
+  return guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    double t0 = now_ms();
+    rcs_impl(h, phis, nphi, R);
+    h->stats.t_solve_ms = now_ms() - t0;
   });
 }
 

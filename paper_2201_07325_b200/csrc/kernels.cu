@@ -2975,6 +2975,129 @@ void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, in
   FMMLU_LAUNCH();
 }
 
+// ---- multi-RHS sweep data movement (gathers / scatters around the batched GEMMs)
+constexpr int MV_QB = 8;  // RHS columns per CTA
+__global__ void __launch_bounds__(256) k_sweep_move(const BoxRec* __restrict__ recs, const SweepWs* __restrict__ wsr,
+                                                   const int* __restrict__ idx, cplx* y, int ldy, int Q,
+                                                   cplx* __restrict__ ws, int mode) {
+  const BoxRec R = recs[blockIdx.x];
+  const SweepWs W = wsr[blockIdx.x];
+  const int k = R.k, r = R.r, kn = R.k + R.nN;
+  const int q0 = blockIdx.y * MV_QB, nq = min(MV_QB, Q - q0);
+  const int rows = kn + r;
+  for (int e = threadIdx.x; e < rows * nq; e += blockDim.x) {
+    const int i = e % rows, q = q0 + e / rows;
+    if (i < kn) {  // S ∪ N rows
+      const int gi = i < k ? idx[R.idxS + i] : idx[R.idxN + i - k];
+      cplx* d = y + gi + (size_t)q * ldy;
+      if (mode == 0) {
+        ws[W.ysn + i + (size_t)q * kn] = *d;
+      } else if (mode == 1) {
+        const cplx v = ws[W.dsn + i + (size_t)q * kn];
+        if (i < k) {
+          *d = csub(*d, v);  // S rows belong to this box alone within the phase
+        } else {
+          atomicAdd(&d->x, -v.x);
+          atomicAdd(&d->y, -v.y);
+        }
+      } else if (i < k) {
+        *d = csub(*d, ws[W.dsn + i + (size_t)q * k]);
+      }
+    } else {  // R rows
+      const int ir = i - kn;
+      cplx* d = y + idx[R.idxR + ir] + (size_t)q * ldy;
+      if (mode == 0) ws[W.yr + ir + (size_t)q * r] = *d;
+      else if (mode == 1) *d = ws[W.z + ir + (size_t)q * r];
+      else *d = ws[W.yr + ir + (size_t)q * r];
+    }
+  }
+}
+
+void launch_sweep_move(const BoxRec* d_recs, const SweepWs* d_ws, int nrec, const int* idx, cplx* y, int ldy,
+                       int Q, cplx* ws, int mode, cudaStream_t st) {
+  if (nrec <= 0 || Q <= 0) return;
+  k_sweep_move<<<dim3(nrec, (Q + MV_QB - 1) / MV_QB), 256, 0, st>>>(d_recs, d_ws, idx, y, ldy, Q, ws, mode);
+  FMMLU_LAUNCH();
+}
+
+__global__ void k_rows_move(const int* __restrict__ rows, int n0, cplx* y, int ldy, cplx* Y0, int Q, int dir) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n0 * Q;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n0), q = (int)(e / n0);
+    cplx* d = y + rows[i] + (size_t)q * ldy;
+    if (dir == 0) Y0[e] = *d;
+    else *d = Y0[e];
+  }
+}
+
+void launch_rows_move(const int* rows, int n0, cplx* y, int ldy, cplx* Y0, int Q, int dir, cudaStream_t st) {
+  if (n0 <= 0 || Q <= 0) return;
+  const long long tot = (long long)n0 * Q;
+  const int blocks = (int)std::min<long long>((tot + 255) / 256, 148 * 16);
+  k_rows_move<<<blocks, 256, 0, st>>>(rows, n0, y, ldy, Y0, Q, dir);
+  FMMLU_LAUNCH();
+}
+
+// ---- plane-wave right-hand sides and the monostatic cross section (§6.3)
+__global__ void k_plane_wave(Geo g, int n, double k, const double* __restrict__ phis, int Q, cplx* y, int ldy) {
+  const int a = blockIdx.y;
+  double s, c;
+  sincos(phis[a], &s, &c);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincos(k * (g.x[i] * c + g.y[i] * s), &sn, &cs);
+    const double w = g.sw[i];
+    y[i + (size_t)a * ldy] = cmk(-cs * w, -sn * w);  // −e^{ik x·d} √w
+  }
+}
+
+void launch_plane_wave(Geo g, int n, double k, const double* phis, int Q, cplx* y, int ldy, cudaStream_t st) {
+  if (n <= 0 || Q <= 0) return;
+  const int bx = std::min((n + 255) / 256, 64);
+  k_plane_wave<<<dim3(bx, Q), 256, 0, st>>>(g, n, k, phis, Q, y, ldy);
+  FMMLU_LAUNCH();
+}
+
+__global__ void __launch_bounds__(256) k_rcs_reduce(Geo g, int n, double k, const double* __restrict__ phis, int Q,
+                                                   const cplx* __restrict__ y, int ldy, cplx* R) {
+  const int a = blockIdx.y;
+  double s, c;
+  sincos(phis[a], &s, &c);
+  cplx acc = cmk(0.0, 0.0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double sn, cs;
+    sincos(k * (g.x[i] * c + g.y[i] * s), &sn, &cs);
+    const double f = g.sw[i] * (1.0 - (g.nx[i] * c + g.ny[i] * s));  // √w (1 − n·d); y = √w σ
+    acc = cfma(cmk(f * cs, f * sn), y[i + (size_t)a * ldy], acc);
+  }
+  acc.x = warp_sum(acc.x);
+  acc.y = warp_sum(acc.y);
+  __shared__ double sx[8], sy[8];
+  if ((threadIdx.x & 31) == 0) {
+    sx[threadIdx.x >> 5] = acc.x;
+    sy[threadIdx.x >> 5] = acc.y;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tx = 0, ty = 0;
+    for (int w = 0; w < 8; ++w) {
+      tx += sx[w];
+      ty += sy[w];
+    }
+    const double c4 = k / (4.0 * 3.14159265358979323846);  // (−ik/4π)(tx + i ty)
+    atomicAdd(&R[a].x, c4 * ty);
+    atomicAdd(&R[a].y, -c4 * tx);
+  }
+}
+
+void launch_rcs_reduce(Geo g, int n, double k, const double* phis, int Q, const cplx* y, int ldy, cplx* R,
+                       cudaStream_t st) {
+  if (n <= 0 || Q <= 0) return;
+  const int bx = std::min((n + 255) / 256, 32);
+  k_rcs_reduce<<<dim3(bx, Q), 256, 0, st>>>(g, n, k, phis, Q, y, ldy, R);
+  FMMLU_LAUNCH();
+}
+
 void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
                        cplx* tmp, cudaStream_t st) {
   if (n0 <= 0) return;

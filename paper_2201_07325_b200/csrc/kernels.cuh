@@ -205,6 +205,25 @@ void launch_apply_d(const BoxRec* d_recsX, int nrec, const cplx* xs, const int* 
                     cplx* tmp, cudaStream_t st, int rmax);
 void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                     const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax);
+// ---- multi-RHS sweeps on DMMA GEMMs: per-box dense blocks gathered from /
+// scattered to the tree-order RHS y (ld ldy) around batched GEMMs.
+struct SweepWs {   // complex offsets into the phase workspace, per box
+  long long ysn;   // (k+nN) × Q: rows [S | N]
+  long long yr;    // r × Q
+  long long z;     // r × Q   (up: X_RR⁻¹ t)
+  long long dsn;   // (k+nN) × Q (up: Lp t; down: T y_R in its first k rows)
+};
+// mode 0: YSN ← y[S∪N], YR ← y[R];  1: up scatter y[R] = Z, y[S∪N] −= DSN;  2: down scatter
+// y[R] = YR, y[S] −= DSN[0:k].  grid (nrec, ceil(Q / qb)).
+void launch_sweep_move(const BoxRec* d_recs, const SweepWs* d_ws, int nrec, const int* idx, cplx* y, int ldy,
+                       int Q, cplx* ws, int mode, cudaStream_t st);
+// y[rows[i], q] ↔ Y0[i + q n0] (dir 0: gather, 1: scatter)
+void launch_rows_move(const int* rows, int n0, cplx* y, int ldy, cplx* Y0, int Q, int dir, cudaStream_t st);
+// y[i + a·ldy] = −e^{ik x_i·d_a} √w_i (tree order, scaled: the solve's input W^{½}b), d_a = (cos φ_a, sin φ_a, 0)
+void launch_plane_wave(Geo g, int n, double k, const double* phis, int Q, cplx* y, int ldy, cudaStream_t st);
+// R[a] += (−ik/4π) Σ_i √w_i (1 − n_i·d_a) e^{ik x_i·d_a} y[i + a·ldy]   (y = W^{½}σ in tree order)
+void launch_rcs_reduce(Geo g, int n, double k, const double* phis, int Q, const cplx* y, int ldy, cplx* R,
+                       cudaStream_t st);
 // y[rows] = Xinv (n0×n0) · y[rows] for the root block
 void launch_root_apply(const cplx* Xinv, int n0, const int* d_rows, cplx* y, int ldy, int nrhs,
                        cplx* tmp, cudaStream_t st);

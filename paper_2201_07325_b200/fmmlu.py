@@ -50,7 +50,7 @@ class Stats(ctypes.Structure):
 
 KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur", "root", "solve", "apply"]
 
-EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_matvec", "fmmlu_destroy",
+EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_monostatic_rcs", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
            "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes")
 
@@ -75,6 +75,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_factor.argtypes = [vp, cd, cd]
     L.fmmlu_solve.argtypes = [vp, vp, ci]
     L.fmmlu_apply.argtypes = [vp, vp, ci]
+    L.fmmlu_monostatic_rcs.argtypes = [vp, vp, ci, vp]
     L.fmmlu_matvec.argtypes = [vp, cd, vp, vp, ci]
     L.fmmlu_destroy.argtypes = [vp]
     L.fmmlu_last_error.restype = ctypes.c_char_p
@@ -150,6 +151,17 @@ class FmmLu:
             assert x.dtype == np.complex128 and (x.ndim == 1 or x.flags.f_contiguous)
         _check(load().fmmlu_apply(self.h, _ptr(x), int(nrhs)))
         return x
+
+    def monostatic_rcs(self, phis, out=None):
+        """R(φ₀) for every azimuth in `phis` (§6.3): plane-wave solves with the stored
+        factors and the backscatter functional, all on the device.  Returns complex128 (nphi,)."""
+        if isinstance(phis, np.ndarray) or not hasattr(phis, "data_ptr"):
+            phis = np.ascontiguousarray(np.asarray(phis, dtype=np.float64))
+        nphi = int(phis.shape[0])
+        if out is None:
+            out = np.empty(nphi, dtype=np.complex128)
+        _check(load().fmmlu_monostatic_rcs(self.h, _ptr(phis), nphi, _ptr(out)))
+        return out
 
     def matvec(self, k: float, x, y=None):
         nrhs = 1 if x.ndim == 1 else int(x.shape[1])

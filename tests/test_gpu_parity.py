@@ -257,3 +257,51 @@ def test_apply_parity(F, case):
     h.solve(w)
     h.apply(w)
     assert dense.rel_diff(w, x) < 1e-10
+
+
+# ---- multi-RHS sweeps on the DMMA GEMM (nrhs ≥ 32) and the monostatic cross section
+#      (§6.3)
+@pytest.mark.parametrize("case", ["ellipsoid3000", "cube1500"])
+def test_many_rhs_gemm_solve_parity(F, case):
+    eps = 1e-6
+    if case == "ellipsoid3000":
+        g, k, leaf = fi.ellipsoid(3000), 2 * math.pi, 32
+    else:
+        g, k, leaf = fi.random_cube(1500, seed=2), 3.0, 16
+    b = fi.gaussian_rhs(g.n, 40, 11)
+    h = F.FmmLu(g.points, g.normals, g.weights, leaf).factor(k, eps)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)                                    # 40 columns: GEMM sweeps
+    x4 = np.asfortranarray(b[:, :4].copy())
+    h.solve(x4)                                   # 4 columns: per-box kernels, same factors
+    assert dense.rel_diff(x[:, :4], x4) < 1e-11
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf)
+    assert dense.rel_diff(x, rss.solve(f, b)) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
+
+
+@pytest.mark.parametrize("nphi", [5, 40])
+def test_monostatic_rcs_parity(F, nphi):
+    from oracle import rcs
+    eps = 1e-6
+    g, k, leaf = fi.ellipsoid(3000), 2 * math.pi, 32
+    phis = np.linspace(0.0, 2 * math.pi, nphi, endpoint=False)
+    h = F.FmmLu(g.points, g.normals, g.weights, leaf).factor(k, eps)
+    R = h.monostatic_rcs(phis)
+    b = rcs.plane_wave_rhs(g.points, k, phis)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf)
+    Ro = rcs.monostatic_rcs(g.points, g.normals, g.weights, k, phis, rss.solve(f, b))
+    Rd = rcs.monostatic_rcs(g.points, g.normals, g.weights, k, phis,
+                            dense.dense_solve(g.points, g.normals, g.weights, k, b))
+    scale = np.max(np.abs(Rd))
+    assert np.max(np.abs(R - Ro)) <= 10 * eps * scale
+    assert np.max(np.abs(R - Rd)) <= 10 * eps * scale
+
+
+def test_monostatic_rcs_sphere_mie(F):
+    from oracle import rcs
+    g, k = fi.fibonacci_sphere(3200), 2.0
+    h = F.FmmLu(g.points, g.normals, g.weights, 64).factor(k, 1e-8)
+    R = h.monostatic_rcs(np.linspace(0.0, 2 * math.pi, 36, endpoint=False))
+    ref = rcs.mie_backscatter_sphere(k)
+    assert np.max(np.abs(R - ref)) / abs(ref) < 0.06   # the O(h) Nyström error of the oracle pin
