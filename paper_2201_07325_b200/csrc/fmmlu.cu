@@ -26,6 +26,8 @@
 #include <cstring>
 #include <string>
 #include <unordered_map>
+#include <condition_variable>
+#include <functional>
 #include <future>
 #include <mutex>
 #include <thread>
@@ -830,6 +832,67 @@ void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mro
 // ancestors), and the block-pair set = all pairs (x, y) with x, y ∈ {B} ∪ N(B) plus (B, q), (q, B),
 // q ∈ Q(B), over the level-ℓ boxes B: exactly the blocks the level can read or modify (and every
 // block modified at level ℓ+1 maps into it, since both owners touch the parent box).
+// Persistent host worker pool for the per-box bookkeeping loops (spawning threads per phase cost
+// more than the loops themselves).  parallel_for(count, fn(lo, hi)) splits [0, count) into chunks
+// run by the workers and the caller; small counts run inline.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed (workers live until process exit)
+    return *p;
+  }
+  template <class F>
+  void parallel_for(int count, int min_par, F&& fn) {
+    const int nw = (int)workers_.size();
+    if (nw == 0 || count < min_par) {
+      fn(0, count);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    const int parts = nw + 1, chunk = (count + parts - 1) / parts;
+    job_ = [&fn, chunk, count](int w) {
+      const int lo = w * chunk, hi = std::min(count, lo + chunk);
+      if (lo < hi) fn(lo, hi);
+    };
+    pending_ = nw;
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    job_(nw);  // the caller takes the last chunk
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int n = std::max(0, std::min<int>(7, (int)std::thread::hardware_concurrency() / 2 - 1));
+    for (int w = 0; w < n; ++w) workers_.emplace_back([this, w] { loop(w); });
+    for (auto& t : workers_) t.detach();
+  }
+  void loop(int w) {
+    unsigned long long seen = 0;
+    for (;;) {
+      std::function<void(int)> job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        job = job_;
+      }
+      job(w);
+      std::lock_guard<std::mutex> lk(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::function<void(int)> job_;
+  int pending_ = 0;
+  unsigned long long gen_ = 0;
+};
+
 void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
   tp.owners.clear();
   for (int b : T.levels[lvl]) tp.owners.push_back(b);
@@ -1456,74 +1519,100 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::vector<CopyTask> cps;
         std::vector<int> maps;
         std::vector<ProxyTask> pts;
-        std::vector<IdTask> ids;
+        std::vector<IdTask> ids(nj);
         std::vector<int> gidx;
-        for (auto& J : jobs) {
-          int row = 0;
-          for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
-            int mo = -1;
-            if (!ident[q]) {
-              mo = (int)maps.size();
-              maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
+        // pass 1: per-box offsets into every array;  pass 2: fill on the host worker pool
+        struct Cnt { int maps, cps, pts, gidx; };
+        std::vector<Cnt> at(nj + 1);
+        {
+          Cnt c{0, 0, 0, 0};
+          for (int j = 0; j < nj; ++j) {
+            at[j] = c;
+            const BoxJob& J = jobs[j];
+            for (int q : J.Q)
+              if (!ident[q]) c.maps += 2 * (int)curpos[q].size();
+            c.cps += 2 * (int)J.Q.size();
+            if (J.proxy) {
+              c.pts += 1;
+              c.gidx += (int)cur.act[J.a].size();
             }
-            CopyTask c{};
-            c.src = cur.off(q, J.a);
-            c.lds = (int)cur.act[q].size();
-            c.dst = J.Moff + row;
-            c.ldd = J.m;
-            c.rows = (int)curpos[q].size();
-            c.cols = J.b;
-            c.trans = 0;
-            c.rmap_off = mo;
-            c.cmap_off = -1;
-            cps.push_back(c);
-            row += c.rows;
           }
-          for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
-            int mo = -1;
-            if (!ident[q]) {
-              mo = (int)maps.size();
-              maps.insert(maps.end(), curpos[q].begin(), curpos[q].end());
-            }
-            CopyTask c{};
-            c.src = cur.off(J.a, q);
-            c.lds = J.b;
-            c.dst = J.Moff + row;
-            c.ldd = J.m;
-            c.rows = (int)curpos[q].size();
-            c.cols = J.b;
-            c.trans = 1;
-            c.rmap_off = mo;
-            c.cmap_off = -1;
-            cps.push_back(c);
-            row += c.rows;
-          }
-          if (J.proxy) {
-            ProxyTask p{};
-            p.dst = J.Moff;
-            p.ld = J.m;
-            p.row0 = row;
-            p.b = J.b;
-            p.idx_off = (int)gidx.size();
-            gidx.insert(gidx.end(), cur.act[J.a].begin(), cur.act[J.a].end());
-            p.ngamma = ngamma;
-            double c3[3];
-            T.box_centre(cur.owners()[J.a], c3);
-            p.cx = c3[0];
-            p.cy = c3[1];
-            p.cz = c3[2];
-            p.rho = rho;
-            p.sg = sg;
-            pts.push_back(p);
-          }
-          IdTask it{};
-          it.Mp = nullptr;
-          it.m = J.m;
-          it.b = J.b;
-          it.out_off = J.permoff;
-          it.T = J.Toff;
-          ids.push_back(it);
+          at[nj] = c;
+          maps.resize(c.maps);
+          cps.resize(c.cps);
+          pts.resize(c.pts);
+          gidx.resize(c.gidx);
         }
+        HostPool::get().parallel_for(nj, 8, [&](int j0, int j1) {
+          for (int j = j0; j < j1; ++j) {
+            BoxJob& J = jobs[j];
+            int mi = at[j].maps, ci = at[j].cps;
+            int row = 0;
+            for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
+              int mo = -1;
+              if (!ident[q]) {
+                mo = mi;
+                for (int v : curpos[q]) maps[mi++] = v;
+              }
+              CopyTask c{};
+              c.src = cur.off(q, J.a);
+              c.lds = (int)cur.act[q].size();
+              c.dst = J.Moff + row;
+              c.ldd = J.m;
+              c.rows = (int)curpos[q].size();
+              c.cols = J.b;
+              c.trans = 0;
+              c.rmap_off = mo;
+              c.cmap_off = -1;
+              cps[ci++] = c;
+              row += c.rows;
+            }
+            for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
+              int mo = -1;
+              if (!ident[q]) {
+                mo = mi;
+                for (int v : curpos[q]) maps[mi++] = v;
+              }
+              CopyTask c{};
+              c.src = cur.off(J.a, q);
+              c.lds = J.b;
+              c.dst = J.Moff + row;
+              c.ldd = J.m;
+              c.rows = (int)curpos[q].size();
+              c.cols = J.b;
+              c.trans = 1;
+              c.rmap_off = mo;
+              c.cmap_off = -1;
+              cps[ci++] = c;
+              row += c.rows;
+            }
+            if (J.proxy) {
+              ProxyTask p{};
+              p.dst = J.Moff;
+              p.ld = J.m;
+              p.row0 = row;
+              p.b = J.b;
+              p.idx_off = at[j].gidx;
+              std::copy(cur.act[J.a].begin(), cur.act[J.a].end(), gidx.begin() + at[j].gidx);
+              p.ngamma = ngamma;
+              double c3[3];
+              T.box_centre(cur.owners()[J.a], c3);
+              p.cx = c3[0];
+              p.cy = c3[1];
+              p.cz = c3[2];
+              p.rho = rho;
+              p.sg = sg;
+              pts[at[j].pts] = p;
+            }
+            IdTask it{};
+            it.Mp = nullptr;
+            it.m = J.m;
+            it.b = J.b;
+            it.out_off = J.permoff;
+            it.T = J.Toff;
+            ids[j] = it;
+          }
+        });
         if (maps.empty()) maps.push_back(0);
         if (gidx.empty()) gidx.push_back(0);
         Stage s;
@@ -1678,115 +1767,152 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::vector<long long> gjoff;
         std::vector<int> gjdim;
         struct FrameRef { int slot_off, tab_off, bld_off, ns; };
-        std::vector<FrameRef> frames;
-        for (size_t e = 0; e < el.size(); ++e) {
-          BoxJob& J = jobs[el[e]];
-          BoxRec& R = recs[e];
-          const int kk = J.k, r = R.r, b = J.b;
-          const int* pm = &hperm[J.permoff];
-          // local order [R | S] of B's columns
-          int rf = (int)maps.size();
-          for (int i = kk; i < b; ++i) maps.push_back(pm[i]);
-          for (int i = 0; i < kk; ++i) maps.push_back(pm[i]);
-          const std::vector<int>& aB = cur.act[J.a];
-          for (int i = 0; i < kk; ++i) hidx[R.idxS + i] = aB[pm[i]];
-          for (int i = 0; i < r; ++i) hidx[R.idxR + i] = aB[pm[kk + i]];
-          // W_B = [A_BB | A_BN] (rows/cols of B in [R|S] order), W_N = A_NB
-          CopyTask c{};
-          c.src = cur.off(J.a, J.a);
-          c.lds = b;
-          c.dst = WBoff[el[e]];
-          c.ldd = b;
-          c.rows = b;
-          c.cols = b;
-          c.trans = 0;
-          c.rmap_off = rf;
-          c.cmap_off = rf;
-          cps.push_back(c);
-          int noff = 0;
-          for (int o : J.N) {
-            int mo = -1;
-            if (!ident[o]) {
-              mo = (int)maps.size();
-              maps.insert(maps.end(), curpos[o].begin(), curpos[o].end());
+        std::vector<FrameRef> frames(el.size());
+        // pass 1 (serial, O(|N|) per box): where each box's entries go in every array
+        struct Counts { int maps, cps, cpsT, fs, tab, bld; };
+        std::vector<Counts> at(el.size() + 1);
+        {
+          Counts c{0, 0, 0, 0, 0, 0};
+          for (size_t e = 0; e < el.size(); ++e) {
+            at[e] = c;
+            const BoxJob& J = jobs[el[e]];
+            const int ns = 1 + (int)J.N.size();
+            int nm = J.b, nf = J.k;
+            for (int o : J.N) {
+              if (!ident[o]) nm += (int)curpos[o].size();
+              nf += (int)curpos[o].size();
             }
-            int no_ = (int)curpos[o].size();
-            for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
-            CopyTask a{};
-            a.src = cur.off(J.a, o);
-            a.lds = b;
-            a.dst = WBoff[el[e]] + (long long)(b + noff) * b;
-            a.ldd = b;
-            a.rows = b;
-            a.cols = no_;
-            a.trans = 0;
-            a.rmap_off = rf;
-            a.cmap_off = mo;
-            cps.push_back(a);
-            CopyTask d{};
-            d.src = cur.off(o, J.a);
-            d.lds = (int)cur.act[o].size();
-            d.dst = WNoff[el[e]] + noff;
-            d.ldd = std::max(J.nN, 1);
-            d.rows = no_;
-            d.cols = b;
-            d.trans = 0;
-            d.rmap_off = mo;
-            d.cmap_off = rf;
-            cps.push_back(d);
-            noff += no_;
+            c.maps += nm;
+            c.cps += 1 + 2 * (int)J.N.size();
+            c.cpsT += (J.k > 0 && J.b - J.k > 0) ? 1 : 0;
+            c.fs += nf;
+            c.tab += ns * ns;
+            c.bld += ns;
           }
-          // T → factor store (k × r)
-          if (kk > 0 && r > 0) {
-            CopyTask t{};
-            t.src = J.Toff;
-            t.lds = kk;
-            t.dst = R.T;
-            t.ldd = kk;
-            t.rows = kk;
-            t.cols = r;
-            t.trans = 0;
-            t.rmap_off = -1;
-            t.cmap_off = -1;
-            cpsT.push_back(t);
-          }
-          // X_RR → Xinv slot (after E/F)
-          CopyTask x{};
-          x.src = WBoff[el[e]];
-          x.lds = b;
-          x.dst = R.Xi;
-          x.ldd = r;
-          x.rows = r;
-          x.cols = r;
-          x.trans = 0;
-          x.rmap_off = -1;
-          x.cmap_off = -1;
-          cpsX.push_back(x);
-          gjoff.push_back(R.Xi);
-          gjdim.push_back(r);
-          // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
-          FrameRef fr;
-          fr.slot_off = (int)fslot.size();
-          fr.ns = 1 + (int)J.N.size();
-          for (int i = 0; i < kk; ++i) {
-            fslot.push_back(0);
-            fpos.push_back(pm[i]);
-          }
-          for (size_t i = 0; i < J.N.size(); ++i)
-            for (int p : curpos[J.N[i]]) {
-              fslot.push_back(1 + (int)i);
-              fpos.push_back(p);
-            }
-          fr.tab_off = (int)ftab.size();
-          std::vector<int> own;
-          own.push_back(J.a);
-          for (int o : J.N) own.push_back(o);
-          for (int s1 = 0; s1 < fr.ns; ++s1)
-            for (int s2 = 0; s2 < fr.ns; ++s2) ftab.push_back(cur.off(own[s1], own[s2]));
-          fr.bld_off = (int)fbld.size();
-          for (int s1 = 0; s1 < fr.ns; ++s1) fbld.push_back((int)cur.act[own[s1]].size());
-          frames.push_back(fr);
+          at[el.size()] = c;
+          maps.resize(c.maps);
+          cps.resize(c.cps);
+          cpsT.resize(c.cpsT);
+          cpsX.resize(el.size());
+          gjoff.resize(el.size());
+          gjdim.resize(el.size());
+          fslot.resize(c.fs);
+          fpos.resize(c.fs);
+          ftab.resize(c.tab);
+          fbld.resize(c.bld);
         }
+        // pass 2 (host worker pool): fill
+        HostPool::get().parallel_for((int)el.size(), 8, [&](int e0, int e1) {
+          for (int e = e0; e < e1; ++e) {
+            BoxJob& J = jobs[el[e]];
+            BoxRec& R = recs[e];
+            const int kk = J.k, r = R.r, b = J.b;
+            const int* pm = &hperm[J.permoff];
+            int mi = at[e].maps, ci = at[e].cps, fi = at[e].fs;
+            // local order [R | S] of B's columns
+            const int rf = mi;
+            for (int i = kk; i < b; ++i) maps[mi++] = pm[i];
+            for (int i = 0; i < kk; ++i) maps[mi++] = pm[i];
+            const std::vector<int>& aB = cur.act[J.a];
+            for (int i = 0; i < kk; ++i) hidx[R.idxS + i] = aB[pm[i]];
+            for (int i = 0; i < r; ++i) hidx[R.idxR + i] = aB[pm[kk + i]];
+            // W_B = [A_BB | A_BN] (rows/cols of B in [R|S] order), W_N = A_NB
+            CopyTask c{};
+            c.src = cur.off(J.a, J.a);
+            c.lds = b;
+            c.dst = WBoff[el[e]];
+            c.ldd = b;
+            c.rows = b;
+            c.cols = b;
+            c.trans = 0;
+            c.rmap_off = rf;
+            c.cmap_off = rf;
+            cps[ci++] = c;
+            int noff = 0;
+            for (int o : J.N) {
+              int mo = -1;
+              if (!ident[o]) {
+                mo = mi;
+                for (int v : curpos[o]) maps[mi++] = v;
+              }
+              const int no_ = (int)curpos[o].size();
+              for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
+              CopyTask a{};
+              a.src = cur.off(J.a, o);
+              a.lds = b;
+              a.dst = WBoff[el[e]] + (long long)(b + noff) * b;
+              a.ldd = b;
+              a.rows = b;
+              a.cols = no_;
+              a.trans = 0;
+              a.rmap_off = rf;
+              a.cmap_off = mo;
+              cps[ci++] = a;
+              CopyTask d{};
+              d.src = cur.off(o, J.a);
+              d.lds = (int)cur.act[o].size();
+              d.dst = WNoff[el[e]] + noff;
+              d.ldd = std::max(J.nN, 1);
+              d.rows = no_;
+              d.cols = b;
+              d.trans = 0;
+              d.rmap_off = mo;
+              d.cmap_off = rf;
+              cps[ci++] = d;
+              noff += no_;
+            }
+            // T → factor store (k × r)
+            if (kk > 0 && r > 0) {
+              CopyTask t{};
+              t.src = J.Toff;
+              t.lds = kk;
+              t.dst = R.T;
+              t.ldd = kk;
+              t.rows = kk;
+              t.cols = r;
+              t.trans = 0;
+              t.rmap_off = -1;
+              t.cmap_off = -1;
+              cpsT[at[e].cpsT] = t;
+            }
+            // X_RR → Xinv slot (after E/F)
+            CopyTask x{};
+            x.src = WBoff[el[e]];
+            x.lds = b;
+            x.dst = R.Xi;
+            x.ldd = r;
+            x.rows = r;
+            x.cols = r;
+            x.trans = 0;
+            x.rmap_off = -1;
+            x.cmap_off = -1;
+            cpsX[e] = x;
+            gjoff[e] = R.Xi;
+            gjdim[e] = r;
+            // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
+            FrameRef fr;
+            fr.slot_off = fi;
+            fr.ns = 1 + (int)J.N.size();
+            for (int i = 0; i < kk; ++i) {
+              fslot[fi] = 0;
+              fpos[fi++] = pm[i];
+            }
+            for (size_t i = 0; i < J.N.size(); ++i)
+              for (int p : curpos[J.N[i]]) {
+                fslot[fi] = 1 + (int)i;
+                fpos[fi++] = p;
+              }
+            fr.tab_off = at[e].tab;
+            int ti = at[e].tab;
+            for (int s1 = 0; s1 < fr.ns; ++s1) {
+              const int o1 = s1 == 0 ? J.a : J.N[s1 - 1];
+              for (int s2 = 0; s2 < fr.ns; ++s2) ftab[ti++] = cur.off(o1, s2 == 0 ? J.a : J.N[s2 - 1]);
+            }
+            fr.bld_off = at[e].bld;
+            for (int s1 = 0; s1 < fr.ns; ++s1) fbld[at[e].bld + s1] = (int)cur.act[s1 == 0 ? J.a : J.N[s1 - 1]].size();
+            frames[e] = fr;
+          }
+        });
         if (maps.empty()) maps.push_back(0);
         if (fslot.empty()) { fslot.push_back(0); fpos.push_back(0); }
         if (ftab.empty()) ftab.push_back(-1);
