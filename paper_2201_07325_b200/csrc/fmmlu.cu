@@ -29,6 +29,7 @@
 #include <condition_variable>
 #include <functional>
 #include <future>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -457,7 +458,17 @@ namespace {
 // cudaStreamSynchronize with the blocked time accounted (stats: host vs device-wait split)
 void wait_stream(fmmlu_handle* h, cudaStream_t st) {
   double t0 = now_ms();
-  FMMLU_CUDA(cudaStreamSynchronize(st));
+  // spin on the stream instead of a blocking synchronize: the factorization waits here once per
+  // phase for the ranks, and the blocking wake-up added tens of µs of device idle each time
+  static const bool spin = !(getenv("FMMLU_BLOCKING_SYNC") && atoi(getenv("FMMLU_BLOCKING_SYNC")));
+  if (spin) {
+    cudaError_t e;
+    while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) {
+    }
+    FMMLU_CUDA(e);
+  } else {
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+  }
   h->stats.t_sync_wait_ms += now_ms() - t0;
   tl_pin.reset();
   auto it = tl_devarena.find(st);
@@ -1320,6 +1331,17 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     tmark = t;
     wmark = w;
   };
+  // GPU timeline markers (FMMLU_TRACE): events recorded in stream order at the stage boundaries; the
+  // device time between consecutive markers is attributed to the (from, to) pair, so e.g. the gap
+  // id_end → el_begin is device idle time while the host prepared the elimination.
+  std::vector<std::pair<int, cudaEvent_t>> gmarks;
+  auto gmark = [&](int lbl) {
+    if (!trace) return;
+    cudaEvent_t e;
+    FMMLU_CUDA(cudaEventCreate(&e));
+    FMMLU_CUDA(cudaEventRecord(e, st));
+    gmarks.push_back({lbl, e});
+  };
   // per-level topologies depend only on the tree: build the not-yet-cached ones concurrently
   if ((int)h->topo.size() < L) h->topo.resize(L);
   if (h->topo_ready.size() < (size_t)L) h->topo_ready.resize(L, 0);
@@ -1497,6 +1519,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       const int nj = (int)jobs.size();
 
       lap(2);
+      gmark(0);
       // ------------------------------------------------ ID stage
       long long wsM = 0, wsT = 0;
       int permtot = 0, bmax = 0;
@@ -1651,6 +1674,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         }
         lap(13);
       }
+      gmark(1);
       std::vector<int> hk(nj), hperm(permtot);
       int* pin = h->d2h(nj + permtot);
       FMMLU_CUDA(cudaMemcpyAsync(pin, kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1670,9 +1694,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       } else {
         h->prof.resolve();
       }
-      keep.clear();
+      // the ID temporaries and M are freed at the end of the phase, after the elimination is
+      // launched: the device is idle from here until the first elimination kernel
+      std::vector<DBuf> idkeep;
+      idkeep.swap(keep);
       track(h, -(long long)M.bytes);
-      M.release();
 
       lap(3);
       // ------------------------------------------------ elimination stage
@@ -1926,6 +1952,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
                o_rec = s.add(recs);
         s.upload(st);
+        gmark(2);
         int gid = h->prof.begin(FMMLU_K_GATHER, st);
         launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), Wp, st);
         launch_copy(s.ptr<CopyTask>(o_ct), (int)cpsT.size(), s.ptr<int>(o_m), Tb.as<cplx>(), F, st);
@@ -2090,6 +2117,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             h2d(ph.items.p, items.data(), items.size() * sizeof(SolveItem), st);
         }
         // no sync here: the next phase's ID preparation overlaps with this elimination on the GPU
+        gmark(3);
         keep.push_back(std::move(s.dev));
         track(h, -(long long)W.bytes);
         W.release();
@@ -2143,6 +2171,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8], tr[9], tr[10], tr[11], tr[12], tr[13],
             tr[14], tr[15], tr[16], tr[17], tr[18], tr[19], tr[20], tr[21], tr[4], S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root
+  gmark(4);
   double tr0 = now_ms();
   std::vector<int> Bt;
   if (prev.level >= 0) {
@@ -2216,6 +2245,26 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   wait_stream(h, st);
   h->prof.resolve();
   S.t_root_ms = now_ms() - tr0;
+  if (trace && !gmarks.empty()) {
+    gmark(5);
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    static const char* nm[6] = {"id_begin", "id_end", "el_begin", "el_end", "root_begin", "end"};
+    std::map<std::pair<int, int>, std::pair<double, int>> agg;
+    for (size_t i = 0; i + 1 < gmarks.size(); ++i) {
+      float ms = 0.f;
+      FMMLU_CUDA(cudaEventElapsedTime(&ms, gmarks[i].second, gmarks[i + 1].second));
+      auto& a = agg[{gmarks[i].first, gmarks[i + 1].first}];
+      a.first += ms;
+      a.second += 1;
+    }
+    float tot = 0.f;
+    FMMLU_CUDA(cudaEventElapsedTime(&tot, gmarks.front().second, gmarks.back().second));
+    fprintf(stderr, "[fmmlu] device timeline (%.2f ms from the first ID to the end):", tot);
+    for (auto& kv : agg)
+      fprintf(stderr, " %s->%s %.2f ms (%d)", nm[kv.first.first], nm[kv.first.second], kv.second.first, kv.second.second);
+    fprintf(stderr, "\n");
+    for (auto& m : gmarks) cudaEventDestroy(m.second);
+  }
   if (hstatus) throw Error(FMMLU_ESINGULAR, "exactly singular pivot block (X_RR or root)");
   h->k = k;
   h->eps = eps;
