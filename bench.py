@@ -264,6 +264,7 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
         for _ in range(args.steps):
+            h.close()  # the previous step's handle is released outside the timed region
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -290,7 +291,10 @@ def main():
     resid = None
     for _ in range(2):  # untimed warm-up of the host-buffer path (first calls pay one-time setup)
         step_e2e()
+    h2 = None
     for _ in range(args.steps):
+        if h2 is not None:
+            h2.close()  # the previous step's handle is released outside the timed region
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()

@@ -34,6 +34,8 @@
 #include <thread>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/fmmlu.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
@@ -3055,40 +3057,73 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     h->n = n;
-    std::vector<double> P(3 * n), N(3 * n), W(n);
-    auto fetch = [&](const double* src, double* dst, size_t cnt) {
-      if (is_device_ptr(src))
-        FMMLU_CUDA(cudaMemcpy(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToHost));
-      else
-        std::memcpy(dst, src, cnt * sizeof(double));
+    cudaStream_t st = h->stream;
+    // ---- device front end (reading C14/R1): the inputs stay on the device;
+    // checks, bounding box, quantisation, Morton keys, the key sort and the tree-order geometry run
+    // there, and only (perm, sorted q) come back for the box-level bookkeeping on the host
+    DBuf dP, dN, dW;
+    const double* P = points;
+    const double* N = normals;
+    const double* W = weights;
+    auto upload = [&](const double* src, size_t cnt, DBuf& b) -> const double* {
+      if (is_device_ptr(src)) return src;
+      b.alloc(cnt * sizeof(double), st);
+      FMMLU_CUDA(cudaMemcpyAsync(b.p, src, cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+      return b.as<double>();
     };
-    fetch(points, P.data(), 3 * n);
-    fetch(normals, N.data(), 3 * n);
-    fetch(weights, W.data(), n);
-    for (int64_t i = 0; i < n; ++i) {
-      if (!(W[i] > 0.0) || !std::isfinite(W[i])) throw Error(FMMLU_EINVAL, "weights must be finite and > 0");
-      double nn = std::sqrt(N[3 * i] * N[3 * i] + N[3 * i + 1] * N[3 * i + 1] + N[3 * i + 2] * N[3 * i + 2]);
-      if (!(std::fabs(nn - 1.0) <= 1e-10)) throw Error(FMMLU_EINVAL, "normals must be unit vectors");
-      for (int a = 0; a < 3; ++a)
-        if (!std::isfinite(P[3 * i + a])) throw Error(FMMLU_EINVAL, "points must be finite");
-    }
-    h->tree.build(P.data(), n, leaf_max);
-    // geometry in tree order, SoA
-    std::vector<double> G(7 * (size_t)n);
-    for (int64_t i = 0; i < n; ++i) {
-      int64_t p = h->tree.perm[i];
-      for (int a = 0; a < 3; ++a) {
-        G[a * n + i] = P[3 * p + a];
-        G[(3 + a) * n + i] = N[3 * p + a];
+    P = upload(points, 3 * (size_t)n, dP);
+    N = upload(normals, 3 * (size_t)n, dN);
+    W = upload(weights, (size_t)n, dW);
+    const int nb = tree_scan_blocks(n);
+    DBuf part;
+    part.alloc((size_t)6 * nb * sizeof(double) + sizeof(int) * 4, st);
+    int* dflag = reinterpret_cast<int*>(part.as<double>() + 6 * nb);
+    FMMLU_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), st));
+    launch_tree_scan(P, N, W, n, part.as<double>(), dflag, st);
+    std::vector<double> hp(6 * (size_t)nb + 2);
+    FMMLU_CUDA(cudaMemcpyAsync(hp.data(), part.p, (size_t)6 * nb * sizeof(double) + sizeof(int), cudaMemcpyDeviceToHost,
+                               st));
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    int hflag = 0;
+    std::memcpy(&hflag, hp.data() + 6 * nb, sizeof(int));
+    if (hflag & 1) throw Error(FMMLU_EINVAL, "weights must be finite and > 0");
+    if (hflag & 2) throw Error(FMMLU_EINVAL, "normals must be unit vectors");
+    if (hflag & 4) throw Error(FMMLU_EINVAL, "points must be finite");
+    double mn[3], mx[3], lo[3], side;
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = hp[a];
+      mx[a] = hp[3 + a];
+      for (int b = 1; b < nb; ++b) {
+        mn[a] = std::min(mn[a], hp[6 * b + a]);
+        mx[a] = std::max(mx[a], hp[6 * b + 3 + a]);
       }
-      G[6 * n + i] = std::sqrt(W[p]);
     }
-    h->geo.alloc(G.size() * sizeof(double), h->stream);
-    FMMLU_CUDA(cudaMemcpyAsync(h->geo.p, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    h->perm.alloc(n * sizeof(long long), h->stream);
-    FMMLU_CUDA(cudaMemcpyAsync(h->perm.p, h->tree.perm.data(), n * sizeof(long long), cudaMemcpyHostToDevice,
-                               h->stream));
-    FMMLU_CUDA(cudaStreamSynchronize(h->stream));
+    Tree::root_cube(mn, mx, lo, side);
+    DBuf keys, idx, qb;
+    keys.alloc(2 * (size_t)n * sizeof(unsigned long long), st);
+    idx.alloc(2 * (size_t)n * sizeof(int), st);
+    qb.alloc(6 * (size_t)n * sizeof(int), st);  // q (input order) | q (tree order)
+    unsigned long long* k_in = keys.as<unsigned long long>();
+    unsigned long long* k_out = k_in + n;
+    int* i_in = idx.as<int>();
+    int* i_out = i_in + n;
+    int* q_in = qb.as<int>();
+    int* q_out = q_in + 3 * n;
+    launch_tree_keys(P, n, lo, side, k_in, i_in, q_in, st);
+    size_t tmpb = 0;
+    FMMLU_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmpb, k_in, k_out, i_in, i_out, (int)n, 0, 3 * kDepth, st));
+    DBuf tmp;
+    tmp.alloc(std::max<size_t>(tmpb, 16), st);
+    // stable LSD radix sort of (key, index): ties stay in index order, as the host's stable order
+    FMMLU_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmpb, k_in, k_out, i_in, i_out, (int)n, 0, 3 * kDepth, st));
+    h->geo.alloc(7 * (size_t)n * sizeof(double), st);
+    h->perm.alloc(n * sizeof(long long), st);
+    launch_tree_gather(P, N, W, n, i_out, q_in, h->geo.as<double>(), h->perm.as<long long>(), q_out, st);
+    std::vector<int> hperm(n), hq(3 * (size_t)n);
+    FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), i_out, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMMLU_CUDA(cudaMemcpyAsync(hq.data(), q_out, 3 * (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    FMMLU_CUDA(cudaStreamSynchronize(st));
+    h->tree.build_sorted(hq.data(), hperm.data(), lo, side, n, leaf_max);
     double* gp = h->geo.as<double>();
     h->g = Geo{gp, gp + n, gp + 2 * n, gp + 3 * n, gp + 4 * n, gp + 5 * n, gp + 6 * n};
     track(h, h->geo.bytes + h->perm.bytes);

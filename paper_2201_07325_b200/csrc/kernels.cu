@@ -2975,6 +2975,111 @@ void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, in
   FMMLU_LAUNCH();
 }
 
+// ---- device tree front end (readings C14/R1): input checks and bounding box,
+// quantisation q = ⌊((x − lo)/side)·2²⁰⌋ in the same IEEE operation sequence as the host/oracle
+// (explicit _rn intrinsics: no contraction), 60-bit Morton keys, and the tree-order geometry.
+__device__ __forceinline__ unsigned long long tree_spread3(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_tree_scan(const double* __restrict__ P, const double* __restrict__ N,
+                                                  const double* __restrict__ W, long long n, double* part, int* bad) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int flags = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double w = W[i];
+    if (!(w > 0.0) || !isfinite(w)) flags |= 1;
+    const double nx = N[3 * i], ny = N[3 * i + 1], nz = N[3 * i + 2];
+    const double nn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny)), __dmul_rn(nz, nz)));
+    if (!(fabs(__dsub_rn(nn, 1.0)) <= 1e-10)) flags |= 2;
+    for (int a = 0; a < 3; ++a) {
+      const double v = P[3 * i + a];
+      if (!isfinite(v)) flags |= 4;
+      mn[a] = fmin(mn[a], v);
+      mx[a] = fmax(mx[a], v);
+    }
+  }
+  __shared__ double smn[3][256], smx[3][256];
+  for (int a = 0; a < 3; ++a) {
+    smn[a][threadIdx.x] = mn[a];
+    smx[a][threadIdx.x] = mx[a];
+  }
+  if (flags) atomicOr(bad, flags);
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int a = 0; a < 3; ++a) {
+        smn[a][threadIdx.x] = fmin(smn[a][threadIdx.x], smn[a][threadIdx.x + st]);
+        smx[a][threadIdx.x] = fmax(smx[a][threadIdx.x], smx[a][threadIdx.x + st]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int a = 0; a < 3; ++a) {
+      part[6 * blockIdx.x + a] = smn[a][0];
+      part[6 * blockIdx.x + 3 + a] = smx[a][0];
+    }
+}
+
+__global__ void k_tree_keys(const double* __restrict__ P, long long n, double lx, double ly, double lz, double side,
+                            unsigned long long* key, int* idx, int* q) {
+  const double scale = 1048576.0;  // 2^20 (kDepth)
+  const double lo[3] = {lx, ly, lz};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long c[3];
+    for (int a = 0; a < 3; ++a) {
+      double t = floor(__dmul_rn(__ddiv_rn(__dsub_rn(P[3 * i + a], lo[a]), side), scale));
+      if (t < 0) t = 0;
+      if (t > scale - 1) t = scale - 1;
+      q[3 * i + a] = (int)t;
+      c[a] = (unsigned long long)t;
+    }
+    key[i] = (tree_spread3(c[0]) << 2) | (tree_spread3(c[1]) << 1) | tree_spread3(c[2]);
+    idx[i] = (int)i;
+  }
+}
+
+__global__ void k_tree_gather(const double* __restrict__ P, const double* __restrict__ N, const double* __restrict__ W,
+                              long long n, const int* __restrict__ perm, const int* __restrict__ q, double* G,
+                              long long* perm64, int* qs) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long p = perm[i];
+    for (int a = 0; a < 3; ++a) {
+      G[a * n + i] = P[3 * p + a];
+      G[(3 + a) * n + i] = N[3 * p + a];
+      qs[3 * i + a] = q[3 * p + a];
+    }
+    G[6 * n + i] = sqrt(W[p]);
+    perm64[i] = p;
+  }
+}
+
+int tree_scan_blocks(long long n) { return (int)std::max(1LL, std::min<long long>((n + 255) / 256, 592)); }
+
+void launch_tree_scan(const double* P, const double* N, const double* W, long long n, double* part, int* bad,
+                      cudaStream_t st) {
+  k_tree_scan<<<tree_scan_blocks(n), 256, 0, st>>>(P, N, W, n, part, bad);
+  FMMLU_LAUNCH();
+}
+
+void launch_tree_keys(const double* P, long long n, const double lo[3], double side, unsigned long long* key, int* idx,
+                      int* q, cudaStream_t st) {
+  k_tree_keys<<<tree_scan_blocks(n), 256, 0, st>>>(P, n, lo[0], lo[1], lo[2], side, key, idx, q);
+  FMMLU_LAUNCH();
+}
+
+void launch_tree_gather(const double* P, const double* N, const double* W, long long n, const int* perm, const int* q,
+                        double* G, long long* perm64, int* qs, cudaStream_t st) {
+  k_tree_gather<<<tree_scan_blocks(n), 256, 0, st>>>(P, N, W, n, perm, q, G, perm64, qs);
+  FMMLU_LAUNCH();
+}
+
 // ---- multi-RHS sweep data movement (gathers / scatters around the batched GEMMs)
 constexpr int MV_QB = 8;  // RHS columns per CTA
 __global__ void __launch_bounds__(256) k_sweep_move(const BoxRec* __restrict__ recs, const SweepWs* __restrict__ wsr,

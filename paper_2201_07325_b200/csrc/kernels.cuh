@@ -205,6 +205,15 @@ void launch_apply_d(const BoxRec* d_recsX, int nrec, const cplx* xs, const int* 
                     cplx* tmp, cudaStream_t st, int rmax);
 void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                     const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax);
+// ---- device tree front end: checks + bounding box (per-block partials: 6 doubles per block),
+// quantisation + Morton keys, tree-order geometry (SoA x,y,z,nx,ny,nz,√w) and sorted q
+int tree_scan_blocks(long long n);
+void launch_tree_scan(const double* P, const double* N, const double* W, long long n, double* part, int* bad,
+                      cudaStream_t st);
+void launch_tree_keys(const double* P, long long n, const double lo[3], double side, unsigned long long* key, int* idx,
+                      int* q, cudaStream_t st);
+void launch_tree_gather(const double* P, const double* N, const double* W, long long n, const int* perm, const int* q,
+                        double* G, long long* perm64, int* qs, cudaStream_t st);
 // ---- multi-RHS sweeps on DMMA GEMMs: per-box dense blocks gathered from /
 // scattered to the tree-order RHS y (ld ldy) around batched GEMMs.
 struct SweepWs {   // complex offsets into the phase workspace, per box

@@ -14,14 +14,23 @@
 
 namespace fmmlu {
 
+namespace {
+// spread the low 21 bits of v to every third bit (bit b -> bit 3b)
+inline uint64_t spread3(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+}  // namespace
+
 uint64_t morton_code(uint64_t x, uint64_t y, uint64_t z, int bits) {
-  uint64_t key = 0;
-  for (int b = 0; b < bits; ++b) {
-    key |= ((x >> b) & 1ull) << (3 * b + 2);
-    key |= ((y >> b) & 1ull) << (3 * b + 1);
-    key |= ((z >> b) & 1ull) << (3 * b);
-  }
-  return key;
+  // interleave the low `bits` bits: x → bit 3b+2, y → 3b+1, z → 3b
+  const uint64_t m = bits >= 21 ? ~0ull : ((1ull << bits) - 1);
+  return (spread3(x & m) << 2) | (spread3(y & m) << 1) | spread3(z & m);
 }
 
 int Tree::add_box(int level, const int c[3], int s, int e, int parent) {
@@ -107,6 +116,14 @@ void Tree::balance() {
   }
 }
 
+void Tree::root_cube(const double mn[3], const double mx[3], double lo_out[3], double& side_out) {
+  double ext = 0.0;
+  for (int a = 0; a < 3; ++a) ext = std::max(ext, mx[a] - mn[a]);
+  side_out = ext * (1.0 + 1e-12);
+  if (!(side_out > 0.0)) side_out = 1.0;
+  for (int a = 0; a < 3; ++a) lo_out[a] = 0.5 * (mn[a] + mx[a]) - 0.5 * side_out;
+}
+
 void Tree::build(const double* pts, int64_t n_, int leaf_max_) {
   n = n_;
   leaf_max = leaf_max_;
@@ -120,11 +137,7 @@ void Tree::build(const double* pts, int64_t n_, int leaf_max_) {
       mn[a] = std::min(mn[a], v);
       mx[a] = std::max(mx[a], v);
     }
-  double ext = 0.0;
-  for (int a = 0; a < 3; ++a) ext = std::max(ext, mx[a] - mn[a]);
-  side = ext * (1.0 + 1e-12);
-  if (!(side > 0.0)) side = 1.0;
-  for (int a = 0; a < 3; ++a) lo[a] = 0.5 * (mn[a] + mx[a]) - 0.5 * side;
+  root_cube(mn, mx, lo, side);
   const double scale = double(1u << kDepth);
   std::vector<int32_t> q0(3 * (size_t)n);
   std::vector<uint64_t> key(n);
@@ -137,14 +150,30 @@ void Tree::build(const double* pts, int64_t n_, int leaf_max_) {
     }
     key[i] = morton_code(q0[3 * i], q0[3 * i + 1], q0[3 * i + 2], kDepth);
   }
+  // stable order by key = sort of (key, index) pairs
+  std::vector<std::pair<uint64_t, int64_t>> ki(n);
+  for (int64_t i = 0; i < n; ++i) ki[i] = {key[i], i};
+  std::sort(ki.begin(), ki.end());
   perm.resize(n);
-  std::iota(perm.begin(), perm.end(), 0);
-  std::stable_sort(perm.begin(), perm.end(),
-                   [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  for (int64_t i = 0; i < n; ++i) perm[i] = ki[i].second;
   q.resize(3 * (size_t)n);
   for (int64_t i = 0; i < n; ++i)
     for (int a = 0; a < 3; ++a) q[3 * i + a] = q0[3 * perm[i] + a];
+  build_boxes();
+}
 
+void Tree::build_sorted(const int32_t* q_sorted, const int32_t* perm_, const double lo_[3], double side_, int64_t n_,
+                        int leaf_max_) {
+  n = n_;
+  leaf_max = leaf_max_;
+  for (int a = 0; a < 3; ++a) lo[a] = lo_[a];
+  side = side_;
+  perm.assign(perm_, perm_ + n);
+  q.assign(q_sorted, q_sorted + 3 * (size_t)n);
+  build_boxes();
+}
+
+void Tree::build_boxes() {
   boxes.clear();
   by_code.clear();
   int c0[3] = {0, 0, 0};

@@ -36,6 +36,12 @@ struct Tree {
 
   // Build (throws fmmlu::Error(EDEPTH) on duplicate points).
   void build(const double* pts, int64_t n, int leaf_max);
+  // Back end only: points already quantised and sorted by Morton key on the device (tree order):
+  // q_sorted 3n ints, perm n (tree position -> caller index), root cube (lo, side).
+  void build_sorted(const int32_t* q_sorted, const int32_t* perm, const double lo_[3], double side_, int64_t n,
+                    int leaf_max);
+  // Root cube rule (reading C14): centred at the bounding-box centre, side = max extent × (1 + 1e-12).
+  static void root_cube(const double mn[3], const double mx[3], double lo_out[3], double& side_out);
 
   double box_side(int level) const { return side / double(1u << level); }
   void box_centre(int b, double out[3]) const;
@@ -56,6 +62,7 @@ struct Tree {
   int add_box(int level, const int c[3], int s, int e, int parent);
   void split(int b);
   void balance();
+  void build_boxes();
 };
 
 uint64_t morton_code(uint64_t x, uint64_t y, uint64_t z, int bits);
