@@ -1821,7 +1821,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           maps.resize(c.maps);
           cps.resize(c.cps);
           cpsT.resize(c.cpsT);
-          cpsX.resize(el.size());
+          cpsX.resize(3 * el.size());
           gjoff.resize(el.size());
           gjdim.resize(el.size());
           fslot.resize(c.fs);
@@ -1914,7 +1914,29 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             x.trans = 0;
             x.rmap_off = -1;
             x.cmap_off = -1;
-            cpsX[e] = x;
+            cpsX[3 * e] = x;
+            // X_{(S∪N)R} → the Lp slot: the factor keeps X_{(S∪N)R} itself (the solve applies it to
+            // X_RR⁻¹ t, and the Schur update is X_{(S∪N)R}·Up), so no Lp = X_{(S∪N)R} X_RR⁻¹ product
+            CopyTask xs{};
+            xs.src = WBoff[el[e]] + r;  // rows S of W_B (after E/F), columns R
+            xs.lds = b;
+            xs.dst = R.Lp;
+            xs.ldd = kk + J.nN;
+            xs.rows = kk;
+            xs.cols = r;
+            xs.rmap_off = -1;
+            xs.cmap_off = -1;
+            cpsX[3 * e + 1] = xs;
+            CopyTask xn{};
+            xn.src = WNoff[el[e]];  // W_N = X_{N,B}: columns R
+            xn.lds = std::max(J.nN, 1);
+            xn.dst = R.Lp + kk;
+            xn.ldd = kk + J.nN;
+            xn.rows = J.nN;
+            xn.cols = r;
+            xn.rmap_off = -1;
+            xn.cmap_off = -1;
+            cpsX[3 * e + 2] = xn;
             gjoff[e] = R.Xi;
             gjdim[e] = r;
             // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
@@ -2024,7 +2046,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           for (size_t e = 0; e < gjdim.size(); ++e) mats.push_back({F + gjoff[e], gjdim[e]});
           gj_blocked(h, mats, status.as<int>(), keep, FMMLU_K_INV);
         }
-        // Up = X_RR⁻¹ X_{R(S∪N)} ;  Lp = X_{(S∪N)R} X_RR⁻¹
+        // Up = X_RR⁻¹ X_{R(S∪N)}
         for (size_t e = 0; e < el.size(); ++e) {
           BoxJob& J = jobs[el[e]];
           BoxRec& R = recs[e];
@@ -2042,39 +2064,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.C = F + R.Up;
           P.ldc = R.r;
           add_gemm(gp, gt, P);
-          if (R.k > 0) {
-            GemmProblem Q{};
-            Q.m = R.k;
-            Q.n = R.r;
-            Q.k = R.r;
-            Q.opA = kOpN;
-            Q.opB = kOpN;
-            Q.A = Wp + WBoff[el[e]] + R.r;
-            Q.lda = J.b;
-            Q.B = F + R.Xi;
-            Q.ldb = R.r;
-            Q.C = F + R.Lp;
-            Q.ldc = kn;
-            add_gemm(gp, gt, Q);
-          }
-          if (J.nN > 0) {
-            GemmProblem Q{};
-            Q.m = J.nN;
-            Q.n = R.r;
-            Q.k = R.r;
-            Q.opA = kOpN;
-            Q.opB = kOpN;
-            Q.A = Wp + WNoff[el[e]];
-            Q.lda = J.nN;
-            Q.B = F + R.Xi;
-            Q.ldb = R.r;
-            Q.C = F + R.Lp + R.k;
-            Q.ldc = kn;
-            add_gemm(gp, gt, Q);
-          }
         }
         run_gemms(gp, gt, p1, 0, nullptr, st, keep, h->prof, FMMLU_K_PANEL);
-        // Schur complement: Δ_{(S∪N)²} −= Lp · X_{R(S∪N)}, scattered into the level BSR
+        // Schur complement: Δ_{(S∪N)²} −= X_{(S∪N)R} · Up  (= X_{(S∪N)R} X_RR⁻¹ X_{R(S∪N)}), scattered
+        // into the level BSR
         for (size_t e = 0; e < el.size(); ++e) {
           BoxJob& J = jobs[el[e]];
           BoxRec& R = recs[e];
@@ -2086,10 +2079,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.k = R.r;
           P.opA = kOpN;
           P.opB = kOpN;
-          P.A = F + R.Lp;
+          P.A = F + R.Lp;  // X_{(S∪N)R}
           P.lda = kn;
-          P.B = Wp + WBoff[el[e]] + (long long)R.r * J.b;
-          P.ldb = J.b;
+          P.B = F + R.Up;
+          P.ldb = R.r;
           P.C = nullptr;
           P.ldc = 0;
           P.row0 = 0;
@@ -2351,11 +2344,15 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
       if (R.k > 0) prob(R.r, Q, R.k, kOpT, F + R.T, R.k, W + L[e].ysn, R.k + R.nN, W + L[e].yr, R.r);
     }
     run_gemms(gp, gt, m1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
-    for (size_t e = 0; e < L.size(); ++e) {
+    for (size_t e = 0; e < L.size(); ++e) {  // z = X_RR⁻¹ t
+      const BoxRec& R = ph.hrecs[e];
+      prob(R.r, Q, R.r, kOpN, F + R.Xi, R.r, W + L[e].yr, R.r, W + L[e].z, R.r);
+    }
+    run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
+    for (size_t e = 0; e < L.size(); ++e) {  // X_{(S∪N)R} z  (= Lp t)
       const BoxRec& R = ph.hrecs[e];
       const int kn = R.k + R.nN;
-      prob(R.r, Q, R.r, kOpN, F + R.Xi, R.r, W + L[e].yr, R.r, W + L[e].z, R.r);
-      prob(kn, Q, R.r, kOpN, F + R.Lp, kn, W + L[e].yr, R.r, W + L[e].dsn, kn);
+      prob(kn, Q, R.r, kOpN, F + R.Lp, kn, W + L[e].z, R.r, W + L[e].dsn, kn);
     }
     run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
     launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 1, st);

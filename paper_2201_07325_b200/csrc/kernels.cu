@@ -1641,180 +1641,10 @@ constexpr int SV_NT = 256;
 constexpr int SV_Q = 4;  // RHS processed per pass
 constexpr int SV_U = 8;  // factor loads in flight per thread in the solve products
 
-__global__ void __launch_bounds__(SV_NT) k_solve_up(const BoxRec* __restrict__ recs,
-                                                    const cplx* __restrict__ fac,
-                                                    const int* __restrict__ idx, cplx* y, int ldy,
-                                                    int nrhs) {
-  extern __shared__ double shm[];
-  const BoxRec R = recs[blockIdx.x];
-  const int k = R.k, r = R.r, nN = R.nN, kn = k + nN;
-  cplx* yS = reinterpret_cast<cplx*>(shm);  // k × Q
-  cplx* yR = yS + k * SV_Q;                // r × Q
-  cplx* tmp = yR + r * SV_Q;               // r × Q
-  const int* S = idx + R.idxS;
-  const int* Ri = idx + R.idxR;
-  const int* N = idx + R.idxN;
-  const cplx* T = fac + R.T;
-  const cplx* Xi = fac + R.Xi;
-  const cplx* Lp = fac + R.Lp;
-  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
-    const int nq = min(SV_Q, nrhs - q0);
-    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {
-      int i = e % k, q = e / k;
-      yS[i + q * k] = y[S[i] + (size_t)(q0 + q) * ldy];
-    }
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      yR[i + q * r] = y[Ri[i] + (size_t)(q0 + q) * ldy];
-    }
-    __syncthreads();
-    // E: y_R −= Tᵀ y_S
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      cplx v = yR[i + q * r];
-      for (int l = 0; l < k; ++l) v = cfms(T[l + (size_t)i * k], yS[l + q * k], v);
-      tmp[i + q * r] = v;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) yR[e] = tmp[e];
-    __syncthreads();
-    // L: y_{S∪N} −= Lp y_R  (N rows shared with other boxes of the phase → atomics)
-    for (int f = threadIdx.x; f < kn; f += SV_NT) {
-      cplx acc[SV_Q];
-#pragma unroll
-      for (int q = 0; q < SV_Q; ++q) acc[q] = cmk(0.0, 0.0);
-      for (int i = 0; i < r; ++i) {
-        const cplx l = Lp[f + (size_t)i * kn];
-#pragma unroll
-        for (int q = 0; q < SV_Q; ++q)
-          if (q < nq) acc[q] = cfma(l, yR[i + q * r], acc[q]);
-      }
-      for (int q = 0; q < nq; ++q) {
-        if (f < k) {
-          yS[f + q * k] = csub(yS[f + q * k], acc[q]);
-        } else {
-          cplx* d = y + N[f - k] + (size_t)(q0 + q) * ldy;
-          atomicAdd(&d->x, -acc[q].x);
-          atomicAdd(&d->y, -acc[q].y);
-        }
-      }
-    }
-    // D⁻¹ on R: y_R ← X_RR⁻¹ y_R
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      cplx v = cmk(0.0, 0.0);
-      for (int l = 0; l < r; ++l) v = cfma(Xi[i + (size_t)l * r], yR[l + q * r], v);
-      tmp[i + q * r] = v;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {
-      int i = e % k, q = e / k;
-      y[S[i] + (size_t)(q0 + q) * ldy] = yS[i + q * k];
-    }
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      y[Ri[i] + (size_t)(q0 + q) * ldy] = tmp[i + q * r];
-    }
-    __syncthreads();
-  }
-}
-
 constexpr int SV_FCH = 1024;  // S∪N entries staged per chunk in the downward sweep
-__global__ void __launch_bounds__(SV_NT) k_solve_down(const BoxRec* __restrict__ recs,
-                                                      const cplx* __restrict__ fac,
-                                                      const int* __restrict__ idx, cplx* y,
-                                                      int ldy, int nrhs) {
-  extern __shared__ double shm[];
-  const BoxRec R = recs[blockIdx.x];
-  const int k = R.k, r = R.r, nN = R.nN, kn = k + nN;
-  cplx* ySN = reinterpret_cast<cplx*>(shm);  // SV_FCH × Q
-  cplx* yR = ySN + SV_FCH * SV_Q;            // r × Q
-  const int* S = idx + R.idxS;
-  const int* Ri = idx + R.idxR;
-  const int* N = idx + R.idxN;
-  const cplx* T = fac + R.T;
-  const cplx* Up = fac + R.Up;
-  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
-    const int nq = min(SV_Q, nrhs - q0);
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      yR[i + q * r] = y[Ri[i] + (size_t)(q0 + q) * ldy];
-    }
-    // U: y_R −= Up y_{S∪N}, S∪N staged in chunks
-    for (int f0 = 0; f0 < kn; f0 += SV_FCH) {
-      const int fn = min(SV_FCH, kn - f0);
-      __syncthreads();
-      for (int e = threadIdx.x; e < fn * nq; e += SV_NT) {
-        int f = e % fn, q = e / fn;
-        int gi = (f0 + f) < k ? S[f0 + f] : N[f0 + f - k];
-        ySN[f + q * SV_FCH] = y[gi + (size_t)(q0 + q) * ldy];
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-        int i = e % r, q = e / r;
-        cplx v = yR[i + q * r];
-        for (int f = 0; f < fn; ++f) v = cfms(Up[i + (size_t)(f0 + f) * r], ySN[f + q * SV_FCH], v);
-        yR[i + q * r] = v;
-      }
-    }
-    __syncthreads();
-    // F: y_S −= T y_R
-    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {
-      int l = e % k, q = e / k;
-      cplx v = y[S[l] + (size_t)(q0 + q) * ldy];
-      for (int i = 0; i < r; ++i) v = cfms(T[l + (size_t)i * k], yR[i + q * r], v);
-      y[S[l] + (size_t)(q0 + q) * ldy] = v;
-    }
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      y[Ri[i] + (size_t)(q0 + q) * ldy] = yR[i + q * r];
-    }
-    __syncthreads();
-  }
-}
-
 // ---- split solve kernels (more CTAs per box; the factor store is streamed once)
-__global__ void __launch_bounds__(SV_NT) k_su_a(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
-                                                const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
-                                                cplx* __restrict__ tmp) {
-  extern __shared__ double shm[];
-  const BoxRec R = recs[blockIdx.x];
-  const int k = R.k, r = R.r;
-  cplx* yS = reinterpret_cast<cplx*>(shm);  // k × Q
-  cplx* yR = yS + k * SV_Q;                // r × Q
-  const int* S = idx + R.idxS;
-  const int* Ri = idx + R.idxR;
-  const cplx* T = fac + R.T;
-  const cplx* Xi = fac + R.Xi;
-  cplx* tb = tmp + (size_t)R.tmp * nrhs;
-  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
-    const int nq = min(SV_Q, nrhs - q0);
-    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {
-      int i = e % k, q = e / k;
-      yS[i + q * k] = y[S[i] + (size_t)(q0 + q) * ldy];
-    }
-    __syncthreads();
-    // E: y_R' = y_R − Tᵀ y_S
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      cplx v = y[Ri[i] + (size_t)(q0 + q) * ldy];
-      for (int l = 0; l < k; ++l) v = cfms(T[l + (size_t)i * k], yS[l + q * k], v);
-      yR[i + q * r] = v;
-      tb[i + (size_t)(q0 + q) * r] = v;
-    }
-    __syncthreads();
-    // D⁻¹: y_R ← X_RR⁻¹ y_R'
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      cplx v = cmk(0.0, 0.0);
-      for (int l = 0; l < r; ++l) v = cfma(Xi[i + (size_t)l * r], yR[l + q * r], v);
-      y[Ri[i] + (size_t)(q0 + q) * ldy] = v;
-    }
-    __syncthreads();
-  }
-}
-
-// y_{S∪N} += sg · Lp t for one item (kSolveChunk rows of Lp); SB_P threads per row split the
+// y_{S∪N} += sg · X_{(S∪N)R} z for one item (kSolveChunk rows; z = X_RR⁻¹ t = y_R after the D⁻¹
+// kernel, so the product equals Lp t of PAPER.md L920-924); SB_P threads per row split the
 // r-loop (interleaved batches of SV_U loads) and combine by shuffles: the per-row dot product
 // was HBM-latency-bound with one thread per row.
 constexpr int SB_P = 4;
@@ -1831,13 +1661,13 @@ __global__ void __launch_bounds__(kSolveChunk * SB_P) k_su_b(const BoxRec* __res
   const int f = it.c0 + (threadIdx.x / SB_P);
   cplx* tr = reinterpret_cast<cplx*>(shm);  // r × Q
   const cplx* Lp = fac + R.Lp;
-  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  (void)tmp;
   for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
     const int nq = min(SV_Q, nrhs - q0);
     __syncthreads();
     for (int e = threadIdx.x; e < r * nq; e += kSolveChunk * SB_P) {
       int i = e % r, q = e / r;
-      tr[i + q * r] = tb[i + (size_t)(q0 + q) * r];
+      tr[i + q * r] = y[idx[R.idxR + i] + (size_t)(q0 + q) * ldy];  // z = X_RR⁻¹ t (after k_su_dinv)
     }
     __syncthreads();
     cplx acc[SV_Q];
@@ -1937,38 +1767,6 @@ __global__ void __launch_bounds__(SV_NT) k_sd_a(const BoxRec* __restrict__ recs,
         atomicAdd(&d->y, acc[q].y);
       }
     }
-  }
-}
-
-__global__ void __launch_bounds__(SV_NT) k_sd_b(const BoxRec* __restrict__ recs, const cplx* __restrict__ fac,
-                                                const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
-                                                const cplx* __restrict__ tmp) {
-  extern __shared__ double shm[];
-  const BoxRec R = recs[blockIdx.x];
-  const int k = R.k, r = R.r;
-  cplx* yR = reinterpret_cast<cplx*>(shm);  // r × Q
-  const int* S = idx + R.idxS;
-  const int* Ri = idx + R.idxR;
-  const cplx* T = fac + R.T;
-  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
-  for (int q0 = 0; q0 < nrhs; q0 += SV_Q) {
-    const int nq = min(SV_Q, nrhs - q0);
-    for (int e = threadIdx.x; e < r * nq; e += SV_NT) {
-      int i = e % r, q = e / r;
-      cplx* d = y + Ri[i] + (size_t)(q0 + q) * ldy;
-      const cplx v = csub(*d, tb[i + (size_t)(q0 + q) * r]);  // U: y_R −= Up y_{S∪N}
-      *d = v;
-      yR[i + q * r] = v;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < k * nq; e += SV_NT) {  // F: y_S −= T y_R
-      int l = e % k, q = e / k;
-      cplx* d = y + S[l] + (size_t)(q0 + q) * ldy;
-      cplx v = *d;
-      for (int i = 0; i < r; ++i) v = cfms(T[l + (size_t)i * k], yR[i + q * r], v);
-      *d = v;
-    }
-    __syncthreads();
   }
 }
 
@@ -2822,48 +2620,16 @@ void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaSt
   FMMLU_CUDA(cudaMemcpyAsync(A, B, (size_t)n * n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
 }
 
-void launch_solve_up(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
-                     int ldy, int nrhs, cudaStream_t st, int kmax, int rmax) {
-  if (nrec <= 0) return;
-  size_t smem = (size_t)(kmax + 2 * rmax) * SV_Q * sizeof(cplx) + 16;
-  static size_t cur = 0;
-  if (smem > 48 * 1024 && smem > cur) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_solve_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cur = smem;
-  }
-  k_solve_up<<<nrec, SV_NT, smem, st>>>(d_recs, fac, idx, y, ldy, nrhs);
-  FMMLU_LAUNCH();
-}
-
-void launch_solve_down(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
-                       int ldy, int nrhs, cudaStream_t st, int rmax) {
-  if (nrec <= 0) return;
-  size_t smem = (size_t)(SV_FCH + rmax) * SV_Q * sizeof(cplx) + 16;
-  static size_t cur = 0;
-  if (smem > 48 * 1024 && smem > cur) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_solve_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cur = smem;
-  }
-  k_solve_down<<<nrec, SV_NT, smem, st>>>(d_recs, fac, idx, y, ldy, nrhs);
-  FMMLU_LAUNCH();
-}
-
-
 void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                       const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax) {
   if (nrec <= 0) return;
-  size_t sa = (size_t)(kmax + rmax) * SV_Q * sizeof(cplx) + 16;
+  (void)kmax;
   size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
-  static size_t ca = 0, cb = 0;
-  if (sa > 48 * 1024 && sa > ca) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_su_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa));
-    ca = sa;
-  }
+  static size_t cb = 0;
   if (sb > 48 * 1024 && sb > cb) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_su_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
     cb = sb;
   }
-  (void)sa;
   k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp, 0);
   FMMLU_LAUNCH();
   k_su_dinv<<<dim3(nrec, (rmax + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
@@ -2880,17 +2646,10 @@ void launch_solve_down2(const BoxRec* d_recs, int nrec, const SolveItem* d_items
                         int kmax_down) {
   if (nrec <= 0) return;
   size_t sa = (size_t)kSolveChunk * SV_Q * sizeof(cplx) + 16;
-  size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
-  static size_t cb = 0;
-  if (sb > 48 * 1024 && sb > cb) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_sd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-    cb = sb;
-  }
   if (nitems > 0) {
     k_sd_a<<<nitems, SV_NT, sa, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp);
     FMMLU_LAUNCH();
   }
-  (void)sb;
   k_sd_b1<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp, -1.0);
   FMMLU_LAUNCH();
   k_sd_b2<<<dim3(nrec, (kmax_down + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
@@ -2956,10 +2715,25 @@ void launch_apply_d(const BoxRec* d_recsX, int nrec, const cplx* xs, const int* 
 }
 
 // V_j = P E⁻¹ L⁻¹: y_{S∪N} += Lp y_R, then y_R += Tᵀ y_S
+__global__ void k_ap_put(const BoxRec* __restrict__ recs, const int* __restrict__ idx, cplx* y, int ldy, int nrhs,
+                         const cplx* __restrict__ tmp) {
+  const BoxRec R = recs[blockIdx.x];
+  const cplx* tb = tmp + (size_t)R.tmp * nrhs;
+  for (int e = threadIdx.x; e < R.r * nrhs; e += blockDim.x) {
+    const int i = e % R.r, q = e / R.r;
+    y[idx[R.idxR + i] + (size_t)q * ldy] = tb[i + (size_t)q * R.r];
+  }
+}
+
 void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                     const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int rmax) {
   if (nrec <= 0) return;
-  k_ap_gather<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp, 0);
+  // L⁻¹: y_{S∪N} += Lp y_R = X_{(S∪N)R} (X_RR⁻¹ y_R): y_R is parked in tmp, replaced by X_RR⁻¹ y_R
+  // for the product, and restored afterwards
+  k_ap_gather<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp, 1);
+  FMMLU_LAUNCH();
+  k_su_dinv<<<dim3(nrec, (rmax + 127) / 128, (rmax + SV_CH - 1) / SV_CH), 128, 0, st>>>(d_recs, fac, idx, y, ldy,
+                                                                                       nrhs, tmp);
   FMMLU_LAUNCH();
   if (nitems > 0) {
     const size_t sb = (size_t)rmax * SV_Q * sizeof(cplx) + 16;
@@ -2971,6 +2745,8 @@ void launch_apply_v(const BoxRec* d_recs, int nrec, const SolveItem* d_items, in
     k_su_b<<<nitems, kSolveChunk * SB_P, sb, st>>>(d_recs, d_items, fac, idx, y, ldy, nrhs, tmp, 1.0);
     FMMLU_LAUNCH();
   }
+  k_ap_put<<<nrec, 256, 0, st>>>(d_recs, idx, y, ldy, nrhs, tmp);
+  FMMLU_LAUNCH();
   k_su_e<<<dim3(nrec, (rmax + 7) / 8), 256, 0, st>>>(d_recs, fac, idx, y, ldy, nrhs, tmp, 1);
   FMMLU_LAUNCH();
 }

@@ -76,7 +76,7 @@ struct IdTask {
 
 // Elimination record of one box (offsets in the factor arena, complex units, and index arena).
 struct BoxRec {
-  long long T, Xi, Up, Lp;  // T: k×r, Xinv: r×r, Up: r×(k+nN), Lp: (k+nN)×r
+  long long T, Xi, Up, Lp;  // T: k×r, Xinv: r×r, Up = X_RR⁻¹X_{R(S∪N)}: r×(k+nN), Lp slot holds X_{(S∪N)R}: (k+nN)×r
   int k, r, nN;
   int idxS, idxR, idxN;     // offsets into the index arena (global tree-order indices)
   int tmp;                  // offset (in units of r·nrhs rows) of the box's solve scratch
@@ -182,13 +182,8 @@ void launch_pchol_big_finish(const PcholBig* d_tasks, int ntasks, int* perm_out,
                              int bmax);
 // cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
 void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
-// solve sweeps for one (level, colour) phase
-void launch_solve_up(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
-                     int ldy, int nrhs, cudaStream_t st, int kmax, int rmax);
-void launch_solve_down(const BoxRec* d_recs, int nrec, const cplx* fac, const int* idx, cplx* y,
-                       int ldy, int nrhs, cudaStream_t st, int rmax);
 // Split solve sweeps for one phase:
-//   up:   [a] y_R' = y_R − Tᵀy_S → tmp, y_R ← X_RR⁻¹ y_R'   [b] y_{S∪N} −= Lp tmp (row chunks)
+//   up:   [a] t = y_R − Tᵀy_S → tmp, y_R ← X_RR⁻¹ t   [b] y_{S∪N} −= X_{(S∪N)R} y_R (= Lp t; row chunks)
 //   down: [a] acc = Up y_{S∪N} (column chunks, atomics)    [b] y_R −= acc, y_S −= T y_R
 constexpr int kSolveChunk = 32;
 void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
