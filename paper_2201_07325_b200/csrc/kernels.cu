@@ -278,8 +278,12 @@ constexpr int QR_NT = 512;
 
 // T = R11⁻¹ R12, warp per column, back substitution.
 // grid (ntasks, ceil(bmax / 16)), 16 warps: one redundant column per warp, x staged in shared memory.
+// T = R11⁻¹ R12 by back substitution, one warp per column of T (16 per CTA).  R11's columns are
+// staged in shared memory W at a time (one CTA barrier per chunk), so the per-pivot dependent chain
+// reads shared memory instead of L2.  smem: x 16·kk | 1/R_ll kk | chunk W·kk (complex).
 __global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks, const int* __restrict__ kv,
-                                                const cplx* __restrict__ ws, cplx* __restrict__ tarena) {
+                                                const cplx* __restrict__ ws, cplx* __restrict__ tarena, int W,
+                                                int bmax) {
   extern __shared__ double shm[];
   const IdTask t = tasks[blockIdx.x];
   const int kk = kv[blockIdx.x];
@@ -289,21 +293,33 @@ __global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.y * 16 + warp;
   if (blockIdx.y * 16 >= r) return;  // uniform per block
-  cplx* rd = reinterpret_cast<cplx*>(shm) + (size_t)16 * kk;  // 1 / R_ll (shared by the block's warps)
+  cplx* rd = reinterpret_cast<cplx*>(shm) + (size_t)16 * bmax;  // 1 / R_ll (shared by the block's warps)
+  cplx* Rc = rd + bmax;                                          // R11[:, l0 .. l0+W) (ld kk)
   for (int l = threadIdx.x; l < kk; l += blockDim.x) rd[l] = cdiv(cmk(1.0, 0.0), M[l + (size_t)l * m]);
-  __syncthreads();
-  if (c >= r) return;
-  cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)warp * kk;
-  for (int i = lane; i < kk; i += 32) x[i] = M[i + (size_t)(kk + c) * m];
-  __syncwarp();
-  for (int l = kk - 1; l >= 0; --l) {
-    const cplx xl = cmul(x[l], rd[l]);
-    __syncwarp();
-    if (lane == 0) x[l] = xl;
-    for (int i = lane; i < l; i += 32) x[i] = cfms(M[i + (size_t)l * m], xl, x[i]);
-    __syncwarp();
+  const bool act = c < r;
+  cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)warp * bmax;
+  if (act)
+    for (int i = lane; i < kk; i += 32) x[i] = M[i + (size_t)(kk + c) * m];
+  for (int l0 = ((kk - 1) / W) * W; l0 >= 0; l0 -= W) {
+    const int l1 = min(kk, l0 + W);
+    __syncthreads();  // previous chunk consumed (and rd / x ready on the first pass)
+    for (int e = threadIdx.x; e < (l1 - l0) * kk; e += blockDim.x) {
+      const int i = e % kk, l = l0 + e / kk;
+      if (i < l) Rc[i + (size_t)(l - l0) * kk] = M[i + (size_t)l * m];
+    }
+    __syncthreads();
+    if (act)
+      for (int l = l1 - 1; l >= l0; --l) {
+        const cplx xl = cmul(x[l], rd[l]);
+        __syncwarp();
+        if (lane == 0) x[l] = xl;
+        const cplx* col = Rc + (size_t)(l - l0) * kk;
+        for (int i = lane; i < l; i += 32) x[i] = cfms(col[i], xl, x[i]);
+        __syncwarp();
+      }
   }
-  for (int i = lane; i < kk; i += 32) T[i + (size_t)c * kk] = x[i];
+  if (act)
+    for (int i = lane; i < kk; i += 32) T[i + (size_t)c * kk] = x[i];
 }
 
 // ------------------------------------------------------------------ Gauss-Jordan inverse
@@ -2574,14 +2590,16 @@ void launch_refine_T(const RefineTask* d_tasks, int ntasks, int kmax, int rmax, 
 void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx* ws,
                    cplx* tarena, cudaStream_t st, int bmax) {
   if (ntasks <= 0) return;
-  const size_t smem = 17 * (size_t)bmax * sizeof(cplx) + 16;
+  const int bm = std::max(bmax, 1);
+  const int W = std::max(1, std::min(32, (int)(14000 / bm) - 17));  // chunk width that fits 227 KB
+  const size_t smem = (size_t)(17 + W) * bm * sizeof(cplx) + 16;
   static size_t cur = 0;
   if (smem > 48 * 1024 && smem > cur) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_trsm_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cur = smem;
   }
   dim3 grid(ntasks, (bmax + 15) / 16);
-  k_trsm_T<<<grid, 512, smem, st>>>(d_tasks, d_k, ws, tarena);
+  k_trsm_T<<<grid, 512, smem, st>>>(d_tasks, d_k, ws, tarena, W, bm);
   FMMLU_LAUNCH();
 }
 
