@@ -305,3 +305,69 @@ def test_monostatic_rcs_sphere_mie(F):
     R = h.monostatic_rcs(np.linspace(0.0, 2 * math.pi, 36, endpoint=False))
     ref = rcs.mie_backscatter_sphere(k)
     assert np.max(np.abs(R - ref)) / abs(ref) < 0.06   # the O(h) Nyström error of the oracle pin
+
+
+# ---- degenerate and edge cases of the method / the ABI
+def test_single_point_and_pair(F):
+    # n = 1: A = [½] (K_ii = 0), so x = 2b;  n = 2 with leaf 1: a root-only 2×2 dense system
+    g = fi.fibonacci_sphere(1)
+    b = fi.gaussian_rhs(1, 2, 0)
+    h = F.FmmLu(g.points, g.normals, g.weights, 1).factor(1.0, 1e-6)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    assert np.allclose(x, 2 * b, rtol=1e-14, atol=0)
+    g2 = fi.fibonacci_sphere(2)
+    b2 = fi.gaussian_rhs(2, 1, 1)
+    h2 = F.FmmLu(g2.points, g2.normals, g2.weights, 1).factor(1.0, 1e-6)
+    x2 = np.asfortranarray(b2.copy())
+    h2.solve(x2)
+    assert dense.rel_diff(x2, dense.dense_solve(g2.points, g2.normals, g2.weights, 1.0, b2)) < 1e-13
+
+
+def test_cube_corners_root_only(F):
+    g = fi.cube_corners()
+    b = fi.gaussian_rhs(g.n, 3, 2)
+    h, x = _gpu_solve(F, g, 1.0, 1e-6, 1, b)
+    st = h.stats()
+    assert st["n0"] == 8 and st["n_eliminated"] == 0
+    assert dense.rel_diff(x, dense.dense_solve(g.points, g.normals, g.weights, 1.0, b)) < 1e-13
+
+
+def test_device_input_validation(F):
+    g = fi.fibonacci_sphere(300)
+    bad_n = g.normals.copy()
+    bad_n[17] *= 1.001                      # |‖n‖ − 1| > 1e-10
+    bad_w = g.weights.copy()
+    bad_w[5] = 0.0
+    bad_p = g.points.copy()
+    bad_p[9, 1] = np.nan
+    for P, N, W in ((g.points, bad_n, g.weights), (g.points, g.normals, bad_w), (bad_p, g.normals, g.weights)):
+        with pytest.raises(F.FmmluError) as e:
+            F.FmmLu(P, N, W, 16)
+        assert e.value.code == -1           # EINVAL
+
+
+def test_coarse_eps_parity(F):
+    eps = 1e-2
+    g, k, leaf = fi.ellipsoid(3000), 2 * math.pi, 32
+    b = fi.gaussian_rhs(g.n, 2, 4)
+    h, x = _gpu_solve(F, g, k, eps, leaf, b)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf)
+    assert dense.rel_diff(x, rss.solve(f, b)) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
+    assert h.stats()["n0"] < f.stats["n0"] * 1.05 + 2
+
+
+def test_refactor_same_handle_and_ragged_rhs(F):
+    # a second factor() on the same handle replaces the first; 33 RHS = one ragged GEMM-sweep chunk
+    g = fi.ellipsoid(3000)
+    h = F.FmmLu(g.points, g.normals, g.weights, 32)
+    h.factor(1.0, 1e-3)
+    h.factor(2 * math.pi, 1e-6)
+    b = fi.gaussian_rhs(g.n, 33, 6)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    assert dense.residual(g.points, g.normals, g.weights, 2 * math.pi, x, b) <= 1e-5
+    x1 = np.asfortranarray(b[:, 7:8].copy())
+    h.solve(x1)
+    assert dense.rel_diff(x[:, 7:8], x1) < 1e-11
