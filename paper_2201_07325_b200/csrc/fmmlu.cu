@@ -13,7 +13,7 @@
 //       E/F transforms with T (Eq. pap … X blocks, L739-788)      [DMMA GEMM]
 //       X_RR⁻¹ (Gauss-Jordan), Up = X_RR⁻¹X_{R(S∪N)}, Lp = X_{(S∪N)R}X_RR⁻¹   [k_gj, GEMM]
 //       Schur update Δ_{(S∪N)²} −= Lp X_{R(S∪N)} scattered into the BSR (L813-825) [GEMM+atomics]
-//   root: B_t dense block → X⁻¹ (L894-918)                        [k_build, k_gj_coop]
+//   root: B_t dense block → X⁻¹ (L894-918)                        [k_build, blocked GJ: k_gj_panel_reg + DMMA updates]
 // Solve: upward sweep over phases, root apply, downward sweep.
 #include <cuda_runtime.h>
 #include <malloc.h>

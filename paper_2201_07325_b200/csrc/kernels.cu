@@ -1569,89 +1569,6 @@ __global__ void k_pchol_big_finish(const PcholBig* __restrict__ tasks, int* __re
   if (threadIdx.x == 0) k_out[t.kslot] = kk;
 }
 
-// Cooperative Gauss-Jordan inverse (root block D_t⁻¹): columns are
-// owned round-robin by the CTAs; one grid barrier per elimination step.  Output to B
-// (column permutation undone out-of-place).
-constexpr int GJC_NT = 512;
-__global__ void __launch_bounds__(GJC_NT) k_gj_coop(cplx* A, cplx* B, int n, cplx* scratch,
-                                                    int* piv, int* status) {
-  extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  cg::grid_group grid = cg::this_grid();
-  cplx* col = reinterpret_cast<cplx*>(shm);
-  const int tid = threadIdx.x, G = gridDim.x, gb = blockIdx.x;
-  if (gb == 0)
-    for (int i = tid; i < n; i += GJC_NT) scratch[i] = A[i];
-  grid.sync();
-  for (int j = 0; j < n; ++j) {
-    const cplx* cj = scratch + (size_t)(j & 1) * n;
-    for (int i = tid; i < n; i += GJC_NT) col[i] = cj[i];
-    __syncthreads();
-    double pv = -1.0;
-    int p = INT_MAX;
-    for (int i = j + tid; i < n; i += GJC_NT) argmax_merge(pv, p, cabs2(col[i]), i);
-    block_argmax<GJC_NT>(pv, p, red_v, red_i);
-    if (!(pv > 0.0)) {
-      if (gb == 0 && tid == 0) atomicExch(status, 1);
-      return;  // uniform across the grid (same column data everywhere)
-    }
-    if (gb == 0 && tid == 0) piv[j] = p;
-    const cplx d = col[p];
-    const cplx dinv = cdiv(cmk(1.0, 0.0), d);
-    __syncthreads();
-    if (tid == 0 && p != j) {  // swapped column j
-      cplx a = col[j];
-      col[j] = col[p];
-      col[p] = a;
-    }
-    __syncthreads();
-    for (int c = gb; c < n; c += G) {
-      cplx* Ac = A + (size_t)c * n;
-      cplx rj;
-      if (tid == 0) {
-        if (p != j) {
-          cplx a = Ac[j];
-          Ac[j] = Ac[p];
-          Ac[p] = a;
-        }
-      }
-      __syncthreads();
-      rj = Ac[j];
-      __syncthreads();
-      if (c == j) {
-        for (int i = tid; i < n; i += GJC_NT)
-          Ac[i] = i == j ? dinv : cmk(-(col[i].x * dinv.x - col[i].y * dinv.y), -(col[i].x * dinv.y + col[i].y * dinv.x));
-      } else {
-        const cplx rs = cmul(rj, dinv);
-        for (int i = tid; i < n; i += GJC_NT) Ac[i] = i == j ? rs : cfms(col[i], rs, Ac[i]);
-      }
-      if (c == j + 1) {
-        __syncthreads();
-        for (int i = tid; i < n; i += GJC_NT) scratch[(size_t)((j + 1) & 1) * n + i] = Ac[i];
-      }
-      __syncthreads();
-    }
-    grid.sync();
-  }
-  // undo the column interchanges: final column c = column L[c] (L = swaps applied in reverse)
-  int* L = reinterpret_cast<int*>(shm);
-  for (int c = tid; c < n; c += GJC_NT) L[c] = c;
-  __syncthreads();
-  if (tid == 0)
-    for (int j = n - 1; j >= 0; --j) {
-      int p = piv[j];
-      int a = L[j];
-      L[j] = L[p];
-      L[p] = a;
-    }
-  __syncthreads();
-  for (int c = gb; c < n; c += G) {
-    const cplx* src = A + (size_t)L[c] * n;
-    for (int i = tid; i < n; i += GJC_NT) B[i + (size_t)c * n] = src[i];
-  }
-}
-
 // ------------------------------------------------------------------ solve sweeps
 constexpr int SV_NT = 256;
 constexpr int SV_Q = 4;  // RHS processed per pass
@@ -2616,27 +2533,6 @@ void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx*
   FMMLU_LAUNCH();
 }
 
-
-void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st) {
-  // scratch: 2n complex (column buffers) + n ints (pivots) + n*n complex (output)
-  int dev;
-  FMMLU_CUDA(cudaGetDevice(&dev));
-  int nsm;
-  FMMLU_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  size_t smem = (size_t)n * sizeof(cplx) + 16;
-  FMMLU_CUDA(cudaFuncSetAttribute(k_gj_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  FMMLU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_coop, GJC_NT, smem));
-  if (per_sm < 1) throw Error(-4, "root block too large for the cooperative GJ kernel");
-  int G = nsm;
-  cplx* colbuf = scratch;
-  int* piv = reinterpret_cast<int*>(scratch + 2 * (size_t)n);
-  cplx* B = scratch + 2 * (size_t)n + (n + 1) / 2 + 1;
-  void* args[] = {&A, &B, &n, &colbuf, &piv, &d_status};
-  FMMLU_CUDA(cudaLaunchCooperativeKernel((void*)k_gj_coop, G, GJC_NT, args, smem, st));
-  FMMLU_LAUNCH();
-  FMMLU_CUDA(cudaMemcpyAsync(A, B, (size_t)n * n * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
-}
 
 void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                       const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax) {

@@ -180,8 +180,6 @@ struct PcholBig {
 void launch_pchol_big_panel(const PcholBig* d_tasks, int ntasks, int nb, double eps, cudaStream_t st, int bmax);
 void launch_pchol_big_finish(const PcholBig* d_tasks, int ntasks, int* perm_out, int* k_out, cudaStream_t st,
                              int bmax);
-// cooperative (all SMs) Gauss-Jordan inverse of one large n×n matrix (ld = n)
-void launch_gj_inverse_coop(cplx* A, int n, cplx* scratch, int* d_status, cudaStream_t st);
 // Split solve sweeps for one phase:
 //   up:   [a] t = y_R − Tᵀy_S → tmp, y_R ← X_RR⁻¹ t   [b] y_{S∪N} −= X_{(S∪N)R} y_R (= Lp t; row chunks)
 //   down: [a] acc = Up y_{S∪N} (column chunks, atomics)    [b] y_R −= acc, y_S −= T y_R
