@@ -323,63 +323,6 @@ __global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks
 }
 
 // ------------------------------------------------------------------ Gauss-Jordan inverse
-constexpr int GJ_NT = 512;
-
-__global__ void __launch_bounds__(GJ_NT) k_gj(const long long* __restrict__ offs,
-                                              const int* __restrict__ dims, cplx* arena,
-                                              int* status) {
-  extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  const int n = dims[blockIdx.x];
-  cplx* A = arena + offs[blockIdx.x];
-  cplx* colj = reinterpret_cast<cplx*>(shm);
-  cplx* rowj = colj + n;
-  int* piv = reinterpret_cast<int*>(rowj + n);
-  const int tid = threadIdx.x;
-  for (int j = 0; j < n; ++j) {
-    double pv = -1.0;
-    int p = INT_MAX;
-    for (int i = j + tid; i < n; i += GJ_NT) argmax_merge(pv, p, cabs2(A[i + (size_t)j * n]), i);
-    block_argmax<GJ_NT>(pv, p, red_v, red_i);
-    if (!(pv > 0.0)) {
-      if (tid == 0) atomicExch(status, 1);
-      return;
-    }
-    if (tid == 0) piv[j] = p;
-    if (p != j)
-      for (int c = tid; c < n; c += GJ_NT) {
-        cplx a = A[j + (size_t)c * n];
-        A[j + (size_t)c * n] = A[p + (size_t)c * n];
-        A[p + (size_t)c * n] = a;
-      }
-    __syncthreads();
-    const cplx d = A[j + (size_t)j * n];
-    const cplx dinv = cdiv(cmk(1.0, 0.0), d);
-    for (int i = tid; i < n; i += GJ_NT) colj[i] = A[i + (size_t)j * n];
-    for (int c = tid; c < n; c += GJ_NT) rowj[c] = c == j ? dinv : cmul(A[j + (size_t)c * n], dinv);
-    __syncthreads();
-    for (int e = tid; e < n * n; e += GJ_NT) {
-      const int i = e % n, c = e / n;
-      cplx v;
-      if (i == j) v = rowj[c];
-      else if (c == j) v = cmk(-(colj[i].x * dinv.x - colj[i].y * dinv.y), -(colj[i].x * dinv.y + colj[i].y * dinv.x));
-      else v = cfms(colj[i], rowj[c], A[i + (size_t)c * n]);
-      A[i + (size_t)c * n] = v;
-    }
-    __syncthreads();
-  }
-  for (int j = n - 1; j >= 0; --j) {
-    const int p = piv[j];
-    if (p != j)
-      for (int i = tid; i < n; i += GJ_NT) {
-        cplx a = A[i + (size_t)j * n];
-        A[i + (size_t)j * n] = A[i + (size_t)p * n];
-        A[i + (size_t)p * n] = a;
-      }
-    __syncthreads();
-  }
-}
 
 // ------------------------------------------------------------------ blocked Gauss-Jordan
 // In-place Gauss-Jordan with partial pivoting, blocked by column panels J = [j0, j0+jb):
@@ -2519,20 +2462,6 @@ void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx
   k_trsm_T<<<grid, 512, smem, st>>>(d_tasks, d_k, ws, tarena, W, bm);
   FMMLU_LAUNCH();
 }
-
-void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx* arena,
-                       int* d_status, cudaStream_t st, int nmax) {
-  if (nmat <= 0) return;
-  size_t smem = (size_t)nmax * (2 * sizeof(cplx) + sizeof(int)) + 16;
-  static size_t cur = 0;
-  if (smem > 48 * 1024 && smem > cur) {
-    FMMLU_CUDA(cudaFuncSetAttribute(k_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cur = smem;
-  }
-  k_gj<<<nmat, GJ_NT, smem, st>>>(d_off, d_dim, arena, d_status);
-  FMMLU_LAUNCH();
-}
-
 
 void launch_solve_up2(const BoxRec* d_recs, int nrec, const SolveItem* d_items, int nitems, const cplx* fac,
                       const int* idx, cplx* y, int ldy, int nrhs, cplx* tmp, cudaStream_t st, int kmax, int rmax) {

@@ -128,9 +128,6 @@ void launch_gj_panel_reg(const GjTask* d_tasks, int ntasks, int j0, int nb, int*
                          cudaStream_t st, int nmax);
 void launch_gj_unscramble(const GjTask* d_tasks, int ntasks, cplx* scratch, const long long* d_soff, cudaStream_t st,
                           int nmax);
-// in-place Gauss-Jordan inverse of nmat matrices (dims dim[i], ld[i], offsets off[i] in arena)
-void launch_gj_inverse(const long long* d_off, const int* d_dim, int nmat, cplx* arena,
-                       int* d_status, cudaStream_t st, int nmax);
 // Whole-matrix Gauss-Jordan inverse resident in (distributed) shared memory: one CTA, or a
 // cluster of ≤ 16 CTAs holding the columns cyclically.  Returns false when nmax is too large
 // (the caller uses the blocked panel path).
