@@ -1554,9 +1554,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           for (int j = 0; j < nj; ++j) {
             at[j] = c;
             const BoxJob& J = jobs[j];
-            for (int q : J.Q)
+            for (int q : J.Q) {
               if (!ident[q]) c.maps += 2 * (int)curpos[q].size();
-            c.cps += 2 * (int)J.Q.size();
+              c.cps += 2 * copy_tiles((int)curpos[q].size(), J.b);  // pre-split into 64×64 tiles
+            }
             if (J.proxy) {
               c.pts += 1;
               c.gidx += (int)cur.act[J.a].size();
@@ -1589,7 +1590,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               c.trans = 0;
               c.rmap_off = mo;
               c.cmap_off = -1;
-              cps[ci++] = c;
+              ci += emit_copy_tiles(c, &cps[ci]);
               row += c.rows;
             }
             for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
@@ -1608,7 +1609,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               c.trans = 1;
               c.rmap_off = mo;
               c.cmap_off = -1;
-              cps[ci++] = c;
+              ci += emit_copy_tiles(c, &cps[ci]);
               row += c.rows;
             }
             if (J.proxy) {
@@ -1641,7 +1642,6 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (maps.empty()) maps.push_back(0);
         if (gidx.empty()) gidx.push_back(0);
         Stage s;
-        split_copy_tasks(cps);
         size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_g = s.add(gidx);
         s.upload(st);
         lap(8);
@@ -1797,22 +1797,26 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         struct FrameRef { int slot_off, tab_off, bld_off, ns; };
         std::vector<FrameRef> frames(el.size());
         // pass 1 (serial, O(|N|) per box): where each box's entries go in every array
-        struct Counts { int maps, cps, cpsT, fs, tab, bld; };
+        struct Counts { int maps, cps, cpsT, cpsX, fs, tab, bld; };
         std::vector<Counts> at(el.size() + 1);
         {
-          Counts c{0, 0, 0, 0, 0, 0};
+          Counts c{0, 0, 0, 0, 0, 0, 0};
           for (size_t e = 0; e < el.size(); ++e) {
             at[e] = c;
             const BoxJob& J = jobs[el[e]];
             const int ns = 1 + (int)J.N.size();
-            int nm = J.b, nf = J.k;
+            const int r = J.b - J.k;
+            int nm = J.b, nf = J.k, nc = copy_tiles(J.b, J.b);
             for (int o : J.N) {
-              if (!ident[o]) nm += (int)curpos[o].size();
-              nf += (int)curpos[o].size();
+              const int no_ = (int)curpos[o].size();
+              if (!ident[o]) nm += no_;
+              nf += no_;
+              nc += copy_tiles(J.b, no_) + copy_tiles(no_, J.b);
             }
             c.maps += nm;
-            c.cps += 1 + 2 * (int)J.N.size();
-            c.cpsT += (J.k > 0 && J.b - J.k > 0) ? 1 : 0;
+            c.cps += nc;  // in 64×64 tiles (split here rather than by a serial pass afterwards)
+            c.cpsT += (J.k > 0 && r > 0) ? copy_tiles(J.k, r) : 0;
+            c.cpsX += copy_tiles(r, r) + copy_tiles(J.k, r) + copy_tiles(J.nN, r);
             c.fs += nf;
             c.tab += ns * ns;
             c.bld += ns;
@@ -1821,7 +1825,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           maps.resize(c.maps);
           cps.resize(c.cps);
           cpsT.resize(c.cpsT);
-          cpsX.resize(3 * el.size());
+          cpsX.resize(c.cpsX);
           gjoff.resize(el.size());
           gjdim.resize(el.size());
           fslot.resize(c.fs);
@@ -1855,7 +1859,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             c.trans = 0;
             c.rmap_off = rf;
             c.cmap_off = rf;
-            cps[ci++] = c;
+            ci += emit_copy_tiles(c, &cps[ci]);
             int noff = 0;
             for (int o : J.N) {
               int mo = -1;
@@ -1875,7 +1879,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               a.trans = 0;
               a.rmap_off = rf;
               a.cmap_off = mo;
-              cps[ci++] = a;
+              ci += emit_copy_tiles(a, &cps[ci]);
               CopyTask d{};
               d.src = cur.off(o, J.a);
               d.lds = (int)cur.act[o].size();
@@ -1886,7 +1890,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               d.trans = 0;
               d.rmap_off = mo;
               d.cmap_off = rf;
-              cps[ci++] = d;
+              ci += emit_copy_tiles(d, &cps[ci]);
               noff += no_;
             }
             // T → factor store (k × r)
@@ -1901,7 +1905,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               t.trans = 0;
               t.rmap_off = -1;
               t.cmap_off = -1;
-              cpsT[at[e].cpsT] = t;
+              emit_copy_tiles(t, &cpsT[at[e].cpsT]);
             }
             // X_RR → Xinv slot (after E/F)
             CopyTask x{};
@@ -1914,7 +1918,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             x.trans = 0;
             x.rmap_off = -1;
             x.cmap_off = -1;
-            cpsX[3 * e] = x;
+            int xi = at[e].cpsX;
+            xi += emit_copy_tiles(x, &cpsX[xi]);
             // X_{(S∪N)R} → the Lp slot: the factor keeps X_{(S∪N)R} itself (the solve applies it to
             // X_RR⁻¹ t, and the Schur update is X_{(S∪N)R}·Up), so no Lp = X_{(S∪N)R} X_RR⁻¹ product
             CopyTask xs{};
@@ -1926,7 +1931,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             xs.cols = r;
             xs.rmap_off = -1;
             xs.cmap_off = -1;
-            cpsX[3 * e + 1] = xs;
+            xi += emit_copy_tiles(xs, &cpsX[xi]);
             CopyTask xn{};
             xn.src = WNoff[el[e]];  // W_N = X_{N,B}: columns R
             xn.lds = std::max(J.nN, 1);
@@ -1936,7 +1941,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             xn.cols = r;
             xn.rmap_off = -1;
             xn.cmap_off = -1;
-            cpsX[3 * e + 2] = xn;
+            emit_copy_tiles(xn, &cpsX[xi]);
             gjoff[e] = R.Xi;
             gjdim[e] = r;
             // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
@@ -1969,9 +1974,6 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (fbld.empty()) fbld.push_back(0);
         lap(18);
         Stage s;
-        split_copy_tasks(cps);
-        split_copy_tasks(cpsT);
-        split_copy_tasks(cpsX);
         size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_fs = s.add(fslot),
                o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
                o_rec = s.add(recs);

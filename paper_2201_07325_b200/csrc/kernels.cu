@@ -1986,6 +1986,37 @@ void launch_herm_mirror(cplx* const* d_ptrs, const int* d_dims, int nmats, int b
   FMMLU_LAUNCH();
 }
 
+int copy_tiles(int rows, int cols) {
+  if ((long long)rows * cols <= 4096) return 1;
+  return ((rows + 63) / 64) * ((cols + 63) / 64);
+}
+
+int emit_copy_tiles(const CopyTask& t, CopyTask* out) {
+  if ((long long)t.rows * t.cols <= 4096) {
+    out[0] = t;
+    return 1;
+  }
+  int n = 0;
+  for (int i0 = 0; i0 < t.rows; i0 += 64)
+    for (int j0 = 0; j0 < t.cols; j0 += 64) {
+      CopyTask u = t;
+      u.rows = std::min(64, t.rows - i0);
+      u.cols = std::min(64, t.cols - j0);
+      u.dst = t.dst + i0 + (long long)j0 * t.ldd;
+      u.ti = t.ti + i0;
+      u.tj = t.tj + j0;
+      if (!t.trans) {
+        if (t.rmap_off >= 0) u.rmap_off = t.rmap_off + i0; else u.src += i0;
+        if (t.cmap_off >= 0) u.cmap_off = t.cmap_off + j0; else u.src += (long long)j0 * t.lds;
+      } else {
+        if (t.rmap_off >= 0) u.rmap_off = t.rmap_off + i0; else u.src += (long long)i0 * t.lds;
+        if (t.cmap_off >= 0) u.cmap_off = t.cmap_off + j0; else u.src += j0;
+      }
+      out[n++] = u;
+    }
+  return n;
+}
+
 void split_copy_tasks(std::vector<CopyTask>& v) {
   std::vector<CopyTask> out;
   out.reserve(v.size());

@@ -56,6 +56,8 @@ struct CopyTask {
 void launch_herm_mirror(cplx* const* d_ptrs, const int* d_dims, int nmats, int bmax, cudaStream_t st);
 // Split copy tasks larger than 64×64 into 64×64 tiles (load balance across CTAs).
 void split_copy_tasks(std::vector<CopyTask>& v);
+int copy_tiles(int rows, int cols);                  // tiles split_copy_tasks makes of one task
+int emit_copy_tiles(const CopyTask& t, CopyTask* out);  // writes them, returns the count
 
 // Proxy rows of M (§5.1.3; readings C3-C5): rows row0 .. row0+nγ-1 hold
 // s_γ K(y_ℓ, x_j) √w_j (outgoing, combined field with the box normals), rows row0+nγ ..
