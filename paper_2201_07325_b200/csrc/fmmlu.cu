@@ -134,25 +134,6 @@ struct BigCache {
     std::lock_guard<std::mutex> lk(mu);
     while (!free_.empty()) evict_front(st);
   }
-  // Before a cache miss turns into cudaMallocAsync: hand idle cached blocks back to the pool until the
-  // pool's own free memory covers the request, so that the allocation reuses them instead of growing
-  // the pool (growing maps new physical memory and stalled the host for 50-110 ms).
-  void make_room(size_t need, cudaStream_t st, int dev) {
-    cudaMemPool_t pool;
-    uint64_t reserved = 0, used = 0;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess ||
-        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) != cudaSuccess ||
-        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) != cudaSuccess) {
-      cudaGetLastError();
-      return;
-    }
-    size_t avail = reserved > used ? (size_t)(reserved - used) : 0;
-    std::lock_guard<std::mutex> lk(mu);
-    while (avail < need && !free_.empty()) {
-      avail += free_.front().bytes;
-      evict_front(st);
-    }
-  }
   size_t cached() {
     std::lock_guard<std::mutex> lk(mu);
     return held;
@@ -224,9 +205,6 @@ struct DBuf {
       p = big_cache().take(b, s, &got);
       if (!p) {
         got = (b + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        big_cache().make_room(got, s, dev);
         e = cudaMallocAsync(&p, got, s);
         if (e != cudaSuccess) {  // give the cached blocks back and retry once
           cudaGetLastError();

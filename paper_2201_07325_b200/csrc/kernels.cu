@@ -748,7 +748,7 @@ struct GjCand {
   cplx x;
 };
 
-template <int MR, int MC, bool MULTI, bool TIMING = false>
+template <int MR, int MC, bool MULTI, bool TIMING = false, bool PUSH = false>
 __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__ tasks, int* status) {
   static_assert(MR == 1 || MR == 2, "rows per lane");
   long long tph[5] = {0, 0, 0, 0, 0}, tc = 0;  // TIMING: cycles in P1 | B1 | P2 | B2 | P3
@@ -765,8 +765,11 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
   // single CTA: exchange through shared memory.  Cluster: through global memory / L2 (t.Am is
   // this task's scratch: [2][n] column + [2][16] candidates) — DSMEM reads of one owner CTA by
   // every thread of 16 CTAs would serialise on the owner's shared-memory port.
-  __shared__ cplx pbs[MULTI ? 1 : 2][MULTI ? 1 : GJR_NMAX];
-  __shared__ GjCand cands[MULTI ? 1 : 2][GJR_NW];
+  // PUSH (cluster): the owner of column j writes it and the candidates into every CTA's shared
+  // memory (DSMEM) before the barrier, so everything after it is a local read (small clusters)
+  constexpr bool LOCALX = !MULTI || PUSH;
+  __shared__ cplx pbs[LOCALX ? 2 : 1][LOCALX ? GJR_NMAX : 1];
+  __shared__ GjCand cands[LOCALX ? 2 : 1][GJR_NW];
   __shared__ cplx rowp[GJR_NW * MC];  // m_pc / d, [column group][slot]
   __shared__ int piv[GJR_NMAX], pinv[GJR_NMAX];
   const GjTask t = tasks[blockIdx.y];
@@ -796,8 +799,8 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
   for (int j = 0; j < n; ++j) {
     if (TIMING) tc = clock64();
     const int o = j & (CL - 1), lj = j >> lgCL, par = j & 1;
-    cplx* const pcol = MULTI ? xg + par * n : &pbs[par & (MULTI ? 0 : 1)][0];
-    GjCand* const pcand = MULTI ? cg_ + par * GJR_NW : &cands[par & (MULTI ? 0 : 1)][0];
+    cplx* const pcol = !LOCALX ? xg + par * n : &pbs[par & (LOCALX ? 1 : 0)][0];
+    GjCand* const pcand = !LOCALX ? cg_ + par * GJR_NW : &cands[par & (LOCALX ? 1 : 0)][0];
     int qj = -1;  // slot of column j in this warp
     if (rank == o && lj == nextl && qn < nq) {
       qj = qn;
@@ -817,8 +820,13 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
           if (q == qj) x = a[q][r];
         const int i = row0 + 32 * r;
         if (i < n) {
-          if (MULTI) __stcg(reinterpret_cast<double2*>(pcol + i), x);
-          else pcol[i] = x;
+          if (!LOCALX) {
+            __stcg(reinterpret_cast<double2*>(pcol + i), x);
+          } else if (MULTI) {
+            for (int dr = 0; dr < CL; ++dr) *cl.map_shared_rank(pcol + i, dr) = x;
+          } else {
+            pcol[i] = x;
+          }
           const double v = cabs2(x);
           if (!((used >> r) & 1u) && v > pv) {  // rows ascend with r: strict > keeps the lowest
             pv = v;
@@ -838,7 +846,11 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
         cd.i = p;
         cd.pad = 0;
         cd.x = px;
-        pcand[rg] = cd;
+        if (MULTI && PUSH) {
+          for (int dr = 0; dr < CL; ++dr) *cl.map_shared_rank(pcand + rg, dr) = cd;
+        } else {
+          pcand[rg] = cd;
+        }
       }
     }
     GJ_TICK(0);
@@ -849,7 +861,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
     int p = INT_MAX;
     cplx d = cmk(1.0, 0.0);
     if (lane < RG) {
-      if (MULTI) {
+      if (!LOCALX) {
         const double* cp = reinterpret_cast<const double*>(pcand + lane);
         pv = __ldcg(cp);
         p = __ldcg(reinterpret_cast<const int*>(cp + 1));
@@ -857,13 +869,14 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
       } else {
         pv = pcand[lane].v;
         p = pcand[lane].i;
+        d = pcand[lane].x;
       }
     }
     cplx c[MR];  // issue the column loads early (they do not depend on p)
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int i = row0 + 32 * r;
-      c[r] = i < n ? (MULTI ? __ldcg(reinterpret_cast<const double2*>(pcol + i)) : pcol[i]) : cmk(0.0, 0.0);
+      c[r] = i < n ? (!LOCALX ? __ldcg(reinterpret_cast<const double2*>(pcol + i)) : pcol[i]) : cmk(0.0, 0.0);
     }
     warp_argmax_redux(pv, p);  // every lane gets the result (redux.sync is warp-uniform)
     const bool sing = !(pv > 0.0);
@@ -2263,7 +2276,12 @@ void launch_gjr(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t s
     FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_gj_reg<MR, MC, true, true>, d_tasks, d_status));
     return;
   }
-  if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(k_gj_reg<MR, MC, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // DSMEM-pushed column exchange up to `push_max_cl` CTAs (the owner's outbound DSMEM traffic grows
+  // with CL·n; beyond it the L2 exchange is used)
+  static const int push_max_cl = getenv("FMMLU_GJ_PUSH_CL") ? atoi(getenv("FMMLU_GJ_PUSH_CL")) : 8;
+  const bool push = CL <= push_max_cl;
+  auto kern = push ? k_gj_reg<MR, MC, true, false, true> : k_gj_reg<MR, MC, true>;
+  if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL, ntasks, 1);
   cfg.blockDim = dim3(GJR_NT, 1, 1);
@@ -2276,7 +2294,7 @@ void launch_gjr(const GjTask* d_tasks, int ntasks, int* d_status, cudaStream_t s
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_gj_reg<MR, MC, true>, d_tasks, d_status));
+  FMMLU_CUDA(cudaLaunchKernelEx(&cfg, kern, d_tasks, d_status));
   }
 }
 }  // namespace
