@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
 // for its columns and updates S_ac −= S_ap conj(S_cp)/S_pp in registers.  Stop rule C9 on the
 // diagonal (≤ ε²·initial max).  grid (CL, ntasks), 512 threads; xs = exchange scratch
 // ([2][CL][b] columns + [2][CL] candidates per task, task stride xstride complex).
-template <int MR, int MC, bool MULTI, bool TIMING = false>
+template <int MR, int MC, bool MULTI, bool TIMING = false, bool PUSH = false>
 __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __restrict__ tasks,
                                                         int* __restrict__ perm_out, int* __restrict__ k_out,
                                                         double eps, cplx* __restrict__ xs, long long xstride) {
@@ -1270,8 +1270,12 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
   __shared__ int cis[2];
   __shared__ double ccv[2][16];  // cluster: candidates pushed by every CTA (DSMEM), [parity][rank]
   __shared__ int cci[2][16];
+  // PUSH (clusters ≤ 4, b ≤ 192): every CTA also pushes its candidate column into every CTA's shared
+  // memory, so the winner's column is read locally after the barrier (no L2 round trip)
+  __shared__ cplx ccol[PUSH ? 2 : 1][PUSH ? 4 : 1][PUSH ? 192 : 1];
   const ClusterQrTask t = tasks[blockIdx.y];
   const int b = t.b;
+  if (PUSH && (CL > 4 || b > 192)) __trap();
   const int ncl = (b - rank + CL - 1) >> lgCL;
   const int RG = (b + 32 * MR - 1) >> (5 + LGMR), CG = GJR_NW / RG;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1322,8 +1326,13 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
           if (q == qs) x = a[q][r];
         const int i = row0 + 32 * r;
         if (i < b) {
-          if (MULTI) __stcg(reinterpret_cast<double2*>(dst + i), x);
-          else dst[i] = x;
+          if (PUSH) {
+            for (int dr = 0; dr < CL; ++dr) *cl.map_shared_rank(&ccol[par][rank][i], dr) = x;
+          } else if (MULTI) {
+            __stcg(reinterpret_cast<double2*>(dst + i), x);
+          } else {
+            dst[i] = x;
+          }
         }
       }
     }
@@ -1361,10 +1370,16 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
       break;  // uniform: every CTA reads the same candidates
     }
     jdone = j + 1;
-    const cplx* src = MULTI ? xcol + ((size_t)par * CL + po) * b : &colx[par & (MULTI ? 0 : 1)][0];
-    for (int i = tid; i < b; i += GJR_NT) colp[i] = MULTI ? __ldcg(reinterpret_cast<const double2*>(src + i)) : src[i];
-    if (tid == 0) piv[j] = p;
-    __syncthreads();  // B2
+    const cplx* colq = colp;  // the pivot column, read by P3
+    if (PUSH) {
+      colq = &ccol[par][po][0];  // already local: pushed before the barrier
+      if (tid == 0) piv[j] = p;
+    } else {
+      const cplx* src = MULTI ? xcol + ((size_t)par * CL + po) * b : &colx[par & (MULTI ? 0 : 1)][0];
+      for (int i = tid; i < b; i += GJR_NT) colp[i] = MULTI ? __ldcg(reinterpret_cast<const double2*>(src + i)) : src[i];
+      if (tid == 0) piv[j] = p;
+      __syncthreads();  // B2
+    }
     if (TIMING) { const long long n_ = clock64() + (int)colp[0].x * 0; tph[2] += n_ - tc; tc = n_; }
     // ---- P3: R row j for the local columns, diagonal and register updates
     const double isd = rsqrt(pv), ipv = 1.0 / pv;
@@ -1375,7 +1390,7 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
         Rg[j + (size_t)g * b] = cmk(pv * isd, 0.0);
         dn[l] = 1;
       } else {
-        const cplx u = colp[g];  // S_gp;  R_{j,g} = conj(S_gp)/√S_pp
+        const cplx u = colq[g];  // S_gp;  R_{j,g} = conj(S_gp)/√S_pp
         Rg[j + (size_t)g * b] = cmk(u.x * isd, -u.y * isd);
         dg[l] -= (u.x * u.x + u.y * u.y) * ipv;
       }
@@ -1384,13 +1399,13 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int i = row0 + 32 * r;
-      c[r] = i < b ? cmk(colp[i].x * ipv, colp[i].y * ipv) : cmk(0.0, 0.0);
+      c[r] = i < b ? cmk(colq[i].x * ipv, colq[i].y * ipv) : cmk(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < MC; ++q) {  // branch only every 4 columns (see k_gj_reg)
       if ((q & 3) == 0 && q >= nq) break;
       const int g = min(rank + ((cgp + CG * q) << lgCL), b - 1);
-      const cplx u = colp[g];
+      const cplx u = colq[g];
       const cplx uc = cmk(u.x, -u.y);  // conj(S_gp) = S_pg
 #pragma unroll
       for (int r = 0; r < MR; ++r) a[q][r] = cfms(c[r], uc, a[q][r]);
@@ -2340,7 +2355,7 @@ size_t pchol_smem(int b, int CL) {
 namespace {
 template <int MR, int MC, bool MULTI>
 void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
-                long long xstride, cudaStream_t st, int CL) {
+                long long xstride, cudaStream_t st, int CL, int bmax = 0) {
   static const bool timing = getenv("FMMLU_PCHOL_TIMING") != nullptr;
   if (timing && MULTI) {
     if (CL > 8)
@@ -2368,8 +2383,10 @@ void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_
     k_pchol_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride);
     FMMLU_LAUNCH();
   } else {
-    if (CL > 8)
-      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_reg<MR, MC, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    static const int push_env = getenv("FMMLU_PCHOL_PUSH") ? atoi(getenv("FMMLU_PCHOL_PUSH")) : 1;
+    const bool push = push_env && CL <= 4 && bmax <= 192;
+    auto kern = push ? k_pchol_reg<MR, MC, true, false, true> : k_pchol_reg<MR, MC, true>;
+    if (CL > 8) FMMLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL, ntasks, 1);
     cfg.blockDim = dim3(GJR_NT, 1, 1);
@@ -2381,7 +2398,7 @@ void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_pchol_reg<MR, MC, true>, d_tasks, perm_out, k_out, eps, xs, xstride));
+    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, kern, d_tasks, perm_out, k_out, eps, xs, xstride));
   }
 }
 }  // namespace
@@ -2405,10 +2422,10 @@ bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, i
   const long long xstride = pchol_reg_scratch(bmax);
   if (bmax <= 32) launch_pcr<1, 2, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
   else if (bmax <= 64) launch_pcr<1, 8, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
-  else if (bmax <= 128) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
-  else if (bmax <= 192) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
-  else if (bmax <= 256) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
-  else if (bmax <= 384) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
+  else if (bmax <= 128) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
+  else if (bmax <= 192) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
+  else if (bmax <= 256) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
+  else if (bmax <= 384) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
   else launch_pcr<2, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
   return true;
 }
