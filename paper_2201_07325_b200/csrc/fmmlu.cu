@@ -578,7 +578,7 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   bool cluster_panel = false;
   static const int panel_env = getenv("FMMLU_GJ_PANEL") ? atoi(getenv("FMMLU_GJ_PANEL")) : 0;
   bool reg_panel = false;
-  if (panel_env == 0 && nb < 32 && nmax > 512 && gj_panel_reg_width(nmax) >= 32) {
+  if (panel_env == 0 && nb < 32 && nmax > 512 && gj_panel_reg_width(nmax) >= 16) {
     // tall blocks (root): register-resident panel rows over a 16-CTA cluster, L2 exchange
     nb = gj_panel_reg_width(nmax);
     reg_panel = true;

@@ -2182,8 +2182,12 @@ void launch_cluster(K kern, int CL, int ny, size_t smem, cudaStream_t st, Args..
 }  // namespace
 
 // register panel: panel width for an n-row block (columns per warp ≤ 24, width ≤ 64)
+int gj_panel_reg_cl() {  // cluster size of the root's register panel
+  static const int cl = getenv("FMMLU_ROOT_CL") ? atoi(getenv("FMMLU_ROOT_CL")) : 16;
+  return cl;
+}
 int gj_panel_reg_width(int nmax) {
-  const int CL = 16, rc = (nmax + CL - 1) / CL, RG = (rc + 31) / 32;
+  const int CL = gj_panel_reg_cl(), rc = (nmax + CL - 1) / CL, RG = (rc + 31) / 32;
   if (RG > GJR_NW) return 0;
   const int CG = GJR_NW / RG;
   return std::min(64, 8 * CG);  // ≤ 8 panel columns per warp (registers)
@@ -2194,7 +2198,7 @@ namespace {
 template <int MC>
 void launch_gpr(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cplx* xs, long long xstride,
                 cudaStream_t st) {
-  const int CL = 16;
+  const int CL = gj_panel_reg_cl();
   FMMLU_CUDA(cudaFuncSetAttribute(k_gj_panel_reg<MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   const size_t dyn = 2 * (size_t)CL * nb * sizeof(cplx);
@@ -2221,7 +2225,8 @@ void launch_gpr(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status
 void launch_gj_panel_reg(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_status, cplx* xs,
                          cudaStream_t st, int nmax) {
   if (ntasks <= 0) return;
-  const int rc = (nmax + 15) / 16, RG = (rc + 31) / 32, CG = GJR_NW / RG;
+  const int CL = gj_panel_reg_cl();
+  const int rc = (nmax + CL - 1) / CL, RG = (rc + 31) / 32, CG = GJR_NW / RG;
   const int mc = (nb + CG - 1) / CG;
   const long long xstride = gj_panel_reg_scratch(nb);
   if (mc > 8) throw Error(-6, "register GJ panel: width beyond 8 columns per warp");
