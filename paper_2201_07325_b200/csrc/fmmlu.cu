@@ -857,7 +857,10 @@ class HostPool {
   template <class F>
   void parallel_for(int count, int min_par, F&& fn) {
     const int nw = (int)workers_.size();
-    if (nw == 0 || count < min_par) {
+    // one parallel region at a time: a concurrent caller (another handle on another host thread)
+    // runs its loop inline instead of sharing the workers
+    std::unique_lock<std::mutex> busy(call_mu_, std::try_to_lock);
+    if (nw == 0 || count < min_par || !busy.owns_lock()) {
       fn(0, count);
       return;
     }
@@ -899,6 +902,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> workers_;
+  std::mutex call_mu_;
   std::mutex m_;
   std::condition_variable cv_, done_;
   std::function<void(int)> job_;
@@ -1974,6 +1978,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (fbld.empty()) fbld.push_back(0);
         lap(18);
         Stage s;
+        s.host.reserve(16 * 12 + sizeof(CopyTask) * (cps.size() + cpsT.size() + cpsX.size()) +
+                       sizeof(int) * (maps.size() + fslot.size() + fpos.size() + fbld.size() + gjdim.size()) +
+                       sizeof(long long) * (ftab.size() + gjoff.size()) + sizeof(BoxRec) * recs.size());
         size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_fs = s.add(fslot),
                o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
                o_rec = s.add(recs);
