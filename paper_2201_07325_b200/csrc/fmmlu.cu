@@ -426,6 +426,9 @@ struct fmmlu_handle {
   DBuf root;       // n0 × n0 complex: X_t⁻¹
   DBuf root_rows;  // int n0
   DBuf root_fwd;   // n0 × n0 complex: A_{B_tB_t} for fmmlu_apply (built on first use)
+  // grow-only workspace slots reused by every phase / level of a factorization (borrowed, never
+  // freed per phase): 0/1 level block stores by level parity, 2 M, 3 Tb, 4 W, 5 Gram G|R
+  DBuf ws_slot[6];
   bool apply_ready = false;
   int64_t n0 = 0;
   fmmlu_stats_t stats{};
@@ -475,6 +478,18 @@ void wait_stream(fmmlu_handle* h, cudaStream_t st) {
   tl_pin.reset();
   auto it = tl_devarena.find(st);
   if (it != tl_devarena.end()) it->second.reset();
+}
+
+// dst ← a view of workspace slot `slot` of at least `bytes` (the slot grows by ≥ 25 % when short;
+// its old block is released stream-ordered, after the work that used it)
+void borrow_ws(fmmlu_handle* h, int slot, DBuf& dst, size_t bytes, cudaStream_t st) {
+  DBuf& w = h->ws_slot[slot];
+  if (!w.p || w.bytes < bytes) w.alloc(std::max(bytes, w.bytes + w.bytes / 4), st);
+  dst.release();
+  dst.p = w.p;
+  dst.bytes = bytes;
+  dst.st = st;
+  dst.borrowed = true;
 }
 
 void track(fmmlu_handle* h, long long delta) {
@@ -1065,7 +1080,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
       goff[j] = gsz;
       gsz += (long long)bcol[j] * bcol[j];
     }
-    G.alloc(2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
+    borrow_ws(h, 5, G, 2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
     FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
     std::vector<GemmProblem> gp;
     std::vector<GemmTile> gt;
@@ -1305,6 +1320,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   h->root_fwd.release();
   h->apply_ready = false;
   h->factored = false;
+  for (auto& w : h->ws_slot) w.release();
   fmmlu_stats_t& S = h->stats;
   std::memset(S.t_levels_ms, 0, sizeof(S.t_levels_ms));
   std::memset(S.ranks_sum, 0, sizeof(S.ranks_sum));
@@ -1388,7 +1404,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     }
     cur.size = off;
     lap(15);
-    cur.bsr.alloc((size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
+    borrow_ws(h, lvl & 1, cur.bsr, (size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
     track(h, cur.bsr.bytes);
 
     lap(0);
@@ -1539,8 +1555,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         bmax = std::max(bmax, J.b);
       }
       DBuf M, Tb, permd, kd;
-      M.alloc(wsM * sizeof(cplx), st);
-      Tb.alloc(wsT * sizeof(cplx), st);
+      borrow_ws(h, 2, M, std::max<long long>(wsM, 1) * sizeof(cplx), st);
+      borrow_ws(h, 3, Tb, std::max<long long>(wsT, 1) * sizeof(cplx), st);
       permd.alloc((size_t)permtot * sizeof(int), st);
       kd.alloc((size_t)nj * sizeof(int), st);
       track(h, M.bytes + Tb.bytes);
@@ -1781,7 +1797,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                   el.size(), ph.rmax, kmx, nnmx, hist[0], hist[1], hist[2], hist[3], hist[4], wsW * 16e-9,
                   facsz * 16e-9);
         }
-        W.alloc((size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
+        borrow_ws(h, 4, W, (size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
         ph.fac.alloc((size_t)std::max<long long>(facsz, 1) * sizeof(cplx), st);
         FMMLU_CUDA(cudaMemsetAsync(ph.fac.p, 0, ph.fac.bytes, st));
         ph.idx.alloc((size_t)std::max(idxsz, 1) * sizeof(int), st);
@@ -2244,6 +2260,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   }
   if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
   prev.bsr.release();
+  for (auto& w : h->ws_slot) w.release();  // factorization temporaries (stream-ordered)
   int hstatus = 0;
   FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   wait_stream(h, st);
@@ -3350,6 +3367,7 @@ int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const 
                timing);
   });
   if (h) {
+    for (auto& w : h->ws_slot) w.release();  // stream-ordered frees need the stream alive
     cudaStreamSynchronize(h->stream);
     if (h->own_stream) {
       drop_arena(h->own_stream);
@@ -3367,6 +3385,7 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->root.release();
   h->root_rows.release();
   h->root_fwd.release();
+  for (auto& w : h->ws_slot) w.release();
   h->geo.release();
   h->perm.release();
   if (h->stream) cudaStreamSynchronize(h->stream);
