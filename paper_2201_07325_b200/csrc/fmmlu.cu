@@ -124,7 +124,8 @@ struct BigCache {
     if (cap == 0) {
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      cap = tot / 10 * 6;
+      static const int pct = getenv("FMMLU_CACHE_PCT") ? atoi(getenv("FMMLU_CACHE_PCT")) : 60;
+      cap = tot / 100 * (size_t)std::max(0, std::min(95, pct));
     }
     free_.push_back({p, bytes, ev});
     held += bytes;
