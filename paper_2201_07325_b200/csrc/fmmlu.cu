@@ -430,6 +430,11 @@ struct fmmlu_handle {
   // grow-only workspace slots reused by every phase / level of a factorization (borrowed, never
   // freed per phase): 0/1 level block stores by level parity, 2 M, 3 Tb, 4 W, 5 Gram G|R
   DBuf ws_slot[6];
+  // factor-store arena: the per-phase stores are carved from uniform chunks owned by the handle, so
+  // successive factorizations reuse whole chunks from the big-block cache instead of growing the
+  // stream-ordered pool for every differently sized phase store
+  std::vector<DBuf> fac_chunks;
+  size_t fac_used = 0;  // bytes used in the last chunk
   bool apply_ready = false;
   int64_t n0 = 0;
   fmmlu_stats_t stats{};
@@ -491,6 +496,22 @@ void borrow_ws(fmmlu_handle* h, int slot, DBuf& dst, size_t bytes, cudaStream_t 
   dst.bytes = bytes;
   dst.st = st;
   dst.borrowed = true;
+}
+
+constexpr size_t kFacChunk = 512u << 20;
+void fac_alloc(fmmlu_handle* h, DBuf& dst, size_t bytes, cudaStream_t st) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (h->fac_chunks.empty() || h->fac_used + bytes > h->fac_chunks.back().bytes) {
+    h->fac_chunks.emplace_back();
+    h->fac_chunks.back().alloc(std::max(bytes, kFacChunk), st);
+    h->fac_used = 0;
+  }
+  dst.release();
+  dst.p = h->fac_chunks.back().as<char>() + h->fac_used;
+  dst.bytes = bytes;
+  dst.st = st;
+  dst.borrowed = true;
+  h->fac_used += bytes;
 }
 
 void track(fmmlu_handle* h, long long delta) {
@@ -1316,6 +1337,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   const int L = T.nlevels;
   const int n = (int)h->n;
   h->phases.clear();
+  h->fac_chunks.clear();
+  h->fac_used = 0;
   h->root.release();
   h->root_rows.release();
   h->root_fwd.release();
@@ -1799,7 +1822,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                   facsz * 16e-9);
         }
         borrow_ws(h, 4, W, (size_t)std::max<long long>(wsW, 1) * sizeof(cplx), st);
-        ph.fac.alloc((size_t)std::max<long long>(facsz, 1) * sizeof(cplx), st);
+        fac_alloc(h, ph.fac, (size_t)std::max<long long>(facsz, 1) * sizeof(cplx), st);
         FMMLU_CUDA(cudaMemsetAsync(ph.fac.p, 0, ph.fac.bytes, st));
         ph.idx.alloc((size_t)std::max(idxsz, 1) * sizeof(int), st);
         ph.fac_bytes = ph.fac.bytes + ph.idx.bytes;
@@ -3383,6 +3406,7 @@ int fmmlu_destroy(fmmlu_handle* h) {
   if (!h) return FMMLU_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->phases.clear();
+  h->fac_chunks.clear();
   h->root.release();
   h->root_rows.release();
   h->root_fwd.release();
