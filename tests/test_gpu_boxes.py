@@ -27,7 +27,7 @@ def _rho(h):
     return 1.5 * (math.sqrt(3.0) / 2.0) * h
 
 
-def _check_box(d, i, out, eps):
+def _check_box(d, i, out, eps, rel=None):
     o = ob.eliminate_box(K, eps, d["pts"][i], d["nrm"][i], d["npts"][i], d["nnrm"][i], d["w"], d["h"], n_gamma=NG)
     kg = int(out["ranks"][i])
     # pivot near-ties at the threshold may move the rank by one or two
@@ -39,7 +39,8 @@ def _check_box(d, i, out, eps):
         idx = np.array([pos[c] for c in o["perm"][:kg].tolist()] + list(range(kg, kg + d["npts"].shape[1])))
         D = D[np.ix_(idx, idx)]
         scale = np.abs(Do).max()
-        assert np.abs(D - Do).max() <= 10 * eps * scale + 1e-13
+        tol = 10 * eps if rel is None else rel
+        assert np.abs(D - Do).max() <= tol * scale + 1e-13
         return True
     return False
 
@@ -86,3 +87,19 @@ def test_boxes_errors(F):
     with pytest.raises(F.FmmluError) as e:
         F.boxes(d["pts"], d["nrm"], d["npts"], d["nnrm"], d["w"], K, 1e-6, 64, 0.2, keep=[3])
     assert e.value.code == -1
+
+
+def test_boxes_full_size_sampled_parity(F):
+    """BASELINE configs[3] at full size (8192 boxes, ε = 1e-6, the launch configuration of
+    tools/cfg4_bench.py): Δ of sampled boxes against the oracle, ranks of all boxes in range."""
+    nbox, eps = 8192, 1e-6
+    d = fi.box_batch(nbox, first_id=0)
+    sample = [0, 4095, 8191]
+    out = F.boxes(d["pts"], d["nrm"], d["npts"], d["nnrm"], d["w"], K, eps, NG, _rho(d["h"]), keep=sample,
+                  want_perm=True)
+    assert out["ranks"].shape == (nbox,)
+    assert out["ranks"].min() > 0 and out["ranks"].max() <= 256
+    # Gram-path T (+ one corrected-seminormal step, reading R4) moves Δ by up to ≈ 2e-5 relative on the
+    # worst-conditioned skeletons at ε = 1e-6 (measured on one sampled box); the solution parity of the tree
+    # path is unaffected (E/F are exact transforms for any T with a small ID residual)
+    assert sum(_check_box(d, i, out, eps, rel=1e-4) for i in sample) >= 2
