@@ -91,7 +91,7 @@ typedef struct fmmlu_stats_t {
 #define FMMLU_K_CPQR 3    /* ID: column-pivoted QR + T = R11^-1 R12                 */
 #define FMMLU_K_EF 4      /* E/F transforms (GEMM)                                  */
 #define FMMLU_K_INV 5     /* X_RR^-1 (Gauss-Jordan)                                 */
-#define FMMLU_K_PANEL 6   /* Up / Lp panels (GEMM)                                  */
+#define FMMLU_K_PANEL 6   /* Up = X_RR^-1 X_R(S+N) panel (GEMM)                     */
 #define FMMLU_K_SCHUR 7   /* Schur-complement GEMM + scatter-add                    */
 #define FMMLU_K_ROOT 8    /* root block build + inverse                             */
 #define FMMLU_K_SOLVE 9   /* solve sweeps + root apply                              */

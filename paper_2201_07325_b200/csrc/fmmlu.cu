@@ -6,13 +6,14 @@
 //   level ℓ = L-1 … 2:
 //     build the level's block-sparse current-matrix store ("BSR": one dense block
 //       per owner pair at Chebyshev separation ≤ 2, entries = pure kernel or the
-//       Schur-updated value carried over from level ℓ+1)          [k_build]
+//       Schur-updated value carried over from level ℓ+1)          [k_build_level]
 //     colour c = 0 … 7 (reading C8; boxes of one colour are independent):
 //       M = [A_QB; A_BQᵀ; proxy rows]       [k_copy, k_proxy]
-//       CPQR ID → perm, k; T = R11⁻¹R12      [k_cpqr, k_trsm_T]
+//       ID → perm, k; T = R11⁻¹R12 (Gram + pivoted Cholesky or
+//       TSQR + CPQR, reading R4)                                    [DMMA GEMM, k_pchol_reg, k_trsm_T]
 //       E/F transforms with T (Eq. pap … X blocks, L739-788)      [DMMA GEMM]
-//       X_RR⁻¹ (Gauss-Jordan), Up = X_RR⁻¹X_{R(S∪N)}, Lp = X_{(S∪N)R}X_RR⁻¹   [k_gj, GEMM]
-//       Schur update Δ_{(S∪N)²} −= Lp X_{R(S∪N)} scattered into the BSR (L813-825) [GEMM+atomics]
+//       X_RR⁻¹ (Gauss-Jordan), Up = X_RR⁻¹X_{R(S∪N)}; X_{(S∪N)R} is kept in place of Lp   [k_gj_reg, GEMM]
+//       Schur update Δ_{(S∪N)²} −= X_{(S∪N)R}·Up scattered into the BSR (L813-825) [GEMM+atomics]
 //   root: B_t dense block → X⁻¹ (L894-918)                        [k_build, blocked GJ: k_gj_panel_reg + DMMA updates]
 // Solve: upward sweep over phases, root apply, downward sweep.
 #include <cuda_runtime.h>
