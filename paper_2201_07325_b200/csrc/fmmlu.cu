@@ -380,6 +380,18 @@ struct Prof {
     launches[cls] += nl;
     total_launches += nl;
   }
+  size_t mark() const { return pending.size(); }
+  // resolve the first n records (completed: the stream was synchronised after they were recorded)
+  // while later ones are still in flight; their events stay checked out until the next full resolve
+  void resolve_first(size_t n) {
+    n = std::min(n, pending.size());
+    for (size_t i = 0; i < n; ++i) {
+      float t = 0.f;
+      FMMLU_CUDA(cudaEventElapsedTime(&t, pending[i].a, pending[i].b));
+      ms[pending[i].cls] += t;
+    }
+    pending.erase(pending.begin(), pending.begin() + n);
+  }
   void resolve() {  // call after the stream has been synchronised
     for (auto& r : pending) {
       float t = 0.f;
@@ -1738,9 +1750,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         for (int c = 0; c < 10; ++c)
           if (h->prof.ms[c] - before[c] > 0.005) fprintf(stderr, " %s %.3f", nm[c], h->prof.ms[c] - before[c]);
         fprintf(stderr, "\n");
-      } else {
-        h->prof.resolve();
       }
+      // the completed events are read out after the elimination is launched (off the idle gap)
+      const size_t prof_done = trace ? 0 : h->prof.mark();
       // the ID temporaries and M are freed at the end of the phase, after the elimination is
       // launched: the device is idle from here until the first elimination kernel
       std::vector<DBuf> idkeep;
@@ -2168,6 +2180,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         W.release();
         h->phases.push_back(std::move(ph));
       }
+      if (prof_done) h->prof.resolve_first(prof_done);
       lap(4);
       // update current actives: B keeps its skeleton S (sorted)
       for (int j = 0; j < nj; ++j) {
