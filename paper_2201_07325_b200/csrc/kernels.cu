@@ -274,7 +274,6 @@ __global__ void __launch_bounds__(256) k_proxy(const ProxyTask* __restrict__ tas
   }
 }
 
-constexpr int QR_NT = 512;
 
 // T = R11⁻¹ R12, warp per column, back substitution.
 // grid (ntasks, ceil(bmax / 16)), 16 warps: one redundant column per warp, x staged in shared memory.
@@ -349,8 +348,6 @@ constexpr int GJR_NCAP = 512;
 __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ tasks, int j0, int nb,
                                                      int* status) {
   extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
   __shared__ cplx rowj[64];
   const GjTask t = tasks[blockIdx.x];
   const int n = t.n;
@@ -1140,8 +1137,6 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ double shm[];
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
   __shared__ double cand_v[2], cres_v;  // candidates double-buffered by step parity: one
   __shared__ int cand_i[2], cres_i;     // cluster barrier per step suffices
 
@@ -1545,7 +1540,6 @@ constexpr int SV_NT = 256;
 constexpr int SV_Q = 4;  // RHS processed per pass
 constexpr int SV_U = 8;  // factor loads in flight per thread in the solve products
 
-constexpr int SV_FCH = 1024;  // S∪N entries staged per chunk in the downward sweep
 // ---- split solve kernels (more CTAs per box; the factor store is streamed once)
 // y_{S∪N} += sg · X_{(S∪N)R} z for one item (kSolveChunk rows; z = X_RR⁻¹ t = y_R after the D⁻¹
 // kernel, so the product equals Lp t of PAPER.md L920-924); SB_P threads per row split the
