@@ -78,17 +78,18 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+    def summary(self, first: int = 0):
+        rows = self.rows[first:] if len(self.rows) > first else self.rows  # samples of the timed region
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, nm in enumerate(names):
                 if len(r) > 4 + i and r[4 + i].lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(rows)}
 
 
 # ncu --set full summaries committed under profiles/ (tools/ncu_summary.py full): DRAM traffic
@@ -249,6 +250,9 @@ def main():
         h.solve(x_p, nrhs=nrhs)  # H2D of the rhs and D2H of the result inside the call
         return h, x_p.numpy().T
 
+    # the clock sampler (an nvidia-smi process) starts before the warm-up, so its start-up does not
+    # compete with the host side of the first timed step; only the timed region's samples are reported
+    clk = Clocks(torch.cuda.current_device()).__enter__()
     for _ in range(args.warmup):
         h = step_device()
     torch.cuda.synchronize()
@@ -259,7 +263,8 @@ def main():
     # ---- device-timed leg (CUDA events on the launch stream, L2 flushed between steps)
     ev = []
     stats = []
-    with Clocks(torch.cuda.current_device()) as clk:
+    clk_first = len(clk.rows)
+    try:
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -276,6 +281,8 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
+    finally:
+        clk.__exit__(None, None, None)
     dev_detail = [[round(s_["t_tree_ms"], 1), round(s_["t_factor_ms"], 1), round(s_["t_sync_wait_ms"], 1),
                    round(s_["t_solve_ms"], 1)] for s_ in stats]
     ms = [a.elapsed_time(b) for a, b in ev]
@@ -395,7 +402,7 @@ def main():
         "device_lib_tree_factor_wait_solve_ms": dev_detail,
         "roofline": roof,
         "kernel_breakdown": breakdown,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(clk_first),
         "cpu_baseline": cpu,
         "paper_context": {"note": "PAPER.md Table 2 (L2512), MATLAB on 1 CPU core, quadrature-corrected wiggly "
                                   "torus at eps 5e-7: a different matrix and machine, context only",
