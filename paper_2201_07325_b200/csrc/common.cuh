@@ -36,6 +36,7 @@ __host__ __device__ __forceinline__ cplx cmulc(cplx a, cplx b) {
   return cmk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
 __host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cmk(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return cmk(a.x, -a.y); }
 __host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
 __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   // Smith-free straightforward division (b well away from 0/inf in our use)

@@ -1150,7 +1150,9 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
       add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
     }
     run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
-    {
+    // the register pivoted Cholesky reads the lower triangle from the upper one itself
+    const bool reg_pchol = h->id_mode != 3 && h->pchol_mode == 0 && pchol_reg_scratch(bmax) > 0;
+    if (!reg_pchol) {
       std::vector<cplx*> gptr(nj);
       for (int j = 0; j < nj; ++j) gptr[j] = G.as<cplx>() + goff[j];
       Stage sm;
@@ -1171,7 +1173,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     s2.upload(st);
     int cid = h->prof.begin(FMMLU_K_CPQR, st);
     if (h->id_mode != 3) {
-      if (h->pchol_mode == 0 && pchol_reg_scratch(bmax) > 0) {  // register-resident pivoted Cholesky
+      if (reg_pchol) {  // register-resident pivoted Cholesky
         DBuf xs;
         xs.alloc((size_t)nj * pchol_reg_scratch(bmax) * sizeof(cplx), st);
         done_id = launch_pchol_reg(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, xs.as<cplx>(), st, bmax);

@@ -1286,7 +1286,11 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int i = row0 + 32 * r;
-      a[q][r] = (q < nq && i < b) ? t.A[i + (size_t)(rank + ((cgp + CG * q) << lgCL)) * t.lda] : cmk(0.0, 0.0);
+      const int g = rank + ((cgp + CG * q) << lgCL);
+      // G = MᴴM is Hermitian and only its upper triangle is computed: S_ig = conj(G_gi) below it
+      a[q][r] = (q < nq && i < b)
+                    ? (i <= g ? t.A[i + (size_t)g * t.lda] : cconj(t.A[g + (size_t)i * t.lda]))
+                    : cmk(0.0, 0.0);
     }
   for (int l = tid; l < ncl; l += GJR_NT) {
     const int g = rank + (l << lgCL);
