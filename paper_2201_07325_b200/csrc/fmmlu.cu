@@ -204,9 +204,14 @@ struct DBuf {
     cudaError_t e = cudaSuccess;
     if (b >= kBigBlock) {
       size_t got = 0;
-      p = big_cache().take(b, s, &got);
+      // big blocks are quantised to 8 sizes per octave, so requests that differ slightly between
+      // factorizations (a rank off by one) still map to the same cached block instead of growing the pool
+      size_t q = size_t(1) << (63 - __builtin_clzll((unsigned long long)b));
+      const size_t step = std::max<size_t>(q / 8, 1u << 20);
+      const size_t bq = (b + step - 1) / step * step;
+      p = big_cache().take(bq, s, &got);
       if (!p) {
-        got = (b + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+        got = bq;
         e = cudaMallocAsync(&p, got, s);
         if (e != cudaSuccess) {  // give the cached blocks back and retry once
           cudaGetLastError();
