@@ -397,7 +397,8 @@ def main():
                 "lib_tree_factor_wait_solve_ms": e2e_detail,
                 "host_buffers": "pinned",
                 "timing": "host wall clock around tree+factor+solve incl. H2D/D2H, mean of K steps"},
-        "gpu_launches": int(st["n_launches"]),
+        "gpu_launches": int(sum(s_["n_launches"] for s_ in stats)),  # all K timed steps
+        "gpu_launches_per_step": int(st["n_launches"]),
         "device_ms_steps": [round(v, 2) for v in ms],
         "device_lib_tree_factor_wait_solve_ms": dev_detail,
         "roofline": roof,

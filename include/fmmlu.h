@@ -73,7 +73,7 @@ typedef struct fmmlu_stats_t {
   int32_t n_singular_warn;/* near-singular pivot warnings                         */
   int32_t ranks_sum[24];  /* Σ|S| per level                                       */
   int32_t boxes[24];      /* skeletonized boxes per level                         */
-  int64_t n_launches;     /* kernels launched by the last factor + solve          */
+  int64_t n_launches;     /* kernels launched by the last tree + factor + solve   */
   /* Per kernel class (FMMLU_K_* below), accumulated over the last factor and the
    * last solve: device time from CUDA events recorded on the launch stream, and the
    * ALGORITHMIC real flops / bytes of the launches in that class.                 */

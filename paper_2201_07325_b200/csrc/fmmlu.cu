@@ -454,6 +454,7 @@ struct fmmlu_handle {
   std::vector<DBuf> fac_chunks;
   size_t fac_used = 0;  // bytes used in the last chunk
   bool apply_ready = false;
+  int tree_launches = 0;  // kernels of the last fmmlu_tree (scan, keys, 9 radix-sort passes, gather)
   int64_t n0 = 0;
   fmmlu_stats_t stats{};
   size_t cur_bytes = 0, peak_bytes = 0;
@@ -3192,6 +3193,7 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     FMMLU_CUDA(cudaMemcpyAsync(hq.data(), q_out, 3 * (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, st));
     FMMLU_CUDA(cudaStreamSynchronize(st));
     h->tree.build_sorted(hq.data(), hperm.data(), lo, side, n, leaf_max);
+    h->tree_launches = 3 + 9;  // k_tree_scan/keys/gather + CUB onesweep radix sort (histogram + 8 passes)
     double* gp = h->geo.as<double>();
     h->g = Geo{gp, gp + n, gp + 2 * n, gp + 3 * n, gp + 4 * n, gp + 5 * n, gp + 6 * n};
     track(h, h->geo.bytes + h->perm.bytes);
@@ -3449,7 +3451,7 @@ int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out) {
   if (!h || !out) return fail(FMMLU_EINVAL, "NULL argument");
   *out = h->stats;
   out->peak_bytes = (int64_t)h->peak_bytes;
-  out->n_launches = h->prof.total_launches;
+  out->n_launches = h->prof.total_launches + h->tree_launches;
   for (int i = 0; i < 16; ++i) {
     out->class_ms[i] = h->prof.ms[i];
     out->class_flops[i] = h->prof.flops[i];
