@@ -657,23 +657,58 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_panel_reg(const GjTask* __rest
 
 // Apply the panel's interchanges to every column outside J and gather their rows J into Y
 // (jb × n, ld nb).  grid (ceil(n/128), ntasks).
-__global__ void k_gj_swap(const GjTask* __restrict__ tasks, int j0, int nb) {
+// The panel's row interchanges composed into one permutation σ of the ≤ 2·jb affected rows (one thread,
+// O(jb) steps over a shared-memory map), then applied to every column outside the panel as a parallel
+// gather (read all affected values, barrier, write) — instead of jb dependent swaps per column thread.
+// Also gathers rows J of those columns into Y (jb × n, ld nb).  grid (ceil(n/GS_C), ntasks).
+constexpr int GS_C = 32, GS_NT = 256;
+__global__ void __launch_bounds__(GS_NT) k_gj_swap(const GjTask* __restrict__ tasks, int j0, int nb) {
+  extern __shared__ int gs_sh[];
   const GjTask t = tasks[blockIdx.y];
   const int n = t.n;
   if (j0 >= n) return;
   const int jb = min(nb, n - j0);
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n || (c >= j0 && c < j0 + jb)) return;
-  cplx* col = t.A + (size_t)c * t.lda;
-  for (int s = 0; s < jb; ++s) {
-    const int j = j0 + s, p = t.piv[j];
-    if (p != j) {
-      cplx a = col[j];
-      col[j] = col[p];
-      col[p] = a;
+  int* mp = gs_sh;                                    // [n] row → source row (affected rows only)
+  int* rows = mp + n;                                 // [2 nb] affected rows
+  __shared__ int nr_s;
+  cplx* vals = reinterpret_cast<cplx*>(gs_sh + ((n + 2 * nb + 3) & ~3));  // [GS_C][2 nb], 16-B aligned
+  if (threadIdx.x == 0) {
+    int nr = 0;
+    for (int s = 0; s < jb; ++s) {
+      const int j = j0 + s, p = t.piv[j];
+      mp[j] = -1;
+      mp[p] = -1;
+    }
+    for (int s = 0; s < jb; ++s) {
+      const int j = j0 + s, p = t.piv[j];
+      if (mp[j] < 0) { mp[j] = j; rows[nr++] = j; }
+      if (mp[p] < 0) { mp[p] = p; rows[nr++] = p; }
+    }
+    for (int s = 0; s < jb; ++s) {  // row j ↔ row p, in order: mp[r] = original row now in r
+      const int j = j0 + s, p = t.piv[j];
+      const int a = mp[j];
+      mp[j] = mp[p];
+      mp[p] = a;
+    }
+    nr_s = nr;
+  }
+  __syncthreads();
+  const int nr = nr_s;
+  const int c0 = blockIdx.x * GS_C;
+  for (int e = threadIdx.x; e < GS_C * nr; e += GS_NT) {
+    const int k = e % nr, cl = e / nr, c = c0 + cl;
+    if (c < n && !(c >= j0 && c < j0 + jb)) vals[cl * 2 * nb + k] = t.A[mp[rows[k]] + (size_t)c * t.lda];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < GS_C * nr; e += GS_NT) {
+    const int k = e % nr, cl = e / nr, c = c0 + cl;
+    if (c < n && !(c >= j0 && c < j0 + jb)) {
+      const int r = rows[k];
+      const cplx v = vals[cl * 2 * nb + k];
+      t.A[r + (size_t)c * t.lda] = v;
+      if (r >= j0 && r < j0 + jb) t.Y[(r - j0) + (size_t)c * nb] = v;
     }
   }
-  for (int s = 0; s < jb; ++s) t.Y[s + (size_t)c * nb] = col[j0 + s];
 }
 
 // Undo the column interchanges: column c of the inverse = column L[c], L = swaps in reverse.
@@ -2132,8 +2167,14 @@ void launch_gj_panel_cluster(const GjTask* d_tasks, int ntasks, int j0, int nb, 
 
 void launch_gj_swap(const GjTask* d_tasks, int ntasks, int j0, int nb, cudaStream_t st, int nmax) {
   if (ntasks <= 0) return;
-  dim3 grid((nmax + 127) / 128, ntasks);
-  k_gj_swap<<<grid, 128, 0, st>>>(d_tasks, j0, nb);
+  const size_t smem = (size_t)((nmax + 2 * nb + 3) & ~3) * sizeof(int) + (size_t)GS_C * 2 * nb * sizeof(cplx) + 16;
+  static size_t cur = 0;
+  if (smem > 48 * 1024 && smem > cur) {
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gj_swap, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  dim3 grid((nmax + GS_C - 1) / GS_C, ntasks);
+  k_gj_swap<<<grid, GS_NT, smem, st>>>(d_tasks, j0, nb);
   FMMLU_LAUNCH();
 }
 
