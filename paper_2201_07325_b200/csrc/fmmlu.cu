@@ -146,6 +146,22 @@ BigCache& big_cache() {
   return *c;
 }
 
+// Last resort of a failed allocation: the pool keeps every freed byte reserved (release threshold
+// = max, set at handle creation), and after several factorizations with different block sizes that
+// reservation is fragmented, so one large request can fail with enough memory idle.  Wait for the
+// stream, hand the idle reservation back to the driver and retry once.
+cudaError_t retry_trimmed(void** p, size_t bytes, cudaStream_t s) {
+  cudaGetLastError();
+  cudaStreamSynchronize(s);
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  if (e != cudaSuccess) cudaGetLastError();
+  return e;
+}
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -218,11 +234,16 @@ struct DBuf {
           big_cache().flush(s);
           e = cudaMallocAsync(&p, got, s);
         }
+        if (e != cudaSuccess) e = retry_trimmed(&p, got, s);
       }
       big = e == cudaSuccess;
       cap = got;
     } else {
       e = cudaMallocAsync(&p, b, s);
+      if (e != cudaSuccess) {
+        big_cache().flush(s);
+        e = retry_trimmed(&p, b, s);
+      }
     }
     const double dt = wall_ms() - t0;
     g_ac.alloc_ms += dt;
