@@ -1,9 +1,11 @@
 """bench.py — FMM-LU hot path on B200 (BASELINE.json metric: factor unknowns/s and solve
 ms/RHS at ε = 1e-6, complex128, 1 B200).
 
-Workload (N=1): BASELINE.json configs[1] = "cfg2": ellipsoid (0.5, 1, 2), n = 20,000,
-k = 2π, leaf ≤ 64, ε = 1e-6, 4 Gaussian RHS (seed 0).  One STEP = the whole hot path
-(every SURVEY §8(a) row): fmmlu_tree + fmmlu_factor + fmmlu_solve through the C ABI.
+Workload (N=1): BASELINE.json configs[4] = "cfg5", the largest single-GPU configuration:
+wavy torus (2000×500 grid), n = 10⁶, k = 10, leaf ≤ 64, ε = 1e-6, 32 Gaussian RHS (seed 0).
+One STEP = the whole hot path (every SURVEY §8(a) row): fmmlu_tree + fmmlu_factor +
+fmmlu_solve through the C ABI.  Extra keys (not the headline): cfg2 (configs[1]) device-timed
+steps, and cfg4 (configs[3], 8192 independent boxes) boxes/s at ε ∈ {1e-4, 1e-6, 1e-9}.
 value = unknowns processed per second of step time (tree + factor + solve), summed over
 ranks ("replicas only"); factor-only unknowns/s and solve ms/RHS are extra keys.
 
@@ -32,8 +34,9 @@ import fmmlu_inputs as fi  # noqa: E402
 
 METRIC = "FMM-LU factor unknowns/s and solve ms/RHS at eps=1e-6 (complex128, 1 B200)"
 UNIT = "unknowns/s"
-CFG = "cfg2"
-ORACLE_SAMPLE_N = 4000  # bounded CPU sample (same geometry family / k / leaf / eps)
+CFG = "cfg5"
+# bounded CPU sample for the oracle arm: the cfg5 wavy torus on a coarser grid (same k, leaf, eps)
+ORACLE_GRID = (120, 40)
 
 
 def _peaks():
@@ -140,35 +143,50 @@ def dist_env():
     return rank, world, local
 
 
+def oracle_sample():
+    """The cfg5-family sample the CPU oracle is timed on: the same wavy torus recipe, k, leaf,
+    ε and 32 RHS on a coarser grid (block-mode oracle), ≈ 10–30 s of host work."""
+    c = fi.CONFIGS[CFG]
+    g = fi.wavy_torus(*ORACLE_GRID)
+    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    return c, g, b
+
+
+def oracle_step(c, g, b):
+    from oracle import rss
+    t0 = time.perf_counter()
+    f = rss.factor(g.points, g.normals, g.weights, c["k"], c["eps"], c["leaf_max"], mode="block")
+    rss.solve(f, b)
+    return time.perf_counter() - t0
+
+
+def _sample_desc(g, c):
+    return (f"oracle (NumPy/SciPy, untuned, block mode) tree+factor+solve of the {CFG} wavy torus recipe on a "
+            f"{ORACLE_GRID[0]}x{ORACLE_GRID[1]} grid (n={g.n}; full {CFG} is n=10^6), k={c['k']:g}, "
+            f"leaf {c['leaf_max']}, eps {c['eps']:g}, {c['nrhs']} RHS")
+
+
 def run_reference(args):
     """CPU oracle arm (test-infrastructure oracle, untuned) on a bounded sample."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import rss
-    c = fi.CONFIGS[CFG]
-    g = fi.ellipsoid(ORACLE_SAMPLE_N)
-    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    c, g, b = oracle_sample()
     times = []
     for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        f = rss.factor(g.points, g.normals, g.weights, c["k"], c["eps"], c["leaf_max"])
-        rss.solve(f, b)
-        dt = time.perf_counter() - t0
+        dt = oracle_step(c, g, b)
         if it >= args.warmup:
             times.append(dt)
     t = float(np.mean(times))
-    cores = os.cpu_count()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     value = g.n / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"{CFG} family sample: ellipsoid n={g.n}, k=2pi, leaf 64, eps 1e-6, 4 RHS",
-                   "sample_of": CFG},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"oracle tree+factor+solve of the cfg2-family ellipsoid at n={g.n} "
-                                   f"(full cfg2 n=20000 takes ~200 s on 8 cores)"},
+        "config": {"workload": f"{CFG} family sample: wavy torus n={g.n}, k={c['k']:g}, leaf {c['leaf_max']}, "
+                               f"eps {c['eps']:g}, {c['nrhs']} RHS", "sample_of": CFG},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": _sample_desc(g, c)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -176,17 +194,65 @@ def run_reference(args):
 
 
 def cpu_baseline_sample():
-    from oracle import rss
-    c = fi.CONFIGS[CFG]
-    g = fi.ellipsoid(ORACLE_SAMPLE_N)
-    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
-    t0 = time.perf_counter()
-    f = rss.factor(g.points, g.normals, g.weights, c["k"], c["eps"], c["leaf_max"])
-    rss.solve(f, b)
-    dt = time.perf_counter() - t0
-    return {"value": g.n / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"oracle (NumPy/SciPy, untuned) tree+factor+solve of the cfg2-family ellipsoid at "
-                      f"n={g.n} ({dt:.1f} s); full cfg2 is ~200 s on 8 cores"}
+    c, g, b = oracle_sample()
+    dt = oracle_step(c, g, b)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": g.n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": _sample_desc(g, c) + f" ({dt:.1f} s)"}
+
+
+def bench_cfg2(F, dev, stream, flush, steps: int = 5, warmup: int = 2):
+    """Extra key: BASELINE configs[1] (ellipsoid, n = 2·10⁴, 4 RHS), the same step, device-timed."""
+    import torch
+    c = fi.CONFIGS["cfg2"]
+    g = fi.config_geometry("cfg2")
+    b = np.asfortranarray(fi.gaussian_rhs(g.n, c["nrhs"], 0))
+    P, N, W = (torch.from_numpy(a).to(dev) for a in (g.points, g.normals, g.weights))
+    B = torch.from_numpy(np.ascontiguousarray(b.T)).to(dev)
+    X = torch.empty_like(B)
+    ms, fac, sol = [], [], []
+    h = None
+    for it in range(warmup + steps):
+        if h is not None:
+            h.close()
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h = F.FmmLu(P, N, W, c["leaf_max"])
+        h.set_stream(stream.cuda_stream)
+        h.factor(c["k"], c["eps"])
+        X.copy_(B)
+        h.solve(X, nrhs=c["nrhs"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it >= warmup:
+            st = h.stats()
+            ms.append(e0.elapsed_time(e1))
+            fac.append(st["t_factor_ms"])
+            sol.append(st["t_solve_ms"])
+    h.close()
+    t = float(np.mean(ms))
+    return {"workload": f"cfg2 (BASELINE configs[1]): ellipsoid (0.5,1,2) n={g.n}, k=2pi, leaf 64, eps 1e-6, "
+                        f"{c['nrhs']} RHS", "unknowns_per_s": g.n / (t * 1e-3), "ms_per_step": t,
+            "factor_unknowns_per_s": g.n / (float(np.mean(fac)) * 1e-3),
+            "solve_ms_per_rhs": float(np.mean(sol)) / c["nrhs"], "steps": steps,
+            "device_ms_steps": [round(v, 2) for v in ms]}
+
+
+def bench_cfg4(F):
+    """Extra key: BASELINE configs[3] (8192 independent boxes, b = 256, 1024 near, 512 proxy
+    points, k = 10): batched ID + elimination, boxes/s at each ε (one warm-up + one timed run;
+    device time measured inside fmmlu_boxes with CUDA events)."""
+    d = fi.box_batch(8192)
+    rho = 1.5 * math.sqrt(3) / 2 * d["h"]
+    out = {"workload": "cfg4 (BASELINE configs[3]): 8192 boxes, b=256, 1024 near DOFs, 512 proxy points, k=10"}
+    for eps in (1e-4, 1e-6, 1e-9):
+        F.boxes(d["pts"], d["nrm"], d["npts"], d["nnrm"], d["w"], 10.0, eps, 512, rho, want_perm=False)
+        r = F.boxes(d["pts"], d["nrm"], d["npts"], d["nnrm"], d["w"], 10.0, eps, 512, rho, want_perm=False)
+        out[f"eps={eps:g}"] = {"ms": r["ms"], "boxes_per_s": 8192 / (r["ms"] * 1e-3),
+                               "model_gflop": r["gflop"], "model_tflops": r["gflop"] / r["ms"],
+                               "mean_rank": float(r["ranks"].mean())}
+    return out
 
 
 def main():
@@ -196,6 +262,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg2 / cfg4 extra keys")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -253,7 +320,10 @@ def main():
     # the clock sampler (an nvidia-smi process) starts before the warm-up, so its start-up does not
     # compete with the host side of the first timed step; only the timed region's samples are reported
     clk = Clocks(torch.cuda.current_device()).__enter__()
+    h = None
     for _ in range(args.warmup):
+        if h is not None:
+            h.close()  # one handle alive at a time (a cfg5 factorization holds ≈ 45 GB of factors)
         h = step_device()
     torch.cuda.synchronize()
     import gc
@@ -313,7 +383,8 @@ def main():
     e2e_detail = []  # per step: library-reported tree / factor / factor-wait / solve ms
     resid = None
     for _ in range(2):  # untimed warm-up of the host-buffer path (first calls pay one-time setup)
-        step_e2e()
+        hw, _x = step_e2e()
+        hw.close()
     h2 = None
     for _ in range(args.steps):
         if h2 is not None:
@@ -330,6 +401,7 @@ def main():
     x = np.asfortranarray(x)
     Ax = h2.matvec(c["k"], x)
     resid = float(np.max(np.linalg.norm(Ax - b_host, axis=0) / np.linalg.norm(b_host, axis=0)))
+    h2.close()
     t_e2e = max_over_ranks(float(np.mean(e2e_ms)), world, dev)
 
     # ---- roofline of the dominant kernel class (events recorded inside libfmmlu)
@@ -370,6 +442,11 @@ def main():
                  for i in range(len(cls))}
 
 
+    extras = {}
+    if not args.no_extras:
+        extras["cfg2"] = bench_cfg2(F, dev, stream, flush)
+        extras["cfg4"] = bench_cfg4(F)
+
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -383,7 +460,8 @@ def main():
         "metric": METRIC, "value": job_throughput(n, world, t_step), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"{CFG}: ellipsoid (0.5,1,2) n={n}, k=2pi, leaf 64, eps 1e-6, {nrhs} RHS",
+        "config": {"workload": f"{CFG} (BASELINE configs[4]): wavy torus 2000x500 grid n={n}, k={c['k']:g}, "
+                               f"leaf {c['leaf_max']}, eps {c['eps']:g}, {nrhs} RHS",
                    "step": "fmmlu_tree + fmmlu_factor + fmmlu_solve (device-resident inputs)",
                    "parallelism": f"replicas x{world}", "l2": "flushed (256 MB write) between steps"},
         "factor_unknowns_per_s": n / (t_fac * 1e-3),
@@ -405,6 +483,7 @@ def main():
         "kernel_breakdown": breakdown,
         "clocks": clk.summary(clk_first),
         "cpu_baseline": cpu,
+        "extra_configs": extras,
         "paper_context": {"note": "PAPER.md Table 2 (L2512), MATLAB on 1 CPU core, quadrature-corrected wiggly "
                                   "torus at eps 5e-7: a different matrix and machine, context only",
                           "n": 1075200, "t_f_s": 9756.3, "factor_unknowns_per_s": 110, "t_s_s": 12.1},

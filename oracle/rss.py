@@ -24,9 +24,17 @@ Follows, step by step and in the paper's notation:
 * Reading C1: the √w-scaled matrix Ã = W^{½} A W^{-½} is factorized;
   solve returns x = W^{-½} Ã⁻¹ (W^{½} b) in the caller's ordering.
 
-State is DENSE mode: the whole current Ã is one n×n complex128
-array; Q/N/B blocks are slices, E/F/Schur writes go in place on (S∪N)², R
-rows/columns are never read again.  Suitable for n ≤ ~20,000.
+State, two interchangeable modes that hold the same current matrix:
+* DENSE mode: the whole current Ã is one n×n complex128 array; Q/N/B blocks are
+  slices, the Schur writes go in place on (S∪N)², R rows/columns are never read
+  again.  The most literal transcription; n ≤ ~20,000.
+* BLOCK mode: current entry = pure kernel (regenerated) + Δ, Δ a dict keyed by
+  owner pair (``BlockState``).  Any n (cfg3 in minutes).  Pinned to dense mode:
+  identical skeletons and solutions on the small ladder (tests/test_oracle_block.py).
+Order self-checks (reading C8): ``order="colour_reversed"``
+reverses the order inside each colour and must reproduce the colour-major result
+up to summation order; ``order="sequential"`` is the plain one-box-at-a-time
+sweep and must give an equally accurate factorization.
 
 Pins (tests/test_oracle_rss.py): n ≤ leaf_max → exactly a dense LU solve;
 dense-literal check that the stored factors of each box applied to the whole
@@ -73,44 +81,188 @@ class Factorization:
     A_t: np.ndarray = None  # A_{B_t B_t} (root block of D)
 
 
-def _gen(A, rows, cols):
-    return A[np.ix_(rows, cols)]
+class DenseState:
+    """Dense mode: the whole current Ã as one n×n complex128 array; Q/N/B
+    blocks are slices, the Schur update writes in place on (S∪N)²."""
+
+    def __init__(self, k, X, NX, sw, A_init=None):
+        self.A = kern.dense_scaled(k, X, NX, sw) if A_init is None else A_init.copy()
+
+    def get(self, rows, cols):
+        return self.A[np.ix_(rows, cols)]
+
+    def add(self, rows, cols, V):
+        self.A[np.ix_(rows, cols)] += V
+
+    def begin_level(self, owners, active, parent_of):
+        pass
+
+    def end_phase(self, eliminated):
+        pass
+
+
+class BlockState:
+    """Block mode: current entry = pure kernel (regenerated) + Δ, with Δ a dict
+    (owner a, owner b) → complex128[|act_a|, |act_b|] present only for pairs that were ever
+    updated.  The same matrix as DenseState entry by entry (the Schur complement is the only
+    writer), at memory O(Σ updated blocks) instead of n².
+
+    * ``owner[g]``, ``pos[g]``: the level-ℓ owner of active DOF g and its position in the
+      owner's sorted actives (reading C11); Δ blocks are indexed by those positions.
+    * ``end_phase``: after a colour phase, each eliminated box's blocks are restricted to its
+      skeleton rows/columns (its R DOFs are inactive).  Restriction waits
+      for the end of the phase so that same-colour boxes still read their pre-phase Q rows
+      (the snapshot rule of reading C8).
+    * ``begin_level``: each parent-pair block is gathered from its child-pair blocks,
+      positioned into the parent's sorted actives; coarse-leaf owners
+      carry over unchanged (reading C7)."""
+
+    def __init__(self, k, X, NX, sw, n):
+        self.k, self.X, self.NX, self.sw = k, X, NX, sw
+        self.owner = np.full(n, -1, dtype=np.int64)
+        self.pos = np.full(n, -1, dtype=np.int64)
+        self.act = {}
+        self.D = {}
+
+    def _groups(self, idx):
+        own = self.owner[idx]
+        out = []
+        for o in np.unique(own):
+            sel = np.nonzero(own == o)[0]
+            out.append((int(o), sel, self.pos[idx[sel]]))
+        return out
+
+    def get(self, rows, cols):
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        out = kern.scaled_block(self.k, self.X, self.NX, self.sw, rows, cols)
+        if rows.size == 0 or cols.size == 0:
+            return out
+        gc = self._groups(cols)
+        for a, ri, pa in self._groups(rows):
+            for b, cj, pb in gc:
+                d = self.D.get((a, b))
+                if d is not None:
+                    out[np.ix_(ri, cj)] += d[np.ix_(pa, pb)]
+        return out
+
+    def add(self, rows, cols, V):
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        gc = self._groups(cols)
+        for a, ri, pa in self._groups(rows):
+            for b, cj, pb in gc:
+                d = self.D.get((a, b))
+                if d is None:
+                    d = np.zeros((self.act[a].size, self.act[b].size), dtype=np.complex128)
+                    self.D[(a, b)] = d
+                d[np.ix_(pa, pb)] += V[np.ix_(ri, cj)]
+
+    def _set_owner(self, o, idx):
+        self.act[o] = idx
+        self.owner[idx] = o
+        self.pos[idx] = np.arange(idx.size)
+
+    def begin_level(self, owners, active, parent_of):
+        """owners: the new level's owners; active[o]: their sorted actives; parent_of(o_old)
+        = the new-level owner that contains old owner o_old."""
+        old_act = self.act
+        self.owner[:] = -1
+        self.pos[:] = -1
+        self.act = {}
+        for o in owners:
+            self._set_owner(o, np.asarray(active[o], dtype=np.int64))
+        D = {}
+        for (a, b), d in self.D.items():
+            pa, pb = parent_of(a), parent_of(b)
+            blk = D.get((pa, pb))
+            if blk is None:
+                blk = np.zeros((self.act[pa].size, self.act[pb].size), dtype=np.complex128)
+                D[(pa, pb)] = blk
+            ia = np.searchsorted(self.act[pa], old_act[a])
+            ib = np.searchsorted(self.act[pb], old_act[b])
+            blk[np.ix_(ia, ib)] = d
+        self.D = D
+
+    def end_phase(self, eliminated):
+        """eliminated: {owner: its sorted skeleton (global indices)}."""
+        keep = {}
+        for o, sk in eliminated.items():
+            keep[o] = self.pos[sk]
+            self.owner[self.act[o]] = -1
+            self.pos[self.act[o]] = -1
+            self._set_owner(o, np.asarray(sk, dtype=np.int64))
+        for key in list(self.D):
+            a, b = key
+            if a in keep or b in keep:
+                d = self.D[key]
+                ra = keep[a] if a in keep else slice(None)
+                cb = keep[b] if b in keep else slice(None)
+                self.D[key] = d[ra][:, cb]
 
 
 def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
            rho_factor: float = 2.0, A_init: np.ndarray | None = None,
-           keep_dense: bool = False, hook=None) -> Factorization:
-    """Factorize Ã.  ``hook(stage, ctx)`` (tests only) is called per eliminated box with
-    stage 'pre' (before the Schur update) and 'post' (after); ctx holds the index sets,
-    the ID and the live dense matrix."""
+           keep_dense: bool = False, hook=None, mode: str = "dense",
+           order: str = "colour") -> Factorization:
+    """Factorize Ã.
+
+    mode: "dense" (n ≤ ~20,000) or "block" (any n); both hold the same current matrix and
+    take the same steps, so they give the same skeletons and factors up to rounding.
+    order: "colour" — colours 0..7, Morton order inside a colour, snapshot rule (reading C8);
+    "colour_reversed" — the same with the order inside each colour reversed (C8 says the
+    result is unchanged up to summation order: a self-check of the batched order);
+    "sequential" — every box of the level in Morton order, each reading the actives as they
+    are when it is processed (the plain sequential sweep of PAPER.md L878-884).
+    ``hook(stage, ctx)`` (tests only, dense mode) is called per eliminated box with stage
+    'pre' (before the Schur update) and 'post' (after); ctx holds the index sets, the ID
+    and the live dense matrix."""
+    if mode not in ("dense", "block") or order not in ("colour", "colour_reversed", "sequential"):
+        raise ValueError("mode / order")
     tree = Tree(points, leaf_max)
     perm = tree.perm
     X = np.asarray(points, dtype=np.float64)[perm]
     NX = np.asarray(normals, dtype=np.float64)[perm]
     sw = np.sqrt(np.asarray(weights, dtype=np.float64)[perm])
-    A = kern.dense_scaled(k, X, NX, sw) if A_init is None else A_init.copy()
+    if mode == "dense":
+        state = DenseState(k, X, NX, sw, A_init)
+    else:
+        if A_init is not None or hook is not None or keep_dense:
+            raise ValueError("A_init / hook / keep_dense need mode='dense'")
+        state = BlockState(k, X, NX, sw, tree.n)
 
     active = {}
     for b in range(len(tree.level)):
         if tree.is_leaf(b):
             active[b] = np.arange(tree.start[b], tree.end[b], dtype=np.int64)
     records = []
-    stats = dict(levels={}, n=tree.n, nlevels=tree.nlevels)
+    stats = dict(levels={}, n=tree.n, nlevels=tree.nlevels, skeletons={})
 
     for lvl in range(tree.nlevels - 1, 1, -1):
         for B in tree.levels[lvl]:
             if not tree.is_leaf(B):
                 active[B] = np.sort(np.concatenate([active[c] for c in tree.children[B]]))
         owners = tree.owners(lvl)
+        state.begin_level(owners, active,
+                          lambda o, lvl=lvl: tree.parent[o] if tree.level[o] == lvl + 1 else o)
         side = tree.box_side(lvl)
         rho = rho_factor * side
         n_gamma = proxy_count(k, rho, eps)
         lst = dict(boxes=0, skipped=0, ranks=[], b=[], nN=[], nQ=[], rows=[], n_gamma=n_gamma)
-        for colour in range(8):
-            phase = [B for B in tree.levels[lvl] if tree.colour(B) == colour]
+        if order == "sequential":
+            phases = [list(tree.levels[lvl])]
+        else:
+            phases = [[B for B in tree.levels[lvl] if tree.colour(B) == colour] for colour in range(8)]
+            if order == "colour_reversed":
+                phases = [p[::-1] for p in phases]
+        for phase in phases:
             snap = {o: active[o] for o in owners}
             total = sum(v.size for v in snap.values())
+            eliminated = {}
             for B in phase:
+                if order == "sequential":           # no batching: every box sees the current actives
+                    snap = {o: active[o] for o in owners}
+                    total = sum(v.size for v in snap.values())
                 Bidx = snap[B]
                 b = Bidx.size
                 if b == 0:
@@ -125,7 +277,7 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 nP = nF - nQ
                 Qidx = (np.concatenate([snap[o] for o in Ql]) if Ql
                         else np.zeros(0, dtype=np.int64))
-                rows = [_gen(A, Qidx, Bidx), _gen(A, Bidx, Qidx).T]
+                rows = [state.get(Qidx, Bidx), state.get(Bidx, Qidx).T]
                 if nP > 0:                         # proxy rows iff P ≠ ∅ (C12)
                     Y, s_g = proxy_points(tree.box_centre(B), rho, n_gamma)
                     Kout = kern.combined_field(k, Y, X[Bidx], NX[Bidx]) * sw[Bidx][None, :]
@@ -143,12 +295,13 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 lst["nN"].append(Nidx.size)
                 lst["nQ"].append(Qidx.size)
                 lst["rows"].append(M.shape[0])
+                stats["skeletons"][B] = np.sort(Bs)
                 if Br.size == 0:                   # k = b: nothing to eliminate (C13)
                     continue
                 # --- E/F transforms (Eq. pap and the X blocks that follow it)
-                A_RR = _gen(A, Br, Br); A_RS = _gen(A, Br, Bs); A_SR = _gen(A, Bs, Br)
-                A_SS = _gen(A, Bs, Bs); A_RN = _gen(A, Br, Nidx); A_NR = _gen(A, Nidx, Br)
-                A_SN = _gen(A, Bs, Nidx); A_NS = _gen(A, Nidx, Bs)
+                A_RR = state.get(Br, Br); A_RS = state.get(Br, Bs); A_SR = state.get(Bs, Br)
+                A_SS = state.get(Bs, Bs); A_RN = state.get(Br, Nidx); A_NR = state.get(Nidx, Br)
+                A_SN = state.get(Bs, Nidx); A_NS = state.get(Nidx, Bs)
                 X_RR = A_RR - T.T @ A_SR - A_RS @ T + T.T @ A_SS @ T
                 X_RS = A_RS - T.T @ A_SS
                 X_SR = A_SR - A_SS @ T
@@ -165,13 +318,18 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                     Fidx = np.concatenate([snap[o] for o in owners if o != B and o not in Nl] or
                                           [np.zeros(0, dtype=np.int64)])
                     ctx = dict(B=B, level=lvl, Bs=Bs, Br=Br, Nidx=Nidx, Qidx=Qidx, Fidx=Fidx,
-                               T=T, A=A, M=M, nP=nP)
+                               T=T, A=state.A, M=M, nP=nP)
                     hook("pre", ctx)
-                A[np.ix_(SN, SN)] -= X_cR @ Up         # Schur complement update
+                state.add(SN, SN, -(X_cR @ Up))       # Schur complement update
                 if hook is not None:
                     hook("post", ctx)
                 records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up, X_RR))
                 active[B] = np.sort(Bs)
+                eliminated[B] = active[B]
+                if order == "sequential":
+                    state.end_phase(eliminated)
+                    eliminated = {}
+            state.end_phase(eliminated)
         lst["ranks"] = np.asarray(lst["ranks"])
         stats["levels"][lvl] = lst
 
@@ -182,12 +340,12 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
     for r in records:
         alive[r.Br] = False
     Bt = np.nonzero(alive)[0]
-    A_t = _gen(A, Bt, Bt)
+    A_t = state.get(Bt, Bt)
     root_lu = sla.lu_factor(A_t, check_finite=False)
     stats["n0"] = int(Bt.size)
     f = Factorization(tree, k, eps, sw, records, Bt, root_lu, stats, A_t)
     if keep_dense:
-        f.A_final = A
+        f.A_final = state.A
     return f
 
 

@@ -48,18 +48,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     objdir = os.path.join(LIBDIR, "obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for f in CU:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def cu(f):
         o = os.path.join(objdir, f + ".o")
         out = _run([NVCC, *ARCH, *COMMON, "-Xptxas", "-v" if verbose else "-O3", "-c",
                     os.path.join(CSRC, f), "-o", o])
         if verbose:
             sys.stderr.write(out)
-        objs.append(o)
-    for f in CPP:
+        return o
+
+    def cpp(f):
         o = os.path.join(objdir, f + ".o")
         _run([CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", os.path.join(CSRC, f), "-o", o])
-        objs.append(o)
+        return o
+
+    with ThreadPoolExecutor(max_workers=len(CU) + len(CPP)) as ex:  # one compiler process per source
+        futs = [ex.submit(cu, f) for f in CU] + [ex.submit(cpp, f) for f in CPP]
+        objs = [f.result() for f in futs]
     _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-Xcompiler", "-pthread"])
     return LIB
 
