@@ -23,8 +23,18 @@
  * argument buffers; the handle owns all internal device memory.
  *
  * Streams: all device work is issued on the handle's stream (default: a
- * stream the handle creates; see fmmlu_set_stream).  fmmlu_tree,
+ * non-blocking stream the handle creates; see fmmlu_set_stream).  fmmlu_tree,
  * fmmlu_factor and fmmlu_solve return after their work is complete.
+ * Ordering precondition for DEVICE arguments: the library orders its work after
+ * everything already queued on the legacy default stream, and (after
+ * fmmlu_set_stream) on the given stream; a device buffer written on any OTHER
+ * stream must be complete (that stream synchronised) before the call.  The
+ * Python binding synchronises torch's current stream for CUDA tensors.
+ *
+ * Device memory: handles allocate from a private stream-ordered pool of the
+ * library (never the device's default pool).  Large blocks and the per-device
+ * factorization workspace are kept across handles for reuse;
+ * fmmlu_release_cache() returns them to the driver.
  *
  * Errors: every function returns 0 on success or a negative FMMLU_E* code;
  * fmmlu_last_error() gives a human-readable message for the calling thread's
@@ -149,6 +159,12 @@ int fmmlu_monostatic_rcs(fmmlu_handle* h, const double* phis, int nphi, void* R)
  * Errors: EINVAL, ESTATE (no tree), ECUDA. */
 int fmmlu_matvec(fmmlu_handle* h, double k, const void* x, void* y, int nrhs);
 
+/* Return the library's cached device memory (per-device factorization workspace,
+ * large-block cache, idle pool reservation) to the driver, on every device.  Call
+ * when no handle is in the middle of a call; live handles keep their factors.
+ * Errors: ECUDA. */
+int fmmlu_release_cache(void);
+
 /* Release the handle and all device memory it owns.  NULL is a no-op. */
 int fmmlu_destroy(fmmlu_handle* h);
 
@@ -163,14 +179,15 @@ int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out);
 int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
 
 /* Tuning parameters (apply to the next fmmlu_factor):
- *   "id_mode"   0 = auto (Gram path for eps >= 1e-7, Householder below; default),
+ *   "id_mode"   0 = auto (Gram path where eps^2 >= 4*b_max*u, Householder below; default),
  *               1 = Householder TSQR + column-pivoted QR on the ID matrix,
  *               2 = Gram matrix + pivoted Cholesky (same pivots/rank/T as CPQR in exact
  *                   arithmetic; accurate while eps^2 >> unit roundoff)
  *               3 = as 2 but always with the global-memory blocked pivoted Cholesky
  *                   (the path used automatically for boxes beyond the cluster capacity)
- *   "id_refine" 1 = one corrected-seminormal-equations step on the Gram-path T (T accurate to
- *               u*cond(M_S) instead of u*cond(M_S)^2; R4); default 0
+ *   "id_refine" 0..3 corrected-seminormal-equations steps on the Gram-path T of fmmlu_boxes
+ *               (each contracts the T error by ~u*cond(M_S)^2, to the u*cond(M_S) of a
+ *               Householder ID; R4); fmmlu_boxes uses 2
  *   "pchol_mode" Gram-path pivoted Cholesky: 0 = register-resident kernel (b <= 512; default),
  *               1 = shared-memory cluster kernel
  *   "gj_mode"   X_RR inverse (Gauss-Jordan, partial pivoting): 0 = auto (whole matrix resident

@@ -82,13 +82,50 @@ double wall_ms() {
 // cache holds at most kBigCap bytes (oldest blocks are evicted first); a failed allocation
 // evicts everything and retries.
 constexpr size_t kBigBlock = 32u << 20;
+constexpr int kMaxDev = 64;
+
+// The library's own stream-ordered pool per device (never the device's default pool, which other
+// libraries in the process share): release threshold = max, so memory freed by one factorization is
+// reused by the next without going back to the driver.  fmmlu_release_cache() trims it.
+cudaMemPool_t lib_pool(int dev) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[kMaxDev] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= kMaxDev) throw Error(FMMLU_ECUDA, "device ordinal out of range");
+  if (!pools[dev]) {
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    FMMLU_CUDA(cudaMemPoolCreate(&pools[dev], &pp));
+    uint64_t thr = UINT64_MAX;
+    FMMLU_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return pools[dev];
+}
+
+int cur_dev() {
+  int d = 0;
+  FMMLU_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+// Process-wide cache of large device blocks, one per device.  Repeated factorizations ask for the
+// same large buffers (factor-store chunks, workspaces); handing them back to the pool and
+// re-requesting them occasionally stalls the host for hundreds of ms (pool growth / reclaim), so
+// blocks ≥ kBigBlock are kept here (allocated from, and evicted to, the library pool).  Reuse is
+// stream-ordered: an event recorded at release is waited on by the next user's stream.  The cache
+// holds at most `cap` bytes (oldest blocks are evicted first); a failed allocation evicts
+// everything and retries; fmmlu_release_cache() empties it.
 struct BigCache {
   struct Blk {
     void* p;
     size_t bytes;
     cudaEvent_t ev;
   };
-  size_t cap = 0;  // 60 % of device memory (set on first use)
+  int dev = 0;
+  size_t cap = 0;  // FMMLU_CACHE_PCT (default 60) % of device memory (set on first use)
   std::mutex mu;
   std::vector<Blk> free_;  // oldest first
   size_t held = 0;
@@ -108,19 +145,30 @@ struct BigCache {
     *got = k.bytes;
     return k.p;
   }
-  // caller holds mu; st = a live stream of the caller (the releasing stream may be gone)
+  // caller holds mu and has this cache's device current; st = a live stream of the caller (the
+  // releasing stream may be gone), or null: free synchronously
   void evict_front(cudaStream_t st) {
     Blk k = free_.front();
     free_.erase(free_.begin());
     held -= k.bytes;
-    cudaStreamWaitEvent(st, k.ev, 0);
-    cudaFreeAsync(k.p, st);
+    if (st) {
+      cudaStreamWaitEvent(st, k.ev, 0);
+      cudaFreeAsync(k.p, st);
+    } else {
+      cudaEventSynchronize(k.ev);
+      cudaFree(k.p);
+    }
     cudaEventDestroy(k.ev);
   }
   void give(void* p, size_t bytes, cudaStream_t st) {
     cudaEvent_t ev;
-    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaEventRecord(ev, st);
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, st) != cudaSuccess) {  // no ordering possible: free synchronously
+      cudaGetLastError();
+      cudaDeviceSynchronize();
+      cudaFree(p);
+      return;
+    }
     std::lock_guard<std::mutex> lk(mu);
     if (cap == 0) {
       size_t fr = 0, tot = 0;
@@ -141,23 +189,29 @@ struct BigCache {
     return held;
   }
 };
-BigCache& big_cache() {
-  static BigCache* c = new BigCache();  // never destroyed: blocks live until process exit
-  return *c;
+// never destroyed (no CUDA calls from static destructors at process exit)
+BigCache& big_cache(int dev) {
+  static BigCache* c[kMaxDev] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= kMaxDev) throw Error(FMMLU_ECUDA, "device ordinal out of range");
+  if (!c[dev]) {
+    c[dev] = new BigCache();
+    c[dev]->dev = dev;
+  }
+  return *c[dev];
 }
 
 // Last resort of a failed allocation: the pool keeps every freed byte reserved (release threshold
-// = max, set at handle creation), and after several factorizations with different block sizes that
-// reservation is fragmented, so one large request can fail with enough memory idle.  Wait for the
-// stream, hand the idle reservation back to the driver and retry once.
+// = max), and after several factorizations with different block sizes that reservation is
+// fragmented, so one large request can fail with enough memory idle.  Wait for the stream, hand the
+// idle reservation back to the driver and retry once.
 cudaError_t retry_trimmed(void** p, size_t bytes, cudaStream_t s) {
   cudaGetLastError();
   cudaStreamSynchronize(s);
-  int dev = 0;
-  cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-    cudaMemPoolTrimTo(pool, 0);
-  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  cudaMemPool_t pool = lib_pool(cur_dev());
+  cudaMemPoolTrimTo(pool, 0);
+  cudaError_t e = cudaMallocFromPoolAsync(p, bytes, pool, s);
   if (e != cudaSuccess) cudaGetLastError();
   return e;
 }
@@ -169,7 +223,8 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), big(o.big), borrowed(o.borrowed), cap(o.cap) {
+  DBuf(DBuf&& o) noexcept
+      : p(o.p), bytes(o.bytes), st(o.st), big(o.big), borrowed(o.borrowed), cap(o.cap), dev(o.dev) {
     o.p = nullptr;
     o.bytes = 0;
     o.big = false;
@@ -184,6 +239,7 @@ struct DBuf {
       big = o.big;
       borrowed = o.borrowed;
       cap = o.cap;
+      dev = o.dev;
       o.p = nullptr;
       o.bytes = 0;
       o.big = false;
@@ -203,7 +259,7 @@ struct DBuf {
     }
     if (p) {
       const double t0 = wall_ms();
-      if (big) big_cache().give(p, cap, st);
+      if (big) big_cache(dev).give(p, cap, st);
       else cudaFreeAsync(p, st);
       g_ac.free_ms += wall_ms() - t0;
     }
@@ -212,9 +268,12 @@ struct DBuf {
     big = false;
   }
   size_t cap = 0;
+  int dev = 0;  // the device it lives on (the caller's current device at alloc)
   void alloc(size_t b, cudaStream_t s) {
     release();
     st = s;
+    dev = cur_dev();
+    cudaMemPool_t pool = lib_pool(dev);
     if (b == 0) b = 16;
     const double t0 = wall_ms();
     cudaError_t e = cudaSuccess;
@@ -225,23 +284,23 @@ struct DBuf {
       size_t q = size_t(1) << (63 - __builtin_clzll((unsigned long long)b));
       const size_t step = std::max<size_t>(q / 8, 1u << 20);
       const size_t bq = (b + step - 1) / step * step;
-      p = big_cache().take(bq, s, &got);
+      p = big_cache(dev).take(bq, s, &got);
       if (!p) {
         got = bq;
-        e = cudaMallocAsync(&p, got, s);
+        e = cudaMallocFromPoolAsync(&p, got, pool, s);
         if (e != cudaSuccess) {  // give the cached blocks back and retry once
           cudaGetLastError();
-          big_cache().flush(s);
-          e = cudaMallocAsync(&p, got, s);
+          big_cache(dev).flush(s);
+          e = cudaMallocFromPoolAsync(&p, got, pool, s);
         }
         if (e != cudaSuccess) e = retry_trimmed(&p, got, s);
       }
       big = e == cudaSuccess;
       cap = got;
     } else {
-      e = cudaMallocAsync(&p, b, s);
+      e = cudaMallocFromPoolAsync(&p, b, pool, s);
       if (e != cudaSuccess) {
-        big_cache().flush(s);
+        big_cache(dev).flush(s);
         e = retry_trimmed(&p, b, s);
       }
     }
@@ -257,6 +316,31 @@ struct DBuf {
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
+
+// Factorization workspace per device (level block stores, M, T, W, Gram scratch): kept across
+// handles so that repeated factorizations reuse the same multi-GB blocks instead of growing the
+// pool (a fresh 45 GB level store stalled the host for 0.5–1.4 s on cfg5).  One factorization per
+// device uses it at a time (`mu` is held for the whole fmmlu_factor); fmmlu_release_cache() frees it.
+struct DevWork {
+  std::mutex mu;
+  DBuf slot[6];
+};
+DevWork& dev_work(int dev) {
+  static DevWork* w[kMaxDev] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= kMaxDev) throw Error(FMMLU_ECUDA, "device ordinal out of range");
+  if (!w[dev]) w[dev] = new DevWork();
+  return *w[dev];
+}
+void release_dev_work(int dev) {
+  DevWork& w = dev_work(dev);
+  std::lock_guard<std::mutex> lk(w.mu);
+  for (auto& d : w.slot) {
+    if (d.p) d.st = nullptr;  // the last user's stream may be gone: release on the legacy stream
+    d.release();
+  }
+}
 
 // Pinned host staging for H2D uploads: cudaMemcpyAsync from pageable memory synchronises the
 // stream first, pinned memory keeps uploads asynchronous.  Reset only after a stream sync.
@@ -463,12 +547,15 @@ struct fmmlu_handle {
   bool factored = false;
   double k = 0, eps = 0;
   std::vector<Phase> phases;
-  DBuf root;       // n0 × n0 complex: X_t⁻¹
-  DBuf root_rows;  // int n0
-  DBuf root_fwd;   // n0 × n0 complex: A_{B_tB_t} for fmmlu_apply (built on first use)
+  DBuf root;          // n0 × n0 complex: P·A_{B_tB_t} = L·U (L unit lower, U upper; rootlu.cu)
+  DBuf root_rows;     // int n0: B_t (ascending tree-order indices)
+  DBuf root_rows_in;  // int n0: B_t[σ(i)], σ = the composed row interchanges (gathers P·y)
+  DBuf root_dinv;     // inverses of the diagonal blocks of L and U (blocked triangular solves)
+  DBuf root_flags;    // solve scratch: per row block ready flags + tickets
   // grow-only workspace slots reused by every phase / level of a factorization (borrowed, never
   // freed per phase): 0/1 level block stores by level parity, 2 M, 3 Tb, 4 W, 5 Gram G|R
   DBuf ws_slot[6];
+  DBuf* ws = nullptr;  // during fmmlu_factor: the device's shared workspace (DevWork); else ws_slot
   // factor-store arena: the per-phase stores are carved from uniform chunks owned by the handle, so
   // successive factorizations reuse whole chunks from the big-block cache instead of growing the
   // stream-ordered pool for every differently sized phase store
@@ -499,12 +586,23 @@ struct fmmlu_handle {
   std::vector<char> topo_ready;
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
   int gj_mode = 0;           // 0 auto (shared-memory GJ when it fits), 1 blocked panel GJ always
-  int id_refine = 0;         // 1: one corrected-seminormal-equations step on the Gram-path T
+  int id_refine = 0;         // corrected-seminormal-equations steps on the Gram-path T (0..3)
   int pchol_mode = 0;        // 0 register-resident pivoted Cholesky (b ≤ 512), 1 shared-memory cluster kernel
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
 };
 
 namespace {
+
+// The handle's stream is non-blocking: make it wait for work already queued on the legacy default
+// stream (the usual producer of caller device buffers in plain CUDA code).  Callers that write inputs
+// on another stream must synchronise it, or pass it with fmmlu_set_stream (include/fmmlu.h).
+void order_after_legacy(cudaStream_t st) {
+  cudaEvent_t e;
+  FMMLU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  FMMLU_CUDA(cudaEventRecord(e, cudaStreamLegacy));
+  FMMLU_CUDA(cudaStreamWaitEvent(st, e, 0));
+  FMMLU_CUDA(cudaEventDestroy(e));
+}
 
 // cudaStreamSynchronize with the blocked time accounted (stats: host vs device-wait split)
 void wait_stream(fmmlu_handle* h, cudaStream_t st) {
@@ -529,7 +627,8 @@ void wait_stream(fmmlu_handle* h, cudaStream_t st) {
 // dst ← a view of workspace slot `slot` of at least `bytes` (the slot grows by ≥ 25 % when short;
 // its old block is released stream-ordered, after the work that used it)
 void borrow_ws(fmmlu_handle* h, int slot, DBuf& dst, size_t bytes, cudaStream_t st) {
-  DBuf& w = h->ws_slot[slot];
+  DBuf& w = h->ws ? h->ws[slot] : h->ws_slot[slot];
+  w.st = st;  // stream-ordered release (on growth) after this user's work
   if (!w.p || w.bytes < bytes) w.alloc(std::max(bytes, w.bytes + w.bytes / 4), st);
   dst.release();
   dst.p = w.p;
@@ -609,6 +708,41 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cp
   keep.push_back(std::move(s.dev));
   probs.clear();
   tiles.clear();
+}
+
+// One batch of GEMMs without profiling (the caller brackets a whole stage).
+void gemm_batched_staged(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cplx alpha,
+                         cudaStream_t st, std::vector<DBuf>& keep) {
+  if (tiles.empty()) return;
+  Stage s;
+  size_t op = s.add(probs), ot = s.add(tiles);
+  s.upload(st);
+  gemm_batched(s.ptr<GemmProblem>(op), s.ptr<GemmTile>(ot), (int)tiles.size(), alpha, 0, nullptr, st);
+  keep.push_back(std::move(s.dev));
+  probs.clear();
+  tiles.clear();
+}
+
+// Root block solve / forward product on y (tree order, ld ldy), rows B_t:
+// solve y[B_t] ← A_t⁻¹ y[B_t] = U⁻¹L⁻¹(P y[B_t]);  fwd y[B_t] ← A_t y[B_t] = Pᵀ(L U y[B_t]).
+void root_solve(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st) {
+  if (h->n0 <= 0) return;
+  const int n0 = (int)h->n0;
+  DBuf T;
+  T.alloc((size_t)n0 * nrhs * sizeof(cplx), st);
+  launch_rows_move(h->root_rows_in.as<int>(), n0, y, ldy, T.as<cplx>(), nrhs, 0, st);
+  root_lu_solve(h->root.as<cplx>(), n0, h->root_dinv.as<cplx>(), T.as<cplx>(), n0, nrhs, h->root_flags.as<int>(), st);
+  launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, T.as<cplx>(), nrhs, 1, st);
+}
+void root_fwd(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st) {
+  if (h->n0 <= 0) return;
+  const int n0 = (int)h->n0;
+  DBuf T;
+  T.alloc(2 * (size_t)n0 * nrhs * sizeof(cplx), st);
+  cplx* Y = T.as<cplx>();
+  launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, Y, nrhs, 0, st);
+  root_lu_mult(h->root.as<cplx>(), n0, Y, Y + (size_t)n0 * nrhs, n0, nrhs, st);
+  launch_rows_move(h->root_rows_in.as<int>(), n0, y, ldy, Y, nrhs, 1, st);
 }
 
 // ---------------------------------------------------------------------------- blocked GJ inverse
@@ -1131,7 +1265,10 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     ids[j].out_off = pofs[j];
     ids[j].T = tofs[j];
   }
-  const bool gram = h->id_mode >= 2 || (h->id_mode == 0 && eps >= 1e-7);
+  // Gram path only where its rounding cannot move the stop decision: the squared residual norms
+  // carry O(b·u)·‖M‖² absolute error against the threshold ε²‖M‖² (reading R4), so require
+  // ε² ≥ 4·bmax·u (ε = 1e-6 up to b ≈ 2200; ε = 1e-7 always takes the Householder path)
+  const bool gram = h->id_mode >= 2 || (h->id_mode == 0 && eps * eps >= 4.0 * bmax * 1.1102230246251565e-16);
   std::vector<ClusterQrTask> cq(nj);
   DBuf G;
   bool done_id = false;
@@ -1383,10 +1520,22 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   h->fac_used = 0;
   h->root.release();
   h->root_rows.release();
-  h->root_fwd.release();
+  h->root_rows_in.release();
+  h->root_dinv.release();
+  h->root_flags.release();
   h->apply_ready = false;
   h->factored = false;
   for (auto& w : h->ws_slot) w.release();
+  DevWork& dw = dev_work(h->dev);
+  std::lock_guard<std::mutex> dw_lock(dw.mu);  // one factorization per device uses the shared workspace
+  h->ws = dw.slot;
+  struct WsReset {
+    fmmlu_handle* h;
+    ~WsReset() {  // also on an error path: no work may still use the workspace when the lock drops
+      cudaStreamSynchronize(h->stream);
+      h->ws = nullptr;
+    }
+  } ws_reset{h};
   fmmlu_stats_t& S = h->stats;
   std::memset(S.t_levels_ms, 0, sizeof(S.t_levels_ms));
   std::memset(S.ranks_sum, 0, sizeof(S.ranks_sum));
@@ -2319,15 +2468,56 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                  s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), h->root.as<cplx>(), h->g, k, st);
     h->prof.end(rid, st);
     h->prof.add(FMMLU_K_ROOT, 60.0 * (double)n0 * n0, 16.0 * (double)n0 * n0, 1);
+    // dense LU with partial pivoting of the root block
     std::vector<DBuf> rkeep;
-    gj_blocked(h, {{h->root.as<cplx>(), n0}}, status.as<int>(), rkeep, FMMLU_K_ROOT);
+    DBuf piv;
+    piv.alloc((size_t)n0 * sizeof(int), st);
+    const int TB = root_lu_tb(n0), nblk = (n0 + TB - 1) / TB;
+    h->root_dinv.alloc((size_t)2 * nblk * TB * TB * sizeof(cplx), st);
+    h->root_flags.alloc((size_t)2 * (nblk + 1) * sizeof(int), st);
+    track(h, h->root_dinv.bytes);
+    S.factor_bytes += h->root_dinv.bytes;
+    const cplx m1 = cmk(-1.0, 0.0);
+    int lid = h->prof.begin(FMMLU_K_ROOT, st);
+    root_lu_factor(h->root.as<cplx>(), n0, piv.as<int>(), status.as<int>(), h->root_dinv.as<cplx>(), st,
+                   [&](int m, int nn, int kk, const cplx* A, int lda, const cplx* B, int ldb, cplx* C, int ldc) {
+                     std::vector<GemmProblem> gp;
+                     std::vector<GemmTile> gt;
+                     GemmProblem P{};
+                     P.m = m;
+                     P.n = nn;
+                     P.k = kk;
+                     P.opA = kOpN;
+                     P.opB = kOpN;
+                     P.A = A;
+                     P.lda = lda;
+                     P.B = B;
+                     P.ldb = ldb;
+                     P.C = C;
+                     P.ldc = ldc;
+                     add_gemm(gp, gt, P);
+                     gemm_batched_staged(gp, gt, m1, st, rkeep);
+                   });
+    h->prof.end(lid, st);
+    h->prof.add(FMMLU_K_ROOT, 8.0 / 3.0 * (double)n0 * n0 * n0, 32.0 * (double)n0 * n0, root_lu_launches(n0));
+    int* hp = h->d2h(n0);
+    FMMLU_CUDA(cudaMemcpyAsync(hp, piv.p, (size_t)n0 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    wait_stream(h, st);
+    // σ = the interchanges composed in order (P·y)[i] = y[σ(i)]; rows_in = B_t∘σ
+    std::vector<int> sig(n0), rin(n0);
+    for (int i = 0; i < n0; ++i) sig[i] = i;
+    for (int j = 0; j < n0; ++j) std::swap(sig[j], sig[hp[j]]);
+    for (int i = 0; i < n0; ++i) rin[i] = Bt[sig[i]];
     h->root_rows.alloc((size_t)n0 * sizeof(int), st);
+    h->root_rows_in.alloc((size_t)n0 * sizeof(int), st);
     h2d(h->root_rows.p, Bt.data(), n0 * sizeof(int), st);
+    h2d(h->root_rows_in.p, rin.data(), n0 * sizeof(int), st);
     wait_stream(h, st);
   }
   if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
   prev.bsr.release();
-  for (auto& w : h->ws_slot) w.release();  // factorization temporaries (stream-ordered)
+  // the shared workspace stays allocated for the next factorization on this device; the stream was
+  // synchronised above, so the next user (on any stream) may reuse it at once
   int hstatus = 0;
   FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   wait_stream(h, st);
@@ -2451,18 +2641,12 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
     launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 1, st);
     keep.push_back(std::move(s.dev));
   }
-  // ---- root: y[B_t] ← X_t⁻¹ y[B_t]
-  DBuf r0;
+  // ---- root: y[B_t] ← A_t⁻¹ y[B_t] (LU triangular solves)
   if (h->n0 > 0) {
-    const int n0 = (int)h->n0;
-    r0.alloc(2 * (size_t)n0 * Q * sizeof(cplx), st);
-    cplx* Y0 = r0.as<cplx>();
-    cplx* Z0 = Y0 + (size_t)n0 * Q;
-    launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, Y0, Q, 0, st);
-    FMMLU_CUDA(cudaMemsetAsync(Z0, 0, (size_t)n0 * Q * sizeof(cplx), st));
-    prob(n0, Q, n0, kOpN, h->root.as<cplx>(), n0, Y0, n0, Z0, n0);
-    run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
-    launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, Z0, Q, 1, st);
+    int rid = P.begin(FMMLU_K_SOLVE, st);
+    root_solve(h, y, ldy, Q, st);
+    P.end(rid, st);
+    P.add(FMMLU_K_SOLVE, 8.0 * (double)h->n0 * h->n0 * Q, 16.0 * (double)h->n0 * h->n0, 4);
   }
   // ---- downward (reverse order): U (y_R −= Up y_{S∪N}), then F (y_S −= T y_R)
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
@@ -2544,11 +2728,7 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   for (auto& ph : h->phases)
     launch_solve_up2(ph.recs.as<BoxRec>(), ph.nrec, ph.items.as<SolveItem>(), ph.nitems, ph.fac.as<cplx>(),
                      ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.kmax, ph.rmax);
-  DBuf tmp;
-  if (h->n0 > 0) {
-    tmp.alloc(2 * (size_t)h->n0 * nrhs * sizeof(cplx), st);
-    launch_root_apply(h->root.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), yp, n, nrhs, tmp.as<cplx>(), st);
-  }
+  root_solve(h, yp, n, nrhs, st);
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
     FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
     launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
@@ -2604,13 +2784,6 @@ void apply_prepare(fmmlu_handle* h) {
     FMMLU_CUDA(cudaStreamSynchronize(st));  // recs (host) and the staging arena are reused next phase
     keep.clear();
   }
-  if (h->n0 > 0) {
-    const size_t bytes = (size_t)h->n0 * h->n0 * sizeof(cplx);
-    h->root_fwd.alloc(bytes, st);
-    track(h, bytes);
-    FMMLU_CUDA(cudaMemcpyAsync(h->root_fwd.p, h->root.p, bytes, cudaMemcpyDeviceToDevice, st));
-    gj_blocked(h, {{h->root_fwd.as<cplx>(), (int)h->n0}}, status.as<int>(), keep, FMMLU_K_APPLY);
-  }
   int hstatus = 0;
   FMMLU_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   wait_stream(h, st);
@@ -2648,11 +2821,7 @@ void apply_impl(fmmlu_handle* h, void* xio, int nrhs) {
   for (auto& ph : h->phases)  // D on the R blocks
     launch_apply_d(ph.ap_recs.as<BoxRec>(), ph.nrec, ph.ap_xs.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs,
                    scr.as<cplx>(), st, ph.rmax);
-  DBuf tmp;
-  if (h->n0 > 0) {  // P_t A_{B_tB_t} P_tᵀ
-    tmp.alloc(2 * (size_t)h->n0 * nrhs * sizeof(cplx), st);
-    launch_root_apply(h->root_fwd.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), yp, n, nrhs, tmp.as<cplx>(), st);
-  }
+  root_fwd(h, yp, n, nrhs, st);  // P_t A_{B_tB_t} P_tᵀ from the stored L·U
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it)  // V₁⋯V_M: V_M first
     launch_apply_v(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
                    it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax);
@@ -2738,7 +2907,7 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
                          8.0 * 13.0 * npb + 64.0 * b;
   size_t fr = 0, tot = 0;
   FMMLU_CUDA(cudaMemGetInfo(&fr, &tot));
-  fr += big_cache().cached();  // cached blocks are reusable (or evicted on demand)
+  fr += big_cache(h->dev).cached();  // cached blocks are reusable (or evicted on demand)
   const int wave = (int)std::max(1.0, std::min<double>({(double)nbox, 1024.0, 0.45 * fr / per_box}));
   cudaEvent_t e0, e1;
   FMMLU_CUDA(cudaEventCreate(&e0));
@@ -2840,7 +3009,8 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
       }
     }
     h->prof.resolve();
-    if (aux.gram && h->id_refine)
+    // corrected-seminormal-equations steps: each contracts the T error by ≈ u·cond(M_S)² (R4)
+    for (int it = 0; aux.gram && it < h->id_refine; ++it)
       refine_T(h, mp_keep, std::vector<int>(nw, m), std::vector<int>(nw, b), hk, hp, pofs_keep, Tb.as<cplx>(),
                tofs_keep, aux, keep);
     // ---- elimination
@@ -3094,7 +3264,7 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
       fprintf(stderr, "[fmmlu boxes] wave %d (%d boxes): %.1f ms (host %.1f, wait %.1f) | allocator: %.1f ms in %lld "
                       "calls (max %.1f), cached %.1f GB\n",
               w0 / wave, nw, now_ms() - tw0, now_ms() - tw0 - (h->stats.t_sync_wait_ms - ww0),
-              h->stats.t_sync_wait_ms - ww0, g_ac.alloc_ms, g_ac.nalloc, g_ac.alloc_max, big_cache().cached() / 1e9);
+              h->stats.t_sync_wait_ms - ww0, g_ac.alloc_ms, g_ac.nalloc, g_ac.alloc_max, big_cache(h->dev).cached() / 1e9);
       g_ac = AllocClock{};
     }
   }
@@ -3141,11 +3311,7 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     FMMLU_CUDA(cudaGetDevice(&h->dev));
     FMMLU_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, h->dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    order_after_legacy(h->stream);  // device inputs written on the legacy default stream are complete
     h->n = n;
     cudaStream_t st = h->stream;
     // ---- device front end (reading C14/R1): the inputs stay on the device;
@@ -3257,6 +3423,7 @@ int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs) {
   if (!h->factored) return fail(FMMLU_ESTATE, "fmmlu_solve called before a successful fmmlu_factor");
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
+    if (h->stream == h->own_stream) order_after_legacy(h->stream);
     double t0 = now_ms();
     solve_impl(h, rhs, nrhs);
     h->stats.t_solve_ms = now_ms() - t0;
@@ -3270,6 +3437,7 @@ int fmmlu_apply(fmmlu_handle* h, void* x, int nrhs) {
   if (!h->factored) return fail(FMMLU_ESTATE, "fmmlu_apply called before a successful fmmlu_factor");
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
+    if (h->stream == h->own_stream) order_after_legacy(h->stream);
     apply_impl(h, x, nrhs);
   });
 }
@@ -3315,10 +3483,7 @@ void rcs_impl(fmmlu_handle* h, const double* phis, int nphi, void* Rout) {
       for (auto& p : h->phases)
         launch_solve_up2(p.recs.as<BoxRec>(), p.nrec, p.items.as<SolveItem>(), p.nitems, p.fac.as<cplx>(),
                          p.idx.as<int>(), y, n, q, scr.as<cplx>(), st, p.kmax, p.rmax);
-      if (h->n0 > 0) {
-        tmp.alloc(2 * (size_t)h->n0 * q * sizeof(cplx), st);
-        launch_root_apply(h->root.as<cplx>(), (int)h->n0, h->root_rows.as<int>(), y, n, q, tmp.as<cplx>(), st);
-      }
+      root_solve(h, y, n, q, st);
       for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
         FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * q * sizeof(cplx), st));
         launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems,
@@ -3343,6 +3508,7 @@ int fmmlu_monostatic_rcs(fmmlu_handle* h, const double* phis, int nphi, void* R)
   if (!h->factored) return fail(FMMLU_ESTATE, "fmmlu_monostatic_rcs called before a successful fmmlu_factor");
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
+    if (h->stream == h->own_stream) order_after_legacy(h->stream);
     double t0 = now_ms();
     rcs_impl(h, phis, nphi, R);
     h->stats.t_solve_ms = now_ms() - t0;
@@ -3355,6 +3521,7 @@ int fmmlu_matvec(fmmlu_handle* h, double k, const void* x, void* y, int nrhs) {
   if (!std::isfinite(k) || k < 0) return fail(FMMLU_EINVAL, "k must be finite and >= 0");
   return guarded([&] {
     FMMLU_CUDA(cudaSetDevice(h->dev));
+    if (h->stream == h->own_stream) order_after_legacy(h->stream);
     cudaStream_t st = h->stream;
     const int n = (int)h->n;
     size_t bytes = (size_t)n * nrhs * sizeof(cplx);
@@ -3424,11 +3591,12 @@ int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const 
     FMMLU_CUDA(cudaGetDevice(&h->dev));
     FMMLU_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
+    order_after_legacy(h->stream);
     // Δ is this workload's output and multiplies T by A_SS: T must be accurate to ≈ u·cond(M_S).
     // Gram path (ε ≥ 1e-7) + one corrected-seminormal-equations step gives that at GEMM speed;
     // the Householder path (ε < 1e-7) has it by construction.
     h->id_mode = 0;
-    h->id_refine = 1;
+    h->id_refine = 2;
     if (const char* e = getenv("FMMLU_BOXES_ID_MODE")) h->id_mode = atoi(e);
     if (const char* e = getenv("FMMLU_BOXES_REFINE")) h->id_refine = atoi(e);
     boxes_impl(h, pts, nrm, npts, nnrm, nbox, b, nnear, w, k, eps, n_gamma, rho, ranks, perm, nkeep, keep, delta,
@@ -3448,12 +3616,17 @@ int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const 
 
 int fmmlu_destroy(fmmlu_handle* h) {
   if (!h) return FMMLU_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->dev);  // blocks go back to this device's cache / pool, events on its streams
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->phases.clear();
   h->fac_chunks.clear();
   h->root.release();
   h->root_rows.release();
-  h->root_fwd.release();
+  h->root_rows_in.release();
+  h->root_dinv.release();
+  h->root_flags.release();
   for (auto& w : h->ws_slot) w.release();
   h->geo.release();
   h->perm.release();
@@ -3463,7 +3636,24 @@ int fmmlu_destroy(fmmlu_handle* h) {
     cudaStreamDestroy(h->own_stream);
   }
   delete h;
+  if (prev >= 0) cudaSetDevice(prev);
   return FMMLU_OK;
+}
+
+int fmmlu_release_cache(void) {
+  return guarded([&] {
+    int ndev = 0, prev = 0;
+    FMMLU_CUDA(cudaGetDeviceCount(&ndev));
+    FMMLU_CUDA(cudaGetDevice(&prev));
+    for (int d = 0; d < std::min(ndev, kMaxDev); ++d) {
+      FMMLU_CUDA(cudaSetDevice(d));
+      release_dev_work(d);
+      big_cache(d).flush(nullptr);
+      FMMLU_CUDA(cudaDeviceSynchronize());
+      FMMLU_CUDA(cudaMemPoolTrimTo(lib_pool(d), 0));
+    }
+    FMMLU_CUDA(cudaSetDevice(prev));
+  });
 }
 
 const char* fmmlu_last_error(void) { return g_last_error.c_str(); }
@@ -3499,7 +3689,7 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "pchol_mode must be 0 or 1");
     h->pchol_mode = (int)value;
   } else if (k == "id_refine") {
-    if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "id_refine must be 0 or 1");
+    if (!(value >= 0 && value <= 3 && value == (int)value)) return fail(FMMLU_EINVAL, "id_refine must be 0..3");
     h->id_refine = (int)value;
   } else if (k == "gj_mode") {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "gj_mode must be 0 or 1");

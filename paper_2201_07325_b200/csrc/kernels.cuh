@@ -1,5 +1,6 @@
 // Task descriptors and launchers for the libfmmlu device kernels.
 #pragma once
+#include <functional>
 #include "common.cuh"
 
 #include <vector>
@@ -240,5 +241,23 @@ double probe_fp64(int kind);
 // cfg4: row-major per-box geometry → SoA (x|y|z|nx|ny|nz|√w), box i at [i·(b+nnear), (i+1)·(b+nnear))
 void launch_box_geo(const double* pts, const double* nrm, const double* npts, const double* nnrm, int nbox, int b,
                     int nnear, double sw, double* out, cudaStream_t st);
+
+// ---- root block: blocked right-looking LU with partial pivoting, rootlu.cu
+constexpr int kRootNB = 64;  // outer panel (trailing-update GEMM depth)
+constexpr int kRootIB = 16;  // inner register panel width
+// C −= A·B (m×n, k) on the library's DMMA GEMM; supplied by the host orchestration
+using GemmFn = std::function<void(int m, int n, int k, const cplx* A, int lda, const cplx* B, int ldb, cplx* C,
+                                  int ldc)>;
+int root_lu_max_n();
+int root_lu_tb(int n);  // row-block height of the blocked triangular solves / Dinv blocks
+// In place P·A = L·U of the n × n column-major A (ld n); piv[j] = row interchanged with j at step j;
+// Dinv (2·ceil(n/TB)·TB² complex): inverses of L's and U's TB × TB diagonal blocks; *status = 1 on an
+// exactly zero pivot column.
+void root_lu_factor(cplx* A, int n, int* piv, int* status, cplx* Dinv, cudaStream_t st, const GemmFn& gemm);
+int root_lu_launches(int n);
+// Y (n × nrhs, ld ldy, rows already permuted by P) ← U⁻¹ L⁻¹ Y.  flags: 2·(ceil(n/TB)+1) ints scratch.
+void root_lu_solve(const cplx* A, int n, const cplx* Dinv, cplx* Y, int ldy, int nrhs, int* flags, cudaStream_t st);
+// Y ← L·U·Y (Z: n × nrhs scratch, ld ldy); the caller applies Pᵀ when scattering.
+void root_lu_mult(const cplx* A, int n, cplx* Y, cplx* Z, int ldy, int nrhs, cudaStream_t st);
 
 }  // namespace fmmlu

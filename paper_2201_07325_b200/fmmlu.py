@@ -52,7 +52,7 @@ KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur"
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_monostatic_rcs", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
-           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes")
+           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes", "fmmlu_release_cache")
 
 
 def lib_path() -> str:
@@ -87,6 +87,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_set_param.argtypes = [vp, ctypes.c_char_p, cd]
     L.fmmlu_inverse_batch.argtypes = [vp, vp, ci, ci, ctypes.POINTER(cd)]
     L.fmmlu_boxes.argtypes = [vp, vp, vp, vp, ci, ci, ci, cd, cd, cd, ci, cd, vp, vp, ci, vp, vp, vp]
+    L.fmmlu_release_cache.argtypes = []
     for f in EXPORTS:
         getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
     _LIB = L
@@ -107,6 +108,21 @@ def _ptr(a):
     raise TypeError(type(a))
 
 
+def _sync_producer(*arrays):
+    """Stream-ordering precondition of include/fmmlu.h: a CUDA tensor argument may have been
+    written on torch's current stream; make that work complete before the library reads it."""
+    for a in arrays:
+        if hasattr(a, "is_cuda") and a.is_cuda:
+            import torch
+            torch.cuda.current_stream(a.device).synchronize()
+            return
+
+
+def release_cache():
+    """Return the library's cached device memory to the driver (fmmlu_release_cache)."""
+    _check(load().fmmlu_release_cache())
+
+
 def _f64_rows3(a):
     if isinstance(a, np.ndarray):
         return np.ascontiguousarray(a, dtype=np.float64)
@@ -121,6 +137,8 @@ class FmmLu:
         L = load()
         self._keep = [_f64_rows3(points), _f64_rows3(normals), _f64_rows3(weights)]
         n = int(self._keep[2].shape[0])
+        _sync_producer(*self._keep)
+        self._stream = None
         h = ctypes.c_void_p()
         _check(L.fmmlu_tree(_ptr(self._keep[0]), _ptr(self._keep[1]), _ptr(self._keep[2]), n, int(leaf_max),
                             ctypes.byref(h)))
@@ -139,6 +157,8 @@ class FmmLu:
             nrhs = 1 if rhs.ndim == 1 else int(rhs.shape[1])
         if isinstance(rhs, np.ndarray):
             assert rhs.dtype == np.complex128 and (rhs.ndim == 1 or rhs.flags.f_contiguous)
+        elif self._stream is None:
+            _sync_producer(rhs)
         _check(load().fmmlu_solve(self.h, _ptr(rhs), int(nrhs)))
         return rhs
 
@@ -149,6 +169,8 @@ class FmmLu:
             nrhs = 1 if x.ndim == 1 else int(x.shape[1])
         if isinstance(x, np.ndarray):
             assert x.dtype == np.complex128 and (x.ndim == 1 or x.flags.f_contiguous)
+        elif self._stream is None:
+            _sync_producer(x)
         _check(load().fmmlu_apply(self.h, _ptr(x), int(nrhs)))
         return x
 
@@ -167,6 +189,8 @@ class FmmLu:
         nrhs = 1 if x.ndim == 1 else int(x.shape[1])
         if y is None:
             y = np.empty_like(x, order="F") if isinstance(x, np.ndarray) else x.clone()
+        if self._stream is None:
+            _sync_producer(x, y)
         _check(load().fmmlu_matvec(self.h, float(k), _ptr(x), _ptr(y), nrhs))
         return y
 
@@ -193,6 +217,7 @@ class FmmLu:
 
     def set_stream(self, stream_ptr: int | None):
         _check(load().fmmlu_set_stream(self.h, stream_ptr or None))
+        self._stream = stream_ptr or None
 
     def close(self):
         if getattr(self, "h", None):
@@ -236,6 +261,7 @@ def boxes(pts, nrm, npts, nnrm, w: float, k: float, eps: float, n_gamma: int, rh
     delta: {box id: Δ (k+nnear)²}, ms, gflop, wave)."""
     L = load()
     arrs = [_f64_rows3(a) for a in (pts, nrm, npts, nnrm)]
+    _sync_producer(*arrs)
     nbox, b = int(arrs[0].shape[0]), int(arrs[0].shape[1])
     nnear = int(arrs[2].shape[1])
     ranks = np.zeros(nbox, dtype=np.int32)

@@ -65,3 +65,21 @@ def test_box_degenerate_ranks():
     assert o["k"] == 32 and np.all(o["Delta"] == 0)
     o = ob.eliminate_box(10.0, 0.9, pts, nrm, npts, nnrm, w, h, n_gamma=128)
     assert 1 <= o["k"] <= 2
+
+
+def test_given_split_with_cpqr_order_reproduces_the_id():
+    """split = (CPQR perm, k) reproduces T = R11⁻¹R12 and Δ: the least-squares fit for the CPQR
+    pivot order is the ID's T (M_S = Q₁R11, M_R = Q₁R12 + Q₂R22, Q₂ ⊥ Q₁)."""
+    pts, nrm, npts, nnrm, w, h = _small_box(4, b=160, nnear=64)
+    o = ob.eliminate_box(10.0, 1e-4, pts, nrm, npts, nnrm, w, h, n_gamma=256)
+    g = ob.eliminate_box(10.0, 1e-4, pts, nrm, npts, nnrm, w, h, n_gamma=256, split=(o["perm"], o["k"]))
+    assert 0 < o["k"] < 160
+    assert np.abs(g["T"] - o["T"]).max() <= 1e-8 * np.abs(o["T"]).max()
+    assert np.abs(g["Delta"] - o["Delta"]).max() <= 1e-10 * np.abs(o["Delta"]).max()
+    # a different (valid) split of the same size: swap the last skeleton and first redundant column
+    P2 = o["perm"].copy()
+    kk = o["k"]
+    P2[kk - 1], P2[kk] = P2[kk], P2[kk - 1]
+    g2 = ob.eliminate_box(10.0, 1e-4, pts, nrm, npts, nnrm, w, h, n_gamma=256, split=(P2, kk))
+    res = g2["M"][:, P2[kk:]] - g2["M"][:, P2[:kk]] @ g2["T"]
+    assert np.linalg.norm(res, axis=0).max() <= 2e-4 * np.linalg.norm(g2["M"], axis=0).max()
