@@ -310,7 +310,16 @@ struct DBuf {
     ++g_ac.nalloc;
     if (e != cudaSuccess) {
       cudaGetLastError();
-      throw Error(FMMLU_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed");
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      uint64_t res = 0, used = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      throw Error(FMMLU_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed (device free " +
+                                    std::to_string(fr >> 20) + " MiB of " + std::to_string(tot >> 20) +
+                                    ", library pool reserved " + std::to_string(res >> 20) + " MiB / used " +
+                                    std::to_string(used >> 20) + " MiB, block cache " +
+                                    std::to_string(big_cache(dev).cached() >> 20) + " MiB)");
     }
     bytes = b;
   }
@@ -629,7 +638,16 @@ void wait_stream(fmmlu_handle* h, cudaStream_t st) {
 void borrow_ws(fmmlu_handle* h, int slot, DBuf& dst, size_t bytes, cudaStream_t st) {
   DBuf& w = h->ws ? h->ws[slot] : h->ws_slot[slot];
   w.st = st;  // stream-ordered release (on growth) after this user's work
-  if (!w.p || w.bytes < bytes) w.alloc(std::max(bytes, w.bytes + w.bytes / 4), st);
+  if (!w.p || w.bytes < bytes) {
+    const size_t grown = std::max(bytes, w.bytes + w.bytes / 4);
+    if (w.p && w.big && h->ws) {  // outgrown shared workspace: back to the pool, not the block cache
+      cudaFreeAsync(w.p, st);
+      w.p = nullptr;
+      w.big = false;
+      w.bytes = 0;
+    }
+    w.alloc(grown, st);
+  }
   dst.release();
   dst.p = w.p;
   dst.bytes = bytes;
