@@ -686,17 +686,27 @@ int proxy_count(double k, double rho, double eps) {
 
 constexpr int kTile = 64;
 
-// upper = true: only output tiles with tile-row ≤ tile-column (Hermitian results)
-void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, const GemmProblem& p,
+// upper = true: only output tiles with tile-row ≤ tile-column (Hermitian results).  One group per
+// problem; the 64×64 tile list is expanded on the device (gemm_run).
+void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& groups, const GemmProblem& p,
               bool upper = false) {
-  if (p.m <= 0 || p.n <= 0 || p.k <= 0) return;
-  int id = (int)probs.size();
+  const int cnt = gemm_tile_count(p, upper);
+  if (cnt <= 0) return;
+  const int first = groups.empty() ? 0 : groups.back().first + groups.back().count;
+  groups.push_back(GemmGroup{(int)probs.size(), first, cnt, upper ? 1 : 0});
   probs.push_back(p);
-  const int nks = p.kchunk > 0 ? (p.k + p.kchunk - 1) / p.kchunk : 1;
-  for (int tm = 0; tm < (p.m + kTile - 1) / kTile; ++tm)
-    for (int tn = upper ? tm : 0; tn < (p.n + kTile - 1) / kTile; ++tn)
-      for (int ks = 0; ks < nks; ++ks) tiles.push_back({id, tm, tn, ks});
 }
+long long group_tiles(const GemmGroup* g, size_t n) { return n ? (long long)g[n - 1].first + g[n - 1].count : 0; }
+
+// Expand the groups' tiles into a stream-ordered scratch list and run the batched GEMM.
+void gemm_run(const GemmProblem* d_probs, const GemmGroup* d_groups, int ngroups, long long ntiles, cplx alpha,
+              int scatter, cplx* bsr, cudaStream_t st) {
+  if (ntiles <= 0) return;
+  DBuf tb;
+  tb.alloc((size_t)ntiles * sizeof(GemmTile), st);
+  gemm_expand(d_probs, d_groups, ngroups, tb.as<GemmTile>(), st);
+  gemm_batched(d_probs, tb.as<GemmTile>(), (int)ntiles, alpha, scatter, bsr, st);
+}  // tb is released in stream order after the launches
 
 // Algorithmic work of a batch: 8mnk real flops per complex GEMM; bytes = read A and B once,
 // read-modify-write C once (16 B per complex element).
@@ -708,7 +718,7 @@ void gemm_work(const std::vector<GemmProblem>& probs, double& fl, double& by) {
   }
 }
 
-void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cplx alpha,
+void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, cplx alpha,
                int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep, Prof& P, int cls,
                double work_scale = 1.0) {
   if (tiles.empty()) return;
@@ -720,7 +730,8 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cp
   fl *= work_scale;  // e.g. 0.5 for Hermitian products computed on upper tiles only
   by *= work_scale;
   int id = P.begin(cls, st);
-  gemm_batched(s.ptr<GemmProblem>(op), s.ptr<GemmTile>(ot), (int)tiles.size(), alpha, scatter, bsr, st);
+  gemm_run(s.ptr<GemmProblem>(op), s.ptr<GemmGroup>(ot), (int)tiles.size(), group_tiles(tiles.data(), tiles.size()),
+           alpha, scatter, bsr, st);
   P.end(id, st);
   P.add(cls, fl, by, 1);
   keep.push_back(std::move(s.dev));
@@ -729,13 +740,14 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cp
 }
 
 // One batch of GEMMs without profiling (the caller brackets a whole stage).
-void gemm_batched_staged(std::vector<GemmProblem>& probs, std::vector<GemmTile>& tiles, cplx alpha,
+void gemm_batched_staged(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, cplx alpha,
                          cudaStream_t st, std::vector<DBuf>& keep) {
   if (tiles.empty()) return;
   Stage s;
   size_t op = s.add(probs), ot = s.add(tiles);
   s.upload(st);
-  gemm_batched(s.ptr<GemmProblem>(op), s.ptr<GemmTile>(ot), (int)tiles.size(), alpha, 0, nullptr, st);
+  gemm_run(s.ptr<GemmProblem>(op), s.ptr<GemmGroup>(ot), (int)tiles.size(), group_tiles(tiles.data(), tiles.size()),
+           alpha, 0, nullptr, st);
   keep.push_back(std::move(s.dev));
   probs.clear();
   tiles.clear();
@@ -849,11 +861,11 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
     by += 32.0 * (double)m.second * m.second;
   }
   std::vector<GemmProblem> gp;
-  std::vector<GemmTile> gt;
-  std::vector<std::pair<size_t, size_t>> launches;  // (tile offset, tile count) per panel
+  std::vector<GemmGroup> gt;
+  std::vector<std::pair<size_t, size_t>> launches;  // (group offset, group count) per panel
   for (int j0 = 0; j0 < nmax; j0 += nb) {
     std::vector<GemmProblem> pp;
-    std::vector<GemmTile> tt;
+    std::vector<GemmGroup> tt;
     for (auto& t : tasks) {
       if (j0 >= t.n) continue;
       const int jb = std::min(nb, t.n - j0);
@@ -899,8 +911,8 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
     launch_gj_swap(s.ptr<GjTask>(o_t), (int)tasks.size(), j0, nb, st, nmax);
     nl += 2;
     if (launches[pi].second) {
-      gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_g) + launches[pi].first, (int)launches[pi].second,
-                   cmk(1.0, 0.0), 0, nullptr, st);
+      gemm_run(s.ptr<GemmProblem>(o_p), s.ptr<GemmGroup>(o_g) + launches[pi].first, (int)launches[pi].second,
+               group_tiles(gt.data() + launches[pi].first, launches[pi].second), cmk(1.0, 0.0), 0, nullptr, st);
       ++nl;
     }
   }
@@ -956,7 +968,7 @@ void pchol_big(fmmlu_handle* h, cplx* G, const std::vector<long long>& goff, lon
     t.kslot = j;
   }
   std::vector<GemmProblem> gp;
-  std::vector<GemmTile> gt;
+  std::vector<GemmGroup> gt;
   for (int j = 0; j < nbx; ++j) {
     GemmProblem P{};
     P.m = bcol[j];
@@ -979,7 +991,8 @@ void pchol_big(fmmlu_handle* h, cplx* G, const std::vector<long long>& goff, lon
   int id = h->prof.begin(FMMLU_K_CPQR, st);
   for (int j0 = 0; j0 < bmax; j0 += NB) {
     launch_pchol_big_panel(s.ptr<PcholBig>(o_t), nbx, NB, eps, st, bmax);
-    gemm_batched(s.ptr<GemmProblem>(o_p), s.ptr<GemmTile>(o_g), (int)gt.size(), cmk(-1.0, 0.0), 0, nullptr, st);
+    gemm_run(s.ptr<GemmProblem>(o_p), s.ptr<GemmGroup>(o_g), (int)gt.size(), group_tiles(gt.data(), gt.size()),
+             cmk(-1.0, 0.0), 0, nullptr, st);
   }
   launch_pchol_big_finish(s.ptr<PcholBig>(o_t), nbx, d_perm, d_k, st, bmax);
   h->prof.end(id, st);
@@ -1300,7 +1313,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     borrow_ws(h, 5, G, 2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
     FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
     std::vector<GemmProblem> gp;
-    std::vector<GemmTile> gt;
+    std::vector<GemmGroup> gt;
     // split-K: as few chunks as keep ≈ 4 CTAs per SM busy (each chunk ends in an atomic
     // read-modify-write of its 64×64 tile, so short chunks are epilogue-bound)
     long long utiles = 0;
@@ -1459,7 +1472,7 @@ void refine_T(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<i
   launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), mp[sel[0]], Mg.as<cplx>(), st);
   h->prof.end(id, st);
   std::vector<GemmProblem> gp;
-  std::vector<GemmTile> gt;
+  std::vector<GemmGroup> gt;
   cplx* MG = Mg.as<cplx>();
   for (int j : sel) {  // E = M_R − M_S T (in place over the gathered M_R)
     const int kk = kv[j], r = bcol[j] - kk, m = mrows[j];
@@ -2248,7 +2261,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         lap(19);
         // E: W_B[R,:] −= Tᵀ W_B[S,:]
         std::vector<GemmProblem> gp;
-        std::vector<GemmTile> gt;
+        std::vector<GemmGroup> gt;
         const cplx m1 = cmk(-1.0, 0.0), p1 = cmk(1.0, 0.0);
         for (size_t e = 0; e < el.size(); ++e) {
           BoxJob& J = jobs[el[e]];
@@ -2500,7 +2513,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     root_lu_factor(h->root.as<cplx>(), n0, piv.as<int>(), status.as<int>(), h->root_dinv.as<cplx>(), st,
                    [&](int m, int nn, int kk, const cplx* A, int lda, const cplx* B, int ldb, cplx* C, int ldc) {
                      std::vector<GemmProblem> gp;
-                     std::vector<GemmTile> gt;
+                     std::vector<GemmGroup> gt;
                      GemmProblem P{};
                      P.m = m;
                      P.n = nn;
@@ -2578,7 +2591,7 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
   Prof& P = h->prof;
   std::vector<DBuf> keep;
   std::vector<GemmProblem> gp;
-  std::vector<GemmTile> gt;
+  std::vector<GemmGroup> gt;
   const cplx m1 = cmk(-1.0, 0.0), p1 = cmk(1.0, 0.0);
   size_t wsmax = 1;
   for (auto& ph : h->phases) {
@@ -3129,7 +3142,7 @@ void boxes_impl(fmmlu_handle* h, const double* pts, const double* nrm, const dou
       h->prof.add(FMMLU_K_BUILD, 70.0 * (double)wsW, 16.0 * (double)wsW, 1);
       launch_copy(sb.ptr<CopyTask>(o_ct), (int)cpT.size(), sb.ptr<int>(o_m), Tb.as<cplx>(), Fp, st);
       std::vector<GemmProblem> gp;
-      std::vector<GemmTile> gt;
+      std::vector<GemmGroup> gt;
       for (int j : el) {  // E: W_B[R,:] −= Tᵀ W_B[S,:]
         const int kk = hk[j], r = b - kk;
         GemmProblem P{};

@@ -4,6 +4,7 @@
 // Complex product as 4 real DMMAs: Re += ArBr − AiBi, Im += ArBi + AiBr.
 #include "gemm.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace fmmlu {
@@ -248,7 +249,49 @@ __global__ void __launch_bounds__(NT) k_gemm_schur3(const GemmProblem* __restric
   gemm_body<1, true>(probs, tiles, alpha, bsr);
 }
 
+__global__ void k_gemm_expand(const GemmProblem* __restrict__ probs, const GemmGroup* __restrict__ groups,
+                              int ngroups, GemmTile* __restrict__ tiles) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= ngroups) return;
+  const GemmGroup g = groups[w];
+  const GemmProblem& P = probs[g.p];
+  const int nks = P.kchunk > 0 ? (P.k + P.kchunk - 1) / P.kchunk : 1;
+  const int ntn = (P.n + BN - 1) / BN;
+  for (int t = lane; t < g.count; t += 32) {
+    const int ks = t % nks;
+    int r = t / nks, tm = 0, tn;
+    if (g.upper) {
+      while (r >= ntn - tm) {
+        r -= ntn - tm;
+        ++tm;
+      }
+      tn = tm + r;
+    } else {
+      tm = r / ntn;
+      tn = r % ntn;
+    }
+    tiles[g.first + t] = GemmTile{g.p, tm, tn, ks};
+  }
+}
+
 }  // namespace
+
+int gemm_tile_count(const GemmProblem& p, bool upper) {
+  if (p.m <= 0 || p.n <= 0 || p.k <= 0) return 0;
+  const int nks = p.kchunk > 0 ? (p.k + p.kchunk - 1) / p.kchunk : 1;
+  const int tm = (p.m + BM - 1) / BM, tn = (p.n + BN - 1) / BN;
+  if (!upper) return tm * tn * nks;
+  int c = 0;
+  for (int i = 0; i < tm; ++i) c += std::max(0, tn - i);
+  return c * nks;
+}
+
+void gemm_expand(const GemmProblem* d_probs, const GemmGroup* d_groups, int ngroups, GemmTile* d_tiles,
+                 cudaStream_t st) {
+  if (ngroups <= 0) return;
+  k_gemm_expand<<<(ngroups * 32 + 255) / 256, 256, 0, st>>>(d_probs, d_groups, ngroups, d_tiles);
+  FMMLU_LAUNCH();
+}
 
 void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
                   int scatter, cplx* bsr_base, cudaStream_t st) {

@@ -45,4 +45,14 @@ struct GemmTile {
 void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
                   int scatter, cplx* bsr_base, cudaStream_t st);
 
+// Compact host description of a problem's tiles: tiles [first, first + count) of the launch belong
+// to problem p (upper = 1: only tile rows ≤ tile columns, Hermitian results).  The per-tile list is
+// expanded on the device (one warp per group), so the host never enumerates tiles.
+struct GemmGroup {
+  int p, first, count, upper;
+};
+int gemm_tile_count(const GemmProblem& p, bool upper);
+void gemm_expand(const GemmProblem* d_probs, const GemmGroup* d_groups, int ngroups, GemmTile* d_tiles,
+                 cudaStream_t st);
+
 }  // namespace fmmlu

@@ -2047,22 +2047,25 @@ void launch_herm_mirror(cplx* const* d_ptrs, const int* d_dims, int nmats, int b
   FMMLU_LAUNCH();
 }
 
+// Copy tasks are split into chunks of at most kCopyChunk × kCopyChunk (one CTA each): few enough
+// descriptors for the host to build and upload cheaply, enough CTAs to balance a launch.
+constexpr int kCopyChunk = 256;
 int copy_tiles(int rows, int cols) {
-  if ((long long)rows * cols <= 4096) return 1;
-  return ((rows + 63) / 64) * ((cols + 63) / 64);
+  if ((long long)rows * cols <= (long long)kCopyChunk * kCopyChunk) return 1;
+  return ((rows + kCopyChunk - 1) / kCopyChunk) * ((cols + kCopyChunk - 1) / kCopyChunk);
 }
 
 int emit_copy_tiles(const CopyTask& t, CopyTask* out) {
-  if ((long long)t.rows * t.cols <= 4096) {
+  if ((long long)t.rows * t.cols <= (long long)kCopyChunk * kCopyChunk) {
     out[0] = t;
     return 1;
   }
   int n = 0;
-  for (int i0 = 0; i0 < t.rows; i0 += 64)
-    for (int j0 = 0; j0 < t.cols; j0 += 64) {
+  for (int i0 = 0; i0 < t.rows; i0 += kCopyChunk)
+    for (int j0 = 0; j0 < t.cols; j0 += kCopyChunk) {
       CopyTask u = t;
-      u.rows = std::min(64, t.rows - i0);
-      u.cols = std::min(64, t.cols - j0);
+      u.rows = std::min(kCopyChunk, t.rows - i0);
+      u.cols = std::min(kCopyChunk, t.cols - j0);
       u.dst = t.dst + i0 + (long long)j0 * t.ldd;
       u.ti = t.ti + i0;
       u.tj = t.tj + j0;
@@ -2082,27 +2085,9 @@ void split_copy_tasks(std::vector<CopyTask>& v) {
   std::vector<CopyTask> out;
   out.reserve(v.size());
   for (const CopyTask& t : v) {
-    if ((long long)t.rows * t.cols <= 4096) {
-      out.push_back(t);
-      continue;
-    }
-    for (int i0 = 0; i0 < t.rows; i0 += 64)
-      for (int j0 = 0; j0 < t.cols; j0 += 64) {
-        CopyTask u = t;
-        u.rows = std::min(64, t.rows - i0);
-        u.cols = std::min(64, t.cols - j0);
-        u.dst = t.dst + i0 + (long long)j0 * t.ldd;
-        u.ti = t.ti + i0;
-        u.tj = t.tj + j0;
-        if (!t.trans) {
-          if (t.rmap_off >= 0) u.rmap_off = t.rmap_off + i0; else u.src += i0;
-          if (t.cmap_off >= 0) u.cmap_off = t.cmap_off + j0; else u.src += (long long)j0 * t.lds;
-        } else {
-          if (t.rmap_off >= 0) u.rmap_off = t.rmap_off + i0; else u.src += (long long)i0 * t.lds;
-          if (t.cmap_off >= 0) u.cmap_off = t.cmap_off + j0; else u.src += j0;
-        }
-        out.push_back(u);
-      }
+    const size_t at = out.size();
+    out.resize(at + copy_tiles(t.rows, t.cols));
+    emit_copy_tiles(t, out.data() + at);
   }
   v.swap(out);
 }

@@ -55,7 +55,7 @@ struct CopyTask {
 };
 // Mirror the upper triangle of Hermitian b×b matrices (ld b) into the lower one.
 void launch_herm_mirror(cplx* const* d_ptrs, const int* d_dims, int nmats, int bmax, cudaStream_t st);
-// Split copy tasks larger than 64×64 into 64×64 tiles (load balance across CTAs).
+// Split copy tasks larger than 256×256 into 256×256 chunks (one CTA each).
 void split_copy_tasks(std::vector<CopyTask>& v);
 int copy_tiles(int rows, int cols);                  // tiles split_copy_tasks makes of one task
 int emit_copy_tiles(const CopyTask& t, CopyTask* out);  // writes them, returns the count
