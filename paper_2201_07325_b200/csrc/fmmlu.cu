@@ -1281,9 +1281,55 @@ struct IdAux {  // Gram path: R' = [R11 R12] over G (ld b) per box, for the refi
   std::vector<long long> goff;
 };
 
+bool id_uses_gram(const fmmlu_handle* h, double eps, int bmax) {
+  // Gram path only where its rounding cannot move the stop decision: the squared residual norms
+  // carry O(b·u)·‖M‖² absolute error against the threshold ε²‖M‖² (reading R4), so require
+  // ε² ≥ 4·bmax·u (ε = 1e-6 up to b ≈ 2200; ε = 1e-7 always takes the Householder path)
+  return h->id_mode >= 2 || (h->id_mode == 0 && eps * eps >= 4.0 * bmax * 1.1102230246251565e-16);
+}
+
+// G_j += M_jᴴ M_j (upper 64×64 tiles; split-K with atomic accumulation where few tiles would keep
+// the GPU busy) for boxes j0 ≤ j < j1.  G must be zeroed beforehand.
+void gram_gemm(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<int>& mrows,
+               const std::vector<int>& bcol, cplx* G, const std::vector<long long>& goff, int j0, int j1,
+               std::vector<DBuf>& keep) {
+  cudaStream_t st = h->stream;
+  std::vector<GemmProblem> gp;
+  std::vector<GemmGroup> gt;
+  long long utiles = 0;
+  for (int j = j0; j < j1; ++j) {
+    const long long t = (bcol[j] + kTile - 1) / kTile;
+    utiles += t * (t + 1) / 2;
+  }
+  static const int g_cps = getenv("FMMLU_GRAM_CPS") ? atoi(getenv("FMMLU_GRAM_CPS")) : 8;
+  static const int g_minch = getenv("FMMLU_GRAM_MINCH") ? atoi(getenv("FMMLU_GRAM_MINCH")) : 128;
+  const long long want = std::max<long long>(1, ((long long)g_cps * 148 + utiles - 1) / std::max<long long>(utiles, 1));
+  for (int j = j0; j < j1; ++j) {
+    GemmProblem P{};
+    P.m = bcol[j];
+    P.n = bcol[j];
+    P.k = mrows[j];
+    P.opA = kOpC;
+    P.opB = kOpN;
+    P.A = mp[j];
+    P.lda = mrows[j];
+    P.B = mp[j];
+    P.ldb = mrows[j];
+    P.C = G + goff[j];
+    P.ldc = bcol[j];
+    long long ch = (mrows[j] + want - 1) / want;
+    ch = std::max<long long>(g_minch, (ch + 15) / 16 * 16);
+    P.kchunk = mrows[j] > ch ? (int)ch : 0;
+    add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
+  }
+  run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
+}
+
+// gram_done: the caller already accumulated G = MᴴM into workspace slot 5 (M in waves).
 void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, const std::vector<int>& bcol,
               const std::vector<int>& pofs, const std::vector<long long>& tofs, double eps, int* permd, int* kd,
-              cplx* Tb, std::vector<DBuf>& keep, std::vector<int>& mfin, IdAux* aux = nullptr) {
+              cplx* Tb, std::vector<DBuf>& keep, std::vector<int>& mfin, IdAux* aux = nullptr,
+              bool gram_done = false) {
   cudaStream_t st = h->stream;
   const int nj = (int)mp.size();
   int bmax = 1;
@@ -1296,10 +1342,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     ids[j].out_off = pofs[j];
     ids[j].T = tofs[j];
   }
-  // Gram path only where its rounding cannot move the stop decision: the squared residual norms
-  // carry O(b·u)·‖M‖² absolute error against the threshold ε²‖M‖² (reading R4), so require
-  // ε² ≥ 4·bmax·u (ε = 1e-6 up to b ≈ 2200; ε = 1e-7 always takes the Householder path)
-  const bool gram = h->id_mode >= 2 || (h->id_mode == 0 && eps * eps >= 4.0 * bmax * 1.1102230246251565e-16);
+  const bool gram = id_uses_gram(h, eps, bmax);
   std::vector<ClusterQrTask> cq(nj);
   DBuf G;
   bool done_id = false;
@@ -1311,40 +1354,10 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
       gsz += (long long)bcol[j] * bcol[j];
     }
     borrow_ws(h, 5, G, 2 * (size_t)gsz * sizeof(cplx), st);  // G | R scratch
-    FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
-    std::vector<GemmProblem> gp;
-    std::vector<GemmGroup> gt;
-    // split-K: as few chunks as keep ≈ 4 CTAs per SM busy (each chunk ends in an atomic
-    // read-modify-write of its 64×64 tile, so short chunks are epilogue-bound)
-    long long utiles = 0;
-    for (int j = 0; j < nj; ++j) {
-      const long long t = (bcol[j] + kTile - 1) / kTile;
-      utiles += t * (t + 1) / 2;
+    if (!gram_done) {
+      FMMLU_CUDA(cudaMemsetAsync(G.p, 0, (size_t)gsz * sizeof(cplx), st));
+      gram_gemm(h, mp, mrows, bcol, G.as<cplx>(), goff, 0, nj, keep);
     }
-    static const int g_cps = getenv("FMMLU_GRAM_CPS") ? atoi(getenv("FMMLU_GRAM_CPS")) : 8;
-    static const int g_minch = getenv("FMMLU_GRAM_MINCH") ? atoi(getenv("FMMLU_GRAM_MINCH")) : 128;
-    const long long want = std::max<long long>(1, ((long long)g_cps * 148 + utiles - 1) / std::max<long long>(utiles, 1));
-    for (int j = 0; j < nj; ++j) {
-      GemmProblem P{};
-      P.m = bcol[j];
-      P.n = bcol[j];
-      P.k = mrows[j];
-      P.opA = kOpC;
-      P.opB = kOpN;
-      P.A = mp[j];
-      P.lda = mrows[j];
-      P.B = mp[j];
-      P.ldb = mrows[j];
-      P.C = G.as<cplx>() + goff[j];
-      P.ldc = bcol[j];
-      {
-        long long ch = (mrows[j] + want - 1) / want;
-        ch = std::max<long long>(g_minch, (ch + 15) / 16 * 16);
-        P.kchunk = mrows[j] > ch ? (int)ch : 0;
-      }
-      add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
-    }
-    run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
     // the register pivoted Cholesky reads the lower triangle from the upper one itself
     const bool reg_pchol = h->id_mode != 3 && h->pchol_mode == 0 && pchol_reg_scratch(bmax) > 0;
     if (!reg_pchol) {
@@ -1800,6 +1813,28 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         permtot += J.b;
         bmax = std::max(bmax, J.b);
       }
+      // Gram path: M is only needed until its Gram matrix is formed, so it is gathered in waves of
+      // ≤ FMMLU_M_WAVE_GB (default 4 GB) and each wave's G_j = M_jᴴM_j accumulated before the next
+      // (cfg5 level 6 would otherwise hold ≈ 30 GB of M at once).
+      const bool gram_waves = id_uses_gram(h, eps, bmax);
+      std::vector<int> wave_start{0};
+      if (gram_waves) {
+        static const double wave_gb = getenv("FMMLU_M_WAVE_GB") ? atof(getenv("FMMLU_M_WAVE_GB")) : 4.0;
+        const long long cap = std::max<long long>(1, (long long)(wave_gb * 1e9 / sizeof(cplx)));
+        long long w = 0, wmax = 0;
+        for (int j = 0; j < nj; ++j) {
+          const long long sz = (long long)jobs[j].m * jobs[j].b;
+          if (w > 0 && w + sz > cap) {
+            wave_start.push_back(j);
+            w = 0;
+          }
+          jobs[j].Moff = w;
+          w += sz;
+          wmax = std::max(wmax, w);
+        }
+        wsM = wmax;
+      }
+      wave_start.push_back(nj);
       DBuf M, Tb, permd, kd;
       borrow_ws(h, 2, M, std::max<long long>(wsM, 1) * sizeof(cplx), st);
       borrow_ws(h, 3, Tb, std::max<long long>(wsT, 1) * sizeof(cplx), st);
@@ -1911,10 +1946,38 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_g = s.add(gidx);
         s.upload(st);
         lap(8);
-        int pid = h->prof.begin(FMMLU_K_GATHER, st);
-        launch_copy(s.ptr<CopyTask>(o_c), (int)cps.size(), s.ptr<int>(o_m), cur.bsr.as<cplx>(), M.as<cplx>(), st);
-        launch_proxy(s.ptr<ProxyTask>(o_p), (int)pts.size(), s.ptr<int>(o_g), M.as<cplx>(), h->g, k, st, ngamma);
-        h->prof.end(pid, st);
+        const int nwaves = (int)wave_start.size() - 1;
+        std::vector<cplx*> mp(nj);
+        std::vector<int> mrows(nj), bcol(nj), pofs(nj), mfin(nj);
+        std::vector<long long> tofs(nj);
+        for (int j = 0; j < nj; ++j) {
+          mp[j] = M.as<cplx>() + jobs[j].Moff;
+          mrows[j] = jobs[j].m;
+          bcol[j] = jobs[j].b;
+          pofs[j] = jobs[j].permoff;
+          tofs[j] = jobs[j].Toff;
+        }
+        DBuf Gw;
+        std::vector<long long> goff(nj);
+        if (gram_waves) {
+          long long gsz = 0;
+          for (int j = 0; j < nj; ++j) {
+            goff[j] = gsz;
+            gsz += (long long)bcol[j] * bcol[j];
+          }
+          borrow_ws(h, 5, Gw, 2 * (size_t)gsz * sizeof(cplx), st);  // the slot id_stage uses
+          FMMLU_CUDA(cudaMemsetAsync(Gw.p, 0, (size_t)gsz * sizeof(cplx), st));
+        }
+        for (int w = 0; w < nwaves; ++w) {
+          const int j0 = wave_start[w], j1 = wave_start[w + 1];
+          int pid = h->prof.begin(FMMLU_K_GATHER, st);
+          launch_copy(s.ptr<CopyTask>(o_c) + at[j0].cps, at[j1].cps - at[j0].cps, s.ptr<int>(o_m),
+                      cur.bsr.as<cplx>(), M.as<cplx>(), st);
+          launch_proxy(s.ptr<ProxyTask>(o_p) + at[j0].pts, at[j1].pts - at[j0].pts, s.ptr<int>(o_g), M.as<cplx>(),
+                       h->g, k, st, ngamma);
+          h->prof.end(pid, st);
+          if (gram_waves) gram_gemm(h, mp, mrows, bcol, Gw.as<cplx>(), goff, j0, j1, keep);
+        }
         {
           double by = 0, fl = 0;
           for (auto& c : cps) by += 32.0 * c.rows * c.cols;
@@ -1922,22 +1985,13 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             by += 32.0 * p.ngamma * p.b;
             fl += 2.0 * p.ngamma * p.b * 60.0;  // ~60 flops per kernel entry (estimate)
           }
-          h->prof.add(FMMLU_K_GATHER, fl, by, (cps.empty() ? 0 : 1) + (pts.empty() ? 0 : 1));
+          h->prof.add(FMMLU_K_GATHER, fl, by, nwaves * ((cps.empty() ? 0 : 1) + (pts.empty() ? 0 : 1)));
         }
         keep.push_back(std::move(s.dev));
         {
-          std::vector<cplx*> mp(nj);
-          std::vector<int> mrows(nj), bcol(nj), pofs(nj), mfin(nj);
-          std::vector<long long> tofs(nj);
-          for (int j = 0; j < nj; ++j) {
-            mp[j] = M.as<cplx>() + jobs[j].Moff;
-            mrows[j] = jobs[j].m;
-            bcol[j] = jobs[j].b;
-            pofs[j] = jobs[j].permoff;
-            tofs[j] = jobs[j].Toff;
-          }
           lap(9);
-          id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin);
+          id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin,
+                   nullptr, gram_waves);
           for (int j = 0; j < nj; ++j) jobs[j].mfin = mfin[j];
         }
         lap(13);
@@ -2450,6 +2504,28 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   std::sort(Bt.begin(), Bt.end());
   const int n0 = (int)Bt.size();
   h->n0 = n0;
+  {
+    // The idle shared-workspace slots (M, T, W, Gram, and the level store the root does not read)
+    // are kept for the next factorization unless the root block would not fit beside them: cfg5
+    // holds ≈ 120 GB of workspace + 45 GB of factors at this point.
+    size_t fr = 0, tot = 0;
+    FMMLU_CUDA(cudaMemGetInfo(&fr, &tot));
+    uint64_t res = 0, used = 0;
+    cudaMemPool_t pool = lib_pool(h->dev);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    const size_t avail = fr + (size_t)(res - used) + big_cache(h->dev).cached();
+    const size_t need = (size_t)n0 * n0 * sizeof(cplx) * 2 + (4ull << 30);
+    if (avail < need) {
+      const int keep_slot = prev.level >= 0 ? (prev.level & 1) : -1;
+      for (int sl = 0; sl < 6; ++sl)
+        if (sl != keep_slot && h->ws[sl].p) {
+          h->ws[sl].st = st;
+          h->ws[sl].release();
+        }
+      big_cache(h->dev).flush(st);
+    }
+  }
   S.n0 = n0;
   if (n0 > 0) {
     h->root.alloc((size_t)n0 * n0 * sizeof(cplx), st);
@@ -2584,7 +2660,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
 // per-box kernels below): y (tree order, W^{½}-scaled, ld ldy) ← Ã⁻¹ y for
 // Q columns.  Per phase the boxes' rows are gathered into dense blocks, the products run as
 // batched GEMMs (C += α op(A) B), and the results are scattered back (atomics on shared N rows).
-constexpr int kGemmSolveMin = 32;  // nrhs from which the GEMM sweeps replace the per-box kernels
+// nrhs from which the GEMM sweeps replace the per-box kernels (FMMLU_GEMM_SOLVE_MIN overrides)
+const int kGemmSolveMin = getenv("FMMLU_GEMM_SOLVE_MIN") ? std::max(1, atoi(getenv("FMMLU_GEMM_SOLVE_MIN"))) : 32;
 
 void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
   cudaStream_t st = h->stream;

@@ -1,7 +1,9 @@
 // Batched complex128 GEMM on DMMA (mma.sync.aligned.m8n8k4.f64) for sm_100a.
 // 64×64 output tile per CTA, 8 warps (2×4), warp tile 32×16, K-step 16 complex,
-// cp.async double-buffered shared-memory staging with zero-fill at the edges.
-// Complex product as 4 real DMMAs: Re += ArBr − AiBi, Im += ArBi + AiBr.
+// cp.async double-buffered shared-memory staging with zero-fill at the edges (k4 steps past the
+// end of K are skipped).  Complex product as 3 real DMMAs (P1 = ArBr, P2 = AiBi,
+// P3 = (Ar+Ai)(Br+Bi); Re = P1 − P2, Im = P3 − P1 − P2), or 4 (Re += ArBr − AiBi, Im += ArBi + AiBr).
+// Measured (tools/ubench_gemm.cu, B200): a 3-stage pipeline was not faster than 2 stages.
 #include "gemm.cuh"
 
 #include <algorithm>
@@ -11,7 +13,11 @@ namespace fmmlu {
 
 namespace {
 
+#ifndef FMMLU_GEMM_STAGES
+#define FMMLU_GEMM_STAGES 2
+#endif
 constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int STAGES = FMMLU_GEMM_STAGES;  // cp.async pipeline depth (tiles in flight + 1)
 constexpr int PADA = BM + 2, PADB = BN + 2;  // +2 complex: conflict-free fragment loads
 constexpr int NT = 256;
 
@@ -28,6 +34,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0, int k0, cplx* As,
                                            cplx* Bs, int tid) {
@@ -74,8 +82,8 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
                                           const GemmTile* __restrict__ tiles, cplx alpha,
                                           cplx* __restrict__ bsr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* As = reinterpret_cast<cplx*>(smem_raw);      // [2][BK][PADA]
-  cplx* Bs = As + 2 * BK * PADA;                     // [2][BK][PADB]
+  cplx* As = reinterpret_cast<cplx*>(smem_raw);      // [STAGES][BK][PADA]
+  cplx* Bs = As + STAGES * BK * PADA;                // [STAGES][BK][PADB]
   const GemmTile T = tiles[blockIdx.x];
   const GemmProblem P = probs[T.p];
   if (P.active != nullptr && *P.active == 0) return;
@@ -102,22 +110,26 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
   const int kbeg = P.kchunk > 0 ? T.ks * P.kchunk : 0;
   const int kend = P.kchunk > 0 ? min(P.k, kbeg + P.kchunk) : P.k;
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-  if (nk > 0) {
-    load_tiles(P, m0, n0, kbeg, As, Bs, tid);
+  // prologue: tiles 0 .. STAGES-2 in flight (one commit group per tile, empty groups past the end)
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_tiles(P, m0, n0, kbeg + s * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait_all();
-    __syncthreads();
-    if (kt + 1 < nk) {
-      int s = (kt + 1) & 1;
-      load_tiles(P, m0, n0, kbeg + (kt + 1) * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
+    cp_async_wait<STAGES - 2>();  // tile kt has landed (this thread's copies)
+    __syncthreads();              // ... everybody's; and tile kt-1's buffer is free
+    {
+      const int kn = kt + STAGES - 1, s = kn % STAGES;
+      if (kn < nk) load_tiles(P, m0, n0, kbeg + kn * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
       cp_async_commit();
     }
-    const cplx* as = As + (kt & 1) * BK * PADA;
-    const cplx* bs = Bs + (kt & 1) * BK * PADB;
+    const cplx* as = As + (kt % STAGES) * BK * PADA;
+    const cplx* bs = Bs + (kt % STAGES) * BK * PADB;
+    const int kleft = kend - (kbeg + kt * BK);  // k4 steps past the end are zero-filled: skip them
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
+      if (ks * 4 >= kleft) break;  // warp-uniform
       const int kk = ks * 4 + t;
       cplx a[4], b[2];
 #pragma unroll
@@ -180,6 +192,7 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
   bool tab_in_smem = false;
   if (SCATTER) {
     tab_in_smem = P.ns <= 64 && P.ns * P.ns <= 2048;
+    cp_async_wait_all();  // (only empty groups can be pending)
     __syncthreads();  // operand buffers are free
     for (int e = tid; e < BM; e += NT) {
       const int r = m0 + e;
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(NT) k_gemm_schur(const GemmProblem* __restrict
                                                    cplx* __restrict__ bsr) {
   gemm_body<1, false>(probs, tiles, alpha, bsr);
 }
-__global__ void __launch_bounds__(NT) k_gemm_schur3(const GemmProblem* __restrict__ probs,
+__global__ void __launch_bounds__(NT, 2) k_gemm_schur3(const GemmProblem* __restrict__ probs,
                                                     const GemmTile* __restrict__ tiles, cplx alpha,
                                                     cplx* __restrict__ bsr) {
   gemm_body<1, true>(probs, tiles, alpha, bsr);
@@ -296,7 +309,7 @@ void gemm_expand(const GemmProblem* d_probs, const GemmGroup* d_groups, int ngro
 void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
                   int scatter, cplx* bsr_base, cudaStream_t st) {
   if (ntiles <= 0) return;
-  const size_t smem = 2 * BK * (PADA + PADB) * sizeof(cplx);
+  const size_t smem = (size_t)STAGES * BK * (PADA + PADB) * sizeof(cplx);
   static bool init = false;
   if (!init) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_store, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -305,7 +318,9 @@ void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntile
     init = true;
   }
   // grid.x limit is 2^31-1; tiles are enumerated explicitly
-  static const bool schur3 = getenv("FMMLU_SCHUR_3M") && atoi(getenv("FMMLU_SCHUR_3M"));
+  // 3-multiplication complex product in the Schur GEMM too (25 % fewer DMMAs; measured 7-10 % faster
+  // on cfg5 level-5/6 shapes, tools/ubench_gemm.cu); FMMLU_SCHUR_3M=0 selects the 4-product form
+  static const bool schur3 = !(getenv("FMMLU_SCHUR_3M") && atoi(getenv("FMMLU_SCHUR_3M")) == 0);
   if (scatter && schur3)
     k_gemm_schur3<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
   else if (scatter)
