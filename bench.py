@@ -35,8 +35,10 @@ import fmmlu_inputs as fi  # noqa: E402
 METRIC = "FMM-LU factor unknowns/s and solve ms/RHS at eps=1e-6 (complex128, 1 B200)"
 UNIT = "unknowns/s"
 CFG = "cfg5"
-# bounded CPU sample for the oracle arm: the cfg5 wavy torus on a coarser grid (same k, leaf, eps)
+# bounded CPU sample for the oracle: the cfg5 wavy torus recipe on a coarser grid, with the same
+# points per wavelength (k scaled by sqrt(n/10^6), so the boxes compress as in cfg5), leaf and eps
 ORACLE_GRID = (120, 40)
+ORACLE_GRIDS = [(60, 20), (84, 28), (120, 40)]
 
 
 def _peaks():
@@ -143,11 +145,13 @@ def dist_env():
     return rank, world, local
 
 
-def oracle_sample():
-    """The cfg5-family sample the CPU oracle is timed on: the same wavy torus recipe, k, leaf,
-    ε and 32 RHS on a coarser grid (block-mode oracle), ≈ 10–30 s of host work."""
-    c = fi.CONFIGS[CFG]
-    g = fi.wavy_torus(*ORACLE_GRID)
+def oracle_sample(grid=ORACLE_GRID):
+    """The cfg5-family sample the CPU oracle is timed on: the same wavy torus recipe on a coarser
+    grid at cfg5's points per wavelength (k = 10·sqrt(n/10⁶)), leaf, ε and 32 RHS (block-mode
+    oracle); the default grid is ≈ 10–30 s of host work."""
+    c = dict(fi.CONFIGS[CFG])
+    g = fi.wavy_torus(*grid)
+    c["k"] = c["k"] * math.sqrt(g.n / 1e6)
     b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
     return c, g, b
 
@@ -160,10 +164,10 @@ def oracle_step(c, g, b):
     return time.perf_counter() - t0
 
 
-def _sample_desc(g, c):
+def _sample_desc(g, c, grid=ORACLE_GRID):
     return (f"oracle (NumPy/SciPy, untuned, block mode) tree+factor+solve of the {CFG} wavy torus recipe on a "
-            f"{ORACLE_GRID[0]}x{ORACLE_GRID[1]} grid (n={g.n}; full {CFG} is n=10^6), k={c['k']:g}, "
-            f"leaf {c['leaf_max']}, eps {c['eps']:g}, {c['nrhs']} RHS")
+            f"{grid[0]}x{grid[1]} grid (n={g.n}; full {CFG} is n=10^6) at cfg5's points per wavelength "
+            f"(k={c['k']:.3f} = 10*sqrt(n/1e6)), leaf {c['leaf_max']}, eps {c['eps']:g}, {c['nrhs']} RHS")
 
 
 def run_reference(args):
@@ -171,7 +175,16 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    c, g, b = oracle_sample()
+    # per-step sample sized so that warmup + steps finish within a few minutes: calibrate on the
+    # smallest grid (untimed), then take the largest grid whose extrapolated time (∝ n^1.5) fits
+    budget = max(3.0, min(30.0, 150.0 / max(1, args.warmup + args.steps)))
+    c0, g0, b0 = oracle_sample(ORACLE_GRIDS[0])
+    t_small = oracle_step(c0, g0, b0)
+    grid = ORACLE_GRIDS[0]
+    for gr in ORACLE_GRIDS:
+        if t_small * ((gr[0] * gr[1]) / (g0.n)) ** 1.5 <= budget:
+            grid = gr
+    c, g, b = oracle_sample(grid)
     times = []
     for it in range(args.warmup + args.steps):
         dt = oracle_step(c, g, b)
@@ -184,9 +197,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"{CFG} family sample: wavy torus n={g.n}, k={c['k']:g}, leaf {c['leaf_max']}, "
+        "config": {"workload": f"{CFG} family sample: wavy torus n={g.n}, k={c['k']:.3f}, leaf {c['leaf_max']}, "
                                f"eps {c['eps']:g}, {c['nrhs']} RHS", "sample_of": CFG},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": _sample_desc(g, c)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": _sample_desc(g, c, grid)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -47,14 +47,28 @@ def proxy_rows(k: float, pts, nrm, w, centre, rho: float, n_gamma: int):
 
 
 def eliminate_box(k: float, eps: float, pts, nrm, npts, nnrm, w, h,
-                  n_gamma: int = 512, rho: float | None = None):
-    """Return dict(perm, k, T, M, Delta) for one cfg4 box (centre 0, side h)."""
+                  n_gamma: int = 512, rho: float | None = None, split=None):
+    """Return dict(perm, k, T, M, Delta) for one cfg4 box (centre 0, side h).
+
+    split = (perm, kk): use the given skeleton S = perm[:kk] (in that order) and redundant
+    R = perm[kk:] instead of the CPQR choice, with T the least-squares interpolation matrix
+    T = argmin ‖M_R − M_S T‖ (PAPER.md L614-616 defines the ID by that fit; for the CPQR pivot
+    order it is exactly R11⁻¹R12, since M_S = Q₁R11 and M_R = Q₁R12 + Q₂R22).  Used to judge a
+    GPU result whose skeleton differs from the oracle's at a pivot near-tie: the elimination
+    steps are the same, only the column split is taken from the GPU."""
     b = pts.shape[0]
     if rho is None:
         rho = 1.5 * (math.sqrt(3.0) / 2.0) * h     # 1.5 × half-diagonal (BJ configs[3])
     A = box_matrix(k, pts, nrm, npts, nnrm, w)
     M = proxy_rows(k, pts, nrm, w, np.zeros(3), rho, n_gamma)
-    P, kk, T = interp_decomp(M, eps)
+    if split is None:
+        P, kk, T = interp_decomp(M, eps)
+    else:
+        P, kk = np.asarray(split[0], dtype=np.int64), int(split[1])
+        if kk > 0 and kk < b:
+            T = np.linalg.lstsq(M[:, P[:kk]], M[:, P[kk:]], rcond=None)[0]
+        else:
+            T = np.zeros((kk, b - kk), dtype=np.complex128)
     S, R = P[:kk], P[kk:]
     N = np.arange(b, A.shape[0])
     g = lambda r, c: A[np.ix_(r, c)]

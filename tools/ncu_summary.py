@@ -56,6 +56,7 @@ FULL_METRICS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
     "launch__grid_size": "grid",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
 }
 
 
@@ -94,5 +95,9 @@ if __name__ == "__main__":
         if n:
             for k in ("dram_read", "dram_write", "duration"):
                 summ[k + "_per_launch"] = sum(r.get(k) or 0 for r in recs) / n
+            tot = sum(r.get("duration") or 0 for r in recs)
+            for k in ("dmma_pipe_pct", "fp64_pipe_pct", "sm_pct"):  # duration-weighted means
+                if tot > 0 and any(r.get(k) is not None for r in recs):
+                    summ[k + "_weighted"] = sum((r.get(k) or 0) * (r.get("duration") or 0) for r in recs) / tot
             summ["traffic_per_launch"] = summ["dram_read_per_launch"] + summ["dram_write_per_launch"]
         print(json.dumps({"summary": summ, "launches": recs}, indent=1))
