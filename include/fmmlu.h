@@ -197,6 +197,14 @@ int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
  * Errors: EINVAL (unknown name or value out of range). */
 int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);
 
+/* The octree's boxes (built on the device): level-major, Morton order within a
+ * level.  Call with all arrays NULL to get the count in *nboxes; otherwise *nboxes is the capacity
+ * on entry and the count on return.  level[b], coord[3b..3b+2] (cell coordinates at that level),
+ * start[b]/end[b] (point range in tree order; fmmlu_tree_perm maps tree positions to caller
+ * indices).  Host arrays.  Errors: EINVAL (NULL nboxes, capacity too small). */
+int fmmlu_tree_boxes(const fmmlu_handle* h, int32_t* nboxes, int32_t* level, int32_t* coord, int32_t* start,
+                     int32_t* end);
+
 /* Tree order: perm[i] = caller index of the i-th point in tree (Morton) order.
  * perm: int64[n] host buffer. */
 int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm);

@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
           "-I", os.path.join(HERE, "..", "include")] + os.environ.get("FMMLU_NVCC_EXTRA", "").split()
-CU = ["fmmlu.cu", "kernels.cu", "gemm.cu", "rootlu.cu"]
+CU = ["fmmlu.cu", "kernels.cu", "gemm.cu", "rootlu.cu", "devtree.cu"]
 CPP = ["tree.cpp"]
 CXX = os.environ.get("CXX", "g++")
 

@@ -40,6 +40,7 @@
 #include "../../include/fmmlu.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "devtree.h"
 #include "tree.h"
 
 using namespace fmmlu;
@@ -460,6 +461,11 @@ struct Phase {  // one (level, colour) elimination phase
   size_t fac_bytes = 0;
   DBuf ap_xs, ap_recs;  // fmmlu_apply: X_RR blocks (re-inverted X_RR⁻¹) and records pointing at them
   std::vector<BoxRec> hrecs;  // host copy of recs (multi-RHS GEMM sweeps build their problems from it)
+  // Sub-waves of records (boundaries into recs / items; one wave unless deterministic): no two boxes
+  // of a wave share a target owner, so every atomic update of a wave lands on a distinct entry and
+  // the waves run in a fixed order.  SolveItem::rec is relative to its wave's first record.
+  std::vector<int> wrec{0}, witem{0};
+  int nwaves() const { return (int)wrec.size() - 1; }
 };
 
 double now_ms() {
@@ -593,6 +599,7 @@ struct fmmlu_handle {
     return buf;
   }
   std::vector<char> topo_ready;
+  int deterministic = -1;    // 1: bitwise-reproducible factor/solve (no racing fp64 atomics); -1: env default
   int id_mode = 0;           // 0 auto, 1 Householder TSQR + CPQR, 2 Gram + pivoted Cholesky
   int gj_mode = 0;           // 0 auto (shared-memory GJ when it fits), 1 blocked panel GJ always
   int id_refine = 0;         // corrected-seminormal-equations steps on the Gram-path T (0..3)
@@ -1281,6 +1288,11 @@ struct IdAux {  // Gram path: R' = [R11 R12] over G (ld b) per box, for the refi
   std::vector<long long> goff;
 };
 
+bool is_deterministic(const fmmlu_handle* h) {
+  static const bool env = getenv("FMMLU_DETERMINISTIC") && atoi(getenv("FMMLU_DETERMINISTIC"));
+  return h->deterministic < 0 ? env : h->deterministic != 0;
+}
+
 bool id_uses_gram(const fmmlu_handle* h, double eps, int bmax) {
   // Gram path only where its rounding cannot move the stop decision: the squared residual norms
   // carry O(b·u)·‖M‖² absolute error against the threshold ε²‖M‖² (reading R4), so require
@@ -1319,7 +1331,7 @@ void gram_gemm(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<
     P.ldc = bcol[j];
     long long ch = (mrows[j] + want - 1) / want;
     ch = std::max<long long>(g_minch, (ch + 15) / 16 * 16);
-    P.kchunk = mrows[j] > ch ? (int)ch : 0;
+    P.kchunk = (mrows[j] > ch && !is_deterministic(h)) ? (int)ch : 0;  // split-K adds with atomics
     add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
   }
   run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
@@ -2044,6 +2056,37 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         Phase ph;
         ph.level = lvl;
         ph.colour = colour;
+        if (is_deterministic(h)) {
+          // greedy sub-waves: a box joins the first wave none of whose boxes shares an owner of
+          // {B} ∪ N(B) with it (its Schur update and solve scatters then never race); the boxes are
+          // reordered wave by wave (stable), so records stay contiguous per wave
+          std::vector<std::vector<char>> used;
+          std::vector<int> wv(el.size());
+          for (size_t e = 0; e < el.size(); ++e) {
+            const BoxJob& J = jobs[el[e]];
+            int w = 0;
+            for (;; ++w) {
+              if (w == (int)used.size()) used.emplace_back(no, 0);
+              bool ok = !used[w][J.a];
+              for (int o : J.N) ok = ok && !used[w][o];
+              if (ok) break;
+            }
+            used[w][J.a] = 1;
+            for (int o : J.N) used[w][o] = 1;
+            wv[e] = w;
+          }
+          std::vector<int> order(el.size());
+          for (size_t e = 0; e < el.size(); ++e) order[e] = (int)e;
+          std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return wv[x] < wv[y]; });
+          std::vector<int> el2(el.size());
+          for (size_t e = 0; e < el.size(); ++e) el2[e] = el[order[e]];
+          for (size_t e = 0; e < el.size(); ++e)
+            if (e == 0 || wv[order[e]] != wv[order[e - 1]]) {
+              if (e) ph.wrec.push_back((int)e);
+            }
+          el.swap(el2);
+        }
+        ph.wrec.push_back((int)el.size());
         // sizes
         long long wsW = 0, facsz = 0;
         int idxsz = 0;
@@ -2393,7 +2436,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         run_gemms(gp, gt, p1, 0, nullptr, st, keep, h->prof, FMMLU_K_PANEL);
         // Schur complement: Δ_{(S∪N)²} −= X_{(S∪N)R} · Up  (= X_{(S∪N)R} X_RR⁻¹ X_{R(S∪N)}), scattered
         // into the level BSR
-        for (size_t e = 0; e < el.size(); ++e) {
+        for (int w = 0; w < ph.nwaves(); ++w) {
+        for (size_t e = ph.wrec[w]; e < (size_t)ph.wrec[w + 1]; ++e) {
           BoxJob& J = jobs[el[e]];
           BoxRec& R = recs[e];
           const int kn = R.k + J.nN;
@@ -2420,6 +2464,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           add_gemm(gp, gt, P);
         }
         run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep, h->prof, FMMLU_K_SCHUR);
+        }
         lap(21);
         // index arena + records
         h2d(ph.idx.p, hidx.data(), hidx.size() * sizeof(int), st);
@@ -2429,8 +2474,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         ph.hrecs = recs;
         {
           std::vector<SolveItem> items;
-          for (size_t e = 0; e < recs.size(); ++e)
-            for (int c0 = 0; c0 < recs[e].k + recs[e].nN; c0 += kSolveChunk) items.push_back({(int)e, c0});
+          for (int w = 0; w < ph.nwaves(); ++w) {
+            for (int e = ph.wrec[w]; e < ph.wrec[w + 1]; ++e)
+              for (int c0 = 0; c0 < recs[e].k + recs[e].nN; c0 += kSolveChunk) items.push_back({e - ph.wrec[w], c0});
+            ph.witem.push_back((int)items.size());
+          }
           ph.nitems = (int)items.size();
           ph.items.alloc(std::max<size_t>(1, items.size()) * sizeof(SolveItem), st);
           if (!items.empty())
@@ -2746,7 +2794,9 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
       prob(kn, Q, R.r, kOpN, F + R.Lp, kn, W + L[e].z, R.r, W + L[e].dsn, kn);
     }
     run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
-    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 1, st);
+    for (int w = 0; w < ph.nwaves(); ++w)
+      launch_sweep_move(ph.recs.as<BoxRec>() + ph.wrec[w], dL + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
+                        ph.idx.as<int>(), y, ldy, Q, W, 1, st);
     keep.push_back(std::move(s.dev));
   }
   // ---- root: y[B_t] ← A_t⁻¹ y[B_t] (LU triangular solves)
@@ -2781,7 +2831,9 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
       if (R.k > 0) prob(R.k, Q, R.r, kOpN, F + R.T, R.k, W + L[e].yr, R.r, W + L[e].dsn, R.k);
     }
     run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
-    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 2, st);
+    for (int w = 0; w < ph.nwaves(); ++w)
+      launch_sweep_move(ph.recs.as<BoxRec>() + ph.wrec[w], dL + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
+                        ph.idx.as<int>(), y, ldy, Q, W, 2, st);
     keep.push_back(std::move(s.dev));
   }
   P.end(id, st);
@@ -2800,6 +2852,24 @@ int sweep_chunk(const fmmlu_handle* h, int nrhs) {
   return (int)std::max<size_t>(kGemmSolveMin, std::min<size_t>({(size_t)nrhs, cap, (size_t)1024}));
 }
 
+// The per-box solve sweeps: V⁻¹ phase by phase, the root, W⁻¹ in reverse; each
+// phase's kernels run once per sub-wave (one wave unless deterministic).  scr: Σr × nrhs scratch.
+void sweeps_boxes(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cplx* scr, cudaStream_t st) {
+  for (auto& ph : h->phases)
+    for (int w = 0; w < ph.nwaves(); ++w)
+      launch_solve_up2(ph.recs.as<BoxRec>() + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
+                       ph.items.as<SolveItem>() + ph.witem[w], ph.witem[w + 1] - ph.witem[w], ph.fac.as<cplx>(),
+                       ph.idx.as<int>(), y, ldy, nrhs, scr, st, ph.kmax, ph.rmax);
+  root_solve(h, y, ldy, nrhs, st);
+  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
+    FMMLU_CUDA(cudaMemsetAsync(scr, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
+    for (int w = it->nwaves() - 1; w >= 0; --w)
+      launch_solve_down2(it->recs.as<BoxRec>() + it->wrec[w], it->wrec[w + 1] - it->wrec[w],
+                         it->items.as<SolveItem>() + it->witem[w], it->witem[w + 1] - it->witem[w],
+                         it->fac.as<cplx>(), it->idx.as<int>(), y, ldy, nrhs, scr, st, it->rmax, it->kmax);
+  }
+}
+
 void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   cudaStream_t st = h->stream;
   const int n = (int)h->n;
@@ -2816,7 +2886,9 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   Prof& P = h->prof;
   int sid = P.begin(FMMLU_K_SOLVE, st);
   launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
-  if (nrhs >= kGemmSolveMin) {  // many right-hand sides: the sweeps as batched DMMA GEMMs
+  // many right-hand sides: the sweeps as batched DMMA GEMMs; also the deterministic path (the
+  // per-box kernels split a box's product over CTAs that meet in fp64 atomics)
+  if (nrhs >= kGemmSolveMin || is_deterministic(h)) {
     P.end(sid, st);
     const int qc = sweep_chunk(h, nrhs);
     for (int q0 = 0; q0 < nrhs; q0 += qc) sweeps_gemm(h, yp + (size_t)q0 * n, n, std::min(qc, nrhs - q0));
@@ -2833,15 +2905,7 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
   DBuf scr;
   scr.alloc(scr_rows * nrhs * sizeof(cplx), st);
-  for (auto& ph : h->phases)
-    launch_solve_up2(ph.recs.as<BoxRec>(), ph.nrec, ph.items.as<SolveItem>(), ph.nitems, ph.fac.as<cplx>(),
-                     ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.kmax, ph.rmax);
-  root_solve(h, yp, n, nrhs, st);
-  for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
-    FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
-    launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
-                       it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax, it->kmax);
-  }
+  sweeps_boxes(h, yp, n, nrhs, scr.as<cplx>(), st);
   launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
   P.end(sid, st);
   {
@@ -2923,16 +2987,20 @@ void apply_impl(fmmlu_handle* h, void* xio, int nrhs) {
   scr.alloc(scr_rows * nrhs * sizeof(cplx), st);
   for (auto& ph : h->phases) {  // W_M⋯W₁ x: W₁ first
     FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)ph.tmp_rows * nrhs * sizeof(cplx), st));
-    launch_apply_w(ph.recs.as<BoxRec>(), ph.nrec, ph.items.as<SolveItem>(), ph.nitems, ph.fac.as<cplx>(),
-                   ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.rmax, ph.kmax);
+    for (int w = 0; w < ph.nwaves(); ++w)
+      launch_apply_w(ph.recs.as<BoxRec>() + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
+                     ph.items.as<SolveItem>() + ph.witem[w], ph.witem[w + 1] - ph.witem[w], ph.fac.as<cplx>(),
+                     ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.rmax, ph.kmax);
   }
   for (auto& ph : h->phases)  // D on the R blocks
     launch_apply_d(ph.ap_recs.as<BoxRec>(), ph.nrec, ph.ap_xs.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs,
                    scr.as<cplx>(), st, ph.rmax);
   root_fwd(h, yp, n, nrhs, st);  // P_t A_{B_tB_t} P_tᵀ from the stored L·U
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it)  // V₁⋯V_M: V_M first
-    launch_apply_v(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems, it->fac.as<cplx>(),
-                   it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax);
+    for (int w = it->nwaves() - 1; w >= 0; --w)
+      launch_apply_v(it->recs.as<BoxRec>() + it->wrec[w], it->wrec[w + 1] - it->wrec[w],
+                     it->items.as<SolveItem>() + it->witem[w], it->witem[w + 1] - it->witem[w], it->fac.as<cplx>(),
+                     it->idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, it->rmax);
   launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);  // W^{-½}, caller order
   P.end(sid, st);
   {
@@ -3483,12 +3551,17 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     h->geo.alloc(7 * (size_t)n * sizeof(double), st);
     h->perm.alloc(n * sizeof(long long), st);
     launch_tree_gather(P, N, W, n, i_out, q_in, h->geo.as<double>(), h->perm.as<long long>(), q_out, st);
-    std::vector<int> hperm(n), hq(3 * (size_t)n);
+    // boxes: subdivision + 2:1 balance on the device from the sorted keys (devtree.cu); the host
+    // receives the per-level box arrays for the owner / list bookkeeping
+    DevTreeResult dt;
+    int dt_launches = 0;
+    device_octree(k_out, n, leaf_max, st, dt, &dt_launches);
+    std::vector<int> hperm(n);
     FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), i_out, n * sizeof(int), cudaMemcpyDeviceToHost, st));
-    FMMLU_CUDA(cudaMemcpyAsync(hq.data(), q_out, 3 * (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, st));
     FMMLU_CUDA(cudaStreamSynchronize(st));
-    h->tree.build_sorted(hq.data(), hperm.data(), lo, side, n, leaf_max);
-    h->tree_launches = 3 + 9;  // k_tree_scan/keys/gather + CUB onesweep radix sort (histogram + 8 passes)
+    h->tree.build_from_levels(dt.level_n, dt.code, dt.start, dt.end, dt.parent, hperm.data(), lo, side, n, leaf_max);
+    // k_tree_scan/keys/gather + CUB onesweep radix sort (histogram + 8 passes) + device octree
+    h->tree_launches = 3 + 9 + dt_launches;
     double* gp = h->geo.as<double>();
     h->g = Geo{gp, gp + n, gp + 2 * n, gp + 3 * n, gp + 4 * n, gp + 5 * n, gp + 6 * n};
     track(h, h->geo.bytes + h->perm.bytes);
@@ -3571,7 +3644,8 @@ void rcs_impl(fmmlu_handle* h, const double* phis, int nphi, void* Rout) {
     R = dR.as<cplx>();
   }
   FMMLU_CUDA(cudaMemsetAsync(R, 0, (size_t)nphi * sizeof(cplx), st));
-  const int qc = nphi >= kGemmSolveMin ? sweep_chunk(h, nphi) : nphi;
+  const bool gemm_sweeps = nphi >= kGemmSolveMin || is_deterministic(h);
+  const int qc = gemm_sweeps ? sweep_chunk(h, nphi) : nphi;
   DBuf yb;
   yb.alloc((size_t)n * qc * sizeof(cplx), st);
   cplx* y = yb.as<cplx>();
@@ -3580,7 +3654,7 @@ void rcs_impl(fmmlu_handle* h, const double* phis, int nphi, void* Rout) {
     int id = h->prof.begin(FMMLU_K_SOLVE, st);
     launch_plane_wave(h->g, n, h->k, ph + a0, q, y, n, st);
     h->prof.end(id, st);
-    if (q >= kGemmSolveMin) {
+    if (gemm_sweeps) {
       sweeps_gemm(h, y, n, q);
     } else {  // few angles: the per-box solve kernels (the same path as fmmlu_solve)
       size_t scr_rows = 1;
@@ -3588,15 +3662,7 @@ void rcs_impl(fmmlu_handle* h, const double* phis, int nphi, void* Rout) {
       DBuf scr, tmp;
       scr.alloc(scr_rows * q * sizeof(cplx), st);
       id = h->prof.begin(FMMLU_K_SOLVE, st);
-      for (auto& p : h->phases)
-        launch_solve_up2(p.recs.as<BoxRec>(), p.nrec, p.items.as<SolveItem>(), p.nitems, p.fac.as<cplx>(),
-                         p.idx.as<int>(), y, n, q, scr.as<cplx>(), st, p.kmax, p.rmax);
-      root_solve(h, y, n, q, st);
-      for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
-        FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)it->tmp_rows * q * sizeof(cplx), st));
-        launch_solve_down2(it->recs.as<BoxRec>(), it->nrec, it->items.as<SolveItem>(), it->nitems,
-                           it->fac.as<cplx>(), it->idx.as<int>(), y, n, q, scr.as<cplx>(), st, it->rmax, it->kmax);
-      }
+      sweeps_boxes(h, y, n, q, scr.as<cplx>(), st);
       h->prof.end(id, st);
       wait_stream(h, st);
     }
@@ -3802,12 +3868,36 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
   } else if (k == "gj_mode") {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "gj_mode must be 0 or 1");
     h->gj_mode = (int)value;
+  } else if (k == "deterministic") {
+    if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "deterministic must be 0 or 1");
+    h->deterministic = (int)value;
   } else if (k == "proxy_rho") {
     if (!(value > 0.87 && value < 2.5)) return fail(FMMLU_EINVAL, "proxy_rho must lie in (0.87, 2.5)");
     h->rho_factor = value;
   } else {
     return fail(FMMLU_EINVAL, "unknown parameter " + k);
   }
+  return FMMLU_OK;
+}
+
+int fmmlu_tree_boxes(const fmmlu_handle* h, int32_t* nboxes, int32_t* level, int32_t* coord, int32_t* start,
+                     int32_t* end) {
+  if (!h || !nboxes) return fail(FMMLU_EINVAL, "NULL argument");
+  const int nb = (int)h->tree.boxes.size();
+  if (!level && !coord && !start && !end) {
+    *nboxes = nb;
+    return FMMLU_OK;
+  }
+  if (*nboxes < nb) return fail(FMMLU_EINVAL, "box arrays too small");
+  for (int b = 0; b < nb; ++b) {
+    const Box& B = h->tree.boxes[b];
+    if (level) level[b] = B.level;
+    if (coord)
+      for (int a = 0; a < 3; ++a) coord[3 * b + a] = B.c[a];
+    if (start) start[b] = B.start;
+    if (end) end[b] = B.end;
+  }
+  *nboxes = nb;
   return FMMLU_OK;
 }
 

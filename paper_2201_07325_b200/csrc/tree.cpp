@@ -173,6 +173,43 @@ void Tree::build_sorted(const int32_t* q_sorted, const int32_t* perm_, const dou
   build_boxes();
 }
 
+void Tree::build_from_levels(const std::vector<int>& level_n, const std::vector<unsigned long long>& code,
+                             const std::vector<int>& start, const std::vector<int>& end,
+                             const std::vector<int>& parent, const int32_t* perm_, const double lo_[3], double side_,
+                             int64_t n_, int leaf_max_) {
+  n = n_;
+  leaf_max = leaf_max_;
+  for (int a = 0; a < 3; ++a) lo[a] = lo_[a];
+  side = side_;
+  perm.assign(perm_, perm_ + n);
+  q.clear();
+  boxes.clear();
+  by_code.clear();
+  nlevels = (int)level_n.size();
+  levels.assign(nlevels, {});
+  int base = 0, pbase = 0;
+  for (int l = 0; l < nlevels; ++l) {
+    for (int i = 0; i < level_n[l]; ++i) {
+      const size_t g = (size_t)base + i;
+      int c[3] = {0, 0, 0};
+      for (int b = 0; b < l; ++b) {
+        c[0] |= (int)((code[g] >> (3 * b + 2)) & 1) << b;
+        c[1] |= (int)((code[g] >> (3 * b + 1)) & 1) << b;
+        c[2] |= (int)((code[g] >> (3 * b)) & 1) << b;
+      }
+      const int par = l == 0 ? -1 : pbase + parent[g];
+      const int id = add_box(l, c, start[g], end[g], par);
+      levels[l].push_back(id);
+      if (par >= 0) {
+        Box& P = boxes[par];
+        P.child[P.nchild++] = id;
+      }
+    }
+    pbase = base;
+    base += level_n[l];
+  }
+}
+
 void Tree::build_boxes() {
   boxes.clear();
   by_code.clear();

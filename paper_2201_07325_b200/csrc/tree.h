@@ -40,6 +40,11 @@ struct Tree {
   // q_sorted 3n ints, perm n (tree position -> caller index), root cube (lo, side).
   void build_sorted(const int32_t* q_sorted, const int32_t* perm, const double lo_[3], double side_, int64_t n,
                     int leaf_max);
+  // Boxes built on the device (devtree.cu): per level, Morton codes, point ranges and parent
+  // indices within the level above, level-major; box ids are assigned in that order.
+  void build_from_levels(const std::vector<int>& level_n, const std::vector<unsigned long long>& code,
+                         const std::vector<int>& start, const std::vector<int>& end, const std::vector<int>& parent,
+                         const int32_t* perm, const double lo_[3], double side_, int64_t n, int leaf_max);
   // Root cube rule (reading C14): centred at the bounding-box centre, side = max extent × (1 + 1e-12).
   static void root_cube(const double mn[3], const double mx[3], double lo_out[3], double& side_out);
 

@@ -52,7 +52,7 @@ KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur"
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_monostatic_rcs", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
-           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes", "fmmlu_release_cache")
+           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes", "fmmlu_release_cache", "fmmlu_tree_boxes")
 
 
 def lib_path() -> str:
@@ -88,6 +88,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_inverse_batch.argtypes = [vp, vp, ci, ci, ctypes.POINTER(cd)]
     L.fmmlu_boxes.argtypes = [vp, vp, vp, vp, ci, ci, ci, cd, cd, cd, ci, cd, vp, vp, ci, vp, vp, vp]
     L.fmmlu_release_cache.argtypes = []
+    L.fmmlu_tree_boxes.argtypes = [vp, vp, vp, vp, vp, vp]
     for f in EXPORTS:
         getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
     _LIB = L
@@ -198,6 +199,19 @@ class FmmLu:
         s = Stats()
         _check(load().fmmlu_stats(self.h, ctypes.byref(s)))
         return s.as_dict()
+
+    def tree_boxes(self) -> dict:
+        """The device-built octree: level, coord (nbox×3), start, end per box (level-major, Morton)."""
+        L = load()
+        nb = ctypes.c_int32(0)
+        _check(L.fmmlu_tree_boxes(self.h, ctypes.byref(nb), None, None, None, None))
+        lev = np.empty(nb.value, dtype=np.int32)
+        crd = np.empty((nb.value, 3), dtype=np.int32)
+        st = np.empty(nb.value, dtype=np.int32)
+        en = np.empty(nb.value, dtype=np.int32)
+        _check(L.fmmlu_tree_boxes(self.h, ctypes.byref(nb), lev.ctypes.data, crd.ctypes.data, st.ctypes.data,
+                                  en.ctypes.data))
+        return dict(level=lev, coord=crd, start=st, end=en)
 
     def tree_perm(self) -> np.ndarray:
         p = np.empty(self.n, dtype=np.int64)

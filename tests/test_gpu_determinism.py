@@ -1,0 +1,65 @@
+"""Deterministic mode (fmmlu_set_param("deterministic", 1)): bitwise run-to-run reproducible factor
+and solve.  The default mode adds Schur updates of same-colour boxes that share a neighbour, and
+split-K Gram partial sums, with fp64 atomics in whatever order the hardware runs them; the
+deterministic mode runs those boxes in sub-waves with disjoint targets (each entry receives at most
+one atomic add per launch, the launches in a fixed order), turns split-K off, and solves with the
+GEMM sweeps whose scatters use the same sub-waves."""
+import math
+
+import numpy as np
+import pytest
+
+import fmmlu_inputs as fi
+from oracle import dense, rss
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2201_07325_b200 import fmmlu
+    fmmlu.load()
+    return fmmlu
+
+
+def _run(F, g, k, eps, leaf, b, det):
+    h = F.FmmLu(g.points, g.normals, g.weights, leaf).set_param("deterministic", det).factor(k, eps)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    st = h.stats()
+    h.close()
+    return x, st
+
+
+@pytest.mark.parametrize("nrhs", [3, 40])
+def test_deterministic_mode_is_bitwise_reproducible(F, nrhs):
+    g = fi.ellipsoid(8000)
+    k, eps, leaf = 2 * math.pi, 1e-6, 64
+    b = fi.gaussian_rhs(g.n, nrhs, 5)
+    x1, s1 = _run(F, g, k, eps, leaf, b, 1)
+    x2, s2 = _run(F, g, k, eps, leaf, b, 1)
+    assert s1["n0"] == s2["n0"] and list(s1["ranks_sum"]) == list(s2["ranks_sum"])
+    assert np.array_equal(x1.view(np.float64), x2.view(np.float64))   # bit for bit
+    # and it is the same method: residual ≤ 10ε against the brute-force matvec
+    assert dense.residual(g.points, g.normals, g.weights, k, x1[:, :3], b[:, :3]) <= 10 * eps
+
+
+def test_deterministic_mode_matches_oracle(F):
+    g = fi.ellipsoid(3000)
+    k, eps, leaf = 2 * math.pi, 1e-6, 32
+    b = fi.gaussian_rhs(g.n, 2, 1)
+    x, st = _run(F, g, k, eps, leaf, b, 1)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf)
+    assert dense.rel_diff(x, rss.solve(f, b)) <= 10 * eps
+    assert abs(st["n0"] - f.stats["n0"]) <= 0.05 * f.stats["n0"] + 2
+
+
+def test_deterministic_param_validation(F):
+    g = fi.fibonacci_sphere(200)
+    h = F.FmmLu(g.points, g.normals, g.weights, 16)
+    with pytest.raises(F.FmmluError) as e:
+        h.set_param("deterministic", 2)
+    assert e.value.code == -1

@@ -39,6 +39,32 @@ def test_tree_order_matches_oracle(F):
     assert s["nlevels"] == t.nlevels and s["nboxes"] == len(t.level)
 
 
+@pytest.mark.parametrize("case", ["bump", "cube", "corners", "single", "ellipsoid_s8"])
+def test_device_tree_equals_oracle_tree(F, case):
+    """a1 (reading C14): the octree built on the device (subdivision while a box
+    holds more than s points, 2:1 balance to a fixed point) has exactly the oracle's boxes: per level
+    the same cells, in Morton order, with the same point ranges in tree order."""
+    from oracle.tree import Tree
+    if case == "bump":
+        g, s = fi.bump_sphere(n_base=3000, n_cap=1500, theta_c=0.05, height=0.02), 16
+    elif case == "cube":
+        g, s = fi.random_cube(2000, seed=3), 8
+    elif case == "corners":
+        g, s = fi.cube_corners(), 1
+    elif case == "single":
+        g, s = fi.fibonacci_sphere(40), 64
+    else:
+        g, s = fi.ellipsoid(6000), 8
+    h = F.FmmLu(g.points, g.normals, g.weights, s)
+    d = h.tree_boxes()
+    t = Tree(g.points, s)
+    assert np.array_equal(h.tree_perm(), t.perm)
+    ours = [(int(l), tuple(int(x) for x in c), int(a), int(e))
+            for l, c, a, e in zip(d["level"], d["coord"], d["start"], d["end"])]
+    ref = [(t.level[b], tuple(t.coord[b]), t.start[b], t.end[b]) for lvl in t.levels for b in lvl]
+    assert ours == ref
+
+
 def test_matvec_kernel_parity(F):
     g = fi.ellipsoid(1500)
     k = 2 * math.pi
