@@ -1757,111 +1757,106 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     const double sg = std::sqrt(4.0 * M_PI * rho * rho / ngamma);
 
     lap(1);
-    for (int colour = 0; colour < 8; ++colour) {
-      lap(7);
-      // ------------------------------------------------ boxes of this phase
-      struct BoxJob {
-        int a;  // local owner index of B
-        int b;
-        std::vector<int> N, Q;  // local owner indices
-        int nN = 0, nQ = 0;
-        bool proxy = false;
-        int m = 0;
-        long long Moff = 0, Toff = 0;
-        int permoff = 0;
-        int k = 0;
-        int mfin = 0;  // rows of the matrix the pivoted pass ran on
-      };
+    struct BoxJob {
+      int a;  // local owner index of B
+      int b;
+      std::vector<int> N, Q;  // local owner indices
+      int nN = 0, nQ = 0;
+      bool proxy = false;
+      int m = 0;
+      long long Moff = 0, Toff = 0;
+      int permoff = 0;
+      int k = 0;
+      int mfin = 0;  // rows of the matrix the pivoted pass ran on
+    };
+    struct Cnt { int maps, cps, pts, gidx; };
+    // Host-only preparation of a colour phase's ID stage (its boxes, M layout, gather and proxy
+    // tasks).  It depends on the previous phase only through the current actives, so it runs on a
+    // worker thread while the previous phase's elimination is prepared and launched (PAPER.md
+    // L878-884: the phases of a level are sequential; only the host bookkeeping is overlapped).
+    struct IdPrep {
+      int colour = 8;  // 8: no further phase at this level
       std::vector<BoxJob> jobs;
-      for (int bx : T.levels[lvl]) {
-        if (T.colour(bx) != colour) continue;
-        int a = cur.local(bx);
-        int b = (int)curpos[a].size();
-        if (b == 0) continue;
-        BoxJob J;
-        J.a = a;
-        J.b = b;
-        for (int o : cur.tp->boxN[a])
-          if (!curpos[o].empty()) {
-            J.N.push_back(o);
-            J.nN += (int)curpos[o].size();
-          }
-        for (int o : cur.tp->boxQ[a])
-          if (!curpos[o].empty()) {
-            J.Q.push_back(o);
-            J.nQ += (int)curpos[o].size();
-          }
-        long long nF = total_active - b - J.nN;
-        if (nF == 0) continue;  // F = ∅ → S = B (reading C12)
-        long long nP = nF - J.nQ;
-        J.proxy = nP > 0;
-        J.m = 2 * J.nQ + (J.proxy ? 2 * ngamma : 0);
-        jobs.push_back(std::move(J));
-      }
-      if (jobs.empty()) continue;
-      if (trace) {
-        int bmx = 0, mmx = 0, nmx = 0;
-        for (auto& J : jobs) {
-          bmx = std::max(bmx, J.b);
-          mmx = std::max(mmx, J.m);
-          nmx = std::max(nmx, J.nN);
-        }
-        fprintf(stderr, "[fmmlu] L%d c%d boxes %zu bmax %d mmax %d nNmax %d ngamma %d mem %.2f GB t %.1f ms\n", lvl,
-                colour, jobs.size(), bmx, mmx, nmx, ngamma, h->cur_bytes / 1e9, now_ms() - tl0);
-      }
-      const int nj = (int)jobs.size();
-
-      lap(2);
-      gmark(0);
-      // ------------------------------------------------ ID stage
       long long wsM = 0, wsT = 0;
       int permtot = 0, bmax = 0;
-      for (auto& J : jobs) {
-        J.Moff = wsM;
-        wsM += (long long)J.m * J.b;
-        J.Toff = wsT;
-        wsT += (long long)(J.b / 2 + 1) * (J.b - J.b / 2 + 1);
-        J.permoff = permtot;
-        permtot += J.b;
-        bmax = std::max(bmax, J.b);
-      }
-      // Gram path: M is only needed until its Gram matrix is formed, so it is gathered in waves of
-      // ≤ FMMLU_M_WAVE_GB (default 4 GB) and each wave's G_j = M_jᴴM_j accumulated before the next
-      // (cfg5 level 6 would otherwise hold ≈ 30 GB of M at once).
-      const bool gram_waves = id_uses_gram(h, eps, bmax);
-      std::vector<int> wave_start{0};
-      if (gram_waves) {
-        static const double wave_gb = getenv("FMMLU_M_WAVE_GB") ? atof(getenv("FMMLU_M_WAVE_GB")) : 4.0;
-        const long long cap = std::max<long long>(1, (long long)(wave_gb * 1e9 / sizeof(cplx)));
-        long long w = 0, wmax = 0;
-        for (int j = 0; j < nj; ++j) {
-          const long long sz = (long long)jobs[j].m * jobs[j].b;
-          if (w > 0 && w + sz > cap) {
-            wave_start.push_back(j);
-            w = 0;
-          }
-          jobs[j].Moff = w;
-          w += sz;
-          wmax = std::max(wmax, w);
+      bool gram_waves = false;
+      std::vector<int> wave_start;
+      std::vector<Cnt> at;
+      std::vector<CopyTask> cps;
+      std::vector<int> maps;
+      std::vector<ProxyTask> pts;
+      std::vector<int> gidx;
+      double t_jobs = 0, t_tasks = 0;
+    };
+    auto prep_id = [&](int c0) -> IdPrep {
+      IdPrep P;
+      for (int colour = c0; colour < 8; ++colour) {
+        const double t0 = now_ms();
+        std::vector<BoxJob> jobs;
+        for (int bx : T.levels[lvl]) {
+          if (T.colour(bx) != colour) continue;
+          int a = cur.local(bx);
+          int b = (int)curpos[a].size();
+          if (b == 0) continue;
+          BoxJob J;
+          J.a = a;
+          J.b = b;
+          for (int o : cur.tp->boxN[a])
+            if (!curpos[o].empty()) {
+              J.N.push_back(o);
+              J.nN += (int)curpos[o].size();
+            }
+          for (int o : cur.tp->boxQ[a])
+            if (!curpos[o].empty()) {
+              J.Q.push_back(o);
+              J.nQ += (int)curpos[o].size();
+            }
+          long long nF = total_active - b - J.nN;
+          if (nF == 0) continue;  // F = ∅ → S = B (reading C12)
+          long long nP = nF - J.nQ;
+          J.proxy = nP > 0;
+          J.m = 2 * J.nQ + (J.proxy ? 2 * ngamma : 0);
+          jobs.push_back(std::move(J));
         }
-        wsM = wmax;
-      }
-      wave_start.push_back(nj);
-      DBuf M, Tb, permd, kd;
-      borrow_ws(h, 2, M, std::max<long long>(wsM, 1) * sizeof(cplx), st);
-      borrow_ws(h, 3, Tb, std::max<long long>(wsT, 1) * sizeof(cplx), st);
-      permd.alloc((size_t)permtot * sizeof(int), st);
-      kd.alloc((size_t)nj * sizeof(int), st);
-      track(h, M.bytes + Tb.bytes);
-      {
-        std::vector<CopyTask> cps;
-        std::vector<int> maps;
-        std::vector<ProxyTask> pts;
-        std::vector<IdTask> ids(nj);
-        std::vector<int> gidx;
+        P.t_jobs += now_ms() - t0;
+        if (jobs.empty()) continue;
+        const double t1 = now_ms();
+        P.colour = colour;
+        const int nj = (int)jobs.size();
+        for (auto& J : jobs) {
+          J.Moff = P.wsM;
+          P.wsM += (long long)J.m * J.b;
+          J.Toff = P.wsT;
+          P.wsT += (long long)(J.b / 2 + 1) * (J.b - J.b / 2 + 1);
+          J.permoff = P.permtot;
+          P.permtot += J.b;
+          P.bmax = std::max(P.bmax, J.b);
+        }
+        // Gram path: M is only needed until its Gram matrix is formed, so it is gathered in waves of
+        // ≤ FMMLU_M_WAVE_GB (default 4 GB) and each wave's G_j = M_jᴴM_j accumulated before the next
+        // (cfg5 level 6 would otherwise hold ≈ 30 GB of M at once).
+        P.gram_waves = id_uses_gram(h, eps, P.bmax);
+        P.wave_start.assign(1, 0);
+        if (P.gram_waves) {
+          static const double wave_gb = getenv("FMMLU_M_WAVE_GB") ? atof(getenv("FMMLU_M_WAVE_GB")) : 4.0;
+          const long long cap = std::max<long long>(1, (long long)(wave_gb * 1e9 / sizeof(cplx)));
+          long long w = 0, wmax = 0;
+          for (int j = 0; j < nj; ++j) {
+            const long long sz = (long long)jobs[j].m * jobs[j].b;
+            if (w > 0 && w + sz > cap) {
+              P.wave_start.push_back(j);
+              w = 0;
+            }
+            jobs[j].Moff = w;
+            w += sz;
+            wmax = std::max(wmax, w);
+          }
+          P.wsM = wmax;
+        }
+        P.wave_start.push_back(nj);
         // pass 1: per-box offsets into every array;  pass 2: fill on the host worker pool
-        struct Cnt { int maps, cps, pts, gidx; };
-        std::vector<Cnt> at(nj + 1);
+        std::vector<Cnt>& at = P.at;
+        at.resize(nj + 1);
         {
           Cnt c{0, 0, 0, 0};
           for (int j = 0; j < nj; ++j) {
@@ -1869,7 +1864,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             const BoxJob& J = jobs[j];
             for (int q : J.Q) {
               if (!ident[q]) c.maps += 2 * (int)curpos[q].size();
-              c.cps += 2 * copy_tiles((int)curpos[q].size(), J.b);  // pre-split into 64×64 tiles
+              c.cps += 2 * copy_tiles((int)curpos[q].size(), J.b);
             }
             if (J.proxy) {
               c.pts += 1;
@@ -1877,11 +1872,15 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             }
           }
           at[nj] = c;
-          maps.resize(c.maps);
-          cps.resize(c.cps);
-          pts.resize(c.pts);
-          gidx.resize(c.gidx);
+          P.maps.resize(c.maps);
+          P.cps.resize(c.cps);
+          P.pts.resize(c.pts);
+          P.gidx.resize(c.gidx);
         }
+        std::vector<CopyTask>& cps = P.cps;
+        std::vector<int>& maps = P.maps;
+        std::vector<ProxyTask>& pts = P.pts;
+        std::vector<int>& gidx = P.gidx;
         HostPool::get().parallel_for(nj, 8, [&](int j0, int j1) {
           for (int j = j0; j < j1; ++j) {
             BoxJob& J = jobs[j];
@@ -1943,19 +1942,54 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               p.sg = sg;
               pts[at[j].pts] = p;
             }
-            IdTask it{};
-            it.Mp = nullptr;
-            it.m = J.m;
-            it.b = J.b;
-            it.out_off = J.permoff;
-            it.T = J.Toff;
-            ids[j] = it;
           }
         });
         if (maps.empty()) maps.push_back(0);
         if (gidx.empty()) gidx.push_back(0);
+        P.jobs = std::move(jobs);
+        P.t_tasks = now_ms() - t1;
+        return P;
+      }
+      return P;
+    };
+    IdPrep nextp = prep_id(0);
+    while (nextp.colour < 8) {
+      IdPrep IP = std::move(nextp);
+      nextp = IdPrep{};
+      const int colour = IP.colour;
+      std::vector<BoxJob>& jobs = IP.jobs;
+      tr[2] += IP.t_jobs;
+      tr[8] += IP.t_tasks;
+      lap(7);
+      if (trace) {
+        int bmx = 0, mmx = 0, nmx = 0;
+        for (auto& J : jobs) {
+          bmx = std::max(bmx, J.b);
+          mmx = std::max(mmx, J.m);
+          nmx = std::max(nmx, J.nN);
+        }
+        fprintf(stderr, "[fmmlu] L%d c%d boxes %zu bmax %d mmax %d nNmax %d ngamma %d mem %.2f GB t %.1f ms\n", lvl,
+                colour, jobs.size(), bmx, mmx, nmx, ngamma, h->cur_bytes / 1e9, now_ms() - tl0);
+      }
+      const int nj = (int)jobs.size();
+      const int permtot = IP.permtot;
+      const bool gram_waves = IP.gram_waves;
+      const std::vector<int>& wave_start = IP.wave_start;
+      const std::vector<Cnt>& at = IP.at;
+
+      gmark(0);
+      // ------------------------------------------------ ID stage
+      DBuf M, Tb, permd, kd;
+      borrow_ws(h, 2, M, std::max<long long>(IP.wsM, 1) * sizeof(cplx), st);
+      borrow_ws(h, 3, Tb, std::max<long long>(IP.wsT, 1) * sizeof(cplx), st);
+      permd.alloc((size_t)permtot * sizeof(int), st);
+      kd.alloc((size_t)nj * sizeof(int), st);
+      track(h, M.bytes + Tb.bytes);
+      {
+        std::vector<CopyTask>& cps = IP.cps;
+        std::vector<ProxyTask>& pts = IP.pts;
         Stage s;
-        size_t o_c = s.add(cps), o_m = s.add(maps), o_p = s.add(pts), o_g = s.add(gidx);
+        size_t o_c = s.add(cps), o_m = s.add(IP.maps), o_p = s.add(pts), o_g = s.add(IP.gidx);
         s.upload(st);
         lap(8);
         const int nwaves = (int)wave_start.size() - 1;
@@ -2033,6 +2067,20 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       std::vector<DBuf> idkeep;
       idkeep.swap(keep);
       track(h, -(long long)M.bytes);
+      // update current actives: B keeps its skeleton S (sorted); then the next phase's ID stage can
+      // be prepared (worker thread) while this phase's elimination is prepared and launched here
+      for (int j = 0; j < nj; ++j) {
+        BoxJob& J = jobs[j];
+        J.k = hk[j];
+        if (J.k == J.b) continue;
+        const int* pm = &hperm[J.permoff];
+        std::vector<int> sk(pm, pm + J.k);
+        std::sort(sk.begin(), sk.end());
+        total_active -= (J.b - J.k);
+        curpos[J.a] = sk;
+        ident[J.a] = 0;
+      }
+      std::future<IdPrep> next_fut = std::async(std::launch::async, prep_id, colour + 1);
 
       lap(3);
       // ------------------------------------------------ elimination stage
@@ -2493,20 +2541,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       }
       if (prof_done) h->prof.resolve_first(prof_done);
       lap(4);
-      // update current actives: B keeps its skeleton S (sorted)
-      for (int j = 0; j < nj; ++j) {
-        BoxJob& J = jobs[j];
-        if (J.k == J.b) continue;
-        const int* pm = &hperm[J.permoff];
-        std::vector<int> sk(pm, pm + J.k);
-        std::sort(sk.begin(), sk.end());
-        total_active -= (J.b - J.k);
-        curpos[J.a] = sk;
-        ident[J.a] = 0;
-      }
       track(h, -(long long)Tb.bytes);
       Tb.release();
       keep.clear();
+      nextp = next_fut.get();
+      lap(22);
     }
     lap(5);
     // carry state to the next (coarser) level
@@ -2536,9 +2575,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     fprintf(stderr, "[fmmlu] host ms: level-setup %.1f build-tasks %.1f phase-jobs %.1f id %.1f elim %.1f "
                     "update %.1f carry %.1f other %.1f | id: tasks %.1f gatherlaunch %.1f gram %.1f prep %.1f "
                     "pchol %.1f rest %.1f | topo %.1f acts %.1f | elim: sizes %.1f alloc %.1f tasks %.1f "
-                    "upload %.1f EF %.1f inv-panel-schur %.1f recs %.1f | wait %.1f\n",
+                    "upload %.1f EF %.1f inv-panel-schur %.1f recs %.1f | next-prep wait %.1f | wait %.1f\n",
             tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8], tr[9], tr[10], tr[11], tr[12], tr[13],
-            tr[14], tr[15], tr[16], tr[17], tr[18], tr[19], tr[20], tr[21], tr[4], S.t_sync_wait_ms);
+            tr[14], tr[15], tr[16], tr[17], tr[18], tr[19], tr[20], tr[21], tr[22], S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root
   gmark(4);
   double tr0 = now_ms();

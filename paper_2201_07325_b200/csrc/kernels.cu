@@ -1576,7 +1576,10 @@ __global__ void k_pchol_big_finish(const PcholBig* __restrict__ tasks, int* __re
 
 // ------------------------------------------------------------------ solve sweeps
 constexpr int SV_NT = 256;
-constexpr int SV_Q = 4;  // RHS processed per pass
+#ifndef FMMLU_SV_Q
+#define FMMLU_SV_Q 4
+#endif
+constexpr int SV_Q = FMMLU_SV_Q;  // RHS processed per pass
 constexpr int SV_U = 8;  // factor loads in flight per thread in the solve products
 
 // ---- split solve kernels (more CTAs per box; the factor store is streamed once)

@@ -56,7 +56,7 @@ EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_mo
 
 
 def lib_path() -> str:
-    return _build.LIB
+    return os.environ.get("FMMLU_LIB") or _build.LIB  # FMMLU_LIB: an alternative build (experiments)
 
 
 def load(build_if_missing: bool = False):
