@@ -425,23 +425,43 @@ void drop_arena(cudaStream_t st) {  // before destroying a stream: free its chun
   tl_devarena.erase(it);
 }
 
-// Collects host arrays and uploads them in one H2D copy.
+// Collects host arrays and uploads them in one H2D copy.  With reserve_pinned(bytes) the arrays are
+// collected straight into pinned staging (one host copy fewer for the large per-phase uploads).
 struct Stage {
   std::vector<char> host;
+  char* pin = nullptr;
+  size_t pin_cap = 0, pin_used = 0;
   DBuf dev;
+  void reserve_pinned(size_t bytes) {
+    pin_cap = bytes + 16 * 64;
+    pin = tl_pin.get(pin_cap);
+    pin_used = 0;
+  }
   template <class T> size_t add(const std::vector<T>& v) {
+    if (pin) {
+      size_t off = (pin_used + 15) & ~size_t(15);
+      if (off + v.size() * sizeof(T) > pin_cap) throw Error(FMMLU_ECUDA, "staging reservation too small");
+      if (!v.empty()) std::memcpy(pin + off, v.data(), v.size() * sizeof(T));
+      pin_used = off + v.size() * sizeof(T);
+      return off;
+    }
     size_t off = (host.size() + 15) & ~size_t(15);
     host.resize(off + v.size() * sizeof(T));
     if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
     return off;
   }
   void upload(cudaStream_t s) {
+    const size_t n = pin ? pin_used : host.size();
     dev.release();
-    dev.p = tl_devarena[s].get(host.size() + 16, s);
-    dev.bytes = host.size() + 16;
+    dev.p = tl_devarena[s].get(n + 16, s);
+    dev.bytes = n + 16;
     dev.st = s;
     dev.borrowed = true;
-    h2d(dev.p, host.data(), host.size(), s);
+    if (pin) {
+      if (n) FMMLU_CUDA(cudaMemcpyAsync(dev.p, pin, n, cudaMemcpyHostToDevice, s));
+    } else {
+      h2d(dev.p, host.data(), host.size(), s);
+    }
   }
   void upload_owned(cudaStream_t s) {  // own allocation: for data that outlives the next sync
     dev.alloc(host.size() + 16, s);
@@ -1989,6 +2009,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::vector<CopyTask>& cps = IP.cps;
         std::vector<ProxyTask>& pts = IP.pts;
         Stage s;
+        s.reserve_pinned(sizeof(CopyTask) * cps.size() + sizeof(int) * (IP.maps.size() + IP.gidx.size()) +
+                         sizeof(ProxyTask) * pts.size());
         size_t o_c = s.add(cps), o_m = s.add(IP.maps), o_p = s.add(pts), o_g = s.add(IP.gidx);
         s.upload(st);
         lap(8);
@@ -2385,9 +2407,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (fbld.empty()) fbld.push_back(0);
         lap(18);
         Stage s;
-        s.host.reserve(16 * 12 + sizeof(CopyTask) * (cps.size() + cpsT.size() + cpsX.size()) +
-                       sizeof(int) * (maps.size() + fslot.size() + fpos.size() + fbld.size() + gjdim.size()) +
-                       sizeof(long long) * (ftab.size() + gjoff.size()) + sizeof(BoxRec) * recs.size());
+        s.reserve_pinned(16 * 12 + sizeof(CopyTask) * (cps.size() + cpsT.size() + cpsX.size()) +
+                         sizeof(int) * (maps.size() + fslot.size() + fpos.size() + fbld.size() + gjdim.size()) +
+                         sizeof(long long) * (ftab.size() + gjoff.size()) + sizeof(BoxRec) * recs.size());
         size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_fs = s.add(fslot),
                o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
                o_rec = s.add(recs);
