@@ -715,24 +715,42 @@ constexpr int kTile = 64;
 
 // upper = true: only output tiles with tile-row ≤ tile-column (Hermitian results).  One group per
 // problem; the 64×64 tile list is expanded on the device (gemm_run).
-void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& groups, const GemmProblem& p,
+void add_gemm(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& groups, const GemmProblem& p0,
               bool upper = false) {
+  GemmProblem p = p0;
+  // 32-wide output tiles for skinny plain stores (the multi-RHS solve sweeps: n = nrhs ≤ 32)
+  p.bn = (p.n <= 32 && p.slot == nullptr && !upper) ? 32 : 64;
   const int cnt = gemm_tile_count(p, upper);
   if (cnt <= 0) return;
   const int first = groups.empty() ? 0 : groups.back().first + groups.back().count;
   groups.push_back(GemmGroup{(int)probs.size(), first, cnt, upper ? 1 : 0});
   probs.push_back(p);
 }
+// One launch needs one tile width: mixed batches fall back to 64 (tile counts recomputed).
+int unify_bn(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& groups) {
+  if (probs.empty()) return 64;
+  bool all32 = true;
+  for (auto& p : probs) all32 = all32 && p.bn == 32;
+  if (all32) return 32;
+  int first = 0;
+  for (auto& g : groups) {
+    probs[g.p].bn = 64;
+    g.first = first;
+    g.count = gemm_tile_count(probs[g.p], g.upper != 0);
+    first += g.count;
+  }
+  return 64;
+}
 long long group_tiles(const GemmGroup* g, size_t n) { return n ? (long long)g[n - 1].first + g[n - 1].count : 0; }
 
 // Expand the groups' tiles into a stream-ordered scratch list and run the batched GEMM.
 void gemm_run(const GemmProblem* d_probs, const GemmGroup* d_groups, int ngroups, long long ntiles, cplx alpha,
-              int scatter, cplx* bsr, cudaStream_t st) {
+              int scatter, cplx* bsr, cudaStream_t st, int bn = 64) {
   if (ntiles <= 0) return;
   DBuf tb;
   tb.alloc((size_t)ntiles * sizeof(GemmTile), st);
   gemm_expand(d_probs, d_groups, ngroups, tb.as<GemmTile>(), st);
-  gemm_batched(d_probs, tb.as<GemmTile>(), (int)ntiles, alpha, scatter, bsr, st);
+  gemm_batched(d_probs, tb.as<GemmTile>(), (int)ntiles, alpha, scatter, bsr, st, bn);
 }  // tb is released in stream order after the launches
 
 // Algorithmic work of a batch: 8mnk real flops per complex GEMM; bytes = read A and B once,
@@ -749,6 +767,7 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, c
                int scatter, cplx* bsr, cudaStream_t st, std::vector<DBuf>& keep, Prof& P, int cls,
                double work_scale = 1.0) {
   if (tiles.empty()) return;
+  const int bn = unify_bn(probs, tiles);
   Stage s;
   size_t op = s.add(probs), ot = s.add(tiles);
   s.upload(st);
@@ -758,7 +777,7 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, c
   by *= work_scale;
   int id = P.begin(cls, st);
   gemm_run(s.ptr<GemmProblem>(op), s.ptr<GemmGroup>(ot), (int)tiles.size(), group_tiles(tiles.data(), tiles.size()),
-           alpha, scatter, bsr, st);
+           alpha, scatter, bsr, st, bn);
   P.end(id, st);
   P.add(cls, fl, by, 1);
   keep.push_back(std::move(s.dev));
@@ -770,11 +789,12 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, c
 void gemm_batched_staged(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, cplx alpha,
                          cudaStream_t st, std::vector<DBuf>& keep) {
   if (tiles.empty()) return;
+  const int bn = unify_bn(probs, tiles);
   Stage s;
   size_t op = s.add(probs), ot = s.add(tiles);
   s.upload(st);
   gemm_run(s.ptr<GemmProblem>(op), s.ptr<GemmGroup>(ot), (int)tiles.size(), group_tiles(tiles.data(), tiles.size()),
-           alpha, 0, nullptr, st);
+           alpha, 0, nullptr, st, bn);
   keep.push_back(std::move(s.dev));
   probs.clear();
   tiles.clear();
@@ -890,6 +910,7 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   std::vector<GemmProblem> gp;
   std::vector<GemmGroup> gt;
   std::vector<std::pair<size_t, size_t>> launches;  // (group offset, group count) per panel
+  std::vector<int> lbn;                             // output tile width per panel launch
   for (int j0 = 0; j0 < nmax; j0 += nb) {
     std::vector<GemmProblem> pp;
     std::vector<GemmGroup> tt;
@@ -915,6 +936,7 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
       R.C = t.A + (size_t)(j0 + jb) * t.lda;
       add_gemm(pp, tt, R);
     }
+    lbn.push_back(unify_bn(pp, tt));
     for (auto& x : tt) x.p += (int)gp.size();
     launches.push_back({gt.size(), tt.size()});
     gp.insert(gp.end(), pp.begin(), pp.end());
@@ -939,7 +961,8 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
     nl += 2;
     if (launches[pi].second) {
       gemm_run(s.ptr<GemmProblem>(o_p), s.ptr<GemmGroup>(o_g) + launches[pi].first, (int)launches[pi].second,
-               group_tiles(gt.data() + launches[pi].first, launches[pi].second), cmk(1.0, 0.0), 0, nullptr, st);
+               group_tiles(gt.data() + launches[pi].first, launches[pi].second), cmk(1.0, 0.0), 0, nullptr, st,
+               lbn[pi]);
       ++nl;
     }
   }
@@ -1012,6 +1035,7 @@ void pchol_big(fmmlu_handle* h, cplx* G, const std::vector<long long>& goff, lon
     P.active = &tasks[j].state->active;
     add_gemm(gp, gt, P);
   }
+  const int pbn = unify_bn(gp, gt);
   Stage s;
   size_t o_t = s.add(tasks), o_p = s.add(gp), o_g = s.add(gt);
   s.upload(st);
@@ -1019,7 +1043,7 @@ void pchol_big(fmmlu_handle* h, cplx* G, const std::vector<long long>& goff, lon
   for (int j0 = 0; j0 < bmax; j0 += NB) {
     launch_pchol_big_panel(s.ptr<PcholBig>(o_t), nbx, NB, eps, st, bmax);
     gemm_run(s.ptr<GemmProblem>(o_p), s.ptr<GemmGroup>(o_g), (int)gt.size(), group_tiles(gt.data(), gt.size()),
-             cmk(-1.0, 0.0), 0, nullptr, st);
+             cmk(-1.0, 0.0), 0, nullptr, st, pbn);
   }
   launch_pchol_big_finish(s.ptr<PcholBig>(o_t), nbx, d_perm, d_k, st, bmax);
   h->prof.end(id, st);

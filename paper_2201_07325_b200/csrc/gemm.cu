@@ -19,6 +19,14 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16;
 constexpr int STAGES = FMMLU_GEMM_STAGES;  // cp.async pipeline depth (tiles in flight + 1)
 constexpr int PADA = BM + 2, PADB = BN + 2;  // +2 complex: conflict-free fragment loads
+// Tile width BN_ ∈ {64, 32}: 32 for skinny products (n ≤ 32, e.g. the multi-RHS solve sweeps), where
+// a 64-wide tile would compute half zeros.  8 warps: 2×4 (warp tile 32×16) or 4×2 (16×16).
+template <int BN_> struct TileCfg {
+  static constexpr int WGM = BN_ == 64 ? 2 : 4, WGN = 8 / WGM;
+  static constexpr int WM = BM / WGM, WN = BN_ / WGN;
+  static constexpr int MI = WM / 8, NJ = WN / 8;
+  static constexpr int PADB_ = BN_ + 2;
+};
 constexpr int NT = 256;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -37,8 +45,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+template <int BN_>
 __device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0, int k0, cplx* As,
                                            cplx* Bs, int tid) {
+  constexpr int PB = TileCfg<BN_>::PADB_;
 #pragma unroll
   for (int e = 0; e < (BM * BK) / NT; ++e) {
     int idx = tid + e * NT;
@@ -58,50 +68,52 @@ __device__ __forceinline__ void load_tiles(const GemmProblem& P, int m0, int n0,
     cp_async16(&As[kk * PADA + mm], src, ok);
   }
 #pragma unroll
-  for (int e = 0; e < (BN * BK) / NT; ++e) {
+  for (int e = 0; e < (BN_ * BK) / NT; ++e) {
     int idx = tid + e * NT;
     int nn, kk;
     if (P.opB == kOpN) {
       kk = idx % BK;
       nn = idx / BK;
     } else {  // T or C
-      nn = idx % BN;
-      kk = idx / BN;
+      nn = idx % BN_;
+      kk = idx / BN_;
     }
     int gn = n0 + nn, gk = k0 + kk;
     bool ok = gn < P.n && gk < P.k;
     const cplx* src = ok ? (P.opB == kOpN ? P.B + gk + (size_t)gn * P.ldb
                                           : P.B + gn + (size_t)gk * P.ldb)
                          : P.B;
-    cp_async16(&Bs[kk * PADB + nn], src, ok);
+    cp_async16(&Bs[kk * PB + nn], src, ok);
   }
 }
 
-template <int SCATTER, bool THREEM>
+template <int SCATTER, bool THREEM, int BN_ = 64>
 __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
                                           const GemmTile* __restrict__ tiles, cplx alpha,
                                           cplx* __restrict__ bsr) {
+  using TC = TileCfg<BN_>;
+  constexpr int MI = TC::MI, NJ = TC::NJ, PB = TC::PADB_;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* As = reinterpret_cast<cplx*>(smem_raw);      // [STAGES][BK][PADA]
-  cplx* Bs = As + STAGES * BK * PADA;                // [STAGES][BK][PADB]
+  cplx* Bs = As + STAGES * BK * PADA;                // [STAGES][BK][PB]
   const GemmTile T = tiles[blockIdx.x];
   const GemmProblem P = probs[T.p];
   if (P.active != nullptr && *P.active == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 × 4 warps
-  const int m0 = T.tm * BM, n0 = T.tn * BN;
+  const int wm = warp / TC::WGN, wn = warp % TC::WGN;
+  const int m0 = T.tm * BM, n0 = T.tn * BN_;
   const double sa = P.opA == kOpC ? -1.0 : 1.0;  // conjugation of A / B at fragment load
   const double sb = P.opB == kOpC ? -1.0 : 1.0;
 
   // THREEM: 3-multiplication complex product (P1 = ArBr, P2 = AiBi, P3 = (Ar+Ai)(Br+Bi);
   // Re = P1 − P2, Im = P3 − P1 − P2): 24 instead of 32 DMMAs per k-step on the tensor pipe.
-  double accr[4][2][2], acci[4][2][2];
-  double acc3[4][2][2];
+  double accr[MI][NJ][2], acci[MI][NJ][2];
+  double acc3[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
       acc3[i][j][0] = acc3[i][j][1] = 0.0;
     }
@@ -113,7 +125,7 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
   // prologue: tiles 0 .. STAGES-2 in flight (one commit group per tile, empty groups past the end)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_tiles(P, m0, n0, kbeg + s * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
+    if (s < nk) load_tiles<BN_>(P, m0, n0, kbeg + s * BK, As + s * BK * PADA, Bs + s * BK * PB, tid);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -121,46 +133,46 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
     __syncthreads();              // ... everybody's; and tile kt-1's buffer is free
     {
       const int kn = kt + STAGES - 1, s = kn % STAGES;
-      if (kn < nk) load_tiles(P, m0, n0, kbeg + kn * BK, As + s * BK * PADA, Bs + s * BK * PADB, tid);
+      if (kn < nk) load_tiles<BN_>(P, m0, n0, kbeg + kn * BK, As + s * BK * PADA, Bs + s * BK * PB, tid);
       cp_async_commit();
     }
     const cplx* as = As + (kt % STAGES) * BK * PADA;
-    const cplx* bs = Bs + (kt % STAGES) * BK * PADB;
+    const cplx* bs = Bs + (kt % STAGES) * BK * PB;
     const int kleft = kend - (kbeg + kt * BK);  // k4 steps past the end are zero-filled: skip them
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       if (ks * 4 >= kleft) break;  // warp-uniform
       const int kk = ks * 4 + t;
-      cplx a[4], b[2];
+      cplx a[MI], b[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a[i] = as[kk * PADA + wm * 32 + i * 8 + g];
+      for (int i = 0; i < MI; ++i) {
+        a[i] = as[kk * PADA + wm * TC::WM + i * 8 + g];
         a[i].y *= sa;
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        b[j] = bs[kk * PADB + wn * 16 + j * 8 + g];
+      for (int j = 0; j < NJ; ++j) {
+        b[j] = bs[kk * PB + wn * TC::WN + j * 8 + g];
         b[j].y *= sb;
       }
       if constexpr (THREEM) {
-      double as_[4], bs_[2];
+      double as_[MI], bs_[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) as_[i] = a[i].x + a[i].y;
+      for (int i = 0; i < MI; ++i) as_[i] = a[i].x + a[i].y;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bs_[j] = b[j].x + b[j].y;
+      for (int j = 0; j < NJ; ++j) bs_[j] = b[j].x + b[j].y;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           dmma(accr[i][j][0], accr[i][j][1], a[i].x, b[j].x);  // P1
           dmma(acci[i][j][0], acci[i][j][1], a[i].y, b[j].y);  // P2
           dmma(acc3[i][j][0], acc3[i][j][1], as_[i], bs_[j]);  // P3
         }
       } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           dmma(accr[i][j][0], accr[i][j][1], a[i].x, b[j].x);
           dmma(accr[i][j][0], accr[i][j][1], a[i].y, -b[j].y);
           dmma(acci[i][j][0], acci[i][j][1], a[i].x, b[j].y);
@@ -171,9 +183,9 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
   }
   if constexpr (THREEM)
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double p1 = accr[i][j][h], p2 = acci[i][j][h];
@@ -199,7 +211,7 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
       rs[e] = r < P.m ? P.slot[P.row0 + r] : 0;
       rp[e] = r < P.m ? P.pos[P.row0 + r] : 0;
     }
-    for (int e = tid; e < BN; e += NT) {
+    for (int e = tid; e < BN_; e += NT) {
       const int c = n0 + e;
       cs[e] = c < P.n ? P.slot[P.col0 + c] : 0;
       cp[e] = c < P.n ? P.pos[P.col0 + c] : 0;
@@ -211,14 +223,14 @@ __device__ __forceinline__ void gemm_body(const GemmProblem* __restrict__ probs,
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + g;
+  for (int i = 0; i < MI; ++i) {
+    const int row = m0 + wm * TC::WM + i * 8 + g;
     if (row >= P.m) continue;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * 16 + j * 8 + 2 * t + h;
+        const int col = n0 + wn * TC::WN + j * 8 + 2 * t + h;
         if (col >= P.n) continue;
         cplx v = cmk(alpha.x * accr[i][j][h] - alpha.y * acci[i][j][h],
                      alpha.x * acci[i][j][h] + alpha.y * accr[i][j][h]);
@@ -251,6 +263,11 @@ __global__ void __launch_bounds__(NT, 2) k_gemm_store(const GemmProblem* __restr
                                                    cplx* __restrict__ bsr) {
   gemm_body<0, true>(probs, tiles, alpha, bsr);
 }
+__global__ void __launch_bounds__(NT, 2) k_gemm_store32(const GemmProblem* __restrict__ probs,
+                                                     const GemmTile* __restrict__ tiles, cplx alpha,
+                                                     cplx* __restrict__ bsr) {
+  gemm_body<0, true, 32>(probs, tiles, alpha, bsr);
+}
 __global__ void __launch_bounds__(NT) k_gemm_schur(const GemmProblem* __restrict__ probs,
                                                    const GemmTile* __restrict__ tiles, cplx alpha,
                                                    cplx* __restrict__ bsr) {
@@ -269,7 +286,8 @@ __global__ void k_gemm_expand(const GemmProblem* __restrict__ probs, const GemmG
   const GemmGroup g = groups[w];
   const GemmProblem& P = probs[g.p];
   const int nks = P.kchunk > 0 ? (P.k + P.kchunk - 1) / P.kchunk : 1;
-  const int ntn = (P.n + BN - 1) / BN;
+  const int bn = P.bn == 32 ? 32 : BN;
+  const int ntn = (P.n + bn - 1) / bn;
   for (int t = lane; t < g.count; t += 32) {
     const int ks = t % nks;
     int r = t / nks, tm = 0, tn;
@@ -292,7 +310,8 @@ __global__ void k_gemm_expand(const GemmProblem* __restrict__ probs, const GemmG
 int gemm_tile_count(const GemmProblem& p, bool upper) {
   if (p.m <= 0 || p.n <= 0 || p.k <= 0) return 0;
   const int nks = p.kchunk > 0 ? (p.k + p.kchunk - 1) / p.kchunk : 1;
-  const int tm = (p.m + BM - 1) / BM, tn = (p.n + BN - 1) / BN;
+  const int bn = p.bn == 32 ? 32 : BN;
+  const int tm = (p.m + BM - 1) / BM, tn = (p.n + bn - 1) / bn;
   if (!upper) return tm * tn * nks;
   int c = 0;
   for (int i = 0; i < tm; ++i) c += std::max(0, tn - i);
@@ -307,12 +326,13 @@ void gemm_expand(const GemmProblem* d_probs, const GemmGroup* d_groups, int ngro
 }
 
 void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
-                  int scatter, cplx* bsr_base, cudaStream_t st) {
+                  int scatter, cplx* bsr_base, cudaStream_t st, int bn) {
   if (ntiles <= 0) return;
   const size_t smem = (size_t)STAGES * BK * (PADA + PADB) * sizeof(cplx);
   static bool init = false;
   if (!init) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_store, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_store32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_schur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FMMLU_CUDA(cudaFuncSetAttribute(k_gemm_schur3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     init = true;
@@ -325,6 +345,8 @@ void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntile
     k_gemm_schur3<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
   else if (scatter)
     k_gemm_schur<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
+  else if (bn == 32)
+    k_gemm_store32<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
   else
     k_gemm_store<<<ntiles, NT, smem, st>>>(d_probs, d_tiles, alpha, bsr_base);
   FMMLU_LAUNCH();

@@ -32,6 +32,7 @@ struct GemmProblem {
   int kchunk;  // split-K: each tile covers K range [ks*kchunk, (ks+1)*kchunk); 0 = whole K.
                // With split-K the kStore epilogue accumulates with fp64 atomics.
   const int* active;  // optional device flag: tile is skipped when *active == 0
+  int bn;             // output tile width: 32 (skinny n ≤ 32 stores) or 64 (0 = 64)
 };
 
 struct GemmTile {
@@ -43,7 +44,7 @@ struct GemmTile {
 
 // C = C + alpha * op(A) op(B) for each problem; `tiles` enumerates 64×64 output tiles.
 void gemm_batched(const GemmProblem* d_probs, const GemmTile* d_tiles, int ntiles, cplx alpha,
-                  int scatter, cplx* bsr_base, cudaStream_t st);
+                  int scatter, cplx* bsr_base, cudaStream_t st, int bn = 64);
 
 // Compact host description of a problem's tiles: tiles [first, first + count) of the launch belong
 // to problem p (upper = 1: only tile rows ≤ tile columns, Hermitian results).  The per-tile list is
