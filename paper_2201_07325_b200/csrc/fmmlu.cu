@@ -1175,7 +1175,7 @@ class HostPool {
 
  private:
   HostPool() {
-    const int n = std::max(0, std::min<int>(7, (int)std::thread::hardware_concurrency() / 2 - 1));
+    const int n = std::max(0, std::min<int>(15, (int)std::thread::hardware_concurrency() / 2 - 1));
     for (int w = 0; w < n; ++w) workers_.emplace_back([this, w] { loop(w); });
     for (auto& t : workers_) t.detach();
   }
