@@ -2940,18 +2940,36 @@ int sweep_chunk(const fmmlu_handle* h, int nrhs) {
 // The per-box solve sweeps: V⁻¹ phase by phase, the root, W⁻¹ in reverse; each
 // phase's kernels run once per sub-wave (one wave unless deterministic).  scr: Σr × nrhs scratch.
 void sweeps_boxes(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cplx* scr, cudaStream_t st) {
+  static const bool trace = getenv("FMMLU_TRACE") != nullptr;
+  cudaEvent_t ev[4];
+  if (trace)
+    for (auto& e : ev) FMMLU_CUDA(cudaEventCreate(&e));
+  if (trace) FMMLU_CUDA(cudaEventRecord(ev[0], st));
   for (auto& ph : h->phases)
     for (int w = 0; w < ph.nwaves(); ++w)
       launch_solve_up2(ph.recs.as<BoxRec>() + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
                        ph.items.as<SolveItem>() + ph.witem[w], ph.witem[w + 1] - ph.witem[w], ph.fac.as<cplx>(),
                        ph.idx.as<int>(), y, ldy, nrhs, scr, st, ph.kmax, ph.rmax);
+  if (trace) FMMLU_CUDA(cudaEventRecord(ev[1], st));
   root_solve(h, y, ldy, nrhs, st);
+  if (trace) FMMLU_CUDA(cudaEventRecord(ev[2], st));
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
     FMMLU_CUDA(cudaMemsetAsync(scr, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
     for (int w = it->nwaves() - 1; w >= 0; --w)
       launch_solve_down2(it->recs.as<BoxRec>() + it->wrec[w], it->wrec[w + 1] - it->wrec[w],
                          it->items.as<SolveItem>() + it->witem[w], it->witem[w + 1] - it->witem[w],
                          it->fac.as<cplx>(), it->idx.as<int>(), y, ldy, nrhs, scr, st, it->rmax, it->kmax);
+  }
+  if (trace) {
+    FMMLU_CUDA(cudaEventRecord(ev[3], st));
+    FMMLU_CUDA(cudaEventSynchronize(ev[3]));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    fprintf(stderr, "[fmmlu] solve (%d RHS, per-box kernels): up %.3f ms, root %.3f ms (n0 %lld), down %.3f ms\n", nrhs,
+            a, b, (long long)h->n0, c);
+    for (auto& e : ev) cudaEventDestroy(e);
   }
 }
 

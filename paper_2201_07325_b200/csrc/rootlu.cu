@@ -282,28 +282,73 @@ __global__ void __launch_bounds__(256) k_lu_diag_inv(const cplx* __restrict__ A,
 // order from *ticket, subtracts M[rows, cols of every earlier block] · Y[those rows] as soon as
 // that block's flag is released, multiplies by its diagonal-block inverse, writes its rows and
 // releases its flag.  flags[nblk] and *ticket must be zero at launch.
-constexpr int TS_NT = 256, TS_Q = 32;
-__global__ void __launch_bounds__(TS_NT) k_lu_trsv(const cplx* __restrict__ A, int lda, int n, int TB,
+constexpr int TS_NT = 256, TS_Q = 32, TS_TB = 64;
+// acc[q][r] −= Σ_c M[r][c]·x[c][q] for r < m, c < mm, q < nq; M (TS_TB × TS_TB, ld TS_TB) and x in
+// shared memory; thread → (row r, group of 8 RHS)
+__device__ __forceinline__ void tile_gemv_sub(const cplx* __restrict__ Ms, const cplx* __restrict__ x,
+                                              cplx* __restrict__ acc, int m, int mm, int nq) {
+  for (int e = threadIdx.x; e < TS_TB * ((nq + 7) / 8); e += TS_NT) {
+    const int r = e % TS_TB, qg = e / TS_TB;
+    if (r >= m) continue;
+    cplx sacc[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc[w] = cmk(0.0, 0.0);
+    for (int c = 0; c < mm; ++c) {
+      const cplx a = Ms[r + c * TS_TB];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc[w] = cfma(a, x[(qg * 8 + w) * TS_TB + c], sacc[w]);
+    }
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int q = qg * 8 + w;
+      if (q < nq) acc[q * TS_TB + r] = csub(acc[q * TS_TB + r], sacc[w]);
+    }
+  }
+}
+// M tile (rows o.., columns oo..) of the n × n column-major A into shared memory: every thread issues
+// its 16 loads before using any (no dependent-latency chain)
+__device__ __forceinline__ void load_tile(const cplx* __restrict__ A, int lda, int o, int m, int oo, int mm,
+                                          cplx* __restrict__ Ms) {
+  cplx v[TS_TB * TS_TB / TS_NT];
+#pragma unroll
+  for (int u = 0; u < TS_TB * TS_TB / TS_NT; ++u) {
+    const int e = threadIdx.x + u * TS_NT, r = e % TS_TB, c = e / TS_TB;
+    v[u] = (r < m && c < mm) ? __ldg(&A[(o + r) + (size_t)(oo + c) * lda]) : cmk(0.0, 0.0);
+  }
+#pragma unroll
+  for (int u = 0; u < TS_TB * TS_TB / TS_NT; ++u) Ms[threadIdx.x + u * TS_NT] = v[u];
+}
+
+// Blocked triangular solve on Y (n × nq, ld ldy, nq ≤ TS_Q) with the LU in A: lower (unit L,
+// forward) or upper (U, backward).  Blocks of TS_TB rows; a CTA takes the next block in dependency
+// order from *ticket (every block it waits on is then already running), and for each earlier block:
+// loads that off-diagonal tile into shared memory (independent of the chain, so it overlaps the
+// wait), waits for the block's release flag, subtracts tile · rows; finally multiplies by its
+// diagonal-block inverse, writes its rows and releases its flag.  flags[nblk], *ticket zero at launch.
+__global__ void __launch_bounds__(TS_NT) k_lu_trsv(const cplx* __restrict__ A, int lda, int n,
                                                    const cplx* __restrict__ Dinv, cplx* Y, int ldy, int nq,
                                                    int upper, int* flags, int* ticket) {
   extern __shared__ __align__(16) unsigned char ts_sh[];
-  cplx* acc = reinterpret_cast<cplx*>(ts_sh);  // [TS_Q][TB]
-  cplx* xb = acc + (size_t)TS_Q * TB;          // [TS_Q][TB] rows of the block being subtracted
+  cplx* acc = reinterpret_cast<cplx*>(ts_sh);  // [TS_Q][TS_TB]
+  cplx* xb = acc + TS_Q * TS_TB;               // [TS_Q][TS_TB] rows of the block being subtracted
+  cplx* Ms = xb + TS_Q * TS_TB;                // [TS_TB][TS_TB] tile
   __shared__ int tk;
-  const int nblk = (n + TB - 1) / TB;
+  const int nblk = (n + TS_TB - 1) / TS_TB;
   if (threadIdx.x == 0) tk = atomicAdd(ticket, 1);
   __syncthreads();
   const int t = tk;
   if (t >= nblk) return;
   const int b = upper ? nblk - 1 - t : t;
-  const int o = b * TB, m = min(TB, n - o);
-  for (int e = threadIdx.x; e < TS_Q * TB; e += TS_NT) {
-    const int r = e % TB, q = e / TB;
+  const int o = b * TS_TB, m = min(TS_TB, n - o);
+  for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) {
+    const int r = e % TS_TB, q = e / TS_TB;
     acc[e] = (r < m && q < nq) ? Y[(o + r) + (size_t)q * ldy] : cmk(0.0, 0.0);
   }
   for (int u = 0; u < t; ++u) {  // dependencies in the order they complete
     const int bb = upper ? nblk - 1 - u : u;
-    const int oo = bb * TB, mm = min(TB, n - oo);
+    const int oo = bb * TS_TB, mm = min(TS_TB, n - oo);
+    __syncthreads();  // previous tile consumed
+    load_tile(A, lda, o, m, oo, mm, Ms);
     if (threadIdx.x == 0) {
       volatile int* f = flags + bb;
       while (*f == 0) {
@@ -311,50 +356,36 @@ __global__ void __launch_bounds__(TS_NT) k_lu_trsv(const cplx* __restrict__ A, i
       __threadfence();
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < TS_Q * TB; e += TS_NT) {
-      const int r = e % TB, q = e / TB;
+    for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) {
+      const int r = e % TS_TB, q = e / TS_TB;
       xb[e] = (r < mm && q < nq) ? __ldcg(&Y[(oo + r) + (size_t)q * ldy]) : cmk(0.0, 0.0);
     }
     __syncthreads();
-    // acc[r][q] −= Σ_c A[o + r, oo + c] · xb[c][q]; thread → row r, RHS group
-    for (int e = threadIdx.x; e < TB * ((nq + 7) / 8); e += TS_NT) {
-      const int r = e % TB, qg = e / TB;
-      if (r >= m) continue;
-      cplx s[8];
-#pragma unroll
-      for (int w = 0; w < 8; ++w) s[w] = cmk(0.0, 0.0);
-      const cplx* col = A + (o + r) + (size_t)oo * lda;
-      for (int c = 0; c < mm; ++c) {
-        const cplx a = col[(size_t)c * lda];
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s[w] = cfma(a, xb[(size_t)(qg * 8 + w) * TB + c], s[w]);
-      }
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int q = qg * 8 + w;
-        if (q < nq) acc[(size_t)q * TB + r] = csub(acc[(size_t)q * TB + r], s[w]);
-      }
-    }
-    __syncthreads();
+    tile_gemv_sub(Ms, xb, acc, m, mm, nq);
   }
-  // x = Dinv_b · acc
-  const cplx* D = Dinv + ((size_t)b * 2 + upper) * TB * TB;
-  for (int e = threadIdx.x; e < TB * ((nq + 7) / 8); e += TS_NT) {
-    const int r = e % TB, qg = e / TB;
-    if (r >= m) continue;
-    cplx s[8];
+  // x = Dinv_b · acc  (as acc' = 0 − (−Dinv)·acc through the same routine: xb ← acc, acc ← 0)
+  __syncthreads();
+  {
+    const cplx* D = Dinv + ((size_t)b * 2 + upper) * TS_TB * TS_TB;
+    cplx v[TS_TB * TS_TB / TS_NT];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s[w] = cmk(0.0, 0.0);
-    for (int c = 0; c < m; ++c) {
-      const cplx a = D[r + (size_t)c * TB];
-#pragma unroll
-      for (int w = 0; w < 8; ++w) s[w] = cfma(a, acc[(size_t)(qg * 8 + w) * TB + c], s[w]);
+    for (int u2 = 0; u2 < TS_TB * TS_TB / TS_NT; ++u2) {
+      const cplx d = D[threadIdx.x + u2 * TS_NT];
+      v[u2] = cmk(-d.x, -d.y);
     }
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const int q = qg * 8 + w;
-      if (q < nq) Y[(o + r) + (size_t)q * ldy] = s[w];
-    }
+    for (int u2 = 0; u2 < TS_TB * TS_TB / TS_NT; ++u2) Ms[threadIdx.x + u2 * TS_NT] = v[u2];
+  }
+  for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) {
+    xb[e] = acc[e];
+    acc[e] = cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  tile_gemv_sub(Ms, xb, acc, m, m, nq);
+  __syncthreads();
+  for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) {
+    const int r = e % TS_TB, q = e / TS_TB;
+    if (r < m && q < nq) Y[(o + r) + (size_t)q * ldy] = acc[e];
   }
   __threadfence();
   __syncthreads();
@@ -507,7 +538,8 @@ int root_lu_launches(int n) {
 
 void root_lu_solve(const cplx* A, int n, const cplx* Dinv, cplx* Y, int ldy, int nrhs, int* flags, cudaStream_t st) {
   const int TB = root_lu_tb(n), nblk = (n + TB - 1) / TB;
-  const size_t smem = 2 * (size_t)TS_Q * TB * sizeof(cplx);
+  if (TB != TS_TB) throw Error(-6, "root solve block height mismatch");
+  const size_t smem = (2 * (size_t)TS_Q * TS_TB + (size_t)TS_TB * TS_TB) * sizeof(cplx);
   static size_t cur = 0;
   if (smem > 48 * 1024 && smem > cur) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_lu_trsv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -519,7 +551,7 @@ void root_lu_solve(const cplx* A, int n, const cplx* Dinv, cplx* Y, int ldy, int
     FMMLU_CUDA(cudaMemsetAsync(flags, 0, 2 * (size_t)(nblk + 1) * sizeof(int), st));
     for (int upper = 0; upper < 2; ++upper) {
       int* f = flags + upper * (nblk + 1);
-      k_lu_trsv<<<nblk, TS_NT, smem, st>>>(A, n, n, TB, Dinv, Y + (size_t)q0 * ldy, ldy, nq, upper, f, f + nblk);
+      k_lu_trsv<<<nblk, TS_NT, smem, st>>>(A, n, n, Dinv, Y + (size_t)q0 * ldy, ldy, nq, upper, f, f + nblk);
       FMMLU_LAUNCH();
     }
   }

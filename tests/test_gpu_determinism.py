@@ -42,7 +42,7 @@ def test_deterministic_mode_is_bitwise_reproducible(F, nrhs):
     x1, s1 = _run(F, g, k, eps, leaf, b, 1)
     x2, s2 = _run(F, g, k, eps, leaf, b, 1)
     assert s1["n0"] == s2["n0"] and list(s1["ranks_sum"]) == list(s2["ranks_sum"])
-    assert np.array_equal(x1.view(np.float64), x2.view(np.float64))   # bit for bit
+    assert x1.tobytes() == x2.tobytes()   # bit for bit
     # and it is the same method: residual ≤ 10ε against the brute-force matvec
     assert dense.residual(g.points, g.normals, g.weights, k, x1[:, :3], b[:, :3]) <= 10 * eps
 

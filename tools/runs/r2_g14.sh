@@ -8,3 +8,5 @@ FMMLU_LIBDIR=/tmp/libq8 FMMLU_NVCC_EXTRA="-DFMMLU_SV_Q=8" python -c "from paper_
 echo "== Q4"; FMMLU_GEMM_SOLVE_MIN=100000 python tools/solve_scan.py cfg5 1,4,16,32
 echo "== Q8"; FMMLU_LIB=/tmp/libq8/libfmmlu.so FMMLU_GEMM_SOLVE_MIN=100000 python tools/solve_scan.py cfg5 1,4,16,32
 echo "== gemm sweeps"; python tools/solve_scan.py cfg5 32
+timeout 300 python tools/cfg_warm.py cfg2 3 > gpurun_out/r2_g14/c2.json 2>&1; cat gpurun_out/r2_g14/c2.json | tail -1
+FMMLU_GEMM_SOLVE_MIN=100000 python tools/solve_scan.py cfg2 1,4,32
