@@ -392,57 +392,46 @@ __global__ void __launch_bounds__(TS_NT) k_lu_trsv(const cplx* __restrict__ A, i
   if (threadIdx.x == 0) atomicExch(flags + b, 1);
 }
 
-// Triangular products for the forward apply: Z = U·Y (upper) or Z = L·Y (unit lower), TB-row
-// blocks, no dependencies.  Y, Z: n × nq (ld ldy), nq ≤ TS_Q, Z ≠ Y.
-__global__ void __launch_bounds__(TS_NT) k_lu_trmv(const cplx* __restrict__ A, int lda, int n, int TB,
+// Triangular products for the forward apply: Z = U·Y (upper) or Z = L·Y (unit lower), TS_TB-row
+// blocks, no dependencies; tiles staged in shared memory (negated, so the same subtract routine
+// accumulates +tile·x).  Y, Z: n × nq (ld ldy), nq ≤ TS_Q, Z ≠ Y.
+__global__ void __launch_bounds__(TS_NT) k_lu_trmv(const cplx* __restrict__ A, int lda, int n,
                                                    const cplx* __restrict__ Y, cplx* __restrict__ Z, int ldy,
                                                    int nq, int upper) {
   extern __shared__ __align__(16) unsigned char tm_sh[];
-  cplx* xb = reinterpret_cast<cplx*>(tm_sh);  // [TS_Q][TB]
-  const int o = blockIdx.x * TB, m = min(TB, n - o);
-  const int nblk = (n + TB - 1) / TB;
-  const int rr = threadIdx.x % TB, qg0 = threadIdx.x / TB, ngr = TS_NT / TB;
-  cplx s[TS_Q / 8][8];
-#pragma unroll
-  for (int g = 0; g < TS_Q / 8; ++g)
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s[g][w] = cmk(0.0, 0.0);
+  cplx* acc = reinterpret_cast<cplx*>(tm_sh);  // [TS_Q][TS_TB]
+  cplx* xb = acc + TS_Q * TS_TB;               // [TS_Q][TS_TB]
+  cplx* Ms = xb + TS_Q * TS_TB;                // [TS_TB][TS_TB]
+  const int o = blockIdx.x * TS_TB, m = min(TS_TB, n - o);
+  const int nblk = (n + TS_TB - 1) / TS_TB;
+  for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) acc[e] = cmk(0.0, 0.0);
   const int bl = upper ? blockIdx.x : 0, bh = upper ? nblk - 1 : blockIdx.x;
   for (int bb = bl; bb <= bh; ++bb) {
-    const int oo = bb * TB, mm = min(TB, n - oo);
+    const int oo = bb * TS_TB, mm = min(TS_TB, n - oo);
     __syncthreads();
-    for (int e = threadIdx.x; e < TS_Q * TB; e += TS_NT) {
-      const int r = e % TB, q = e / TB;
+    load_tile(A, lda, o, m, oo, mm, Ms);
+    for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) {
+      const int r = e % TS_TB, q = e / TS_TB;
       xb[e] = (r < mm && q < nq) ? Y[(oo + r) + (size_t)q * ldy] : cmk(0.0, 0.0);
     }
     __syncthreads();
-    if (rr < m) {
-      for (int c = 0; c < mm; ++c) {
-        const int gc = oo + c, gr = o + rr;
-        cplx a;
-        if (upper) a = gc >= gr ? A[gr + (size_t)gc * lda] : cmk(0.0, 0.0);
-        else a = gc < gr ? A[gr + (size_t)gc * lda] : cmk(gc == gr ? 1.0 : 0.0, 0.0);
-#pragma unroll
-        for (int g = 0; g < TS_Q / 8; ++g) {
-          const int qg = qg0 + g * ngr;
-          if (qg * 8 >= nq) break;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) s[g][w] = cfma(a, xb[(size_t)(qg * 8 + w) * TB + c], s[g][w]);
-        }
+    for (int e = threadIdx.x; e < TS_TB * TS_TB; e += TS_NT) {  // triangle of the diagonal block; negate
+      const int r = e % TS_TB, c = e / TS_TB;
+      cplx v = Ms[e];
+      if (bb == (int)blockIdx.x) {
+        if (upper) v = c >= r ? v : cmk(0.0, 0.0);
+        else v = c < r ? v : (c == r ? cmk(1.0, 0.0) : cmk(0.0, 0.0));
       }
+      Ms[e] = cmk(-v.x, -v.y);
     }
+    __syncthreads();
+    tile_gemv_sub(Ms, xb, acc, m, mm, nq);
   }
-  if (rr < m)
-#pragma unroll
-    for (int g = 0; g < TS_Q / 8; ++g) {
-      const int qg = qg0 + g * ngr;
-      if (qg * 8 >= nq) break;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int q = qg * 8 + w;
-        if (q < nq) Z[(o + rr) + (size_t)q * ldy] = s[g][w];
-      }
-    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < TS_Q * TS_TB; e += TS_NT) {
+    const int r = e % TS_TB, q = e / TS_TB;
+    if (r < m && q < nq) Z[(o + r) + (size_t)q * ldy] = acc[e];
+  }
 }
 
 template <int MC>
@@ -559,7 +548,7 @@ void root_lu_solve(const cplx* A, int n, const cplx* Dinv, cplx* Y, int ldy, int
 
 void root_lu_mult(const cplx* A, int n, cplx* Y, cplx* Z, int ldy, int nrhs, cudaStream_t st) {
   const int TB = root_lu_tb(n), nblk = (n + TB - 1) / TB;
-  const size_t smem = (size_t)TS_Q * TB * sizeof(cplx);
+  const size_t smem = (2 * (size_t)TS_Q * TS_TB + (size_t)TS_TB * TS_TB) * sizeof(cplx);
   static size_t cur = 0;
   if (smem > 48 * 1024 && smem > cur) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_lu_trmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -567,9 +556,9 @@ void root_lu_mult(const cplx* A, int n, cplx* Y, cplx* Z, int ldy, int nrhs, cud
   }
   for (int q0 = 0; q0 < nrhs; q0 += TS_Q) {
     const int nq = std::min(TS_Q, nrhs - q0);
-    k_lu_trmv<<<nblk, TS_NT, smem, st>>>(A, n, n, TB, Y + (size_t)q0 * ldy, Z + (size_t)q0 * ldy, ldy, nq, 1);
+    k_lu_trmv<<<nblk, TS_NT, smem, st>>>(A, n, n, Y + (size_t)q0 * ldy, Z + (size_t)q0 * ldy, ldy, nq, 1);
     FMMLU_LAUNCH();
-    k_lu_trmv<<<nblk, TS_NT, smem, st>>>(A, n, n, TB, Z + (size_t)q0 * ldy, Y + (size_t)q0 * ldy, ldy, nq, 0);
+    k_lu_trmv<<<nblk, TS_NT, smem, st>>>(A, n, n, Z + (size_t)q0 * ldy, Y + (size_t)q0 * ldy, ldy, nq, 0);
     FMMLU_LAUNCH();
   }
 }
