@@ -1898,18 +1898,25 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.wsM = wmax;
         }
         P.wave_start.push_back(nj);
+        // current positions of the owners already skeletonized at this level: one table shared by
+        // every box that reads them (maps[omap[o] ..]), instead of a copy per referencing box
+        std::vector<int> omap(cur.owners().size(), -1);
+        int tabsz = 0;
+        for (const BoxJob& J : jobs)
+          for (int q : J.Q)
+            if (!ident[q] && omap[q] < 0) {
+              omap[q] = tabsz;
+              tabsz += (int)curpos[q].size();
+            }
         // pass 1: per-box offsets into every array;  pass 2: fill on the host worker pool
         std::vector<Cnt>& at = P.at;
         at.resize(nj + 1);
         {
-          Cnt c{0, 0, 0, 0};
+          Cnt c{tabsz, 0, 0, 0};
           for (int j = 0; j < nj; ++j) {
             at[j] = c;
             const BoxJob& J = jobs[j];
-            for (int q : J.Q) {
-              if (!ident[q]) c.maps += 2 * (int)curpos[q].size();
-              c.cps += 2 * copy_tiles((int)curpos[q].size(), J.b);
-            }
+            for (int q : J.Q) c.cps += 2 * copy_tiles((int)curpos[q].size(), J.b);
             if (J.proxy) {
               c.pts += 1;
               c.gidx += (int)cur.act[J.a].size();
@@ -1920,6 +1927,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.cps.resize(c.cps);
           P.pts.resize(c.pts);
           P.gidx.resize(c.gidx);
+          for (size_t q = 0; q < omap.size(); ++q)
+            if (omap[q] >= 0) std::copy(curpos[q].begin(), curpos[q].end(), P.maps.begin() + omap[q]);
         }
         std::vector<CopyTask>& cps = P.cps;
         std::vector<int>& maps = P.maps;
@@ -1928,14 +1937,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         HostPool::get().parallel_for(nj, 8, [&](int j0, int j1) {
           for (int j = j0; j < j1; ++j) {
             BoxJob& J = jobs[j];
-            int mi = at[j].maps, ci = at[j].cps;
+            int ci = at[j].cps;
             int row = 0;
             for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
-              int mo = -1;
-              if (!ident[q]) {
-                mo = mi;
-                for (int v : curpos[q]) maps[mi++] = v;
-              }
+              const int mo = omap[q];
               CopyTask c{};
               c.src = cur.off(q, J.a);
               c.lds = (int)cur.act[q].size();
@@ -1950,11 +1955,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               row += c.rows;
             }
             for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
-              int mo = -1;
-              if (!ident[q]) {
-                mo = mi;
-                for (int v : curpos[q]) maps[mi++] = v;
-              }
+              const int mo = omap[q];
               CopyTask c{};
               c.src = cur.off(J.a, q);
               c.lds = J.b;
@@ -2253,11 +2254,20 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::vector<int> gjdim;
         struct FrameRef { int slot_off, tab_off, bld_off, ns; };
         std::vector<FrameRef> frames(el.size());
+        // current positions of already-skeletonized neighbour owners: one shared table (as in the ID)
+        std::vector<int> nmap(no, -1);
+        int ntab = 0;
+        for (int j : el)
+          for (int o : jobs[j].N)
+            if (!ident[o] && nmap[o] < 0) {
+              nmap[o] = ntab;
+              ntab += (int)curpos[o].size();
+            }
         // pass 1 (serial, O(|N|) per box): where each box's entries go in every array
         struct Counts { int maps, cps, cpsT, cpsX, fs, tab, bld; };
         std::vector<Counts> at(el.size() + 1);
         {
-          Counts c{0, 0, 0, 0, 0, 0, 0};
+          Counts c{ntab, 0, 0, 0, 0, 0, 0};
           for (size_t e = 0; e < el.size(); ++e) {
             at[e] = c;
             const BoxJob& J = jobs[el[e]];
@@ -2266,7 +2276,6 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             int nm = J.b, nf = J.k, nc = copy_tiles(J.b, J.b);
             for (int o : J.N) {
               const int no_ = (int)curpos[o].size();
-              if (!ident[o]) nm += no_;
               nf += no_;
               nc += copy_tiles(J.b, no_) + copy_tiles(no_, J.b);
             }
@@ -2289,6 +2298,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           fpos.resize(c.fs);
           ftab.resize(c.tab);
           fbld.resize(c.bld);
+          for (int o = 0; o < no; ++o)
+            if (nmap[o] >= 0) std::copy(curpos[o].begin(), curpos[o].end(), maps.begin() + nmap[o]);
         }
         // pass 2 (host worker pool): fill
         HostPool::get().parallel_for((int)el.size(), 8, [&](int e0, int e1) {
@@ -2319,11 +2330,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             ci += emit_copy_tiles(c, &cps[ci]);
             int noff = 0;
             for (int o : J.N) {
-              int mo = -1;
-              if (!ident[o]) {
-                mo = mi;
-                for (int v : curpos[o]) maps[mi++] = v;
-              }
+              const int mo = nmap[o];
               const int no_ = (int)curpos[o].size();
               for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
               CopyTask a{};
@@ -2621,7 +2628,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     fprintf(stderr, "[fmmlu] host ms: level-setup %.1f build-tasks %.1f phase-jobs %.1f id %.1f elim %.1f "
                     "update %.1f carry %.1f other %.1f | id: tasks %.1f gatherlaunch %.1f gram %.1f prep %.1f "
                     "pchol %.1f rest %.1f | topo %.1f acts %.1f | elim: sizes %.1f alloc %.1f tasks %.1f "
-                    "upload %.1f EF %.1f inv-panel-schur %.1f recs %.1f | next-prep wait %.1f | wait %.1f\n",
+                    "upload %.1f EF %.1f inv-panel-schur+recs %.1f | next-prep wait %.1f | wait %.1f\n",
             tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7], tr[8], tr[9], tr[10], tr[11], tr[12], tr[13],
             tr[14], tr[15], tr[16], tr[17], tr[18], tr[19], tr[20], tr[21], tr[22], S.t_sync_wait_ms);
   // ------------------------------------------------------------------ root

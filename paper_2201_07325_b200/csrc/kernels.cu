@@ -222,6 +222,30 @@ __global__ void k_copy(const CopyTask* __restrict__ tasks, const int* __restrict
                        const cplx* __restrict__ src, cplx* __restrict__ dst) {
   const CopyTask t = tasks[blockIdx.x];
   const int n = t.rows * t.cols;
+  if (t.trans && !t.tri) {
+    // transposed gather through 32×32 shared-memory tiles: reads run along the source's contiguous
+    // dimension (j), writes along the destination's (i)
+    __shared__ cplx tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+    for (int i0 = 0; i0 < t.rows; i0 += 32)
+      for (int j0 = 0; j0 < t.cols; j0 += 32) {
+        __syncthreads();
+        for (int ii = ty; ii < 32; ii += ny) {
+          const int i = i0 + ii, j = j0 + tx;
+          if (i < t.rows && j < t.cols) {
+            const int ri = t.rmap_off >= 0 ? maps[t.rmap_off + i] : i;
+            const int cj = t.cmap_off >= 0 ? maps[t.cmap_off + j] : j;
+            tile[ii][tx] = src[t.src + cj + (size_t)ri * t.lds];
+          }
+        }
+        __syncthreads();
+        for (int jj = ty; jj < 32; jj += ny) {
+          const int j = j0 + jj, i = i0 + tx;
+          if (i < t.rows && j < t.cols) dst[t.dst + i + (size_t)j * t.ldd] = tile[tx][jj];
+        }
+      }
+    return;
+  }
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int i = e % t.rows, j = e / t.rows;
     const int ri = t.rmap_off >= 0 ? maps[t.rmap_off + i] : i;
