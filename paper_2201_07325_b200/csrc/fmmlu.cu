@@ -775,6 +775,9 @@ void run_gemms(std::vector<GemmProblem>& probs, std::vector<GemmGroup>& tiles, c
   gemm_work(probs, fl, by);
   fl *= work_scale;  // e.g. 0.5 for Hermitian products computed on upper tiles only
   by *= work_scale;
+  static const bool trace = getenv("FMMLU_TRACE") != nullptr;
+  if (trace && cls == FMMLU_K_SCHUR)  // per-launch algorithmic work (to pair with ncu captures)
+    fprintf(stderr, "[fmmlu] schur launch: %zu boxes, %.6g flops, %.6g bytes (algorithmic)\n", probs.size(), fl, by);
   int id = P.begin(cls, st);
   gemm_run(s.ptr<GemmProblem>(op), s.ptr<GemmGroup>(ot), (int)tiles.size(), group_tiles(tiles.data(), tiles.size()),
            alpha, scatter, bsr, st, bn);

@@ -14,7 +14,7 @@ for r in tail:
     v = float(r["Metric Value"].replace(",", ""))
     u = r.get("Metric Unit", "ns")
     ms = v * {"ns": 1e-6, "nsecond": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(u, 1e-6)
-    name = r["Kernel Name"].split("(")[0].split("<")[0]
+    name = r["Kernel Name"].split("(")[0].replace("<unnamed>::", "")
     agg[name][0] += 1
     agg[name][1] += ms
 tot = sum(v[1] for v in agg.values())
