@@ -104,21 +104,31 @@ NCU_FULL = {"schur": "k_gemm_schur", "ef": "k_gemm_store", "panel": "k_gemm_stor
 
 
 def ncu_traffic(cls: str):
-    """(bytes per launch, source file) from the newest committed ncu full capture, or (None, None)."""
+    """(bytes per launch, source, extra) from the committed ncu full capture of the bench config's
+    dominant kernel (profiles/r2_schur_traffic_cfg5.json: launches paired with their algorithmic
+    bytes), else the newest generic summary, else (None, None, {})."""
     kern = NCU_FULL.get(cls)
     if not kern:
-        return None, None
+        return None, None, {}
     pdir = os.path.join(ROOT, "profiles")
+    paired = os.path.join(pdir, f"r2_{cls}_traffic_{CFG}.json")
+    if os.path.exists(paired):
+        try:
+            d = json.load(open(paired))["summary"]
+            return float(d["traffic_per_launch"]), f"profiles/{os.path.basename(paired)}", {
+                "traffic_launches": d["launches"], "traffic_algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"],
+                "traffic_over_algorithmic": d["traffic_over_algorithmic"]}
+        except Exception:
+            pass
     cands = sorted(f for f in os.listdir(pdir) if f.endswith(f"ncu_full_{kern}.json")) if os.path.isdir(pdir) else []
     if not cands:
-        return None, None
+        return None, None, {}
     try:
         d = json.load(open(os.path.join(pdir, cands[-1])))
         big = [l for l in d["launches"] if l.get("dram_read") is not None]
-        # launches of one factorization (ncu -c caps the list; the summary is over the same set)
-        return float(d["summary"]["traffic_per_launch"]), f"profiles/{cands[-1]} ({len(big)} launches)"
+        return float(d["summary"]["traffic_per_launch"]), f"profiles/{cands[-1]} ({len(big)} launches)", {}
     except Exception:
-        return None, None
+        return None, None, {}
 
 
 def max_over_ranks(t_ms: float, world: int, device=None) -> float:
@@ -427,14 +437,14 @@ def main():
     hbm = peaks.get("hbm_gbs", 6650.0)
     fl, by, t = st["class_flops"][dom], st["class_bytes"][dom], cms[dom]
     per_launch = max(1, st["class_launches"][dom])
-    traffic, traffic_src = ncu_traffic(cls[dom])
+    traffic, traffic_src, traffic_extra = ncu_traffic(cls[dom])
     if cls[dom] in ("schur", "ef", "panel", "qr"):
         achieved = fl / (t * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": dmma_tf, "unit": "TFLOP/s",
                 "frac": achieved / dmma_tf, "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": by / per_launch, "kernel": cls[dom],
                 "peak_source": "FP64 DMMA m8n8k4 probe measured in this run (MEASURED_PEAKS has no FP64 entry)",
-                "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch}
+                "flops_per_launch": fl / per_launch, "ms_per_launch": t / per_launch, **traffic_extra}
     elif cls[dom] in ("build", "gather", "solve", "apply"):
         achieved = by / (t * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
