@@ -666,7 +666,10 @@ void borrow_ws(fmmlu_handle* h, int slot, DBuf& dst, size_t bytes, cudaStream_t 
   DBuf& w = h->ws ? h->ws[slot] : h->ws_slot[slot];
   w.st = st;  // stream-ordered release (on growth) after this user's work
   if (!w.p || w.bytes < bytes) {
-    const size_t grown = std::max(bytes, w.bytes + w.bytes / 4);
+    // headroom: the shared workspace is reused by later factorizations whose sizes differ slightly
+    // (a rank off by one); 10 % on top of the request avoids a multi-GB regrowth (and its pool growth)
+    const size_t want = h->ws ? bytes + bytes / 10 : bytes;
+    const size_t grown = std::max(want, w.bytes + w.bytes / 4);
     if (w.p && w.big && h->ws) {  // outgrown shared workspace: back to the pool, not the block cache
       cudaFreeAsync(w.p, st);
       w.p = nullptr;
