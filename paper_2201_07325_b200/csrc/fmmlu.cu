@@ -2314,14 +2314,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             BoxRec& R = recs[e];
             const int kk = J.k, r = R.r, b = J.b;
             const int* pm = &hperm[J.permoff];
-            int mi = at[e].maps, ci = at[e].cps, fi = at[e].fs;
+            int mi = at[e].maps, ci = at[e].cps;
             // local order [R | S] of B's columns
             const int rf = mi;
             for (int i = kk; i < b; ++i) maps[mi++] = pm[i];
             for (int i = 0; i < kk; ++i) maps[mi++] = pm[i];
-            const std::vector<int>& aB = cur.act[J.a];
-            for (int i = 0; i < kk; ++i) hidx[R.idxS + i] = aB[pm[i]];
-            for (int i = 0; i < r; ++i) hidx[R.idxR + i] = aB[pm[kk + i]];
             // W_B = [A_BB | A_BN] (rows/cols of B in [R|S] order), W_N = A_NB
             CopyTask c{};
             c.src = cur.off(J.a, J.a);
@@ -2338,7 +2335,6 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             for (int o : J.N) {
               const int mo = nmap[o];
               const int no_ = (int)curpos[o].size();
-              for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
               CopyTask a{};
               a.src = cur.off(J.a, o);
               a.lds = b;
@@ -2414,6 +2410,29 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             emit_copy_tiles(xn, &cpsX[xi]);
             gjoff[e] = R.Xi;
             gjdim[e] = r;
+          }
+        });
+        // pass 3 (host worker pool, built while the device runs the gathers, E/F, X_RR⁻¹ and Up of
+        // this phase): the Schur scatter frames and the factor's index lists
+        auto fill_frames = [&]() {
+        HostPool::get().parallel_for((int)el.size(), 8, [&](int e0, int e1) {
+          for (int e = e0; e < e1; ++e) {
+            BoxJob& J = jobs[el[e]];
+            BoxRec& R = recs[e];
+            const int kk = J.k, r = R.r;
+            const int* pm = &hperm[J.permoff];
+            int fi = at[e].fs;
+            const std::vector<int>& aB = cur.act[J.a];
+            for (int i = 0; i < kk; ++i) hidx[R.idxS + i] = aB[pm[i]];
+            for (int i = 0; i < r; ++i) hidx[R.idxR + i] = aB[pm[kk + i]];
+            {
+              int noff = 0;
+              for (int o : J.N) {
+                const int no_ = (int)curpos[o].size();
+                for (int i = 0; i < no_; ++i) hidx[R.idxN + noff + i] = cur.act[o][curpos[o][i]];
+                noff += no_;
+              }
+            }
             // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
             FrameRef fr;
             fr.slot_off = fi;
@@ -2438,18 +2457,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             frames[e] = fr;
           }
         });
-        if (maps.empty()) maps.push_back(0);
         if (fslot.empty()) { fslot.push_back(0); fpos.push_back(0); }
         if (ftab.empty()) ftab.push_back(-1);
         if (fbld.empty()) fbld.push_back(0);
+        };
+        if (maps.empty()) maps.push_back(0);
         lap(18);
         Stage s;
-        s.reserve_pinned(16 * 12 + sizeof(CopyTask) * (cps.size() + cpsT.size() + cpsX.size()) +
-                         sizeof(int) * (maps.size() + fslot.size() + fpos.size() + fbld.size() + gjdim.size()) +
-                         sizeof(long long) * (ftab.size() + gjoff.size()) + sizeof(BoxRec) * recs.size());
-        size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_fs = s.add(fslot),
-               o_fp = s.add(fpos), o_ft = s.add(ftab), o_fb = s.add(fbld), o_go = s.add(gjoff), o_gd = s.add(gjdim),
-               o_rec = s.add(recs);
+        s.reserve_pinned(16 * 8 + sizeof(CopyTask) * (cps.size() + cpsT.size() + cpsX.size()) +
+                         sizeof(int) * (maps.size() + gjdim.size()) + sizeof(long long) * gjoff.size() +
+                         sizeof(BoxRec) * recs.size());
+        size_t o_c = s.add(cps), o_ct = s.add(cpsT), o_cx = s.add(cpsX), o_m = s.add(maps), o_go = s.add(gjoff),
+               o_gd = s.add(gjdim), o_rec = s.add(recs);
         s.upload(st);
         gmark(2);
         int gid = h->prof.begin(FMMLU_K_GATHER, st);
@@ -2541,6 +2560,12 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           add_gemm(gp, gt, P);
         }
         run_gemms(gp, gt, p1, 0, nullptr, st, keep, h->prof, FMMLU_K_PANEL);
+        fill_frames();
+        Stage s2;
+        s2.reserve_pinned(16 * 6 + sizeof(int) * (fslot.size() + fpos.size() + fbld.size()) +
+                          sizeof(long long) * ftab.size());
+        const size_t o_fs = s2.add(fslot), o_fp = s2.add(fpos), o_ft = s2.add(ftab), o_fb = s2.add(fbld);
+        s2.upload(st);
         // Schur complement: Δ_{(S∪N)²} −= X_{(S∪N)R} · Up  (= X_{(S∪N)R} X_RR⁻¹ X_{R(S∪N)}), scattered
         // into the level BSR
         for (int w = 0; w < ph.nwaves(); ++w) {
@@ -2564,10 +2589,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.row0 = 0;
           P.col0 = 0;
           P.ns = fr.ns;
-          P.slot = s.ptr<int>(o_fs) + fr.slot_off;
-          P.pos = s.ptr<int>(o_fp) + fr.slot_off;
-          P.tab = s.ptr<long long>(o_ft) + fr.tab_off;
-          P.bld = s.ptr<int>(o_fb) + fr.bld_off;
+          P.slot = s2.ptr<int>(o_fs) + fr.slot_off;
+          P.pos = s2.ptr<int>(o_fp) + fr.slot_off;
+          P.tab = s2.ptr<long long>(o_ft) + fr.tab_off;
+          P.bld = s2.ptr<int>(o_fb) + fr.bld_off;
           add_gemm(gp, gt, P);
         }
         run_gemms(gp, gt, m1, 1, cur.bsr.as<cplx>(), st, keep, h->prof, FMMLU_K_SCHUR);
@@ -2594,6 +2619,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         // no sync here: the next phase's ID preparation overlaps with this elimination on the GPU
         gmark(3);
         keep.push_back(std::move(s.dev));
+        keep.push_back(std::move(s2.dev));
         track(h, -(long long)W.bytes);
         W.release();
         h->phases.push_back(std::move(ph));
