@@ -27,8 +27,13 @@ import scipy.linalg as sla
 GOLDEN_ANGLE = math.pi * (3.0 - math.sqrt(5.0))
 
 
-def interp_decomp(M: np.ndarray, eps: float):
-    """Return (perm, k, T): skeleton columns perm[:k], redundant perm[k:], T (k × (b-k))."""
+def interp_decomp(M: np.ndarray, eps: float, k_min: int = 0):
+    """Return (perm, k, T): skeleton columns perm[:k], redundant perm[k:], T (k × (b-k)).
+
+    k_min (separate in/out IDs, reading R12): continue the same greedy pivot order to
+    k = max(k_ε, k_min) columns (caller guarantees k_min ≤ min(m, b)); T = R11⁻¹R12 of that
+    leading k×k block.  The residual of a greedy CPQR only falls as pivots are added, so the
+    longer ID is still ε-accurate."""
     m, b = M.shape
     if b == 0:
         return np.zeros(0, dtype=np.int64), 0, np.zeros((0, 0), dtype=M.dtype)
@@ -40,6 +45,7 @@ def interp_decomp(M: np.ndarray, eps: float):
     else:
         small = np.nonzero(d[:kmax] <= eps * d[0])[0]
         k = int(small[0]) if small.size else kmax
+    k = max(k, k_min)
     T = sla.solve_triangular(R[:k, :k], R[:k, k:]) if k > 0 else np.zeros((0, b), dtype=M.dtype)
     return P.astype(np.int64), k, T
 

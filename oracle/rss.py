@@ -66,6 +66,19 @@ class BoxRecord:
     Lp: np.ndarray   # X_{(S∪N)R} X_RR⁻¹   ((k+|N|) × r)
     Up: np.ndarray   # X_RR⁻¹ X_{R(S∪N)}   (r × (k+|N|))
     X_RR: np.ndarray  # the pivot block itself (the D factor of the forward form)
+    # separate incoming/outgoing IDs (reading R12): the column side.  None in
+    # the simultaneous form, where the column sets and T are the row ones.
+    Bs_c: np.ndarray = None  # column skeleton (pivot order)
+    Br_c: np.ndarray = None  # redundant columns
+    SN_c: np.ndarray = None  # S_c ∪ N columns (column frame of Up)
+    T_c: np.ndarray = None   # k × r, A_{F R_c} ≈ A_{F S_c} T_c
+
+    @property
+    def cols(self):
+        """(S_c, R_c, (S∪N)_c, T_c): the column-side sets (= the row side when simultaneous)."""
+        if self.Bs_c is None:
+            return self.Bs, self.Br, self.SN, self.T
+        return self.Bs_c, self.Br_c, self.SN_c, self.T_c
 
 
 @dataclasses.dataclass
@@ -79,6 +92,7 @@ class Factorization:
     root_lu: tuple
     stats: dict
     A_t: np.ndarray = None  # A_{B_t B_t} (root block of D)
+    Bt_c: np.ndarray = None  # root columns (separate IDs only; else = Bt)
 
 
 class DenseState:
@@ -204,7 +218,7 @@ class BlockState:
 def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
            rho_factor: float = 2.0, A_init: np.ndarray | None = None,
            keep_dense: bool = False, hook=None, mode: str = "dense",
-           order: str = "colour") -> Factorization:
+           order: str = "colour", separate: bool = False) -> Factorization:
     """Factorize Ã.
 
     mode: "dense" (n ≤ ~20,000) or "block" (any n); both hold the same current matrix and
@@ -216,9 +230,22 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
     are when it is processed (the plain sequential sweep of PAPER.md L878-884).
     ``hook(stage, ctx)`` (tests only, dense mode) is called per eliminated box with stage
     'pre' (before the Schur update) and 'post' (after); ctx holds the index sets, the ID
-    and the live dense matrix."""
+    and the live dense matrix.
+    separate (reading R12):
+    different interpolation matrices for A_FB and A_BFᵀ.  A column ID of
+    M_c = [A_{Q B_c} ; s_γ K_γB √D_B] (outgoing proxy rows) gives (S_c, R_c, T_c) with
+    A_{F R_c} ≈ A_{F S_c} T_c, and a row ID of M_r = [A_{B_r Q}ᵀ ; s_γ (√D_B S_Bγ)ᵀ]
+    (incoming) gives (S_r, R_r, T_r) with A_{R_r F} ≈ T_rᵀ A_{S_r F}.  Both keep
+    k = max(k_c, k_r) pivots of their own greedy CPQR so that the pivot block X_{R_r R_c}
+    of Eq. strong-skel-elim is square (a box whose k exceeds the rows of either M is left
+    uncompressed, k = b).  The box then keeps active rows S_r and active columns S_c;
+    the row and column actives of every owner, the root block A_{B_t^r B_t^c} and the
+    solve's row (equation) and column (unknown) vectors are tracked separately.  Dense
+    mode only."""
     if mode not in ("dense", "block") or order not in ("colour", "colour_reversed", "sequential"):
         raise ValueError("mode / order")
+    if separate and mode != "dense":
+        raise ValueError("separate IDs need mode='dense'")
     tree = Tree(points, leaf_max)
     perm = tree.perm
     X = np.asarray(points, dtype=np.float64)[perm]
@@ -231,10 +258,11 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
             raise ValueError("A_init / hook / keep_dense need mode='dense'")
         state = BlockState(k, X, NX, sw, tree.n)
 
-    active = {}
+    active = {}     # active rows per box (= the actives, simultaneous form)
     for b in range(len(tree.level)):
         if tree.is_leaf(b):
             active[b] = np.arange(tree.start[b], tree.end[b], dtype=np.int64)
+    active_c = dict(active) if separate else active   # active columns
     records = []
     stats = dict(levels={}, n=tree.n, nlevels=tree.nlevels, skeletons={})
 
@@ -242,6 +270,8 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
         for B in tree.levels[lvl]:
             if not tree.is_leaf(B):
                 active[B] = np.sort(np.concatenate([active[c] for c in tree.children[B]]))
+                if separate:
+                    active_c[B] = np.sort(np.concatenate([active_c[c] for c in tree.children[B]]))
         owners = tree.owners(lvl)
         state.begin_level(owners, active,
                           lambda o, lvl=lvl: tree.parent[o] if tree.level[o] == lvl + 1 else o)
@@ -257,13 +287,16 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 phases = [p[::-1] for p in phases]
         for phase in phases:
             snap = {o: active[o] for o in owners}
+            snap_c = {o: active_c[o] for o in owners}
             total = sum(v.size for v in snap.values())
             eliminated = {}
             for B in phase:
                 if order == "sequential":           # no batching: every box sees the current actives
                     snap = {o: active[o] for o in owners}
+                    snap_c = {o: active_c[o] for o in owners}
                     total = sum(v.size for v in snap.values())
                 Bidx = snap[B]
+                Bc = snap_c[B]
                 b = Bidx.size
                 if b == 0:
                     continue
@@ -277,18 +310,46 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 nP = nF - nQ
                 Qidx = (np.concatenate([snap[o] for o in Ql]) if Ql
                         else np.zeros(0, dtype=np.int64))
-                rows = [state.get(Qidx, Bidx), state.get(Bidx, Qidx).T]
-                if nP > 0:                         # proxy rows iff P ≠ ∅ (C12)
-                    Y, s_g = proxy_points(tree.box_centre(B), rho, n_gamma)
-                    Kout = kern.combined_field(k, Y, X[Bidx], NX[Bidx]) * sw[Bidx][None, :]
-                    Sin = kern.green(k, X[Bidx], Y).T * sw[Bidx][None, :]
-                    rows += [s_g * Kout, s_g * Sin]
-                M = np.vstack(rows)
-                P, kk, T = interp_decomp(M, eps)
+                Qc = (np.concatenate([snap_c[o] for o in Ql]) if Ql
+                      else np.zeros(0, dtype=np.int64))
+                if not separate:
+                    rows = [state.get(Qidx, Bidx), state.get(Bidx, Qidx).T]
+                    if nP > 0:                         # proxy rows iff P ≠ ∅ (C12)
+                        Y, s_g = proxy_points(tree.box_centre(B), rho, n_gamma)
+                        Kout = kern.combined_field(k, Y, X[Bidx], NX[Bidx]) * sw[Bidx][None, :]
+                        Sin = kern.green(k, X[Bidx], Y).T * sw[Bidx][None, :]
+                        rows += [s_g * Kout, s_g * Sin]
+                    M = np.vstack(rows)
+                    P, kk, T = interp_decomp(M, eps)
+                    Pc, T_c = P, T
+                else:                                  # f3: one ID per side (reading R12)
+                    rows_c = [state.get(Qidx, Bc)]         # far rows × B's active columns
+                    rows_r = [state.get(Bidx, Qc).T]       # (B's active rows × far columns)ᵀ
+                    if nP > 0:
+                        Y, s_g = proxy_points(tree.box_centre(B), rho, n_gamma)
+                        rows_c.append(s_g * kern.combined_field(k, Y, X[Bc], NX[Bc]) * sw[Bc][None, :])
+                        rows_r.append(s_g * kern.green(k, X[Bidx], Y).T * sw[Bidx][None, :])
+                    Mc, Mr = np.vstack(rows_c), np.vstack(rows_r)
+                    Pc, kc, T_c = interp_decomp(Mc, eps)
+                    P, kr, T = interp_decomp(Mr, eps)
+                    kk = max(kc, kr)
+                    if kk > min(Mc.shape[0], Mr.shape[0]):   # a side cannot reach k pivots: keep B
+                        kk = b
+                        P = Pc = np.arange(b, dtype=np.int64)
+                    else:
+                        if kc < kk:
+                            Pc, _, T_c = interp_decomp(Mc, eps, k_min=kk)
+                        if kr < kk:
+                            P, _, T = interp_decomp(Mr, eps, k_min=kk)
+                    M = Mc
                 Bs = Bidx[P[:kk]]
                 Br = Bidx[P[kk:]]
+                Bs_c = Bc[Pc[:kk]]
+                Br_c = Bc[Pc[kk:]]
                 Nidx = (np.concatenate([active[o] for o in Nl]) if Nl
                         else np.zeros(0, dtype=np.int64))
+                Nc = (np.concatenate([active_c[o] for o in Nl]) if Nl
+                      else np.zeros(0, dtype=np.int64))
                 lst["boxes"] += 1
                 lst["ranks"].append(kk)
                 lst["b"].append(b)
@@ -296,17 +357,21 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 lst["nQ"].append(Qidx.size)
                 lst["rows"].append(M.shape[0])
                 stats["skeletons"][B] = np.sort(Bs)
+                if separate:
+                    stats.setdefault("skeletons_c", {})[B] = np.sort(Bs_c)
+                    stats.setdefault("ranks_rc", []).append((kr, kc))
                 if Br.size == 0:                   # k = b: nothing to eliminate (C13)
                     continue
-                # --- E/F transforms (Eq. pap and the X blocks that follow it)
-                A_RR = state.get(Br, Br); A_RS = state.get(Br, Bs); A_SR = state.get(Bs, Br)
-                A_SS = state.get(Bs, Bs); A_RN = state.get(Br, Nidx); A_NR = state.get(Nidx, Br)
-                A_SN = state.get(Bs, Nidx); A_NS = state.get(Nidx, Bs)
-                X_RR = A_RR - T.T @ A_SR - A_RS @ T + T.T @ A_SS @ T
+                # --- E/F transforms (Eq. pap and the X blocks that follow it); rows use the row
+                # sets and T, columns the column sets and T_c (the same ones when simultaneous)
+                A_RR = state.get(Br, Br_c); A_RS = state.get(Br, Bs_c); A_SR = state.get(Bs, Br_c)
+                A_SS = state.get(Bs, Bs_c); A_RN = state.get(Br, Nc); A_NR = state.get(Nidx, Br_c)
+                A_SN = state.get(Bs, Nc); A_NS = state.get(Nidx, Bs_c)
+                X_RR = A_RR - T.T @ A_SR - A_RS @ T_c + T.T @ A_SS @ T_c
                 X_RS = A_RS - T.T @ A_SS
-                X_SR = A_SR - A_SS @ T
+                X_SR = A_SR - A_SS @ T_c
                 X_RN = A_RN - T.T @ A_SN
-                X_NR = A_NR - A_NS @ T
+                X_NR = A_NR - A_NS @ T_c
                 # --- L/U with pivot block X_RR (Eq. strong-skel-elim)
                 lu = sla.lu_factor(X_RR, check_finite=False)
                 X_cR = np.vstack([X_SR, X_NR])
@@ -314,16 +379,23 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
                 Lp = sla.lu_solve(lu, X_cR.T, trans=1).T
                 Up = sla.lu_solve(lu, X_Rc)
                 SN = np.concatenate([Bs, Nidx])
+                SN_c = np.concatenate([Bs_c, Nc]) if separate else SN
                 if hook is not None:
                     Fidx = np.concatenate([snap[o] for o in owners if o != B and o not in Nl] or
                                           [np.zeros(0, dtype=np.int64)])
+                    Fc = np.concatenate([snap_c[o] for o in owners if o != B and o not in Nl] or
+                                        [np.zeros(0, dtype=np.int64)])
                     ctx = dict(B=B, level=lvl, Bs=Bs, Br=Br, Nidx=Nidx, Qidx=Qidx, Fidx=Fidx,
-                               T=T, A=state.A, M=M, nP=nP)
+                               T=T, A=state.A, M=M, nP=nP, Bs_c=Bs_c, Br_c=Br_c, Nc=Nc, Fc=Fc, T_c=T_c)
                     hook("pre", ctx)
-                state.add(SN, SN, -(X_cR @ Up))       # Schur complement update
+                state.add(SN, SN_c, -(X_cR @ Up))     # Schur complement update
                 if hook is not None:
                     hook("post", ctx)
-                records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up, X_RR))
+                if separate:
+                    records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up, X_RR, Bs_c, Br_c, SN_c, T_c))
+                    active_c[B] = np.sort(Bs_c)
+                else:
+                    records.append(BoxRecord(B, lvl, Bs, Br, SN, T, lu, Lp, Up, X_RR))
                 active[B] = np.sort(Bs)
                 eliminated[B] = active[B]
                 if order == "sequential":
@@ -333,17 +405,17 @@ def factor(points, normals, weights, k: float, eps: float, leaf_max: int,
         lst["ranks"] = np.asarray(lst["ranks"])
         stats["levels"][lvl] = lst
 
-    alive = np.zeros(tree.n, dtype=bool)
-    for b in range(len(tree.level)):
-        if tree.is_leaf(b):
-            alive[tree.start[b]:tree.end[b]] = True
+    alive = np.ones(tree.n, dtype=bool)      # every leaf DOF starts active
+    alive_c = np.ones(tree.n, dtype=bool)
     for r in records:
         alive[r.Br] = False
+        alive_c[r.cols[1]] = False
     Bt = np.nonzero(alive)[0]
-    A_t = state.get(Bt, Bt)
+    Bt_c = np.nonzero(alive_c)[0] if separate else Bt
+    A_t = state.get(Bt, Bt_c)
     root_lu = sla.lu_factor(A_t, check_finite=False)
     stats["n0"] = int(Bt.size)
-    f = Factorization(tree, k, eps, sw, records, Bt, root_lu, stats, A_t)
+    f = Factorization(tree, k, eps, sw, records, Bt, root_lu, stats, A_t, Bt_c if separate else None)
     if keep_dense:
         f.A_final = state.A
     return f
@@ -356,15 +428,22 @@ def solve(f: Factorization, b: np.ndarray) -> np.ndarray:
     bb = b[:, None] if vec else b
     perm = f.tree.perm
     y = bb[perm] * f.sw[:, None]                    # W^{½} b in tree order (C1)
+    # separate IDs (f3): the upward sweep runs on the equation (row) vector y, D⁻¹ maps the
+    # R_r entries to the unknowns at R_c, the downward sweep runs on the unknown (column)
+    # vector yc.  Simultaneous: the two are one vector, updated in place.
+    yc = np.zeros_like(y) if f.Bt_c is not None else y
     for r in f.records:                             # V_M⁻¹ ⋯ V_1⁻¹ : E then L, then D⁻¹ on R
         y[r.Br] -= r.T.T @ y[r.Bs]
         y[r.SN] -= r.Lp @ y[r.Br]
-        y[r.Br] = sla.lu_solve(r.lu, y[r.Br])
+        yc[r.cols[1]] = sla.lu_solve(r.lu, y[r.Br])
+    Bt_c = f.Bt if f.Bt_c is None else f.Bt_c
     if f.Bt.size:
-        y[f.Bt] = sla.lu_solve(f.root_lu, y[f.Bt])  # P_t D⁻¹ P_tᵀ on the root block
+        yc[Bt_c] = sla.lu_solve(f.root_lu, y[f.Bt])  # P_t D⁻¹ P_tᵀ on the root block
+    y = yc
     for r in reversed(f.records):                   # W_1⁻¹ ⋯ W_M⁻¹ : U then F
-        y[r.Br] -= r.Up @ y[r.SN]
-        y[r.Bs] -= r.T @ y[r.Br]
+        Bs_c, Br_c, SN_c, T_c = r.cols
+        y[Br_c] -= r.Up @ y[SN_c]
+        y[Bs_c] -= T_c @ y[Br_c]
     x = np.empty_like(y)
     x[perm] = y / f.sw[:, None]
     return x[:, 0] if vec else x
@@ -381,13 +460,18 @@ def apply(f: Factorization, x: np.ndarray) -> np.ndarray:
     xx = x[:, None] if vec else x
     perm = f.tree.perm
     y = xx[perm] * f.sw[:, None]                    # Ã acts on W^{½} x (C1)
-    for r in f.records:                             # W_j = U⁻¹ F⁻¹ Pᵀ
-        y[r.Bs] += r.T @ y[r.Br]                    # F⁻¹
-        y[r.Br] += r.Up @ y[r.SN]                   # U⁻¹
+    for r in f.records:                             # W_j = U⁻¹ F⁻¹ Pᵀ (unknown/column side)
+        Bs_c, Br_c, SN_c, T_c = r.cols
+        y[Bs_c] += T_c @ y[Br_c]                    # F⁻¹
+        y[Br_c] += r.Up @ y[SN_c]                   # U⁻¹
+    # D maps the unknowns at R_c (root: B_t^c) to the equations at R_r (B_t); one vector when
+    # simultaneous (the blocks are disjoint, so in place is exact)
+    yr = np.zeros_like(y) if f.Bt_c is not None else y
     for r in f.records:                             # D on the R blocks
-        y[r.Br] = r.X_RR @ y[r.Br]
+        yr[r.Br] = r.X_RR @ y[r.cols[1]]
     if f.Bt.size:
-        y[f.Bt] = f.A_t @ y[f.Bt]                   # P_t A_{B_tB_t} P_tᵀ
+        yr[f.Bt] = f.A_t @ y[f.Bt if f.Bt_c is None else f.Bt_c]   # P_t A_{B_tB_t} P_tᵀ
+    y = yr
     for r in reversed(f.records):                   # V_j = P E⁻¹ L⁻¹
         y[r.SN] += r.Lp @ y[r.Br]                   # L⁻¹
         y[r.Br] += r.T.T @ y[r.Bs]                  # E⁻¹
