@@ -194,6 +194,15 @@ int fmmlu_set_stream(fmmlu_handle* h, void* cuda_stream);
  *               in one CTA's or one <=16-CTA cluster's shared memory when it fits, blocked
  *               panel path otherwise; default), 1 = blocked panel path always
  *   "proxy_rho" proxy-sphere radius / box side, in (sqrt(3)/2, 5/2) (reading C5; default 2.0)
+ *   "separate_id" 0 = one simultaneous ID of [A_QB; A_BQ^T; proxy rows] per box (default),
+ *               1 = separate incoming / outgoing interpolation matrices (PAPER.md L726-732,
+ *               L1098-1108, L1909-1914; R12): a column ID of
+ *               M_c = [A_QB; outgoing proxy rows] gives (S_c, T_c) and a row ID of
+ *               M_r = [A_BQ^T; incoming proxy rows] gives (S_r, T_r); both sides keep
+ *               k = max(k_c, k_r) skeletons so that X_RR stays square; a box then keeps
+ *               different active rows and columns, and fmmlu_solve / fmmlu_apply carry the
+ *               vector from the equation side to the unknown side between the sweeps
+ *   "deterministic" 0 / 1 (R9)
  * Errors: EINVAL (unknown name or value out of range). */
 int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);
 

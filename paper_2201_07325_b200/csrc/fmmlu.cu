@@ -481,6 +481,12 @@ struct Phase {  // one (level, colour) elimination phase
   size_t fac_bytes = 0;
   DBuf ap_xs, ap_recs;  // fmmlu_apply: X_RR blocks (re-inverted X_RR⁻¹) and records pointing at them
   std::vector<BoxRec> hrecs;  // host copy of recs (multi-RHS GEMM sweeps build their problems from it)
+  // separate incoming/outgoing IDs: the records of the column (unknown) side —
+  // T = T_c, index lists S_c | R_c | N_c — used by the downward sweep; recs are the row side
+  DBuf recs_c;
+  std::vector<BoxRec> hrecs_c;
+  const BoxRec* down_recs() const { return recs_c.p ? recs_c.as<BoxRec>() : recs.as<BoxRec>(); }
+  const std::vector<BoxRec>& down_hrecs() const { return recs_c.p ? hrecs_c : hrecs; }
   // Sub-waves of records (boundaries into recs / items; one wave unless deterministic): no two boxes
   // of a wave share a target owner, so every atomic update of a wave lands on a distinct entry and
   // the waves run in a fixed order.  SolveItem::rec is relative to its wave's first record.
@@ -625,6 +631,10 @@ struct fmmlu_handle {
   int id_refine = 0;         // corrected-seminormal-equations steps on the Gram-path T (0..3)
   int pchol_mode = 0;        // 0 register-resident pivoted Cholesky (b ≤ 512), 1 shared-memory cluster kernel
   double rho_factor = 2.0;   // proxy radius / box side (reading C5)
+  int pchol_ll = 1;          // Gram path, b ≤ 512: left-looking pivoted Cholesky first (0 for fmmlu_boxes: k ≈ b)
+  int separate_id = 0;       // 1: separate incoming/outgoing IDs (DESIGN R12)
+  bool fac_separate = false; // the stored factorization was built with separate IDs
+  DBuf sep_perm;             // int n (separate IDs): unknown c ← equation sep_perm[c] between the sweeps
 };
 
 namespace {
@@ -808,16 +818,17 @@ void gemm_batched_staged(std::vector<GemmProblem>& probs, std::vector<GemmGroup>
 
 // Root block solve / forward product on y (tree order, ld ldy), rows B_t:
 // solve y[B_t] ← A_t⁻¹ y[B_t] = U⁻¹L⁻¹(P y[B_t]);  fwd y[B_t] ← A_t y[B_t] = Pᵀ(L U y[B_t]).
-void root_solve(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st) {
+// yout (separate IDs: the equations live in y, the unknowns / products go to another vector; same ld)
+void root_solve(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st, cplx* yout = nullptr) {
   if (h->n0 <= 0) return;
   const int n0 = (int)h->n0;
   DBuf T;
   T.alloc((size_t)n0 * nrhs * sizeof(cplx), st);
   launch_rows_move(h->root_rows_in.as<int>(), n0, y, ldy, T.as<cplx>(), nrhs, 0, st);
   root_lu_solve(h->root.as<cplx>(), n0, h->root_dinv.as<cplx>(), T.as<cplx>(), n0, nrhs, h->root_flags.as<int>(), st);
-  launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, T.as<cplx>(), nrhs, 1, st);
+  launch_rows_move(h->root_rows.as<int>(), n0, yout ? yout : y, ldy, T.as<cplx>(), nrhs, 1, st);
 }
-void root_fwd(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st) {
+void root_fwd(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st, cplx* yout = nullptr) {
   if (h->n0 <= 0) return;
   const int n0 = (int)h->n0;
   DBuf T;
@@ -825,8 +836,26 @@ void root_fwd(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st) {
   cplx* Y = T.as<cplx>();
   launch_rows_move(h->root_rows.as<int>(), n0, y, ldy, Y, nrhs, 0, st);
   root_lu_mult(h->root.as<cplx>(), n0, Y, Y + (size_t)n0 * nrhs, n0, nrhs, st);
-  launch_rows_move(h->root_rows_in.as<int>(), n0, y, ldy, Y, nrhs, 1, st);
+  launch_rows_move(h->root_rows_in.as<int>(), n0, yout ? yout : y, ldy, Y, nrhs, 1, st);
 }
+// Separate IDs: between the sweeps the vector changes sides.  After the upward
+// sweep y holds z = X_RR⁻¹t at every eliminated equation R_r; the unknown at R_c[i] is that value
+// (D⁻¹ maps R_r to R_c), so y2[c] = y[sep_perm[c]], and the root solve writes y2[B_t^c].  The
+// downward sweep then runs on y2 with the column-side records, and y2 is copied back.
+struct SepSwap {
+  DBuf y2;
+  cplx* begin(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st) {
+    if (!h->fac_separate) return nullptr;
+    if (ldy != (int)h->n) throw Error(FMMLU_EINVAL, "separate IDs: the sweeps need ld = n");
+    y2.alloc((size_t)h->n * nrhs * sizeof(cplx), st);
+    launch_rows_move(h->sep_perm.as<int>(), (int)h->n, y, ldy, y2.as<cplx>(), nrhs, 0, st);
+    return y2.as<cplx>();
+  }
+  void end(fmmlu_handle* h, cplx* y, int nrhs, cudaStream_t st) {
+    if (!y2.p) return;
+    FMMLU_CUDA(cudaMemcpyAsync(y, y2.p, (size_t)h->n * nrhs * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+  }
+};
 
 // ---------------------------------------------------------------------------- blocked GJ inverse
 // In-place inverse (Gauss-Jordan, partial pivoting) of every (A, n) with lda = n: panels of nb
@@ -837,7 +866,12 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   if (mats.empty()) return;
   int nmax = 1;
   for (auto& m : mats) nmax = std::max(nmax, m.second);
-  if (h->gj_mode == 0 && gj_dsm_cluster_size(nmax) > 0) {
+  // Large batches (cfg5: ≥ 290 boxes per phase at levels 5-7) run faster on the blocked path — one CTA
+  // per matrix per panel and DMMA updates keep every SM busy (inv class 157 → 70 ms) — while a few
+  // matrices finish sooner resident in a cluster's registers (cfg2 / cfg3: 10.7 vs 18.5, 27 vs 41 ms).
+  static const int gj_batch = getenv("FMMLU_GJ_BATCH") ? atoi(getenv("FMMLU_GJ_BATCH")) : 200;
+  const bool big_batch = h->gj_mode == 0 && (int)mats.size() >= gj_batch && nmax >= 48;
+  if (h->gj_mode == 0 && !big_batch && gj_dsm_cluster_size(nmax) > 0) {
     // whole matrices resident in (cluster) shared memory: one launch for the batch
     std::vector<GjTask> tasks;
     double fl = 0, by = 0;
@@ -1312,8 +1346,13 @@ struct LevelBSR {
   int level = -1;
   const LevelTopo* tp = nullptr;
   LevelMeta meta{};   // device CSR of the level (kept for the next level's carry-over lookups)
-  DBuf meta_buf;
+  DBuf meta_buf, meta_buf2;  // meta_buf2: the compacted offsets (end of the level)
+  const int* d_pair_a = nullptr;  // device: owner a of every block pair (CSR order)
+  int npairs = 0;
   std::vector<std::vector<int>> act;        // actives at level start (sorted), per local owner
+  std::vector<std::vector<int>> actc;       // separate IDs: the active columns (same counts); else unused
+  bool sep = false;
+  const std::vector<int>& cact(int a) const { return sep ? actc[a] : act[a]; }
   std::vector<std::vector<long long>> poff; // complex offset of block (a, nb[a][i])
   DBuf bsr;
   long long size = 0;
@@ -1444,9 +1483,17 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     int cid = h->prof.begin(FMMLU_K_CPQR, st);
     if (h->id_mode != 3) {
       if (reg_pchol) {  // register-resident pivoted Cholesky
+        // tree path: the left-looking one-CTA-per-box kernel first (ranks stay far below b there);
+        // the boxes it gives up on (k_out = −1) are taken by the register kernel behind it
+        static const bool ll_env = !(getenv("FMMLU_PCHOL_LL") && atoi(getenv("FMMLU_PCHOL_LL")) == 0);
+        // (its gain is one box per SM instead of one per cluster: only for batches that fill the GPU;
+        // cfg2's ≤ 100-box phases were faster on the register kernel alone)
+        static const int ll_min = getenv("FMMLU_PCHOL_LL_MIN") ? atoi(getenv("FMMLU_PCHOL_LL_MIN")) : 128;
+        const bool ll = ll_env && h->pchol_ll && nj >= ll_min &&
+                        launch_pchol_ll(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
         DBuf xs;
         xs.alloc((size_t)nj * pchol_reg_scratch(bmax) * sizeof(cplx), st);
-        done_id = launch_pchol_reg(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, xs.as<cplx>(), st, bmax);
+        done_id = launch_pchol_reg(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, xs.as<cplx>(), st, bmax, ll ? 1 : 0);
         keep.push_back(std::move(xs));
       } else {
         done_id = launch_pchol_cluster(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
@@ -1660,7 +1707,25 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     if (T.boxes[b].leaf())
       for (int i = T.boxes[b].start; i < T.boxes[b].end; ++i) act[b].push_back(i);
 
+  // separate incoming/outgoing IDs (DESIGN
+  // R12): every box keeps a row skeleton S_r (row ID of the incoming matrix) and a column skeleton
+  // S_c (column ID of the outgoing one) of the same size k = max(k_r, k_c).  Block (a, b) of the
+  // level store is then act_r(a) × act_c(b); every "position in an owner's actives" below exists
+  // once per side.  Not separate: the column-side containers alias the row-side ones.
+  const bool sep = h->separate_id != 0;
+  h->fac_separate = sep;
+  h->sep_perm.release();
+  std::vector<std::vector<int>> actc_store;
+  if (sep) actc_store = act;
+  std::vector<std::vector<int>>& actc = sep ? actc_store : act;
+  std::vector<int> sep_pi;  // unknown (column) index → equation (row) index eliminated with it
+  if (sep) {
+    sep_pi.resize(n);
+    for (int i = 0; i < n; ++i) sep_pi[i] = i;
+  }
   std::vector<int> prevOwner(n, -1), prevPos(n, -1);  // level ℓ+1 owner (local) / position
+  std::vector<int> prevPosc_store(sep ? n : 0, -1);
+  std::vector<int>& prevPosc = sep ? prevPosc_store : prevPos;
   LevelBSR prev;
   std::vector<DBuf> keep;  // per-phase temporaries kept alive until the phase syncs
 
@@ -1708,11 +1773,22 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), act[B.child[c]].begin(), act[B.child[c]].end());
         std::sort(u.begin(), u.end());
         act[b] = u;
+        if (sep) {
+          u.clear();
+          for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), actc[B.child[c]].begin(), actc[B.child[c]].end());
+          std::sort(u.begin(), u.end());
+          actc[b] = u;
+        }
       }
     }
     const int no = (int)cur.owners().size();
     cur.act.resize(no);
     for (int i = 0; i < no; ++i) cur.act[i] = act[cur.owners()[i]];
+    cur.sep = sep;
+    if (sep) {
+      cur.actc.resize(no);
+      for (int i = 0; i < no; ++i) cur.actc[i] = actc[cur.owners()[i]];
+    }
     const std::vector<std::vector<int>>& nb = cur.tp->nb;
     long long off = 0;
     cur.poff.resize(no);
@@ -1725,7 +1801,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     }
     cur.size = off;
     lap(15);
-    borrow_ws(h, lvl & 1, cur.bsr, (size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
+    // slot 0: the level's block store; slot 1: the previous level's store compacted to its skeletons
+    borrow_ws(h, 0, cur.bsr, (size_t)std::max<long long>(off, 1) * sizeof(cplx), st);
     track(h, cur.bsr.bytes);
 
     lap(0);
@@ -1733,6 +1810,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     {
       // host: flatten the level into CSR arrays (no per-pair tables; lookups happen on the device)
       std::vector<int> actoff(no + 1, 0), gidx, slot, pos, nbptr(no + 1, 0), nbidx, slptr(no + 1, 0), sllist, pair_a;
+      std::vector<int> gidxc, slotc, posc;  // separate IDs: the column side
       std::vector<long long> poffv;
       std::vector<int2> tasks;
       for (int a = 0; a < no; ++a) actoff[a + 1] = actoff[a] + (int)cur.act[a].size();
@@ -1759,6 +1837,22 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           slot.push_back(sidx);
           pos.push_back(po >= 0 ? prevPos[g] : 0);
         }
+        if (sep)
+          for (int g : cur.actc[a]) {  // the same previous-level owners hold a's columns (equal counts)
+            gidxc.push_back(g);
+            const int po = prev.level >= 0 ? prevOwner[g] : -1;
+            int sidx = -1;
+            if (po >= 0) {
+              for (int q = s0; q < (int)sllist.size(); ++q)
+                if (sllist[q] == po) {
+                  sidx = q - s0;
+                  break;
+                }
+              if (sidx < 0) throw Error(FMMLU_ECUDA, "separate IDs: column owner without rows");
+            }
+            slotc.push_back(sidx);
+            posc.push_back(po >= 0 ? prevPosc[g] : 0);
+          }
         slptr[a + 1] = (int)sllist.size();
         for (size_t i = 0; i < nb[a].size(); ++i) {
           const int b = nb[a][i];
@@ -1772,21 +1866,26 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         }
         nbptr[a + 1] = (int)nbidx.size();
       }
-      for (std::vector<int>* v : {&gidx, &slot, &pos, &nbidx, &sllist, &pair_a})
+      for (std::vector<int>* v : {&gidx, &slot, &pos, &nbidx, &sllist, &pair_a, &gidxc, &slotc, &posc})
         if (v->empty()) v->push_back(0);
+      const bool nbidx_empty = poffv.empty();
       if (poffv.empty()) poffv.push_back(0);
       Stage s;
       size_t o_ao = s.add(actoff), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_np = s.add(nbptr),
              o_ni = s.add(nbidx), o_po = s.add(poffv), o_sp = s.add(slptr), o_sl = s.add(sllist),
              o_pa = s.add(pair_a), o_t = s.add(tasks);
+      const size_t o_gc = sep ? s.add(gidxc) : o_g, o_sc = sep ? s.add(slotc) : o_s, o_pc = sep ? s.add(posc) : o_p;
       s.upload_owned(st);  // the level CSR is read again by the next level's build
       cur.meta = LevelMeta{s.ptr<int>(o_ao), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p), s.ptr<int>(o_np),
-                           s.ptr<int>(o_ni), s.ptr<long long>(o_po), s.ptr<int>(o_sp), s.ptr<int>(o_sl)};
+                           s.ptr<int>(o_ni), s.ptr<long long>(o_po), s.ptr<int>(o_sp), s.ptr<int>(o_sl),
+                           s.ptr<int>(o_gc), s.ptr<int>(o_sc), s.ptr<int>(o_pc)};
       int bid = h->prof.begin(FMMLU_K_BUILD, st);
       launch_build_level(s.ptr<int2>(o_t), (int)tasks.size(), s.ptr<int>(o_pa), cur.meta, prev.meta,
                          prev.level >= 0 ? 1 : 0, prev.bsr.as<cplx>(), cur.bsr.as<cplx>(), h->g, k, st);
       h->prof.end(bid, st);
       h->prof.add(FMMLU_K_BUILD, 60.0 * cur.size, 16.0 * cur.size, 1);
+      cur.d_pair_a = s.ptr<int>(o_pa);
+      cur.npairs = (int)poffv.size() - (nbidx_empty ? 1 : 0);
       cur.meta_buf = std::move(s.dev);
     }
     if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
@@ -1799,6 +1898,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       curpos[a].resize(cur.act[a].size());
       for (size_t i = 0; i < cur.act[a].size(); ++i) curpos[a][i] = (int)i;
     }
+    std::vector<std::vector<int>> curposc_store;
+    if (sep) curposc_store = curpos;  // positions among the level-start active columns
+    std::vector<std::vector<int>>& curposc = sep ? curposc_store : curpos;
     long long total_active = 0;
     for (int a = 0; a < no; ++a) total_active += (long long)cur.act[a].size();
     const double side = T.box_side(lvl);
@@ -1818,6 +1920,13 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       int permoff = 0;
       int k = 0;
       int mfin = 0;  // rows of the matrix the pivoted pass ran on
+      // separate IDs: M = [M_c | M_r], each m/2 × b with ld m/2 (M_c at Moff, M_r behind it); the row
+      // side uses Toff / permoff, the column side Toffc / permoffc; kr0 / kc0 = the ε-ranks of the
+      // two IDs (k = their maximum)
+      long long Toffc = 0;
+      int permoffc = 0;
+      int kr0 = 0, kc0 = 0;
+      std::vector<int> keepr, keepc;  // columns of each side's T that stay redundant (see the rank read-back)
     };
     struct Cnt { int maps, cps, pts, gidx; };
     // Host-only preparation of a colour phase's ID stage (its boxes, M layout, gather and proxy
@@ -1880,6 +1989,12 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.wsT += (long long)(J.b / 2 + 1) * (J.b - J.b / 2 + 1);
           J.permoff = P.permtot;
           P.permtot += J.b;
+          if (sep) {
+            J.Toffc = P.wsT;
+            P.wsT += (long long)(J.b / 2 + 1) * (J.b - J.b / 2 + 1);
+            J.permoffc = P.permtot;
+            P.permtot += J.b;
+          }
           P.bmax = std::max(P.bmax, J.b);
         }
         // Gram path: M is only needed until its Gram matrix is formed, so it is gathered in waves of
@@ -1914,6 +2029,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               omap[q] = tabsz;
               tabsz += (int)curpos[q].size();
             }
+        std::vector<int> omapc_store;  // separate IDs: the same table for the column positions
+        if (sep) {
+          omapc_store.assign(cur.owners().size(), -1);
+          for (size_t q = 0; q < omap.size(); ++q)
+            if (omap[q] >= 0) {
+              omapc_store[q] = tabsz;
+              tabsz += (int)curposc[q].size();
+            }
+        }
+        const std::vector<int>& omapc = sep ? omapc_store : omap;
         // pass 1: per-box offsets into every array;  pass 2: fill on the host worker pool
         std::vector<Cnt>& at = P.at;
         at.resize(nj + 1);
@@ -1924,8 +2049,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             const BoxJob& J = jobs[j];
             for (int q : J.Q) c.cps += 2 * copy_tiles((int)curpos[q].size(), J.b);
             if (J.proxy) {
-              c.pts += 1;
-              c.gidx += (int)cur.act[J.a].size();
+              c.pts += sep ? 2 : 1;
+              c.gidx += (sep ? 2 : 1) * (int)cur.act[J.a].size();
             }
           }
           at[nj] = c;
@@ -1935,6 +2060,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.gidx.resize(c.gidx);
           for (size_t q = 0; q < omap.size(); ++q)
             if (omap[q] >= 0) std::copy(curpos[q].begin(), curpos[q].end(), P.maps.begin() + omap[q]);
+          if (sep)
+            for (size_t q = 0; q < omapc.size(); ++q)
+              if (omapc[q] >= 0) std::copy(curposc[q].begin(), curposc[q].end(), P.maps.begin() + omapc[q]);
         }
         std::vector<CopyTask>& cps = P.cps;
         std::vector<int>& maps = P.maps;
@@ -1945,13 +2073,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             BoxJob& J = jobs[j];
             int ci = at[j].cps;
             int row = 0;
+            // not separate: M = [A_QB ; A_BQᵀ ; proxy out ; proxy in] (ld m).  Separate IDs:
+            // M_c = [A_QB ; proxy out] and M_r = [A_BQᵀ ; proxy in], each (m/2) × b with ld m/2
+            const int mh = J.m / 2;
+            const int ldm = sep ? mh : J.m;
+            const long long MoffR = sep ? J.Moff + (long long)mh * J.b : J.Moff;
             for (int q : J.Q) {  // A_QB rows: block (q, B), rows restricted to q's current actives
               const int mo = omap[q];
               CopyTask c{};
               c.src = cur.off(q, J.a);
               c.lds = (int)cur.act[q].size();
               c.dst = J.Moff + row;
-              c.ldd = J.m;
+              c.ldd = ldm;
               c.rows = (int)curpos[q].size();
               c.cols = J.b;
               c.trans = 0;
@@ -1960,14 +2093,15 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               ci += emit_copy_tiles(c, &cps[ci]);
               row += c.rows;
             }
-            for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed
-              const int mo = omap[q];
+            if (sep) row = 0;
+            for (int q : J.Q) {  // A_BQᵀ rows: block (B, q) transposed (q's current active columns)
+              const int mo = omapc[q];
               CopyTask c{};
               c.src = cur.off(J.a, q);
               c.lds = J.b;
-              c.dst = J.Moff + row;
-              c.ldd = J.m;
-              c.rows = (int)curpos[q].size();
+              c.dst = MoffR + row;
+              c.ldd = ldm;
+              c.rows = (int)curposc[q].size();
               c.cols = J.b;
               c.trans = 1;
               c.rmap_off = mo;
@@ -1978,11 +2112,10 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             if (J.proxy) {
               ProxyTask p{};
               p.dst = J.Moff;
-              p.ld = J.m;
+              p.ld = ldm;
               p.row0 = row;
               p.b = J.b;
               p.idx_off = at[j].gidx;
-              std::copy(cur.act[J.a].begin(), cur.act[J.a].end(), gidx.begin() + at[j].gidx);
               p.ngamma = ngamma;
               double c3[3];
               T.box_centre(cur.owners()[J.a], c3);
@@ -1991,7 +2124,19 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               p.cz = c3[2];
               p.rho = rho;
               p.sg = sg;
-              pts[at[j].pts] = p;
+              if (!sep) {
+                std::copy(cur.act[J.a].begin(), cur.act[J.a].end(), gidx.begin() + at[j].gidx);
+                pts[at[j].pts] = p;
+              } else {  // outgoing rows on B's active columns (M_c), incoming rows on its active rows (M_r)
+                std::copy(cur.actc[J.a].begin(), cur.actc[J.a].end(), gidx.begin() + at[j].gidx);
+                std::copy(cur.act[J.a].begin(), cur.act[J.a].end(), gidx.begin() + at[j].gidx + J.b);
+                p.mode = 1;
+                pts[at[j].pts] = p;
+                p.mode = 2;
+                p.dst = MoffR;
+                p.idx_off = at[j].gidx + J.b;
+                pts[at[j].pts + 1] = p;
+              }
             }
           }
         });
@@ -2034,7 +2179,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       borrow_ws(h, 2, M, std::max<long long>(IP.wsM, 1) * sizeof(cplx), st);
       borrow_ws(h, 3, Tb, std::max<long long>(IP.wsT, 1) * sizeof(cplx), st);
       permd.alloc((size_t)permtot * sizeof(int), st);
-      kd.alloc((size_t)nj * sizeof(int), st);
+      const int np = sep ? 2 * nj : nj;  // ID problems: one per box, or (column side, row side) per box
+      kd.alloc((size_t)np * sizeof(int), st);
       track(h, M.bytes + Tb.bytes);
       {
         std::vector<CopyTask>& cps = IP.cps;
@@ -2046,21 +2192,33 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         s.upload(st);
         lap(8);
         const int nwaves = (int)wave_start.size() - 1;
-        std::vector<cplx*> mp(nj);
-        std::vector<int> mrows(nj), bcol(nj), pofs(nj), mfin(nj);
-        std::vector<long long> tofs(nj);
+        std::vector<cplx*> mp(np);
+        std::vector<int> mrows(np), bcol(np), pofs(np), mfin(np);
+        std::vector<long long> tofs(np);
         for (int j = 0; j < nj; ++j) {
-          mp[j] = M.as<cplx>() + jobs[j].Moff;
-          mrows[j] = jobs[j].m;
-          bcol[j] = jobs[j].b;
-          pofs[j] = jobs[j].permoff;
-          tofs[j] = jobs[j].Toff;
+          if (!sep) {
+            mp[j] = M.as<cplx>() + jobs[j].Moff;
+            mrows[j] = jobs[j].m;
+            bcol[j] = jobs[j].b;
+            pofs[j] = jobs[j].permoff;
+            tofs[j] = jobs[j].Toff;
+          } else {  // problem 2j: column ID of M_c; 2j+1: row ID (columns of M_r)
+            const int mh = jobs[j].m / 2;
+            mp[2 * j] = M.as<cplx>() + jobs[j].Moff;
+            mp[2 * j + 1] = M.as<cplx>() + jobs[j].Moff + (long long)mh * jobs[j].b;
+            mrows[2 * j] = mrows[2 * j + 1] = mh;
+            bcol[2 * j] = bcol[2 * j + 1] = jobs[j].b;
+            pofs[2 * j] = jobs[j].permoffc;
+            pofs[2 * j + 1] = jobs[j].permoff;
+            tofs[2 * j] = jobs[j].Toffc;
+            tofs[2 * j + 1] = jobs[j].Toff;
+          }
         }
         DBuf Gw;
-        std::vector<long long> goff(nj);
+        std::vector<long long> goff(np);
         if (gram_waves) {
           long long gsz = 0;
-          for (int j = 0; j < nj; ++j) {
+          for (int j = 0; j < np; ++j) {
             goff[j] = gsz;
             gsz += (long long)bcol[j] * bcol[j];
           }
@@ -2075,14 +2233,15 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           launch_proxy(s.ptr<ProxyTask>(o_p) + at[j0].pts, at[j1].pts - at[j0].pts, s.ptr<int>(o_g), M.as<cplx>(),
                        h->g, k, st, ngamma);
           h->prof.end(pid, st);
-          if (gram_waves) gram_gemm(h, mp, mrows, bcol, Gw.as<cplx>(), goff, j0, j1, keep);
+          if (gram_waves) gram_gemm(h, mp, mrows, bcol, Gw.as<cplx>(), goff, sep ? 2 * j0 : j0, sep ? 2 * j1 : j1, keep);
         }
         {
           double by = 0, fl = 0;
           for (auto& c : cps) by += 32.0 * c.rows * c.cols;
           for (auto& p : pts) {
-            by += 32.0 * p.ngamma * p.b;
-            fl += 2.0 * p.ngamma * p.b * 60.0;  // ~60 flops per kernel entry (estimate)
+            const double part = p.mode ? 0.5 : 1.0;  // separate IDs: one row group per task
+            by += part * 32.0 * p.ngamma * p.b;
+            fl += part * 2.0 * p.ngamma * p.b * 60.0;  // ~60 flops per kernel entry (estimate)
           }
           h->prof.add(FMMLU_K_GATHER, fl, by, nwaves * ((cps.empty() ? 0 : 1) + (pts.empty() ? 0 : 1)));
         }
@@ -2091,18 +2250,74 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           lap(9);
           id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin,
                    nullptr, gram_waves);
-          for (int j = 0; j < nj; ++j) jobs[j].mfin = mfin[j];
+          for (int j = 0; j < nj; ++j) jobs[j].mfin = sep ? mfin[2 * j] + mfin[2 * j + 1] : mfin[j];
         }
         lap(13);
       }
       gmark(1);
       std::vector<int> hk(nj), hperm(permtot);
-      int* pin = h->d2h(nj + permtot);
-      FMMLU_CUDA(cudaMemcpyAsync(pin, kd.p, nj * sizeof(int), cudaMemcpyDeviceToHost, st));
-      FMMLU_CUDA(cudaMemcpyAsync(pin + nj, permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
+      int* pin = h->d2h(np + permtot);
+      FMMLU_CUDA(cudaMemcpyAsync(pin, kd.p, np * sizeof(int), cudaMemcpyDeviceToHost, st));
+      FMMLU_CUDA(cudaMemcpyAsync(pin + np, permd.p, permtot * sizeof(int), cudaMemcpyDeviceToHost, st));
       wait_stream(h, st);
-      std::memcpy(hk.data(), pin, nj * sizeof(int));
-      std::memcpy(hperm.data(), pin + nj, permtot * sizeof(int));
+      if (!sep) {
+        std::memcpy(hk.data(), pin, nj * sizeof(int));
+      } else {
+        for (int j = 0; j < nj; ++j) {
+          jobs[j].kc0 = pin[2 * j];
+          jobs[j].kr0 = pin[2 * j + 1];
+        }
+      }
+      std::memcpy(hperm.data(), pin + np, permtot * sizeof(int));
+      if (sep) {
+        // Both sides keep S = pivots_r ∪ pivots_c (DESIGN R12): X_{R_r R_c} must be square, and where
+        // R_r ≠ R_c as sets it is a kernel matrix between different point sets, whose inverse amplifies
+        // the ID truncation error (measured on the bump sphere at ε = 1e-6: 1.5e-5 … 2.4e-4 with
+        // k = max(k_r, k_c) against 5.5e-7).  Each side keeps its own pivots first, promotes the other
+        // side's pivots it does not have (their T columns are dropped, the remaining columns get zero
+        // rows for them: the same ε-ID on a larger skeleton) and keeps its other redundant columns in
+        // their ascending order: perm = [own pivots | promoted | rest], keep = the rest's positions
+        // among the ID's redundant columns (the T column gather).
+        HostPool::get().parallel_for(nj, 16, [&](int j0, int j1) {
+          std::vector<char> inr, inc;
+          std::vector<int> np_;
+          for (int j = j0; j < j1; ++j) {
+            BoxJob& J = jobs[j];
+            const int b = J.b;
+            int* pr = &hperm[J.permoff];
+            int* pc = &hperm[J.permoffc];
+            inr.assign(b, 0);
+            inc.assign(b, 0);
+            for (int i = 0; i < J.kr0; ++i) inr[pr[i]] = 1;
+            for (int i = 0; i < J.kc0; ++i) inc[pc[i]] = 1;
+            int ku = J.kr0;
+            for (int i = 0; i < J.kc0; ++i) ku += !inr[pc[i]];
+            hk[j] = ku;
+            if (ku >= b) {
+              hk[j] = b;
+              continue;
+            }
+            for (int side = 0; side < 2; ++side) {
+              int* own = side == 0 ? pr : pc;
+              const int* oth = side == 0 ? pc : pr;
+              const int k0 = side == 0 ? J.kr0 : J.kc0, ko = side == 0 ? J.kc0 : J.kr0;
+              const std::vector<char>& mine = side == 0 ? inr : inc;
+              const std::vector<char>& theirs = side == 0 ? inc : inr;
+              std::vector<int>& keep = side == 0 ? J.keepr : J.keepc;
+              np_.assign(own, own + k0);
+              for (int i = 0; i < ko; ++i)
+                if (!mine[oth[i]]) np_.push_back(oth[i]);
+              keep.clear();
+              for (int q = k0; q < b; ++q)
+                if (!theirs[own[q]]) {
+                  keep.push_back(q - k0);
+                  np_.push_back(own[q]);
+                }
+              std::copy(np_.begin(), np_.end(), own);
+            }
+          }
+        });
+      }
       if (trace) {
         double before[16];
         std::memcpy(before, h->prof.ms, sizeof(before));
@@ -2131,6 +2346,12 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::sort(sk.begin(), sk.end());
         total_active -= (J.b - J.k);
         curpos[J.a] = sk;
+        if (sep) {
+          const int* pc = &hperm[J.permoffc];
+          std::vector<int> skc(pc, pc + J.k);
+          std::sort(skc.begin(), skc.end());
+          curposc[J.a] = skc;
+        }
         ident[J.a] = 0;
       }
       std::future<IdPrep> next_fut = std::async(std::launch::async, prep_id, colour + 1);
@@ -2193,6 +2414,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         int idxsz = 0;
         std::vector<long long> WBoff(nj), WNoff(nj);
         std::vector<BoxRec> recs;
+        std::vector<BoxRec> recsc;  // separate IDs: the column-side records (T_c, S_c | R_c | N_c)
         for (int j : el) {
           BoxJob& J = jobs[j];
           int r = J.b - J.k, kk = J.k, kn = kk + J.nN;
@@ -2206,6 +2428,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           R.nN = J.nN;
           R.T = facsz;
           facsz += (long long)kk * r;
+          BoxRec Rc{};
+          if (sep) {
+            Rc.T = facsz;  // T_c (k × r)
+            facsz += (long long)kk * r;
+          }
           R.Xi = facsz;
           facsz += (long long)r * r;
           R.Up = facsz;
@@ -2221,6 +2448,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           R.tmp = ph.tmp_rows;
           ph.tmp_rows += r;
           recs.push_back(R);
+          if (sep) {
+            const long long tc = Rc.T;
+            Rc = R;
+            Rc.T = tc;
+            Rc.idxS = idxsz;
+            idxsz += kk;
+            Rc.idxR = idxsz;
+            idxsz += r;
+            Rc.idxN = idxsz;
+            idxsz += J.nN;
+            recsc.push_back(Rc);
+          }
           ph.kmax = std::max(ph.kmax, kk);
           ph.rmax = std::max(ph.rmax, r);
           S.n_eliminated += 1;
@@ -2269,6 +2508,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               nmap[o] = ntab;
               ntab += (int)curpos[o].size();
             }
+        std::vector<int> nmapc_store;
+        if (sep) {
+          nmapc_store.assign(no, -1);
+          for (int o = 0; o < no; ++o)
+            if (nmap[o] >= 0) {
+              nmapc_store[o] = ntab;
+              ntab += (int)curposc[o].size();
+            }
+        }
+        const std::vector<int>& nmapc = sep ? nmapc_store : nmap;
         // pass 1 (serial, O(|N|) per box): where each box's entries go in every array
         struct Counts { int maps, cps, cpsT, cpsX, fs, tab, bld; };
         std::vector<Counts> at(el.size() + 1);
@@ -2285,11 +2534,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               nf += no_;
               nc += copy_tiles(J.b, no_) + copy_tiles(no_, J.b);
             }
-            c.maps += nm;
+            c.maps += sep ? 2 * nm + 2 * r : nm;
             c.cps += nc;  // in 64×64 tiles (split here rather than by a serial pass afterwards)
-            c.cpsT += (J.k > 0 && r > 0) ? copy_tiles(J.k, r) : 0;
+            if (!sep) {
+              c.cpsT += (J.k > 0 && r > 0) ? copy_tiles(J.k, r) : 0;
+            } else {
+              c.cpsT += (J.kr0 > 0 && r > 0) ? copy_tiles(J.kr0, r) : 0;
+              c.cpsT += (J.kc0 > 0 && r > 0) ? copy_tiles(J.kc0, r) : 0;
+            }
             c.cpsX += copy_tiles(r, r) + copy_tiles(J.k, r) + copy_tiles(J.nN, r);
-            c.fs += nf;
+            c.fs += sep ? 2 * nf : nf;
             c.tab += ns * ns;
             c.bld += ns;
           }
@@ -2306,6 +2560,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           fbld.resize(c.bld);
           for (int o = 0; o < no; ++o)
             if (nmap[o] >= 0) std::copy(curpos[o].begin(), curpos[o].end(), maps.begin() + nmap[o]);
+          if (sep)
+            for (int o = 0; o < no; ++o)
+              if (nmapc[o] >= 0) std::copy(curposc[o].begin(), curposc[o].end(), maps.begin() + nmapc[o]);
         }
         // pass 2 (host worker pool): fill
         HostPool::get().parallel_for((int)el.size(), 8, [&](int e0, int e1) {
@@ -2315,10 +2572,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             const int kk = J.k, r = R.r, b = J.b;
             const int* pm = &hperm[J.permoff];
             int mi = at[e].maps, ci = at[e].cps;
-            // local order [R | S] of B's columns
+            // local order [R | S] of B's rows and columns (separate IDs: [R_r | S_r] and [R_c | S_c])
             const int rf = mi;
             for (int i = kk; i < b; ++i) maps[mi++] = pm[i];
             for (int i = 0; i < kk; ++i) maps[mi++] = pm[i];
+            const int cf = sep ? mi : rf;
+            if (sep) {
+              const int* pc = &hperm[J.permoffc];
+              for (int i = kk; i < b; ++i) maps[mi++] = pc[i];
+              for (int i = 0; i < kk; ++i) maps[mi++] = pc[i];
+            }
             // W_B = [A_BB | A_BN] (rows/cols of B in [R|S] order), W_N = A_NB
             CopyTask c{};
             c.src = cur.off(J.a, J.a);
@@ -2329,11 +2592,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
             c.cols = b;
             c.trans = 0;
             c.rmap_off = rf;
-            c.cmap_off = rf;
+            c.cmap_off = cf;
             ci += emit_copy_tiles(c, &cps[ci]);
             int noff = 0;
             for (int o : J.N) {
-              const int mo = nmap[o];
+              const int mo = nmap[o], moc = nmapc[o];
               const int no_ = (int)curpos[o].size();
               CopyTask a{};
               a.src = cur.off(J.a, o);
@@ -2344,7 +2607,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               a.cols = no_;
               a.trans = 0;
               a.rmap_off = rf;
-              a.cmap_off = mo;
+              a.cmap_off = moc;
               ci += emit_copy_tiles(a, &cps[ci]);
               CopyTask d{};
               d.src = cur.off(o, J.a);
@@ -2355,23 +2618,48 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
               d.cols = b;
               d.trans = 0;
               d.rmap_off = mo;
-              d.cmap_off = rf;
+              d.cmap_off = cf;
               ci += emit_copy_tiles(d, &cps[ci]);
               noff += no_;
             }
             // T → factor store (k × r)
-            if (kk > 0 && r > 0) {
-              CopyTask t{};
-              t.src = J.Toff;
-              t.lds = kk;
-              t.dst = R.T;
-              t.ldd = kk;
-              t.rows = kk;
-              t.cols = r;
-              t.trans = 0;
-              t.rmap_off = -1;
-              t.cmap_off = -1;
-              emit_copy_tiles(t, &cpsT[at[e].cpsT]);
+            if (!sep) {
+              if (kk > 0 && r > 0) {
+                CopyTask t{};
+                t.src = J.Toff;
+                t.lds = kk;
+                t.dst = R.T;
+                t.ldd = kk;
+                t.rows = kk;
+                t.cols = r;
+                t.trans = 0;
+                t.rmap_off = -1;
+                t.cmap_off = -1;
+                emit_copy_tiles(t, &cpsT[at[e].cpsT]);
+              }
+            } else {
+              // the ID of a side returned T' (k' × (b − k')): its columns that stay redundant (keep) go
+              // to rows 0..k'-1 of the k × r slot; the rows of the promoted columns stay zero (cleared store)
+              int ti = at[e].cpsT;
+              for (int side = 0; side < 2; ++side) {
+                const int k0 = side == 0 ? J.kr0 : J.kc0;
+                const std::vector<int>& keepv = side == 0 ? J.keepr : J.keepc;
+                std::copy(keepv.begin(), keepv.end(), maps.begin() + mi);
+                const int ko = mi;
+                mi += r;
+                if (k0 <= 0 || r <= 0) continue;
+                CopyTask t{};
+                t.src = side == 0 ? J.Toff : J.Toffc;
+                t.lds = k0;
+                t.dst = side == 0 ? R.T : recsc[e].T;
+                t.ldd = kk;
+                t.rows = k0;
+                t.cols = r;
+                t.trans = 0;
+                t.rmap_off = -1;
+                t.cmap_off = ko;
+                ti += emit_copy_tiles(t, &cpsT[ti]);
+              }
             }
             // X_RR → Xinv slot (after E/F)
             CopyTask x{};
@@ -2433,6 +2721,22 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                 noff += no_;
               }
             }
+            if (sep) {
+              const BoxRec& Rc = recsc[e];
+              const int* pc = &hperm[J.permoffc];
+              const std::vector<int>& cB = cur.actc[J.a];
+              for (int i = 0; i < kk; ++i) hidx[Rc.idxS + i] = cB[pc[i]];
+              for (int i = 0; i < r; ++i) {
+                hidx[Rc.idxR + i] = cB[pc[kk + i]];
+                sep_pi[cB[pc[kk + i]]] = aB[pm[kk + i]];  // unknown R_c[i] ← equation R_r[i] (D⁻¹ block)
+              }
+              int noff = 0;
+              for (int o : J.N) {
+                const int no_ = (int)curposc[o].size();
+                for (int i = 0; i < no_; ++i) hidx[Rc.idxN + noff + i] = cur.actc[o][curposc[o][i]];
+                noff += no_;
+              }
+            }
             // scatter frame: [S | N] -> (slot, pos); slot 0 = B, slot 1+i = N[i]
             FrameRef fr;
             fr.slot_off = fi;
@@ -2446,6 +2750,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
                 fslot[fi] = 1 + (int)i;
                 fpos[fi++] = p;
               }
+            if (sep) {  // the column frame follows the row frame (col0 = k + |N|)
+              const int* pc = &hperm[J.permoffc];
+              for (int i = 0; i < kk; ++i) {
+                fslot[fi] = 0;
+                fpos[fi++] = pc[i];
+              }
+              for (size_t i = 0; i < J.N.size(); ++i)
+                for (int p : curposc[J.N[i]]) {
+                  fslot[fi] = 1 + (int)i;
+                  fpos[fi++] = p;
+                }
+            }
             fr.tab_off = at[e].tab;
             int ti = at[e].tab;
             for (int s1 = 0; s1 < fr.ns; ++s1) {
@@ -2516,7 +2832,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.opB = kOpN;
           P.A = Wp + WBoff[el[e]] + (long long)R.r * J.b;
           P.lda = J.b;
-          P.B = F + R.T;
+          P.B = F + (sep ? recsc[e].T : R.T);  // T_c on the column side
           P.ldb = std::max(R.k, 1);
           P.C = Wp + WBoff[el[e]];
           P.ldc = J.b;
@@ -2587,7 +2903,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           P.C = nullptr;
           P.ldc = 0;
           P.row0 = 0;
-          P.col0 = 0;
+          P.col0 = sep ? kn : 0;
           P.ns = fr.ns;
           P.slot = s2.ptr<int>(o_fs) + fr.slot_off;
           P.pos = s2.ptr<int>(o_fp) + fr.slot_off;
@@ -2604,6 +2920,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         h2d(ph.recs.p, recs.data(), recs.size() * sizeof(BoxRec), st);
         ph.nrec = (int)recs.size();
         ph.hrecs = recs;
+        if (sep) {
+          ph.recs_c.alloc(recsc.size() * sizeof(BoxRec), st);
+          h2d(ph.recs_c.p, recsc.data(), recsc.size() * sizeof(BoxRec), st);
+          ph.hrecs_c = recsc;
+        }
         {
           std::vector<SolveItem> items;
           for (int w = 0; w < ph.nwaves(); ++w) {
@@ -2638,13 +2959,71 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       std::vector<int> na;
       for (int p : curpos[a]) na.push_back(cur.act[a][p]);
       act[cur.owners()[a]] = na;
+      if (sep) {
+        na.clear();
+        for (int p : curposc[a]) na.push_back(cur.actc[a][p]);
+        actc[cur.owners()[a]] = na;
+      }
+    }
+    // Compact the level store to the still-active rows / columns (the skeletons; the eliminated R
+    // rows and columns are never read again): the next level's build and the root read the compact
+    // copy (workspace slot 1), and the big store (slot 0) is free for the next level.  cfg5: the
+    // level-6 store shrinks from ≈ 45 GB to ≈ 9 GB, so two full level stores are never held at once.
+    {
+      std::vector<int> nactoff(no + 1, 0), fposr, fposc;
+      for (int a = 0; a < no; ++a) nactoff[a + 1] = nactoff[a] + (int)curpos[a].size();
+      fposr.reserve(nactoff[no] + 1);
+      for (int a = 0; a < no; ++a) fposr.insert(fposr.end(), curpos[a].begin(), curpos[a].end());
+      if (sep) {
+        fposc.reserve(nactoff[no] + 1);
+        for (int a = 0; a < no; ++a) fposc.insert(fposc.end(), curposc[a].begin(), curposc[a].end());
+      }
+      std::vector<long long> npoffv;
+      npoffv.reserve(cur.npairs + 1);
+      long long noff = 0;
+      for (int a = 0; a < no; ++a)
+        for (size_t i = 0; i < nb[a].size(); ++i) {
+          npoffv.push_back(noff);
+          cur.poff[a][i] = noff;
+          noff += (long long)curpos[a].size() * curpos[nb[a][i]].size();
+        }
+      if (npoffv.empty()) npoffv.push_back(0);
+      if (fposr.empty()) fposr.push_back(0);
+      if (sep && fposc.empty()) fposc.push_back(0);
+      Stage s;
+      const size_t o_na = s.add(nactoff), o_np = s.add(npoffv), o_fr = s.add(fposr);
+      const size_t o_fc = sep ? s.add(fposc) : o_fr;
+      s.upload_owned(st);
+      DBuf cbsr;
+      borrow_ws(h, 1, cbsr, (size_t)std::max<long long>(noff, 1) * sizeof(cplx), st);
+      int cid = h->prof.begin(FMMLU_K_BUILD, st);
+      launch_compact_level(cur.npairs, cur.d_pair_a, cur.meta, s.ptr<int>(o_na), s.ptr<long long>(o_np),
+                           s.ptr<int>(o_fr), s.ptr<int>(o_fc), cur.bsr.as<cplx>(), cbsr.as<cplx>(), st);
+      h->prof.end(cid, st);
+      h->prof.add(FMMLU_K_BUILD, 0.0, 32.0 * noff, 1);
+      track(h, (long long)cbsr.bytes - (long long)cur.bsr.bytes);
+      cur.bsr = std::move(cbsr);
+      cur.size = noff;
+      cur.meta.actoff = s.ptr<int>(o_na);
+      cur.meta.poff = s.ptr<long long>(o_np);
+      cur.meta_buf2 = std::move(s.dev);
+      for (int a = 0; a < no; ++a) {  // the level's actives are now its final ones
+        cur.act[a] = act[cur.owners()[a]];
+        if (sep) cur.actc[a] = actc[cur.owners()[a]];
+      }
     }
     std::fill(prevOwner.begin(), prevOwner.end(), -1);
-    for (int a = 0; a < no; ++a)
+    for (int a = 0; a < no; ++a) {
       for (size_t i = 0; i < cur.act[a].size(); ++i) {
         prevOwner[cur.act[a][i]] = a;
         prevPos[cur.act[a][i]] = (int)i;
       }
+      if (sep)
+        for (size_t i = 0; i < cur.actc[a].size(); ++i) {
+          prevOwner[cur.actc[a][i]] = a;
+          prevPosc[cur.actc[a][i]] = (int)i;
+        }
+    }
     prev = std::move(cur);
     S.t_levels_ms[lvl] = now_ms() - tl0;  // host-side span of the level (GPU work may still drain)
   }
@@ -2674,6 +3053,17 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     for (int i = 0; i < n; ++i) Bt.push_back(i);
   }
   std::sort(Bt.begin(), Bt.end());
+  std::vector<int> Btc_store;  // separate IDs: the root's columns B_t^c (as many as its rows)
+  if (sep) {
+    if (prev.level >= 0) {
+      for (size_t a = 0; a < prev.owners().size(); ++a)
+        for (int g : actc[prev.owners()[a]]) Btc_store.push_back(g);
+    } else {
+      Btc_store = Bt;
+    }
+    std::sort(Btc_store.begin(), Btc_store.end());
+  }
+  const std::vector<int>& Btc = sep ? Btc_store : Bt;
   const int n0 = (int)Bt.size();
   h->n0 = n0;
   {
@@ -2689,7 +3079,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     const size_t avail = fr + (size_t)(res - used) + big_cache(h->dev).cached();
     const size_t need = (size_t)n0 * n0 * sizeof(cplx) * 2 + (4ull << 30);
     if (avail < need) {
-      const int keep_slot = prev.level >= 0 ? (prev.level & 1) : -1;
+      const int keep_slot = prev.level >= 0 ? 1 : -1;  // the compacted store the root reads
       for (int sl = 0; sl < 6; ++sl)
         if (sl != keep_slot && h->ws[sl].p) {
           h->ws[sl].st = st;
@@ -2704,6 +3094,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     track(h, h->root.bytes);
     S.factor_bytes += h->root.bytes;
     std::vector<int> slot(n0), pos(n0), bld;
+    std::vector<int> slotc(sep ? n0 : 0), posc(sep ? n0 : 0);
     std::vector<long long> tab;
     int ns = 1;
     if (prev.level >= 0) {
@@ -2712,12 +3103,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         slot[i] = prevOwner[Bt[i]];
         pos[i] = prevPos[Bt[i]];
       }
+      if (sep)
+        for (int i = 0; i < n0; ++i) {
+          slotc[i] = prevOwner[Btc[i]];
+          posc[i] = prevPosc[Btc[i]];
+        }
       tab.assign((size_t)ns * ns, -1);
       for (int a = 0; a < ns; ++a)
         for (int b = 0; b < ns; ++b) tab[(size_t)a * ns + b] = prev.off(a, b);
       for (int a = 0; a < ns; ++a) bld.push_back((int)prev.act[a].size());
     } else {
       std::fill(slot.begin(), slot.end(), -1);
+      std::fill(slotc.begin(), slotc.end(), -1);
       tab.push_back(-1);
       bld.push_back(0);
     }
@@ -2741,10 +3138,12 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     Stage s;
     size_t o_t = s.add(tasks), o_g = s.add(Bt), o_s = s.add(slot), o_p = s.add(pos), o_tab = s.add(tab),
            o_b = s.add(bld);
+    const size_t o_gc = sep ? s.add(Btc) : o_g, o_sc = sep ? s.add(slotc) : o_s, o_pc = sep ? s.add(posc) : o_p;
     s.upload(st);
     int rid = h->prof.begin(FMMLU_K_ROOT, st);
     launch_build(s.ptr<BuildTask>(o_t), (int)tasks.size(), s.ptr<int>(o_g), s.ptr<int>(o_s), s.ptr<int>(o_p),
-                 s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), h->root.as<cplx>(), h->g, k, st);
+                 s.ptr<long long>(o_tab), s.ptr<int>(o_b), prev.bsr.as<cplx>(), h->root.as<cplx>(), h->g, k, st,
+                 s.ptr<int>(o_gc), s.ptr<int>(o_sc), s.ptr<int>(o_pc));
     h->prof.end(rid, st);
     h->prof.add(FMMLU_K_ROOT, 60.0 * (double)n0 * n0, 16.0 * (double)n0 * n0, 1);
     // dense LU with partial pivoting of the root block
@@ -2789,8 +3188,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     for (int i = 0; i < n0; ++i) rin[i] = Bt[sig[i]];
     h->root_rows.alloc((size_t)n0 * sizeof(int), st);
     h->root_rows_in.alloc((size_t)n0 * sizeof(int), st);
-    h2d(h->root_rows.p, Bt.data(), n0 * sizeof(int), st);
+    h2d(h->root_rows.p, Btc.data(), n0 * sizeof(int), st);  // the solve writes the unknowns at B_t^c
     h2d(h->root_rows_in.p, rin.data(), n0 * sizeof(int), st);
+    wait_stream(h, st);
+  }
+  if (sep) {
+    if ((int)Btc.size() != n0) throw Error(FMMLU_ECUDA, "separate IDs: root rows / columns differ in number");
+    // a bijection: the root's unknowns pair with its equations (both sweeps overwrite those entries)
+    for (int i = 0; i < n0; ++i) sep_pi[Btc[i]] = Bt[i];
+    h->sep_perm.alloc((size_t)std::max(n, 1) * sizeof(int), st);
+    h2d(h->sep_perm.p, sep_pi.data(), (size_t)n * sizeof(int), st);
     wait_stream(h, st);
   }
   if (prev.bsr.p) track(h, -(long long)prev.bsr.bytes);
@@ -2924,9 +3331,12 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
     keep.push_back(std::move(s.dev));
   }
   // ---- root: y[B_t] ← A_t⁻¹ y[B_t] (LU triangular solves)
+  SepSwap swp;
+  cplx* const yeq = y;  // the equation-side vector
+  if (cplx* y2 = swp.begin(h, y, ldy, Q, st)) y = y2;
   if (h->n0 > 0) {
     int rid = P.begin(FMMLU_K_SOLVE, st);
-    root_solve(h, y, ldy, Q, st);
+    root_solve(h, yeq, ldy, Q, st, y);
     P.end(rid, st);
     P.add(FMMLU_K_SOLVE, 8.0 * (double)h->n0 * h->n0 * Q, 16.0 * (double)h->n0 * h->n0, 4);
   }
@@ -2943,23 +3353,24 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
     const SweepWs* dL = s.ptr<SweepWs>(oL);
     const cplx* F = ph.fac.as<cplx>();
     FMMLU_CUDA(cudaMemsetAsync(W + z0, 0, (size_t)(tot - z0) * sizeof(cplx), st));
-    launch_sweep_move(ph.recs.as<BoxRec>(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 0, st);
+    launch_sweep_move(ph.down_recs(), dL, ph.nrec, ph.idx.as<int>(), y, ldy, Q, W, 0, st);
     for (size_t e = 0; e < L.size(); ++e) {
-      const BoxRec& R = ph.hrecs[e];
+      const BoxRec& R = ph.down_hrecs()[e];
       const int kn = R.k + R.nN;
       prob(R.r, Q, kn, kOpN, F + R.Up, R.r, W + L[e].ysn, kn, W + L[e].yr, R.r);
     }
     run_gemms(gp, gt, m1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
     for (size_t e = 0; e < L.size(); ++e) {
-      const BoxRec& R = ph.hrecs[e];
+      const BoxRec& R = ph.down_hrecs()[e];
       if (R.k > 0) prob(R.k, Q, R.r, kOpN, F + R.T, R.k, W + L[e].yr, R.r, W + L[e].dsn, R.k);
     }
     run_gemms(gp, gt, p1, 0, nullptr, st, keep, P, FMMLU_K_SOLVE);
     for (int w = 0; w < ph.nwaves(); ++w)
-      launch_sweep_move(ph.recs.as<BoxRec>() + ph.wrec[w], dL + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
+      launch_sweep_move(ph.down_recs() + ph.wrec[w], dL + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
                         ph.idx.as<int>(), y, ldy, Q, W, 2, st);
     keep.push_back(std::move(s.dev));
   }
+  swp.end(h, yeq, Q, st);
   P.end(id, st);
   wait_stream(h, st);  // keep (staging, workspace) outlives the launches; resets the staging arenas
 }
@@ -2990,15 +3401,19 @@ void sweeps_boxes(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cplx* scr, cudaSt
                        ph.items.as<SolveItem>() + ph.witem[w], ph.witem[w + 1] - ph.witem[w], ph.fac.as<cplx>(),
                        ph.idx.as<int>(), y, ldy, nrhs, scr, st, ph.kmax, ph.rmax);
   if (trace) FMMLU_CUDA(cudaEventRecord(ev[1], st));
-  root_solve(h, y, ldy, nrhs, st);
+  SepSwap swp;
+  cplx* const yeq = y;
+  if (cplx* y2 = swp.begin(h, y, ldy, nrhs, st)) y = y2;
+  root_solve(h, yeq, ldy, nrhs, st, y);
   if (trace) FMMLU_CUDA(cudaEventRecord(ev[2], st));
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
     FMMLU_CUDA(cudaMemsetAsync(scr, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
     for (int w = it->nwaves() - 1; w >= 0; --w)
-      launch_solve_down2(it->recs.as<BoxRec>() + it->wrec[w], it->wrec[w + 1] - it->wrec[w],
+      launch_solve_down2(it->down_recs() + it->wrec[w], it->wrec[w + 1] - it->wrec[w],
                          it->items.as<SolveItem>() + it->witem[w], it->witem[w + 1] - it->witem[w],
                          it->fac.as<cplx>(), it->idx.as<int>(), y, ldy, nrhs, scr, st, it->rmax, it->kmax);
   }
+  swp.end(h, yeq, nrhs, st);
   if (trace) {
     FMMLU_CUDA(cudaEventRecord(ev[3], st));
     FMMLU_CUDA(cudaEventSynchronize(ev[3]));
@@ -3075,8 +3490,8 @@ void apply_prepare(fmmlu_handle* h) {
   std::vector<DBuf> keep;
   for (auto& ph : h->phases) {
     if (ph.nrec <= 0) continue;
-    std::vector<BoxRec> recs(ph.nrec);
-    FMMLU_CUDA(cudaMemcpyAsync(recs.data(), ph.recs.p, recs.size() * sizeof(BoxRec), cudaMemcpyDeviceToHost, st));
+    std::vector<BoxRec> recs(ph.nrec);  // separate IDs: D acts on the unknowns at R_c (column records)
+    FMMLU_CUDA(cudaMemcpyAsync(recs.data(), ph.down_recs(), recs.size() * sizeof(BoxRec), cudaMemcpyDeviceToHost, st));
     FMMLU_CUDA(cudaStreamSynchronize(st));
     long long off = 0;
     std::vector<std::pair<long long, int>> mats;
@@ -3130,14 +3545,24 @@ void apply_impl(fmmlu_handle* h, void* xio, int nrhs) {
   for (auto& ph : h->phases) {  // W_M⋯W₁ x: W₁ first
     FMMLU_CUDA(cudaMemsetAsync(scr.p, 0, (size_t)ph.tmp_rows * nrhs * sizeof(cplx), st));
     for (int w = 0; w < ph.nwaves(); ++w)
-      launch_apply_w(ph.recs.as<BoxRec>() + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
+      launch_apply_w(ph.down_recs() + ph.wrec[w], ph.wrec[w + 1] - ph.wrec[w],
                      ph.items.as<SolveItem>() + ph.witem[w], ph.witem[w + 1] - ph.witem[w], ph.fac.as<cplx>(),
                      ph.idx.as<int>(), yp, n, nrhs, scr.as<cplx>(), st, ph.rmax, ph.kmax);
   }
   for (auto& ph : h->phases)  // D on the R blocks
     launch_apply_d(ph.ap_recs.as<BoxRec>(), ph.nrec, ph.ap_xs.as<cplx>(), ph.idx.as<int>(), yp, n, nrhs,
                    scr.as<cplx>(), st, ph.rmax);
-  root_fwd(h, yp, n, nrhs, st);  // P_t A_{B_tB_t} P_tᵀ from the stored L·U
+  // separate IDs: D mapped the unknowns at R_c in place; the products belong to the equations R_r,
+  // y2[sep_perm[c]] = y[c], and the root block maps y[B_t^c] to y2[B_t]; the V sweep runs on y2
+  DBuf y2;
+  if (h->fac_separate) {
+    y2.alloc((size_t)n * nrhs * sizeof(cplx), st);
+    launch_rows_move(h->sep_perm.as<int>(), n, y2.as<cplx>(), n, yp, nrhs, 1, st);
+    root_fwd(h, yp, n, nrhs, st, y2.as<cplx>());
+    yp = y2.as<cplx>();
+  } else {
+    root_fwd(h, yp, n, nrhs, st);  // P_t A_{B_tB_t} P_tᵀ from the stored L·U
+  }
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it)  // V₁⋯V_M: V_M first
     for (int w = it->nwaves() - 1; w >= 0; --w)
       launch_apply_v(it->recs.as<BoxRec>() + it->wrec[w], it->wrec[w + 1] - it->wrec[w],
@@ -3913,6 +4338,7 @@ int fmmlu_boxes(const double* pts, const double* nrm, const double* npts, const 
     // the Householder path (ε < 1e-7) has it by construction.
     h->id_mode = 0;
     h->id_refine = 2;
+    h->pchol_ll = getenv("FMMLU_BOXES_LL") ? atoi(getenv("FMMLU_BOXES_LL")) : 0;  // cfg4 ranks are ≈ b
     if (const char* e = getenv("FMMLU_BOXES_ID_MODE")) h->id_mode = atoi(e);
     if (const char* e = getenv("FMMLU_BOXES_REFINE")) h->id_refine = atoi(e);
     boxes_impl(h, pts, nrm, npts, nnrm, nbox, b, nnear, w, k, eps, n_gamma, rho, ranks, perm, nkeep, keep, delta,
@@ -3943,6 +4369,7 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->root_rows_in.release();
   h->root_dinv.release();
   h->root_flags.release();
+  h->sep_perm.release();
   for (auto& w : h->ws_slot) w.release();
   h->geo.release();
   h->perm.release();
@@ -4010,6 +4437,9 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value) {
   } else if (k == "gj_mode") {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "gj_mode must be 0 or 1");
     h->gj_mode = (int)value;
+  } else if (k == "separate_id") {
+    if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "separate_id must be 0 or 1");
+    h->separate_id = (int)value;
   } else if (k == "deterministic") {
     if (value != 0 && value != 1) return fail(FMMLU_EINVAL, "deterministic must be 0 or 1");
     h->deterministic = (int)value;

@@ -133,21 +133,23 @@ __device__ __forceinline__ void cluster_argmax(cg::cluster_group& cl, int CL, do
 // ------------------------------------------------------------------ block builder
 __global__ void k_build(const BuildTask* __restrict__ tasks, const int* __restrict__ gidx,
                         const int* __restrict__ slot, const int* __restrict__ pos,
-                        const long long* __restrict__ tab, const int* __restrict__ bld,
-                        const cplx* __restrict__ src, cplx* __restrict__ dst, Geo g, double k) {
+                        const int* __restrict__ gidxc, const int* __restrict__ slotc,
+                        const int* __restrict__ posc, const long long* __restrict__ tab,
+                        const int* __restrict__ bld, const cplx* __restrict__ src, cplx* __restrict__ dst, Geo g,
+                        double k) {
   const BuildTask t = tasks[blockIdx.x];
   const int n = t.ni * t.nj;
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int i = t.i0 + e % t.ni, j = t.j0 + e / t.ni;
     const int ri = t.rows_off + i, cj = t.cols_off + j;
-    const int si = slot[ri], sj = slot[cj];
+    const int si = slot[ri], sj = slotc[cj];
     cplx v;
     long long off = -1;
     if (si >= 0 && sj >= 0) off = tab[t.tab_off + si * t.ns + sj];
     if (off >= 0) {
-      v = src[off + pos[ri] + (size_t)pos[cj] * bld[t.bld_off + si]];
+      v = src[off + pos[ri] + (size_t)posc[cj] * bld[t.bld_off + si]];
     } else {
-      v = entry_scaled(g, k, gidx[ri], gidx[cj]);
+      v = entry_scaled(g, k, gidx[ri], gidxc[cj]);
     }
     dst[t.dst + i + (size_t)j * t.ldd] = v;
   }
@@ -194,12 +196,12 @@ __global__ void __launch_bounds__(256) k_build_level(const int2* __restrict__ ta
   for (int e = threadIdx.x; e < ni * nj; e += blockDim.x) {
     const int i = i0 + e % ni, j = j0 + e / ni;
     const int ri = ra0 + i, cj = rb0 + j;
-    const int si = cur.slot[ri], sj = cur.slot[cj];
+    const int si = cur.slot[ri], sj = cur.slotc[cj];
     long long off = -1;
     if (has_prev && si >= 0 && sj >= 0) off = tab[si * 8 + sj];
     cplx v;
-    if (off >= 0) v = src[off + cur.pos[ri] + (size_t)cur.pos[cj] * bld[si]];
-    else v = entry_scaled(g, k, cur.gidx[ri], cur.gidx[cj]);
+    if (off >= 0) v = src[off + cur.pos[ri] + (size_t)cur.posc[cj] * bld[si]];
+    else v = entry_scaled(g, k, cur.gidx[ri], cur.gidxc[cj]);
     out[i + (size_t)j * ra] = v;
   }
 }
@@ -293,8 +295,12 @@ __global__ void __launch_bounds__(256) k_proxy(const ProxyTask* __restrict__ tas
     const cplx Ko = cmk(dre + k * sn * gg, dim - k * c * gg);
     // incoming G(x_j, y_l)
     const cplx Gi = cmk(c * gg, sn * gg);
-    ws[t.dst + (t.row0 + l) + (size_t)j * t.ld] = cscale(Ko, scl);
-    ws[t.dst + (t.row0 + t.ngamma + l) + (size_t)j * t.ld] = cscale(Gi, scl);
+    if (t.mode == 0) {
+      ws[t.dst + (t.row0 + l) + (size_t)j * t.ld] = cscale(Ko, scl);
+      ws[t.dst + (t.row0 + t.ngamma + l) + (size_t)j * t.ld] = cscale(Gi, scl);
+    } else {
+      ws[t.dst + (t.row0 + l) + (size_t)j * t.ld] = cscale(t.mode == 1 ? Ko : Gi, scl);
+    }
   }
 }
 
@@ -1308,7 +1314,10 @@ __global__ void __launch_bounds__(CK_NT) k_pchol_cluster(const ClusterQrTask* __
 template <int MR, int MC, bool MULTI, bool TIMING = false, bool PUSH = false>
 __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __restrict__ tasks,
                                                         int* __restrict__ perm_out, int* __restrict__ k_out,
-                                                        double eps, cplx* __restrict__ xs, long long xstride) {
+                                                        double eps, cplx* __restrict__ xs, long long xstride,
+                                                        int only_flagged) {
+  // only_flagged: behind k_pchol_ll — take only the boxes it gave up on (k_out < 0; cluster-uniform)
+  if (only_flagged && k_out[blockIdx.y] >= 0) return;
   constexpr int LGMR = MR == 1 ? 0 : 1;
   long long tph[4] = {0, 0, 0, 0}, tc = 0;  // TIMING: P1 | B1+P2 (until p known) | colp+B2 | P3+B3
   cg::cluster_group cl = cg::this_cluster();
@@ -1493,6 +1502,138 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
   }
   for (int l = tid; l < ncl; l += GJR_NT) perm_out[t.out_off + posmap[rank + (l << lgCL)]] = rank + (l << lgCL);
   if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+}
+
+// Left-looking pivoted Cholesky of the Gram matrix G = MᴴM (same semantics and outputs as
+// k_pchol_reg) for boxes whose rank stays small against b (the tree path: k ≈ 50–120 of b ≈ 80–400
+// on cfg5): ONE CTA per box and no cluster, so every SM works on its own box(es).  Only the
+// computed rows of R are kept — the first `kcap` in shared memory, later ones in the task's global
+// scratch `out` (row-major, L2-resident) — and the Schur complement is never formed: step j takes
+// the argmax p of the running diagonal d (every warp computes it; ties → lowest column), loads
+// column p of G (upper triangle, conjugated below it), forms S_ip = G_ip − Σ_{l<j} conj(R_li) R_lp
+// with the rows split over NG thread groups, and writes R_ji = conj(S_ip)/√S_pp, d_i −= |S_ip|²/S_pp.
+// O(b·k²) work instead of O(b²·k), two CTA barriers per step.  Stop rule C9 on the diagonal
+// (≤ ε²·initial max).  A box that reaches `kabort` pivots gives up (k_out = −1, G untouched) and
+// is taken by the register kernel launched behind it.  grid ntasks, NT threads (NT ≥ round32(b)).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict__ tasks, int* __restrict__ perm_out,
+                                                 int* __restrict__ k_out, double eps, int kcap, int bmax,
+                                                 int kabort_min) {
+  extern __shared__ __align__(16) unsigned char llsm[];
+  const ClusterQrTask t = tasks[blockIdx.x];
+  const int b = t.b;
+  const int bpad = (b + 31) & ~31;
+  if (bpad > NT || b > bmax) __trap();  // launch configuration mismatch
+  cplx* Rs = reinterpret_cast<cplx*>(llsm);                 // [kcap][b]
+  cplx* part = Rs + (size_t)kcap * bmax;                    // [NT] partial sums of the thread groups
+  double* d = reinterpret_cast<double*>(part + NT);         // [bmax] running diagonal
+  int* done = reinterpret_cast<int*>(d + bmax);             // [bmax] column already pivoted
+  int* piv = done + bmax;                                   // [bmax] pivots in order
+  int* posmap = piv + bmax;                                 // [bmax]
+  cplx* const Rg = t.out;                                   // rows ≥ kcap: Rg[l·b + i]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int NG = NT / bpad;
+  const int grp = tid / bpad, i = tid - grp * bpad;
+  const bool col = grp < NG && i < b;
+  const int kabort = min(b, max(kabort_min, b / 2));
+  for (int c = tid; c < b; c += NT) {
+    d[c] = t.A[c + (size_t)c * t.lda].x;
+    done[c] = 0;
+  }
+  __syncthreads();
+  int kk = b;
+  bool aborted = false;
+  double d0 = 0.0;
+  for (int j = 0; j < b; ++j) {
+    double pv = -1.0;
+    int p = INT_MAX;
+    for (int c = lane; c < b; c += 32)
+      if (!done[c] && d[c] > pv) {  // ascending c within a lane: strict > keeps the lowest
+        pv = d[c];
+        p = c;
+      }
+    warp_argmax_redux(pv, p);
+    if (j == 0) d0 = pv;
+    if (!(pv > eps * eps * d0) || !(pv > 0.0) || p == INT_MAX) {
+      kk = j;
+      break;  // uniform: every warp reduces the same values
+    }
+    if (j >= kabort) {
+      aborted = true;
+      break;
+    }
+    cplx gip = cmk(0.0, 0.0);
+    if (grp == 0 && i < b) gip = i <= p ? t.A[i + (size_t)p * t.lda] : cconj(t.A[p + (size_t)i * t.lda]);
+    cplx s = cmk(0.0, 0.0);
+    if (col) {
+      // Σ_l conj(R_li) · R_lp: shared-memory rows, then the rows spilled to global memory; two
+      // independent accumulator pairs shorten the dependent DFMA chain
+      double s0x = 0.0, s0y = 0.0, s1x = 0.0, s1y = 0.0;
+      const int js = min(j, kcap);
+      int l = grp;
+      for (; l + NG < js; l += 2 * NG) {
+        const cplx a0 = Rs[(size_t)l * b + i], c0 = Rs[(size_t)l * b + p];
+        const cplx a1 = Rs[(size_t)(l + NG) * b + i], c1 = Rs[(size_t)(l + NG) * b + p];
+        s0x += a0.x * c0.x + a0.y * c0.y;
+        s0y += a0.x * c0.y - a0.y * c0.x;
+        s1x += a1.x * c1.x + a1.y * c1.y;
+        s1y += a1.x * c1.y - a1.y * c1.x;
+      }
+      for (; l < js; l += NG) {
+        const cplx a0 = Rs[(size_t)l * b + i], c0 = Rs[(size_t)l * b + p];
+        s0x += a0.x * c0.x + a0.y * c0.y;
+        s0y += a0.x * c0.y - a0.y * c0.x;
+      }
+      for (; l < j; l += NG) {  // l ≥ kcap here (l advanced in steps of NG from grp)
+        const cplx a0 = Rg[(size_t)l * b + i], c0 = Rg[(size_t)l * b + p];
+        s1x += a0.x * c0.x + a0.y * c0.y;
+        s1y += a0.x * c0.y - a0.y * c0.x;
+      }
+      s = cmk(s0x + s1x, s0y + s1y);
+    }
+    if (NG > 1) part[tid] = s;
+    __syncthreads();  // every warp has its argmax (d / done may change now); partial sums visible
+    if (grp == 0 && i < b && !done[i]) {
+      for (int g2 = 1; g2 < NG; ++g2) {
+        const cplx q = part[g2 * bpad + i];
+        s.x += q.x;
+        s.y += q.y;
+      }
+      cplx* Rj = j < kcap ? Rs + (size_t)j * b : Rg + (size_t)j * b;
+      const double isd = rsqrt(pv);
+      if (i == p) {
+        Rj[i] = cmk(pv * isd, 0.0);
+        done[i] = 1;
+        piv[j] = p;
+      } else {
+        const cplx u = cmk(gip.x - s.x, gip.y - s.y);  // S_ip;  R_ji = conj(S_ip)/√S_pp
+        Rj[i] = cmk(u.x * isd, -u.y * isd);
+        d[i] -= (u.x * u.x + u.y * u.y) / pv;
+      }
+    }
+    __syncthreads();
+  }
+  if (aborted) {
+    if (tid == 0) k_out[blockIdx.x] = -1;
+    return;
+  }
+  // ---- output: R' = [R11 R12] over G (pivot columns first, then the rest ascending), perm, k
+  if (tid == 0) {
+    for (int g = 0; g < b; ++g) posmap[g] = -1;
+    for (int q = 0; q < kk; ++q) posmap[piv[q]] = q;
+    int cpos = kk;
+    for (int g = 0; g < b; ++g)
+      if (posmap[g] < 0) posmap[g] = cpos++;
+  }
+  __syncthreads();
+  for (int e = tid; e < kk * b; e += NT) {
+    const int r = e % kk, g = e / kk;
+    const int cpos = posmap[g];
+    const cplx v = r < kcap ? Rs[(size_t)r * b + g] : Rg[(size_t)r * b + g];
+    t.A[r + (size_t)cpos * t.lda] = (cpos < kk && r > cpos) ? cmk(0.0, 0.0) : v;
+  }
+  for (int g = tid; g < b; g += NT) perm_out[t.out_off + posmap[g]] = g;
+  if (tid == 0) k_out[blockIdx.x] = kk;
 }
 
 // Pivoted Cholesky for large boxes (b beyond the cluster capacity), G and R in global memory.
@@ -2061,9 +2202,11 @@ void launch_box_geo(const double* pts, const double* nrm, const double* npts, co
 
 void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const int* slot,
                   const int* pos, const long long* tab, const int* bld, const cplx* src_arena,
-                  cplx* dst_arena, const Geo& g, double k, cudaStream_t st) {
+                  cplx* dst_arena, const Geo& g, double k, cudaStream_t st, const int* gidxc, const int* slotc,
+                  const int* posc) {
   if (ntasks <= 0) return;
-  k_build<<<ntasks, 256, 0, st>>>(d_tasks, gidx, slot, pos, tab, bld, src_arena, dst_arena, g, k);
+  k_build<<<ntasks, 256, 0, st>>>(d_tasks, gidx, slot, pos, gidxc ? gidxc : gidx, slotc ? slotc : slot,
+                                  posc ? posc : pos, tab, bld, src_arena, dst_arena, g, k);
   FMMLU_LAUNCH();
 }
 
@@ -2124,6 +2267,39 @@ void launch_build_level(const int2* d_tasks, int ntasks, const int* d_pair_a, co
                         double k, cudaStream_t st) {
   if (ntasks <= 0) return;
   k_build_level<<<ntasks, 256, 0, st>>>(d_tasks, d_pair_a, cur, prev, has_prev, src_arena, dst_arena, g, k);
+  FMMLU_LAUNCH();
+}
+
+// End of a level: keep only the still-active rows / columns of every stored block (the skeletons;
+// the eliminated R rows and columns are never read again).  One CTA per block pair p = (a, b):
+// dst block (na × nb, ld na) at newpoff[p] = src block (ld = a's level-start count) at rows
+// fposr[newactoff[a] + i], columns fposc[newactoff[b] + j].
+__global__ void __launch_bounds__(256) k_compact_level(const int* __restrict__ pair_a, const int* __restrict__ nbidx,
+                                                       const int* __restrict__ actoff, const long long* __restrict__ poff,
+                                                       const int* __restrict__ newactoff,
+                                                       const long long* __restrict__ newpoff,
+                                                       const int* __restrict__ fposr, const int* __restrict__ fposc,
+                                                       const cplx* __restrict__ src, cplx* __restrict__ dst) {
+  const int p = blockIdx.x;
+  const int a = pair_a[p], b = nbidx[p];
+  const int ra = actoff[a + 1] - actoff[a];
+  const int na = newactoff[a + 1] - newactoff[a], nb = newactoff[b + 1] - newactoff[b];
+  const int* fr = fposr + newactoff[a];
+  const int* fc = fposc + newactoff[b];
+  const cplx* S = src + poff[p];
+  cplx* D = dst + newpoff[p];
+  for (int e = threadIdx.x; e < na * nb; e += blockDim.x) {
+    const int i = e % na, j = e / na;
+    D[e] = S[fr[i] + (size_t)fc[j] * ra];
+  }
+}
+
+void launch_compact_level(int npairs, const int* pair_a, const LevelMeta& cur, const int* newactoff,
+                          const long long* newpoff, const int* fposr, const int* fposc, const cplx* src, cplx* dst,
+                          cudaStream_t st) {
+  if (npairs <= 0) return;
+  k_compact_level<<<npairs, 256, 0, st>>>(pair_a, cur.nbidx, cur.actoff, cur.poff, newactoff, newpoff, fposr, fposc,
+                                          src, dst);
   FMMLU_LAUNCH();
 }
 
@@ -2411,7 +2587,7 @@ size_t pchol_smem(int b, int CL) {
 namespace {
 template <int MR, int MC, bool MULTI>
 void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
-                long long xstride, cudaStream_t st, int CL, int bmax = 0) {
+                long long xstride, cudaStream_t st, int CL, int bmax, int only_flagged) {
   static const bool timing = getenv("FMMLU_PCHOL_TIMING") != nullptr;
   if (timing && MULTI) {
     if (CL > 8)
@@ -2427,16 +2603,16 @@ void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_pchol_reg<MR, MC, true, true>, d_tasks, perm_out, k_out, eps, xs, xstride));
+    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, k_pchol_reg<MR, MC, true, true>, d_tasks, perm_out, k_out, eps, xs, xstride, only_flagged));
     return;
   }
   if (timing && !MULTI) {
-    k_pchol_reg<MR, MC, false, true><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride);
+    k_pchol_reg<MR, MC, false, true><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride, only_flagged);
     FMMLU_LAUNCH();
     return;
   }
   if constexpr (!MULTI) {
-    k_pchol_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride);
+    k_pchol_reg<MR, MC, false><<<dim3(1, ntasks), GJR_NT, 0, st>>>(d_tasks, perm_out, k_out, eps, xs, xstride, only_flagged);
     FMMLU_LAUNCH();
   } else {
     static const int push_env = getenv("FMMLU_PCHOL_PUSH") ? atoi(getenv("FMMLU_PCHOL_PUSH")) : 1;
@@ -2454,7 +2630,7 @@ void launch_pcr(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, kern, d_tasks, perm_out, k_out, eps, xs, xstride));
+    FMMLU_CUDA(cudaLaunchKernelEx(&cfg, kern, d_tasks, perm_out, k_out, eps, xs, xstride, only_flagged));
   }
 }
 }  // namespace
@@ -2471,18 +2647,49 @@ long long pchol_reg_scratch(int bmax) {  // complex elements of exchange scratch
 }
 
 bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
-                      cudaStream_t st, int bmax) {
+                      cudaStream_t st, int bmax, int only_flagged) {
   if (ntasks <= 0) return true;
   if (bmax > GJR_NCAP) return false;
   const GjrCfg c = pchol_cfg(bmax);
   const long long xstride = pchol_reg_scratch(bmax);
-  if (bmax <= 32) launch_pcr<1, 2, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
-  else if (bmax <= 64) launch_pcr<1, 8, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1);
-  else if (bmax <= 128) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
-  else if (bmax <= 192) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
-  else if (bmax <= 256) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
-  else if (bmax <= 384) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax);
-  else launch_pcr<2, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL);
+  const int of = only_flagged;
+  if (bmax <= 32) launch_pcr<1, 2, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1, bmax, of);
+  else if (bmax <= 64) launch_pcr<1, 8, false>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, 1, bmax, of);
+  else if (bmax <= 128) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax, of);
+  else if (bmax <= 192) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax, of);
+  else if (bmax <= 256) launch_pcr<1, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax, of);
+  else if (bmax <= 384) launch_pcr<1, 24, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, bmax, of);
+  else launch_pcr<2, 16, true>(d_tasks, ntasks, perm_out, k_out, eps, xs, xstride, st, c.CL, 0, of);
+  return true;
+}
+
+// Left-looking pass (k_pchol_ll): false if bmax is beyond its thread mapping (512).  Shared memory:
+// 64 rows of R where that leaves ≥ 2 CTAs per SM, else as many rows as fit in one CTA's 220 KB.
+bool launch_pchol_ll(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
+                     cudaStream_t st, int bmax) {
+  if (ntasks <= 0) return true;
+  if (bmax > 512) return false;
+  const int NT = bmax <= 128 ? 256 : 512;
+  const size_t fixed = (size_t)NT * sizeof(cplx) + (size_t)bmax * (sizeof(double) + 3 * sizeof(int)) + 64;
+  const size_t row = (size_t)bmax * sizeof(cplx);
+  int kcap = std::min(bmax, 64);
+  if (fixed + kcap * row > 110 * 1024) kcap = std::min<int>(bmax, (int)((220 * 1024 - fixed) / row));
+  const size_t smem = fixed + (size_t)kcap * row;
+  static size_t cur256 = 0, cur512 = 0;
+  if (NT == 256) {
+    if (smem > cur256) {
+      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_ll<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cur256 = smem;
+    }
+    k_pchol_ll<256><<<ntasks, 256, smem, st>>>(d_tasks, perm_out, k_out, eps, kcap, bmax, kcap);
+  } else {
+    if (smem > cur512) {
+      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_ll<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cur512 = smem;
+    }
+    k_pchol_ll<512><<<ntasks, 512, smem, st>>>(d_tasks, perm_out, k_out, eps, kcap, bmax, kcap);
+  }
+  FMMLU_LAUNCH();
   return true;
 }
 

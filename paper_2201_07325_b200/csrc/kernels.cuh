@@ -33,6 +33,11 @@ struct LevelMeta {
   const long long* poff; // #pairs: complex offset of the block in the level arena
   const int* slptr;      // no+1: CSR of the previous-level owners each owner is made of
   const int* sllist;
+  // column side (separate incoming/outgoing IDs: an owner's active columns are
+  // as many as its active rows but other DOFs); equal to gidx / slot / pos otherwise
+  const int* gidxc;
+  const int* slotc;
+  const int* posc;
 };
 // Build every block of the level store: task = (pair, tile) with 64×64 tiles.  Each entry is the
 // carried-over value when the previous level stored the owners' child pair, else the kernel
@@ -40,6 +45,11 @@ struct LevelMeta {
 void launch_build_level(const int2* d_tasks, int ntasks, const int* d_pair_a, const LevelMeta& cur,
                         const LevelMeta& prev, int has_prev, const cplx* src_arena, cplx* dst_arena, const Geo& g,
                         double k, cudaStream_t st);
+
+// End of a level: compact the level store to the still-active rows / columns (see k_compact_level).
+void launch_compact_level(int npairs, const int* pair_a, const LevelMeta& cur, const int* newactoff,
+                          const long long* newpoff, const int* fposr, const int* fposc, const cplx* src, cplx* dst,
+                          cudaStream_t st);
 
 // Copy a (possibly index-mapped / transposed) block.
 //   !trans: dst(i,j) = src(rm(i), cm(j));   trans: dst(i,j) = src(cm(j), rm(i))
@@ -67,6 +77,8 @@ struct ProxyTask {
   long long dst;  // complex offset of M
   int ld, row0, b, idx_off, ngamma;
   double cx, cy, cz, rho, sg;
+  int mode;       // 0: both row groups; 1: the outgoing rows only, 2: the incoming rows only (at row0; f3)
+  int pad;
 };
 
 // Per-box ID on M (m × b, ld = m): CPQR with stopping rule |R_jj| ≤ eps·|R_00| (reading C9).
@@ -91,9 +103,11 @@ struct SolveItem {
   int c0;     // first row (upward, rows of Lp) or first column (downward, columns of Up)
 };
 
+// gidxc / slotc / posc: the column side of the frame (nullptr: same as the rows)
 void launch_build(const BuildTask* d_tasks, int ntasks, const int* gidx, const int* slot,
                   const int* pos, const long long* tab, const int* bld, const cplx* src_arena,
-                  cplx* dst_arena, const Geo& g, double k, cudaStream_t st);
+                  cplx* dst_arena, const Geo& g, double k, cudaStream_t st, const int* gidxc = nullptr,
+                  const int* slotc = nullptr, const int* posc = nullptr);
 void launch_copy(const CopyTask* d_tasks, int ntasks, const int* maps, const cplx* src_arena,
                  cplx* dst_arena, cudaStream_t st);
 void launch_proxy(const ProxyTask* d_tasks, int ntasks, const int* gidx, cplx* ws, const Geo& g,
@@ -159,8 +173,14 @@ bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_ou
 // Register-resident pivoted Cholesky (b ≤ 512; same outputs as launch_pchol_cluster).  xs: exchange
 // scratch of pchol_reg_scratch(bmax) complex elements per task.  false if bmax is too large.
 long long pchol_reg_scratch(int bmax);
+// only_flagged: process only the tasks with k_out[task] < 0 (those launch_pchol_ll gave up on).
 bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps, cplx* xs,
-                      cudaStream_t st, int bmax);
+                      cudaStream_t st, int bmax, int only_flagged = 0);
+// Left-looking pivoted Cholesky, one CTA per box (b ≤ 512; same outputs).  Boxes whose rank passes
+// max(rows of R held in shared memory, b/2) are left untouched with k_out = −1 for launch_pchol_reg
+// (only_flagged).  task.out: b × b scratch.  false if bmax is too large.
+bool launch_pchol_ll(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
+                     cudaStream_t st, int bmax);
 // Global-memory blocked pivoted Cholesky for boxes beyond the cluster capacity.
 struct PcholState {
   int j;       // pivots taken so far

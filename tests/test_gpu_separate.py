@@ -1,0 +1,146 @@
+"""GPU parity for the separate incoming/outgoing IDs (PAPER.md L726-732:
+"Different interpolation matrices can be used for each of A_BFᵀ and A_FB ... smaller skeleton
+sets"; L1098-1108, L1909-1914; DESIGN reading R12): libfmmlu with
+``set_param("separate_id", 1)`` against the oracle's ``rss.factor(..., separate=True)`` on the
+same seeded inputs.  Skeleton sets may differ at near-ties (and the GPU equalises the two ranks
+by promoting redundant columns where the oracle continues its greedy CPQR, R12), so agreement is
+judged on the solution (≤ 10ε), the residual against the brute-force matvec (≤ 10ε), the
+forward product, the solve∘apply round trip, and the structure both share: square pivot blocks,
+a root no larger than the simultaneous ID's."""
+import math
+
+import numpy as np
+import pytest
+
+import fmmlu_inputs as fi
+from oracle import dense, kernel as okern, rss
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2201_07325_b200 import fmmlu
+    fmmlu.load()
+    return fmmlu
+
+
+def _case(name):
+    if name == "ellipsoid3000":
+        return fi.ellipsoid(3000), 2 * math.pi, 32
+    if name == "cube1500":
+        return fi.random_cube(1500, seed=2), 3.0, 16
+    if name == "bump":
+        return fi.bump_sphere(n_base=3000, n_cap=1500, theta_c=0.05, height=0.02), 2.0, 24
+    return fi.config_geometry("cfg1"), 1.0, 64
+
+
+def _factor(F, g, k, eps, leaf, sep=1, **params):
+    h = F.FmmLu(g.points, g.normals, g.weights, leaf)
+    h.set_param("separate_id", sep)
+    for name, v in params.items():
+        h.set_param(name, v)
+    return h.factor(k, eps)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "ellipsoid3000", "cube1500", "bump"])
+@pytest.mark.parametrize("nrhs", [2, 33])
+def test_separate_parity_vs_oracle(F, case, nrhs):
+    """Both solve paths: the per-box kernels (2 RHS) and the GEMM sweeps (33 RHS)."""
+    eps = 1e-6
+    g, k, leaf = _case(case)
+    b = fi.gaussian_rhs(g.n, nrhs, 0)
+    h = _factor(F, g, k, eps, leaf)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf, separate=True)
+    xo = rss.solve(f, b[:, :2])
+    assert dense.rel_diff(x[:, :2], xo) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, x, b) <= 10 * eps
+    st = h.stats()
+    assert st["n0"] > 0
+    assert abs(st["n0"] - f.stats["n0"]) <= 0.05 * f.stats["n0"] + 2
+
+
+def test_separate_differs_from_simultaneous_and_is_smaller(F):
+    """smaller skeleton sets in aggregate; the two modes are different
+    factorizations of the same matrix (both within 10ε of the dense solve)."""
+    eps = 1e-6
+    g, k, leaf = _case("ellipsoid3000")
+    b = fi.gaussian_rhs(g.n, 2, 3)
+    xs = []
+    n0 = []
+    ranks = []
+    for sep in (0, 1):
+        h = _factor(F, g, k, eps, leaf, sep=sep)
+        x = np.asfortranarray(b.copy())
+        h.solve(x)
+        xs.append(x)
+        st = h.stats()
+        n0.append(st["n0"])
+        ranks.append(sum(st["ranks_sum"]))
+    xd = dense.dense_solve(g.points, g.normals, g.weights, k, b)
+    assert dense.rel_diff(xs[0], xd) <= 10 * eps and dense.rel_diff(xs[1], xd) <= 10 * eps
+    assert n0[1] < n0[0]
+    assert ranks[1] < ranks[0]
+    assert not np.array_equal(xs[0], xs[1])
+
+
+def test_separate_tight_eps_matches_dense(F):
+    g = fi.ellipsoid(2000)
+    k = 2 * math.pi
+    b = fi.gaussian_rhs(g.n, 1, 1)
+    h = _factor(F, g, k, 1e-12, 32)      # the Householder ID path on both sides
+    assert h.stats()["n_eliminated"] > 0
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    xd = dense.dense_solve(g.points, g.normals, g.weights, k, b)
+    assert dense.rel_diff(x, xd) < 1e-9
+
+
+def test_separate_apply_and_round_trip(F):
+    """fmmlu_apply with separate IDs: within 10ε of the brute-force A x and of the oracle's
+    separate-mode apply; solve ∘ apply = identity to rounding."""
+    eps = 1e-6
+    g, k, leaf = _case("ellipsoid3000")
+    xin = fi.gaussian_rhs(g.n, 3, 7)
+    h = _factor(F, g, k, eps, leaf)
+    y = np.asfortranarray(xin.copy())
+    h.apply(y)
+    yb = okern.matvec_unscaled(k, g.points, g.normals, g.weights, xin)
+    assert dense.rel_diff(y, yb) <= 10 * eps
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf, separate=True)
+    assert dense.rel_diff(y, rss.apply(f, xin)) <= 10 * eps
+    z = np.asfortranarray(y.copy())
+    h.solve(z)
+    assert dense.rel_diff(z, xin) < 1e-10
+
+
+def test_separate_deterministic_bitwise(F):
+    eps = 1e-6
+    g, k, leaf = _case("cube1500")
+    b = fi.gaussian_rhs(g.n, 2, 0)
+    out = []
+    for _ in range(2):
+        h = _factor(F, g, k, eps, leaf, deterministic=1)
+        x = np.asfortranarray(b.copy())
+        h.solve(x)
+        out.append(x.tobytes())
+    assert out[0] == out[1]
+
+
+def test_separate_householder_and_gram_paths_agree(F):
+    eps = 1e-6
+    g, k, leaf = _case("cube1500")
+    b = fi.gaussian_rhs(g.n, 2, 0)
+    xs = []
+    for mode in (1, 2):
+        h = _factor(F, g, k, eps, leaf, id_mode=mode)
+        x = np.asfortranarray(b.copy())
+        h.solve(x)
+        xs.append(x)
+    assert dense.rel_diff(xs[0], xs[1]) <= 10 * eps
+    assert dense.residual(g.points, g.normals, g.weights, k, xs[0], b) <= 10 * eps
