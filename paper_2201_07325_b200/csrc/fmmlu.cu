@@ -464,8 +464,13 @@ struct Stage {
     }
   }
   void upload_owned(cudaStream_t s) {  // own allocation: for data that outlives the next sync
-    dev.alloc(host.size() + 16, s);
-    h2d(dev.p, host.data(), host.size(), s);
+    const size_t n = pin ? pin_used : host.size();
+    dev.alloc(n + 16, s);
+    if (pin) {
+      if (n) FMMLU_CUDA(cudaMemcpyAsync(dev.p, pin, n, cudaMemcpyHostToDevice, s));
+    } else {
+      h2d(dev.p, host.data(), host.size(), s);
+    }
   }
   template <class T> T* ptr(size_t off) const { return reinterpret_cast<T*>(dev.as<char>() + off); }
 };
@@ -1430,9 +1435,16 @@ void gram_gemm(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<
 void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, const std::vector<int>& bcol,
               const std::vector<int>& pofs, const std::vector<long long>& tofs, double eps, int* permd, int* kd,
               cplx* Tb, std::vector<DBuf>& keep, std::vector<int>& mfin, IdAux* aux = nullptr,
-              bool gram_done = false) {
+              bool gram_done = false, bool sep_pairs = false) {
   cudaStream_t st = h->stream;
   const int nj = (int)mp.size();
+  // sep_pairs (separate IDs, DESIGN R12): problems (2j, 2j+1) are the column and row side of box j.
+  // The pivoting runs down to eps_stop < ε and reports the ε-rank beside it, so that both sides can
+  // take k = max(k_c, k_r) from their own greedy order (k_sep_ranks); kd then holds each side's
+  // final rank (smaller than k only where its pivoting stopped earlier: the host promotes there).
+  DBuf keps;
+  if (sep_pairs) keps.alloc((size_t)std::max(nj, 1) * sizeof(int), st);
+  bool have_keps = false;
   int bmax = 1;
   for (int b : bcol) bmax = std::max(bmax, b);
   std::vector<IdTask> ids(nj);
@@ -1481,7 +1493,14 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     size_t o_i = s2.add(ids), o_q = s2.add(cq);
     s2.upload(st);
     int cid = h->prof.begin(FMMLU_K_CPQR, st);
-    if (h->id_mode != 3) {
+    if (sep_pairs && h->id_mode != 3) {
+      // deeper stop, bounded by the Gram path's noise floor (R4: squared norms carry ≈ b·u·‖M‖²)
+      const double eps_stop = std::min(eps, std::max(eps / 30.0, std::sqrt(4.0 * bmax * 1.1102230246251565e-16)));
+      done_id = launch_pchol_ll(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps_stop, st, bmax, eps, keps.as<int>(),
+                                true);
+      have_keps = done_id;
+    }
+    if (!done_id && h->id_mode != 3) {
       if (reg_pchol) {  // register-resident pivoted Cholesky
         // tree path: the left-looking one-CTA-per-box kernel first (ranks stay far below b there);
         // the boxes it gives up on (k_out = −1) are taken by the register kernel behind it
@@ -1503,6 +1522,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
       pchol_big(h, G.as<cplx>(), goff, gsz, bcol, pofs, permd, kd, eps, keep);
       done_id = true;
     }
+    if (have_keps) launch_sep_ranks(kd, keps.as<int>(), nj / 2, st);
     launch_trsm_T(s2.ptr<IdTask>(o_i), kd, nj, nullptr, Tb, st, bmax);
     h->prof.end(cid, st);
     h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
@@ -1520,7 +1540,13 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     size_t o_i = s2.add(ids), o_q = s2.add(cq);
     s2.upload(st);
     int cid = h->prof.begin(FMMLU_K_CPQR, st);
-    launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd, kd, eps, st, mrows.data(), bcol.data());
+    if (sep_pairs) {
+      launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd, kd, eps / 30.0, st, mrows.data(), bcol.data(), eps,
+                         keps.as<int>());
+      launch_sep_ranks(kd, keps.as<int>(), nj / 2, st);
+    } else {
+      launch_hqr_cluster(s2.ptr<ClusterQrTask>(o_q), nj, 1, permd, kd, eps, st, mrows.data(), bcol.data());
+    }
     launch_trsm_T(s2.ptr<IdTask>(o_i), kd, nj, nullptr, Tb, st, bmax);
     h->prof.end(cid, st);
     h->prof.add(FMMLU_K_CPQR, 0, 0, 2);
@@ -1538,6 +1564,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
   } else {
     keep.push_back(std::move(G));
   }
+  keep.push_back(std::move(keps));
 }
 
 // One corrected-seminormal-equations step for the Gram-path T (R4): E = M_R − M_S T from M
@@ -1817,6 +1844,18 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       gidx.reserve(actoff[no]);
       slot.reserve(actoff[no]);
       pos.reserve(actoff[no]);
+      {
+        size_t np_ = 0, nt_ = 0;
+        for (int a = 0; a < no; ++a) {
+          np_ += nb[a].size();
+          const int ra = (int)cur.act[a].size();
+          for (int b : nb[a]) nt_ += (size_t)((ra + 63) / 64) * (((int)cur.act[b].size() + 63) / 64);
+        }
+        nbidx.reserve(np_);
+        poffv.reserve(np_);
+        pair_a.reserve(np_);
+        tasks.reserve(nt_);
+      }
       for (int a = 0; a < no; ++a) {
         const int s0 = (int)sllist.size();
         for (int g : cur.act[a]) {
@@ -1870,7 +1909,11 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (v->empty()) v->push_back(0);
       const bool nbidx_empty = poffv.empty();
       if (poffv.empty()) poffv.push_back(0);
-      Stage s;
+      Stage s;  // straight into pinned staging (tens of MB on the leaf levels of cfg5)
+      s.reserve_pinned(16 * 16 + sizeof(int) * (actoff.size() + gidx.size() + slot.size() + pos.size() + nbptr.size() +
+                                                nbidx.size() + slptr.size() + sllist.size() + pair_a.size() +
+                                                gidxc.size() + slotc.size() + posc.size()) +
+                       sizeof(long long) * poffv.size() + sizeof(int2) * tasks.size());
       size_t o_ao = s.add(actoff), o_g = s.add(gidx), o_s = s.add(slot), o_p = s.add(pos), o_np = s.add(nbptr),
              o_ni = s.add(nbidx), o_po = s.add(poffv), o_sp = s.add(slptr), o_sl = s.add(sllist),
              o_pa = s.add(pair_a), o_t = s.add(tasks);
@@ -2249,7 +2292,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         {
           lap(9);
           id_stage(h, mp, mrows, bcol, pofs, tofs, eps, permd.as<int>(), kd.as<int>(), Tb.as<cplx>(), keep, mfin,
-                   nullptr, gram_waves);
+                   nullptr, gram_waves, sep);
           for (int j = 0; j < nj; ++j) jobs[j].mfin = sep ? mfin[2 * j] + mfin[2 * j + 1] : mfin[j];
         }
         lap(13);
@@ -2270,46 +2313,57 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       }
       std::memcpy(hperm.data(), pin + np, permtot * sizeof(int));
       if (sep) {
-        // Both sides keep S = pivots_r ∪ pivots_c (DESIGN R12): X_{R_r R_c} must be square, and where
-        // R_r ≠ R_c as sets it is a kernel matrix between different point sets, whose inverse amplifies
-        // the ID truncation error (measured on the bump sphere at ε = 1e-6: 1.5e-5 … 2.4e-4 with
-        // k = max(k_r, k_c) against 5.5e-7).  Each side keeps its own pivots first, promotes the other
-        // side's pivots it does not have (their T columns are dropped, the remaining columns get zero
-        // rows for them: the same ε-ID on a larger skeleton) and keeps its other redundant columns in
-        // their ascending order: perm = [own pivots | promoted | rest], keep = the rest's positions
-        // among the ID's redundant columns (the T column gather).
+        // k = max(k_r, k_c) so that X_{R_r R_c} is square (DESIGN R12).  The ID stage already continued
+        // each side's greedy pivoting to that rank where its (deeper) stop tolerance allowed, so
+        // usually k_r = k_c here.  Where a side stopped short it keeps its pivots and promotes redundant
+        // columns — those that are skeletons on the other side first, so that R_r and R_c stay as
+        // close as possible — to skeletons: their T columns are dropped and the remaining columns get
+        // zero rows for them (the same ε-ID on a larger skeleton).  perm = [own pivots | promoted |
+        // rest in the ID's order], keep = the rest's positions among the ID's redundant columns.
         HostPool::get().parallel_for(nj, 16, [&](int j0, int j1) {
-          std::vector<char> inr, inc;
+          std::vector<char> mine, theirs;
           std::vector<int> np_;
           for (int j = j0; j < j1; ++j) {
             BoxJob& J = jobs[j];
             const int b = J.b;
-            int* pr = &hperm[J.permoff];
-            int* pc = &hperm[J.permoffc];
-            inr.assign(b, 0);
-            inc.assign(b, 0);
-            for (int i = 0; i < J.kr0; ++i) inr[pr[i]] = 1;
-            for (int i = 0; i < J.kc0; ++i) inc[pc[i]] = 1;
-            int ku = J.kr0;
-            for (int i = 0; i < J.kc0; ++i) ku += !inr[pc[i]];
-            hk[j] = ku;
-            if (ku >= b) {
+            const int kk = std::max(J.kr0, J.kc0);
+            hk[j] = kk;
+            if (kk >= b) {
               hk[j] = b;
               continue;
             }
             for (int side = 0; side < 2; ++side) {
-              int* own = side == 0 ? pr : pc;
-              const int* oth = side == 0 ? pc : pr;
+              int* own = &hperm[side == 0 ? J.permoff : J.permoffc];
+              const int* oth = &hperm[side == 0 ? J.permoffc : J.permoff];
               const int k0 = side == 0 ? J.kr0 : J.kc0, ko = side == 0 ? J.kc0 : J.kr0;
-              const std::vector<char>& mine = side == 0 ? inr : inc;
-              const std::vector<char>& theirs = side == 0 ? inc : inr;
               std::vector<int>& keep = side == 0 ? J.keepr : J.keepc;
-              np_.assign(own, own + k0);
-              for (int i = 0; i < ko; ++i)
-                if (!mine[oth[i]]) np_.push_back(oth[i]);
               keep.clear();
+              const int d = kk - k0;
+              if (d == 0) {
+                for (int q = 0; q < b - k0; ++q) keep.push_back(q);
+                continue;
+              }
+              // (the other side has ko = kk pivots here and is not rewritten)
+              mine.assign(b, 0);
+              theirs.assign(b, 0);
+              for (int i = 0; i < k0; ++i) mine[own[i]] = 1;
+              for (int i = 0; i < ko; ++i) theirs[oth[i]] = 1;
+              np_.assign(own, own + k0);
+              int taken = 0;
+              for (int q = k0; q < b && taken < d; ++q)  // the other side's skeletons first
+                if (theirs[own[q]]) {
+                  np_.push_back(own[q]);
+                  mine[own[q]] = 1;
+                  ++taken;
+                }
+              for (int q = k0; q < b && taken < d; ++q)
+                if (!mine[own[q]]) {
+                  np_.push_back(own[q]);
+                  mine[own[q]] = 1;
+                  ++taken;
+                }
               for (int q = k0; q < b; ++q)
-                if (!theirs[own[q]]) {
+                if (!mine[own[q]]) {
                   keep.push_back(q - k0);
                   np_.push_back(own[q]);
                 }
@@ -2991,6 +3045,8 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       if (fposr.empty()) fposr.push_back(0);
       if (sep && fposc.empty()) fposc.push_back(0);
       Stage s;
+      s.reserve_pinned(16 * 6 + sizeof(int) * (nactoff.size() + fposr.size() + fposc.size()) +
+                       sizeof(long long) * npoffv.size());
       const size_t o_na = s.add(nactoff), o_np = s.add(npoffv), o_fr = s.add(fposr);
       const size_t o_fc = sep ? s.add(fposc) : o_fr;
       s.upload_owned(st);
@@ -4050,11 +4106,19 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
   int rc = guarded([&] {
     ensure_device();
     double t0 = now_ms();
+    static const bool trace = getenv("FMMLU_TRACE") != nullptr || getenv("FMMLU_TREE_TRACE") != nullptr;
+    double tl[8] = {0}, tm = t0;
+    auto lap = [&](int i) {  // FMMLU_TRACE: where the host time of fmmlu_tree goes
+      const double t = now_ms();
+      tl[i] += t - tm;
+      tm = t;
+    };
     h = new fmmlu_handle();
     FMMLU_CUDA(cudaGetDevice(&h->dev));
     FMMLU_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
     order_after_legacy(h->stream);  // device inputs written on the legacy default stream are complete
+    lap(0);
     h->n = n;
     cudaStream_t st = h->stream;
     // ---- device front end (reading C14/R1): the inputs stay on the device;
@@ -4083,6 +4147,7 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     FMMLU_CUDA(cudaMemcpyAsync(hp.data(), part.p, (size_t)6 * nb * sizeof(double) + sizeof(int), cudaMemcpyDeviceToHost,
                                st));
     FMMLU_CUDA(cudaStreamSynchronize(st));
+    lap(1);
     int hflag = 0;
     std::memcpy(&hflag, hp.data() + 6 * nb, sizeof(int));
     if (hflag & 1) throw Error(FMMLU_EINVAL, "weights must be finite and > 0");
@@ -4118,15 +4183,19 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     h->geo.alloc(7 * (size_t)n * sizeof(double), st);
     h->perm.alloc(n * sizeof(long long), st);
     launch_tree_gather(P, N, W, n, i_out, q_in, h->geo.as<double>(), h->perm.as<long long>(), q_out, st);
+    lap(2);
     // boxes: subdivision + 2:1 balance on the device from the sorted keys (devtree.cu); the host
     // receives the per-level box arrays for the owner / list bookkeeping
     DevTreeResult dt;
     int dt_launches = 0;
     device_octree(k_out, n, leaf_max, st, dt, &dt_launches);
-    std::vector<int> hperm(n);
-    FMMLU_CUDA(cudaMemcpyAsync(hperm.data(), i_out, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    lap(3);
+    int* hperm = h->d2h(n);  // pinned landing buffer (a pageable copy is staged by the driver)
+    FMMLU_CUDA(cudaMemcpyAsync(hperm, i_out, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     FMMLU_CUDA(cudaStreamSynchronize(st));
-    h->tree.build_from_levels(dt.level_n, dt.code, dt.start, dt.end, dt.parent, hperm.data(), lo, side, n, leaf_max);
+    lap(4);
+    h->tree.build_from_levels(dt.level_n, dt.code, dt.start, dt.end, dt.parent, hperm, lo, side, n, leaf_max);
+    lap(5);
     // k_tree_scan/keys/gather + CUB onesweep radix sort (histogram + 8 passes) + device octree
     h->tree_launches = 3 + 9 + dt_launches;
     double* gp = h->geo.as<double>();
@@ -4139,6 +4208,12 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     S.nleaves = 0;
     for (auto& b : h->tree.boxes) S.nleaves += b.leaf();
     S.t_tree_ms = now_ms() - t0;
+    if (trace) {
+      fprintf(stderr, "[fmmlu] tree host ms: stream+order %.1f scan+sync %.1f keys/sort/gather launch %.1f octree %.1f "
+                      "perm d2h %.1f boxes %.1f | total %.1f | allocator %.1f ms in %lld calls (max %.1f)\n",
+              tl[0], tl[1], tl[2], tl[3], tl[4], tl[5], S.t_tree_ms, g_ac.alloc_ms, g_ac.nalloc, g_ac.alloc_max);
+      g_ac = AllocClock{};
+    }
   });
   if (rc != FMMLU_OK) {
     if (h) fmmlu_destroy(h);

@@ -312,7 +312,8 @@ __global__ void __launch_bounds__(256) k_proxy(const ProxyTask* __restrict__ tas
 // reads shared memory instead of L2.  smem: x 16·kk | 1/R_ll kk | chunk W·kk (complex).
 __global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks, const int* __restrict__ kv,
                                                 const cplx* __restrict__ ws, cplx* __restrict__ tarena, int W,
-                                                int bmax) {
+                                                int bmax, int NWX) {
+  // NWX: columns of T per CTA (16; fewer for boxes so large that 16 x vectors do not fit)
   extern __shared__ double shm[];
   const IdTask t = tasks[blockIdx.x];
   const int kk = kv[blockIdx.x];
@@ -320,13 +321,13 @@ __global__ void __launch_bounds__(512) k_trsm_T(const IdTask* __restrict__ tasks
   const cplx* M = t.Mp;
   cplx* T = tarena + t.T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = blockIdx.y * 16 + warp;
-  if (blockIdx.y * 16 >= r) return;  // uniform per block
-  cplx* rd = reinterpret_cast<cplx*>(shm) + (size_t)16 * bmax;  // 1 / R_ll (shared by the block's warps)
+  const int c = blockIdx.y * NWX + warp;
+  if (blockIdx.y * NWX >= r) return;  // uniform per block
+  cplx* rd = reinterpret_cast<cplx*>(shm) + (size_t)NWX * bmax;  // 1 / R_ll (shared by the block's warps)
   cplx* Rc = rd + bmax;                                          // R11[:, l0 .. l0+W) (ld kk)
   for (int l = threadIdx.x; l < kk; l += blockDim.x) rd[l] = cdiv(cmk(1.0, 0.0), M[l + (size_t)l * m]);
-  const bool act = c < r;
-  cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)warp * bmax;
+  const bool act = c < r && warp < NWX;
+  cplx* x = reinterpret_cast<cplx*>(shm) + (size_t)(warp < NWX ? warp : 0) * bmax;
   if (act)
     for (int i = lane; i < kk; i += 32) x[i] = M[i + (size_t)(kk + c) * m];
   for (int l0 = ((kk - 1) / W) * W; l0 >= 0; l0 -= W) {
@@ -1033,7 +1034,9 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_gj_reg(const GjTask* __restrict__
 // (min(m,b) × b) to t.out (ld t.ldo).  grid (CL, ntasks).
 template <int PIVOT>
 __global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __restrict__ tasks, int* __restrict__ perm_out,
-                                                       int* __restrict__ k_out, double eps) {
+                                                       int* __restrict__ k_out, double eps, double eps_rank,
+                                                       int* __restrict__ keps_out) {
+  int keps = -1;  // rank at eps_rank ≥ eps (separate IDs; see k_pchol_ll)
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ double shm[];
@@ -1090,6 +1093,7 @@ __global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __re
       cl.sync();  // (A) candidates published
       cluster_argmax(cl, CL, &cand_v, &cand_i, &cres_v, &cres_i, pv, p);
       if (j == 0) norm0 = pv;
+      if (keps < 0 && !(pv > eps_rank * norm0)) keps = j;
       if (!(pv > eps * norm0) || pv == 0.0) {
         kk = j;
         break;  // uniform across the cluster
@@ -1186,7 +1190,10 @@ __global__ void __launch_bounds__(CK_NT) k_hqr_cluster(const ClusterQrTask* __re
       const int g = rank + l * CL;
       perm_out[t.out_off + posmap[g]] = g;
     }
-    if (rank == 0 && tid == 0) k_out[blockIdx.y] = kk;
+    if (rank == 0 && tid == 0) {
+      k_out[blockIdx.y] = kk;
+      if (keps_out) keps_out[blockIdx.y] = keps < 0 ? kk : min(keps, kk);
+    }
   }
 }
 
@@ -1518,7 +1525,11 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
 template <int NT>
 __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict__ tasks, int* __restrict__ perm_out,
                                                  int* __restrict__ k_out, double eps, int kcap, int bmax,
-                                                 int kabort_min) {
+                                                 int kabort_min, double eps_rank, int* __restrict__ keps_out) {
+  // eps: where the pivoting stops; eps_rank ≥ eps: the tolerance whose rank is reported in keps_out
+  // (separate IDs, DESIGN R12: the pivoting runs deeper than ε so that the side whose ε-rank is the
+  // smaller one can take the other side's rank from the same greedy order; else eps_rank = eps and
+  // keps_out = nullptr).  kabort_min < 0: never give up.
   extern __shared__ __align__(16) unsigned char llsm[];
   const ClusterQrTask t = tasks[blockIdx.x];
   const int b = t.b;
@@ -1535,7 +1546,8 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
   const int NG = NT / bpad;
   const int grp = tid / bpad, i = tid - grp * bpad;
   const bool col = grp < NG && i < b;
-  const int kabort = min(b, max(kabort_min, b / 2));
+  const int kabort = kabort_min < 0 ? b + 1 : min(b, max(kabort_min, b / 2));
+  int keps = -1;
   for (int c = tid; c < b; c += NT) {
     d[c] = t.A[c + (size_t)c * t.lda].x;
     done[c] = 0;
@@ -1554,6 +1566,7 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
       }
     warp_argmax_redux(pv, p);
     if (j == 0) d0 = pv;
+    if (keps < 0 && !(pv > eps_rank * eps_rank * d0)) keps = j;
     if (!(pv > eps * eps * d0) || !(pv > 0.0) || p == INT_MAX) {
       kk = j;
       break;  // uniform: every warp reduces the same values
@@ -1633,7 +1646,21 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
     t.A[r + (size_t)cpos * t.lda] = (cpos < kk && r > cpos) ? cmk(0.0, 0.0) : v;
   }
   for (int g = tid; g < b; g += NT) perm_out[t.out_off + posmap[g]] = g;
-  if (tid == 0) k_out[blockIdx.x] = kk;
+  if (tid == 0) {
+    k_out[blockIdx.x] = kk;
+    if (keps_out) keps_out[blockIdx.x] = keps < 0 ? kk : min(keps, kk);
+  }
+}
+
+// Separate IDs: problems (2j, 2j+1) are the two sides of box j.  klow = the pivots each side computed
+// (down to the deeper tolerance), keps = its rank at ε.  Both sides take k = max of the two ε-ranks
+// where their pivoting reached it (the same greedy order continued); klow ← min(k, klow).
+__global__ void k_sep_ranks(int* __restrict__ klow, const int* __restrict__ keps, int npairs) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= npairs) return;
+  const int k = max(keps[2 * j], keps[2 * j + 1]);
+  klow[2 * j] = min(k, klow[2 * j]);
+  klow[2 * j + 1] = min(k, klow[2 * j + 1]);
 }
 
 // Pivoted Cholesky for large boxes (b beyond the cluster capacity), G and R in global memory.
@@ -2339,7 +2366,13 @@ void launch_gj_panel(const GjTask* d_tasks, int ntasks, int j0, int nb, int* d_s
     cur = smem;
   }
   k_gj_panel<<<ntasks, GJP_NT, smem, st>>>(d_tasks, j0, nb, d_status);
-  FMMLU_LAUNCH();
+  {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+      throw Error(-7, std::string("k_gj_panel launch: ") + cudaGetErrorString(e) + " (ntasks " +
+                                   std::to_string(ntasks) + ", nmax " + std::to_string(nmax) + ", nb " +
+                                   std::to_string(nb) + ", smem " + std::to_string(smem) + ")");
+  }
 }
 
 int gj_panel_cluster_size(int nmax, int nb) {
@@ -2666,31 +2699,36 @@ bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, i
 // Left-looking pass (k_pchol_ll): false if bmax is beyond its thread mapping (512).  Shared memory:
 // 64 rows of R where that leaves ≥ 2 CTAs per SM, else as many rows as fit in one CTA's 220 KB.
 bool launch_pchol_ll(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
-                     cudaStream_t st, int bmax) {
+                     cudaStream_t st, int bmax, double eps_rank, int* keps_out, bool no_abort) {
   if (ntasks <= 0) return true;
-  if (bmax > 512) return false;
-  const int NT = bmax <= 128 ? 256 : 512;
+  if (bmax > (no_abort ? 1024 : 512)) return false;
+  if (eps_rank <= 0.0) eps_rank = eps;
+  const int NT = bmax <= 128 ? 256 : bmax <= 512 ? 512 : 1024;
   const size_t fixed = (size_t)NT * sizeof(cplx) + (size_t)bmax * (sizeof(double) + 3 * sizeof(int)) + 64;
   const size_t row = (size_t)bmax * sizeof(cplx);
   int kcap = std::min(bmax, 64);
   if (fixed + kcap * row > 110 * 1024) kcap = std::min<int>(bmax, (int)((220 * 1024 - fixed) / row));
   const size_t smem = fixed + (size_t)kcap * row;
-  static size_t cur256 = 0, cur512 = 0;
-  if (NT == 256) {
-    if (smem > cur256) {
-      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_ll<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      cur256 = smem;
+  const int kab = no_abort ? -1 : kcap;
+  static size_t cur[3] = {0, 0, 0};
+  auto go = [&](auto kern, int slot) {
+    if (smem > cur[slot]) {
+      FMMLU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cur[slot] = smem;
     }
-    k_pchol_ll<256><<<ntasks, 256, smem, st>>>(d_tasks, perm_out, k_out, eps, kcap, bmax, kcap);
-  } else {
-    if (smem > cur512) {
-      FMMLU_CUDA(cudaFuncSetAttribute(k_pchol_ll<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      cur512 = smem;
-    }
-    k_pchol_ll<512><<<ntasks, 512, smem, st>>>(d_tasks, perm_out, k_out, eps, kcap, bmax, kcap);
-  }
+    kern<<<ntasks, NT, smem, st>>>(d_tasks, perm_out, k_out, eps, kcap, bmax, kab, eps_rank, keps_out);
+  };
+  if (NT == 256) go(k_pchol_ll<256>, 0);
+  else if (NT == 512) go(k_pchol_ll<512>, 1);
+  else go(k_pchol_ll<1024>, 2);
   FMMLU_LAUNCH();
   return true;
+}
+
+void launch_sep_ranks(int* klow, const int* keps, int npairs, cudaStream_t st) {
+  if (npairs <= 0) return;
+  k_sep_ranks<<<(npairs + 255) / 256, 256, 0, st>>>(klow, keps, npairs);
+  FMMLU_LAUNCH();
 }
 
 bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
@@ -2706,7 +2744,8 @@ bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_ou
 }
 
 void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
-                        cudaStream_t st, const int* m_of, const int* b_of) {
+                        cudaStream_t st, const int* m_of, const int* b_of, double eps_rank, int* keps_out) {
+  if (eps_rank <= 0.0) eps_rank = eps;
   if (ntasks <= 0) return;
   // smallest cluster in which every task's (m, b) fits; smem = the largest task's need
   int CL = 1;
@@ -2719,10 +2758,10 @@ void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int
   if (CL > 16) throw Error(-6, "ID matrix too large for a 16-CTA cluster");
   if (pivot) {
     cluster_attrs(k_hqr_cluster<1>, smem, CL);
-    launch_cluster(k_hqr_cluster<1>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps);
+    launch_cluster(k_hqr_cluster<1>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps, eps_rank, keps_out);
   } else {
     cluster_attrs(k_hqr_cluster<0>, smem, CL);
-    launch_cluster(k_hqr_cluster<0>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps);
+    launch_cluster(k_hqr_cluster<0>, CL, ntasks, smem, st, d_tasks, perm_out, k_out, eps, eps_rank, keps_out);
   }
 }
 
@@ -2780,15 +2819,17 @@ void launch_trsm_T(const IdTask* d_tasks, const int* d_k, int ntasks, const cplx
                    cplx* tarena, cudaStream_t st, int bmax) {
   if (ntasks <= 0) return;
   const int bm = std::max(bmax, 1);
-  const int W = std::max(1, std::min(32, (int)(14000 / bm) - 17));  // chunk width that fits 227 KB
-  const size_t smem = (size_t)(17 + W) * bm * sizeof(cplx) + 16;
+  int NWX = 16;  // x vectors (columns of T) per CTA: halved until they and a chunk of ≥ 4 columns fit 227 KB
+  while (NWX > 1 && 14000 / bm - (NWX + 1) < 4) NWX /= 2;
+  const int W = std::max(1, std::min(32, (int)(14000 / bm) - (NWX + 1)));
+  const size_t smem = (size_t)(NWX + 1 + W) * bm * sizeof(cplx) + 16;
   static size_t cur = 0;
   if (smem > 48 * 1024 && smem > cur) {
     FMMLU_CUDA(cudaFuncSetAttribute(k_trsm_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cur = smem;
   }
-  dim3 grid(ntasks, (bmax + 15) / 16);
-  k_trsm_T<<<grid, 512, smem, st>>>(d_tasks, d_k, ws, tarena, W, bm);
+  dim3 grid(ntasks, (bmax + NWX - 1) / NWX);
+  k_trsm_T<<<grid, 512, smem, st>>>(d_tasks, d_k, ws, tarena, W, bm, NWX);
   FMMLU_LAUNCH();
 }
 

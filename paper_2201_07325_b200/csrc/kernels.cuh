@@ -165,7 +165,8 @@ int hqr_cluster_size(int m, int b);  // CTAs needed to hold m × b (0 = too larg
 int hqr_max_rows(int b, int CL);     // largest m that fits a CL-CTA cluster with b columns
 // m_of / b_of: host arrays with each task's (m, b) (they size the cluster and its shared memory)
 void launch_hqr_cluster(const ClusterQrTask* d_tasks, int ntasks, int pivot, int* perm_out, int* k_out, double eps,
-                        cudaStream_t st, const int* m_of, const int* b_of);
+                        cudaStream_t st, const int* m_of, const int* b_of, double eps_rank = 0.0,
+                        int* keps_out = nullptr);
 // Pivoted Cholesky of G = MᴴM (b × b) in a cluster, same outputs as the pivoted launch above
 // (R' over G with ld b).  false if b is too large for a 16-CTA cluster.
 bool launch_pchol_cluster(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
@@ -179,8 +180,13 @@ bool launch_pchol_reg(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, i
 // Left-looking pivoted Cholesky, one CTA per box (b ≤ 512; same outputs).  Boxes whose rank passes
 // max(rows of R held in shared memory, b/2) are left untouched with k_out = −1 for launch_pchol_reg
 // (only_flagged).  task.out: b × b scratch.  false if bmax is too large.
+// eps_rank / keps_out (separate IDs): the pivoting stops at eps (< eps_rank) and keps_out receives
+// the rank at eps_rank; no_abort: never give up (b ≤ 1024 then).
 bool launch_pchol_ll(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, int* k_out, double eps,
-                     cudaStream_t st, int bmax);
+                     cudaStream_t st, int bmax, double eps_rank = 0.0, int* keps_out = nullptr,
+                     bool no_abort = false);
+// Separate IDs: klow[2j], klow[2j+1] ← min(max(keps[2j], keps[2j+1]), klow[·]) (see k_sep_ranks).
+void launch_sep_ranks(int* klow, const int* keps, int npairs, cudaStream_t st);
 // Global-memory blocked pivoted Cholesky for boxes beyond the cluster capacity.
 struct PcholState {
   int j;       // pivots taken so far
