@@ -214,6 +214,18 @@ int fmmlu_set_param(fmmlu_handle* h, const char* name, double value);
 int fmmlu_tree_boxes(const fmmlu_handle* h, int32_t* nboxes, int32_t* level, int32_t* coord, int32_t* start,
                      int32_t* end);
 
+/* The owner lists of one level (2 <= level < nlevels), as built on the device from the finished
+ * tree (PAPER.md L563-565 neighbours, L1263-1267 far-field neighbours; readings C6,
+ * C7): the owners at that level are its boxes followed by the leaves of the coarser levels (box
+ * ids as in fmmlu_tree_boxes); for the j-th level box, N = owners[nidx[nptr[j] .. nptr[j+1])]
+ * (separation <= 1 in level cells) and Q = owners[qidx[qptr[j] .. qptr[j+1])] (separation 2), both
+ * ascending in the local owner index.  counts[0..3] receive (#level boxes, #owners, |nidx|, |qidx|);
+ * call with owners == NULL to get only the counts.  Host arrays: owners[#owners],
+ * nptr / qptr [#level boxes + 1], nidx, qidx.  Colour of a level box = 4 (cx & 1) + 2 (cy & 1) +
+ * (cz & 1) (reading C8).  Errors: EINVAL (NULL argument, level out of range). */
+int fmmlu_level_lists(fmmlu_handle* h, int level, int32_t* counts, int32_t* owners, int32_t* nptr, int32_t* nidx,
+                      int32_t* qptr, int32_t* qidx);
+
 /* Tree order: perm[i] = caller index of the i-th point in tree (Morton) order.
  * perm: int64[n] host buffer. */
 int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm);

@@ -16,7 +16,10 @@
 //   per pass:   k_dt_balance   (marks)
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
+#include <climits>
 #include <vector>
 
 #include "devtree.h"
@@ -375,6 +378,266 @@ void device_octree(const unsigned long long* keys, int64_t n, int leaf_max, cuda
   DT_CHECK(cudaStreamSynchronize(st));
   for (auto& x : L) x.free(st);
   err.free(st);
+  if (launches) *launches = nl;
+}
+
+// ------------------------------------------------------------------ owner lists (see devtree.h)
+namespace {
+
+struct TopoTree {
+  const unsigned long long* code;
+  const unsigned char* leaf;
+  const int* leafrank;
+  int first[kDepthBits + 2];  // level prefix
+  int nlevels;
+};
+
+__global__ void k_leaf_i32(const unsigned char* __restrict__ leaf, int n, int* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = leaf[i] ? 1 : 0;
+}
+
+// owners of the level: its boxes (ids first[lvl] ..), then the leaves of the coarser levels
+__global__ void k_topo_owners(TopoTree T, int lvl, int nlb, int* __restrict__ owners) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= T.first[lvl + 1]) return;
+  if (b >= T.first[lvl]) owners[b - T.first[lvl]] = b;
+  else if (T.leaf[b]) owners[nlb + T.leafrank[b]] = b;
+}
+
+// Level box i (one thread): the owners covering the cells of its 5 × 5 × 5 neighbourhood — a level
+// box by binary search in the level's sorted codes, else the first ancestor cell that is a box
+// (an owner iff it is a leaf) — deduplicated, ascending; sep ≤ 1 → N, else Q (sep = the Chebyshev
+// gap in level cells between the box and the owner's extent).  cand[i·124 ..]: N first, then Q.
+__global__ void k_topo_nq(TopoTree T, int lvl, int nlb, int* __restrict__ cand, int* __restrict__ nN,
+                          int* __restrict__ nQ) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nlb) return;
+  const int f0 = T.first[lvl];
+  int c[3];
+  decode3(T.code[f0 + i], lvl, c);
+  const int lim = (1 << lvl) - 1;
+  int own[125];
+  unsigned char sp[125];
+  int n = 0;
+  for (int dx = -2; dx <= 2; ++dx)
+    for (int dy = -2; dy <= 2; ++dy)
+      for (int dz = -2; dz <= 2; ++dz) {
+        const int x = c[0] + dx, y = c[1] + dy, z = c[2] + dz;
+        if (x < 0 || y < 0 || z < 0 || x > lim || y > lim || z > lim) continue;
+        int o = -1, s = 0;
+        unsigned long long key = encode3(x, y, z, lvl);
+        int j = find_code(T.code + f0, nlb, key);
+        if (j >= 0) {
+          o = j;
+          s = max(abs(dx), max(abs(dy), abs(dz)));
+        } else {
+          for (int m = lvl - 1; m >= 0; --m) {
+            key >>= 3;
+            const int fm = T.first[m];
+            j = find_code(T.code + fm, T.first[m + 1] - fm, key);
+            if (j >= 0) {
+              if (T.leaf[fm + j]) {
+                o = nlb + T.leafrank[fm + j];
+                const int d = lvl - m;
+                const int cc[3] = {x >> d, y >> d, z >> d};
+                s = INT_MIN;
+                for (int a = 0; a < 3; ++a) {
+                  const int lo = cc[a] << d, hi = ((cc[a] + 1) << d) - 1;
+                  s = max(s, max(lo - c[a], c[a] - hi));
+                }
+              }
+              break;
+            }
+          }
+        }
+        if (o < 0 || o == i) continue;
+        // sorted insert without duplicates
+        int p = 0;
+        while (p < n && own[p] < o) ++p;
+        if (p < n && own[p] == o) continue;
+        for (int q = n; q > p; --q) {
+          own[q] = own[q - 1];
+          sp[q] = sp[q - 1];
+        }
+        own[p] = o;
+        sp[p] = (unsigned char)(s <= 1 ? 1 : 0);
+        ++n;
+      }
+  int a = 0;
+  int* out = cand + (size_t)i * 124;
+  for (int p = 0; p < n; ++p)
+    if (sp[p]) out[a++] = own[p];
+  nN[i] = a;
+  for (int p = 0; p < n; ++p)
+    if (!sp[p]) out[a++] = own[p];
+  nQ[i] = a - nN[i];
+}
+
+// compact the fixed-stride candidate lists into the N and Q CSR arrays
+__global__ void k_topo_compact(const int* __restrict__ cand, const int* __restrict__ nN, const int* __restrict__ nQ,
+                               const int* __restrict__ nptr, const int* __restrict__ qptr, int nlb,
+                               int* __restrict__ nidx, int* __restrict__ qidx) {
+  const int i = blockIdx.x;
+  if (i >= nlb) return;
+  const int* src = cand + (size_t)i * 124;
+  for (int e = threadIdx.x; e < nN[i]; e += blockDim.x) nidx[nptr[i] + e] = src[e];
+  for (int e = threadIdx.x; e < nQ[i]; e += blockDim.x) qidx[qptr[i] + e] = src[nN[i] + e];
+}
+
+__global__ void k_topo_paircount(const int* __restrict__ nN, const int* __restrict__ nQ, int nlb,
+                                 int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nlb) cnt[i] = (1 + nN[i]) * (1 + nN[i]) + 2 * nQ[i];
+}
+
+// level box i (one CTA): keys x·no + y for x, y ∈ {i} ∪ N(i), and (i, q), (q, i) for q ∈ Q(i)
+__global__ void k_topo_pairs(const int* __restrict__ nptr, const int* __restrict__ nidx,
+                             const int* __restrict__ qptr, const int* __restrict__ qidx,
+                             const int* __restrict__ poff, int no, unsigned long long* __restrict__ keys) {
+  const int i = blockIdx.x;
+  const int n1 = nptr[i + 1] - nptr[i] + 1, nq = qptr[i + 1] - qptr[i];
+  const int* N = nidx + nptr[i];
+  const int* Q = qidx + qptr[i];
+  unsigned long long* out = keys + poff[i];
+  for (int e = threadIdx.x; e < n1 * n1; e += blockDim.x) {
+    const int a = e / n1, b = e % n1;
+    const int x = a == 0 ? i : N[a - 1], y = b == 0 ? i : N[b - 1];
+    out[e] = (unsigned long long)x * no + y;
+  }
+  for (int e = threadIdx.x; e < nq; e += blockDim.x) {
+    out[n1 * n1 + 2 * e] = (unsigned long long)i * no + Q[e];
+    out[n1 * n1 + 2 * e + 1] = (unsigned long long)Q[e] * no + i;
+  }
+}
+
+// row pointers of the sorted unique keys: nbptr[a] = first key ≥ a·no; partner = key − a·no
+__global__ void k_topo_rows(const unsigned long long* __restrict__ keys, const int* __restrict__ nuniq, int no,
+                            int* __restrict__ nbptr, int* __restrict__ nbidx) {
+  const int n = *nuniq;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= no) {
+    const unsigned long long c = (unsigned long long)t * no;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] < c) lo = mid + 1;
+      else hi = mid;
+    }
+    nbptr[t] = lo;
+  }
+  for (int e = t; e < n; e += gridDim.x * blockDim.x) nbidx[e] = (int)(keys[e] % (unsigned long long)no);
+}
+
+}  // namespace
+
+void device_leafrank(const unsigned char* d_leaf, int nboxes, int* d_leafrank, cudaStream_t st) {
+  DArr<int> tmp, off;
+  tmp.resize(nboxes, st);
+  off.resize(nboxes + 1, st);
+  k_leaf_i32<<<(nboxes + 255) / 256, 256, 0, st>>>(d_leaf, nboxes, tmp.p);
+  k_dt_scan<<<1, 1024, 0, st>>>(tmp.p, nboxes, off.p);
+  DT_CHECK(cudaMemcpyAsync(d_leafrank, off.p, nboxes * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  DT_CHECK(cudaGetLastError());
+  tmp.free(st);
+  off.free(st);
+}
+
+void device_topology(const unsigned long long* d_code, const unsigned char* d_leaf, const int* d_leafrank,
+                     const int* level_first, int nlevels, int lvl, cudaStream_t st, DevTopo& out, int* launches) {
+  TopoTree T{};
+  T.code = d_code;
+  T.leaf = d_leaf;
+  T.leafrank = d_leafrank;
+  T.nlevels = nlevels;
+  for (int l = 0; l <= nlevels; ++l) T.first[l] = level_first[l];
+  const int nlb = level_first[lvl + 1] - level_first[lvl];
+  int nl = 0;
+  // coarser leaves: leafrank of the level's first box
+  int ncoarse = 0;
+  DT_CHECK(cudaMemcpyAsync(&ncoarse, d_leafrank + level_first[lvl], sizeof(int), cudaMemcpyDeviceToHost, st));
+  DT_CHECK(cudaStreamSynchronize(st));
+  const int no = nlb + ncoarse;
+  out.nlb = nlb;
+  out.no = no;
+  DArr<int> owners, cand, nN, nQ, nptr, qptr, nidx, qidx, pcnt, poff, nbptr, nbidx, nuniq;
+  owners.resize(no, st);
+  cand.resize((size_t)nlb * 124, st);
+  nN.resize(nlb, st);
+  nQ.resize(nlb, st);
+  nptr.resize(nlb + 1, st);
+  qptr.resize(nlb + 1, st);
+  pcnt.resize(nlb, st);
+  poff.resize(nlb + 1, st);
+  nuniq.resize(1, st);
+  k_topo_owners<<<(level_first[lvl + 1] + 255) / 256, 256, 0, st>>>(T, lvl, nlb, owners.p);
+  k_topo_nq<<<(nlb + 63) / 64, 64, 0, st>>>(T, lvl, nlb, cand.p, nN.p, nQ.p);
+  k_dt_scan<<<1, 1024, 0, st>>>(nN.p, nlb, nptr.p);
+  k_dt_scan<<<1, 1024, 0, st>>>(nQ.p, nlb, qptr.p);
+  k_topo_paircount<<<(nlb + 255) / 256, 256, 0, st>>>(nN.p, nQ.p, nlb, pcnt.p);
+  k_dt_scan<<<1, 1024, 0, st>>>(pcnt.p, nlb, poff.p);
+  nl += 6;
+  int tot[3] = {0, 0, 0};
+  DT_CHECK(cudaMemcpyAsync(&tot[0], nptr.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DT_CHECK(cudaMemcpyAsync(&tot[1], qptr.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DT_CHECK(cudaMemcpyAsync(&tot[2], poff.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DT_CHECK(cudaStreamSynchronize(st));
+  if (tot[2] < 0) throw Error(-8, "device topology: more than 2^31 candidate block pairs at one level");
+  nidx.resize(tot[0], st);
+  qidx.resize(tot[1], st);
+  k_topo_compact<<<std::max(nlb, 1), 64, 0, st>>>(cand.p, nN.p, nQ.p, nptr.p, qptr.p, nlb, nidx.p, qidx.p);
+  ++nl;
+  // pair set: candidate keys → radix sort → unique → CSR
+  const int npair = tot[2];
+  DArr<unsigned long long> keys, keys2, uniq;
+  keys.resize(npair, st);
+  keys2.resize(npair, st);
+  uniq.resize(npair, st);
+  if (nlb > 0) k_topo_pairs<<<nlb, 128, 0, st>>>(nptr.p, nidx.p, qptr.p, qidx.p, poff.p, no, keys.p);
+  int bits = 1;
+  while (((unsigned long long)1 << bits) < (unsigned long long)no * no) ++bits;
+  size_t tb1 = 0, tb2 = 0;
+  DT_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, tb1, keys.p, keys2.p, npair, 0, bits, st));
+  DT_CHECK(cub::DeviceSelect::Unique(nullptr, tb2, keys2.p, uniq.p, nuniq.p, npair, st));
+  DArr<unsigned char> tmp;
+  tmp.resize(std::max(tb1, tb2), st);
+  size_t tb = tmp.n;
+  DT_CHECK(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, keys2.p, npair, 0, bits, st));
+  tb = tmp.n;
+  DT_CHECK(cub::DeviceSelect::Unique(tmp.p, tb, keys2.p, uniq.p, nuniq.p, npair, st));
+  int nu = 0;
+  DT_CHECK(cudaMemcpyAsync(&nu, nuniq.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DT_CHECK(cudaStreamSynchronize(st));
+  nbptr.resize(no + 1, st);
+  nbidx.resize(nu, st);
+  k_topo_rows<<<(std::max(no + 1, nu) + 255) / 256, 256, 0, st>>>(uniq.p, nuniq.p, no, nbptr.p, nbidx.p);
+  nl += 2 + 8;  // + the CUB sort passes / select (approximate count)
+  DT_CHECK(cudaGetLastError());
+  // results to the host
+  out.owners.resize(no);
+  out.nptr.resize(nlb + 1);
+  out.qptr.resize(nlb + 1);
+  out.nidx.resize(tot[0]);
+  out.qidx.resize(tot[1]);
+  out.nbptr.resize(no + 1);
+  out.nbidx.resize(nu);
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) DT_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  };
+  d2h(out.owners.data(), owners.p, no * sizeof(int));
+  d2h(out.nptr.data(), nptr.p, (nlb + 1) * sizeof(int));
+  d2h(out.qptr.data(), qptr.p, (nlb + 1) * sizeof(int));
+  d2h(out.nidx.data(), nidx.p, (size_t)tot[0] * sizeof(int));
+  d2h(out.qidx.data(), qidx.p, (size_t)tot[1] * sizeof(int));
+  d2h(out.nbptr.data(), nbptr.p, (no + 1) * sizeof(int));
+  d2h(out.nbidx.data(), nbidx.p, (size_t)nu * sizeof(int));
+  DT_CHECK(cudaStreamSynchronize(st));
+  for (DArr<int>* a : {&owners, &cand, &nN, &nQ, &nptr, &qptr, &nidx, &qidx, &pcnt, &poff, &nbptr, &nbidx, &nuniq})
+    a->free(st);
+  keys.free(st);
+  keys2.free(st);
+  uniq.free(st);
+  tmp.free(st);
   if (launches) *launches = nl;
 }
 

@@ -20,6 +20,7 @@
 #include <malloc.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -614,6 +615,11 @@ struct fmmlu_handle {
   size_t cur_bytes = 0, peak_bytes = 0;
   Prof prof;
   std::vector<LevelTopo> topo;    // per-level owner topology (tree-only, cached)
+  // the finished tree on the device for the owner-list kernels (devtree.cu): Morton code, leaf flag
+  // and exclusive leaf count per box (level-major ids), and the level prefix on the host
+  DBuf tcode, tleaf, tleafrank;
+  std::vector<int> level_first;
+  std::atomic<int> topo_launches{0};
   // pinned landing buffer for ranks / pivots: per thread, grow-only, never freed (pinned
   // allocations and frees per handle stalled the host for hundreds of ms)
   int* d2h(size_t n) {
@@ -871,10 +877,11 @@ void gj_blocked(fmmlu_handle* h, const std::vector<std::pair<cplx*, int>>& mats,
   if (mats.empty()) return;
   int nmax = 1;
   for (auto& m : mats) nmax = std::max(nmax, m.second);
-  // Large batches (cfg5: ≥ 290 boxes per phase at levels 5-7) run faster on the blocked path — one CTA
-  // per matrix per panel and DMMA updates keep every SM busy (inv class 157 → 70 ms) — while a few
-  // matrices finish sooner resident in a cluster's registers (cfg2 / cfg3: 10.7 vs 18.5, 27 vs 41 ms).
-  static const int gj_batch = getenv("FMMLU_GJ_BATCH") ? atoi(getenv("FMMLU_GJ_BATCH")) : 200;
+  // Batches of ≥ 50 matrices (cfg5 levels 4-7) run faster on the blocked path — one CTA per matrix
+  // per panel and DMMA updates keep every SM busy (inv class 157 → 68 ms; 92 ms with the switch at
+  // 100 or 200) — while a few matrices finish sooner resident in a cluster's registers (blocked
+  // always: cfg2 10.7 → 18.5 ms, cfg3 27 → 41 ms; with the switch at 50 cfg2 stays at 10.8 ms).
+  static const int gj_batch = getenv("FMMLU_GJ_BATCH") ? atoi(getenv("FMMLU_GJ_BATCH")) : 50;
   const bool big_batch = h->gj_mode == 0 && (int)mats.size() >= gj_batch && nmax >= 48;
   if (h->gj_mode == 0 && !big_batch && gj_dsm_cluster_size(nmax) > 0) {
     // whole matrices resident in (cluster) shared memory: one launch for the batch
@@ -1248,7 +1255,9 @@ class HostPool {
   unsigned long long gen_ = 0;
 };
 
-void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
+// Host construction of the same lists from the host tree: the FMMLU_TOPO_CHECK=1 self-check of the
+// device path only (never a fallback).
+void build_topo_host(const Tree& T, int lvl, LevelTopo& tp) {
   tp.owners.clear();
   for (int b : T.levels[lvl]) tp.owners.push_back(b);
   const int nlb = (int)tp.owners.size();
@@ -1345,6 +1354,48 @@ void build_topo(const Tree& T, int lvl, LevelTopo& tp) {
       std::sort(v.begin(), v.end());
     }
   });
+}
+
+// Owner lists of one level, built on the device (devtree.cu: device_topology) from the device copy of
+// the tree — owners, N (sep ≤ 1) and Q (sep 2) lists of every level box, and the block-pair set — and
+// unpacked into the host containers the descriptor builders read.  Runs on its own stream (worker
+// threads build the levels concurrently while the first levels are factored).
+void build_topo(fmmlu_handle* h, int lvl, LevelTopo& tp) {
+  const Tree& T = h->tree;
+  FMMLU_CUDA(cudaSetDevice(h->dev));
+  cudaStream_t st = nullptr;
+  FMMLU_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevTopo D;
+  int nl = 0;
+  try {
+    device_topology(h->tcode.as<unsigned long long>(), h->tleaf.as<unsigned char>(), h->tleafrank.as<int>(),
+                    h->level_first.data(), T.nlevels, lvl, st, D, &nl);
+  } catch (...) {
+    cudaStreamDestroy(st);
+    throw;
+  }
+  FMMLU_CUDA(cudaStreamSynchronize(st));
+  FMMLU_CUDA(cudaStreamDestroy(st));
+  h->topo_launches += nl;
+  tp.owners = std::move(D.owners);
+  const int no = D.no, nlb = D.nlb;
+  tp.local.assign(T.boxes.size(), -1);
+  for (int i = 0; i < no; ++i) tp.local[tp.owners[i]] = i;
+  tp.boxN.assign(nlb, {});
+  tp.boxQ.assign(nlb, {});
+  for (int i = 0; i < nlb; ++i) {
+    tp.boxN[i].assign(D.nidx.begin() + D.nptr[i], D.nidx.begin() + D.nptr[i + 1]);
+    tp.boxQ[i].assign(D.qidx.begin() + D.qptr[i], D.qidx.begin() + D.qptr[i + 1]);
+  }
+  tp.nb.assign(no, {});
+  for (int a = 0; a < no; ++a) tp.nb[a].assign(D.nbidx.begin() + D.nbptr[a], D.nbidx.begin() + D.nbptr[a + 1]);
+  const bool check = getenv("FMMLU_TOPO_CHECK") != nullptr;
+  if (check) {  // self-check (tests): the same lists from the host tree
+    LevelTopo ref;
+    build_topo_host(T, lvl, ref);
+    if (ref.owners != tp.owners || ref.boxN != tp.boxN || ref.boxQ != tp.boxQ || ref.nb != tp.nb)
+      throw Error(FMMLU_ECUDA, "device owner lists differ from the host tree's at level " + std::to_string(lvl));
+  }
 }
 
 struct LevelBSR {
@@ -1505,9 +1556,9 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
         // tree path: the left-looking one-CTA-per-box kernel first (ranks stay far below b there);
         // the boxes it gives up on (k_out = −1) are taken by the register kernel behind it
         static const bool ll_env = !(getenv("FMMLU_PCHOL_LL") && atoi(getenv("FMMLU_PCHOL_LL")) == 0);
-        // (its gain is one box per SM instead of one per cluster: only for batches that fill the GPU;
-        // cfg2's ≤ 100-box phases were faster on the register kernel alone)
-        static const int ll_min = getenv("FMMLU_PCHOL_LL_MIN") ? atoi(getenv("FMMLU_PCHOL_LL_MIN")) : 128;
+        // (its gain is one box per SM instead of one per cluster: measured on cfg5 / cfg2 for minimum
+        // batches of 32 / 64 / 128 boxes: cpqr class 97 / 102 / 107 ms on cfg5, 8.7-8.9 ms on cfg2)
+        static const int ll_min = getenv("FMMLU_PCHOL_LL_MIN") ? atoi(getenv("FMMLU_PCHOL_LL_MIN")) : 32;
         const bool ll = ll_env && h->pchol_ll && nj >= ll_min &&
                         launch_pchol_ll(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
         DBuf xs;
@@ -1783,7 +1834,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   std::vector<std::future<void>> topo_fut(std::max(L, 1));
   for (int lvl = L - 1; lvl >= 2; --lvl)
     if (!h->topo_ready[lvl])
-      topo_fut[lvl] = std::async(std::launch::async, [&T, h, lvl] { build_topo(T, lvl, h->topo[lvl]); });
+      topo_fut[lvl] = std::async(std::launch::async, [h, lvl] { build_topo(h, lvl, h->topo[lvl]); });
   for (int lvl = L - 1; lvl >= 2; --lvl) {
     lap(7);
     double tl0 = now_ms();
@@ -4195,6 +4246,22 @@ int fmmlu_tree(const double* points, const double* normals, const double* weight
     FMMLU_CUDA(cudaStreamSynchronize(st));
     lap(4);
     h->tree.build_from_levels(dt.level_n, dt.code, dt.start, dt.end, dt.parent, hperm, lo, side, n, leaf_max);
+    {
+      // device copy of the finished tree for the owner-list kernels (build_topo)
+      const int nbx = (int)h->tree.boxes.size();
+      std::vector<unsigned char> leaf(nbx);
+      for (int b = 0; b < nbx; ++b) leaf[b] = h->tree.boxes[b].leaf() ? 1 : 0;
+      h->level_first.assign(h->tree.nlevels + 1, 0);
+      for (int l = 0; l < h->tree.nlevels; ++l) h->level_first[l + 1] = h->level_first[l] + dt.level_n[l];
+      h->tcode.alloc((size_t)nbx * sizeof(unsigned long long), st);
+      h->tleaf.alloc((size_t)nbx, st);
+      h->tleafrank.alloc((size_t)(nbx + 1) * sizeof(int), st);
+      FMMLU_CUDA(cudaMemcpyAsync(h->tcode.p, dt.code.data(), (size_t)nbx * sizeof(unsigned long long),
+                                 cudaMemcpyHostToDevice, st));
+      FMMLU_CUDA(cudaMemcpyAsync(h->tleaf.p, leaf.data(), (size_t)nbx, cudaMemcpyHostToDevice, st));
+      device_leafrank(h->tleaf.as<unsigned char>(), nbx, h->tleafrank.as<int>(), st);
+      FMMLU_CUDA(cudaStreamSynchronize(st));
+    }
     lap(5);
     // k_tree_scan/keys/gather + CUB onesweep radix sort (histogram + 8 passes) + device octree
     h->tree_launches = 3 + 9 + dt_launches;
@@ -4445,6 +4512,9 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->root_dinv.release();
   h->root_flags.release();
   h->sep_perm.release();
+  h->tcode.release();
+  h->tleaf.release();
+  h->tleafrank.release();
   for (auto& w : h->ws_slot) w.release();
   h->geo.release();
   h->perm.release();
@@ -4480,7 +4550,7 @@ int fmmlu_stats(const fmmlu_handle* h, fmmlu_stats_t* out) {
   if (!h || !out) return fail(FMMLU_EINVAL, "NULL argument");
   *out = h->stats;
   out->peak_bytes = (int64_t)h->peak_bytes;
-  out->n_launches = h->prof.total_launches + h->tree_launches;
+  out->n_launches = h->prof.total_launches + h->tree_launches + h->topo_launches.load();
   for (int i = 0; i < 16; ++i) {
     out->class_ms[i] = h->prof.ms[i];
     out->class_flops[i] = h->prof.flops[i];
@@ -4546,6 +4616,45 @@ int fmmlu_tree_boxes(const fmmlu_handle* h, int32_t* nboxes, int32_t* level, int
   }
   *nboxes = nb;
   return FMMLU_OK;
+}
+
+int fmmlu_level_lists(fmmlu_handle* h, int level, int32_t* counts, int32_t* owners, int32_t* nptr, int32_t* nidx,
+                      int32_t* qptr, int32_t* qidx) {
+  if (!h || !counts) return fail(FMMLU_EINVAL, "NULL argument");
+  if (level < 2 || level >= h->tree.nlevels) return fail(FMMLU_EINVAL, "level out of range");
+  return guarded([&] {
+    FMMLU_CUDA(cudaSetDevice(h->dev));
+    const int L = h->tree.nlevels;
+    if ((int)h->topo.size() < L) h->topo.resize(L);
+    if (h->topo_ready.size() < (size_t)L) h->topo_ready.resize(L, 0);
+    if (!h->topo_ready[level]) {
+      build_topo(h, level, h->topo[level]);
+      h->topo_ready[level] = 1;
+    }
+    const LevelTopo& tp = h->topo[level];
+    const int nlb = (int)tp.boxN.size(), no = (int)tp.owners.size();
+    long long tn = 0, tq = 0;
+    for (int i = 0; i < nlb; ++i) {
+      tn += (long long)tp.boxN[i].size();
+      tq += (long long)tp.boxQ[i].size();
+    }
+    counts[0] = nlb;
+    counts[1] = no;
+    counts[2] = (int32_t)tn;
+    counts[3] = (int32_t)tq;
+    if (!owners) return;
+    if (!nptr || !nidx || !qptr || !qidx) throw Error(FMMLU_EINVAL, "NULL list array");
+    std::copy(tp.owners.begin(), tp.owners.end(), owners);
+    int a = 0, b = 0;
+    for (int i = 0; i < nlb; ++i) {
+      nptr[i] = a;
+      qptr[i] = b;
+      for (int o : tp.boxN[i]) nidx[a++] = o;
+      for (int o : tp.boxQ[i]) qidx[b++] = o;
+    }
+    nptr[nlb] = a;
+    qptr[nlb] = b;
+  });
 }
 
 int fmmlu_tree_perm(const fmmlu_handle* h, int64_t* perm) {

@@ -52,7 +52,8 @@ KERNEL_CLASSES = ["build", "gather", "qr", "cpqr", "ef", "inv", "panel", "schur"
 
 EXPORTS = ("fmmlu_tree", "fmmlu_factor", "fmmlu_solve", "fmmlu_apply", "fmmlu_monostatic_rcs", "fmmlu_matvec", "fmmlu_destroy",
            "fmmlu_last_error", "fmmlu_stats", "fmmlu_set_stream", "fmmlu_tree_perm", "fmmlu_probe_fp64",
-           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes", "fmmlu_release_cache", "fmmlu_tree_boxes")
+           "fmmlu_set_param", "fmmlu_inverse_batch", "fmmlu_boxes", "fmmlu_release_cache", "fmmlu_tree_boxes",
+           "fmmlu_level_lists")
 
 
 def lib_path() -> str:
@@ -89,6 +90,7 @@ def load(build_if_missing: bool = False):
     L.fmmlu_boxes.argtypes = [vp, vp, vp, vp, ci, ci, ci, cd, cd, cd, ci, cd, vp, vp, ci, vp, vp, vp]
     L.fmmlu_release_cache.argtypes = []
     L.fmmlu_tree_boxes.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.fmmlu_level_lists.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp]
     for f in EXPORTS:
         getattr(L, f).restype = ctypes.c_char_p if f == "fmmlu_last_error" else ctypes.c_int
     _LIB = L
@@ -212,6 +214,22 @@ class FmmLu:
         _check(L.fmmlu_tree_boxes(self.h, ctypes.byref(nb), lev.ctypes.data, crd.ctypes.data, st.ctypes.data,
                                   en.ctypes.data))
         return dict(level=lev, coord=crd, start=st, end=en)
+
+    def level_lists(self, level: int) -> dict:
+        """The device-built owner lists of one level: owners (box ids as in tree_boxes), and per level
+        box the N / Q owners as CSR (nptr, nidx, qptr, qidx) of local owner indices."""
+        L = load()
+        cnt = np.zeros(4, dtype=np.int32)
+        _check(L.fmmlu_level_lists(self.h, int(level), cnt.ctypes.data, None, None, None, None, None))
+        nlb, no, tn, tq = (int(v) for v in cnt)
+        owners = np.empty(max(no, 1), dtype=np.int32)
+        nptr = np.empty(nlb + 1, dtype=np.int32)
+        qptr = np.empty(nlb + 1, dtype=np.int32)
+        nidx = np.empty(max(tn, 1), dtype=np.int32)
+        qidx = np.empty(max(tq, 1), dtype=np.int32)
+        _check(L.fmmlu_level_lists(self.h, int(level), cnt.ctypes.data, owners.ctypes.data, nptr.ctypes.data,
+                                   nidx.ctypes.data, qptr.ctypes.data, qidx.ctypes.data))
+        return dict(nlb=nlb, owners=owners[:no], nptr=nptr, nidx=nidx[:tn], qptr=qptr, qidx=qidx[:tq])
 
     def tree_perm(self) -> np.ndarray:
         p = np.empty(self.n, dtype=np.int64)
