@@ -1461,10 +1461,18 @@ void gram_gemm(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<
   static const int g_cps = getenv("FMMLU_GRAM_CPS") ? atoi(getenv("FMMLU_GRAM_CPS")) : 8;
   static const int g_minch = getenv("FMMLU_GRAM_MINCH") ? atoi(getenv("FMMLU_GRAM_MINCH")) : 128;
   const long long want = std::max<long long>(1, ((long long)g_cps * 148 + utiles - 1) / std::max<long long>(utiles, 1));
+  // A ragged last block column of ≤ 32 columns (b mod 64 in 1..32) is computed with 64×32 tiles, as a
+  // second, rectangular problem G[:, 64·nf ..) = Mᴴ M[:, 64·nf ..), instead of 64×64 tiles that would
+  // be more than half padding (b = 200: 10 + 4·½ = 12 tile units instead of 14)
+  std::vector<GemmProblem> gp32;
+  std::vector<GemmGroup> gt32;
+  static const bool split32 = !(getenv("FMMLU_GRAM_SPLIT32") && atoi(getenv("FMMLU_GRAM_SPLIT32")) == 0);
   for (int j = j0; j < j1; ++j) {
+    const int b = bcol[j], nf = b / kTile, rem = b % kTile;
+    const bool split = split32 && nf >= 1 && rem >= 1 && rem <= 32;
     GemmProblem P{};
-    P.m = bcol[j];
-    P.n = bcol[j];
+    P.m = split ? nf * kTile : b;
+    P.n = P.m;
     P.k = mrows[j];
     P.opA = kOpC;
     P.opB = kOpN;
@@ -1478,7 +1486,17 @@ void gram_gemm(fmmlu_handle* h, const std::vector<cplx*>& mp, const std::vector<
     ch = std::max<long long>(g_minch, (ch + 15) / 16 * 16);
     P.kchunk = (mrows[j] > ch && !is_deterministic(h)) ? (int)ch : 0;  // split-K adds with atomics
     add_gemm(gp, gt, P, true);  // G is Hermitian: upper tiles only, then mirrored
+    if (split) {
+      GemmProblem Q = P;
+      Q.m = b;
+      Q.n = rem;
+      Q.B = mp[j] + (size_t)(nf * kTile) * mrows[j];
+      Q.C = G + goff[j] + (size_t)(nf * kTile) * bcol[j];
+      add_gemm(gp32, gt32, Q);  // n ≤ 32 → 32-wide tiles
+    }
   }
+  // (algorithmic share of the rectangular part: ½·(b + 64·nf)/b of its 8·m·b·rem flops, 0.83 … 1)
+  if (!gt32.empty()) run_gemms(gp32, gt32, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.9);
   run_gemms(gp, gt, cmk(1.0, 0.0), 0, nullptr, st, keep, h->prof, FMMLU_K_QR, 0.5);
 }
 
