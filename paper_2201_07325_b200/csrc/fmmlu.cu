@@ -1195,9 +1195,11 @@ void tsqr_cluster(fmmlu_handle* h, std::vector<cplx*>& mp, std::vector<int>& mro
 // run by the workers and the caller; small counts run inline.
 class HostPool {
  public:
-  static HostPool& get() {
-    static HostPool* p = new HostPool();  // never destroyed (workers live until process exit)
-    return *p;
+  // Two pools: 0 for the thread that runs the factorization, 1 for its ID-preparation worker, so
+  // that the two do not serialise each other's loops (one parallel region at a time per pool).
+  static HostPool& get(int which = 0) {
+    static HostPool* p[2] = {new HostPool(), new HostPool()};  // never destroyed (workers live until process exit)
+    return *p[which ? 1 : 0];
   }
   template <class F>
   void parallel_for(int count, int min_par, F&& fn) {
@@ -2180,7 +2182,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         std::vector<int>& maps = P.maps;
         std::vector<ProxyTask>& pts = P.pts;
         std::vector<int>& gidx = P.gidx;
-        HostPool::get().parallel_for(nj, 8, [&](int j0, int j1) {
+        HostPool::get(1).parallel_for(nj, 8, [&](int j0, int j1) {
           for (int j = j0; j < j1; ++j) {
             BoxJob& J = jobs[j];
             int ci = at[j].cps;
