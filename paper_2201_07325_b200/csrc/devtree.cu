@@ -582,7 +582,15 @@ void device_topology(const unsigned long long* d_code, const unsigned char* d_le
   DT_CHECK(cudaMemcpyAsync(&tot[1], qptr.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, st));
   DT_CHECK(cudaMemcpyAsync(&tot[2], poff.p + nlb, sizeof(int), cudaMemcpyDeviceToHost, st));
   DT_CHECK(cudaStreamSynchronize(st));
-  if (tot[2] < 0) throw Error(-8, "device topology: more than 2^31 candidate block pairs at one level");
+  if ((long long)nlb * 15873 > INT_MAX) {  // (1 + 124)² + 2·124 candidates per box at most: check the 32-bit scan
+    std::vector<int> hn(nlb), hq(nlb);
+    DT_CHECK(cudaMemcpyAsync(hn.data(), nN.p, nlb * sizeof(int), cudaMemcpyDeviceToHost, st));
+    DT_CHECK(cudaMemcpyAsync(hq.data(), nQ.p, nlb * sizeof(int), cudaMemcpyDeviceToHost, st));
+    DT_CHECK(cudaStreamSynchronize(st));
+    long long sum = 0;
+    for (int i = 0; i < nlb; ++i) sum += (long long)(1 + hn[i]) * (1 + hn[i]) + 2LL * hq[i];
+    if (sum > INT_MAX) throw Error(-8, "device topology: more than 2^31 candidate block pairs at one level");
+  }
   nidx.resize(tot[0], st);
   qidx.resize(tot[1], st);
   k_topo_compact<<<std::max(nlb, 1), 64, 0, st>>>(cand.p, nN.p, nQ.p, nptr.p, qptr.p, nlb, nidx.p, qidx.p);

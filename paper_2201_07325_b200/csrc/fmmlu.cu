@@ -1544,7 +1544,12 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     }
     // the register pivoted Cholesky reads the lower triangle from the upper one itself
     const bool reg_pchol = h->id_mode != 3 && h->pchol_mode == 0 && pchol_reg_scratch(bmax) > 0;
-    if (!reg_pchol) {
+    // ... and the left-looking kernel copies whole columns of G with the TMA engine: both triangles
+    static const bool ll_env = !(getenv("FMMLU_PCHOL_LL") && atoi(getenv("FMMLU_PCHOL_LL")) == 0);
+    static const int ll_min = getenv("FMMLU_PCHOL_LL_MIN") ? atoi(getenv("FMMLU_PCHOL_LL_MIN")) : 32;
+    const bool want_ll = h->id_mode != 3 && ((sep_pairs && bmax <= 1024) ||
+                                             (reg_pchol && ll_env && h->pchol_ll && nj >= ll_min && bmax <= 512));
+    if (!reg_pchol || want_ll) {
       std::vector<cplx*> gptr(nj);
       for (int j = 0; j < nj; ++j) gptr[j] = G.as<cplx>() + goff[j];
       Stage sm;
@@ -1564,7 +1569,7 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
     size_t o_i = s2.add(ids), o_q = s2.add(cq);
     s2.upload(st);
     int cid = h->prof.begin(FMMLU_K_CPQR, st);
-    if (sep_pairs && h->id_mode != 3) {
+    if (sep_pairs && want_ll) {
       // deeper stop, bounded by the Gram path's noise floor (R4: squared norms carry ≈ b·u·‖M‖²)
       const double eps_stop = std::min(eps, std::max(eps / 30.0, std::sqrt(4.0 * bmax * 1.1102230246251565e-16)));
       done_id = launch_pchol_ll(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps_stop, st, bmax, eps, keps.as<int>(),
@@ -1575,12 +1580,9 @@ void id_stage(fmmlu_handle* h, std::vector<cplx*> mp, std::vector<int> mrows, co
       if (reg_pchol) {  // register-resident pivoted Cholesky
         // tree path: the left-looking one-CTA-per-box kernel first (ranks stay far below b there);
         // the boxes it gives up on (k_out = −1) are taken by the register kernel behind it
-        static const bool ll_env = !(getenv("FMMLU_PCHOL_LL") && atoi(getenv("FMMLU_PCHOL_LL")) == 0);
         // (its gain is one box per SM instead of one per cluster: measured on cfg5 / cfg2 for minimum
         // batches of 32 / 64 / 128 boxes: cpqr class 97 / 102 / 107 ms on cfg5, 8.7-8.9 ms on cfg2)
-        static const int ll_min = getenv("FMMLU_PCHOL_LL_MIN") ? atoi(getenv("FMMLU_PCHOL_LL_MIN")) : 32;
-        const bool ll = ll_env && h->pchol_ll && nj >= ll_min &&
-                        launch_pchol_ll(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
+        const bool ll = want_ll && launch_pchol_ll(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, st, bmax);
         DBuf xs;
         xs.alloc((size_t)nj * pchol_reg_scratch(bmax) * sizeof(cplx), st);
         done_id = launch_pchol_reg(s2.ptr<ClusterQrTask>(o_q), nj, permd, kd, eps, xs.as<cplx>(), st, bmax, ll ? 1 : 0);

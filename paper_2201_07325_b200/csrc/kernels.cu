@@ -13,6 +13,37 @@ namespace fmmlu {
 
 namespace {
 
+// ------------------------------------------------------------------ bulk async copies (TMA engine)
+// cp.async.bulk global → shared (1-D: contiguous panels / columns of complex128, 16-byte units)
+// completing on an mbarrier.  One thread arms the barrier with the byte count and issues the copies;
+// every thread waits on the phase parity.  The wait traps instead of hanging if a copy never lands.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  long long spins = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!done && ++spins > (1ll << 26)) __trap();
+  }
+}
+
 // ------------------------------------------------------------------ reductions
 __device__ __forceinline__ void argmax_merge(double& v, int& i, double v2, int i2) {
   if (v2 > v || (v2 == v && i2 < i)) {
@@ -387,11 +418,18 @@ __global__ void __launch_bounds__(GJP_NT) k_gj_panel(const GjTask* __restrict__ 
   cplx* P = reinterpret_cast<cplx*>(shm);  // n × jb (ld n)
   cplx* colf = P + (size_t)n * jb;         // n: multipliers of the current step
   const int tid = threadIdx.x;
-  for (int e = tid; e < n * jb; e += GJP_NT) {
-    const int i = e % n, c = e / n;
-    P[e] = t.A[i + (size_t)(j0 + c) * t.lda];
-  }
+  // the panel's columns are contiguous runs of n complex numbers: staged by the TMA engine
+  // (cp.async.bulk, one copy per column issued by the lanes of warp 0, one mbarrier phase)
+  __shared__ unsigned long long pbar;
+  if (tid == 0) mbar_init(&pbar, 1);
   __syncthreads();
+  if (tid < 32) {
+    if (tid == 0) mbar_expect_tx(&pbar, (unsigned)((size_t)n * jb * sizeof(cplx)));
+    __syncwarp();
+    for (int c = tid; c < jb; c += 32)
+      bulk_g2s(P + (size_t)c * n, t.A + (size_t)(j0 + c) * t.lda, (unsigned)(n * sizeof(cplx)), &pbar);
+  }
+  mbar_wait(&pbar, 0);
   __shared__ cplx sdinv;
   for (int s = 0; s < jb; ++s) {
     const int j = j0 + s;
@@ -1516,8 +1554,8 @@ __global__ void __launch_bounds__(GJR_NT, 1) k_pchol_reg(const ClusterQrTask* __
 // on cfg5): ONE CTA per box and no cluster, so every SM works on its own box(es).  Only the
 // computed rows of R are kept — the first `kcap` in shared memory, later ones in the task's global
 // scratch `out` (row-major, L2-resident) — and the Schur complement is never formed: step j takes
-// the argmax p of the running diagonal d (every warp computes it; ties → lowest column), loads
-// column p of G (upper triangle, conjugated below it), forms S_ip = G_ip − Σ_{l<j} conj(R_li) R_lp
+// the argmax p of the running diagonal d (every warp computes it; ties → lowest column), has the
+// TMA engine stage column p of G (cp.async.bulk; both triangles stored), forms S_ip = G_ip − Σ_{l<j} conj(R_li) R_lp
 // with the rows split over NG thread groups, and writes R_ji = conj(S_ip)/√S_pp, d_i −= |S_ip|²/S_pp.
 // O(b·k²) work instead of O(b²·k), two CTA barriers per step.  Stop rule C9 on the diagonal
 // (≤ ε²·initial max).  A box that reaches `kabort` pivots gives up (k_out = −1, G untouched) and
@@ -1537,7 +1575,8 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
   if (bpad > NT || b > bmax) __trap();  // launch configuration mismatch
   cplx* Rs = reinterpret_cast<cplx*>(llsm);                 // [kcap][b]
   cplx* part = Rs + (size_t)kcap * bmax;                    // [NT] partial sums of the thread groups
-  double* d = reinterpret_cast<double*>(part + NT);         // [bmax] running diagonal
+  cplx* colbuf = part + NT;                                 // [bmax] column p of G (bulk copy target)
+  double* d = reinterpret_cast<double*>(colbuf + bmax);     // [bmax] running diagonal
   int* done = reinterpret_cast<int*>(d + bmax);             // [bmax] column already pivoted
   int* piv = done + bmax;                                   // [bmax] pivots in order
   int* posmap = piv + bmax;                                 // [bmax]
@@ -1548,6 +1587,8 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
   const bool col = grp < NG && i < b;
   const int kabort = kabort_min < 0 ? b + 1 : min(b, max(kabort_min, b / 2));
   int keps = -1;
+  __shared__ unsigned long long cbar;  // completion of the column copies (phase parity = step parity)
+  if (tid == 0) mbar_init(&cbar, 1);
   for (int c = tid; c < b; c += NT) {
     d[c] = t.A[c + (size_t)c * t.lda].x;
     done[c] = 0;
@@ -1575,8 +1616,12 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
       aborted = true;
       break;
     }
-    cplx gip = cmk(0.0, 0.0);
-    if (grp == 0 && i < b) gip = i <= p ? t.A[i + (size_t)p * t.lda] : cconj(t.A[p + (size_t)i * t.lda]);
+    // column p of G (both triangles are stored: k_herm_mirror ran before) is one contiguous run of
+    // b complex numbers: staged by the TMA engine while the inner products below run
+    if (tid == 0) {
+      mbar_expect_tx(&cbar, (unsigned)(b * sizeof(cplx)));
+      bulk_g2s(colbuf, t.A + (size_t)p * t.lda, (unsigned)(b * sizeof(cplx)), &cbar);
+    }
     cplx s = cmk(0.0, 0.0);
     if (col) {
       // Σ_l conj(R_li) · R_lp: shared-memory rows, then the rows spilled to global memory; two
@@ -1605,6 +1650,8 @@ __global__ void __launch_bounds__(NT) k_pchol_ll(const ClusterQrTask* __restrict
       s = cmk(s0x + s1x, s0y + s1y);
     }
     if (NG > 1) part[tid] = s;
+    mbar_wait(&cbar, (unsigned)(j & 1));
+    const cplx gip = (grp == 0 && i < b) ? colbuf[i] : cmk(0.0, 0.0);
     __syncthreads();  // every warp has its argmax (d / done may change now); partial sums visible
     if (grp == 0 && i < b && !done[i]) {
       for (int g2 = 1; g2 < NG; ++g2) {
@@ -2704,7 +2751,7 @@ bool launch_pchol_ll(const ClusterQrTask* d_tasks, int ntasks, int* perm_out, in
   if (bmax > (no_abort ? 1024 : 512)) return false;
   if (eps_rank <= 0.0) eps_rank = eps;
   const int NT = bmax <= 128 ? 256 : bmax <= 512 ? 512 : 1024;
-  const size_t fixed = (size_t)NT * sizeof(cplx) + (size_t)bmax * (sizeof(double) + 3 * sizeof(int)) + 64;
+  const size_t fixed = (size_t)(NT + bmax) * sizeof(cplx) + (size_t)bmax * (sizeof(double) + 3 * sizeof(int)) + 64;
   const size_t row = (size_t)bmax * sizeof(cplx);
   int kcap = std::min(bmax, 64);
   if (fixed + kcap * row > 110 * 1024) kcap = std::min<int>(bmax, (int)((220 * 1024 - fixed) / row));
