@@ -2,11 +2,12 @@
 "Different interpolation matrices can be used for each of A_BFᵀ and A_FB ... smaller skeleton
 sets"; L1098-1108, L1909-1914; DESIGN reading R12): libfmmlu with
 ``set_param("separate_id", 1)`` against the oracle's ``rss.factor(..., separate=True)`` on the
-same seeded inputs.  Skeleton sets may differ at near-ties (and the GPU equalises the two ranks
-by promoting redundant columns where the oracle continues its greedy CPQR, R12), so agreement is
-judged on the solution (≤ 10ε), the residual against the brute-force matvec (≤ 10ε), the
+same seeded inputs.  Skeleton sets may differ at near-ties (both sides continue the lower-rank
+side's greedy order to k = max(k_r, k_c); the GPU pivots on the Gram matrix, R4/R12), so agreement
+is judged on the solution (≤ 10ε), the residual against the brute-force matvec (≤ 10ε), the
 forward product, the solve∘apply round trip, and the structure both share: square pivot blocks,
-a root no larger than the simultaneous ID's."""
+a root smaller than the simultaneous ID's.  cfg2 at full size is compared with a stored oracle
+solution (tests/golden/cfg2_oracle_separate_solution.*)."""
 import math
 
 import numpy as np
@@ -144,3 +145,28 @@ def test_separate_householder_and_gram_paths_agree(F):
         xs.append(x)
     assert dense.rel_diff(xs[0], xs[1]) <= 10 * eps
     assert dense.residual(g.points, g.normals, g.weights, k, xs[0], b) <= 10 * eps
+
+
+def test_separate_cfg2_fullsize(F):
+    """BASELINE configs[1] (n = 20,000, 4 RHS) with separate IDs against the oracle's dense-mode
+    separate factorization (tests/golden/cfg2_oracle_separate_solution.npz, written by
+    `tools/make_golden.py cfg2 --separate`, which calls only oracle/): solution within 10ε, root
+    size within 5 %, and smaller than the simultaneous ID's root."""
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(__file__), "golden", "cfg2_oracle_separate_solution")
+    if not os.path.exists(gold + ".npz"):
+        pytest.skip("golden file not generated")
+    meta = json.load(open(gold + ".json"))
+    xo = np.load(gold + ".npz")["x_full"]
+    c = fi.CONFIGS["cfg2"]
+    g = fi.config_geometry("cfg2")
+    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    h = _factor(F, g, c["k"], c["eps"], c["leaf_max"])
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    assert dense.rel_diff(x, xo) <= 10 * c["eps"]
+    n0 = h.stats()["n0"]
+    assert abs(n0 - meta["n0"]) <= 0.05 * meta["n0"] + 2
+    h0 = _factor(F, g, c["k"], c["eps"], c["leaf_max"], sep=0)
+    assert n0 < h0.stats()["n0"]

@@ -2,6 +2,7 @@
 fmmlu_inputs/; nothing from the CUDA path).
 
     python tools/make_golden.py cfg1|cfg2|cfg3
+    python tools/make_golden.py cfg2 --separate      (separate incoming/outgoing IDs, dense mode)
 
 * cfg1, cfg2: dense mode AND block mode ("both must give identical S/T on
   cfg1–2"); the script asserts identical skeleton sets for every box and solutions within
@@ -27,6 +28,29 @@ import fmmlu_inputs as fi  # noqa: E402
 from oracle import dense, rss  # noqa: E402
 
 GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def run_separate(name):
+    """Separate incoming/outgoing IDs (DESIGN R12): the oracle's dense-mode
+    separate factorization (the only mode that has it), all RHS columns stored."""
+    c = fi.CONFIGS[name]
+    g = fi.config_geometry(name)
+    b = fi.gaussian_rhs(g.n, c["nrhs"], 0)
+    t0 = time.time()
+    f = rss.factor(g.points, g.normals, g.weights, c["k"], c["eps"], c["leaf_max"], mode="dense", separate=True)
+    t1 = time.time()
+    x = rss.solve(f, b)
+    rc = np.array(f.stats["ranks_rc"])
+    meta = dict(config=name, separate=True, n=g.n, k=c["k"], eps=c["eps"], leaf_max=c["leaf_max"], nrhs=c["nrhs"],
+                rhs="fmmlu_inputs.gaussian_rhs(n, nrhs, 0)", cores=os.cpu_count(), dense_factor_s=t1 - t0,
+                n0=int(f.stats["n0"]), boxes_with_different_ranks=int((rc[:, 0] != rc[:, 1]).sum()), boxes=int(rc.shape[0]),
+                skeleton_sum=int(sum(v.size for v in f.stats["skeletons"].values())),
+                stored="x_full = all columns")
+    np.savez_compressed(os.path.join(GOLD, f"{name}_oracle_separate_solution.npz"), x_full=np.ascontiguousarray(x),
+                        colnorm=np.linalg.norm(x, axis=0))
+    with open(os.path.join(GOLD, f"{name}_oracle_separate_solution.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(json.dumps(meta), flush=True)
 
 
 def run(name):
@@ -74,5 +98,6 @@ def run(name):
 
 
 if __name__ == "__main__":
-    for nm in sys.argv[1:]:
-        run(nm)
+    sep = "--separate" in sys.argv
+    for nm in [a for a in sys.argv[1:] if not a.startswith("--")]:
+        (run_separate if sep else run)(nm)
