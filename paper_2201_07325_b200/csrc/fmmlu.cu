@@ -2904,6 +2904,9 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
         if (ftab.empty()) ftab.push_back(-1);
         if (fbld.empty()) fbld.push_back(0);
         };
+        // on its own host thread (with the worker pool, idle from here on) while this thread uploads
+        // the descriptors and launches the gathers, E/F, X_RR⁻¹ and Up; joined before the Schur launch
+        std::future<void> frames_fut = std::async(std::launch::async, fill_frames);
         if (maps.empty()) maps.push_back(0);
         lap(18);
         Stage s;
@@ -3003,7 +3006,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
           add_gemm(gp, gt, P);
         }
         run_gemms(gp, gt, p1, 0, nullptr, st, keep, h->prof, FMMLU_K_PANEL);
-        fill_frames();
+        frames_fut.get();
         Stage s2;
         s2.reserve_pinned(16 * 6 + sizeof(int) * (fslot.size() + fpos.size() + fbld.size()) +
                           sizeof(long long) * ftab.size());
