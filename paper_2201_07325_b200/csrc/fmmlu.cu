@@ -1043,7 +1043,10 @@ void pchol_big(fmmlu_handle* h, cplx* G, const std::vector<long long>& goff, lon
     is += 2LL * b;
   }
   DBuf cb, db, ib, sb;
-  cb.alloc((size_t)cs * sizeof(cplx), st);
+  // at least a big block: it then comes from the quantised block cache and is reused by the next
+  // factorization (as a ≈ 26 MB pool allocation of a slightly different size every time it made the
+  // pool grow: one 46 ms cudaMallocAsync per cfg5 factorization, FMMLU_TRACE allocator line)
+  cb.alloc(std::max<size_t>((size_t)cs * sizeof(cplx), kBigBlock), st);
   db.alloc((size_t)ds * sizeof(double), st);
   ib.alloc((size_t)is * sizeof(int), st);
   sb.alloc((size_t)nbx * sizeof(PcholState), st);
@@ -3158,6 +3161,16 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     }
     prev = std::move(cur);
     S.t_levels_ms[lvl] = now_ms() - tl0;  // host-side span of the level (GPU work may still drain)
+    if (trace) {  // host-time sections of this level (same order as the summary line at the end)
+      static double trp[24];
+      if (lvl == L - 1) std::memset(trp, 0, sizeof(trp));
+      fprintf(stderr, "[fmmlu] L%d host ms by section:", lvl);
+      for (int i = 0; i < 23; ++i) {
+        if (tr[i] - trp[i] > 0.05) fprintf(stderr, " s%d %.1f", i, tr[i] - trp[i]);
+        trp[i] = tr[i];
+      }
+      fprintf(stderr, " | span %.1f\n", S.t_levels_ms[lvl]);
+    }
   }
 
   lap(6);
