@@ -1917,70 +1917,91 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       std::vector<long long> poffv;
       std::vector<int2> tasks;
       for (int a = 0; a < no; ++a) actoff[a + 1] = actoff[a] + (int)cur.act[a].size();
-      gidx.reserve(actoff[no]);
-      slot.reserve(actoff[no]);
-      pos.reserve(actoff[no]);
-      {
-        size_t np_ = 0, nt_ = 0;
-        for (int a = 0; a < no; ++a) {
-          np_ += nb[a].size();
-          const int ra = (int)cur.act[a].size();
-          for (int b : nb[a]) nt_ += (size_t)((ra + 63) / 64) * (((int)cur.act[b].size() + 63) / 64);
-        }
-        nbidx.reserve(np_);
-        poffv.reserve(np_);
-        pair_a.reserve(np_);
-        tasks.reserve(nt_);
+      // Two passes over the owners on the host worker pool (31k owners, 2M actives, 850k block pairs
+      // and 1.2M tiles on cfg5's level 7).  Pass A: per active its previous-level owner's slot and
+      // position (slots numbered in order of first appearance within the owner), per owner its
+      // slot list and its pair / tile counts.  Serial prefix sums.  Pass B: the pair and tile arrays.
+      const int nact = actoff[no];
+      gidx.resize(nact);
+      slot.resize(nact);
+      pos.resize(nact);
+      if (sep) {
+        gidxc.resize(nact);
+        slotc.resize(nact);
+        posc.resize(nact);
       }
+      std::vector<int> slcnt(no, 0), sltmp((size_t)no * 8, -1);
+      std::vector<long long> tileoff(no + 1, 0);
+      std::atomic<int> bad{0};
+      const bool has_prev = prev.level >= 0;
+      HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {
+        for (int a = a0; a < a1; ++a) {
+          int* sl = &sltmp[(size_t)a * 8];
+          int ns = 0;
+          const int o0 = actoff[a];
+          auto slot_of = [&](int po, bool may_add) {
+            for (int q = 0; q < ns; ++q)
+              if (sl[q] == po) return q;
+            if (!may_add || ns >= 8) {
+              bad = 1;
+              return -1;
+            }
+            sl[ns] = po;
+            return ns++;
+          };
+          const std::vector<int>& ar = cur.act[a];
+          for (size_t i = 0; i < ar.size(); ++i) {
+            const int g = ar[i];
+            const int po = has_prev ? prevOwner[g] : -1;
+            gidx[o0 + i] = g;
+            slot[o0 + i] = po >= 0 ? slot_of(po, true) : -1;
+            pos[o0 + i] = po >= 0 ? prevPos[g] : 0;
+          }
+          if (sep) {  // the same previous-level owners hold a's columns (equal counts)
+            const std::vector<int>& ac = cur.actc[a];
+            for (size_t i = 0; i < ac.size(); ++i) {
+              const int g = ac[i];
+              const int po = has_prev ? prevOwner[g] : -1;
+              gidxc[o0 + i] = g;
+              slotc[o0 + i] = po >= 0 ? slot_of(po, false) : -1;
+              posc[o0 + i] = po >= 0 ? prevPosc[g] : 0;
+            }
+          }
+          slcnt[a] = ns;
+          const int ra = (int)ar.size();
+          long long nt = 0;
+          for (int b : nb[a]) nt += (long long)((ra + 63) / 64) * (((int)cur.act[b].size() + 63) / 64);
+          tileoff[a + 1] = nt;
+        }
+      });
+      if (bad) throw Error(FMMLU_ECUDA, "level build: an owner made of more than 8 previous-level owners, or a column owner without rows");
       for (int a = 0; a < no; ++a) {
-        const int s0 = (int)sllist.size();
-        for (int g : cur.act[a]) {
-          gidx.push_back(g);
-          const int po = prev.level >= 0 ? prevOwner[g] : -1;
-          int sidx = -1;
-          if (po >= 0) {
-            for (int q = s0; q < (int)sllist.size(); ++q)
-              if (sllist[q] == po) {
-                sidx = q - s0;
-                break;
-              }
-            if (sidx < 0) {
-              sllist.push_back(po);
-              sidx = (int)sllist.size() - 1 - s0;
-            }
-          }
-          slot.push_back(sidx);
-          pos.push_back(po >= 0 ? prevPos[g] : 0);
-        }
-        if (sep)
-          for (int g : cur.actc[a]) {  // the same previous-level owners hold a's columns (equal counts)
-            gidxc.push_back(g);
-            const int po = prev.level >= 0 ? prevOwner[g] : -1;
-            int sidx = -1;
-            if (po >= 0) {
-              for (int q = s0; q < (int)sllist.size(); ++q)
-                if (sllist[q] == po) {
-                  sidx = q - s0;
-                  break;
-                }
-              if (sidx < 0) throw Error(FMMLU_ECUDA, "separate IDs: column owner without rows");
-            }
-            slotc.push_back(sidx);
-            posc.push_back(po >= 0 ? prevPosc[g] : 0);
-          }
-        slptr[a + 1] = (int)sllist.size();
-        for (size_t i = 0; i < nb[a].size(); ++i) {
-          const int b = nb[a][i];
-          const int p = (int)nbidx.size();
-          nbidx.push_back(b);
-          poffv.push_back(cur.poff[a][i]);
-          pair_a.push_back(a);
-          const int ra = (int)cur.act[a].size(), cb = (int)cur.act[b].size();
-          const int nt = ((ra + 63) / 64) * ((cb + 63) / 64);
-          for (int q = 0; q < nt; ++q) tasks.push_back(make_int2(p, q));
-        }
-        nbptr[a + 1] = (int)nbidx.size();
+        slptr[a + 1] = slptr[a] + slcnt[a];
+        nbptr[a + 1] = nbptr[a] + (int)nb[a].size();
+        tileoff[a + 1] += tileoff[a];
       }
+      if (tileoff[no] > INT_MAX) throw Error(FMMLU_ENOTIMPL, "level build: more than 2^31 block tiles at one level");
+      sllist.resize(slptr[no]);
+      nbidx.resize(nbptr[no]);
+      poffv.resize(nbptr[no]);
+      pair_a.resize(nbptr[no]);
+      tasks.resize((size_t)tileoff[no]);
+      HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {
+        for (int a = a0; a < a1; ++a) {
+          for (int q = 0; q < slcnt[a]; ++q) sllist[slptr[a] + q] = sltmp[(size_t)a * 8 + q];
+          const int ra = (int)cur.act[a].size();
+          long long t = tileoff[a];
+          for (size_t i = 0; i < nb[a].size(); ++i) {
+            const int b = nb[a][i];
+            const int p = nbptr[a] + (int)i;
+            nbidx[p] = b;
+            poffv[p] = cur.poff[a][i];
+            pair_a[p] = a;
+            const int nt = ((ra + 63) / 64) * (((int)cur.act[b].size() + 63) / 64);
+            for (int q = 0; q < nt; ++q) tasks[(size_t)t++] = make_int2(p, q);
+          }
+        }
+      });
       for (std::vector<int>* v : {&gidx, &slot, &pos, &nbidx, &sllist, &pair_a, &gidxc, &slotc, &posc})
         if (v->empty()) v->push_back(0);
       const bool nbidx_empty = poffv.empty();
@@ -2467,22 +2488,28 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       track(h, -(long long)M.bytes);
       // update current actives: B keeps its skeleton S (sorted); then the next phase's ID stage can
       // be prepared (worker thread) while this phase's elimination is prepared and launched here
-      for (int j = 0; j < nj; ++j) {
-        BoxJob& J = jobs[j];
-        J.k = hk[j];
-        if (J.k == J.b) continue;
-        const int* pm = &hperm[J.permoff];
-        std::vector<int> sk(pm, pm + J.k);
-        std::sort(sk.begin(), sk.end());
-        total_active -= (J.b - J.k);
-        curpos[J.a] = sk;
-        if (sep) {
-          const int* pc = &hperm[J.permoffc];
-          std::vector<int> skc(pc, pc + J.k);
-          std::sort(skc.begin(), skc.end());
-          curposc[J.a] = skc;
-        }
-        ident[J.a] = 0;
+      {
+        std::atomic<long long> removed{0};  // (the boxes of a phase are distinct owners: no two jobs share J.a)
+        HostPool::get().parallel_for(nj, 64, [&](int j0, int j1) {
+          long long rem = 0;
+          for (int j = j0; j < j1; ++j) {
+            BoxJob& J = jobs[j];
+            J.k = hk[j];
+            if (J.k == J.b) continue;
+            const int* pm = &hperm[J.permoff];
+            curpos[J.a].assign(pm, pm + J.k);
+            std::sort(curpos[J.a].begin(), curpos[J.a].end());
+            rem += J.b - J.k;
+            if (sep) {
+              const int* pc = &hperm[J.permoffc];
+              curposc[J.a].assign(pc, pc + J.k);
+              std::sort(curposc[J.a].begin(), curposc[J.a].end());
+            }
+            ident[J.a] = 0;
+          }
+          removed += rem;
+        });
+        total_active -= removed.load();
       }
       std::future<IdPrep> next_fut = std::async(std::launch::async, prep_id, colour + 1);
 
