@@ -1413,7 +1413,6 @@ struct LevelBSR {
   std::vector<std::vector<int>> act;        // actives at level start (sorted), per local owner
   std::vector<std::vector<int>> actc;       // separate IDs: the active columns (same counts); else unused
   bool sep = false;
-  const std::vector<int>& cact(int a) const { return sep ? actc[a] : act[a]; }
   std::vector<std::vector<long long>> poff; // complex offset of block (a, nb[a][i])
   DBuf bsr;
   long long size = 0;
