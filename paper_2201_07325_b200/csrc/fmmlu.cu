@@ -1868,39 +1868,59 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     h->topo_ready[lvl] = 1;
     cur.tp = &h->topo[lvl];
     lap(14);
-    for (int b : T.levels[lvl]) {
-      if (!T.boxes[b].leaf()) {
+    {
+      const std::vector<int>& lb = T.levels[lvl];
+      HostPool::get().parallel_for((int)lb.size(), 64, [&](int i0, int i1) {  // actives = ∪ children's skeletons
         std::vector<int> u;
-        const Box& B = T.boxes[b];
-        for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), act[B.child[c]].begin(), act[B.child[c]].end());
-        std::sort(u.begin(), u.end());
-        act[b] = u;
-        if (sep) {
+        for (int i = i0; i < i1; ++i) {
+          const int b = lb[i];
+          const Box& B = T.boxes[b];
+          if (B.leaf()) continue;
           u.clear();
-          for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), actc[B.child[c]].begin(), actc[B.child[c]].end());
+          for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), act[B.child[c]].begin(), act[B.child[c]].end());
           std::sort(u.begin(), u.end());
-          actc[b] = u;
+          act[b] = u;
+          if (sep) {
+            u.clear();
+            for (int c = 0; c < B.nchild; ++c) u.insert(u.end(), actc[B.child[c]].begin(), actc[B.child[c]].end());
+            std::sort(u.begin(), u.end());
+            actc[b] = u;
+          }
         }
-      }
+      });
     }
     const int no = (int)cur.owners().size();
     cur.act.resize(no);
-    for (int i = 0; i < no; ++i) cur.act[i] = act[cur.owners()[i]];
     cur.sep = sep;
-    if (sep) {
-      cur.actc.resize(no);
-      for (int i = 0; i < no; ++i) cur.actc[i] = actc[cur.owners()[i]];
-    }
+    if (sep) cur.actc.resize(no);
     const std::vector<std::vector<int>>& nb = cur.tp->nb;
-    long long off = 0;
     cur.poff.resize(no);
-    for (int a = 0; a < no; ++a) {
-      cur.poff[a].resize(nb[a].size());
-      for (size_t i = 0; i < nb[a].size(); ++i) {
-        cur.poff[a][i] = off;
-        off += (long long)cur.act[a].size() * cur.act[nb[a][i]].size();
+    std::vector<long long> rowoff(no + 1, 0);
+    HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {
+      for (int a = a0; a < a1; ++a) {
+        cur.act[a] = act[cur.owners()[a]];
+        if (sep) cur.actc[a] = actc[cur.owners()[a]];
       }
-    }
+    });
+    HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {  // block-row sizes (needs every cur.act)
+      for (int a = a0; a < a1; ++a) {
+        long long t = 0;
+        for (int b : nb[a]) t += (long long)cur.act[a].size() * cur.act[b].size();
+        rowoff[a + 1] = t;
+      }
+    });
+    for (int a = 0; a < no; ++a) rowoff[a + 1] += rowoff[a];
+    const long long off = rowoff[no];
+    HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {
+      for (int a = a0; a < a1; ++a) {
+        cur.poff[a].resize(nb[a].size());
+        long long o = rowoff[a];
+        for (size_t i = 0; i < nb[a].size(); ++i) {
+          cur.poff[a][i] = o;
+          o += (long long)cur.act[a].size() * cur.act[nb[a][i]].size();
+        }
+      }
+    });
     cur.size = off;
     lap(15);
     // slot 0: the level's block store; slot 1: the previous level's store compacted to its skeletons
@@ -2091,30 +2111,38 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
       for (int colour = c0; colour < 8; ++colour) {
         const double t0 = now_ms();
         std::vector<BoxJob> jobs;
-        for (int bx : T.levels[lvl]) {
-          if (T.colour(bx) != colour) continue;
-          int a = cur.local(bx);
-          int b = (int)curpos[a].size();
-          if (b == 0) continue;
-          BoxJob J;
-          J.a = a;
-          J.b = b;
-          for (int o : cur.tp->boxN[a])
-            if (!curpos[o].empty()) {
-              J.N.push_back(o);
-              J.nN += (int)curpos[o].size();
+        {
+          std::vector<int> cand;  // the colour's boxes with actives, in Morton order
+          for (int bx : T.levels[lvl])
+            if (T.colour(bx) == colour && !curpos[cur.local(bx)].empty()) cand.push_back(bx);
+          std::vector<BoxJob> all(cand.size());
+          std::vector<char> keepj(cand.size(), 0);
+          HostPool::get(1).parallel_for((int)cand.size(), 64, [&](int i0, int i1) {
+            for (int i = i0; i < i1; ++i) {
+              const int a = cur.local(cand[i]);
+              BoxJob& J = all[i];
+              J.a = a;
+              J.b = (int)curpos[a].size();
+              for (int o : cur.tp->boxN[a])
+                if (!curpos[o].empty()) {
+                  J.N.push_back(o);
+                  J.nN += (int)curpos[o].size();
+                }
+              for (int o : cur.tp->boxQ[a])
+                if (!curpos[o].empty()) {
+                  J.Q.push_back(o);
+                  J.nQ += (int)curpos[o].size();
+                }
+              const long long nF = total_active - J.b - J.nN;
+              if (nF == 0) continue;  // F = ∅ → S = B (reading C12)
+              const long long nP = nF - J.nQ;
+              J.proxy = nP > 0;
+              J.m = 2 * J.nQ + (J.proxy ? 2 * ngamma : 0);
+              keepj[i] = 1;
             }
-          for (int o : cur.tp->boxQ[a])
-            if (!curpos[o].empty()) {
-              J.Q.push_back(o);
-              J.nQ += (int)curpos[o].size();
-            }
-          long long nF = total_active - b - J.nN;
-          if (nF == 0) continue;  // F = ∅ → S = B (reading C12)
-          long long nP = nF - J.nQ;
-          J.proxy = nP > 0;
-          J.m = 2 * J.nQ + (J.proxy ? 2 * ngamma : 0);
-          jobs.push_back(std::move(J));
+          });
+          for (size_t i = 0; i < all.size(); ++i)
+            if (keepj[i]) jobs.push_back(std::move(all[i]));
         }
         P.t_jobs += now_ms() - t0;
         if (jobs.empty()) continue;
@@ -3129,23 +3157,36 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     // copy (workspace slot 1), and the big store (slot 0) is free for the next level.  cfg5: the
     // level-6 store shrinks from ≈ 45 GB to ≈ 9 GB, so two full level stores are never held at once.
     {
-      std::vector<int> nactoff(no + 1, 0), fposr, fposc;
-      for (int a = 0; a < no; ++a) nactoff[a + 1] = nactoff[a] + (int)curpos[a].size();
-      fposr.reserve(nactoff[no] + 1);
-      for (int a = 0; a < no; ++a) fposr.insert(fposr.end(), curpos[a].begin(), curpos[a].end());
-      if (sep) {
-        fposc.reserve(nactoff[no] + 1);
-        for (int a = 0; a < no; ++a) fposc.insert(fposc.end(), curposc[a].begin(), curposc[a].end());
+      std::vector<int> nactoff(no + 1, 0), fposr, fposc, pairoff(no + 1, 0);
+      std::vector<long long> rowtot(no + 1, 0);
+      for (int a = 0; a < no; ++a) {
+        nactoff[a + 1] = nactoff[a] + (int)curpos[a].size();
+        pairoff[a + 1] = pairoff[a] + (int)nb[a].size();
       }
-      std::vector<long long> npoffv;
-      npoffv.reserve(cur.npairs + 1);
-      long long noff = 0;
-      for (int a = 0; a < no; ++a)
-        for (size_t i = 0; i < nb[a].size(); ++i) {
-          npoffv.push_back(noff);
-          cur.poff[a][i] = noff;
-          noff += (long long)curpos[a].size() * curpos[nb[a][i]].size();
+      fposr.resize(nactoff[no]);
+      if (sep) fposc.resize(nactoff[no]);
+      HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {  // per owner: positions, block-row size
+        for (int a = a0; a < a1; ++a) {
+          std::copy(curpos[a].begin(), curpos[a].end(), fposr.begin() + nactoff[a]);
+          if (sep) std::copy(curposc[a].begin(), curposc[a].end(), fposc.begin() + nactoff[a]);
+          long long t = 0;
+          for (int b : nb[a]) t += (long long)curpos[a].size() * curpos[b].size();
+          rowtot[a + 1] = t;
         }
+      });
+      for (int a = 0; a < no; ++a) rowtot[a + 1] += rowtot[a];
+      std::vector<long long> npoffv(pairoff[no]);
+      const long long noff = rowtot[no];
+      HostPool::get().parallel_for(no, 64, [&](int a0, int a1) {  // compact offsets of the owner's blocks
+        for (int a = a0; a < a1; ++a) {
+          long long o = rowtot[a];
+          for (size_t i = 0; i < nb[a].size(); ++i) {
+            npoffv[pairoff[a] + i] = o;
+            cur.poff[a][i] = o;
+            o += (long long)curpos[a].size() * curpos[nb[a][i]].size();
+          }
+        }
+      });
       if (npoffv.empty()) npoffv.push_back(0);
       if (fposr.empty()) fposr.push_back(0);
       if (sep && fposc.empty()) fposc.push_back(0);
@@ -3328,25 +3369,43 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
     S.factor_bytes += h->root_dinv.bytes;
     const cplx m1 = cmk(-1.0, 0.0);
     int lid = h->prof.begin(FMMLU_K_ROOT, st);
-    root_lu_factor(h->root.as<cplx>(), n0, piv.as<int>(), status.as<int>(), h->root_dinv.as<cplx>(), st,
-                   [&](int m, int nn, int kk, const cplx* A, int lda, const cplx* B, int ldb, cplx* C, int ldc) {
-                     std::vector<GemmProblem> gp;
-                     std::vector<GemmGroup> gt;
-                     GemmProblem P{};
-                     P.m = m;
-                     P.n = nn;
-                     P.k = kk;
-                     P.opA = kOpN;
-                     P.opB = kOpN;
-                     P.A = A;
-                     P.lda = lda;
-                     P.B = B;
-                     P.ldb = ldb;
-                     P.C = C;
-                     P.ldc = ldc;
-                     add_gemm(gp, gt, P);
-                     gemm_batched_staged(gp, gt, m1, st, rkeep);
-                   });
+    {
+      static const bool lookahead = !(getenv("FMMLU_ROOT_LOOKAHEAD") && atoi(getenv("FMMLU_ROOT_LOOKAHEAD")) == 0);
+      cudaStream_t sp = st;
+      if (lookahead) FMMLU_CUDA(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
+      struct SideStream {  // its staging arena is dropped and the stream destroyed on every path
+        cudaStream_t s, main;
+        ~SideStream() {
+          if (s != main) {
+            cudaStreamSynchronize(s);
+            drop_arena(s);
+            cudaStreamDestroy(s);
+          }
+        }
+      } side{sp, st};
+      root_lu_factor(h->root.as<cplx>(), n0, piv.as<int>(), status.as<int>(), h->root_dinv.as<cplx>(), st, sp,
+                     [&](cudaStream_t gs, int m, int nn, int kk, const cplx* A, int lda, const cplx* B, int ldb, cplx* C,
+                         int ldc) {
+                       std::vector<GemmProblem> gp;
+                       std::vector<GemmGroup> gt;
+                       GemmProblem P{};
+                       P.m = m;
+                       P.n = nn;
+                       P.k = kk;
+                       P.opA = kOpN;
+                       P.opB = kOpN;
+                       P.A = A;
+                       P.lda = lda;
+                       P.B = B;
+                       P.ldb = ldb;
+                       P.C = C;
+                       P.ldc = ldc;
+                       add_gemm(gp, gt, P);
+                       gemm_batched_staged(gp, gt, m1, gs, rkeep);
+                     });
+      // the staging buffers of the side stream (rkeep entries borrowed from its arena) end with it
+      FMMLU_CUDA(cudaStreamSynchronize(sp));
+    }
     h->prof.end(lid, st);
     h->prof.add(FMMLU_K_ROOT, 8.0 / 3.0 * (double)n0 * n0 * n0, 32.0 * (double)n0 * n0, root_lu_launches(n0));
     int* hp = h->d2h(n0);

@@ -272,14 +272,16 @@ void launch_box_geo(const double* pts, const double* nrm, const double* npts, co
 constexpr int kRootNB = 64;  // outer panel (trailing-update GEMM depth)
 constexpr int kRootIB = 16;  // inner register panel width
 // C −= A·B (m×n, k) on the library's DMMA GEMM; supplied by the host orchestration
-using GemmFn = std::function<void(int m, int n, int k, const cplx* A, int lda, const cplx* B, int ldb, cplx* C,
-                                  int ldc)>;
+using GemmFn = std::function<void(cudaStream_t s, int m, int n, int k, const cplx* A, int lda, const cplx* B, int ldb,
+                                  cplx* C, int ldc)>;
 int root_lu_max_n();
 int root_lu_tb(int n);  // row-block height of the blocked triangular solves / Dinv blocks
 // In place P·A = L·U of the n × n column-major A (ld n); piv[j] = row interchanged with j at step j;
 // Dinv (2·ceil(n/TB)·TB² complex): inverses of L's and U's TB × TB diagonal blocks; *status = 1 on an
-// exactly zero pivot column.
-void root_lu_factor(cplx* A, int n, int* piv, int* status, cplx* Dinv, cudaStream_t st, const GemmFn& gemm);
+// exactly zero pivot column.  sp: side stream for the lookahead (the next outer panel is factored on it
+// while the rest of the trailing update runs on st); sp == st: none.  gemm(s, ...) runs C −= A·B on s.
+void root_lu_factor(cplx* A, int n, int* piv, int* status, cplx* Dinv, cudaStream_t st, cudaStream_t sp,
+                    const GemmFn& gemm);
 int root_lu_launches(int n);
 // Y (n × nrhs, ld ldy, rows already permuted by P) ← U⁻¹ L⁻¹ Y.  flags: 2·(ceil(n/TB)+1) ints scratch.
 void root_lu_solve(const cplx* A, int n, const cplx* Dinv, cplx* Y, int ldy, int nrhs, int* flags, cudaStream_t st);

@@ -471,7 +471,8 @@ int root_lu_tb(int n) {
   return 64;
 }
 
-void root_lu_factor(cplx* A, int n, int* piv, int* status, cplx* Dinv, cudaStream_t st, const GemmFn& gemm) {
+void root_lu_factor(cplx* A, int n, int* piv, int* status, cplx* Dinv, cudaStream_t st, cudaStream_t sp,
+                    const GemmFn& gemm) {
   const int lda = n;
   if (n > root_lu_max_n()) throw Error(-6, "root block larger than the register LU panel supports");
   static size_t sw_cur = 0;
@@ -480,29 +481,68 @@ void root_lu_factor(cplx* A, int n, int* piv, int* status, cplx* Dinv, cudaStrea
                                     (int)swap_smem(kRootNB, n)));
     sw_cur = swap_smem(kRootNB, n);
   }
-  for (int J0 = 0; J0 < n; J0 += kRootNB) {
-    const int NB = std::min(kRootNB, n - J0);
-    for (int j0 = J0; j0 < J0 + NB; j0 += kRootIB) {
-      const int jb = std::min(kRootIB, J0 + NB - j0);
-      launch_panel<kRootIB>(A, lda, n, piv, j0, jb, status, st);
-      const int cw = NB;  // columns of J
-      k_lu_swap_trsm<<<(cw + SW_C - 1) / SW_C, SW_NT, swap_smem(jb, n), st>>>(A, lda, n, piv, j0, jb, J0, J0 + NB, j0,
-                                                                            j0 + jb, j0 + jb);
-      FMMLU_LAUNCH();
-      const int m = n - (j0 + jb), nc = J0 + NB - (j0 + jb);
-      if (m > 0 && nc > 0)
-        gemm(m, nc, jb, A + (j0 + jb) + (size_t)j0 * lda, lda, A + j0 + (size_t)(j0 + jb) * lda, lda,
-             A + (j0 + jb) + (size_t)(j0 + jb) * lda, lda);
+  // Lookahead: the trailing update of outer panel J is split into the next panel's columns (first) and
+  // the rest; the next panel is then factored on a side stream while the rest of the update runs on st
+  // (the panel kernels are latency-bound 16-CTA clusters, the update is a DMMA GEMM: they share the GPU).
+  // sp: the side stream (sp == st: no lookahead)
+  const bool lookahead = sp != st;
+  cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
+  if (lookahead) {
+    FMMLU_CUDA(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
+    FMMLU_CUDA(cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming));
+    FMMLU_CUDA(cudaEventRecord(ev_cols, st));  // the block is built on st
+  }
+  try {
+    for (int J0 = 0; J0 < n; J0 += kRootNB) {
+      const int NB = std::min(kRootNB, n - J0);
+      if (lookahead) FMMLU_CUDA(cudaStreamWaitEvent(sp, ev_cols, 0));  // this panel's columns are up to date
+      for (int j0 = J0; j0 < J0 + NB; j0 += kRootIB) {
+        const int jb = std::min(kRootIB, J0 + NB - j0);
+        launch_panel<kRootIB>(A, lda, n, piv, j0, jb, status, sp);
+        const int cw = NB;  // columns of J
+        k_lu_swap_trsm<<<(cw + SW_C - 1) / SW_C, SW_NT, swap_smem(jb, n), sp>>>(A, lda, n, piv, j0, jb, J0, J0 + NB, j0,
+                                                                              j0 + jb, j0 + jb);
+        FMMLU_LAUNCH();
+        const int m = n - (j0 + jb), nc = J0 + NB - (j0 + jb);
+        if (m > 0 && nc > 0)
+          gemm(sp, m, nc, jb, A + (j0 + jb) + (size_t)j0 * lda, lda, A + j0 + (size_t)(j0 + jb) * lda, lda,
+               A + (j0 + jb) + (size_t)(j0 + jb) * lda, lda);
+      }
+      if (lookahead) {
+        FMMLU_CUDA(cudaEventRecord(ev_panel, sp));
+        FMMLU_CUDA(cudaStreamWaitEvent(st, ev_panel, 0));
+      }
+      if (n > NB) {
+        k_lu_swap_trsm<<<(n + SW_C - 1) / SW_C, SW_NT, swap_smem(NB, n), st>>>(A, lda, n, piv, J0, NB, 0, n, J0, J0 + NB,
+                                                                            J0 + NB);
+        FMMLU_LAUNCH();
+      }
+      const int m = n - (J0 + NB);
+      if (m > 0) {
+        const cplx* Lp = A + (J0 + NB) + (size_t)J0 * lda;
+        const int nn = lookahead ? std::min(kRootNB, m) : 0;  // the next panel's columns first
+        if (nn > 0) {
+          gemm(st, m, nn, NB, Lp, lda, A + J0 + (size_t)(J0 + NB) * lda, lda, A + (J0 + NB) + (size_t)(J0 + NB) * lda, lda);
+          FMMLU_CUDA(cudaEventRecord(ev_cols, st));
+        }
+        if (m - nn > 0)
+          gemm(st, m, m - nn, NB, Lp, lda, A + J0 + (size_t)(J0 + NB + nn) * lda, lda,
+               A + (J0 + NB) + (size_t)(J0 + NB + nn) * lda, lda);
+      }
     }
-    if (n > NB) {
-      k_lu_swap_trsm<<<(n + SW_C - 1) / SW_C, SW_NT, swap_smem(NB, n), st>>>(A, lda, n, piv, J0, NB, 0, n, J0, J0 + NB,
-                                                                          J0 + NB);
-      FMMLU_LAUNCH();
+  } catch (...) {
+    if (lookahead) {
+      cudaStreamSynchronize(sp);
+      cudaEventDestroy(ev_cols);
+      cudaEventDestroy(ev_panel);
     }
-    const int m = n - (J0 + NB);
-    if (m > 0)
-      gemm(m, m, NB, A + (J0 + NB) + (size_t)J0 * lda, lda, A + J0 + (size_t)(J0 + NB) * lda, lda,
-           A + (J0 + NB) + (size_t)(J0 + NB) * lda, lda);
+    throw;
+  }
+  if (lookahead) {
+    FMMLU_CUDA(cudaEventRecord(ev_panel, sp));
+    FMMLU_CUDA(cudaStreamWaitEvent(st, ev_panel, 0));
+    FMMLU_CUDA(cudaEventDestroy(ev_cols));
+    FMMLU_CUDA(cudaEventDestroy(ev_panel));
   }
   const int TB = root_lu_tb(n), nblk = (n + TB - 1) / TB;
   const size_t smem = 2 * (size_t)TB * TB * sizeof(cplx);
