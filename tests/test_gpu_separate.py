@@ -170,3 +170,23 @@ def test_separate_cfg2_fullsize(F):
     assert abs(n0 - meta["n0"]) <= 0.05 * meta["n0"] + 2
     h0 = _factor(F, g, c["k"], c["eps"], c["leaf_max"], sep=0)
     assert n0 < h0.stats()["n0"]
+
+
+@pytest.mark.parametrize("case", ["single_leaf", "two_levels"])
+def test_separate_degenerate_trees(F, case):
+    """No eliminated box (one leaf, or a tree whose levels stop at 1): the separate path reduces to the
+    dense LU of the whole matrix, rows and columns both the identity order."""
+    if case == "single_leaf":
+        g, leaf = fi.fibonacci_sphere(60), 64
+    else:
+        g, leaf = fi.fibonacci_sphere(300), 64      # levels 0..1 or 0..2 only: nothing below level 2
+    b = fi.gaussian_rhs(g.n, 2, 1)
+    h = _factor(F, g, 1.0, 1e-6, leaf)
+    x = np.asfortranarray(b.copy())
+    h.solve(x)
+    xd = dense.dense_solve(g.points, g.normals, g.weights, 1.0, b)
+    assert h.stats()["n0"] == g.n and h.stats()["n_eliminated"] == 0
+    assert dense.rel_diff(x, xd) < 1e-9
+    y = np.asfortranarray(x.copy())
+    h.apply(y)
+    assert dense.rel_diff(y, b) < 1e-9
