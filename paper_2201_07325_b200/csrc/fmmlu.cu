@@ -646,6 +646,20 @@ struct fmmlu_handle {
   int separate_id = 0;       // 1: separate incoming/outgoing IDs (DESIGN R12)
   bool fac_separate = false; // the stored factorization was built with separate IDs
   DBuf sep_perm;             // int n (separate IDs): unknown c ← equation sep_perm[c] between the sweeps
+  // Repeated small-RHS solves (the factorization is computed once and applied to
+  // many right-hand sides): from the second fmmlu_solve with the same nrhs on, the ≈ 5 launches per
+  // phase of the per-box sweeps are replayed as one CUDA graph captured on persistent buffers.
+  struct SolveGraph {
+    cudaGraphExec_t exec = nullptr;
+    int uses = 0;
+  };
+  std::map<int, SolveGraph> solve_graphs;  // by nrhs
+  DBuf sv_y, sv_scr, sv_root;              // persistent solve buffers (their pointers are baked into the graphs)
+  void drop_solve_graphs() {
+    for (auto& kv : solve_graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    solve_graphs.clear();
+  }
 };
 
 namespace {
@@ -830,14 +844,19 @@ void gemm_batched_staged(std::vector<GemmProblem>& probs, std::vector<GemmGroup>
 // Root block solve / forward product on y (tree order, ld ldy), rows B_t:
 // solve y[B_t] ← A_t⁻¹ y[B_t] = U⁻¹L⁻¹(P y[B_t]);  fwd y[B_t] ← A_t y[B_t] = Pᵀ(L U y[B_t]).
 // yout (separate IDs: the equations live in y, the unknowns / products go to another vector; same ld)
-void root_solve(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st, cplx* yout = nullptr) {
+// tbuf: caller-owned n0 × nrhs scratch (the graph-captured solve; nullptr: allocated here)
+void root_solve(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st, cplx* yout = nullptr,
+                cplx* tbuf = nullptr) {
   if (h->n0 <= 0) return;
   const int n0 = (int)h->n0;
   DBuf T;
-  T.alloc((size_t)n0 * nrhs * sizeof(cplx), st);
-  launch_rows_move(h->root_rows_in.as<int>(), n0, y, ldy, T.as<cplx>(), nrhs, 0, st);
-  root_lu_solve(h->root.as<cplx>(), n0, h->root_dinv.as<cplx>(), T.as<cplx>(), n0, nrhs, h->root_flags.as<int>(), st);
-  launch_rows_move(h->root_rows.as<int>(), n0, yout ? yout : y, ldy, T.as<cplx>(), nrhs, 1, st);
+  if (!tbuf) {
+    T.alloc((size_t)n0 * nrhs * sizeof(cplx), st);
+    tbuf = T.as<cplx>();
+  }
+  launch_rows_move(h->root_rows_in.as<int>(), n0, y, ldy, tbuf, nrhs, 0, st);
+  root_lu_solve(h->root.as<cplx>(), n0, h->root_dinv.as<cplx>(), tbuf, n0, nrhs, h->root_flags.as<int>(), st);
+  launch_rows_move(h->root_rows.as<int>(), n0, yout ? yout : y, ldy, tbuf, nrhs, 1, st);
 }
 void root_fwd(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cudaStream_t st, cplx* yout = nullptr) {
   if (h->n0 <= 0) return;
@@ -1780,6 +1799,7 @@ void factor_impl(fmmlu_handle* h, double k, double eps) {
   h->root_flags.release();
   h->apply_ready = false;
   h->factored = false;
+  h->drop_solve_graphs();
   for (auto& w : h->ws_slot) w.release();
   DevWork& dw = dev_work(h->dev);
   std::lock_guard<std::mutex> dw_lock(dw.mu);  // one factorization per device uses the shared workspace
@@ -3619,8 +3639,9 @@ int sweep_chunk(const fmmlu_handle* h, int nrhs) {
 
 // The per-box solve sweeps: V⁻¹ phase by phase, the root, W⁻¹ in reverse; each
 // phase's kernels run once per sub-wave (one wave unless deterministic).  scr: Σr × nrhs scratch.
-void sweeps_boxes(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cplx* scr, cudaStream_t st) {
-  static const bool trace = getenv("FMMLU_TRACE") != nullptr;
+void sweeps_boxes(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cplx* scr, cudaStream_t st, cplx* root_tmp = nullptr) {
+  static const bool trace_env = getenv("FMMLU_TRACE") != nullptr;
+  const bool trace = trace_env && root_tmp == nullptr;  // (no event queries inside a stream capture)
   cudaEvent_t ev[4];
   if (trace)
     for (auto& e : ev) FMMLU_CUDA(cudaEventCreate(&e));
@@ -3634,7 +3655,7 @@ void sweeps_boxes(fmmlu_handle* h, cplx* y, int ldy, int nrhs, cplx* scr, cudaSt
   SepSwap swp;
   cplx* const yeq = y;
   if (cplx* y2 = swp.begin(h, y, ldy, nrhs, st)) y = y2;
-  root_solve(h, yeq, ldy, nrhs, st, y);
+  root_solve(h, yeq, ldy, nrhs, st, y, root_tmp);
   if (trace) FMMLU_CUDA(cudaEventRecord(ev[2], st));
   for (auto it = h->phases.rbegin(); it != h->phases.rend(); ++it) {
     FMMLU_CUDA(cudaMemsetAsync(scr, 0, (size_t)it->tmp_rows * nrhs * sizeof(cplx), st));
@@ -3668,14 +3689,39 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
     FMMLU_CUDA(cudaMemcpyAsync(io.p, rhs, (size_t)n * nrhs * sizeof(cplx), cudaMemcpyHostToDevice, st));
     b = io.as<cplx>();
   }
-  y.alloc((size_t)n * nrhs * sizeof(cplx), st);
-  cplx* yp = y.as<cplx>();
+  // Small-RHS solves from the second call with the same nrhs on: one CUDA graph (see SolveGraph).
+  static const bool graph_env = !(getenv("FMMLU_SOLVE_GRAPH") && atoi(getenv("FMMLU_SOLVE_GRAPH")) == 0);
+  static const bool trace_env = getenv("FMMLU_TRACE") != nullptr;
+  const bool gemm_path = nrhs >= kGemmSolveMin || is_deterministic(h);
+  const bool graph_ok = graph_env && !trace_env && !gemm_path && !h->fac_separate;
+  size_t scr_rows = 1;
+  for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
+  DBuf scr;
+  cplx* yp = nullptr;
+  cplx* scrp = nullptr;
+  cplx* rootp = nullptr;
+  if (graph_ok) {  // persistent buffers: the graphs hold their addresses
+    const size_t ny = (size_t)n * nrhs * sizeof(cplx), ns = scr_rows * nrhs * sizeof(cplx),
+                 nr = (size_t)std::max<long long>(h->n0, 1) * nrhs * sizeof(cplx);
+    if (h->sv_y.bytes < ny || h->sv_scr.bytes < ns || h->sv_root.bytes < nr) {
+      h->drop_solve_graphs();
+      if (h->sv_y.bytes < ny) h->sv_y.alloc(ny, st);
+      if (h->sv_scr.bytes < ns) h->sv_scr.alloc(ns, st);
+      if (h->sv_root.bytes < nr) h->sv_root.alloc(nr, st);
+    }
+    yp = h->sv_y.as<cplx>();
+    scrp = h->sv_scr.as<cplx>();
+    rootp = h->sv_root.as<cplx>();
+  } else {
+    y.alloc((size_t)n * nrhs * sizeof(cplx), st);
+    yp = y.as<cplx>();
+  }
   Prof& P = h->prof;
   int sid = P.begin(FMMLU_K_SOLVE, st);
   launch_permute_in(b, n, yp, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
   // many right-hand sides: the sweeps as batched DMMA GEMMs; also the deterministic path (the
   // per-box kernels split a box's product over CTAs that meet in fp64 atomics)
-  if (nrhs >= kGemmSolveMin || is_deterministic(h)) {
+  if (gemm_path) {
     P.end(sid, st);
     const int qc = sweep_chunk(h, nrhs);
     for (int q0 = 0; q0 < nrhs; q0 += qc) sweeps_gemm(h, yp + (size_t)q0 * n, n, std::min(qc, nrhs - q0));
@@ -3688,11 +3734,33 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
     P.resolve();
     return;
   }
-  size_t scr_rows = 1;
-  for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
-  DBuf scr;
-  scr.alloc(scr_rows * nrhs * sizeof(cplx), st);
-  sweeps_boxes(h, yp, n, nrhs, scr.as<cplx>(), st);
+  if (graph_ok) {
+    fmmlu_handle::SolveGraph& G = h->solve_graphs[nrhs];
+    if (!G.exec && G.uses >= 1) {  // second solve with this nrhs: capture the sweeps
+      cudaGraph_t graph = nullptr;
+      FMMLU_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        sweeps_boxes(h, yp, n, nrhs, scrp, st, rootp);
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      FMMLU_CUDA(cudaStreamEndCapture(st, &graph));
+      const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        G.exec = nullptr;
+        FMMLU_CUDA(ie);
+      }
+    }
+    if (G.exec) FMMLU_CUDA(cudaGraphLaunch(G.exec, st));
+    else sweeps_boxes(h, yp, n, nrhs, scrp, st, rootp);
+    ++G.uses;
+  } else {
+    scr.alloc(scr_rows * nrhs * sizeof(cplx), st);
+    sweeps_boxes(h, yp, n, nrhs, scr.as<cplx>(), st);
+  }
   launch_permute_out(yp, b, n, n, nrhs, h->perm.as<long long>(), h->g.sw, 1, st);
   P.end(sid, st);
   {
@@ -4635,6 +4703,10 @@ int fmmlu_destroy(fmmlu_handle* h) {
   h->root_dinv.release();
   h->root_flags.release();
   h->sep_perm.release();
+  h->drop_solve_graphs();
+  h->sv_y.release();
+  h->sv_scr.release();
+  h->sv_root.release();
   h->tcode.release();
   h->tleaf.release();
   h->tleafrank.release();

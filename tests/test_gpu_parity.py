@@ -397,3 +397,33 @@ def test_refactor_same_handle_and_ragged_rhs(F):
     x1 = np.asfortranarray(b[:, 7:8].copy())
     h.solve(x1)
     assert dense.rel_diff(x[:, 7:8], x1) < 1e-11
+
+
+def test_repeated_solves_replay_graph(F):
+    """fmmlu_solve called repeatedly on one factorization: from the second call
+    with the same nrhs on the per-box sweeps are replayed from a captured CUDA graph.  Every call
+    must give the first call's solution (to the rounding of the fp64 atomics), also for another
+    nrhs in between and after a re-factorization at another tolerance."""
+    g = fi.ellipsoid(3000)
+    k = 2 * math.pi
+    b2 = fi.gaussian_rhs(g.n, 2, 0)
+    b5 = fi.gaussian_rhs(g.n, 5, 1)
+    h = F.FmmLu(g.points, g.normals, g.weights, 32).factor(k, 1e-6)
+    ref2 = ref5 = None
+    for it in range(4):
+        x2 = np.asfortranarray(b2.copy())
+        h.solve(x2)
+        x5 = np.asfortranarray(b5.copy())
+        h.solve(x5)
+        if it == 0:
+            ref2, ref5 = x2, x5
+            assert dense.residual(g.points, g.normals, g.weights, k, x2, b2) <= 1e-5
+        else:
+            assert dense.rel_diff(x2, ref2) < 1e-11 and dense.rel_diff(x5, ref5) < 1e-11
+    h.factor(k, 1e-9)            # the graphs of the old factors must not survive
+    for it in range(3):
+        x2 = np.asfortranarray(b2.copy())
+        h.solve(x2)
+        assert dense.residual(g.points, g.normals, g.weights, k, x2, b2) <= 1e-8
+    xd = dense.dense_solve(g.points, g.normals, g.weights, k, b2)
+    assert dense.rel_diff(x2, xd) <= 1e-8
