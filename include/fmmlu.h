@@ -130,6 +130,8 @@ int fmmlu_factor(fmmlu_handle* h, double k, double eps);
  * A⁻¹ ≈ W₁⁻¹⋯W_M⁻¹ P_t D⁻¹ P_tᵀ V_M⁻¹⋯V₁⁻¹, sign-toggled factors L833-858).
  *   rhs  : n×nrhs column-major complex128 (host or device); in: b, out: x
  *   nrhs : ≥ 1
+ * The handle keeps n×nrhs complex work buffers between calls for nrhs < 32 (repeated solves with the
+ * same nrhs replay one captured CUDA graph); they are released by fmmlu_destroy.
  * Errors: EINVAL (NULL rhs, nrhs < 1), ESTATE (no factorization), ENOMEM, ECUDA. */
 int fmmlu_solve(fmmlu_handle* h, void* rhs, int nrhs);
 
