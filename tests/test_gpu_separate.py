@@ -190,3 +190,23 @@ def test_separate_degenerate_trees(F, case):
     y = np.asfortranarray(x.copy())
     h.apply(y)
     assert dense.rel_diff(y, b) < 1e-9
+
+
+@pytest.mark.parametrize("nphi", [7, 40])
+def test_separate_monostatic_rcs(F, nphi):
+    """The cross-section workload on a separate-ID factorization: per-box sweeps
+    (7 angles) and GEMM sweeps (40 angles) against the oracle's separate mode and the dense solve."""
+    from oracle import rcs
+    eps = 1e-6
+    g, k, leaf = _case("ellipsoid3000")
+    phis = np.linspace(0.0, 2 * math.pi, nphi, endpoint=False)
+    h = _factor(F, g, k, eps, leaf)
+    R = h.monostatic_rcs(phis)
+    b = rcs.plane_wave_rhs(g.points, k, phis)
+    f = rss.factor(g.points, g.normals, g.weights, k, eps, leaf, separate=True)
+    Ro = rcs.monostatic_rcs(g.points, g.normals, g.weights, k, phis, rss.solve(f, b))
+    Rd = rcs.monostatic_rcs(g.points, g.normals, g.weights, k, phis,
+                            dense.dense_solve(g.points, g.normals, g.weights, k, b))
+    scale = np.max(np.abs(Rd))
+    assert np.max(np.abs(R - Ro)) <= 10 * eps * scale
+    assert np.max(np.abs(R - Rd)) <= 10 * eps * scale
