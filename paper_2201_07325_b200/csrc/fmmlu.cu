@@ -3625,6 +3625,17 @@ void sweeps_gemm(fmmlu_handle* h, cplx* y, int ldy, int Q) {
   wait_stream(h, st);  // keep (staging, workspace) outlives the launches; resets the staging arenas
 }
 
+// GEMM sweeps or per-box kernels?  Deterministic mode and ≥ 32 RHS: GEMM sweeps.  Between 16 and 31 RHS
+// the crossover depends on the size of the factor store (measured, tools/solve_scan.py: cfg5 with 44.7 GB
+// of factors 113 vs 132 ms at 16 RHS and 160 vs 252 ms at 31 in favour of the GEMM sweeps; cfg3 with
+// 4.3 GB 35 vs 22 ms at 16 RHS in favour of the per-box kernels): GEMM sweeps from 16 RHS for stores
+// of ≥ 16 GB.  FMMLU_GEMM_SOLVE_MIN overrides both thresholds.
+bool use_gemm_sweeps(const fmmlu_handle* h, int nrhs) {
+  static const bool forced = getenv("FMMLU_GEMM_SOLVE_MIN") != nullptr;
+  if (is_deterministic(h) || nrhs >= kGemmSolveMin) return true;
+  return !forced && nrhs >= 16 && h->stats.factor_bytes >= (16ll << 30);
+}
+
 // RHS columns per GEMM-sweep pass: bounded so the phase workspace stays ≤ ~2 GB
 int sweep_chunk(const fmmlu_handle* h, int nrhs) {
   size_t per = 1;
@@ -3692,7 +3703,7 @@ void solve_impl(fmmlu_handle* h, void* rhs, int nrhs) {
   // Small-RHS solves from the second call with the same nrhs on: one CUDA graph (see SolveGraph).
   static const bool graph_env = !(getenv("FMMLU_SOLVE_GRAPH") && atoi(getenv("FMMLU_SOLVE_GRAPH")) == 0);
   static const bool trace_env = getenv("FMMLU_TRACE") != nullptr;
-  const bool gemm_path = nrhs >= kGemmSolveMin || is_deterministic(h);
+  const bool gemm_path = use_gemm_sweeps(h, nrhs);
   const bool graph_ok = graph_env && !trace_env && !gemm_path && !h->fac_separate;
   size_t scr_rows = 1;
   for (auto& ph : h->phases) scr_rows = std::max(scr_rows, (size_t)ph.tmp_rows);
@@ -4544,7 +4555,7 @@ void rcs_impl(fmmlu_handle* h, const double* phis, int nphi, void* Rout) {
     R = dR.as<cplx>();
   }
   FMMLU_CUDA(cudaMemsetAsync(R, 0, (size_t)nphi * sizeof(cplx), st));
-  const bool gemm_sweeps = nphi >= kGemmSolveMin || is_deterministic(h);
+  const bool gemm_sweeps = use_gemm_sweeps(h, nphi);
   const int qc = gemm_sweeps ? sweep_chunk(h, nphi) : nphi;
   DBuf yb;
   yb.alloc((size_t)n * qc * sizeof(cplx), st);
